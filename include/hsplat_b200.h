@@ -1,0 +1,236 @@
+/* hsplat_b200.h — C ABI of the B200-native LOD cut + 3DGS forward renderer.
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2406.12080's
+ * reference library `hsplat` (header-only C++20, /root/reference/proj/include/
+ * hsplat).  The reference has no FFI of its own; its public C++ API is the
+ * boundary (proj/README.md:139-158).  Each entry point below replaces one
+ * reference function (file:line cited); the C++ shim include/hsplat/gpu.hpp
+ * re-exposes them with the reference's signatures and exception behaviour.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; every array is caller-owned host memory
+ *    unless the name says otherwise.  Objects (context, hierarchy, cut,
+ *    frame) are opaque, device-resident and reusable across calls.
+ *  - Status codes: HS_OK, then the reference's hsplat::Errc values + 1
+ *    (proj/include/hsplat/errors.hpp:11-25), then CUDA failures.  The message
+ *    of the last failure on a context is hs_last_error(ctx); it is prefixed
+ *    with the Errc name exactly like hsplat::Error::what() (errors.hpp:46-54).
+ *  - One context per device; all work is ordered on the context's CUDA stream.
+ *    Calls are synchronous (return when results are final) unless the
+ *    context's HS_OPT_ASYNC option is set, in which case render calls return
+ *    after enqueueing and hs_frame_wait() completes them.
+ *  - Camera: pinhole, world_to_camera [R|t] as 12 floats ROW-major (the
+ *    reference's text format order, io.hpp:423-429), camera looks down +z.
+ */
+#ifndef HSPLAT_B200_H
+#define HSPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum hs_status {
+    HS_OK = 0,
+    /* hsplat::Errc (errors.hpp:11-25) + 1 */
+    HS_ALL_ZERO_WEIGHTS = 1,
+    HS_DEGENERATE_COVARIANCE = 2,
+    HS_NOT_SPD = 3,
+    HS_MISSING_FORWARD_STATE = 4,
+    HS_NO_INTERIOR_NODES = 5,
+    HS_DEGENERATE_SPREAD = 6,
+    HS_MALFORMED_HEADER = 7,
+    HS_TRUNCATED_RECORD = 8,
+    HS_UNSUPPORTED_SH_DEGREE = 9,
+    HS_EMPTY_SCENE = 10,
+    HS_DIMENSION_MISMATCH = 11,
+    HS_INVALID_ARGUMENT = 12,
+    HS_IO_FAILURE = 13,
+    /* device-side failures (no reference equivalent) */
+    HS_CUDA_ERROR = 100,
+    HS_OUT_OF_MEMORY = 101,
+    HS_NO_DEVICE = 102,
+    HS_CAPACITY_EXCEEDED = 103
+} hs_status;
+
+#define HS_NO_NODE 0xFFFFFFFFu /* model.hpp:15 kNoNode */
+
+/* CameraModel (model.hpp:64-82). */
+typedef struct hs_camera {
+    int32_t width, height;
+    float fx, fy, cx, cy;
+    float w2c[12]; /* row-major 3x4 [R|t] */
+} hs_camera;
+
+/* Hierarchy nodes (model.hpp:93-115), structure-of-arrays, N nodes, root at 0,
+ * children of a node contiguous at [first_child, first_child + child_count). */
+typedef struct hs_node_soa {
+    const uint32_t* parent;      /* N, HS_NO_NODE for the root */
+    const uint32_t* first_child; /* N, HS_NO_NODE for leaves */
+    const uint32_t* child_count; /* N */
+    const float* bmin;           /* 3N  Aabb::min */
+    const float* bmax;           /* 3N  Aabb::max */
+    const float* mean;           /* 3N */
+    const float* scale;          /* 3N */
+    const float* rot_wxyz;       /* 4N  Quaternion (w, x, y, z) */
+    const float* falloff;        /* N */
+    const float* sh;             /* 48N sh[coeff*3 + channel] */
+} hs_node_soa;
+
+typedef struct hs_node_soa_out {
+    uint32_t* parent;
+    uint32_t* first_child;
+    uint32_t* child_count;
+    float* bmin;
+    float* bmax;
+    float* mean;
+    float* scale;
+    float* rot_wxyz;
+    float* falloff;
+    float* sh;
+} hs_node_soa_out;
+
+/* RenderSplat (model.hpp:157-177), structure-of-arrays. */
+typedef struct hs_splat_soa {
+    const float* mean;           /* 3N */
+    const float* scale;          /* 3N */
+    const float* rot_wxyz;       /* 4N, need not be unit */
+    const float* sh;             /* 48N */
+    const float* falloff;        /* N */
+    const float* parent_falloff; /* N */
+    const float* t;              /* N */
+    const int32_t* siblings;     /* N  transition_siblings (K) */
+} hs_splat_soa;
+
+typedef struct hs_splat_soa_out {
+    float* mean;
+    float* scale;
+    float* rot_wxyz;
+    float* sh;
+    float* falloff;
+    float* parent_falloff;
+    float* t;
+    int32_t* siblings;
+} hs_splat_soa_out;
+
+/* StageTimes (render.hpp:24-31): seconds, accumulated with += like the
+ * reference's StageTimer (render.hpp:35-48).  Measured with CUDA events on the
+ * context stream.  `weights` stays 0: the parent/child interpolation
+ * (lod.hpp:116-146) is fused into the preprocess kernel.  `duplicate` covers
+ * the per-splat offset scan, key duplication and the radix sort. */
+typedef struct hs_stage_times {
+    double cut_expand, weights, preprocess, duplicate, tile_ranges, alpha_blend;
+} hs_stage_times;
+
+/* Per-frame counters (device-computed). */
+typedef struct hs_frame_info {
+    int32_t width, height, tiles_x, tiles_y;
+    uint64_t n_splats;       /* C: cut entries / input splats */
+    uint64_t n_visible;      /* V: splats that survived projection culling */
+    uint64_t n_duplicates;   /* D: (tile, splat) pairs = sorted key count */
+    int32_t rendered_count;  /* RenderOutput::rendered_count (render.hpp:82) */
+    int32_t sort_passes;     /* radix passes run for this frame */
+} hs_frame_info;
+
+typedef struct hs_context hs_context;
+typedef struct hs_hierarchy hs_hierarchy;
+typedef struct hs_cut hs_cut;
+typedef struct hs_frame hs_frame;
+
+/* ------------------------------------------------------------ context */
+const char* hs_status_name(hs_status s);
+hs_status hs_context_create(int device, hs_context** out);
+void hs_context_destroy(hs_context* ctx);
+const char* hs_last_error(const hs_context* ctx);
+void* hs_context_stream(hs_context* ctx); /* the cudaStream_t all work runs on */
+hs_status hs_context_synchronize(hs_context* ctx);
+
+enum {
+    HS_OPT_ASYNC = 1,       /* 0 (default): calls block; 1: render calls only enqueue */
+    HS_OPT_BLEND_MODE = 2,  /* 0: exact (glibc expf/powf replicas, bit-exact), 1: fast */
+    HS_OPT_DEBUG = 3        /* 1: keep pre-sort keys + per-splat projection dumps */
+};
+hs_status hs_context_set_option(hs_context* ctx, int option, int64_t value);
+
+/* ------------------------------------------------------------ hierarchy
+ * Device-resident structure-of-arrays copy (reference node order). */
+/* replaces: Hierarchy construction + validate_hierarchy (model.hpp:118-139) */
+hs_status hs_hierarchy_upload(hs_context* ctx, const hs_node_soa* nodes, uint64_t n_nodes, uint32_t sh_degree,
+                              int validate, hs_hierarchy** out);
+/* replaces: read_hierarchy (io.hpp:375-408) */
+hs_status hs_hierarchy_load_h3dg(hs_context* ctx, const char* path, hs_hierarchy** out);
+void hs_hierarchy_destroy(hs_hierarchy* h);
+uint64_t hs_hierarchy_node_count(const hs_hierarchy* h);
+uint64_t hs_hierarchy_leaf_count(const hs_hierarchy* h); /* Hierarchy::leaf_count (model.hpp:108-112) */
+
+/* ------------------------------------------------------------ cut */
+hs_status hs_cut_create(hs_context* ctx, hs_cut** out);
+void hs_cut_destroy(hs_cut* cut);
+/* replaces: select_cut (lod.hpp:52-92).  Result stays on the device, in
+ * ascending node order. */
+hs_status hs_select_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cam, float tau, hs_cut* cut);
+/* cut size (waits for the cut to be final) */
+hs_status hs_cut_size(hs_context* ctx, const hs_cut* cut, uint64_t* n);
+/* CutEntry fields (model.hpp:144-148); any pointer may be NULL */
+hs_status hs_cut_download(hs_context* ctx, const hs_cut* cut, uint32_t* node, float* t, float* alpha_prime);
+/* install a caller-made cut (e.g. the t = 0 transition cuts of the tests) */
+hs_status hs_cut_upload(hs_context* ctx, const hs_hierarchy* h, const uint32_t* node, const float* t,
+                        const float* alpha_prime, uint64_t n, hs_cut* cut);
+/* replaces: cut_render_splats (lod.hpp:148-153) — the interpolated RenderSplats
+ * the fused preprocess computes, downloaded for inspection */
+hs_status hs_cut_render_splats(hs_context* ctx, const hs_hierarchy* h, const hs_cut* cut, hs_splat_soa_out* out);
+
+/* ------------------------------------------------------------ frames */
+hs_status hs_frame_create(hs_context* ctx, hs_frame** out);
+void hs_frame_destroy(hs_frame* f);
+/* replaces: render_hierarchy (render.hpp:706-720) = select_cut + cut_render_splats
+ * + render_forward; `cut` receives the cut (may be NULL) */
+hs_status hs_render_hierarchy(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cam, float tau, hs_cut* cut,
+                              hs_frame* f, hs_stage_times* times);
+/* render an existing cut (bench_path's odd frames, bench.hpp:84) */
+hs_status hs_render_cut(hs_context* ctx, const hs_hierarchy* h, const hs_cut* cut, const hs_camera* cam, hs_frame* f,
+                        hs_stage_times* times);
+/* replaces: render_forward<float> (render.hpp:244-354) over caller splats */
+hs_status hs_render_splats(hs_context* ctx, const hs_splat_soa* splats, uint64_t n, const hs_camera* cam, hs_frame* f,
+                           hs_stage_times* times);
+/* completes an async render (no-op when synchronous) */
+hs_status hs_frame_wait(hs_context* ctx, hs_frame* f);
+hs_status hs_frame_get_info(hs_context* ctx, hs_frame* f, hs_frame_info* info);
+/* RenderOutput (render.hpp:77-83): color 3*H*W plane-major (image.hpp:21),
+ * inverse depth H*W, transmittance H*W; any pointer may be NULL */
+hs_status hs_frame_download(hs_context* ctx, hs_frame* f, float* color, float* depth, float* transmittance,
+                            int32_t* rendered_count);
+/* Parity hooks (ForwardContext, render.hpp:87-98, expressed as sort keys):
+ *  tile_start     tiles+1 offsets (== ForwardContext::tile_start)
+ *  sorted_keys    D keys (tile << 32 | float_bits(z)), sorted
+ *  sorted_vals    D splat ids (== ForwardContext::tile_entries)
+ *  dup_keys/vals  D pre-sort duplicated keys/ids (needs HS_OPT_DEBUG)
+ *  proj16         16 floats per splat (needs HS_OPT_DEBUG): culled, z, mean2d.xy,
+ *                 conic[3], alpha_scale, color[3], inv_depth, radius(int bits),
+ *                 packed rect, tx0, ty0 (int bits) */
+hs_status hs_frame_debug(hs_context* ctx, hs_frame* f, uint64_t* tile_start, uint64_t* sorted_keys,
+                         uint32_t* sorted_vals, uint64_t* dup_keys, uint32_t* dup_vals, float* proj16);
+
+/* ------------------------------------------------------------ host-side tools
+ * Deterministic synthetic city hierarchy (build_bvh layout, build.hpp:73-149)
+ * written into caller arrays sized hs_synth_node_count(leaves). */
+uint64_t hs_synth_node_count(uint64_t leaves);
+float hs_synth_scene_side(uint64_t leaves);
+hs_status hs_synth_city(uint64_t leaves, uint64_t seed, int threads, const hs_node_soa_out* out);
+/* build_bvh (build.hpp:73-149) over caller leaves (mean 3N, scale 3N, rotation
+ * wxyz 4N, falloff N, sh 48N) into arrays sized 2N-1 (test fixtures) */
+hs_status hs_build_bvh(const float* mean, const float* scale, const float* rot_wxyz, const float* falloff,
+                       const float* sh, uint64_t n, int threads, const hs_node_soa_out* out);
+/* .h3dg IO (io.hpp:342-408) on host arrays */
+hs_status hs_h3dg_read_header(const char* path, uint64_t* n_nodes, uint32_t* sh_degree);
+hs_status hs_h3dg_read(const char* path, const hs_node_soa_out* out, uint64_t n_nodes);
+hs_status hs_h3dg_write(const char* path, const hs_node_soa* nodes, uint64_t n_nodes, uint32_t sh_degree);
+/* validate_hierarchy (model.hpp:118-139) on host arrays; msg receives the reason */
+hs_status hs_validate_hierarchy(const hs_node_soa* nodes, uint64_t n_nodes, char* msg, size_t msg_len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSPLAT_B200_H */

@@ -1,0 +1,1081 @@
+// hsplat_oracle.cpp — TEST INFRASTRUCTURE ONLY (the checker, never the product).
+//
+// Eigen-free CPU restatement of the reference hot path of arXiv 2406.12080's
+// `hsplat` library (/root/reference/proj/include/hsplat):
+//   select_cut            lod.hpp:52-92   (granularity :18-26, interp_weight :34-37,
+//                                          transition_alpha :41-45)
+//   cut_render_splats     lod.hpp:116-153
+//   project               render.hpp:104-174 (+ sh.hpp:20-42, :71-78)
+//   splat_alpha           render.hpp:189-231
+//   render_forward        render.hpp:244-354
+//   render_reference      render.hpp:360-408
+//   render_hierarchy      render.hpp:706-720
+//   bench_path            bench.hpp:55-103
+//   psnr                  image.hpp:111-122
+//   parallel_for          parallel.hpp:13-45
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+// reference legs may load this library.
+//
+// Parity status: the reference cannot be compiled in this image (Eigen3,
+// libpng, Catch2 and CLI11 are absent), so the bit-level semantics of Eigen
+// 3.4's small fixed-size expressions are restated by hand (3-term sums
+// x0 + (x1 + x2); Vec4f SSE reductions (x0 + x2) + (x1 + x3); no FMA since the
+// reference builds with CMake Release defaults, no -march).  The oracle is
+// pinned at tolerance level by the reference's own known-answer tests
+// (tests/test_oracle_kat.py ports tests/test_lod.cpp, tests/test_render.cpp,
+// tests/test_bench.cpp closed forms); at bit level versus the compiled
+// reference it is "parity unpinned".  expf/powf are the host glibc calls the
+// reference makes (std::exp / std::pow on float).
+//
+// Build: oracle/Makefile (g++ -O3 -DNDEBUG, no -march: SSE2 scalar, no FMA).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <set>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace oracle {
+
+// ---------------------------------------------------------------- math.hpp:27-37
+constexpr int kTileSize = 16;
+constexpr float kAlphaMin = 1.0f / 255.0f;
+constexpr float kAlphaMax = 0.99f;
+constexpr float kTransmittanceEps = 1e-4f;
+constexpr float kDilation2d = 0.3f;
+constexpr float kNearPlane = 0.01f;
+constexpr int kShCoeffs = 16;
+constexpr int kShValues = 48;
+constexpr float kInf = std::numeric_limits<float>::infinity();
+constexpr std::uint32_t kNoNode = 0xFFFFFFFFu;
+
+// status codes mirror errors.hpp:11-25 (+1; 0 = ok)
+enum Status : int {
+    kOk = 0,
+    kAllZeroWeights,
+    kDegenerateCovariance,
+    kNotSPD,
+    kMissingForwardState,
+    kNoInteriorNodes,
+    kDegenerateSpread,
+    kMalformedHeader,
+    kTruncatedRecord,
+    kUnsupportedShDegree,
+    kEmptyScene,
+    kDimensionMismatch,
+    kInvalidArgument,
+    kIoFailure,
+};
+
+struct Error {
+    int code;
+    std::string what;
+};
+[[noreturn]] inline void fail(int code, const std::string& what) { throw Error{code, what}; }
+inline void require(bool ok, int code, const std::string& what) {
+    if (!ok) fail(code, what);
+}
+
+// std::min/std::max semantics (algorithm: (b < a) ? b : a)
+inline float smin(float a, float b) { return (b < a) ? b : a; }
+inline float smax(float a, float b) { return (a < b) ? b : a; }
+// Eigen 3-term redux: x0 + (x1 + x2)
+inline float sum3(float a, float b, float c) { return a + (b + c); }
+// Eigen Vec4f SSE predux: (x0 + x2) + (x1 + x3)
+inline float sum4(float a, float b, float c, float d) { return (a + c) + (b + d); }
+
+// ---------------------------------------------------------------- parallel.hpp:13-45
+inline std::atomic<int>& thread_count_slot() {
+    static std::atomic<int> n{0};
+    return n;
+}
+inline int thread_count() {
+    int n = thread_count_slot().load();
+    if (n > 0) return n;
+    unsigned hw = std::thread::hardware_concurrency();
+    return hw == 0 ? 1 : static_cast<int>(hw);
+}
+inline void parallel_for(std::size_t n, const std::function<void(std::size_t, std::size_t)>& body) {
+    int workers = static_cast<int>(std::min<std::size_t>(thread_count(), n));
+    if (workers <= 1) {
+        if (n) body(0, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    pool.reserve(workers);
+    std::size_t chunk = (n + workers - 1) / workers;
+    for (int w = 0; w < workers; ++w) {
+        std::size_t lo = w * chunk;
+        std::size_t hi = std::min(n, lo + chunk);
+        if (lo >= hi) break;
+        pool.emplace_back([&body, lo, hi] { body(lo, hi); });
+    }
+    for (auto& t : pool) t.join();
+}
+
+// ---------------------------------------------------------------- model.hpp
+struct Aabb {
+    float mn[3];
+    float mx[3];
+    bool contains(const float p[3]) const {
+        return (p[0] >= mn[0] && p[1] >= mn[1] && p[2] >= mn[2]) &&
+               (p[0] <= mx[0] && p[1] <= mx[1] && p[2] <= mx[2]);
+    }
+    float largest_dim() const {
+        // extent().maxCoeff(): max(e0, max(e1, e2))
+        const float e0 = mx[0] - mn[0], e1 = mx[1] - mn[1], e2 = mx[2] - mn[2];
+        return smax(e0, smax(e1, e2));
+    }
+};
+
+// GaussianT<float> (model.hpp:21-48). Eigen::Quaternionf is 16-byte aligned
+// and stores (x, y, z, w); the alignas reproduces the reference's 304-byte
+// HierarchyNode stride so the CPU timing sees the same memory traffic.
+struct Gaussian {
+    float mean[3];
+    float scale[3];
+    alignas(16) float q_xyzw[4];
+    float falloff;
+    float sh[kShValues];
+};
+
+struct HierarchyNode {  // model.hpp:93-101
+    std::uint32_t parent = kNoNode;
+    std::uint32_t first_child = kNoNode;
+    std::uint32_t child_count = 0;
+    Aabb bounds;
+    Gaussian g;
+    bool is_leaf() const { return child_count == 0; }
+};
+
+struct Hierarchy {  // model.hpp:105-115
+    std::vector<HierarchyNode> nodes;
+    std::uint32_t sh_degree = 3;
+    std::size_t leaf_count() const {
+        std::size_t n = 0;
+        for (const auto& node : nodes) n += node.is_leaf();
+        return n;
+    }
+};
+
+struct Camera {  // model.hpp:64-82 (w2c row-major here; Eigen stores it column-major)
+    int width = 0, height = 0;
+    float fx = 0, fy = 0, cx = 0, cy = 0;
+    float w2c[3][4] = {};
+    // position() = -R^T t  (model.hpp:79): unary minus on R^T, then the 3-term product
+    void position(float p[3]) const {
+        for (int i = 0; i < 3; ++i)
+            p[i] = sum3((-w2c[0][i]) * w2c[0][3], (-w2c[1][i]) * w2c[1][3], (-w2c[2][i]) * w2c[2][3]);
+    }
+    float max_focal() const { return smax(fx, fy); }
+};
+
+inline void validate_camera(const Camera& c) {  // model.hpp:84-91
+    require(c.width > 0 && c.height > 0, kInvalidArgument, "camera resolution must be positive");
+    require(c.fx > 0.0f && c.fy > 0.0f, kInvalidArgument, "camera focal must be positive");
+    bool finite = true;
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 4; ++k) finite = finite && std::isfinite(c.w2c[r][k]);
+    require(finite, kInvalidArgument, "camera pose must be finite");
+    // (R R^T - I).norm() < 1e-3
+    float acc = 0.0f;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            float v = sum3(c.w2c[i][0] * c.w2c[j][0], c.w2c[i][1] * c.w2c[j][1], c.w2c[i][2] * c.w2c[j][2]);
+            v -= (i == j) ? 1.0f : 0.0f;
+            acc += v * v;
+        }
+    require(std::sqrt(acc) < 1e-3f, kInvalidArgument, "world_to_camera rotation block must be orthonormal");
+}
+
+struct CutEntry {  // model.hpp:144-148
+    std::uint32_t node = kNoNode;
+    float t = 1.0f;
+    float alpha_prime = 0.0f;
+};
+
+struct RenderSplat {  // model.hpp:157-177
+    float mean[3] = {0, 0, 0};
+    float scale[3] = {1, 1, 1};
+    alignas(16) float rot_wxyz[4] = {1, 0, 0, 0};
+    float sh[kShValues] = {};
+    float falloff = 1.0f;
+    float parent_falloff = 0.0f;
+    float t = 1.0f;
+    int transition_siblings = 1;
+
+    static RenderSplat plain(const Gaussian& g) {
+        RenderSplat s;
+        for (int k = 0; k < 3; ++k) s.mean[k] = g.mean[k], s.scale[k] = g.scale[k];
+        s.rot_wxyz[0] = g.q_xyzw[3];
+        s.rot_wxyz[1] = g.q_xyzw[0];
+        s.rot_wxyz[2] = g.q_xyzw[1];
+        s.rot_wxyz[3] = g.q_xyzw[2];
+        std::memcpy(s.sh, g.sh, sizeof(s.sh));
+        s.falloff = g.falloff;
+        return s;
+    }
+};
+
+// ---------------------------------------------------------------- lod.hpp
+inline float granularity(const Aabb& b, const Camera& cam) {  // lod.hpp:18-26
+    float pos[3];
+    cam.position(pos);
+    if (b.contains(pos)) return kInf;
+    float z = cam.w2c[2][3];
+    for (int k = 0; k < 3; ++k) z += smin(cam.w2c[2][k] * b.mn[k], cam.w2c[2][k] * b.mx[k]);
+    if (z <= kNearPlane) return kInf;
+    return cam.max_focal() * b.largest_dim() / z;
+}
+
+inline float interp_weight(float eps_node, float eps_parent, float tau) {  // lod.hpp:34-37
+    if (eps_parent == eps_node || eps_parent == kInf) return 1.0f;
+    float v = (eps_parent - tau) / (eps_parent - eps_node);
+    return smin(1.0f, smax(0.0f, v));  // clamp01 (math.hpp:93-94)
+}
+
+inline float transition_alpha(float parent_alpha, int siblings) {  // lod.hpp:41-45
+    require(siblings >= 1, kInvalidArgument, "transition_alpha needs K >= 1");
+    float a = smin(smax(parent_alpha, 0.0f), kAlphaMax);
+    return 1.0f - std::pow(1.0f - a, 1.0f / static_cast<float>(siblings));
+}
+
+inline std::vector<CutEntry> select_cut(const Hierarchy& h, const Camera& cam, float tau) {  // lod.hpp:52-92
+    require(tau >= 0.0f && !h.nodes.empty(), kInvalidArgument, "select_cut needs tau >= 0 and nodes");
+    const std::size_t n = h.nodes.size();
+    std::vector<float> eps(n);
+    parallel_for(n, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) eps[i] = granularity(h.nodes[i].bounds, cam);
+    });
+    std::vector<unsigned char> in_cut(n, 0);
+    std::vector<float> t_of(n, 1.0f);
+    parallel_for(n, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            const HierarchyNode& node = h.nodes[i];
+            bool fine_enough = eps[i] <= tau;
+            if (!fine_enough && !node.is_leaf()) continue;
+            float t = 1.0f;
+            if (node.parent != kNoNode) {
+                float eps_p = eps[node.parent];
+                if (!(eps_p > tau)) continue;
+                t = interp_weight(eps[i], eps_p, tau);
+            }
+            in_cut[i] = 1;
+            t_of[i] = t;
+        }
+    });
+    std::vector<CutEntry> cut;
+    for (std::size_t i = 0; i < n; ++i) {
+        if (!in_cut[i]) continue;
+        CutEntry e;
+        e.node = static_cast<std::uint32_t>(i);
+        e.t = t_of[i];
+        if (h.nodes[i].parent != kNoNode) {
+            const HierarchyNode& p = h.nodes[h.nodes[i].parent];
+            e.alpha_prime = transition_alpha(smin(p.g.falloff, kAlphaMax), static_cast<int>(p.child_count));
+        }
+        cut.push_back(e);
+    }
+    return cut;
+}
+
+// align_quat (math.hpp:86-88): Vec4 dot in wxyz storage order, SSE predux.
+inline void quat_wxyz(const Gaussian& g, float q[4]) {
+    q[0] = g.q_xyzw[3];
+    q[1] = g.q_xyzw[0];
+    q[2] = g.q_xyzw[1];
+    q[3] = g.q_xyzw[2];
+}
+
+inline std::vector<RenderSplat> assemble_cut_splats(const Hierarchy& h, const std::vector<Gaussian>& attrs,
+                                                    const CutEntry* cut, std::size_t ncut) {  // lod.hpp:116-146
+    require(attrs.size() == h.nodes.size(), kDimensionMismatch, "attribute array must parallel hierarchy nodes");
+    std::vector<RenderSplat> out;
+    out.reserve(ncut);
+    for (std::size_t c = 0; c < ncut; ++c) {
+        const CutEntry& e = cut[c];
+        const HierarchyNode& node = h.nodes[e.node];
+        const Gaussian& g = attrs[e.node];
+        if (node.parent == kNoNode || e.t >= 1.0f) {
+            out.push_back(RenderSplat::plain(g));
+            continue;
+        }
+        const Gaussian& p = attrs[node.parent];
+        const float u = e.t;
+        const float v = 1.0f - u;
+        RenderSplat s;
+        for (int k = 0; k < 3; ++k) s.mean[k] = u * g.mean[k] + v * p.mean[k];
+        for (int k = 0; k < 3; ++k) s.scale[k] = u * g.scale[k] + v * p.scale[k];
+        float qg[4], qp[4];
+        quat_wxyz(g, qg);
+        quat_wxyz(p, qp);
+        const float dot = sum4(qg[0] * qp[0], qg[1] * qp[1], qg[2] * qp[2], qg[3] * qp[3]);
+        if (dot < 0.0f)
+            for (int k = 0; k < 4; ++k) qg[k] = -qg[k];
+        for (int k = 0; k < 4; ++k) s.rot_wxyz[k] = u * qg[k] + v * qp[k];
+        for (int k = 0; k < kShValues; ++k) s.sh[k] = u * g.sh[k] + v * p.sh[k];
+        s.falloff = g.falloff;
+        s.parent_falloff = p.falloff;
+        s.t = e.t;
+        s.transition_siblings = static_cast<int>(h.nodes[node.parent].child_count);
+        out.push_back(s);
+    }
+    return out;
+}
+
+inline std::vector<RenderSplat> cut_render_splats(const Hierarchy& h, const CutEntry* cut, std::size_t ncut) {
+    std::vector<Gaussian> attrs;  // lod.hpp:149-151: copies every node's Gaussian first
+    attrs.reserve(h.nodes.size());
+    for (const auto& n : h.nodes) attrs.push_back(n.g);
+    return assemble_cut_splats(h, attrs, cut, ncut);
+}
+
+// ---------------------------------------------------------------- sh.hpp
+constexpr double kSh0 = 0.28209479177387814;
+constexpr double kSh1 = 0.4886025119029199;
+constexpr double kSh2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792,
+                            0.5462742152960396};
+constexpr double kSh3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
+                            -0.4570457994644658, 1.445305721320277,  -0.5900435899266435};
+
+inline void sh_basis(float x, float y, float z, float b[16]) {  // sh.hpp:20-42
+    const float xx = x * x, yy = y * y, zz = z * z;
+    b[0] = float(kSh0);
+    b[1] = float(-kSh1) * y;
+    b[2] = float(kSh1) * z;
+    b[3] = float(-kSh1) * x;
+    b[4] = float(kSh2[0]) * x * y;
+    b[5] = float(kSh2[1]) * y * z;
+    b[6] = float(kSh2[2]) * (2.0f * zz - xx - yy);
+    b[7] = float(kSh2[3]) * x * z;
+    b[8] = float(kSh2[4]) * (xx - yy);
+    b[9] = float(kSh3[0]) * y * (3.0f * xx - yy);
+    b[10] = float(kSh3[1]) * x * y * z;
+    b[11] = float(kSh3[2]) * y * (4.0f * zz - xx - yy);
+    b[12] = float(kSh3[3]) * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    b[13] = float(kSh3[4]) * x * (4.0f * zz - xx - yy);
+    b[14] = float(kSh3[5]) * z * (xx - yy);
+    b[15] = float(kSh3[6]) * x * (xx - 3.0f * yy);
+}
+
+// ---------------------------------------------------------------- render.hpp
+struct StageTimes {  // render.hpp:24-31
+    double cut_expand = 0, weights = 0, preprocess = 0, duplicate = 0, tile_ranges = 0, alpha_blend = 0;
+};
+
+class StageTimer {  // render.hpp:35-48
+public:
+    explicit StageTimer(double* slot) : slot_(slot), start_(std::chrono::steady_clock::now()) {}
+    ~StageTimer() {
+        if (slot_) *slot_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - start_).count();
+    }
+
+private:
+    double* slot_;
+    std::chrono::steady_clock::time_point start_;
+};
+
+struct Projected {  // render.hpp:52-73
+    bool culled = true;
+    float mean2d[2] = {0, 0};
+    float inv_depth = 0;
+    float cam_point[3] = {0, 0, 0};
+    float cov2d[4] = {0, 0, 0, 0};  // (00, 01, 10, 11)
+    float det_pre = 0, det_post = 0;
+    float conic[3] = {0, 0, 0};
+    float alpha_scale = 0;
+    float color[3] = {0, 0, 0};
+    int radius = 0;
+    int tx0 = 0, tx1 = 0, ty0 = 0, ty1 = 0;
+    float falloff_eff = 0, parent_falloff_eff = 0;
+    float t = 1.0f;
+    float inv_k = 1.0f;
+};
+
+// x86-64 cvttss2si: NaN, +-inf and out-of-range values produce INT_MIN.
+inline int f2i_x86(float v) {
+    if (!(v >= -2147483648.0f && v < 2147483648.0f)) return std::numeric_limits<int>::min();
+    return static_cast<int>(v);
+}
+inline int iclamp(int v, int lo, int hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+inline Projected project(const RenderSplat& s, const Camera& cam) {  // render.hpp:104-174
+    Projected p;
+    const float(&W)[3][4] = cam.w2c;
+    float tc[3];
+    for (int i = 0; i < 3; ++i) tc[i] = sum3(W[i][0] * s.mean[0], W[i][1] * s.mean[1], W[i][2] * s.mean[2]) + W[i][3];
+    if (!(tc[2] > kNearPlane)) return p;
+
+    const float* q4 = s.rot_wxyz;
+    const float qn = std::sqrt(sum4(q4[0] * q4[0], q4[1] * q4[1], q4[2] * q4[2], q4[3] * q4[3]));
+    if (!(qn > 0.0f)) return p;
+    const float w = q4[0] / qn, x = q4[1] / qn, y = q4[2] / qn, z = q4[3] / qn;
+    // Quaternion::toRotationMatrix (Eigen)
+    const float tx = 2.0f * x, ty = 2.0f * y, tz = 2.0f * z;
+    const float twx = tx * w, twy = ty * w, twz = tz * w;
+    const float txx = tx * x, txy = ty * x, txz = tz * x;
+    const float tyy = ty * y, tyz = tz * y, tzz = tz * z;
+    float r[3][3];
+    r[0][0] = 1.0f - (tyy + tzz);
+    r[0][1] = txy - twz;
+    r[0][2] = txz + twy;
+    r[1][0] = txy + twz;
+    r[1][1] = 1.0f - (txx + tzz);
+    r[1][2] = tyz - twx;
+    r[2][0] = txz - twy;
+    r[2][1] = tyz + twx;
+    r[2][2] = 1.0f - (txx + tyy);
+    float m[3][3];  // rot * diag(scale)
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) m[i][j] = r[i][j] * s.scale[j];
+    float S[3][3];  // m * m^T
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) S[i][j] = sum3(m[i][0] * m[j][0], m[i][1] * m[j][1], m[i][2] * m[j][2]);
+    float A[3][3];  // W_rot * S
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) A[i][j] = sum3(W[i][0] * S[0][j], W[i][1] * S[1][j], W[i][2] * S[2][j]);
+    float C[3][3];  // A * W_rot^T
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) C[i][j] = sum3(A[i][0] * W[j][0], A[i][1] * W[j][1], A[i][2] * W[j][2]);
+
+    const float fx = cam.fx, fy = cam.fy;
+    const float tzc = tc[2], tz2 = tzc * tzc;
+    const float J[2][3] = {{fx / tzc, 0.0f, -fx * tc[0] / tz2}, {0.0f, fy / tzc, -fy * tc[1] / tz2}};
+    float B[2][3];  // J * C
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 3; ++j) B[i][j] = sum3(J[i][0] * C[0][j], J[i][1] * C[1][j], J[i][2] * C[2][j]);
+    float P[2][2];  // B * J^T
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) P[i][j] = sum3(B[i][0] * J[j][0], B[i][1] * J[j][1], B[i][2] * J[j][2]);
+    float pre[2][2];
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) pre[i][j] = 0.5f * (P[i][j] + P[j][i]);
+    float post[2][2] = {{pre[0][0], pre[0][1]}, {pre[1][0], pre[1][1]}};
+    post[0][0] += kDilation2d;
+    post[1][1] += kDilation2d;
+    const float det_pre = pre[0][0] * pre[1][1] - pre[1][0] * pre[0][1];
+    const float det_post = post[0][0] * post[1][1] - post[1][0] * post[0][1];
+    if (!(det_post > 0.0f) || !std::isfinite(det_post)) return p;
+
+    p.mean2d[0] = fx * tc[0] / tzc + cam.cx;
+    p.mean2d[1] = fy * tc[1] / tzc + cam.cy;
+    p.inv_depth = 1.0f / tzc;
+    p.cam_point[0] = tc[0];
+    p.cam_point[1] = tc[1];
+    p.cam_point[2] = tc[2];
+    p.cov2d[0] = post[0][0];
+    p.cov2d[1] = post[0][1];
+    p.cov2d[2] = post[1][0];
+    p.cov2d[3] = post[1][1];
+    p.det_pre = det_pre;
+    p.det_post = det_post;
+    p.conic[0] = post[1][1] / det_post;
+    p.conic[1] = -post[0][1] / det_post;
+    p.conic[2] = post[0][0] / det_post;
+    p.alpha_scale = std::sqrt(smax(det_pre, 0.0f) / det_post);
+
+    const float mid = 0.5f * (post[0][0] + post[1][1]);
+    const float lmax = mid + std::sqrt(smax(0.0f, mid * mid - det_post));
+    p.radius = f2i_x86(std::ceil(3.0f * std::sqrt(lmax)));
+
+    const int tiles_x = (cam.width + kTileSize - 1) / kTileSize;
+    const int tiles_y = (cam.height + kTileSize - 1) / kTileSize;
+    const float rr = static_cast<float>(p.radius);
+    p.tx0 = iclamp(f2i_x86(std::floor((p.mean2d[0] - rr) / kTileSize)), 0, tiles_x);
+    p.tx1 = iclamp(f2i_x86(std::floor((p.mean2d[0] + rr) / kTileSize)) + 1, 0, tiles_x);
+    p.ty0 = iclamp(f2i_x86(std::floor((p.mean2d[1] - rr) / kTileSize)), 0, tiles_y);
+    p.ty1 = iclamp(f2i_x86(std::floor((p.mean2d[1] + rr) / kTileSize)) + 1, 0, tiles_y);
+    if (p.tx0 >= p.tx1 || p.ty0 >= p.ty1) return p;
+
+    float campos[3];
+    cam.position(campos);
+    float d[3] = {s.mean[0] - campos[0], s.mean[1] - campos[1], s.mean[2] - campos[2]};
+    const float n2 = sum3(d[0] * d[0], d[1] * d[1], d[2] * d[2]);
+    if (n2 > 0.0f) {
+        const float sn = std::sqrt(n2);
+        d[0] = d[0] / sn;
+        d[1] = d[1] / sn;
+        d[2] = d[2] / sn;
+    }
+    float b[16];
+    sh_basis(d[0], d[1], d[2], b);
+    float c[3] = {0.5f, 0.5f, 0.5f};
+    for (int k = 0; k < kShCoeffs; ++k)
+        for (int ch = 0; ch < 3; ++ch) c[ch] += b[k] * s.sh[k * 3 + ch];
+    for (int ch = 0; ch < 3; ++ch) p.color[ch] = smax(c[ch], 0.0f);
+
+    p.falloff_eff = smax(s.falloff, 0.0f);
+    p.parent_falloff_eff = smax(s.parent_falloff, 0.0f);
+    p.t = s.t;
+    p.inv_k = 1.0f / static_cast<float>(std::max(1, s.transition_siblings));
+    p.culled = false;
+    return p;
+}
+
+struct PixelAlpha {
+    bool skip = true;
+    float alpha = 0.0f;
+};
+
+inline PixelAlpha splat_alpha(const Projected& p, float px, float py) {  // render.hpp:201-231
+    PixelAlpha r;
+    const float dx = px - p.mean2d[0];
+    const float dy = py - p.mean2d[1];
+    const float power = -0.5f * (p.conic[0] * dx * dx + p.conic[2] * dy * dy) - p.conic[1] * dx * dy;
+    if (!(power <= 0.0f)) return r;
+    const float g = std::exp(power);
+    const float self_raw = p.falloff_eff * p.alpha_scale * g;
+    const float self = self_raw > kAlphaMax ? kAlphaMax : self_raw;
+    const float a_self = self >= kAlphaMin ? self : 0.0f;
+    if (p.t < 1.0f) {
+        const float par_raw = p.parent_falloff_eff * p.alpha_scale * g;
+        const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
+        float split = 0.0f;
+        if (par >= kAlphaMin) split = 1.0f - std::pow(1.0f - par, p.inv_k);
+        r.alpha = p.t * a_self + (1.0f - p.t) * split;
+    } else {
+        r.alpha = a_self;
+    }
+    r.skip = !(r.alpha > 0.0f);
+    return r;
+}
+
+struct RenderOutput {
+    int width = 0, height = 0;
+    std::vector<float> color;  // 3 x H x W, plane-major (image.hpp:21)
+    std::vector<float> depth;  // H x W
+    std::vector<float> transmittance;
+    int rendered_count = 0;
+    // ForwardContext retention (render.hpp:87-98, :339-352) for parity dumps
+    std::vector<Projected> projected;
+    std::vector<std::uint32_t> order;
+    std::vector<std::size_t> tile_start;
+    std::vector<std::uint32_t> tile_entries;
+    int tiles_x = 0, tiles_y = 0;
+};
+
+inline void render_forward(const RenderSplat* splats, std::size_t n, const Camera& cam, RenderOutput& out,
+                           StageTimes* stages, bool keep_ctx) {  // render.hpp:244-354
+    validate_camera(cam);
+    const int w = cam.width, h = cam.height;
+    const int tiles_x = (w + kTileSize - 1) / kTileSize;
+    const int tiles_y = (h + kTileSize - 1) / kTileSize;
+
+    std::vector<Projected> projected(n);
+    {
+        StageTimer timer(stages ? &stages->preprocess : nullptr);
+        parallel_for(n, [&](std::size_t lo, std::size_t hi) {
+            for (std::size_t i = lo; i < hi; ++i) projected[i] = project(splats[i], cam);
+        });
+    }
+    std::vector<std::uint32_t> order;
+    std::vector<std::size_t> tile_start(static_cast<std::size_t>(tiles_x) * tiles_y + 1, 0);
+    std::vector<std::uint32_t> tile_entries;
+    {
+        StageTimer timer(stages ? &stages->duplicate : nullptr);
+        order.reserve(n);
+        for (std::uint32_t i = 0; i < n; ++i)
+            if (!projected[i].culled) order.push_back(i);
+        std::stable_sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
+            return projected[a].cam_point[2] < projected[b].cam_point[2];
+        });
+        for (std::uint32_t id : order) {
+            const auto& p = projected[id];
+            for (int ty = p.ty0; ty < p.ty1; ++ty)
+                for (int tx = p.tx0; tx < p.tx1; ++tx) tile_start[ty * tiles_x + tx + 1]++;
+        }
+    }
+    {
+        StageTimer timer(stages ? &stages->tile_ranges : nullptr);
+        for (std::size_t t = 1; t < tile_start.size(); ++t) tile_start[t] += tile_start[t - 1];
+        tile_entries.resize(tile_start.back());
+    }
+    {
+        StageTimer timer(stages ? &stages->duplicate : nullptr);
+        std::vector<std::size_t> cursor(tile_start.begin(), tile_start.end() - 1);
+        for (std::uint32_t id : order) {
+            const auto& p = projected[id];
+            for (int ty = p.ty0; ty < p.ty1; ++ty)
+                for (int tx = p.tx0; tx < p.tx1; ++tx) tile_entries[cursor[ty * tiles_x + tx]++] = id;
+        }
+    }
+    out.width = w;
+    out.height = h;
+    const std::size_t plane = static_cast<std::size_t>(w) * h;
+    out.color.assign(3 * plane, 0.0f);
+    out.depth.assign(plane, 0.0f);
+    out.transmittance.assign(plane, 1.0f);
+    out.rendered_count = 0;
+    std::vector<unsigned char> touched(n, 0);
+    {
+        StageTimer timer(stages ? &stages->alpha_blend : nullptr);
+        const std::size_t n_tiles = static_cast<std::size_t>(tiles_x) * tiles_y;
+        parallel_for(n_tiles, [&](std::size_t lo, std::size_t hi) {
+            for (std::size_t tile = lo; tile < hi; ++tile) {
+                const int bx = static_cast<int>(tile % tiles_x) * kTileSize;
+                const int by = static_cast<int>(tile / tiles_x) * kTileSize;
+                const std::size_t begin = tile_start[tile], end = tile_start[tile + 1];
+                for (int y = by; y < std::min(by + kTileSize, h); ++y) {
+                    for (int x = bx; x < std::min(bx + kTileSize, w); ++x) {
+                        const float px = static_cast<float>(x) + 0.5f;
+                        const float py = static_cast<float>(y) + 0.5f;
+                        float trans = 1.0f;
+                        float c0 = 0, c1 = 0, c2 = 0, d = 0;
+                        for (std::size_t e = begin; e < end; ++e) {
+                            const std::uint32_t id = tile_entries[e];
+                            const auto& p = projected[id];
+                            auto a = splat_alpha(p, px, py);
+                            if (a.skip) continue;
+                            const float test = trans * (1.0f - a.alpha);
+                            if (test < kTransmittanceEps) break;
+                            const float wgt = a.alpha * trans;
+                            c0 += p.color[0] * wgt;
+                            c1 += p.color[1] * wgt;
+                            c2 += p.color[2] * wgt;
+                            d += p.inv_depth * a.alpha * trans;
+                            trans = test;
+                            std::atomic_ref<unsigned char>(touched[id]).store(1, std::memory_order_relaxed);
+                        }
+                        const std::size_t px_i = static_cast<std::size_t>(y) * w + x;
+                        out.color[px_i] = c0;
+                        out.color[plane + px_i] = c1;
+                        out.color[2 * plane + px_i] = c2;
+                        out.depth[px_i] = d;
+                        out.transmittance[px_i] = trans;
+                    }
+                }
+            }
+        });
+    }
+    for (unsigned char f : touched) out.rendered_count += f;
+    out.tiles_x = tiles_x;
+    out.tiles_y = tiles_y;
+    if (keep_ctx) {
+        out.projected = std::move(projected);
+        out.order = std::move(order);
+        out.tile_start = std::move(tile_start);
+        out.tile_entries = std::move(tile_entries);
+    }
+}
+
+inline void render_reference(const RenderSplat* splats, std::size_t n, const Camera& cam,
+                             RenderOutput& out) {  // render.hpp:360-408
+    validate_camera(cam);
+    const int w = cam.width, h = cam.height;
+    std::vector<Projected> projected(n);
+    for (std::size_t i = 0; i < n; ++i) projected[i] = project(splats[i], cam);
+    std::vector<std::uint32_t> order;
+    for (std::uint32_t i = 0; i < n; ++i)
+        if (!projected[i].culled) order.push_back(i);
+    std::stable_sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
+        return projected[a].cam_point[2] < projected[b].cam_point[2];
+    });
+    out.width = w;
+    out.height = h;
+    const std::size_t plane = static_cast<std::size_t>(w) * h;
+    out.color.assign(3 * plane, 0.0f);
+    out.depth.assign(plane, 0.0f);
+    out.transmittance.assign(plane, 1.0f);
+    std::vector<unsigned char> touched(n, 0);
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            const int tx = x / kTileSize, ty = y / kTileSize;
+            const float px = static_cast<float>(x) + 0.5f, py = static_cast<float>(y) + 0.5f;
+            float trans = 1.0f, c0 = 0, c1 = 0, c2 = 0, d = 0;
+            for (std::uint32_t id : order) {
+                const auto& p = projected[id];
+                if (tx < p.tx0 || tx >= p.tx1 || ty < p.ty0 || ty >= p.ty1) continue;
+                auto a = splat_alpha(p, px, py);
+                if (a.skip) continue;
+                const float test = trans * (1.0f - a.alpha);
+                if (test < kTransmittanceEps) break;
+                const float wgt = a.alpha * trans;
+                c0 += p.color[0] * wgt;
+                c1 += p.color[1] * wgt;
+                c2 += p.color[2] * wgt;
+                d += p.inv_depth * a.alpha * trans;
+                trans = test;
+                touched[id] = 1;
+            }
+            const std::size_t px_i = static_cast<std::size_t>(y) * w + x;
+            out.color[px_i] = c0;
+            out.color[plane + px_i] = c1;
+            out.color[2 * plane + px_i] = c2;
+            out.depth[px_i] = d;
+            out.transmittance[px_i] = trans;
+        }
+    out.rendered_count = 0;
+    for (unsigned char f : touched) out.rendered_count += f;
+}
+
+inline void render_hierarchy(const Hierarchy& h, const Camera& cam, float tau, RenderOutput& out,
+                             StageTimes* stages, bool keep_ctx, std::vector<CutEntry>* cut_out) {  // render.hpp:706-720
+    std::vector<CutEntry> cut;
+    {
+        StageTimer timer(stages ? &stages->cut_expand : nullptr);
+        cut = select_cut(h, cam, tau);
+    }
+    std::vector<RenderSplat> splats;
+    {
+        StageTimer timer(stages ? &stages->weights : nullptr);
+        splats = cut_render_splats(h, cut.data(), cut.size());
+    }
+    render_forward(splats.data(), splats.size(), cam, out, stages, keep_ctx);
+    if (cut_out) *cut_out = std::move(cut);
+}
+
+}  // namespace oracle
+
+// =====================================================================
+// extern "C" surface for tests (ctypes).  Structures mirror the product's
+// C ABI (include/hsplat_b200.h) so tests feed identical host buffers to both.
+// =====================================================================
+using namespace oracle;
+
+extern "C" {
+
+typedef struct {
+    int32_t width, height;
+    float fx, fy, cx, cy;
+    float w2c[12];  // row-major 3x4 [R|t]
+} or_camera;
+
+typedef struct {
+    const uint32_t* parent;
+    const uint32_t* first_child;
+    const uint32_t* child_count;
+    const float* bmin;      // 3N
+    const float* bmax;      // 3N
+    const float* mean;      // 3N
+    const float* scale;     // 3N
+    const float* rot_wxyz;  // 4N
+    const float* falloff;   // N
+    const float* sh;        // 48N
+} or_nodes;
+
+typedef struct {
+    const float* mean;      // 3N
+    const float* scale;     // 3N
+    const float* rot_wxyz;  // 4N
+    const float* sh;        // 48N
+    const float* falloff;   // N
+    const float* parent_falloff;  // N
+    const float* t;         // N
+    const int32_t* siblings;  // N
+} or_splats;
+
+typedef struct {
+    double cut_expand, weights, preprocess, duplicate, tile_ranges, alpha_blend;
+} or_stage_times;
+
+static thread_local std::string g_err;
+const char* or_last_error() { return g_err.c_str(); }
+
+#define OR_TRY(...)                  \
+    try {                            \
+        __VA_ARGS__;                 \
+        return 0;                    \
+    } catch (const Error& e) {       \
+        g_err = e.what;              \
+        return e.code;               \
+    } catch (const std::exception& e) { \
+        g_err = e.what();            \
+        return kIoFailure;           \
+    }
+
+static Camera to_cam(const or_camera* c) {
+    Camera cam;
+    cam.width = c->width;
+    cam.height = c->height;
+    cam.fx = c->fx;
+    cam.fy = c->fy;
+    cam.cx = c->cx;
+    cam.cy = c->cy;
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 4; ++k) cam.w2c[r][k] = c->w2c[r * 4 + k];
+    return cam;
+}
+
+void or_set_thread_count(int n) { thread_count_slot().store(n); }
+int or_thread_count() { return thread_count(); }
+
+float or_granularity(const float* bmin, const float* bmax, const or_camera* c) {
+    Aabb b;
+    for (int k = 0; k < 3; ++k) b.mn[k] = bmin[k], b.mx[k] = bmax[k];
+    return granularity(b, to_cam(c));
+}
+float or_interp_weight(float en, float ep, float tau) { return interp_weight(en, ep, tau); }
+int or_transition_alpha(float a, int k, float* out) { OR_TRY(*out = transition_alpha(a, k)); }
+float or_expf(float x) { return std::exp(x); }
+float or_powf(float x, float y) { return std::pow(x, y); }
+int or_validate_camera(const or_camera* c) { OR_TRY(validate_camera(to_cam(c))); }
+
+// Hierarchy handle: the reference's AoS std::vector<HierarchyNode>.
+void* or_hierarchy_create(const or_nodes* s, uint64_t n) {
+    auto* h = new Hierarchy();
+    h->nodes.resize(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        HierarchyNode& nd = h->nodes[i];
+        nd.parent = s->parent[i];
+        nd.first_child = s->first_child[i];
+        nd.child_count = s->child_count[i];
+        for (int k = 0; k < 3; ++k) {
+            nd.bounds.mn[k] = s->bmin[3 * i + k];
+            nd.bounds.mx[k] = s->bmax[3 * i + k];
+            nd.g.mean[k] = s->mean[3 * i + k];
+            nd.g.scale[k] = s->scale[3 * i + k];
+        }
+        nd.g.q_xyzw[3] = s->rot_wxyz[4 * i + 0];
+        nd.g.q_xyzw[0] = s->rot_wxyz[4 * i + 1];
+        nd.g.q_xyzw[1] = s->rot_wxyz[4 * i + 2];
+        nd.g.q_xyzw[2] = s->rot_wxyz[4 * i + 3];
+        nd.g.falloff = s->falloff[i];
+        std::memcpy(nd.g.sh, s->sh + 48 * i, 48 * sizeof(float));
+    }
+    return h;
+}
+void or_hierarchy_free(void* h) { delete static_cast<Hierarchy*>(h); }
+uint64_t or_hierarchy_leaf_count(void* h) { return static_cast<Hierarchy*>(h)->leaf_count(); }
+
+// select_cut: caller passes capacity n (node count); *count receives the cut size.
+int or_select_cut(void* hv, const or_camera* c, float tau, uint32_t* node, float* t, float* alpha, uint64_t* count,
+                  double* seconds) {
+    OR_TRY({
+        auto t0 = std::chrono::steady_clock::now();
+        auto cut = select_cut(*static_cast<Hierarchy*>(hv), to_cam(c), tau);
+        if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *count = cut.size();
+        for (std::size_t i = 0; i < cut.size(); ++i) {
+            if (node) node[i] = cut[i].node;
+            if (t) t[i] = cut[i].t;
+            if (alpha) alpha[i] = cut[i].alpha_prime;
+        }
+    });
+}
+
+static void splats_to_soa(const std::vector<RenderSplat>& sp, float* mean, float* scale, float* rot, float* sh,
+                          float* falloff, float* pfall, float* t, int32_t* sib) {
+    for (std::size_t i = 0; i < sp.size(); ++i) {
+        const RenderSplat& s = sp[i];
+        for (int k = 0; k < 3; ++k) mean[3 * i + k] = s.mean[k], scale[3 * i + k] = s.scale[k];
+        for (int k = 0; k < 4; ++k) rot[4 * i + k] = s.rot_wxyz[k];
+        std::memcpy(sh + 48 * i, s.sh, 48 * sizeof(float));
+        falloff[i] = s.falloff;
+        pfall[i] = s.parent_falloff;
+        t[i] = s.t;
+        sib[i] = s.transition_siblings;
+    }
+}
+
+// cut_render_splats on a given cut (node, t, alpha) of length ncut.
+int or_cut_render_splats(void* hv, const uint32_t* node, const float* t, const float* alpha, uint64_t ncut,
+                         float* mean, float* scale, float* rot, float* sh, float* falloff, float* pfall, float* tt,
+                         int32_t* sib) {
+    OR_TRY({
+        std::vector<CutEntry> cut(ncut);
+        for (uint64_t i = 0; i < ncut; ++i) cut[i] = CutEntry{node[i], t[i], alpha ? alpha[i] : 0.0f};
+        auto sp = cut_render_splats(*static_cast<Hierarchy*>(hv), cut.data(), cut.size());
+        splats_to_soa(sp, mean, scale, rot, sh, falloff, pfall, tt, sib);
+    });
+}
+
+static std::vector<RenderSplat> soa_to_splats(const or_splats* s, uint64_t n) {
+    std::vector<RenderSplat> v(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        RenderSplat& r = v[i];
+        for (int k = 0; k < 3; ++k) r.mean[k] = s->mean[3 * i + k], r.scale[k] = s->scale[3 * i + k];
+        for (int k = 0; k < 4; ++k) r.rot_wxyz[k] = s->rot_wxyz[4 * i + k];
+        std::memcpy(r.sh, s->sh + 48 * i, 48 * sizeof(float));
+        r.falloff = s->falloff[i];
+        r.parent_falloff = s->parent_falloff[i];
+        r.t = s->t[i];
+        r.transition_siblings = s->siblings[i];
+    }
+    return v;
+}
+
+// Projected per-splat record for parity dumps (16 floats):
+// culled, zbits-as-float(cam z), mean2d x/y, conic 0/1/2, alpha_scale, color rgb,
+// inv_depth, radius, tx0, tx1, ty0, ty1 (ints stored as float bit patterns? no: as floats)
+static void dump_projected(const std::vector<Projected>& pr, float* out16) {
+    for (std::size_t i = 0; i < pr.size(); ++i) {
+        const Projected& p = pr[i];
+        float* o = out16 + 16 * i;
+        o[0] = p.culled ? 1.0f : 0.0f;
+        o[1] = p.cam_point[2];
+        o[2] = p.mean2d[0];
+        o[3] = p.mean2d[1];
+        o[4] = p.conic[0];
+        o[5] = p.conic[1];
+        o[6] = p.conic[2];
+        o[7] = p.alpha_scale;
+        o[8] = p.color[0];
+        o[9] = p.color[1];
+        o[10] = p.color[2];
+        o[11] = p.inv_depth;
+        std::memcpy(&o[12], &p.radius, 4);
+        int rect = (p.tx0 & 0xff) | ((p.tx1 & 0xff) << 8) | ((p.ty0 & 0xff) << 16) | ((p.ty1 & 0xff) << 24);
+        std::memcpy(&o[13], &rect, 4);
+        std::memcpy(&o[14], &p.tx0, 4);
+        std::memcpy(&o[15], &p.ty0, 4);
+    }
+}
+
+struct OrFrame {
+    RenderOutput out;
+    std::vector<CutEntry> cut;
+    StageTimes times;
+};
+
+void* or_frame_new() { return new OrFrame(); }
+void or_frame_free(void* f) { delete static_cast<OrFrame*>(f); }
+
+int or_render_forward(const or_splats* s, uint64_t n, const or_camera* c, void* fv, int keep_ctx) {
+    OR_TRY({
+        auto* f = static_cast<OrFrame*>(fv);
+        auto sp = soa_to_splats(s, n);
+        f->times = StageTimes{};
+        render_forward(sp.data(), sp.size(), to_cam(c), f->out, &f->times, keep_ctx != 0);
+    });
+}
+
+int or_render_reference(const or_splats* s, uint64_t n, const or_camera* c, void* fv) {
+    OR_TRY({
+        auto* f = static_cast<OrFrame*>(fv);
+        auto sp = soa_to_splats(s, n);
+        render_reference(sp.data(), sp.size(), to_cam(c), f->out);
+    });
+}
+
+int or_render_hierarchy(void* hv, const or_camera* c, float tau, void* fv, int keep_ctx) {
+    OR_TRY({
+        auto* f = static_cast<OrFrame*>(fv);
+        f->times = StageTimes{};
+        render_hierarchy(*static_cast<Hierarchy*>(hv), to_cam(c), tau, f->out, &f->times, keep_ctx != 0, &f->cut);
+    });
+}
+
+// sizes: [width, height, tiles_x, tiles_y, n_projected, n_order, n_entries, rendered_count, ncut]
+void or_frame_sizes(void* fv, uint64_t* sz) {
+    auto* f = static_cast<OrFrame*>(fv);
+    sz[0] = f->out.width;
+    sz[1] = f->out.height;
+    sz[2] = f->out.tiles_x;
+    sz[3] = f->out.tiles_y;
+    sz[4] = f->out.projected.size();
+    sz[5] = f->out.order.size();
+    sz[6] = f->out.tile_entries.size();
+    sz[7] = static_cast<uint64_t>(f->out.rendered_count);
+    sz[8] = f->cut.size();
+}
+void or_frame_images(void* fv, float* color, float* depth, float* trans) {
+    auto* f = static_cast<OrFrame*>(fv);
+    if (color) std::memcpy(color, f->out.color.data(), f->out.color.size() * 4);
+    if (depth) std::memcpy(depth, f->out.depth.data(), f->out.depth.size() * 4);
+    if (trans) std::memcpy(trans, f->out.transmittance.data(), f->out.transmittance.size() * 4);
+}
+void or_frame_ctx(void* fv, uint64_t* tile_start, uint32_t* tile_entries, uint32_t* order, float* proj16) {
+    auto* f = static_cast<OrFrame*>(fv);
+    if (tile_start)
+        for (std::size_t i = 0; i < f->out.tile_start.size(); ++i) tile_start[i] = f->out.tile_start[i];
+    if (tile_entries) std::memcpy(tile_entries, f->out.tile_entries.data(), f->out.tile_entries.size() * 4);
+    if (order) std::memcpy(order, f->out.order.data(), f->out.order.size() * 4);
+    if (proj16) dump_projected(f->out.projected, proj16);
+}
+void or_frame_cut(void* fv, uint32_t* node, float* t, float* alpha) {
+    auto* f = static_cast<OrFrame*>(fv);
+    for (std::size_t i = 0; i < f->cut.size(); ++i) {
+        node[i] = f->cut[i].node;
+        t[i] = f->cut[i].t;
+        alpha[i] = f->cut[i].alpha_prime;
+    }
+}
+void or_frame_times(void* fv, or_stage_times* t) {
+    auto* f = static_cast<OrFrame*>(fv);
+    t->cut_expand = f->times.cut_expand;
+    t->weights = f->times.weights;
+    t->preprocess = f->times.preprocess;
+    t->duplicate = f->times.duplicate;
+    t->tile_ranges = f->times.tile_ranges;
+    t->alpha_blend = f->times.alpha_blend;
+}
+
+// project() of one splat (render.hpp:105); out16 as dump_projected.
+int or_project(const or_splats* s, const or_camera* c, float* out16, float* cov4, float* dets) {
+    OR_TRY({
+        auto sp = soa_to_splats(s, 1);
+        Projected p = project(sp[0], to_cam(c));
+        std::vector<Projected> v{p};
+        dump_projected(v, out16);
+        if (cov4)
+            for (int k = 0; k < 4; ++k) cov4[k] = p.cov2d[k];
+        if (dets) dets[0] = p.det_pre, dets[1] = p.det_post;
+    });
+}
+
+// bench_path (bench.hpp:55-103).  Per frame: rendered, rendered_pct, transferred,
+// 6 stage seconds -> stats[9*i ...].
+int or_bench_path(void* hv, const or_camera* cams, uint64_t ncam, const double* timestamps, uint64_t nts, float tau,
+                  double* stats) {
+    OR_TRY({
+        const Hierarchy& h = *static_cast<Hierarchy*>(hv);
+        require(ncam > 0, kInvalidArgument, "camera path is empty");
+        require(nts == 0 || nts == ncam, kDimensionMismatch, "one timestamp per camera");
+        (void)timestamps;
+        const double leaf_count = static_cast<double>(h.leaf_count());
+        std::vector<CutEntry> cut;
+        std::vector<RenderSplat> splats;
+        std::set<std::uint32_t> prev;
+        RenderOutput out;
+        for (uint64_t i = 0; i < ncam; ++i) {
+            StageTimes st;
+            std::size_t transferred = 0;
+            const Camera cam = to_cam(&cams[i]);
+            if (i % 2 == 0) {
+                {
+                    StageTimer timer(&st.cut_expand);
+                    cut = select_cut(h, cam, tau);
+                }
+                {
+                    StageTimer timer(&st.weights);
+                    splats = cut_render_splats(h, cut.data(), cut.size());
+                }
+                std::set<std::uint32_t> cur;
+                for (const CutEntry& e : cut) cur.insert(e.node);
+                for (std::uint32_t nd : cur) transferred += prev.count(nd) == 0;
+                prev = std::move(cur);
+            }
+            render_forward(splats.data(), splats.size(), cam, out, &st, false);
+            double* o = stats + 9 * i;
+            o[0] = static_cast<double>(cut.size());
+            o[1] = 100.0 * static_cast<double>(cut.size()) / leaf_count;
+            o[2] = static_cast<double>(transferred);
+            o[3] = st.cut_expand;
+            o[4] = st.weights;
+            o[5] = st.preprocess;
+            o[6] = st.duplicate;
+            o[7] = st.tile_ranges;
+            o[8] = st.alpha_blend;
+        }
+    });
+}
+
+// psnr (image.hpp:111-122): over all channels in double; mse <= 0 -> 99 dB; capped at 99.
+double or_psnr(const float* a, const float* b, uint64_t n) {
+    double mse = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        double d = static_cast<double>(a[i]) - static_cast<double>(b[i]);
+        mse += d * d;
+    }
+    mse /= static_cast<double>(n);
+    if (mse <= 0.0) return 99.0;
+    return static_cast<double>(static_cast<float>(std::min(99.0, -10.0 * std::log10(mse))));
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+"""ctypes binding of the C ABI in include/hsplat_b200.h (libhsplat_b200.so).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2406_12080_b200/csrc``).  There is no fallback: if the library
+is missing, importing the renderer raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhsplat_b200.so")
+
+u32p = C.POINTER(C.c_uint32)
+f32p = C.POINTER(C.c_float)
+i32p = C.POINTER(C.c_int32)
+u64p = C.POINTER(C.c_uint64)
+
+
+class hs_camera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("w2c", C.c_float * 12)]
+
+
+class hs_node_soa(C.Structure):
+    _fields_ = [("parent", u32p), ("first_child", u32p), ("child_count", u32p), ("bmin", f32p), ("bmax", f32p),
+                ("mean", f32p), ("scale", f32p), ("rot_wxyz", f32p), ("falloff", f32p), ("sh", f32p)]
+
+
+hs_node_soa_out = hs_node_soa  # identical layout (mutable pointers)
+
+
+class hs_splat_soa(C.Structure):
+    _fields_ = [("mean", f32p), ("scale", f32p), ("rot_wxyz", f32p), ("sh", f32p), ("falloff", f32p),
+                ("parent_falloff", f32p), ("t", f32p), ("siblings", i32p)]
+
+
+hs_splat_soa_out = hs_splat_soa
+
+
+class hs_stage_times(C.Structure):
+    _fields_ = [("cut_expand", C.c_double), ("weights", C.c_double), ("preprocess", C.c_double),
+                ("duplicate", C.c_double), ("tile_ranges", C.c_double), ("alpha_blend", C.c_double)]
+
+
+class hs_frame_info(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
+                ("n_splats", C.c_uint64), ("n_visible", C.c_uint64), ("n_duplicates", C.c_uint64),
+                ("rendered_count", C.c_int32), ("sort_passes", C.c_int32)]
+
+
+HS_OPT_ASYNC = 1
+HS_OPT_BLEND_MODE = 2
+HS_OPT_DEBUG = 3
+
+# every symbol include/hsplat_b200.h declares: name -> (restype, argtypes)
+_vp = C.c_void_p
+_SIGS = {
+    "hs_status_name": (C.c_char_p, [C.c_int]),
+    "hs_context_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "hs_context_destroy": (None, [_vp]),
+    "hs_last_error": (C.c_char_p, [_vp]),
+    "hs_context_stream": (_vp, [_vp]),
+    "hs_context_synchronize": (C.c_int, [_vp]),
+    "hs_context_set_option": (C.c_int, [_vp, C.c_int, C.c_int64]),
+    "hs_hierarchy_upload": (C.c_int, [_vp, C.POINTER(hs_node_soa), C.c_uint64, C.c_uint32, C.c_int,
+                                      C.POINTER(_vp)]),
+    "hs_hierarchy_load_h3dg": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
+    "hs_hierarchy_destroy": (None, [_vp]),
+    "hs_hierarchy_node_count": (C.c_uint64, [_vp]),
+    "hs_hierarchy_leaf_count": (C.c_uint64, [_vp]),
+    "hs_cut_create": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "hs_cut_destroy": (None, [_vp]),
+    "hs_select_cut": (C.c_int, [_vp, _vp, C.POINTER(hs_camera), C.c_float, _vp]),
+    "hs_cut_size": (C.c_int, [_vp, _vp, u64p]),
+    "hs_cut_download": (C.c_int, [_vp, _vp, u32p, f32p, f32p]),
+    "hs_cut_upload": (C.c_int, [_vp, _vp, u32p, f32p, f32p, C.c_uint64, _vp]),
+    "hs_cut_render_splats": (C.c_int, [_vp, _vp, _vp, C.POINTER(hs_splat_soa)]),
+    "hs_frame_create": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "hs_frame_destroy": (None, [_vp]),
+    "hs_render_hierarchy": (C.c_int, [_vp, _vp, C.POINTER(hs_camera), C.c_float, _vp, _vp,
+                                      C.POINTER(hs_stage_times)]),
+    "hs_render_cut": (C.c_int, [_vp, _vp, _vp, C.POINTER(hs_camera), _vp, C.POINTER(hs_stage_times)]),
+    "hs_render_splats": (C.c_int, [_vp, C.POINTER(hs_splat_soa), C.c_uint64, C.POINTER(hs_camera), _vp,
+                                   C.POINTER(hs_stage_times)]),
+    "hs_frame_wait": (C.c_int, [_vp, _vp]),
+    "hs_frame_get_info": (C.c_int, [_vp, _vp, C.POINTER(hs_frame_info)]),
+    "hs_frame_download": (C.c_int, [_vp, _vp, f32p, f32p, f32p, i32p]),
+    "hs_frame_debug": (C.c_int, [_vp, _vp, u64p, u64p, u32p, u64p, u32p, f32p]),
+    "hs_synth_node_count": (C.c_uint64, [C.c_uint64]),
+    "hs_synth_scene_side": (C.c_float, [C.c_uint64]),
+    "hs_synth_city": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.POINTER(hs_node_soa)]),
+    "hs_build_bvh": (C.c_int, [f32p, f32p, f32p, f32p, f32p, C.c_uint64, C.c_int, C.POINTER(hs_node_soa)]),
+    "hs_h3dg_read_header":(C.c_int, [C.c_char_p, u64p, C.POINTER(C.c_uint32)]),
+    "hs_h3dg_read": (C.c_int, [C.c_char_p, C.POINTER(hs_node_soa), C.c_uint64]),
+    "hs_h3dg_write": (C.c_int, [C.c_char_p, C.POINTER(hs_node_soa), C.c_uint64, C.c_uint32]),
+    "hs_validate_hierarchy": (C.c_int, [C.POINTER(hs_node_soa), C.c_uint64, C.c_char_p, C.c_size_t]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libhsplat_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (the CUDA path has no fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def ptr(a: np.ndarray | None, ctype):
+    if a is None:
+        return C.cast(None, C.POINTER(ctype))
+    assert a.flags["C_CONTIGUOUS"], "arrays passed to the C ABI must be contiguous"
+    return a.ctypes.data_as(C.POINTER(ctype))

@@ -1,0 +1,858 @@
+// api.cu — the C ABI (include/hsplat_b200.h): contexts, device-resident
+// hierarchies, cuts and frames, and the per-frame launch sequence.
+//
+// Frame = k_select_cut -> k_preprocess -> k_scan -> k_duplicate -> radix sort
+// -> k_ranges -> k_blend -> k_count_touched, all on the context stream with no
+// host synchronisation in between: every data-dependent size (C, D) is read
+// by the kernels from device memory, so the sequence is a fixed launch list.
+// The only host round trip is the final 40-byte stats read that tells the
+// caller the frame is complete (and whether the duplicate buffer overflowed,
+// in which case a synchronous call grows it and re-runs the raster stages).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hs_device.cuh"
+#include "hs_kernels.h"
+#include "hsplat_b200_internal.h"
+
+using hs::CamParams;
+using hs::ProjRec;
+
+namespace {
+
+const char* kErrcNames[] = {"Ok",
+                            "AllZeroWeights",
+                            "DegenerateCovariance",
+                            "NotSPD",
+                            "MissingForwardState",
+                            "NoInteriorNodes",
+                            "DegenerateSpread",
+                            "MalformedHeader",
+                            "TruncatedRecord",
+                            "UnsupportedShDegree",
+                            "EmptyScene",
+                            "DimensionMismatch",
+                            "InvalidArgument",
+                            "IoFailure"};
+
+struct DevStats {
+    uint64_t n_splats;             // C
+    unsigned long long n_visible;  // V
+    uint64_t n_dup;                // D
+    uint64_t sort_n;               // D if it fits the duplicate buffers, else 0
+    unsigned long long rendered;   // rendered_count
+    unsigned long long pad[2];
+    unsigned long long overflows;  // sticky: frames whose D exceeded capacity since the last wait
+};
+
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t ensure(size_t need) {
+        if (need <= bytes && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, std::max<size_t>(need, 256));
+        if (e == cudaSuccess) bytes = std::max<size_t>(need, 256);
+        return e;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace
+
+struct hs_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    bool async = false;
+    int blend_mode = 0;
+    bool debug = false;
+    DBuf cut_scratch;
+};
+
+struct hs_hierarchy {
+    hs_context* ctx = nullptr;
+    uint64_t n = 0, leaves = 0;
+    uint32_t sh_degree = 3;
+    DBuf cull_a, cull_b, attr;
+};
+
+struct hs_cut {
+    hs_context* ctx = nullptr;
+    uint64_t cap = 0;
+    DBuf node, t, alpha, count;
+    uint64_t* h_count = nullptr;  // pinned
+    const hs_hierarchy* h = nullptr;
+    cudaEvent_t done = nullptr;
+    ~hs_cut() {
+        if (h_count) cudaFreeHost(h_count);
+        if (done) cudaEventDestroy(done);
+    }
+};
+
+struct hs_frame {
+    hs_context* ctx = nullptr;
+    uint64_t cap_splats = 0, cap_dup = 0;
+    int W = 0, H = 0, tiles_x = 0, tiles_y = 0, passes = 0;
+    DBuf proj, dupcount, offsets, keys[2], vals[2], dupk, dupv, ranges, color, depth, trans, touched, dbg16,
+        splat_attr, stats, scratch;
+    DevStats* h_stats = nullptr;  // pinned
+    uint64_t* h_n = nullptr;      // pinned
+    cudaEvent_t ev[6] = {};
+    cudaEvent_t done = nullptr;
+    bool pending = false, timed = false, have_result = false;
+    hs_stage_times* times = nullptr;
+    bool cut_timed = false;
+    hs_cut* own_cut = nullptr;
+    // last raster call (for an overflow re-run)
+    bool from_cut = false;
+    const float4* attr = nullptr;
+    const uint32_t* cut_node = nullptr;
+    const float* cut_t = nullptr;
+    const uint64_t* n_ptr = nullptr;
+    uint64_t n_max = 0;
+    CamParams cam{};
+    ~hs_frame() {
+        if (h_stats) cudaFreeHost(h_stats);
+        if (h_n) cudaFreeHost(h_n);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (done) cudaEventDestroy(done);
+        delete own_cut;
+    }
+};
+
+namespace {
+
+hs_status set_err(hs_context* ctx, hs_status s, const std::string& msg) {
+    if (ctx) {
+        const char* name = (s >= 0 && s <= HS_IO_FAILURE) ? kErrcNames[s] : (s == HS_OUT_OF_MEMORY ? "OutOfMemory"
+                                                                             : s == HS_CAPACITY_EXCEEDED
+                                                                                 ? "CapacityExceeded"
+                                                                                 : "CudaError");
+        ctx->err = std::string(name) + ": " + msg;
+    }
+    return s;
+}
+
+hs_status cuda_err(hs_context* ctx, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return HS_OK;
+    cudaGetLastError();
+    return set_err(ctx, e == cudaErrorMemoryAllocation ? HS_OUT_OF_MEMORY : HS_CUDA_ERROR,
+                   std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define HS_CUDA(ctx, call)                                     \
+    do {                                                       \
+        cudaError_t e__ = (call);                              \
+        if (e__ != cudaSuccess) return cuda_err(ctx, e__, #call); \
+    } while (0)
+
+// Stream-ordered copy that returns when the bytes have landed.
+hs_status copy_sync(hs_context* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    if (!bytes) return HS_OK;
+    HS_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, kind, ctx->stream));
+    HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return HS_OK;
+}
+
+#define HS_TRY(expr)                  \
+    do {                              \
+        hs_status s__ = (expr);       \
+        if (s__ != HS_OK) return s__; \
+    } while (0)
+
+inline float hmin(float a, float b) { return (b < a) ? b : a; }
+inline float hmax(float a, float b) { return (a < b) ? b : a; }
+
+// validate_camera (model.hpp:84-91)
+hs_status validate_camera(hs_context* ctx, const hs_camera* c) {
+    if (!(c->width > 0 && c->height > 0)) return set_err(ctx, HS_INVALID_ARGUMENT, "camera resolution must be positive");
+    if (!(c->fx > 0.0f && c->fy > 0.0f)) return set_err(ctx, HS_INVALID_ARGUMENT, "camera focal must be positive");
+    for (int i = 0; i < 12; ++i)
+        if (!std::isfinite(c->w2c[i])) return set_err(ctx, HS_INVALID_ARGUMENT, "camera pose must be finite");
+    float acc = 0.0f;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            float v = c->w2c[4 * i] * c->w2c[4 * j] + (c->w2c[4 * i + 1] * c->w2c[4 * j + 1] +
+                                                        c->w2c[4 * i + 2] * c->w2c[4 * j + 2]);
+            v -= (i == j) ? 1.0f : 0.0f;
+            acc += v * v;
+        }
+    if (!(std::sqrt(acc) < 1e-3f))
+        return set_err(ctx, HS_INVALID_ARGUMENT, "world_to_camera rotation block must be orthonormal");
+    return HS_OK;
+}
+
+CamParams make_cam(const hs_camera* c) {
+    CamParams p{};
+    std::memcpy(p.w2c, c->w2c, sizeof(p.w2c));
+    p.fx = c->fx;
+    p.fy = c->fy;
+    p.cx = c->cx;
+    p.cy = c->cy;
+    // position() = (-R^T) t, Eigen 3-term order (model.hpp:79)
+    for (int i = 0; i < 3; ++i)
+        p.pos[i] = (-c->w2c[i]) * c->w2c[3] + ((-c->w2c[4 + i]) * c->w2c[7] + (-c->w2c[8 + i]) * c->w2c[11]);
+    p.maxf = hmax(c->fx, c->fy);
+    p.width = c->width;
+    p.height = c->height;
+    p.tiles_x = (c->width + hs::kTile - 1) / hs::kTile;
+    p.tiles_y = (c->height + hs::kTile - 1) / hs::kTile;
+    return p;
+}
+
+int sort_passes_for(int tiles) {
+    int tb = 0;
+    while ((1ll << tb) < tiles) ++tb;
+    return (32 + tb + 7) / 8;
+}
+
+uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+// Layout of the per-frame scratch (zeroed once per frame):
+//   [0]        scan tile counter (u32) + pad
+//   [64]       sort counters (8 x u32)
+//   [128]      sort histogram (8 x 256 u32)
+//   [8320]     scan status (u64 words)
+//   [...]      sort status (passes x sort_status_words u32)
+struct ScratchLayout {
+    size_t scan_counter = 0, sort_counters = 64, sort_hist = 128, scan_status = 8320, sort_status = 0, total = 0;
+};
+ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int passes) {
+    ScratchLayout L;
+    L.sort_status = round_up(L.scan_status + hs::scan_status_words(n_max) * 8, 256);
+    L.total = L.sort_status + (size_t)passes * hs::sort_status_words(cap_dup) * 4;
+    return L;
+}
+
+hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamParams& cp) {
+    const int tiles = cp.tiles_x * cp.tiles_y;
+    if (f->cap_splats < n_max) f->cap_splats = n_max;
+    if (f->cap_dup == 0) f->cap_dup = std::max<uint64_t>(1 << 20, 4 * n_max);
+    const uint64_t cs = std::max<uint64_t>(f->cap_splats, 1);
+    HS_CUDA(ctx, f->proj.ensure(cs * sizeof(ProjRec)));
+    HS_CUDA(ctx, f->dupcount.ensure(cs * 4));
+    HS_CUDA(ctx, f->offsets.ensure(cs * 4));
+    const bool fresh_touched = f->touched.bytes < cs;
+    HS_CUDA(ctx, f->touched.ensure(cs));
+    if (fresh_touched) HS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, f->touched.bytes, ctx->stream));
+    for (int b = 0; b < 2; ++b) {
+        HS_CUDA(ctx, f->keys[b].ensure(f->cap_dup * 8));
+        HS_CUDA(ctx, f->vals[b].ensure(f->cap_dup * 4));
+    }
+    if (ctx->debug) {
+        HS_CUDA(ctx, f->dupk.ensure(f->cap_dup * 8));
+        HS_CUDA(ctx, f->dupv.ensure(f->cap_dup * 4));
+        HS_CUDA(ctx, f->dbg16.ensure(cs * 64));
+    }
+    HS_CUDA(ctx, f->ranges.ensure((size_t)tiles * 8));
+    const size_t plane = (size_t)cp.width * cp.height;
+    HS_CUDA(ctx, f->color.ensure(plane * 12));
+    HS_CUDA(ctx, f->depth.ensure(plane * 4));
+    HS_CUDA(ctx, f->trans.ensure(plane * 4));
+    HS_CUDA(ctx, f->stats.ensure(sizeof(DevStats)));
+    f->passes = sort_passes_for(tiles);
+    HS_CUDA(ctx, f->scratch.ensure(scratch_layout(f->cap_splats, f->cap_dup, f->passes).total));
+    if (!f->h_stats) HS_CUDA(ctx, cudaMallocHost(&f->h_stats, sizeof(DevStats)));
+    if (!f->h_n) HS_CUDA(ctx, cudaMallocHost(&f->h_n, 8));
+    for (auto& e : f->ev)
+        if (!e) HS_CUDA(ctx, cudaEventCreate(&e));
+    if (!f->done) HS_CUDA(ctx, cudaEventCreateWithFlags(&f->done, cudaEventDisableTiming));
+    f->W = cp.width;
+    f->H = cp.height;
+    f->tiles_x = cp.tiles_x;
+    f->tiles_y = cp.tiles_y;
+    return HS_OK;
+}
+
+// Enqueue the raster stages (preprocess .. count) for the call stored in f.
+hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
+    cudaStream_t s = ctx->stream;
+    const CamParams& cp = f->cam;
+    DevStats* ds = f->stats.as<DevStats>();
+    const ScratchLayout L = scratch_layout(f->cap_splats, f->cap_dup, f->passes);
+    unsigned char* sc = f->scratch.as<unsigned char>();
+    HS_CUDA(ctx, cudaMemsetAsync(sc, 0, L.total, s));
+    HS_CUDA(ctx, cudaMemsetAsync(&ds->n_visible, 0, offsetof(DevStats, overflows) - 8, s));
+    if (f->from_cut) HS_CUDA(ctx, cudaMemcpyAsync(&ds->n_splats, f->n_ptr, 8, cudaMemcpyDeviceToDevice, s));
+    HS_CUDA(ctx, cudaMemsetAsync(f->ranges.p, 0, (size_t)cp.tiles_x * cp.tiles_y * 8, s));
+    if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[1], s));
+    hs::launch_preprocess(f->from_cut, f->attr, f->cut_node, f->cut_t, f->n_ptr, f->n_max, cp, f->proj.as<ProjRec>(),
+                          f->dupcount.as<uint32_t>(), ctx->debug ? f->dbg16.as<float>() : nullptr, &ds->n_visible, s);
+    if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[2], s));
+    hs::launch_scan(f->dupcount.as<uint32_t>(), f->n_ptr, f->n_max, f->offsets.as<uint32_t>(),
+                    reinterpret_cast<uint64_t*>(sc + L.scan_status), reinterpret_cast<uint32_t*>(sc + L.scan_counter),
+                    &ds->n_dup, &ds->sort_n, f->cap_dup, &ds->overflows, s);
+    hs::launch_duplicate(f->proj.as<ProjRec>(), f->dupcount.as<uint32_t>(), f->offsets.as<uint32_t>(), f->n_ptr,
+                         f->n_max, &ds->sort_n, cp.tiles_x, f->keys[0].as<uint64_t>(), f->vals[0].as<uint32_t>(), s);
+    if (ctx->debug) {
+        HS_CUDA(ctx, cudaMemcpyAsync(f->dupk.p, f->keys[0].p, f->cap_dup * 8, cudaMemcpyDeviceToDevice, s));
+        HS_CUDA(ctx, cudaMemcpyAsync(f->dupv.p, f->vals[0].p, f->cap_dup * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    uint64_t* kb[2] = {f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>()};
+    uint32_t* vb[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
+    hs::launch_radix_sort(kb, vb, &ds->sort_n, f->cap_dup, f->passes, reinterpret_cast<uint32_t*>(sc + L.sort_hist),
+                          reinterpret_cast<uint32_t*>(sc + L.sort_status),
+                          reinterpret_cast<uint32_t*>(sc + L.sort_counters), s);
+    if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[3], s));
+    const int fin = f->passes & 1;
+    hs::launch_ranges(kb[fin], &ds->sort_n, f->cap_dup, f->ranges.as<uint2>(), s);
+    if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[4], s));
+    hs::launch_blend(ctx->blend_mode, f->ranges.as<uint2>(), vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
+                     f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(), s);
+    hs::launch_count_touched(f->touched.as<uint8_t>(), f->n_ptr, f->n_max, &ds->rendered, s);
+    if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[5], s));
+    HS_CUDA(ctx, cudaGetLastError());
+    HS_CUDA(ctx, cudaMemcpyAsync(f->h_stats, ds, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    HS_CUDA(ctx, cudaEventRecord(f->done, s));
+    f->pending = true;
+    return HS_OK;
+}
+
+hs_status finish_frame(hs_context* ctx, hs_frame* f, bool allow_retry) {
+    if (!f->pending) return HS_OK;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        HS_CUDA(ctx, cudaEventSynchronize(f->done));
+        f->pending = false;
+        const DevStats st = *f->h_stats;
+        if (st.overflows > 0 && !allow_retry) {
+            HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, ctx->stream));
+            return set_err(ctx, HS_CAPACITY_EXCEEDED,
+                           std::to_string(st.overflows) +
+                               " async frame(s) overflowed the duplicate buffer; render once synchronously to grow it");
+        }
+        if (st.n_dup > 0 && st.sort_n == 0) {
+            HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, ctx->stream));
+            if (!allow_retry)
+                return set_err(ctx, HS_CAPACITY_EXCEEDED,
+                               "duplicate buffer too small (" + std::to_string(st.n_dup) + " > " +
+                                   std::to_string(f->cap_dup) + "); render once synchronously to grow it");
+            f->cap_dup = st.n_dup + st.n_dup / 4 + 1024;
+            if (f->cap_dup >= (1ull << 31))
+                return set_err(ctx, HS_CAPACITY_EXCEEDED, "more than 2^31 duplicated keys in one frame");
+            hs_status s = ensure_frame(ctx, f, f->n_max, f->cam);
+            if (s != HS_OK) return s;
+            s = enqueue_raster(ctx, f);
+            if (s != HS_OK) return s;
+            continue;
+        }
+        f->have_result = true;
+        if (f->timed && f->times) {
+            float ms[5] = {0, 0, 0, 0, 0};
+            if (f->cut_timed) cudaEventElapsedTime(&ms[0], f->ev[0], f->ev[1]);
+            cudaEventElapsedTime(&ms[1], f->ev[1], f->ev[2]);
+            cudaEventElapsedTime(&ms[2], f->ev[2], f->ev[3]);
+            cudaEventElapsedTime(&ms[3], f->ev[3], f->ev[4]);
+            cudaEventElapsedTime(&ms[4], f->ev[4], f->ev[5]);
+            f->times->cut_expand += ms[0] * 1e-3;
+            f->times->preprocess += ms[1] * 1e-3;
+            f->times->duplicate += ms[2] * 1e-3;
+            f->times->tile_ranges += ms[3] * 1e-3;
+            f->times->alpha_blend += ms[4] * 1e-3;
+        }
+        return HS_OK;
+    }
+    return set_err(ctx, HS_CAPACITY_EXCEEDED, "duplicate buffer kept overflowing");
+}
+
+hs_status ensure_cut(hs_context* ctx, hs_cut* cut, uint64_t cap) {
+    if (cut->cap < cap) {
+        HS_CUDA(ctx, cut->node.ensure(cap * 4));
+        HS_CUDA(ctx, cut->t.ensure(cap * 4));
+        HS_CUDA(ctx, cut->alpha.ensure(cap * 4));
+        cut->cap = cap;
+    }
+    HS_CUDA(ctx, cut->count.ensure(8));
+    if (!cut->h_count) HS_CUDA(ctx, cudaMallocHost(&cut->h_count, 8));
+    if (!cut->done) HS_CUDA(ctx, cudaEventCreateWithFlags(&cut->done, cudaEventDisableTiming));
+    return HS_OK;
+}
+
+hs_status enqueue_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cam, float tau, hs_cut* cut) {
+    if (!(tau >= 0.0f) || h->n == 0)
+        return set_err(ctx, HS_INVALID_ARGUMENT, "select_cut needs tau >= 0 and nodes");  // lod.hpp:53
+    hs_status st = ensure_cut(ctx, cut, h->n);
+    if (st != HS_OK) return st;
+    const uint64_t words = hs::select_cut_status_words(h->n);
+    HS_CUDA(ctx, ctx->cut_scratch.ensure(64 + words * 8));
+    unsigned char* sc = ctx->cut_scratch.as<unsigned char>();
+    HS_CUDA(ctx, cudaMemsetAsync(sc, 0, 64 + words * 8, ctx->stream));
+    const CamParams cp = make_cam(cam);
+    hs::launch_select_cut(h->cull_a.as<float4>(), h->cull_b.as<float4>(), h->attr.as<float4>(), h->n, cp, tau,
+                          cut->node.as<uint32_t>(), cut->t.as<float>(), cut->alpha.as<float>(),
+                          reinterpret_cast<uint64_t*>(sc + 64), reinterpret_cast<uint32_t*>(sc),
+                          cut->count.as<uint64_t>(), ctx->stream);
+    HS_CUDA(ctx, cudaGetLastError());
+    HS_CUDA(ctx, cudaMemcpyAsync(cut->h_count, cut->count.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    HS_CUDA(ctx, cudaEventRecord(cut->done, ctx->stream));
+    cut->h = h;
+    return HS_OK;
+}
+
+// Pack host SoA node arrays [lo, hi) into the device layout (hs_device.cuh).
+void pack_nodes(const hs_node_soa* s, uint64_t lo, uint64_t hi, float4* ca, float4* cb, float4* at) {
+    for (uint64_t i = lo; i < hi; ++i) {
+        const uint64_t k = i - lo;
+        float4* a = at + 16 * k;
+        ca[k] = make_float4(s->bmin[3 * i], s->bmin[3 * i + 1], s->bmin[3 * i + 2], s->bmax[3 * i]);
+        float pbits, ccbits, fcbits;
+        std::memcpy(&pbits, &s->parent[i], 4);
+        std::memcpy(&ccbits, &s->child_count[i], 4);
+        std::memcpy(&fcbits, &s->first_child[i], 4);
+        cb[k] = make_float4(s->bmax[3 * i + 1], s->bmax[3 * i + 2], pbits, ccbits);
+        a[0] = make_float4(s->mean[3 * i], s->mean[3 * i + 1], s->mean[3 * i + 2], s->falloff[i]);
+        a[1] = make_float4(s->scale[3 * i], s->scale[3 * i + 1], s->scale[3 * i + 2], pbits);
+        a[2] = make_float4(s->rot_wxyz[4 * i], s->rot_wxyz[4 * i + 1], s->rot_wxyz[4 * i + 2], s->rot_wxyz[4 * i + 3]);
+        std::memcpy(&a[3], s->sh + 48 * i, 48 * 4);
+        a[15] = make_float4(ccbits, fcbits, 0.0f, 0.0f);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hs_status_name(hs_status s) {
+    if (s >= 0 && s <= HS_IO_FAILURE) return kErrcNames[s];
+    switch (s) {
+        case HS_CUDA_ERROR: return "CudaError";
+        case HS_OUT_OF_MEMORY: return "OutOfMemory";
+        case HS_NO_DEVICE: return "NoDevice";
+        case HS_CAPACITY_EXCEEDED: return "CapacityExceeded";
+        default: return "Unknown";
+    }
+}
+
+hs_status hs_context_create(int device, hs_context** out) {
+    if (!out) return HS_INVALID_ARGUMENT;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return HS_NO_DEVICE;
+    }
+    if (device < 0 || device >= count) return HS_INVALID_ARGUMENT;
+    if (cudaSetDevice(device) != cudaSuccess) return HS_CUDA_ERROR;
+    auto* ctx = new hs_context();
+    ctx->device = device;
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return HS_CUDA_ERROR;
+    }
+    *out = ctx;
+    return HS_OK;
+}
+
+void hs_context_destroy(hs_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStream_t st = ctx->stream;
+    delete ctx;
+    cudaStreamDestroy(st);
+}
+
+const char* hs_last_error(const hs_context* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+void* hs_context_stream(hs_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+hs_status hs_context_synchronize(hs_context* ctx) {
+    HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return HS_OK;
+}
+
+hs_status hs_context_set_option(hs_context* ctx, int option, int64_t value) {
+    switch (option) {
+        case HS_OPT_ASYNC: ctx->async = value != 0; return HS_OK;
+        case HS_OPT_BLEND_MODE:
+            if (value != 0 && value != 1) return set_err(ctx, HS_INVALID_ARGUMENT, "blend mode is 0 (exact) or 1 (fast)");
+            ctx->blend_mode = (int)value;
+            return HS_OK;
+        case HS_OPT_DEBUG: ctx->debug = value != 0; return HS_OK;
+        default: return set_err(ctx, HS_INVALID_ARGUMENT, "unknown option");
+    }
+}
+
+// ------------------------------------------------------------------ hierarchy
+hs_status hs_hierarchy_upload(hs_context* ctx, const hs_node_soa* nodes, uint64_t n, uint32_t sh_degree, int validate,
+                              hs_hierarchy** out) {
+    if (!ctx || !nodes || !out) return HS_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (n == 0) return set_err(ctx, HS_INVALID_ARGUMENT, "hierarchy has no nodes");
+    if (n >= 0xFFFFFFFFull) return set_err(ctx, HS_INVALID_ARGUMENT, "node indices must fit in 32 bits");
+    if (sh_degree > 3) return set_err(ctx, HS_UNSUPPORTED_SH_DEGREE, "SH degree above 3 is not supported");
+    if (validate) {
+        char msg[256] = {0};
+        hs_status v = hs_validate_hierarchy(nodes, n, msg, sizeof(msg));
+        if (v != HS_OK) return set_err(ctx, v, msg);
+    }
+    cudaSetDevice(ctx->device);
+    auto* h = new hs_hierarchy();
+    h->ctx = ctx;
+    h->n = n;
+    h->sh_degree = sh_degree;
+    auto fail = [&](hs_status s) {
+        delete h;
+        return s;
+    };
+    cudaError_t e;
+    if ((e = h->cull_a.ensure(n * 16)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc cull_a"));
+    if ((e = h->cull_b.ensure(n * 16)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc cull_b"));
+    if ((e = h->attr.ensure(n * 256)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc attributes"));
+    const uint64_t chunk = 1 << 18;
+    const size_t stage_bytes = chunk * (16 + 16 + 256);
+    unsigned char* stage[2] = {nullptr, nullptr};
+    if ((e = cudaMallocHost(&stage[0], stage_bytes)) != cudaSuccess) return fail(cuda_err(ctx, e, "pinned staging"));
+    if ((e = cudaMallocHost(&stage[1], stage_bytes)) != cudaSuccess) {
+        cudaFreeHost(stage[0]);
+        return fail(cuda_err(ctx, e, "pinned staging"));
+    }
+    cudaEvent_t evs[2];
+    cudaEventCreateWithFlags(&evs[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&evs[1], cudaEventDisableTiming);
+    uint64_t leaves = 0;
+    int b = 0;
+    for (uint64_t lo = 0; lo < n; lo += chunk, b ^= 1) {
+        const uint64_t hi = std::min(n, lo + chunk), m = hi - lo;
+        cudaEventSynchronize(evs[b]);
+        float4* ca = reinterpret_cast<float4*>(stage[b]);
+        float4* cb = ca + chunk;
+        float4* at = cb + chunk;
+        pack_nodes(nodes, lo, hi, ca, cb, at);
+        for (uint64_t i = lo; i < hi; ++i) leaves += nodes->child_count[i] == 0;
+        cudaMemcpyAsync(h->cull_a.as<float4>() + lo, ca, m * 16, cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemcpyAsync(h->cull_b.as<float4>() + lo, cb, m * 16, cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemcpyAsync(h->attr.as<float4>() + 16 * lo, at, m * 256, cudaMemcpyHostToDevice, ctx->stream);
+        cudaEventRecord(evs[b], ctx->stream);
+    }
+    e = cudaStreamSynchronize(ctx->stream);
+    cudaEventDestroy(evs[0]);
+    cudaEventDestroy(evs[1]);
+    cudaFreeHost(stage[0]);
+    cudaFreeHost(stage[1]);
+    if (e != cudaSuccess) return fail(cuda_err(ctx, e, "hierarchy upload"));
+    h->leaves = leaves;
+    *out = h;
+    return HS_OK;
+}
+
+void hs_hierarchy_destroy(hs_hierarchy* h) {
+    if (!h) return;
+    cudaSetDevice(h->ctx->device);
+    cudaStreamSynchronize(h->ctx->stream);
+    delete h;
+}
+uint64_t hs_hierarchy_node_count(const hs_hierarchy* h) { return h ? h->n : 0; }
+uint64_t hs_hierarchy_leaf_count(const hs_hierarchy* h) { return h ? h->leaves : 0; }
+
+// ------------------------------------------------------------------ cut
+hs_status hs_cut_create(hs_context* ctx, hs_cut** out) {
+    if (!ctx || !out) return HS_INVALID_ARGUMENT;
+    auto* c = new hs_cut();
+    c->ctx = ctx;
+    *out = c;
+    return HS_OK;
+}
+void hs_cut_destroy(hs_cut* cut) {
+    if (!cut) return;
+    cudaStreamSynchronize(cut->ctx->stream);
+    delete cut;
+}
+
+hs_status hs_select_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cam, float tau, hs_cut* cut) {
+    if (!ctx || !h || !cam || !cut) return HS_INVALID_ARGUMENT;
+    hs_status s = enqueue_cut(ctx, h, cam, tau, cut);
+    if (s != HS_OK) return s;
+    if (!ctx->async) HS_CUDA(ctx, cudaEventSynchronize(cut->done));
+    return HS_OK;
+}
+
+hs_status hs_cut_size(hs_context* ctx, const hs_cut* cut, uint64_t* n) {
+    if (!cut->done) {
+        *n = 0;
+        return HS_OK;
+    }
+    HS_CUDA(ctx, cudaEventSynchronize(cut->done));
+    *n = *cut->h_count;
+    return HS_OK;
+}
+
+hs_status hs_cut_download(hs_context* ctx, const hs_cut* cut, uint32_t* node, float* t, float* alpha) {
+    uint64_t n = 0;
+    hs_status s = hs_cut_size(ctx, cut, &n);
+    if (s != HS_OK || n == 0) return s;
+    if (node) HS_TRY(copy_sync(ctx, node, cut->node.p, n * 4, cudaMemcpyDeviceToHost));
+    if (t) HS_TRY(copy_sync(ctx, t, cut->t.p, n * 4, cudaMemcpyDeviceToHost));
+    if (alpha) HS_TRY(copy_sync(ctx, alpha, cut->alpha.p, n * 4, cudaMemcpyDeviceToHost));
+    return HS_OK;
+}
+
+hs_status hs_cut_upload(hs_context* ctx, const hs_hierarchy* h, const uint32_t* node, const float* t,
+                        const float* alpha, uint64_t n, hs_cut* cut) {
+    for (uint64_t i = 0; i < n; ++i)
+        if (node[i] >= h->n) return set_err(ctx, HS_INVALID_ARGUMENT, "cut node index out of range");
+    hs_status s = ensure_cut(ctx, cut, std::max<uint64_t>(n, 1));
+    if (s != HS_OK) return s;
+    HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (n) {
+        HS_TRY(copy_sync(ctx, cut->node.p, node, n * 4, cudaMemcpyHostToDevice));
+        HS_TRY(copy_sync(ctx, cut->t.p, t, n * 4, cudaMemcpyHostToDevice));
+        if (alpha)
+            HS_TRY(copy_sync(ctx, cut->alpha.p, alpha, n * 4, cudaMemcpyHostToDevice));
+        else
+            HS_CUDA(ctx, cudaMemsetAsync(cut->alpha.p, 0, n * 4, ctx->stream));
+    }
+    *cut->h_count = n;
+    HS_TRY(copy_sync(ctx, cut->count.p, &n, 8, cudaMemcpyHostToDevice));
+    HS_CUDA(ctx, cudaEventRecord(cut->done, ctx->stream));
+    cut->h = h;
+    return HS_OK;
+}
+
+// ------------------------------------------------------------------ frames
+hs_status hs_frame_create(hs_context* ctx, hs_frame** out) {
+    if (!ctx || !out) return HS_INVALID_ARGUMENT;
+    auto* f = new hs_frame();
+    f->ctx = ctx;
+    *out = f;
+    return HS_OK;
+}
+void hs_frame_destroy(hs_frame* f) {
+    if (!f) return;
+    cudaStreamSynchronize(f->ctx->stream);
+    delete f;
+}
+
+static hs_status render_from_cut(hs_context* ctx, const hs_hierarchy* h, const hs_cut* cut, const hs_camera* cam,
+                                 hs_frame* f, hs_stage_times* times, bool cut_timed) {
+    const CamParams cp = make_cam(cam);
+    hs_status s = ensure_frame(ctx, f, cut->cap, cp);
+    if (s != HS_OK) return s;
+    f->cam = cp;
+    f->from_cut = true;
+    f->attr = h->attr.as<float4>();
+    f->cut_node = cut->node.as<uint32_t>();
+    f->cut_t = cut->t.as<float>();
+    f->n_ptr = cut->count.as<uint64_t>();
+    f->n_max = cut->cap;
+    f->times = times;
+    f->timed = times != nullptr;
+    f->cut_timed = cut_timed;
+    s = enqueue_raster(ctx, f);
+    if (s != HS_OK) return s;
+    if (!ctx->async) return finish_frame(ctx, f, true);
+    return HS_OK;
+}
+
+hs_status hs_render_hierarchy(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cam, float tau, hs_cut* cut,
+                              hs_frame* f, hs_stage_times* times) {
+    if (!ctx || !h || !cam || !f) return HS_INVALID_ARGUMENT;
+    if (f->pending && !ctx->async) {
+        hs_status s = finish_frame(ctx, f, false);
+        if (s != HS_OK) return s;
+    }
+    if (!cut) {
+        if (!f->own_cut) {
+            f->own_cut = new hs_cut();
+            f->own_cut->ctx = ctx;
+        }
+        cut = f->own_cut;
+    }
+    hs_status s = HS_OK;
+    if (times) {
+        s = ensure_frame(ctx, f, std::max<uint64_t>(h->n, 1), make_cam(cam));
+        if (s != HS_OK) return s;
+        HS_CUDA(ctx, cudaEventRecord(f->ev[0], ctx->stream));
+    }
+    s = enqueue_cut(ctx, h, cam, tau, cut);
+    if (s != HS_OK) return s;
+    // select_cut does not validate the camera; render_forward does (render.hpp:248)
+    s = validate_camera(ctx, cam);
+    if (s != HS_OK) return s;
+    return render_from_cut(ctx, h, cut, cam, f, times, times != nullptr);
+}
+
+hs_status hs_render_cut(hs_context* ctx, const hs_hierarchy* h, const hs_cut* cut, const hs_camera* cam, hs_frame* f,
+                        hs_stage_times* times) {
+    if (!ctx || !h || !cut || !cam || !f) return HS_INVALID_ARGUMENT;
+    if (cut->cap == 0) return set_err(ctx, HS_INVALID_ARGUMENT, "cut has not been selected");
+    if (f->pending && !ctx->async) {
+        hs_status s = finish_frame(ctx, f, false);
+        if (s != HS_OK) return s;
+    }
+    hs_status s = validate_camera(ctx, cam);
+    if (s != HS_OK) return s;
+    return render_from_cut(ctx, h, cut, cam, f, times, false);
+}
+
+hs_status hs_render_splats(hs_context* ctx, const hs_splat_soa* sp, uint64_t n, const hs_camera* cam, hs_frame* f,
+                           hs_stage_times* times) {
+    if (!ctx || !cam || !f || (n && !sp)) return HS_INVALID_ARGUMENT;
+    if (n >= 0xFFFFFFFFull) return set_err(ctx, HS_INVALID_ARGUMENT, "too many splats");
+    if (f->pending && !ctx->async) {
+        hs_status s = finish_frame(ctx, f, false);
+        if (s != HS_OK) return s;
+    }
+    hs_status s = validate_camera(ctx, cam);
+    if (s != HS_OK) return s;
+    const CamParams cp = make_cam(cam);
+    s = ensure_frame(ctx, f, std::max<uint64_t>(n, 1), cp);
+    if (s != HS_OK) return s;
+    HS_CUDA(ctx, f->splat_attr.ensure(std::max<uint64_t>(n, 1) * 256));
+    HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (n) {
+        std::vector<float4> rec(n * 16);
+        for (uint64_t i = 0; i < n; ++i) {
+            float4* a = rec.data() + 16 * i;
+            float kbits;
+            std::memcpy(&kbits, &sp->siblings[i], 4);
+            a[0] = make_float4(sp->mean[3 * i], sp->mean[3 * i + 1], sp->mean[3 * i + 2], sp->falloff[i]);
+            a[1] = make_float4(sp->scale[3 * i], sp->scale[3 * i + 1], sp->scale[3 * i + 2], sp->parent_falloff[i]);
+            a[2] = make_float4(sp->rot_wxyz[4 * i], sp->rot_wxyz[4 * i + 1], sp->rot_wxyz[4 * i + 2],
+                               sp->rot_wxyz[4 * i + 3]);
+            std::memcpy(&a[3], sp->sh + 48 * i, 48 * 4);
+            a[15] = make_float4(sp->t[i], kbits, 0.0f, 0.0f);
+        }
+        HS_TRY(copy_sync(ctx, f->splat_attr.p, rec.data(), n * 256, cudaMemcpyHostToDevice));
+    }
+    *f->h_n = n;
+    DevStats* ds = f->stats.as<DevStats>();
+    HS_CUDA(ctx, cudaMemcpyAsync(&ds->n_splats, f->h_n, 8, cudaMemcpyHostToDevice, ctx->stream));
+    f->cam = cp;
+    f->from_cut = false;
+    f->attr = f->splat_attr.as<float4>();
+    f->cut_node = nullptr;
+    f->cut_t = nullptr;
+    f->n_ptr = &ds->n_splats;
+    f->n_max = std::max<uint64_t>(n, 1);
+    f->times = times;
+    f->timed = times != nullptr;
+    f->cut_timed = false;
+    s = enqueue_raster(ctx, f);
+    if (s != HS_OK) return s;
+    if (!ctx->async) return finish_frame(ctx, f, true);
+    return HS_OK;
+}
+
+hs_status hs_frame_wait(hs_context* ctx, hs_frame* f) {
+    if (!ctx || !f) return HS_INVALID_ARGUMENT;
+    return finish_frame(ctx, f, false);
+}
+
+hs_status hs_frame_get_info(hs_context* ctx, hs_frame* f, hs_frame_info* info) {
+    hs_status s = finish_frame(ctx, f, false);
+    if (s != HS_OK) return s;
+    if (!f->have_result) return set_err(ctx, HS_MISSING_FORWARD_STATE, "frame has not been rendered");
+    const DevStats st = *f->h_stats;
+    info->width = f->W;
+    info->height = f->H;
+    info->tiles_x = f->tiles_x;
+    info->tiles_y = f->tiles_y;
+    info->n_splats = st.n_splats;
+    info->n_visible = st.n_visible;
+    info->n_duplicates = st.n_dup;
+    info->rendered_count = (int32_t)st.rendered;
+    info->sort_passes = f->passes;
+    return HS_OK;
+}
+
+hs_status hs_frame_download(hs_context* ctx, hs_frame* f, float* color, float* depth, float* trans, int32_t* rc) {
+    hs_status s = finish_frame(ctx, f, false);
+    if (s != HS_OK) return s;
+    if (!f->have_result) return set_err(ctx, HS_MISSING_FORWARD_STATE, "frame has not been rendered");
+    const size_t plane = (size_t)f->W * f->H;
+    if (color) HS_CUDA(ctx, cudaMemcpyAsync(color, f->color.p, plane * 12, cudaMemcpyDeviceToHost, ctx->stream));
+    if (depth) HS_CUDA(ctx, cudaMemcpyAsync(depth, f->depth.p, plane * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (trans) HS_CUDA(ctx, cudaMemcpyAsync(trans, f->trans.p, plane * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (rc) *rc = (int32_t)f->h_stats->rendered;
+    return HS_OK;
+}
+
+hs_status hs_frame_debug(hs_context* ctx, hs_frame* f, uint64_t* tile_start, uint64_t* sorted_keys,
+                         uint32_t* sorted_vals, uint64_t* dup_keys, uint32_t* dup_vals, float* proj16) {
+    hs_status s = finish_frame(ctx, f, false);
+    if (s != HS_OK) return s;
+    if (!f->have_result) return set_err(ctx, HS_MISSING_FORWARD_STATE, "frame has not been rendered");
+    const DevStats st = *f->h_stats;
+    const uint64_t D = st.sort_n;
+    const int fin = f->passes & 1;
+    if (tile_start) {
+        const int tiles = f->tiles_x * f->tiles_y;
+        std::vector<uint2> r(tiles);
+        HS_TRY(copy_sync(ctx, r.data(), f->ranges.p, (size_t)tiles * 8, cudaMemcpyDeviceToHost));
+        tile_start[0] = 0;
+        for (int t = 0; t < tiles; ++t) tile_start[t + 1] = tile_start[t] + (r[t].y - r[t].x);
+    }
+    if (D && sorted_keys) HS_TRY(copy_sync(ctx, sorted_keys, f->keys[fin].p, D * 8, cudaMemcpyDeviceToHost));
+    if (D && sorted_vals) HS_TRY(copy_sync(ctx, sorted_vals, f->vals[fin].p, D * 4, cudaMemcpyDeviceToHost));
+    if (dup_keys || dup_vals || proj16) {
+        if (!ctx->debug) return set_err(ctx, HS_INVALID_ARGUMENT, "pre-sort keys and projections need HS_OPT_DEBUG");
+        if (D && dup_keys) HS_TRY(copy_sync(ctx, dup_keys, f->dupk.p, D * 8, cudaMemcpyDeviceToHost));
+        if (D && dup_vals) HS_TRY(copy_sync(ctx, dup_vals, f->dupv.p, D * 4, cudaMemcpyDeviceToHost));
+        if (proj16 && st.n_splats) HS_TRY(copy_sync(ctx, proj16, f->dbg16.p, st.n_splats * 64, cudaMemcpyDeviceToHost));
+    }
+    return HS_OK;
+}
+
+}  // extern "C"
+
+extern "C" hs_status hs_hierarchy_load_h3dg(hs_context* ctx, const char* path, hs_hierarchy** out) {
+    if (!ctx || !path || !out) return HS_INVALID_ARGUMENT;
+    uint64_t n = 0;
+    uint32_t degree = 0;
+    hs_status s = hs_h3dg_read_header(path, &n, &degree);
+    if (s != HS_OK)
+        return set_err(ctx, s, s == HS_IO_FAILURE ? std::string("cannot open ") + path : "not a valid hierarchy file");
+    std::vector<uint32_t> parent(n), fc(n), cc(n);
+    std::vector<float> bmin(3 * n), bmax(3 * n), mean(3 * n), scale(3 * n), rot(4 * n), fall(n), sh(48 * n);
+    hs_node_soa_out o{parent.data(), fc.data(), cc.data(), bmin.data(), bmax.data(),
+                      mean.data(),   scale.data(), rot.data(), fall.data(), sh.data()};
+    s = hs_h3dg_read(path, &o, n);
+    if (s != HS_OK) return set_err(ctx, s, std::string("cannot read ") + path);
+    hs_node_soa in{parent.data(), fc.data(), cc.data(), bmin.data(), bmax.data(),
+                   mean.data(),   scale.data(), rot.data(), fall.data(), sh.data()};
+    return hs_hierarchy_upload(ctx, &in, n, degree, 1, out);
+}
+
+extern "C" hs_status hs_cut_render_splats(hs_context* ctx, const hs_hierarchy* h, const hs_cut* cut,
+                                          hs_splat_soa_out* out) {
+    if (!ctx || !h || !cut || !out) return HS_INVALID_ARGUMENT;
+    uint64_t n = 0;
+    HS_TRY(hs_cut_size(ctx, cut, &n));
+    if (n == 0) return HS_OK;
+    DBuf buf;
+    const size_t per = (3 + 3 + 4 + 48 + 1 + 1 + 1 + 1) * 4;
+    HS_CUDA(ctx, buf.ensure(n * per));
+    float* base = buf.as<float>();
+    float *mean = base, *scale = mean + 3 * n, *rot = scale + 3 * n, *sh = rot + 4 * n, *fall = sh + 48 * n,
+          *pfall = fall + n, *t = pfall + n;
+    int* k = reinterpret_cast<int*>(t + n);
+    hs::launch_assemble(h->attr.as<float4>(), cut->node.as<uint32_t>(), cut->t.as<float>(), cut->count.as<uint64_t>(),
+                        n, mean, scale, rot, sh, fall, pfall, t, k, ctx->stream);
+    HS_CUDA(ctx, cudaGetLastError());
+    HS_TRY(copy_sync(ctx, out->mean, mean, n * 12, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->scale, scale, n * 12, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->rot_wxyz, rot, n * 16, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->sh, sh, n * 192, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->falloff, fall, n * 4, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->parent_falloff, pfall, n * 4, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->t, t, n * 4, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->siblings, k, n * 4, cudaMemcpyDeviceToHost));
+    return HS_OK;
+}

@@ -1,0 +1,137 @@
+// cut.cu — k_select_cut: per-view LOD cut selection (lod.hpp:52-92) as one
+// HBM-streaming pass with order-preserving compaction.
+//
+// Per node i (reference semantics, lod.hpp:55-90):
+//   eps_i = granularity(bounds_i)                       (lod.hpp:18-26)
+//   keep  = (eps_i <= tau || leaf_i) && (root_i || eps_parent > tau)
+//   t     = root ? 1 : interp_weight(eps_i, eps_parent, tau)   (lod.hpp:34-37)
+//   alpha'= transition_alpha(min(falloff_p, 0.99), K_p)        (lod.hpp:41-45)
+// The parent's granularity is recomputed from its own box (bit-identical to
+// the reference's eps[] lookup) instead of materialising eps[N].
+// Output is written in ascending node order via a single-pass decoupled
+// look-back scan over 2048-node tiles, so no second pass or sort is needed.
+//
+// Bytes per node: 32 (own cull record) + <= 32 (parent cull record, shared by
+// siblings) + 4 (parent falloff, selected nodes only); 12 per cut entry out.
+#include "hs_device.cuh"
+#include "hs_kernels.h"
+#include "hs_scan.cuh"
+
+namespace hs {
+
+constexpr int kCutThreads = 256;
+constexpr int kCutItems = 8;
+constexpr int kCutTile = kCutThreads * kCutItems;
+
+__global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __restrict__ cull_a,
+                                                            const float4* __restrict__ cull_b,
+                                                            const float4* __restrict__ attr, uint64_t n, CamParams cam,
+                                                            float tau, uint32_t* __restrict__ out_node,
+                                                            float* __restrict__ out_t, float* __restrict__ out_alpha,
+                                                            uint64_t* status, uint32_t* tile_counter,
+                                                            uint64_t* count_out) {
+    __shared__ uint64_t s_exp_tab[32];
+    __shared__ uint64_t s_log_tab[32];
+    __shared__ uint32_t s_cnt[kCutItems * 8];
+    __shared__ uint64_t s_base;
+    __shared__ uint32_t s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < 32) {
+        s_exp_tab[tid] = c_exp2f_tab[tid];
+        s_log_tab[tid] = c_powf_log2_tab[tid];
+    }
+    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t base = (uint64_t)tile * kCutTile;
+    const uint64_t num_tiles = (n + kCutTile - 1) / kCutTile;
+
+    uint32_t ballots[kCutItems];
+    uint32_t sel_mask = 0;
+    float tv[kCutItems], av[kCutItems];
+#pragma unroll
+    for (int k = 0; k < kCutItems; ++k) {
+        const uint64_t i = base + (uint64_t)k * kCutThreads + tid;
+        bool sel = false;
+        tv[k] = 1.0f;
+        av[k] = 0.0f;
+        if (i < n) {
+            const float4 a = cull_a[i];
+            const float4 b = cull_b[i];
+            const uint32_t parent = __float_as_uint(b.z);
+            const uint32_t cc = __float_as_uint(b.w);
+            const float e = granularity(a.x, a.y, a.z, a.w, b.x, b.y, cam);
+            if (e <= tau || cc == 0) {
+                if (parent == kNoNode) {
+                    sel = true;
+                } else {
+                    const float4 pa = cull_a[parent];
+                    const float4 pb = cull_b[parent];
+                    const float ep = granularity(pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, cam);
+                    if (ep > tau) {
+                        sel = true;
+                        tv[k] = interp_weight(e, ep, tau);
+                        const uint32_t K = __float_as_uint(pb.w);
+                        const float pf = attr[(uint64_t)parent * kAttrVec4].w;
+                        const float aa = smin(smax(smin(pf, kAlphaMax), 0.0f), kAlphaMax);
+                        av[k] = 1.0f - hs_libm::powf_glibc(1.0f - aa, 1.0f / (float)(int)K, s_log_tab, s_exp_tab);
+                    }
+                }
+            }
+        }
+        ballots[k] = __ballot_sync(0xffffffffu, sel);
+        if (sel) sel_mask |= 1u << k;
+        if (lane == 0) s_cnt[k * 8 + warp] = __popc(ballots[k]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // exclusive scan over 64 (item, warp) counts in node order: entries 2*lane, 2*lane+1
+        const uint32_t c0 = s_cnt[2 * lane], c1 = s_cnt[2 * lane + 1];
+        uint32_t incl = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - (c0 + c1);
+        s_cnt[2 * lane] = excl;
+        s_cnt[2 * lane + 1] = excl + c0;
+        uint64_t prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) st_volatile_u64(status, kFlagInc64 | total);
+        } else {
+            if (lane == 0) st_volatile_u64(status + tile, kFlagAgg64 | total);
+            prefix = lookback_u64(status, tile);
+            if (lane == 0) st_volatile_u64(status + tile, kFlagInc64 | (prefix + total));
+        }
+        if (lane == 0) {
+            s_base = prefix;
+            if (tile == num_tiles - 1) *count_out = prefix + total;
+        }
+    }
+    __syncthreads();
+    const uint64_t blk = s_base;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < kCutItems; ++k) {
+        if (sel_mask & (1u << k)) {
+            const uint64_t pos = blk + s_cnt[k * 8 + warp] + __popc(ballots[k] & lt_mask);
+            out_node[pos] = (uint32_t)(base + (uint64_t)k * kCutThreads + tid);
+            out_t[pos] = tv[k];
+            out_alpha[pos] = av[k];
+        }
+    }
+}
+
+void launch_select_cut(const float4* cull_a, const float4* cull_b, const float4* attr, uint64_t n,
+                       const CamParams& cam, float tau, uint32_t* out_node, float* out_t, float* out_alpha,
+                       uint64_t* status, uint32_t* tile_counter, uint64_t* count_out, cudaStream_t stream) {
+    const uint64_t tiles = (n + kCutTile - 1) / kCutTile;
+    k_select_cut<<<(unsigned)tiles, kCutThreads, 0, stream>>>(cull_a, cull_b, attr, n, cam, tau, out_node, out_t,
+                                                              out_alpha, status, tile_counter, count_out);
+}
+
+uint64_t select_cut_status_words(uint64_t n) { return (n + kCutTile - 1) / kCutTile; }
+
+}  // namespace hs

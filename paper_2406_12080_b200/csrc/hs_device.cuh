@@ -1,0 +1,96 @@
+// hs_device.cuh — device-side data layout and the float contract of the
+// reference hot path.
+//
+// All units including this header are compiled with -fmad=false, IEEE div and
+// sqrt (nvcc defaults without --use_fast_math) and no FTZ, so every float
+// expression below rounds exactly like the reference's SSE2 scalar code
+// (GCC -O3, no -march: no FMA contraction).  Eigen 3.4 small fixed-size
+// expression order is spelled out explicitly: 3-term sums are x0 + (x1 + x2),
+// Vec4f reductions are (x0 + x2) + (x1 + x3).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "hs_libm.cuh"
+
+namespace hs {
+
+constexpr int kTile = 16;                       // math.hpp:27 kTileSize
+constexpr float kAlphaMin = 1.0f / 255.0f;      // math.hpp:28
+constexpr float kAlphaMax = 0.99f;              // math.hpp:29
+constexpr float kTransmittanceEps = 1e-4f;      // math.hpp:30
+constexpr float kDilation2d = 0.3f;             // math.hpp:31
+constexpr float kNearPlane = 0.01f;             // math.hpp:32
+constexpr uint32_t kNoNode = 0xFFFFFFFFu;       // model.hpp:15
+
+// ------------------------------------------------------------------ layout
+// Hierarchy in HBM (reference node order, structure of arrays):
+//   cull_a[i] = {min.x, min.y, min.z, max.x}            16 B
+//   cull_b[i] = {max.y, max.z, bits(parent), bits(child_count)}   16 B
+//   attr[16*i + 0] = {mean.xyz, falloff}
+//   attr[16*i + 1] = {scale.xyz, bits(parent)}
+//   attr[16*i + 2] = rotation (w, x, y, z)
+//   attr[16*i + 3..14] = sh[48]
+//   attr[16*i + 15] = {bits(child_count), bits(first_child), 0, 0}
+// Caller splats (render_forward input) use the same 256-byte record with
+//   [0].w = falloff, [1].w = parent_falloff, [15] = {t, bits(K), 0, 0}.
+constexpr int kAttrVec4 = 16;
+
+// Projected splat record consumed by the blend (64 B):
+//   p0 = {mean2d.x, mean2d.y, conic0, conic1}
+//   p1 = {conic2, falloff_eff*alpha_scale, parent_falloff_eff*alpha_scale, t}
+//   p2 = {color.r, color.g, color.b, inv_depth}
+//   p3 = {inv_k, bits(tx0 | tx1 << 16), bits(ty0 | ty1 << 16), bits(cam z)}
+struct __align__(16) ProjRec {
+    float4 p0, p1, p2, p3;
+};
+
+struct CamParams {
+    float w2c[12];  // row-major
+    float fx, fy, cx, cy;
+    float pos[3];   // camera position -R^T t (model.hpp:79)
+    float maxf;     // max_focal (model.hpp:81)
+    int width, height, tiles_x, tiles_y;
+};
+
+// glibc tables for the expf/powf replicas (copied to shared memory per block).
+static __constant__ uint64_t c_exp2f_tab[32] = HS_EXP2F_TAB_INIT;
+static __constant__ uint64_t c_powf_log2_tab[32] = HS_POWF_LOG2_TAB_INIT;
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ float smin(float a, float b) { return (b < a) ? b : a; }  // std::min
+__device__ __forceinline__ float smax(float a, float b) { return (a < b) ? b : a; }  // std::max
+__device__ __forceinline__ float sum3(float a, float b, float c) { return a + (b + c); }
+__device__ __forceinline__ float sum4(float a, float b, float c, float d) { return (a + c) + (b + d); }
+
+// x86-64 cvttss2si: NaN / inf / out of range -> INT_MIN (the reference's
+// static_cast<int> of a float; CUDA's conversion would saturate instead).
+__device__ __forceinline__ int f2i_x86(float v) {
+    if (!(v >= -2147483648.0f && v < 2147483648.0f)) return (int)0x80000000;
+    return __float2int_rz(v);
+}
+__device__ __forceinline__ int iclamp(int v, int lo, int hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+// granularity (lod.hpp:18-26) of a node box.
+__device__ __forceinline__ float granularity(float mnx, float mny, float mnz, float mxx, float mxy, float mxz,
+                                             const CamParams& c) {
+    if ((c.pos[0] >= mnx && c.pos[1] >= mny && c.pos[2] >= mnz) &&
+        (c.pos[0] <= mxx && c.pos[1] <= mxy && c.pos[2] <= mxz))
+        return __int_as_float(0x7f800000);
+    float z = c.w2c[11];
+    z = z + smin(c.w2c[8] * mnx, c.w2c[8] * mxx);
+    z = z + smin(c.w2c[9] * mny, c.w2c[9] * mxy);
+    z = z + smin(c.w2c[10] * mnz, c.w2c[10] * mxz);
+    if (z <= kNearPlane) return __int_as_float(0x7f800000);
+    const float L = smax(mxx - mnx, smax(mxy - mny, mxz - mnz));
+    return c.maxf * L / z;
+}
+
+// interp_weight (lod.hpp:34-37)
+__device__ __forceinline__ float interp_weight(float en, float ep, float tau) {
+    if (ep == en || ep == __int_as_float(0x7f800000)) return 1.0f;
+    const float v = (ep - tau) / (ep - en);
+    return smin(1.0f, smax(0.0f, v));
+}
+
+}  // namespace hs

@@ -1,0 +1,43 @@
+// hs_kernels.h — host-side launchers of the hot-path kernels (stream-ordered).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace hs {
+
+struct CamParams;
+struct ProjRec;
+
+// cut.cu
+void launch_select_cut(const float4* cull_a, const float4* cull_b, const float4* attr, uint64_t n,
+                       const CamParams& cam, float tau, uint32_t* out_node, float* out_t, float* out_alpha,
+                       uint64_t* status, uint32_t* tile_counter, uint64_t* count_out, cudaStream_t stream);
+uint64_t select_cut_status_words(uint64_t n);
+
+// raster.cu
+void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,
+                       const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint32_t* dupcount,
+                       float* dbg16, unsigned long long* n_visible, cudaStream_t s);
+uint64_t scan_status_words(uint64_t n_max);
+void launch_scan(const uint32_t* counts, const uint64_t* n_ptr, uint64_t n_max, uint32_t* offsets, uint64_t* status,
+                 uint32_t* tile_counter, uint64_t* total_out, uint64_t* sort_n_out, uint64_t capacity,
+                 unsigned long long* overflows, cudaStream_t s);
+void launch_duplicate(const ProjRec* proj, const uint32_t* dupcount, const uint32_t* offsets, const uint64_t* n_ptr,
+                      uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint64_t* keys, uint32_t* vals,
+                      cudaStream_t s);
+void launch_ranges(const uint64_t* keys, const uint64_t* sort_n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s);
+void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
+                  const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched, cudaStream_t s);
+void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr,
+                     uint64_t n_max, float* mean, float* scale, float* rot, float* sh, float* fall, float* pfall,
+                     float* t, int* k, cudaStream_t s);
+void launch_count_touched(const uint8_t* touched, const uint64_t* n_ptr, uint64_t n_max, unsigned long long* out,
+                          cudaStream_t s);
+
+// sort.cu
+uint64_t sort_status_words(uint64_t n_max);
+void launch_radix_sort(uint64_t* keys[2], uint32_t* vals[2], const uint64_t* n_ptr, uint64_t n_max, int passes,
+                       uint32_t* scratch_hist, uint32_t* status, uint32_t* counters, cudaStream_t s);
+
+}  // namespace hs

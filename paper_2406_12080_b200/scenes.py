@@ -1,0 +1,87 @@
+"""Synthetic benchmark inputs: the BASELINE.json configurations.
+
+Hierarchies come from csrc/synth.cpp (build_bvh layout).  Cameras fly a
+closed loop around the outside of the city at a fixed altitude and stand-off
+from its edge, always looking inward and down.  Keeping every camera outside
+the scene with its view direction inside the inward cone guarantees that no
+geometry lies near the camera's image plane: the reference renderer only culls
+at z <= 0.01 (render.hpp:110) and has no frustum guard band, so a splat just in
+front of the image plane projects to a screen-covering ellipse; a camera
+inside the point cloud would render mostly those.  The near half of the city
+is within the leaf-level LOD range, the far half is coarse, so the cut mixes
+leaves, interior nodes and transitions as the paper's Table 5 paths do.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import CameraModel, look_at_camera, scene_side, synth_city
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    leaves: int
+    width: int
+    height: int
+    focal: float
+    tau: float
+    altitude: float = 40.0
+    standoff: float = 30.0
+    lookahead: float = 150.0
+
+
+CONFIGS = {
+    # BASELINE.json configs[0]: 100K leaves, single 640x480 view, tau = 3 px (CPU reference runs it)
+    "c1": Config("c1_100k_640x480_tau3", 100_000, 640, 480, 300.0, 3.0, altitude=15.0, standoff=10.0,
+                 lookahead=50.0),
+    # configs[1]: 10M leaves, 1920x1080, tau = 3 px, 1 B200 (the headline metric)
+    "c2": Config("c2_10m_1080p_tau3", 10_000_000, 1920, 1080, 1100.0, 3.0),
+    # configs[4]: 100M leaves multi-chunk, 3840x2160 (generated on demand; ~54 GB of SoA)
+    "c5": Config("c5_100m_2160p_tau3", 100_000_000, 3840, 2160, 2200.0, 3.0, altitude=60.0, standoff=40.0,
+                 lookahead=250.0),
+}
+
+
+def trajectory(cfg: Config, n_frames: int, first: int = 0) -> list[CameraModel]:
+    """Frames [first, first + n_frames) of a closed loop of `1000` frames by default period."""
+    side = scene_side(cfg.leaves)
+    half = 0.5 * side + cfg.standoff
+    period = 1000
+    cams = []
+    for i in range(first, first + n_frames):
+        u = (i % period) / period * 4.0  # 4 edges, parameter along the square loop
+        edge = int(u) % 4
+        s = u - int(u)
+        # square corners counter-clockwise starting at the south-west corner
+        corners = [(-half, -half), (half, -half), (half, half), (-half, half)]
+        x0, z0 = corners[edge]
+        x1, z1 = corners[(edge + 1) % 4]
+        px, pz = x0 + (x1 - x0) * s, z0 + (z1 - z0) * s
+        # inward normals of the south, east, north, west edges; blend near corners
+        normals = [(0.0, 1.0), (-1.0, 0.0), (0.0, -1.0), (1.0, 0.0)]
+        n0 = np.array(normals[edge])
+        w = 0.0
+        if s > 0.9:
+            w = (s - 0.9) / 0.2
+            n1 = np.array(normals[(edge + 1) % 4])
+        elif s < 0.1:
+            w = (0.1 - s) / 0.2
+            n1 = np.array(normals[(edge - 1) % 4])
+        d = n0 if w == 0.0 else (1 - w) * n0 + w * n1
+        d = d / np.linalg.norm(d)
+        pos = np.array([px, cfg.altitude, pz], np.float32)
+        target = np.array([px + d[0] * cfg.lookahead, 0.0, pz + d[1] * cfg.lookahead], np.float32)
+        cams.append(look_at_camera(pos, target, cfg.width, cfg.height, cfg.focal))
+    return cams
+
+
+def camera(cfg: Config, frame: int = 0) -> CameraModel:
+    return trajectory(cfg, 1, frame)[0]
+
+
+def hierarchy(cfg: Config, seed: int = 1, threads: int = 0):
+    return synth_city(cfg.leaves, seed=seed, threads=threads)
