@@ -1,0 +1,336 @@
+"""Benchmark: frames/sec of per-view LOD cut + 3DGS forward render.
+
+Metric (BASELINE.json): frames/sec at 1080p, tau = 3 px, 10M-leaf hierarchy;
+cut+render ms/frame.  One step = one frame of the camera trajectory: k_select_cut
+over all 20M nodes, fused interpolation/preprocess, duplication, radix sort,
+tile ranges and alpha blend (BASELINE.json configs[1] = SURVEY.md config C2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun (one rank per GPU): the 1000-frame trajectory is
+partitioned into contiguous per-rank blocks with the hierarchy replicated on
+every GPU (weak scaling: K frames per rank); there is no data-path collective.
+Timing: CUDA events on the renderer's stream, barrier + synchronize on both
+sides, max over ranks.  --impl reference times the reference's CPU path (the
+oracle restatement, oracle/hsplat_oracle.cpp) on this box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec at 1080p, tau=3px, 10M-leaf hierarchy; cut+render ms/frame"
+UNIT = "frames/s"
+KERNELS_PER_FRAME = 15  # cut, preprocess, scan, duplicate, sort hist+offs+6 passes, ranges, blend, count
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def reader():
+            for line in self.proc.stdout:
+                self.rows.append([x.strip() for x in line.split(",")])
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 7 for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def frames_for_rank(rank: int, world: int, steps: int, warmup: int):
+    """Contiguous, even-length per-rank blocks of the trajectory."""
+    per = steps + warmup
+    per += per % 2
+    return rank * per, per
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference's CPU path (oracle port) on this box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    from oracle import oracle as orc
+    from paper_2406_12080_b200 import scenes
+
+    h = scenes.hierarchy(cfg)
+    oh = orc.OracleHierarchy(h)
+    del h
+    cores = orc.thread_count()
+    cams = scenes.trajectory(cfg, args.warmup + args.steps, first=0)
+    for cam in cams[: min(args.warmup, 1)]:
+        orc.render_hierarchy(oh, cam, cfg.tau, keep_ctx=False)
+    budget = args.reference_budget_s
+    done, t0 = 0, time.perf_counter()
+    for cam in cams[args.warmup:]:
+        orc.render_hierarchy(oh, cam, cfg.tau, keep_ctx=False)
+        done += 1
+        if time.perf_counter() - t0 > budget:
+            break
+    el = time.perf_counter() - t0
+    v = done / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": done,
+        "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * el / done, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "leaves": cfg.leaves, "width": cfg.width, "height": cfg.height,
+                   "tau": cfg.tau, "l2": "inputs larger than L2 (host run)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{done} frame(s) of the {cfg.name} trajectory (steps capped at "
+                                   f"{budget:.0f} s of CPU time)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, h, frames: int = 2):
+    from oracle import oracle as orc
+    from paper_2406_12080_b200 import scenes
+
+    oh = orc.OracleHierarchy(h)
+    cams = scenes.trajectory(cfg, frames, first=100)
+    t0 = time.perf_counter()
+    for cam in cams:
+        orc.render_hierarchy(oh, cam, cfg.tau, keep_ctx=False)
+    el = time.perf_counter() - t0
+    return {"value": frames / el, "unit": UNIT, "cores": orc.thread_count(), "kind": "port",
+            "sample": f"{frames} frames (100..{99 + frames}) of the {cfg.name} trajectory, oracle "
+                      f"render_hierarchy incl. select_cut + cut_render_splats + render_forward"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reference-budget-s", type=float, default=120.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    from paper_2406_12080_b200 import scenes
+    cfg = scenes.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2406_12080_b200 as hs
+    from paper_2406_12080_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    t0 = time.perf_counter()
+    h = scenes.hierarchy(cfg)
+    gen_s = time.perf_counter() - t0
+    r = hs.Renderer(local, exact=(args.mode == "exact"))
+    t0 = time.perf_counter()
+    dh = r.upload(h, validate=False)
+    upload_s = time.perf_counter() - t0
+    L = N.lib()
+    first, count = frames_for_rank(rank, world, args.steps, args.warmup)
+    cams = scenes.trajectory(cfg, count, first=first)
+    ccams = [c.to_c() for c in cams]
+    warm, timed = ccams[: args.warmup], ccams[args.warmup: args.warmup + args.steps]
+
+    # warm-up (synchronous: grows the duplicate buffers to this trajectory's needs)
+    for c in warm:
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, None), r.ctx)
+    stream = torch.cuda.ExternalStream(r.stream_handle())
+
+    # ---- timed region: K frames, async enqueue, CUDA events on the renderer stream
+    r.set_async(True)
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    r.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for c in timed:
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, None), r.ctx)
+    e1.record(stream)
+    e1.synchronize()
+    r.synchronize()
+    clocks = sampler.stop()
+    barrier()
+    hs._check(L.hs_frame_wait(r.ctx, r._frame), r.ctx)  # fails if any timed frame overflowed
+    r.set_async(False)
+    ms_local = e0.elapsed_time(e1)
+    ms_total = max_over_ranks(ms_local)
+    value = world * len(timed) / (ms_total / 1e3)
+
+    # ---- stage breakdown + roofline inputs: the same frames, per-stage CUDA events
+    st = hs.StageTimes()
+    infos = []
+    for c in timed[: min(len(timed), 16)]:
+        s = N.hs_stage_times()
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, s), r.ctx)
+        st.add(s)
+        fi = N.hs_frame_info()
+        hs._check(L.hs_frame_get_info(r.ctx, r._frame, fi), r.ctx)
+        infos.append(fi)
+    nf = len(infos)
+    stage_ms = {k: 1e3 * getattr(st, k) / nf for k in ("cut_expand", "weights", "preprocess", "duplicate",
+                                                      "tile_ranges", "alpha_blend")}
+    mean = lambda k: sum(getattr(fi, k) for fi in infos) / nf  # noqa: E731
+    C_, V_, D_ = mean("n_splats"), mean("n_visible"), mean("n_duplicates")
+    NE, NC = mean("n_eval"), mean("n_contrib")
+    nodes = dh.n
+    pk, pk_kind = peaks()
+    hbm = pk.get("hbm_gbs", 6450.9)
+    # algorithmic bytes per frame
+    passes = infos[0].sort_passes
+    bytes_cut = 32 * nodes + 12 * C_
+    bytes_pre = C_ * (256 + 8) + V_ * (64 + 4)
+    bytes_sort = 8 * D_ + passes * 24 * D_ + 12 * D_ + 8 * V_  # histogram read + passes + dup write + dup reads
+    stages = {
+        "cut": {"ms": stage_ms["cut_expand"], "bound": "hbm", "bytes": bytes_cut,
+                "gbs": bytes_cut / (stage_ms["cut_expand"] * 1e6) if stage_ms["cut_expand"] else None},
+        "preprocess": {"ms": stage_ms["preprocess"], "bound": "hbm", "bytes": bytes_pre,
+                       "gbs": bytes_pre / (stage_ms["preprocess"] * 1e6) if stage_ms["preprocess"] else None},
+        "duplicate+sort": {"ms": stage_ms["duplicate"], "bound": "hbm", "bytes": bytes_sort,
+                           "gbs": bytes_sort / (stage_ms["duplicate"] * 1e6) if stage_ms["duplicate"] else None},
+        "tile_ranges": {"ms": stage_ms["tile_ranges"]},
+        "alpha_blend": {"ms": stage_ms["alpha_blend"], "bound": "fp32", "n_eval": NE, "n_contrib": NC},
+    }
+    # blend roofline: FP32 ops per (pixel, entry) evaluation (power + gate: 12) and per
+    # contribution (exp/alpha/accumulate: 24), against the FP32 peak at the sampled clock
+    sm_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+    props = torch.cuda.get_device_properties(local)
+    fp32_peak = props.multi_processor_count * 128 * 2 * sm_mhz * 1e6 / 1e12
+    blend_flops = 12 * NE + 24 * NC
+    blend_tf = blend_flops / (stage_ms["alpha_blend"] * 1e-3) / 1e12
+    roofline = {"bound": "fp32", "kernel": "k_blend", "achieved": blend_tf, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": blend_tf / fp32_peak, "traffic": None,
+                "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz "
+                               f"(no measured FP32 peak in MEASURED_PEAKS.json)",
+                "hbm_stages": {k: {"gbs": v.get("gbs"), "frac": (v["gbs"] / hbm) if v.get("gbs") else None}
+                               for k, v in stages.items() if v.get("bound") == "hbm"},
+                "hbm_peak_gbs": hbm, "hbm_peak_source": pk_kind}
+
+    # ---- end to end through the public API: camera in, image out to pinned host memory
+    import numpy as np
+    W, H = cfg.width, cfg.height
+    pinned = torch.empty(5 * W * H, dtype=torch.float32, pin_memory=True)
+    base = pinned.data_ptr()
+    f32 = N.C.POINTER(N.C.c_float)
+    col = N.C.cast(base, f32)
+    dep = N.C.cast(base + 12 * W * H, f32)
+    trn = N.C.cast(base + 16 * W * H, f32)
+    rc = N.C.c_int32()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for cam in cams[args.warmup: args.warmup + args.steps]:
+        c = cam.to_c()  # host camera -> kernel parameters (H2D)
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, None), r.ctx)
+        hs._check(L.hs_frame_download(r.ctx, r._frame, col, dep, trn, N.C.byref(rc)), r.ctx)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": world * len(timed) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": N.C.sizeof(N.hs_camera),
+           "d2h_bytes_per_step": 20 * W * H + 4}
+    _ = np
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, h)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(timed),
+            "warmup": args.warmup, "ms_per_step": ms_total / len(timed), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "leaves": cfg.leaves, "nodes": nodes, "width": W, "height": H,
+                       "tau": cfg.tau, "blend_mode": args.mode, "frames": f"trajectory frames {first}.. per rank",
+                       "parallelism": f"view-parallel x{world} (hierarchy replicated)",
+                       "l2": "inputs larger than L2 (hierarchy 5.8 GB resident; no flush needed)"},
+            "roofline": roofline,
+            "stages_ms": stage_ms,
+            "stages": stages,
+            "per_frame": {"cut_entries": C_, "visible": V_, "duplicates": D_, "n_eval": NE, "n_contrib": NC},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": KERNELS_PER_FRAME * len(timed),
+            "clocks": clocks,
+            "setup_s": {"generate": gen_s, "upload": upload_s},
+        }
+        print(json.dumps(line), flush=True)
+    r.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

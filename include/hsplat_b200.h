@@ -132,6 +132,8 @@ typedef struct hs_frame_info {
     uint64_t n_duplicates;   /* D: (tile, splat) pairs = sorted key count */
     int32_t rendered_count;  /* RenderOutput::rendered_count (render.hpp:82) */
     int32_t sort_passes;     /* radix passes run for this frame */
+    uint64_t n_eval;         /* N_eval: (pixel, entry) pairs visited by the blend */
+    uint64_t n_contrib;      /* (pixel, entry) pairs that contributed */
 } hs_frame_info;
 
 typedef struct hs_context hs_context;

@@ -423,9 +423,12 @@ class DeviceHierarchy:
         return self.leaves
 
     def __del__(self):
-        if getattr(self, "handle", None) and N._lib is not None:
-            N.lib().hs_hierarchy_destroy(self.handle)
-            self.handle = None
+        try:
+            if getattr(self, "handle", None) and N._lib is not None and self._r.ctx is not None:
+                N.lib().hs_hierarchy_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
 
 
 class Renderer:
@@ -547,7 +550,8 @@ class Renderer:
         _check(L.hs_frame_download(self.ctx, self._frame, N.ptr(color, C.c_float), N.ptr(depth, C.c_float),
                                    N.ptr(trans, C.c_float), C.byref(rc)), self.ctx)
         d = dict(width=W, height=H, tiles_x=info.tiles_x, tiles_y=info.tiles_y, n_splats=int(info.n_splats),
-                 n_visible=int(info.n_visible), n_duplicates=int(info.n_duplicates), sort_passes=info.sort_passes)
+                 n_visible=int(info.n_visible), n_duplicates=int(info.n_duplicates), sort_passes=info.sort_passes,
+                 n_eval=int(info.n_eval), n_contrib=int(info.n_contrib))
         out = RenderOutput(color, depth, trans, int(rc.value), d)
         if want_context:
             out.context = self.frame_debug(d)

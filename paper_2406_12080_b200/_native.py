@@ -49,7 +49,8 @@ class hs_stage_times(C.Structure):
 class hs_frame_info(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
                 ("n_splats", C.c_uint64), ("n_visible", C.c_uint64), ("n_duplicates", C.c_uint64),
-                ("rendered_count", C.c_int32), ("sort_passes", C.c_int32)]
+                ("rendered_count", C.c_int32), ("sort_passes", C.c_int32), ("n_eval", C.c_uint64),
+                ("n_contrib", C.c_uint64)]
 
 
 HS_OPT_ASYNC = 1

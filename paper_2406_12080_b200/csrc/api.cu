@@ -48,7 +48,8 @@ struct DevStats {
     uint64_t n_dup;                // D
     uint64_t sort_n;               // D if it fits the duplicate buffers, else 0
     unsigned long long rendered;   // rendered_count
-    unsigned long long pad[2];
+    unsigned long long n_eval;     // (pixel, entry) pairs evaluated by the blend
+    unsigned long long n_contrib;  // pairs that contributed
     unsigned long long overflows;  // sticky: frames whose D exceeded capacity since the last wait
 };
 
@@ -315,7 +316,8 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     hs::launch_ranges(kb[fin], &ds->sort_n, f->cap_dup, f->ranges.as<uint2>(), s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[4], s));
     hs::launch_blend(ctx->blend_mode, f->ranges.as<uint2>(), vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
-                     f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(), s);
+                     f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(),
+                     &ds->n_eval, s);
     hs::launch_count_touched(f->touched.as<uint8_t>(), f->n_ptr, f->n_max, &ds->rendered, s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[5], s));
     HS_CUDA(ctx, cudaGetLastError());
@@ -768,6 +770,8 @@ hs_status hs_frame_get_info(hs_context* ctx, hs_frame* f, hs_frame_info* info) {
     info->n_duplicates = st.n_dup;
     info->rendered_count = (int32_t)st.rendered;
     info->sort_passes = f->passes;
+    info->n_eval = st.n_eval;
+    info->n_contrib = st.n_contrib;
     return HS_OK;
 }
 

@@ -464,7 +464,8 @@ template <int kMode>
 __global__ void __launch_bounds__(256) k_blend(const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                                                const ProjRec* __restrict__ proj, const uint64_t* __restrict__ sort_n_ptr,
                                                CamParams cam, float* __restrict__ color, float* __restrict__ depth,
-                                               float* __restrict__ trans, uint8_t* __restrict__ touched) {
+                                               float* __restrict__ trans, uint8_t* __restrict__ touched,
+                                               unsigned long long* __restrict__ eval_counts) {
     __shared__ float4 s_p0[256], s_p1[256], s_p2[256];
     __shared__ float s_ik[256];
     __shared__ uint32_t s_id[256];
@@ -484,6 +485,7 @@ __global__ void __launch_bounds__(256) k_blend(const uint2* __restrict__ ranges,
     if (*sort_n_ptr) range = ranges[tile];
     float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, d = 0.0f;
     bool done = !inside;
+    uint32_t n_eval = 0, n_contrib = 0;  // N_eval / contributions (roofline accounting)
     for (uint32_t start = range.x; start < range.y; start += 256) {
         if (__syncthreads_count(done) == 256) break;
         const uint32_t j = start + tid;
@@ -501,6 +503,7 @@ __global__ void __launch_bounds__(256) k_blend(const uint2* __restrict__ ranges,
         const int cnt = (int)min(256u, range.y - start);
         if (!done) {
             for (int k = 0; k < cnt; ++k) {
+                ++n_eval;
                 const float4 p0 = s_p0[k];
                 const float4 p1 = s_p1[k];
                 const float dx = px - p0.x, dy = py - p0.y;
@@ -548,6 +551,7 @@ __global__ void __launch_bounds__(256) k_blend(const uint2* __restrict__ ranges,
                 d = d + p2.w * alpha * T;
                 T = test;
                 s_hit[k] = 1;
+                ++n_contrib;
             }
         }
         __syncthreads();
@@ -561,6 +565,14 @@ __global__ void __launch_bounds__(256) k_blend(const uint2* __restrict__ ranges,
         color[2 * plane + i] = c2;
         depth[i] = d;
         trans[i] = T;
+    }
+    for (int o = 16; o; o >>= 1) {
+        n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
+        n_contrib += __shfl_xor_sync(0xffffffffu, n_contrib, o);
+    }
+    if ((tid & 31) == 0) {
+        atomicAdd(eval_counts, (unsigned long long)n_eval);
+        atomicAdd(eval_counts + 1, (unsigned long long)n_contrib);
     }
 }
 
@@ -625,12 +637,13 @@ void launch_ranges(const uint64_t* keys, const uint64_t* sort_n_ptr, uint64_t n_
 }
 
 void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
-                  const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched, cudaStream_t s) {
+                  const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
+                  unsigned long long* eval_counts, cudaStream_t s) {
     const unsigned tiles = (unsigned)(cam.tiles_x * cam.tiles_y);
     if (mode == 0)
-        k_blend<0><<<tiles, 256, 0, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched);
+        k_blend<0><<<tiles, 256, 0, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched, eval_counts);
     else
-        k_blend<1><<<tiles, 256, 0, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched);
+        k_blend<1><<<tiles, 256, 0, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched, eval_counts);
 }
 
 void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr,

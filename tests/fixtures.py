@@ -13,7 +13,8 @@ class Rng:
         self.g = np.random.default_rng(seed)
 
     def uniform(self, lo, hi, size=None):
-        return self.g.uniform(lo, hi, size).astype(np.float32)
+        v = self.g.uniform(lo, hi, size)
+        return np.float32(v) if size is None else v.astype(np.float32)
 
     def randint(self, n):
         return int(self.g.integers(0, n))
