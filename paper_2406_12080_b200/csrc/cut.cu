@@ -48,39 +48,56 @@ __global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __rest
 
     uint32_t ballots[kCutItems];
     uint32_t sel_mask = 0;
-    float tv[kCutItems], av[kCutItems];
+    float tv[kCutItems], av[kCutItems], eps[kCutItems];
+    uint32_t par[kCutItems];
+    // phase 1: own cull records (all items in flight), granularity, parent need
+    uint32_t need = 0;
 #pragma unroll
     for (int k = 0; k < kCutItems; ++k) {
         const uint64_t i = base + (uint64_t)k * kCutThreads + tid;
-        bool sel = false;
-        tv[k] = 1.0f;
-        av[k] = 0.0f;
+        par[k] = kNoNode;
+        eps[k] = 0.0f;
         if (i < n) {
             const float4 a = cull_a[i];
             const float4 b = cull_b[i];
             const uint32_t parent = __float_as_uint(b.z);
             const uint32_t cc = __float_as_uint(b.w);
-            const float e = granularity(a.x, a.y, a.z, a.w, b.x, b.y, cam);
-            if (e <= tau || cc == 0) {
-                if (parent == kNoNode) {
-                    sel = true;
-                } else {
-                    const float4 pa = cull_a[parent];
-                    const float4 pb = cull_b[parent];
-                    const float ep = granularity(pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, cam);
-                    if (ep > tau) {
-                        sel = true;
-                        tv[k] = interp_weight(e, ep, tau);
-                        const uint32_t K = __float_as_uint(pb.w);
-                        const float pf = attr[(uint64_t)parent * kAttrVec4].w;
-                        const float aa = smin(smax(smin(pf, kAlphaMax), 0.0f), kAlphaMax);
-                        av[k] = 1.0f - hs_libm::powf_glibc(1.0f - aa, 1.0f / (float)(int)K, s_log_tab, s_exp_tab);
-                    }
-                }
+            eps[k] = granularity(a.x, a.y, a.z, a.w, b.x, b.y, cam);
+            if (eps[k] <= tau || cc == 0) {  // fine enough, or a leaf (lod.hpp:64-65)
+                if (parent == kNoNode)
+                    sel_mask |= 1u << k;  // the root: t = 1, alpha' = 0
+                else
+                    need |= 1u << k, par[k] = parent;
             }
         }
-        ballots[k] = __ballot_sync(0xffffffffu, sel);
-        if (sel) sel_mask |= 1u << k;
+    }
+    // phase 2: parent cull records for the candidates, parent granularity, t
+    uint32_t kk[kCutItems];
+#pragma unroll
+    for (int k = 0; k < kCutItems; ++k) {
+        tv[k] = 1.0f;
+        av[k] = 0.0f;
+        kk[k] = 0;
+        if (need & (1u << k)) {
+            const float4 pa = cull_a[par[k]];
+            const float4 pb = cull_b[par[k]];
+            const float ep = granularity(pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, cam);
+            if (ep > tau) {  // parent not yet fine enough (lod.hpp:67-69)
+                sel_mask |= 1u << k;
+                tv[k] = interp_weight(eps[k], ep, tau);
+                kk[k] = __float_as_uint(pb.w);
+            }
+        }
+    }
+    // phase 3: transition_alpha from the parent's falloff (lod.hpp:84-88)
+#pragma unroll
+    for (int k = 0; k < kCutItems; ++k) {
+        if (kk[k]) {
+            const float pf = attr[(uint64_t)par[k] * kAttrVec4].w;
+            const float aa = smin(smax(smin(pf, kAlphaMax), 0.0f), kAlphaMax);
+            av[k] = 1.0f - hs_libm::powf_glibc(1.0f - aa, 1.0f / (float)(int)kk[k], s_log_tab, s_exp_tab);
+        }
+        ballots[k] = __ballot_sync(0xffffffffu, (sel_mask >> k) & 1u);
         if (lane == 0) s_cnt[k * 8 + warp] = __popc(ballots[k]);
     }
     __syncthreads();

@@ -33,7 +33,7 @@ void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const Pro
 void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr,
                      uint64_t n_max, float* mean, float* scale, float* rot, float* sh, float* fall, float* pfall,
                      float* t, int* k, cudaStream_t s);
-void launch_count_touched(const uint8_t* touched, const uint64_t* n_ptr, uint64_t n_max, unsigned long long* out,
+void launch_count_touched(uint8_t* touched, const uint64_t* n_ptr, uint64_t n_max, unsigned long long* out,
                           cudaStream_t s);
 
 // sort.cu

@@ -457,131 +457,15 @@ __global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ key
     }
 }
 
-// -------------------------------------------------------------------------
-// alpha blend
-// -------------------------------------------------------------------------
-template <int kMode>
-__global__ void __launch_bounds__(256) k_blend(const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
-                                               const ProjRec* __restrict__ proj, const uint64_t* __restrict__ sort_n_ptr,
-                                               CamParams cam, float* __restrict__ color, float* __restrict__ depth,
-                                               float* __restrict__ trans, uint8_t* __restrict__ touched,
-                                               unsigned long long* __restrict__ eval_counts) {
-    __shared__ float4 s_p0[256], s_p1[256], s_p2[256];
-    __shared__ float s_ik[256];
-    __shared__ uint32_t s_id[256];
-    __shared__ uint8_t s_hit[256];
-    __shared__ uint64_t s_et[32], s_lt[32];
-    const int tid = threadIdx.x;
-    if (tid < 32) {
-        s_et[tid] = c_exp2f_tab[tid];
-        s_lt[tid] = c_powf_log2_tab[tid];
-    }
-    const int tile = blockIdx.x;
-    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
-    const int x = tx * kTile + (tid & 15), y = ty * kTile + (tid >> 4);
-    const bool inside = x < cam.width && y < cam.height;
-    const float px = (float)x + 0.5f, py = (float)y + 0.5f;
-    uint2 range = make_uint2(0, 0);
-    if (*sort_n_ptr) range = ranges[tile];
-    float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, d = 0.0f;
-    bool done = !inside;
-    uint32_t n_eval = 0, n_contrib = 0;  // N_eval / contributions (roofline accounting)
-    for (uint32_t start = range.x; start < range.y; start += 256) {
-        if (__syncthreads_count(done) == 256) break;
-        const uint32_t j = start + tid;
-        if (j < range.y) {
-            const uint32_t id = vals[j];
-            const ProjRec* r = proj + id;
-            s_p0[tid] = r->p0;
-            s_p1[tid] = r->p1;
-            s_p2[tid] = r->p2;
-            s_ik[tid] = r->p3.x;
-            s_id[tid] = id;
-            s_hit[tid] = 0;
-        }
-        __syncthreads();
-        const int cnt = (int)min(256u, range.y - start);
-        if (!done) {
-            for (int k = 0; k < cnt; ++k) {
-                ++n_eval;
-                const float4 p0 = s_p0[k];
-                const float4 p1 = s_p1[k];
-                const float dx = px - p0.x, dy = py - p0.y;
-                const float power = -0.5f * (p0.z * dx * dx + p1.x * dy * dy) - p0.w * dx * dy;
-                if (!(power <= 0.0f)) continue;
-                const float tt = p1.w;
-                const float mfall = tt < 1.0f ? smax(p1.y, p1.z) : p1.y;
-                // Conservative pre-test: the alpha stays below the 1/255 floor for
-                // both laws, so the reference skips this entry; no exact exp needed.
-                if (power <= -80.0f ? mfall < 1e30f : __expf(power) * mfall < kAlphaMin * 0.999f) continue;
-                float g;
-                if (kMode == 0)
-                    g = hs_libm::expf_glibc(power, s_et);
-                else
-                    g = __expf(power);
-                const float self_raw = p1.y * g;
-                const float self = self_raw > kAlphaMax ? kAlphaMax : self_raw;
-                const float a_self = self >= kAlphaMin ? self : 0.0f;
-                float alpha;
-                if (tt < 1.0f) {
-                    const float par_raw = p1.z * g;
-                    const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
-                    float split = 0.0f;
-                    if (par >= kAlphaMin) {
-                        if (kMode == 0)
-                            split = 1.0f - hs_libm::powf_glibc(1.0f - par, s_ik[k], s_lt, s_et);
-                        else
-                            split = 1.0f - exp2f(s_ik[k] * __log2f(1.0f - par));
-                    }
-                    alpha = tt * a_self + (1.0f - tt) * split;
-                } else {
-                    alpha = a_self;
-                }
-                if (!(alpha > 0.0f)) continue;
-                const float test = T * (1.0f - alpha);
-                if (test < kTransmittanceEps) {
-                    done = true;
-                    break;
-                }
-                const float4 p2 = s_p2[k];
-                const float wgt = alpha * T;
-                c0 = c0 + p2.x * wgt;
-                c1 = c1 + p2.y * wgt;
-                c2 = c2 + p2.z * wgt;
-                d = d + p2.w * alpha * T;
-                T = test;
-                s_hit[k] = 1;
-                ++n_contrib;
-            }
-        }
-        __syncthreads();
-        if (j < range.y && s_hit[tid]) touched[s_id[tid]] = 1;
-    }
-    if (inside) {
-        const size_t plane = (size_t)cam.width * cam.height;
-        const size_t i = (size_t)y * cam.width + x;
-        color[i] = c0;
-        color[plane + i] = c1;
-        color[2 * plane + i] = c2;
-        depth[i] = d;
-        trans[i] = T;
-    }
-    for (int o = 16; o; o >>= 1) {
-        n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
-        n_contrib += __shfl_xor_sync(0xffffffffu, n_contrib, o);
-    }
-    if ((tid & 31) == 0) {
-        atomicAdd(eval_counts, (unsigned long long)n_eval);
-        atomicAdd(eval_counts + 1, (unsigned long long)n_contrib);
-    }
-}
-
-__global__ void k_count_touched(const uint8_t* __restrict__ touched, const uint64_t* __restrict__ n_ptr,
+__global__ void k_count_touched(uint8_t* __restrict__ touched, const uint64_t* __restrict__ n_ptr,
                                 unsigned long long* __restrict__ out) {
     const uint64_t n = *n_ptr;
     uint32_t c = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        c += touched[i];
+        if (touched[i]) {  // count, and leave the flags zeroed for the next frame
+            ++c;
+            touched[i] = 0;
+        }
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
 }
@@ -636,15 +520,6 @@ void launch_ranges(const uint64_t* keys, const uint64_t* sort_n_ptr, uint64_t n_
     k_ranges<<<grid_for(n_max, 8), 256, 0, s>>>(keys, sort_n_ptr, ranges);
 }
 
-void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
-                  const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
-                  unsigned long long* eval_counts, cudaStream_t s) {
-    const unsigned tiles = (unsigned)(cam.tiles_x * cam.tiles_y);
-    if (mode == 0)
-        k_blend<0><<<tiles, 256, 0, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched, eval_counts);
-    else
-        k_blend<1><<<tiles, 256, 0, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched, eval_counts);
-}
 
 void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr,
                      uint64_t n_max, float* mean, float* scale, float* rot, float* sh, float* fall, float* pfall,
@@ -653,7 +528,7 @@ void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* 
                                                    k);
 }
 
-void launch_count_touched(const uint8_t* touched, const uint64_t* n_ptr, uint64_t n_max, unsigned long long* out,
+void launch_count_touched(uint8_t* touched, const uint64_t* n_ptr, uint64_t n_max, unsigned long long* out,
                           cudaStream_t s) {
     k_count_touched<<<grid_for(n_max, 4), 256, 0, s>>>(touched, n_ptr, out);
 }
