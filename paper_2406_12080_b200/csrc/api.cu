@@ -233,7 +233,8 @@ uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 //   [8320]     scan status (u64 words)
 //   [...]      sort status (passes x sort_status_words u32)
 struct ScratchLayout {
-    size_t scan_counter = 0, sort_counters = 64, sort_hist = 128, scan_status = 8320, sort_status = 0, total = 0;
+    size_t scan_counter = 0, sort_counters = 64, blend_counter = 120, sort_hist = 128, scan_status = 8320,
+           sort_status = 0, total = 0;
 };
 ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int passes) {
     ScratchLayout L;
@@ -317,7 +318,7 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[4], s));
     hs::launch_blend(ctx->blend_mode, f->ranges.as<uint2>(), vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
                      f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(),
-                     &ds->n_eval, s);
+                     &ds->n_eval, reinterpret_cast<uint32_t*>(sc + L.blend_counter), s);
     hs::launch_count_touched(f->touched.as<uint8_t>(), f->n_ptr, f->n_max, &ds->rendered, s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[5], s));
     HS_CUDA(ctx, cudaGetLastError());

@@ -29,7 +29,7 @@ void launch_duplicate(const ProjRec* proj, const uint32_t* dupcount, const uint3
 void launch_ranges(const uint64_t* keys, const uint64_t* sort_n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s);
 void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
-                  unsigned long long* eval_counts, cudaStream_t s);
+                  unsigned long long* eval_counts, uint32_t* task_counter, cudaStream_t s);
 void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr,
                      uint64_t n_max, float* mean, float* scale, float* rot, float* sh, float* fall, float* pfall,
                      float* t, int* k, cudaStream_t s);
