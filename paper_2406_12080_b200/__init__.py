@@ -190,6 +190,8 @@ def synth_city(leaves: int, seed: int = 1, threads: int = 0) -> Hierarchy:
 def build_bvh(mean, scale, rot_wxyz, falloff, sh, threads: int = 0) -> Hierarchy:
     """build_bvh (build.hpp:73-149): median-split BVH + moment-matched interior nodes."""
     n = len(falloff)
+    if n == 0:
+        raise Error(int(Errc.EmptyScene) + 1, "EmptyScene: build_bvh needs at least one gaussian")
     a = [np.ascontiguousarray(x, np.float32).reshape(n, -1) for x in (mean, scale, rot_wxyz, falloff, sh)]
     h = Hierarchy.empty(2 * n - 1 if n else 0)
     st = N.lib().hs_build_bvh(*[N.ptr(x, C.c_float) for x in a], n, threads, C.byref(h.soa()))
