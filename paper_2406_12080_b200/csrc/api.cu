@@ -110,7 +110,7 @@ struct hs_frame {
     hs_context* ctx = nullptr;
     uint64_t cap_splats = 0, cap_dup = 0;
     int W = 0, H = 0, tiles_x = 0, tiles_y = 0, passes = 0;
-    DBuf proj, dupcount, offsets, keys[2], vals[2], dupk, dupv, ranges, color, depth, trans, touched, dbg16,
+    DBuf proj, dinfo, dupcount, offsets, keys[2], vals[2], dupk, dupv, ranges, color, depth, trans, touched, dbg16,
         splat_attr, stats, scratch;
     DevStats* h_stats = nullptr;  // pinned
     uint64_t* h_n = nullptr;      // pinned
@@ -250,6 +250,7 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
     const uint64_t cs = std::max<uint64_t>(f->cap_splats, 1);
     HS_CUDA(ctx, f->proj.ensure(cs * sizeof(ProjRec)));
     HS_CUDA(ctx, f->dupcount.ensure(cs * 4));
+    HS_CUDA(ctx, f->dinfo.ensure(cs * 16));
     HS_CUDA(ctx, f->offsets.ensure(cs * 4));
     const bool fresh_touched = f->touched.bytes < cs;
     HS_CUDA(ctx, f->touched.ensure(cs));
@@ -296,12 +297,13 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     HS_CUDA(ctx, cudaMemsetAsync(f->ranges.p, 0, (size_t)cp.tiles_x * cp.tiles_y * 8, s));
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[1], s));
     hs::launch_preprocess(f->from_cut, f->attr, f->cut_node, f->cut_t, f->n_ptr, f->n_max, cp, f->proj.as<ProjRec>(),
-                          f->dupcount.as<uint32_t>(), ctx->debug ? f->dbg16.as<float>() : nullptr, &ds->n_visible, s);
+                          f->dinfo.as<uint4>(), f->dupcount.as<uint32_t>(),
+                          ctx->debug ? f->dbg16.as<float>() : nullptr, &ds->n_visible, s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[2], s));
     hs::launch_scan(f->dupcount.as<uint32_t>(), f->n_ptr, f->n_max, f->offsets.as<uint32_t>(),
                     reinterpret_cast<uint64_t*>(sc + L.scan_status), reinterpret_cast<uint32_t*>(sc + L.scan_counter),
                     &ds->n_dup, &ds->sort_n, f->cap_dup, &ds->overflows, s);
-    hs::launch_duplicate(f->proj.as<ProjRec>(), f->dupcount.as<uint32_t>(), f->offsets.as<uint32_t>(), f->n_ptr,
+    hs::launch_duplicate(f->dinfo.as<uint4>(), f->dupcount.as<uint32_t>(), f->offsets.as<uint32_t>(), f->n_ptr,
                          f->n_max, &ds->sort_n, cp.tiles_x, f->keys[0].as<uint64_t>(), f->vals[0].as<uint32_t>(), s);
     if (ctx->debug) {
         HS_CUDA(ctx, cudaMemcpyAsync(f->dupk.p, f->keys[0].p, f->cap_dup * 8, cudaMemcpyDeviceToDevice, s));

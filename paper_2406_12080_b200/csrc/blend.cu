@@ -3,20 +3,24 @@
 //
 // Work unit = one warp on one 8x4 pixel block of a 16x16 tile (8 blocks per
 // tile).  Warps are persistent and pull (tile, block) tasks from an atomic
-// counter, so there is no CTA-wide barrier and no per-tile load imbalance.
-// A warp walks its tile's depth-sorted range 32 entries at a time: each lane
-// loads one 64-byte projected record and tests it against the warp's block —
-// the entry is skipped when its alpha provably stays under the 1/255 floor on
-// every pixel of the block (minimum of the conic quadratic over the block's
-// pixel centres, in double, above 2 ln(255 * max falloff*alpha_scale) with a
-// margin covering the float rounding of the reference's per-pixel power).  A
-// skipped entry is one the reference `continue`s past at every pixel of the
-// block, so results are unchanged bit for bit.  Surviving entries are staged
-// in per-warp shared memory and evaluated by all 32 pixels in depth order.
-//
-// Exact mode evaluates expf / powf with device replicas of the host glibc
-// (hs_libm.cuh): images are bit-identical to the CPU reference.  Fast mode
-// uses the SFU (ex2/lg2) and stays within the north-star tolerance.
+// counter: no CTA-wide barrier, no per-tile load imbalance.  A warp walks its
+// tile's depth-sorted range 32 entries at a time:
+//   1. each lane loads one 64-byte projected record and tests it against the
+//      warp's block — skipped when its alpha provably stays under the 1/255
+//      floor on every pixel of the block (minimum of the conic quadratic over
+//      the block's pixel centres, in double, above the per-splat threshold
+//      k_preprocess stored in p3.y).  A skipped entry is one the reference
+//      `continue`s past at every pixel of the block: results are unchanged;
+//   2. every lane computes its pixel's power for the surviving entries and
+//      marks the ones whose alpha can pass the floor ("live");
+//   3. each lane computes alpha for ITS live entries in a compacted loop.
+//      Alpha does not depend on transmittance, so this expensive part (the
+//      exact expf/powf replicas in double) runs out of order with all lanes
+//      busy instead of once per entry for whichever lanes happen to be live;
+//   4. the warp composites the entries in depth order (test/accumulate/break),
+//      exactly as the reference's per-pixel loop does.
+// Exact mode: expf / powf are device replicas of the host glibc (hs_libm.cuh),
+// images are bit-identical to the CPU reference.  Fast mode: SFU ex2/lg2.
 #include "hs_device.cuh"
 #include "hs_kernels.h"
 
@@ -26,47 +30,45 @@ constexpr int kBlendThreads = 256;
 constexpr int kBlendWarps = kBlendThreads / 32;
 
 // May the entry reach alpha >= 1/255 somewhere in the pixel-centre rectangle
-// [x0, x0+7] x [y0, y0+3] (relative to the splat mean)?
-__device__ __forceinline__ bool may_touch(const float4& p0, const float4& p1, double x0, double y0) {
-    const float m = p1.w < 1.0f ? smax(p1.y, p1.z) : p1.y;
-    if (!(m >= kAlphaMin)) return false;  // fa * g <= fa < 1/255: never passes the floor
-    const double a = p0.z, b = p0.w, c = p1.x;
-    const double det = a * c - b * b;
-    if (!(a > 0.0 && c > 0.0 && det > 0.0)) return true;
-    const double kappa = (a + c) * (a + c) / det;
-    const double shrink = 1.0 - 2e-5 * kappa;
-    if (shrink <= 0.0) return true;
-    const double thr = 2.0 * log(255.0 * (double)m) * (1.0 + 1e-5) + 1e-5;
+// [x0, x0+7] x [y0, y0+3] (relative to the splat mean)?  qthr (p3.y) already
+// carries the rounding margin; ia/ic are 1/a, 1/c (only pick the point where Q
+// is evaluated exactly, so their rounding cannot make the test unsafe beyond
+// a ~1e-14 relative change that the margin covers).
+__device__ __forceinline__ bool may_touch(const float4& p0, const float4& p1, const float4& p3, double x0,
+                                          double y0) {
+    const float qthr = p3.y;
+    if (qthr < 0.0f) return false;
     const double x1 = x0 + 7.0, y1 = y0 + 3.0;
     if (x0 <= 0.0 && 0.0 <= x1 && y0 <= 0.0 && 0.0 <= y1) return true;
-    const double ia = 1.0 / a, ic = 1.0 / c;
+    const double a = p0.z, b = p0.w, c = p1.x, ia = p3.z, ic = p3.w;
     double qm = 1e300;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
         const double x = e ? x1 : x0;
         double y = -b * x * ic;
         y = y < y0 ? y0 : (y > y1 ? y1 : y);
-        qm = fmin(qm, a * x * x + 2.0 * b * x * y + c * y * y);
+        qm = fmin(qm, (a * x + 2.0 * b * y) * x + c * y * y);
         const double yy = e ? y1 : y0;
         double xx = -b * yy * ia;
         xx = xx < x0 ? x0 : (xx > x1 ? x1 : xx);
-        qm = fmin(qm, a * xx * xx + 2.0 * b * xx * yy + c * yy * yy);
+        qm = fmin(qm, (a * xx + 2.0 * b * yy) * xx + c * yy * yy);
     }
-    return !(qm * shrink > thr);
+    return !(qm > (double)qthr);
 }
 
 template <int kMode>
 __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restrict__ ranges,
-                                                         const uint32_t* __restrict__ vals,
-                                                         const ProjRec* __restrict__ proj,
-                                                         const uint64_t* __restrict__ sort_n_ptr, CamParams cam,
-                                                         float* __restrict__ color, float* __restrict__ depth,
-                                                         float* __restrict__ trans, uint8_t* __restrict__ touched,
-                                                         unsigned long long* __restrict__ eval_counts,
-                                                         uint32_t* __restrict__ task_counter) {
+                                                            const uint32_t* __restrict__ vals,
+                                                            const ProjRec* __restrict__ proj,
+                                                            const uint64_t* __restrict__ sort_n_ptr, CamParams cam,
+                                                            float* __restrict__ color, float* __restrict__ depth,
+                                                            float* __restrict__ trans, uint8_t* __restrict__ touched,
+                                                            unsigned long long* __restrict__ eval_counts,
+                                                            uint32_t* __restrict__ task_counter) {
     __shared__ float4 s_p0[kBlendWarps][32], s_p1[kBlendWarps][32], s_p2[kBlendWarps][32];
     __shared__ float s_ik[kBlendWarps][32];
     __shared__ uint32_t s_id[kBlendWarps][32];
+    __shared__ float s_v[kBlendWarps][32][33];  // [entry][lane]: power, then alpha
     __shared__ uint64_t s_et[32], s_lt[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 32) {
@@ -77,6 +79,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
     const uint32_t num_tasks = (uint32_t)(cam.tiles_x * cam.tiles_y) * 8u;
     const bool any_keys = *sort_n_ptr != 0;
     uint32_t n_eval = 0, n_contrib = 0;
+    float(*sv)[33] = s_v[warp];
     while (true) {
         uint32_t task = 0;
         if (lane == 0) task = atomicAdd(task_counter, 1u);
@@ -94,62 +97,82 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
         bool done = !inside;
         for (uint32_t base = range.x; base < range.y; base += 32) {
             if (__all_sync(0xffffffffu, done)) break;
+            // 1. stage the entries that may touch this block
             const uint32_t e = base + lane;
             bool hit = false;
             if (e < range.y) {
                 const uint32_t id = vals[e];
                 const ProjRec* r = proj + id;
-                const float4 p0 = r->p0, p1 = r->p1;
-                hit = may_touch(p0, p1, (double)bx + 0.5 - (double)p0.x, (double)by + 0.5 - (double)p0.y);
+                const float4 p0 = r->p0, p1 = r->p1, p3 = r->p3;
+                hit = may_touch(p0, p1, p3, (double)bx + 0.5 - (double)p0.x, (double)by + 0.5 - (double)p0.y);
                 if (hit) {
                     s_p0[warp][lane] = p0;
                     s_p1[warp][lane] = p1;
                     s_p2[warp][lane] = r->p2;
-                    s_ik[warp][lane] = r->p3.x;
+                    s_ik[warp][lane] = p3.x;
                     s_id[warp][lane] = id;
                 }
             }
-            uint32_t bits = __ballot_sync(0xffffffffu, hit);
+            const uint32_t bits = __ballot_sync(0xffffffffu, hit);
             __syncwarp();
-            while (bits) {
-                const int k = __ffs(bits) - 1;
-                bits &= bits - 1;
-                bool contrib = false;
-                if (!done) {
-                    ++n_eval;
+            // 2. per-pixel power and liveness (cheap, all lanes)
+            uint32_t live = 0;
+            if (!done) {
+                for (uint32_t m = bits; m; m &= m - 1) {
+                    const int k = __ffs(m) - 1;
                     const float4 p0 = s_p0[warp][k];
                     const float4 p1 = s_p1[warp][k];
                     const float dx = px - p0.x, dy = py - p0.y;
                     const float power = -0.5f * (p0.z * dx * dx + p1.x * dy * dy) - p0.w * dx * dy;
-                    const float tt = p1.w;
-                    const float mfall = tt < 1.0f ? smax(p1.y, p1.z) : p1.y;
+                    const float mfall = p1.w < 1.0f ? smax(p1.y, p1.z) : p1.y;
                     // skip exactly when the reference's alpha cannot reach the 1/255 floor
-                    const bool live = (power <= 0.0f) &&
-                                      !(power <= -80.0f ? mfall < 1e30f : __expf(power) * mfall < kAlphaMin * 0.999f);
-                    if (live) {
-                        float g;
+                    const bool lv = (power <= 0.0f) &&
+                                    !(power <= -80.0f ? mfall < 1e30f : __expf(power) * mfall < kAlphaMin * 0.999f);
+                    if (lv) {
+                        live |= 1u << k;
+                        sv[k][lane] = power;
+                    }
+                }
+            }
+            // 3. alpha for this lane's live entries (independent of T: runs compacted)
+            for (uint32_t m = live; m; m &= m - 1) {
+                const int k = __ffs(m) - 1;
+                const float power = sv[k][lane];
+                const float4 p1 = s_p1[warp][k];
+                float g;
+                if (kMode == 0)
+                    g = hs_libm::expf_glibc(power, s_et);
+                else
+                    g = __expf(power);
+                const float tt = p1.w;
+                const float self_raw = p1.y * g;
+                const float self = self_raw > kAlphaMax ? kAlphaMax : self_raw;
+                const float a_self = self >= kAlphaMin ? self : 0.0f;
+                float alpha;
+                if (tt < 1.0f) {
+                    const float par_raw = p1.z * g;
+                    const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
+                    float split = 0.0f;
+                    if (par >= kAlphaMin) {
                         if (kMode == 0)
-                            g = hs_libm::expf_glibc(power, s_et);
+                            split = 1.0f - hs_libm::powf_glibc(1.0f - par, s_ik[warp][k], s_lt, s_et);
                         else
-                            g = __expf(power);
-                        const float self_raw = p1.y * g;
-                        const float self = self_raw > kAlphaMax ? kAlphaMax : self_raw;
-                        const float a_self = self >= kAlphaMin ? self : 0.0f;
-                        float alpha;
-                        if (tt < 1.0f) {
-                            const float par_raw = p1.z * g;
-                            const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
-                            float split = 0.0f;
-                            if (par >= kAlphaMin) {
-                                if (kMode == 0)
-                                    split = 1.0f - hs_libm::powf_glibc(1.0f - par, s_ik[warp][k], s_lt, s_et);
-                                else
-                                    split = 1.0f - exp2f(s_ik[warp][k] * __log2f(1.0f - par));
-                            }
-                            alpha = tt * a_self + (1.0f - tt) * split;
-                        } else {
-                            alpha = a_self;
-                        }
+                            split = 1.0f - exp2f(s_ik[warp][k] * __log2f(1.0f - par));
+                    }
+                    alpha = tt * a_self + (1.0f - tt) * split;
+                } else {
+                    alpha = a_self;
+                }
+                sv[k][lane] = alpha;
+            }
+            // 4. composite in depth order
+            for (uint32_t m = bits; m; m &= m - 1) {
+                const int k = __ffs(m) - 1;
+                bool contrib = false;
+                if (!done) {
+                    ++n_eval;
+                    if ((live >> k) & 1u) {
+                        const float alpha = sv[k][lane];
                         if (alpha > 0.0f) {
                             const float test = T * (1.0f - alpha);
                             if (test < kTransmittanceEps) {
@@ -168,9 +191,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
                         }
                     }
                 }
-                const uint32_t cb = __ballot_sync(0xffffffffu, contrib);
-                if (cb && lane == 0) touched[s_id[warp][k]] = 1;
-                if (__all_sync(0xffffffffu, done)) break;
+                if (__ballot_sync(0xffffffffu, contrib) && lane == 0) touched[s_id[warp][k]] = 1;
             }
             __syncwarp();
         }

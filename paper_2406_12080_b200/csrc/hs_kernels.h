@@ -17,13 +17,13 @@ uint64_t select_cut_status_words(uint64_t n);
 
 // raster.cu
 void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,
-                       const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint32_t* dupcount,
-                       float* dbg16, unsigned long long* n_visible, cudaStream_t s);
+                       const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint4* dinfo,
+                       uint32_t* dupcount, float* dbg16, unsigned long long* n_visible, cudaStream_t s);
 uint64_t scan_status_words(uint64_t n_max);
 void launch_scan(const uint32_t* counts, const uint64_t* n_ptr, uint64_t n_max, uint32_t* offsets, uint64_t* status,
                  uint32_t* tile_counter, uint64_t* total_out, uint64_t* sort_n_out, uint64_t capacity,
                  unsigned long long* overflows, cudaStream_t s);
-void launch_duplicate(const ProjRec* proj, const uint32_t* dupcount, const uint32_t* offsets, const uint64_t* n_ptr,
+void launch_duplicate(const uint4* dinfo, const uint32_t* dupcount, const uint32_t* offsets, const uint64_t* n_ptr,
                       uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint64_t* keys, uint32_t* vals,
                       cudaStream_t s);
 void launch_ranges(const uint64_t* keys, const uint64_t* sort_n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s);

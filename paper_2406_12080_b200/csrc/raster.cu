@@ -145,6 +145,7 @@ template <bool kFromCut>
 __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ attr, const uint32_t* __restrict__ cut_node,
                                                     const float* __restrict__ cut_t, const uint64_t* __restrict__ n_ptr,
                                                     CamParams cam, ProjRec* __restrict__ proj,
+                                                    uint4* __restrict__ dinfo,
                                                     uint32_t* __restrict__ dupcount, float* __restrict__ dbg16,
                                                     unsigned long long* __restrict__ n_visible) {
     const uint64_t n = *n_ptr;
@@ -330,9 +331,27 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ a
         rec.p0 = make_float4(mx, my, con0, con1);
         rec.p1 = make_float4(con2, fe * ascale, pe * ascale, t);
         rec.p2 = make_float4(col[0], col[1], col[2], invd);
-        rec.p3 = make_float4(1.0f / (float)max(1, K), __uint_as_float((uint32_t)tx0 | ((uint32_t)tx1 << 16)),
-                             __uint_as_float((uint32_t)ty0 | ((uint32_t)ty1 << 16)), tc[2]);
+        // Block-culling threshold for the blend (blend.cu may_touch): alpha >= 1/255 needs
+        // Q(dx,dy) = conic quadratic <= 2 ln(255 m); inflated by a margin covering the float
+        // rounding of the reference's per-pixel power (relative ~1e-6 * kappa) and rounded up.
+        float qthr;
+        {
+            const float m = t < 1.0f ? smax(rec.p1.y, rec.p1.z) : rec.p1.y;
+            const double a = con0, b = con1, c = con2, det = a * c - b * b;
+            if (!(m >= kAlphaMin)) {
+                qthr = -1.0f;  // fa * g <= fa < 1/255: never passes the floor anywhere
+            } else if (!(a > 0.0 && c > 0.0 && det > 0.0)) {
+                qthr = __int_as_float(0x7f800000);
+            } else {
+                const double shrink = 1.0 - 2e-5 * ((a + c) * (a + c) / det);
+                const double thr = 2.0 * log(255.0 * (double)m) * (1.0 + 1e-5) + 1e-5;
+                qthr = shrink > 0.0 ? __double2float_ru(thr / shrink) : __int_as_float(0x7f800000);
+            }
+        }
+        rec.p3 = make_float4(1.0f / (float)max(1, K), qthr, 1.0f / con0, 1.0f / con2);
         proj[j] = rec;
+        dinfo[j] = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16),
+                              __float_as_uint(tc[2]), 0u);
         dupcount[j] = (uint32_t)((tx1 - tx0) * (ty1 - ty0));
     }
     // warp-aggregated visible count
@@ -422,7 +441,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
 // -------------------------------------------------------------------------
 // key duplication: keys in (splat id asc, ty asc, tx asc) order
 // -------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_duplicate(const ProjRec* __restrict__ proj, const uint32_t* __restrict__ dupcount,
+__global__ void __launch_bounds__(256) k_duplicate(const uint4* __restrict__ dinfo, const uint32_t* __restrict__ dupcount,
                                                    const uint32_t* __restrict__ offsets, const uint64_t* __restrict__ n_ptr,
                                                    const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
                                                    uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
@@ -430,9 +449,8 @@ __global__ void __launch_bounds__(256) k_duplicate(const ProjRec* __restrict__ p
     if (*sort_n_ptr == 0) return;  // empty or over capacity
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
         if (dupcount[j] == 0) continue;
-        const float4 p3 = proj[j].p3;
-        const uint32_t rx = __float_as_uint(p3.y), ry = __float_as_uint(p3.z);
-        const uint32_t zb = __float_as_uint(p3.w);
+        const uint4 di = dinfo[j];
+        const uint32_t rx = di.x, ry = di.y, zb = di.z;
         const int tx0 = rx & 0xffff, tx1 = rx >> 16, ty0 = ry & 0xffff, ty1 = ry >> 16;
         uint64_t o = offsets[j];
         for (int ty = ty0; ty < ty1; ++ty)
@@ -490,13 +508,15 @@ static unsigned grid_for(uint64_t n_max, int per_sm) {
 }
 
 void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,
-                       const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint32_t* dupcount,
-                       float* dbg16, unsigned long long* n_visible, cudaStream_t s) {
+                       const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint4* dinfo,
+                       uint32_t* dupcount, float* dbg16, unsigned long long* n_visible, cudaStream_t s) {
     const unsigned grid = grid_for(n_max, 8);
     if (from_cut)
-        k_preprocess<true><<<grid, 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, cam, proj, dupcount, dbg16, n_visible);
+        k_preprocess<true><<<grid, 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, cam, proj, dinfo, dupcount, dbg16,
+                                                n_visible);
     else
-        k_preprocess<false><<<grid, 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, cam, proj, dupcount, dbg16, n_visible);
+        k_preprocess<false><<<grid, 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, cam, proj, dinfo, dupcount, dbg16,
+                                                 n_visible);
 }
 
 uint64_t scan_status_words(uint64_t n_max) { return (n_max + kScanTile - 1) / kScanTile + 1; }
@@ -510,10 +530,10 @@ void launch_scan(const uint32_t* counts, const uint64_t* n_ptr, uint64_t n_max, 
                                          overflows);
 }
 
-void launch_duplicate(const ProjRec* proj, const uint32_t* dupcount, const uint32_t* offsets, const uint64_t* n_ptr,
+void launch_duplicate(const uint4* dinfo, const uint32_t* dupcount, const uint32_t* offsets, const uint64_t* n_ptr,
                       uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint64_t* keys, uint32_t* vals,
                       cudaStream_t s) {
-    k_duplicate<<<grid_for(n_max, 8), 256, 0, s>>>(proj, dupcount, offsets, n_ptr, sort_n_ptr, tiles_x, keys, vals);
+    k_duplicate<<<grid_for(n_max, 8), 256, 0, s>>>(dinfo, dupcount, offsets, n_ptr, sort_n_ptr, tiles_x, keys, vals);
 }
 
 void launch_ranges(const uint64_t* keys, const uint64_t* sort_n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s) {
