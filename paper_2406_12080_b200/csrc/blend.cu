@@ -21,6 +21,8 @@
 //      exactly as the reference's per-pixel loop does.
 // Exact mode: expf / powf are device replicas of the host glibc (hs_libm.cuh),
 // images are bit-identical to the CPU reference.  Fast mode: SFU ex2/lg2.
+#include <cuda_pipeline.h>
+
 #include "hs_device.cuh"
 #include "hs_kernels.h"
 
@@ -57,7 +59,7 @@ __device__ __forceinline__ bool may_touch(const float4& p0, const float4& p1, co
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restrict__ ranges,
+__global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2* __restrict__ ranges,
                                                             const uint32_t* __restrict__ vals,
                                                             const ProjRec* __restrict__ proj,
                                                             const uint64_t* __restrict__ sort_n_ptr, CamParams cam,
@@ -65,10 +67,11 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
                                                             float* __restrict__ trans, uint8_t* __restrict__ touched,
                                                             unsigned long long* __restrict__ eval_counts,
                                                             uint32_t* __restrict__ task_counter) {
-    __shared__ float4 s_p0[kBlendWarps][32], s_p1[kBlendWarps][32], s_p2[kBlendWarps][32];
-    __shared__ float s_ik[kBlendWarps][32];
-    __shared__ uint32_t s_id[kBlendWarps][32];
-    __shared__ float s_v[kBlendWarps][32][33];  // [entry][lane]: power, then alpha
+    // per warp: two stages of 32 staged 64-byte records (cp.async double buffer)
+    // (dynamic) s_rec[kBlendWarps][2][32][4] float4, then s_v[kBlendWarps][32][32] float
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto s_rec = reinterpret_cast<float4(*)[2][32][4]>(smem_raw);
+    auto s_v = reinterpret_cast<float(*)[32][32]>(smem_raw + sizeof(float4) * kBlendWarps * 2 * 32 * 4);
     __shared__ uint64_t s_et[32], s_lt[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 32) {
@@ -79,7 +82,16 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
     const uint32_t num_tasks = (uint32_t)(cam.tiles_x * cam.tiles_y) * 8u;
     const bool any_keys = *sort_n_ptr != 0;
     uint32_t n_eval = 0, n_contrib = 0;
-    float(*sv)[33] = s_v[warp];
+    float(*sv)[32] = s_v[warp];  // [entry][lane]: power, then alpha (lane-contiguous, conflict free)
+    // stage entry `e` (if in range) of the current task into stage `st`, lane slot
+    auto issue = [&](int st, uint32_t e, uint32_t end, uint32_t id) {
+        if (e < end) {
+            const float4* src = reinterpret_cast<const float4*>(proj + id);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) __pipeline_memcpy_async(&s_rec[warp][st][lane][q], src + q, 16);
+        }
+        __pipeline_commit();
+    };
     while (true) {
         uint32_t task = 0;
         if (lane == 0) task = atomicAdd(task_counter, 1u);
@@ -91,37 +103,39 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
         const int x = bx + (lane & 7), y = by + (lane >> 3);
         const bool inside = x < cam.width && y < cam.height;
         const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+        const double ox = (double)bx + 0.5, oy = (double)by + 0.5;
         uint2 range = make_uint2(0, 0);
         if (any_keys) range = ranges[tile];
         float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, d = 0.0f;
         bool done = !inside;
-        for (uint32_t base = range.x; base < range.y; base += 32) {
-            if (__all_sync(0xffffffffu, done)) break;
-            // 1. stage the entries that may touch this block
-            const uint32_t e = base + lane;
-            bool hit = false;
-            if (e < range.y) {
-                const uint32_t id = vals[e];
-                const ProjRec* r = proj + id;
-                const float4 p0 = r->p0, p1 = r->p1, p3 = r->p3;
-                hit = may_touch(p0, p1, p3, (double)bx + 0.5 - (double)p0.x, (double)by + 0.5 - (double)p0.y);
-                if (hit) {
-                    s_p0[warp][lane] = p0;
-                    s_p1[warp][lane] = p1;
-                    s_p2[warp][lane] = r->p2;
-                    s_ik[warp][lane] = p3.x;
-                    s_id[warp][lane] = id;
-                }
-            }
-            const uint32_t bits = __ballot_sync(0xffffffffu, hit);
+        // prologue: ids of batches 0 and 1, records of batch 0 in flight
+        uint32_t id_cur = range.x + lane < range.y ? vals[range.x + lane] : 0u;
+        uint32_t id_nxt = range.x + 32 + lane < range.y ? vals[range.x + 32 + lane] : 0u;
+        issue(0, range.x + lane, range.y, id_cur);
+        int b = 0;
+        for (uint32_t base = range.x; base < range.y; base += 32, ++b) {
+            // records of the next batch in flight while this one is processed
+            issue((b + 1) & 1, base + 32 + lane, range.y, id_nxt);
+            const uint32_t id_b = id_cur;
+            id_cur = id_nxt;
+            id_nxt = base + 64 + lane < range.y ? vals[base + 64 + lane] : 0u;
+            __pipeline_wait_prior(1);
             __syncwarp();
+            if (__all_sync(0xffffffffu, done)) break;
+            const float4(*rec)[4] = s_rec[warp][b & 1];
+            // 1. which staged entries may touch this block
+            bool hit = false;
+            if (base + lane < range.y)
+                hit = may_touch(rec[lane][0], rec[lane][1], rec[lane][3], ox - (double)rec[lane][0].x,
+                                oy - (double)rec[lane][0].y);
+            const uint32_t bits = __ballot_sync(0xffffffffu, hit);
             // 2. per-pixel power and liveness (cheap, all lanes)
             uint32_t live = 0;
             if (!done) {
                 for (uint32_t m = bits; m; m &= m - 1) {
                     const int k = __ffs(m) - 1;
-                    const float4 p0 = s_p0[warp][k];
-                    const float4 p1 = s_p1[warp][k];
+                    const float4 p0 = rec[k][0];
+                    const float4 p1 = rec[k][1];
                     const float dx = px - p0.x, dy = py - p0.y;
                     const float power = -0.5f * (p0.z * dx * dx + p1.x * dy * dy) - p0.w * dx * dy;
                     const float mfall = p1.w < 1.0f ? smax(p1.y, p1.z) : p1.y;
@@ -138,7 +152,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
             for (uint32_t m = live; m; m &= m - 1) {
                 const int k = __ffs(m) - 1;
                 const float power = sv[k][lane];
-                const float4 p1 = s_p1[warp][k];
+                const float4 p1 = rec[k][1];
                 float g;
                 if (kMode == 0)
                     g = hs_libm::expf_glibc(power, s_et);
@@ -154,10 +168,11 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
                     const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
                     float split = 0.0f;
                     if (par >= kAlphaMin) {
+                        const float ik = rec[k][3].x;
                         if (kMode == 0)
-                            split = 1.0f - hs_libm::powf_glibc(1.0f - par, s_ik[warp][k], s_lt, s_et);
+                            split = 1.0f - hs_libm::powf_glibc(1.0f - par, ik, s_lt, s_et);
                         else
-                            split = 1.0f - exp2f(s_ik[warp][k] * __log2f(1.0f - par));
+                            split = 1.0f - exp2f(ik * __log2f(1.0f - par));
                     }
                     alpha = tt * a_self + (1.0f - tt) * split;
                 } else {
@@ -178,7 +193,7 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
                             if (test < kTransmittanceEps) {
                                 done = true;
                             } else {
-                                const float4 p2 = s_p2[warp][k];
+                                const float4 p2 = rec[k][2];
                                 const float wgt = alpha * T;
                                 c0 = c0 + p2.x * wgt;
                                 c1 = c1 + p2.y * wgt;
@@ -191,10 +206,14 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
                         }
                     }
                 }
-                if (__ballot_sync(0xffffffffu, contrib) && lane == 0) touched[s_id[warp][k]] = 1;
+                const uint32_t cb = __ballot_sync(0xffffffffu, contrib);
+                const uint32_t idk = __shfl_sync(0xffffffffu, id_b, k);
+                if (cb && lane == 0) touched[idk] = 1;
             }
             __syncwarp();
         }
+        __pipeline_wait_prior(0);
+        __syncwarp();
         if (inside) {
             const size_t plane = (size_t)cam.width * cam.height;
             const size_t i = (size_t)y * cam.width + x;
@@ -218,25 +237,29 @@ __global__ void __launch_bounds__(kBlendThreads, 4) k_blend(const uint2* __restr
 void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
                   unsigned long long* eval_counts, uint32_t* task_counter, cudaStream_t s) {
+    constexpr size_t kSmem = sizeof(float4) * kBlendWarps * 2 * 32 * 4 + sizeof(float) * kBlendWarps * 32 * 32;
     static int grid[2] = {0, 0};
     if (!grid[mode]) {
         int dev = 0, sms = 148, per = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (mode == 0)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blend<0>, kBlendThreads, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blend<1>, kBlendThreads, 0);
+        if (mode == 0) {
+            cudaFuncSetAttribute(k_blend<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blend<0>, kBlendThreads, kSmem);
+        } else {
+            cudaFuncSetAttribute(k_blend<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blend<1>, kBlendThreads, kSmem);
+        }
         grid[mode] = sms * (per > 0 ? per : 1);
     }
     // tiles * 8 warp tasks = `tiles` CTAs of 8 warps at most
     const unsigned g = (unsigned)std::min<int>(grid[mode], std::max(1, cam.tiles_x * cam.tiles_y));
     if (mode == 0)
-        k_blend<0><<<g, kBlendThreads, 0, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
-                                               eval_counts, task_counter);
+        k_blend<0><<<g, kBlendThreads, kSmem, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
+                                                   eval_counts, task_counter);
     else
-        k_blend<1><<<g, kBlendThreads, 0, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
-                                               eval_counts, task_counter);
+        k_blend<1><<<g, kBlendThreads, kSmem, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
+                                                   eval_counts, task_counter);
 }
 
 }  // namespace hs
