@@ -28,8 +28,11 @@
 
 namespace hs {
 
-constexpr int kBlendThreads = 256;
+constexpr int kBlendThreads = 128;
 constexpr int kBlendWarps = kBlendThreads / 32;
+constexpr size_t kSmemRec = sizeof(float4) * kBlendWarps * 2 * 32 * 4;  // 2-stage record staging
+constexpr size_t kSmemV = sizeof(float) * kBlendWarps * 32 * 33;        // power / alpha per (entry, lane)
+constexpr size_t kSmemQ = sizeof(uint16_t) * kBlendWarps * 1024;        // live-pair queue
 
 // May the entry reach alpha >= 1/255 somewhere in the pixel-centre rectangle
 // [x0, x0+7] x [y0, y0+3] (relative to the splat mean)?  qthr (p3.y) already
@@ -59,7 +62,7 @@ __device__ __forceinline__ bool may_touch(const float4& p0, const float4& p1, co
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2* __restrict__ ranges,
+__global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restrict__ ranges,
                                                             const uint32_t* __restrict__ vals,
                                                             const ProjRec* __restrict__ proj,
                                                             const uint64_t* __restrict__ sort_n_ptr, CamParams cam,
@@ -68,10 +71,11 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2* __restr
                                                             unsigned long long* __restrict__ eval_counts,
                                                             uint32_t* __restrict__ task_counter) {
     // per warp: two stages of 32 staged 64-byte records (cp.async double buffer)
-    // (dynamic) s_rec[kBlendWarps][2][32][4] float4, then s_v[kBlendWarps][32][32] float
+    // (dynamic) s_rec[warps][2][32][4] float4 | s_v[warps][32][33] float | s_q[warps][1024] u16
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto s_rec = reinterpret_cast<float4(*)[2][32][4]>(smem_raw);
-    auto s_v = reinterpret_cast<float(*)[32][32]>(smem_raw + sizeof(float4) * kBlendWarps * 2 * 32 * 4);
+    auto s_v = reinterpret_cast<float(*)[32][33]>(smem_raw + kSmemRec);
+    auto s_q = reinterpret_cast<uint16_t(*)[1024]>(smem_raw + kSmemRec + kSmemV);
     __shared__ uint64_t s_et[32], s_lt[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 32) {
@@ -82,7 +86,8 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2* __restr
     const uint32_t num_tasks = (uint32_t)(cam.tiles_x * cam.tiles_y) * 8u;
     const bool any_keys = *sort_n_ptr != 0;
     uint32_t n_eval = 0, n_contrib = 0;
-    float(*sv)[32] = s_v[warp];  // [entry][lane]: power, then alpha (lane-contiguous, conflict free)
+    float(*sv)[33] = s_v[warp];  // [entry][lane]: power, then alpha (row padding: conflict free both ways)
+    uint16_t* sq = s_q[warp];    // queue of live (lane << 5 | entry) pairs
     // stage entry `e` (if in range) of the current task into stage `st`, lane slot
     auto issue = [&](int st, uint32_t e, uint32_t end, uint32_t id) {
         if (e < end) {
@@ -148,11 +153,26 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2* __restr
                     }
                 }
             }
-            // 3. alpha for this lane's live entries (independent of T: runs compacted)
-            for (uint32_t m = live; m; m &= m - 1) {
-                const int k = __ffs(m) - 1;
-                const float power = sv[k][lane];
-                const float4 p1 = rec[k][1];
+            // 3. alpha of every live (pixel, entry) pair.  Alpha does not depend on T, so the
+            //    pairs of all lanes are compacted into one queue and evaluated 32 at a time
+            //    with every lane busy (the exact expf/powf replicas are the costly part).
+            {
+                const uint32_t cnt = __popc(live);
+                uint32_t incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                uint32_t pos = incl - cnt;
+                for (uint32_t m = live; m; m &= m - 1) sq[pos++] = (uint16_t)((lane << 5) | (__ffs(m) - 1));
+                __syncwarp();
+                for (uint32_t pq = lane; pq < total; pq += 32) {
+                    const uint32_t pr = sq[pq];
+                    const int src = (int)(pr >> 5), k = (int)(pr & 31);
+                    const float power = sv[k][src];
+                    const float4 p1 = rec[k][1];
                 float g;
                 if (kMode == 0)
                     g = hs_libm::expf_glibc(power, s_et);
@@ -170,7 +190,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2* __restr
                     if (par >= kAlphaMin) {
                         const float ik = rec[k][3].x;
                         if (kMode == 0)
-                            split = 1.0f - hs_libm::powf_glibc(1.0f - par, ik, s_lt, s_et);
+                            split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, ik, s_lt, s_et);
                         else
                             split = 1.0f - exp2f(ik * __log2f(1.0f - par));
                     }
@@ -178,7 +198,9 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2* __restr
                 } else {
                     alpha = a_self;
                 }
-                sv[k][lane] = alpha;
+                sv[k][src] = alpha;
+                }
+                __syncwarp();
             }
             // 4. composite in depth order
             for (uint32_t m = bits; m; m &= m - 1) {
@@ -237,7 +259,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3) k_blend(const uint2* __restr
 void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
                   unsigned long long* eval_counts, uint32_t* task_counter, cudaStream_t s) {
-    constexpr size_t kSmem = sizeof(float4) * kBlendWarps * 2 * 32 * 4 + sizeof(float) * kBlendWarps * 32 * 32;
+    constexpr size_t kSmem = kSmemRec + kSmemV + kSmemQ;
     static int grid[2] = {0, 0};
     if (!grid[mode]) {
         int dev = 0, sms = 148, per = 1;
@@ -252,8 +274,8 @@ void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const Pro
         }
         grid[mode] = sms * (per > 0 ? per : 1);
     }
-    // tiles * 8 warp tasks = `tiles` CTAs of 8 warps at most
-    const unsigned g = (unsigned)std::min<int>(grid[mode], std::max(1, cam.tiles_x * cam.tiles_y));
+    const int tasks = cam.tiles_x * cam.tiles_y * 8;
+    const unsigned g = (unsigned)std::min<int>(grid[mode], std::max(1, tasks / kBlendWarps));
     if (mode == 0)
         k_blend<0><<<g, kBlendThreads, kSmem, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
                                                    eval_counts, task_counter);

@@ -158,6 +158,38 @@ HS_HD int powf_checkint(uint32_t iy) {
 }
 HS_HD int powf_zeroinfnan(uint32_t ix) { return 2 * ix - 1 >= 2u * 0x7f800000u - 1; }
 
+// __powf_fma restricted to the split law's domain: x normal positive, y finite
+// non-zero with |y * log2(x)| < 126 (x = 1 - par in [0.01, 1), y = 1/K).  On
+// that domain glibc takes exactly this path (no special-case branches).
+HS_HD float powf_glibc_normal(float x, float y, const uint64_t* log2tab, const uint64_t* exptab) {
+    const uint32_t ix = as_u32(x);
+    const uint32_t tmp = ix - 0x3f330000u;
+    const int i = (int)((tmp >> 19) & 15);
+    const uint32_t top = tmp & 0xff800000u;
+    const uint32_t iz = ix - top;
+    const int k = (int32_t)top >> 23;
+    const double invc = as_double(log2tab[2 * i]);
+    const double logc = as_double(log2tab[2 * i + 1]);
+    const double z = (double)as_float(iz);
+    const double r = dfma(z, invc, -1.0);
+    const double y0 = (double)k + logc;
+    const double r2 = r * r;
+    const double yy = dfma(r, HS_POWF_A0, HS_POWF_A1);
+    const double p = dfma(r, HS_POWF_A2, HS_POWF_A3);
+    const double r4 = r2 * r2;
+    double q = dfma(r, HS_POWF_A4, y0);
+    q = dfma(r2, p, q);
+    const double ylogx = (double)y * dfma(yy, r4, q);
+    double kd = ylogx + HS_EXP2F_SHIFT_SCALED;
+    const uint64_t ki = as_u64(kd);
+    kd = kd - HS_EXP2F_SHIFT_SCALED;
+    const double rr = ylogx - kd;
+    const double s = as_double(exptab[ki & 31] + (ki << 47));
+    const double zz = dfma(rr, HS_EXP2F_POLY0, HS_EXP2F_POLY1);
+    const double e = dfma(zz, rr * rr, dfma(rr, HS_EXP2F_POLY2, 1.0));
+    return (float)(e * s);
+}
+
 // glibc __powf_fma.  `log2tab` = HS_POWF_LOG2_TAB_INIT, `exptab` = HS_EXP2F_TAB_INIT.
 HS_HD float powf_glibc(float x, float y, const uint64_t* log2tab, const uint64_t* exptab) {
     uint32_t sign_bias = 0;
