@@ -143,10 +143,9 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
                     const float4 p1 = rec[k][1];
                     const float dx = px - p0.x, dy = py - p0.y;
                     const float power = -0.5f * (p0.z * dx * dx + p1.x * dy * dy) - p0.w * dx * dy;
-                    const float mfall = p1.w < 1.0f ? smax(p1.y, p1.z) : p1.y;
-                    // skip exactly when the reference's alpha cannot reach the 1/255 floor
-                    const bool lv = (power <= 0.0f) &&
-                                    !(power <= -80.0f ? mfall < 1e30f : __expf(power) * mfall < kAlphaMin * 0.999f);
+                    // live iff the alpha can reach the 1/255 floor: m e^power >= 1/255 needs
+                    // power >= -ln(255 m) >= -qthr/2 (qthr carries the margin; *0.5 is exact)
+                    const bool lv = (power <= 0.0f) && (power >= -0.5f * rec[k][3].y);
                     if (lv) {
                         live |= 1u << k;
                         sv[k][lane] = power;
@@ -203,6 +202,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
                 __syncwarp();
             }
             // 4. composite in depth order
+            uint32_t tmask = 0;
             for (uint32_t m = bits; m; m &= m - 1) {
                 const int k = __ffs(m) - 1;
                 bool contrib = false;
@@ -228,10 +228,9 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
                         }
                     }
                 }
-                const uint32_t cb = __ballot_sync(0xffffffffu, contrib);
-                const uint32_t idk = __shfl_sync(0xffffffffu, id_b, k);
-                if (cb && lane == 0) touched[idk] = 1;
+                if (__any_sync(0xffffffffu, contrib)) tmask |= 1u << k;
             }
+            if ((tmask >> lane) & 1u) touched[id_b] = 1;  // rendered_count flags, one store per entry
             __syncwarp();
         }
         __pipeline_wait_prior(0);
