@@ -1,0 +1,126 @@
+// C++ drop-in check: the reference-shaped API of include/hsplat/gpu.hpp, used
+// exactly like the reference's own tests use hsplat:: (tests/test_lod.cpp,
+// tests/test_render.cpp, tests/test_bench.cpp).  Needs a GPU; run by
+// tests/test_dropin_cpp.py.  Exit code = number of failed checks.
+#include <hsplat/gpu.hpp>
+
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+static int failures = 0;
+#define CHECK(cond)                                                       \
+    do {                                                                  \
+        if (!(cond)) {                                                    \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);   \
+            ++failures;                                                   \
+        }                                                                 \
+    } while (0)
+
+static hsplat::CameraModel look_at(float px, float py, float pz, float tx, float ty, float tz, int w, int h, float f) {
+    auto norm = [](float v[3]) {
+        const float n = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+        for (int k = 0; k < 3; ++k) v[k] /= n;
+    };
+    float z[3] = {tx - px, ty - py, tz - pz};
+    norm(z);
+    float x[3] = {1.0f * z[2] - 0.0f * z[1], 0.0f * z[0] - 0.0f * z[2], 0.0f * z[1] - 1.0f * z[0]};  // up x z
+    norm(x);
+    const float y[3] = {z[1] * x[2] - z[2] * x[1], z[2] * x[0] - z[0] * x[2], z[0] * x[1] - z[1] * x[0]};
+    hsplat::CameraModel c;
+    c.width = w;
+    c.height = h;
+    c.focal.x() = c.focal.y() = f;
+    c.principal.x() = w * 0.5f;
+    c.principal.y() = h * 0.5f;
+    const float p[3] = {px, py, pz};
+    for (int k = 0; k < 3; ++k) {
+        c.world_to_camera(0, k) = x[k];
+        c.world_to_camera(1, k) = y[k];
+        c.world_to_camera(2, k) = z[k];
+    }
+    for (int r = 0; r < 3; ++r)
+        c.world_to_camera(r, 3) = -(c.world_to_camera(r, 0) * p[0] + c.world_to_camera(r, 1) * p[1] +
+                                    c.world_to_camera(r, 2) * p[2]);
+    return c;
+}
+
+static hsplat::Hierarchy synth(std::uint64_t leaves) {
+    const std::uint64_t n = hs_synth_node_count(leaves);
+    std::vector<std::uint32_t> parent(n), fc(n), cc(n);
+    std::vector<float> bmin(3 * n), bmax(3 * n), mean(3 * n), scale(3 * n), rot(4 * n), fall(n), sh(48 * n);
+    hs_node_soa_out o{parent.data(), fc.data(), cc.data(), bmin.data(), bmax.data(),
+                      mean.data(),   scale.data(), rot.data(), fall.data(), sh.data()};
+    if (hs_synth_city(leaves, 7, 0, &o) != HS_OK) std::abort();
+    hs_node_soa in{parent.data(), fc.data(), cc.data(), bmin.data(), bmax.data(),
+                   mean.data(),   scale.data(), rot.data(), fall.data(), sh.data()};
+    hs_h3dg_write("/tmp/hs_dropin.h3dg", &in, n, 3);
+    return hsplat::read_hierarchy("/tmp/hs_dropin.h3dg");
+}
+
+int main() {
+    using namespace hsplat;
+    const Hierarchy h = synth(20000);
+    CHECK(h.leaf_count() == 20000);
+    const float side = hs_synth_scene_side(20000);
+    const CameraModel cam = look_at(0, 12, -0.5f * side - 8, 0, 0, -0.5f * side + 40, 160, 120, 120.0f);
+
+    // select_cut: ascending node order, partition sanity, t in [0,1] (test_lod.cpp:160-241)
+    const auto cut = select_cut(h, cam, 3.0f);
+    CHECK(!cut.empty());
+    for (std::size_t i = 1; i < cut.size(); ++i) CHECK(cut[i - 1].node < cut[i].node);
+    for (const auto& e : cut) CHECK(e.t >= 0.0f && e.t <= 1.0f);
+    const auto leaves = select_cut(h, cam, 0.0f);
+    CHECK(leaves.size() == h.leaf_count());
+    bool threw = false;
+    try {
+        select_cut(h, cam, -1.0f);
+    } catch (const Error& e) {
+        threw = e.code() == Errc::InvalidArgument;
+    }
+    CHECK(threw);
+
+    // cut_render_splats: plain entries copy the node (test_lod.cpp:267-292)
+    const auto splats = cut_render_splats(h, cut);
+    CHECK(splats.size() == cut.size());
+    for (std::size_t i = 0; i < cut.size(); ++i)
+        if (cut[i].t >= 1.0f) CHECK(splats[i].falloff == h.nodes[cut[i].node].g.falloff);
+
+    // render_hierarchy == render_forward(cut_render_splats(select_cut)) (render.hpp:706-720)
+    StageTimes st;
+    ForwardContext fctx;
+    const RenderOutput a = render_hierarchy(h, cam, 3.0f, &fctx, &st);
+    const RenderOutput b = render_forward<float>(std::span<const RenderSplat>(splats), cam);
+    CHECK(a.rendered_count > 0 && a.rendered_count == b.rendered_count);
+    CHECK(a.color.data == b.color.data);
+    CHECK(a.transmittance.data == b.transmittance.data);
+    CHECK(fctx.valid && fctx.tile_start.back() == fctx.tile_entries.size());
+    CHECK(st.alpha_blend > 0.0 && st.cut_expand > 0.0);
+    for (float v : a.transmittance.data) CHECK(v >= 0.0f && v <= 1.0f);
+
+    // empty scene (test_render.cpp:234-241)
+    const RenderOutput e = render_forward<float>(std::span<const RenderSplat>(), cam);
+    CHECK(e.rendered_count == 0);
+    for (float v : e.transmittance.data) CHECK(v == 1.0f);
+
+    // bench_path: static path uploads once (test_bench.cpp:91-113)
+    CameraPath path;
+    for (int i = 0; i < 6; ++i) path.cameras.push_back(cam);
+    const BenchReport rep = bench_path(h, path, 3.0f);
+    CHECK(rep.frames.size() == 6);
+    CHECK(rep.frames[0].transferred == rep.frames[0].rendered);
+    for (std::size_t i = 1; i < 6; ++i) CHECK(rep.frames[i].transferred == 0);
+    for (std::size_t i = 1; i < 6; i += 2) CHECK(rep.frames[i].stages.cut_expand == 0.0);
+
+    // read_hierarchy error code (io.hpp:375-387)
+    threw = false;
+    try {
+        read_hierarchy("/nonexistent/x.h3dg");
+    } catch (const Error& err) {
+        threw = err.code() == Errc::IoFailure;
+    }
+    CHECK(threw);
+
+    std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "PASS", failures);
+    return failures;
+}
