@@ -204,6 +204,14 @@ hs_status hs_frame_get_info(hs_context* ctx, hs_frame* f, hs_frame_info* info);
  * inverse depth H*W, transmittance H*W; any pointer may be NULL */
 hs_status hs_frame_download(hs_context* ctx, hs_frame* f, float* color, float* depth, float* transmittance,
                             int32_t* rendered_count);
+/* Asynchronous read-back on the context's copy stream (overlaps the next
+ * frame's kernels; host buffers should be pinned, see hs_host_alloc).  A later
+ * render into the same frame object waits for the copy on the device;
+ * hs_frame_download_wait returns when the bytes have landed. */
+hs_status hs_frame_download_async(hs_context* ctx, hs_frame* f, float* color, float* depth, float* transmittance);
+hs_status hs_frame_download_wait(hs_context* ctx, hs_frame* f, int32_t* rendered_count);
+hs_status hs_host_alloc(size_t bytes, void** out); /* pinned host memory */
+void hs_host_free(void* p);
 /* Parity hooks (ForwardContext, render.hpp:87-98, expressed as sort keys):
  *  tile_start     tiles+1 offsets (== ForwardContext::tile_start)
  *  sorted_keys    D keys (tile << 32 | float_bits(z)), sorted

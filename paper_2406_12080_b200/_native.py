@@ -90,7 +90,11 @@ _SIGS = {
     "hs_frame_wait": (C.c_int, [_vp, _vp]),
     "hs_frame_get_info": (C.c_int, [_vp, _vp, C.POINTER(hs_frame_info)]),
     "hs_frame_download": (C.c_int, [_vp, _vp, f32p, f32p, f32p, i32p]),
-    "hs_frame_debug": (C.c_int, [_vp, _vp, u64p, u64p, u32p, u64p, u32p, f32p]),
+    "hs_frame_download_async": (C.c_int, [_vp, _vp, f32p, f32p, f32p]),
+    "hs_frame_download_wait": (C.c_int, [_vp, _vp, i32p]),
+    "hs_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
+    "hs_host_free": (None, [_vp]),
+    "hs_frame_debug":(C.c_int, [_vp, _vp, u64p, u64p, u32p, u64p, u32p, f32p]),
     "hs_synth_node_count": (C.c_uint64, [C.c_uint64]),
     "hs_synth_scene_side": (C.c_float, [C.c_uint64]),
     "hs_synth_city": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.POINTER(hs_node_soa)]),

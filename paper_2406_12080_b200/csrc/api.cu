@@ -79,6 +79,7 @@ struct DBuf {
 struct hs_context {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // frame read-back overlapping the next frame's kernels
     std::string err;
     bool async = false;
     int blend_mode = 0;
@@ -113,9 +114,12 @@ struct hs_frame {
     DBuf proj, dinfo, dupcount, offsets, keys[2], vals[2], dupk, dupv, ranges, color, depth, trans, touched, dbg16,
         splat_attr, stats, scratch;
     DevStats* h_stats = nullptr;  // pinned
+    DevStats* h_stats_dl = nullptr;  // pinned, snapshot taken with an async read-back
     uint64_t* h_n = nullptr;      // pinned
     cudaEvent_t ev[6] = {};
     cudaEvent_t done = nullptr;
+    cudaEvent_t copy_done = nullptr;  // last async read-back of this frame's images
+    bool copy_pending = false;
     bool pending = false, timed = false, have_result = false;
     hs_stage_times* times = nullptr;
     bool cut_timed = false;
@@ -130,10 +134,12 @@ struct hs_frame {
     CamParams cam{};
     ~hs_frame() {
         if (h_stats) cudaFreeHost(h_stats);
+        if (h_stats_dl) cudaFreeHost(h_stats_dl);
         if (h_n) cudaFreeHost(h_n);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (done) cudaEventDestroy(done);
+        if (copy_done) cudaEventDestroy(copy_done);
         delete own_cut;
     }
 };
@@ -291,6 +297,8 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     DevStats* ds = f->stats.as<DevStats>();
     const ScratchLayout L = scratch_layout(f->cap_splats, f->cap_dup, f->passes);
     unsigned char* sc = f->scratch.as<unsigned char>();
+    // the images of this frame object may still be streaming to the host
+    if (f->copy_pending) HS_CUDA(ctx, cudaStreamWaitEvent(s, f->copy_done, 0));
     HS_CUDA(ctx, cudaMemsetAsync(sc, 0, L.total, s));
     HS_CUDA(ctx, cudaMemsetAsync(&ds->n_visible, 0, offsetof(DevStats, overflows) - 8, s));
     if (f->from_cut) HS_CUDA(ctx, cudaMemcpyAsync(&ds->n_splats, f->n_ptr, 8, cudaMemcpyDeviceToDevice, s));
@@ -456,7 +464,8 @@ hs_status hs_context_create(int device, hs_context** out) {
     if (cudaSetDevice(device) != cudaSuccess) return HS_CUDA_ERROR;
     auto* ctx = new hs_context();
     ctx->device = device;
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete ctx;
         return HS_CUDA_ERROR;
     }
@@ -468,9 +477,11 @@ void hs_context_destroy(hs_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    cudaStream_t st = ctx->stream;
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
     delete ctx;
     cudaStreamDestroy(st);
+    cudaStreamDestroy(cs);
 }
 
 const char* hs_last_error(const hs_context* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
@@ -862,4 +873,46 @@ extern "C" hs_status hs_cut_render_splats(hs_context* ctx, const hs_hierarchy* h
     HS_TRY(copy_sync(ctx, out->t, t, n * 4, cudaMemcpyDeviceToHost));
     HS_TRY(copy_sync(ctx, out->siblings, k, n * 4, cudaMemcpyDeviceToHost));
     return HS_OK;
+}
+
+// Asynchronous read-back: images of `f` are copied to host memory (pinned for
+// real overlap) on the context's copy stream, after the frame's kernels, while
+// the compute stream moves on to the next frame.  A later render into the same
+// frame object waits for this copy on the device.
+extern "C" hs_status hs_frame_download_async(hs_context* ctx, hs_frame* f, float* color, float* depth,
+                                             float* trans) {
+    if (!ctx || !f) return HS_INVALID_ARGUMENT;
+    if (!f->pending && !f->have_result) return set_err(ctx, HS_MISSING_FORWARD_STATE, "frame has not been rendered");
+    if (!f->copy_done) HS_CUDA(ctx, cudaEventCreateWithFlags(&f->copy_done, cudaEventDisableTiming));
+    if (!f->h_stats_dl) HS_CUDA(ctx, cudaMallocHost(&f->h_stats_dl, sizeof(DevStats)));
+    cudaStream_t cs = ctx->copy_stream;
+    HS_CUDA(ctx, cudaStreamWaitEvent(cs, f->done, 0));
+    const size_t plane = (size_t)f->W * f->H;
+    if (color) HS_CUDA(ctx, cudaMemcpyAsync(color, f->color.p, plane * 12, cudaMemcpyDeviceToHost, cs));
+    if (depth) HS_CUDA(ctx, cudaMemcpyAsync(depth, f->depth.p, plane * 4, cudaMemcpyDeviceToHost, cs));
+    if (trans) HS_CUDA(ctx, cudaMemcpyAsync(trans, f->trans.p, plane * 4, cudaMemcpyDeviceToHost, cs));
+    HS_CUDA(ctx, cudaMemcpyAsync(f->h_stats_dl, f->stats.p, sizeof(DevStats), cudaMemcpyDeviceToHost, cs));
+    HS_CUDA(ctx, cudaEventRecord(f->copy_done, cs));
+    f->copy_pending = true;
+    return HS_OK;
+}
+
+extern "C" hs_status hs_frame_download_wait(hs_context* ctx, hs_frame* f, int32_t* rendered_count) {
+    if (!ctx || !f) return HS_INVALID_ARGUMENT;
+    if (!f->copy_pending) return set_err(ctx, HS_MISSING_FORWARD_STATE, "no read-back in flight");
+    HS_CUDA(ctx, cudaEventSynchronize(f->copy_done));
+    f->copy_pending = false;
+    const DevStats st = *f->h_stats_dl;
+    if (st.n_dup > 0 && st.sort_n == 0)
+        return set_err(ctx, HS_CAPACITY_EXCEEDED, "the frame overflowed the duplicate buffer; render it synchronously");
+    if (rendered_count) *rendered_count = (int32_t)st.rendered;
+    return HS_OK;
+}
+
+extern "C" hs_status hs_host_alloc(size_t bytes, void** out) {
+    if (!out) return HS_INVALID_ARGUMENT;
+    return cudaMallocHost(out, bytes) == cudaSuccess ? HS_OK : HS_OUT_OF_MEMORY;
+}
+extern "C" void hs_host_free(void* p) {
+    if (p) cudaFreeHost(p);
 }
