@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __rest
                                                             uint64_t* count_out) {
     __shared__ uint64_t s_exp_tab[32];
     __shared__ uint64_t s_log_tab[32];
-    __shared__ uint32_t s_cnt[kCutItems * 8];
+    __shared__ uint32_t s_cnt[kCutItems * 8], s_off[kCutItems * 8];
     __shared__ uint64_t s_base;
     __shared__ uint32_t s_tile;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -89,14 +89,10 @@ __global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __rest
             }
         }
     }
-    // phase 3: transition_alpha from the parent's falloff (lod.hpp:84-88)
+    // selection is final: publish this tile's count and let warp 0 run the look-back
+    // while every warp (warp 0 afterwards) does phase 3
 #pragma unroll
     for (int k = 0; k < kCutItems; ++k) {
-        if (kk[k]) {
-            const float pf = attr[(uint64_t)par[k] * kAttrVec4].w;
-            const float aa = smin(smax(smin(pf, kAlphaMax), 0.0f), kAlphaMax);
-            av[k] = 1.0f - hs_libm::powf_glibc(1.0f - aa, 1.0f / (float)(int)kk[k], s_log_tab, s_exp_tab);
-        }
         ballots[k] = __ballot_sync(0xffffffffu, (sel_mask >> k) & 1u);
         if (lane == 0) s_cnt[k * 8 + warp] = __popc(ballots[k]);
     }
@@ -112,8 +108,8 @@ __global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __rest
         }
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t excl = incl - (c0 + c1);
-        s_cnt[2 * lane] = excl;
-        s_cnt[2 * lane + 1] = excl + c0;
+        s_off[2 * lane] = excl;
+        s_off[2 * lane + 1] = excl + c0;
         uint64_t prefix = 0;
         if (tile == 0) {
             if (lane == 0) st_volatile_u64(status, kFlagInc64 | total);
@@ -127,13 +123,22 @@ __global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __rest
             if (tile == num_tiles - 1) *count_out = prefix + total;
         }
     }
+    // phase 3: transition_alpha from the parent's falloff (lod.hpp:84-88)
+#pragma unroll
+    for (int k = 0; k < kCutItems; ++k) {
+        if (kk[k]) {
+            const float pf = attr[(uint64_t)par[k] * kAttrVec4].w;
+            const float aa = smin(smax(smin(pf, kAlphaMax), 0.0f), kAlphaMax);
+            av[k] = 1.0f - hs_libm::powf_glibc(1.0f - aa, 1.0f / (float)(int)kk[k], s_log_tab, s_exp_tab);
+        }
+    }
     __syncthreads();
     const uint64_t blk = s_base;
     const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
     for (int k = 0; k < kCutItems; ++k) {
         if (sel_mask & (1u << k)) {
-            const uint64_t pos = blk + s_cnt[k * 8 + warp] + __popc(ballots[k] & lt_mask);
+            const uint64_t pos = blk + s_off[k * 8 + warp] + __popc(ballots[k] & lt_mask);
             out_node[pos] = (uint32_t)(base + (uint64_t)k * kCutThreads + tid);
             out_t[pos] = tv[k];
             out_alpha[pos] = av[k];

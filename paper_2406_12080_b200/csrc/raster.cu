@@ -50,6 +50,8 @@ __device__ __forceinline__ void load_splat(const float4* __restrict__ attr, cons
     float* q = s.q;
     float falloff, pfall = 0.0f, t = 1.0f, u = 1.0f, v = 0.0f;
     int K = 1;
+    // the SH half of the 256-byte record is consumed after projection: start it towards L2 now
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(g + 8));
     const float4 g0 = g[0], g1 = g[1], g2 = g[2];
     bool blend = false;
     {
@@ -59,6 +61,7 @@ __device__ __forceinline__ void load_splat(const float4* __restrict__ attr, cons
             blend = parent != kNoNode && !(te >= 1.0f);  // lod.hpp:128
             if (blend) {
                 p = attr + (uint64_t)parent * kAttrVec4;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 8));
                 t = te;
                 u = te;
                 v = 1.0f - te;
