@@ -50,6 +50,7 @@ struct DevStats {
     unsigned long long rendered;   // rendered_count
     unsigned long long n_eval;     // (pixel, entry) pairs evaluated by the blend
     unsigned long long n_contrib;  // pairs that contributed
+    uint64_t n_visible_sorted;     // V from the order-preserving compaction (key count of the depth sort)
     unsigned long long overflows;  // sticky: frames whose D exceeded capacity since the last wait
 };
 
@@ -111,7 +112,7 @@ struct hs_frame {
     hs_context* ctx = nullptr;
     uint64_t cap_splats = 0, cap_dup = 0;
     int W = 0, H = 0, tiles_x = 0, tiles_y = 0, passes = 0;
-    DBuf proj, dinfo, dupcount, offsets, keys[2], vals[2], dupk, dupv, ranges, color, depth, trans, touched, dbg16,
+    DBuf proj, dinfo, dupcount, offsets, zkeys[2], zvals[2], keys[2], vals[2], dupk, dupv, keys64, ranges, color, depth, trans, touched, dbg16,
         splat_attr, stats, scratch;
     DevStats* h_stats = nullptr;  // pinned
     DevStats* h_stats_dl = nullptr;  // pinned, snapshot taken with an async read-back
@@ -224,10 +225,11 @@ CamParams make_cam(const hs_camera* c) {
     return p;
 }
 
+// 8-bit passes of the tile-index sort (order.cu): 2 at 1080p (8160 tiles, 13 bits)
 int sort_passes_for(int tiles) {
     int tb = 0;
     while ((1ll << tb) < tiles) ++tb;
-    return (32 + tb + 7) / 8;
+    return std::max(1, (tb + 7) / 8);
 }
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
@@ -238,14 +240,21 @@ uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 //   [128]      sort histogram (8 x 256 u32)
 //   [8320]     scan status (u64 words)
 //   [...]      sort status (passes x sort_status_words u32)
+// Per-frame scratch.  [0, zero_bytes) is zeroed once per frame: the tile
+// counters of the two look-back scans and of the blend, and their status words.
+// The two radix sorts zero their own look-back words on the device (sized from
+// the device-side key counts).
 struct ScratchLayout {
-    size_t scan_counter = 0, sort_counters = 64, blend_counter = 120, sort_hist = 128, scan_status = 8320,
-           sort_status = 0, total = 0;
+    size_t vis_counter = 0, dup_counter = 4, blend_counter = 8, vis_status = 64, dup_status = 0, zero_bytes = 0,
+           depth_sort = 0, tile_sort = 0, total = 0;
 };
-ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int passes) {
+ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int tile_passes) {
     ScratchLayout L;
-    L.sort_status = round_up(L.scan_status + hs::scan_status_words(n_max) * 8, 256);
-    L.total = L.sort_status + (size_t)passes * hs::sort_status_words(cap_dup) * 4;
+    L.dup_status = round_up(L.vis_status + hs::scan_status_words(n_max) * 8, 256);
+    L.zero_bytes = round_up(L.dup_status + hs::scan_status_words(n_max) * 8, 256);
+    L.depth_sort = L.zero_bytes;
+    L.tile_sort = round_up(L.depth_sort + hs::sort_scratch_words(n_max, 4) * 4, 256);
+    L.total = L.tile_sort + hs::sort_scratch_words(cap_dup, tile_passes) * 4;
     return L;
 }
 
@@ -262,7 +271,9 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
     HS_CUDA(ctx, f->touched.ensure(cs));
     if (fresh_touched) HS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, f->touched.bytes, ctx->stream));
     for (int b = 0; b < 2; ++b) {
-        HS_CUDA(ctx, f->keys[b].ensure(f->cap_dup * 8));
+        HS_CUDA(ctx, f->zkeys[b].ensure(cs * 4));
+        HS_CUDA(ctx, f->zvals[b].ensure(cs * 4));
+        HS_CUDA(ctx, f->keys[b].ensure(f->cap_dup * 4));
         HS_CUDA(ctx, f->vals[b].ensure(f->cap_dup * 4));
     }
     if (ctx->debug) {
@@ -277,7 +288,7 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
     HS_CUDA(ctx, f->trans.ensure(plane * 4));
     HS_CUDA(ctx, f->stats.ensure(sizeof(DevStats)));
     f->passes = sort_passes_for(tiles);
-    HS_CUDA(ctx, f->scratch.ensure(scratch_layout(f->cap_splats, f->cap_dup, f->passes).total));
+    HS_CUDA(ctx, f->scratch.ensure(scratch_layout(cs, f->cap_dup, f->passes).total));
     if (!f->h_stats) HS_CUDA(ctx, cudaMallocHost(&f->h_stats, sizeof(DevStats)));
     if (!f->h_n) HS_CUDA(ctx, cudaMallocHost(&f->h_n, 8));
     for (auto& e : f->ev)
@@ -295,11 +306,11 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     cudaStream_t s = ctx->stream;
     const CamParams& cp = f->cam;
     DevStats* ds = f->stats.as<DevStats>();
-    const ScratchLayout L = scratch_layout(f->cap_splats, f->cap_dup, f->passes);
+    const ScratchLayout L = scratch_layout(std::max<uint64_t>(f->cap_splats, 1), f->cap_dup, f->passes);
     unsigned char* sc = f->scratch.as<unsigned char>();
     // the images of this frame object may still be streaming to the host
     if (f->copy_pending) HS_CUDA(ctx, cudaStreamWaitEvent(s, f->copy_done, 0));
-    HS_CUDA(ctx, cudaMemsetAsync(sc, 0, L.total, s));
+    HS_CUDA(ctx, cudaMemsetAsync(sc, 0, L.zero_bytes, s));
     HS_CUDA(ctx, cudaMemsetAsync(&ds->n_visible, 0, offsetof(DevStats, overflows) - 8, s));
     if (f->from_cut) HS_CUDA(ctx, cudaMemcpyAsync(&ds->n_splats, f->n_ptr, 8, cudaMemcpyDeviceToDevice, s));
     HS_CUDA(ctx, cudaMemsetAsync(f->ranges.p, 0, (size_t)cp.tiles_x * cp.tiles_y * 8, s));
@@ -308,20 +319,30 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
                           f->dinfo.as<uint4>(), f->dupcount.as<uint32_t>(),
                           ctx->debug ? f->dbg16.as<float>() : nullptr, &ds->n_visible, s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[2], s));
-    hs::launch_scan(f->dupcount.as<uint32_t>(), f->n_ptr, f->n_max, f->offsets.as<uint32_t>(),
-                    reinterpret_cast<uint64_t*>(sc + L.scan_status), reinterpret_cast<uint32_t*>(sc + L.scan_counter),
-                    &ds->n_dup, &ds->sort_n, f->cap_dup, &ds->overflows, s);
-    hs::launch_duplicate(f->dinfo.as<uint4>(), f->dupcount.as<uint32_t>(), f->offsets.as<uint32_t>(), f->n_ptr,
-                         f->n_max, &ds->sort_n, cp.tiles_x, f->keys[0].as<uint64_t>(), f->vals[0].as<uint32_t>(), s);
+    // depth order of the visible splats (stable: ties keep cut order, render.hpp:268-272)
+    uint32_t* zk[2] = {f->zkeys[0].as<uint32_t>(), f->zkeys[1].as<uint32_t>()};
+    uint32_t* zv[2] = {f->zvals[0].as<uint32_t>(), f->zvals[1].as<uint32_t>()};
+    hs::launch_compact_visible(f->dupcount.as<uint32_t>(), f->dinfo.as<uint4>(), f->n_ptr, f->n_max, zk[0], zv[0],
+                               reinterpret_cast<uint64_t*>(sc + L.vis_status),
+                               reinterpret_cast<uint32_t*>(sc + L.vis_counter), &ds->n_visible_sorted, s);
+    hs::launch_radix_sort(zk, zv, &ds->n_visible_sorted, f->n_max, 0, 4,
+                          reinterpret_cast<uint32_t*>(sc + L.depth_sort), s);
+    const uint32_t* ids = zv[0];  // 4 passes: result back in buffer 0
+    // (tile, splat) pairs in depth order, then a stable sort by tile (render.hpp:273-294)
+    hs::launch_dup_offsets(ids, f->dupcount.as<uint32_t>(), &ds->n_visible_sorted, f->n_max, f->offsets.as<uint32_t>(),
+                           reinterpret_cast<uint64_t*>(sc + L.dup_status),
+                           reinterpret_cast<uint32_t*>(sc + L.dup_counter), &ds->n_dup, &ds->sort_n, f->cap_dup,
+                           &ds->overflows, s);
+    uint32_t* kb[2] = {f->keys[0].as<uint32_t>(), f->keys[1].as<uint32_t>()};
+    uint32_t* vb[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
+    hs::launch_duplicate_sorted(ids, f->dinfo.as<uint4>(), f->offsets.as<uint32_t>(), &ds->n_visible_sorted, f->n_max,
+                                &ds->sort_n, cp.tiles_x, kb[0], vb[0], s);
     if (ctx->debug) {
-        HS_CUDA(ctx, cudaMemcpyAsync(f->dupk.p, f->keys[0].p, f->cap_dup * 8, cudaMemcpyDeviceToDevice, s));
+        hs::launch_make_keys(kb[0], vb[0], f->dinfo.as<uint4>(), &ds->sort_n, f->cap_dup, f->dupk.as<uint64_t>(), s);
         HS_CUDA(ctx, cudaMemcpyAsync(f->dupv.p, f->vals[0].p, f->cap_dup * 4, cudaMemcpyDeviceToDevice, s));
     }
-    uint64_t* kb[2] = {f->keys[0].as<uint64_t>(), f->keys[1].as<uint64_t>()};
-    uint32_t* vb[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
-    hs::launch_radix_sort(kb, vb, &ds->sort_n, f->cap_dup, f->passes, reinterpret_cast<uint32_t*>(sc + L.sort_hist),
-                          reinterpret_cast<uint32_t*>(sc + L.sort_status),
-                          reinterpret_cast<uint32_t*>(sc + L.sort_counters), s);
+    hs::launch_radix_sort(kb, vb, &ds->sort_n, f->cap_dup, 0, f->passes, reinterpret_cast<uint32_t*>(sc + L.tile_sort),
+                          s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[3], s));
     const int fin = f->passes & 1;
     hs::launch_ranges(kb[fin], &ds->sort_n, f->cap_dup, f->ranges.as<uint2>(), s);
@@ -817,7 +838,13 @@ hs_status hs_frame_debug(hs_context* ctx, hs_frame* f, uint64_t* tile_start, uin
         tile_start[0] = 0;
         for (int t = 0; t < tiles; ++t) tile_start[t + 1] = tile_start[t] + (r[t].y - r[t].x);
     }
-    if (D && sorted_keys) HS_TRY(copy_sync(ctx, sorted_keys, f->keys[fin].p, D * 8, cudaMemcpyDeviceToHost));
+    if (D && sorted_keys) {  // the reference-equivalent (tile << 32 | bits(z)) list
+        HS_CUDA(ctx, f->keys64.ensure(D * 8));
+        hs::launch_make_keys(f->keys[fin].as<uint32_t>(), f->vals[fin].as<uint32_t>(), f->dinfo.as<uint4>(),
+                             &f->stats.as<DevStats>()->sort_n, D, f->keys64.as<uint64_t>(), ctx->stream);
+        HS_CUDA(ctx, cudaGetLastError());
+        HS_TRY(copy_sync(ctx, sorted_keys, f->keys64.p, D * 8, cudaMemcpyDeviceToHost));
+    }
     if (D && sorted_vals) HS_TRY(copy_sync(ctx, sorted_vals, f->vals[fin].p, D * 4, cudaMemcpyDeviceToHost));
     if (dup_keys || dup_vals || proj16) {
         if (!ctx->debug) return set_err(ctx, HS_INVALID_ARGUMENT, "pre-sort keys and projections need HS_OPT_DEBUG");

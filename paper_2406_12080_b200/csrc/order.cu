@@ -1,0 +1,253 @@
+// order.cu — per-tile depth order of the visible splats (render.hpp:262-294).
+//
+// The reference stable-sorts the visible splats by camera-space z (ties keep
+// cut order) and then buckets them into tiles preserving that order.  The
+// device does the same in two stable radix sorts instead of one sort of
+// duplicated 64-bit (tile << 32 | bits(z)) keys:
+//   k_compact_visible   visible splats in index order -> (bits(z), id)
+//   sort 1              stable LSD radix sort of bits(z) (4 x 8-bit passes, V keys)
+//   k_dup_offsets       exclusive scan of tile counts in depth order -> D
+//   k_duplicate_sorted  (tile, id) pairs in depth order
+//   sort 2              stable LSD radix sort of the tile (2 x 8-bit passes, D keys)
+//   k_ranges            per-tile [start, end)
+// The resulting per-tile lists equal the reference's tile_entries bit for bit
+// and, with bits(z) re-attached (k_make_keys), the sorted (tile << 32 |
+// bits(z)) key list.  Traffic: 4 x 16 B x V + 2 x 16 B x D instead of
+// 6 x 24 B x D for the 64-bit key sort (~2.3x fewer bytes at C2).
+#include "hs_device.cuh"
+#include "hs_kernels.h"
+#include "hs_scan.cuh"
+
+namespace hs {
+
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+
+// Block-wide exclusive scan of 8 consecutive values per thread with a
+// decoupled look-back across tiles; returns the thread's exclusive prefix and
+// the global total (valid in the last tile only).
+struct ScanResult {
+    uint64_t excl;
+    uint64_t total;
+};
+
+__device__ __forceinline__ ScanResult tile_scan(uint32_t sum, uint32_t tile, uint64_t* status, uint32_t* s_warp,
+                                                uint64_t* s_base) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t wv = lane < 8 ? s_warp[lane] : 0u;
+        uint32_t wi = wv;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += x;
+        }
+        const uint64_t total = __shfl_sync(0xffffffffu, wi, 7);
+        if (lane < 8) s_warp[lane] = wi - wv;
+        uint64_t prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) st_volatile_u64(status, kFlagInc64 | total);
+        } else {
+            if (lane == 0) st_volatile_u64(status + tile, kFlagAgg64 | total);
+            prefix = lookback_u64(status, tile);
+            if (lane == 0) st_volatile_u64(status + tile, kFlagInc64 | (prefix + total));
+        }
+        if (lane == 0) {
+            s_base[0] = prefix;
+            s_base[1] = prefix + total;
+        }
+    }
+    __syncthreads();
+    ScanResult r;
+    r.excl = s_base[0] + s_warp[warp] + (incl - sum);
+    r.total = s_base[1];
+    return r;
+}
+
+// Visible splats (tile count > 0) in index order -> (bits(z), id); V.
+__global__ void __launch_bounds__(kScanThreads) k_compact_visible(const uint32_t* __restrict__ dupcount,
+                                                                  const uint4* __restrict__ dinfo,
+                                                                  const uint64_t* __restrict__ n_ptr,
+                                                                  uint32_t* __restrict__ out_keys,
+                                                                  uint32_t* __restrict__ out_vals, uint64_t* status,
+                                                                  uint32_t* tile_counter, uint64_t* v_out) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ uint64_t s_base[2];
+    __shared__ uint32_t s_tile;
+    const uint64_t n = *n_ptr;
+    const uint64_t num_tiles = (n + kScanTile - 1) / kScanTile;
+    if (n == 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *v_out = 0;
+        return;
+    }
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= num_tiles) break;
+        const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+        uint32_t flags = 0, sum = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (base + k < n && dupcount[base + k] != 0) flags |= 1u << k, ++sum;
+        const ScanResult r = tile_scan(sum, tile, status, s_warp, s_base);
+        uint64_t pos = r.excl;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (flags & (1u << k)) {
+                out_keys[pos] = dinfo[base + k].z;
+                out_vals[pos] = (uint32_t)(base + k);
+                ++pos;
+            }
+        if (tile == num_tiles - 1 && threadIdx.x == 0) *v_out = r.total;
+        __syncthreads();
+    }
+}
+
+// Exclusive scan of the tile counts of the depth-sorted splats -> duplicate
+// offsets; D, and D if it fits the key buffers (else 0 + overflow counter).
+__global__ void __launch_bounds__(kScanThreads) k_dup_offsets(const uint32_t* __restrict__ ids,
+                                                              const uint32_t* __restrict__ dupcount,
+                                                              const uint64_t* __restrict__ v_ptr,
+                                                              uint32_t* __restrict__ offsets, uint64_t* status,
+                                                              uint32_t* tile_counter, uint64_t* total_out,
+                                                              uint64_t* sort_n_out, uint64_t capacity,
+                                                              unsigned long long* overflows) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ uint64_t s_base[2];
+    __shared__ uint32_t s_tile;
+    const uint64_t n = *v_ptr;
+    const uint64_t num_tiles = (n + kScanTile - 1) / kScanTile;
+    if (n == 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *total_out = 0, *sort_n_out = 0;
+        return;
+    }
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= num_tiles) break;
+        const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+        uint32_t v[kScanItems];
+        uint32_t sum = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            v[k] = base + k < n ? dupcount[ids[base + k]] : 0u;
+            sum += v[k];
+        }
+        const ScanResult r = tile_scan(sum, tile, status, s_warp, s_base);
+        uint64_t run = r.excl;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            if (base + k < n) offsets[base + k] = (uint32_t)run;
+            run += v[k];
+        }
+        if (tile == num_tiles - 1 && threadIdx.x == 0) {
+            *total_out = r.total;
+            *sort_n_out = r.total <= capacity ? r.total : 0;
+            if (r.total > capacity) atomicAdd(overflows, 1ull);
+        }
+        __syncthreads();
+    }
+}
+
+// (tile, id) pairs of the depth-sorted splats, tiles of a splat row-major.
+__global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __restrict__ ids,
+                                                          const uint4* __restrict__ dinfo,
+                                                          const uint32_t* __restrict__ offsets,
+                                                          const uint64_t* __restrict__ v_ptr,
+                                                          const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
+                                                          uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const uint64_t n = *v_ptr;
+    if (*sort_n_ptr == 0) return;  // nothing to emit, or over capacity
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t id = ids[i];
+        const uint4 di = dinfo[id];
+        const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
+        uint64_t o = offsets[i];
+        for (int ty = ty0; ty < ty1; ++ty)
+            for (int tx = tx0; tx < tx1; ++tx) {
+                keys[o] = (uint32_t)(ty * tiles_x + tx);
+                vals[o] = id;
+                ++o;
+            }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, const uint64_t* __restrict__ n_ptr,
+                                                uint2* __restrict__ ranges) {
+    const uint64_t n = *n_ptr;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = keys[i];
+        if (i == 0 || keys[i - 1] != t) ranges[t].x = (uint32_t)i;
+        if (i == n - 1 || keys[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+    }
+}
+
+// Parity view: the reference-equivalent 64-bit keys (tile << 32 | bits(z)).
+__global__ void k_make_keys(const uint32_t* __restrict__ tiles, const uint32_t* __restrict__ ids,
+                            const uint4* __restrict__ dinfo, const uint64_t* __restrict__ n_ptr,
+                            uint64_t* __restrict__ out) {
+    const uint64_t n = *n_ptr;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = ((uint64_t)tiles[i] << 32) | dinfo[ids[i]].z;
+}
+
+// ------------------------------------------------------------------ launchers
+static int order_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (!sms) sms = 148;
+    }
+    return sms;
+}
+static unsigned scan_grid(uint64_t n_max) {
+    const uint64_t tiles = (n_max + kScanTile - 1) / kScanTile;
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)order_sms() * 4));
+}
+static unsigned flat_grid(uint64_t n_max) {
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)order_sms() * 8));
+}
+
+uint64_t scan_status_words(uint64_t n_max) { return (n_max + kScanTile - 1) / kScanTile + 1; }
+
+void launch_compact_visible(const uint32_t* dupcount, const uint4* dinfo, const uint64_t* n_ptr, uint64_t n_max,
+                            uint32_t* keys, uint32_t* vals, uint64_t* status, uint32_t* counter, uint64_t* v_out,
+                            cudaStream_t s) {
+    k_compact_visible<<<scan_grid(n_max), kScanThreads, 0, s>>>(dupcount, dinfo, n_ptr, keys, vals, status, counter,
+                                                                v_out);
+}
+
+void launch_dup_offsets(const uint32_t* ids, const uint32_t* dupcount, const uint64_t* v_ptr, uint64_t n_max,
+                        uint32_t* offsets, uint64_t* status, uint32_t* counter, uint64_t* total_out,
+                        uint64_t* sort_n_out, uint64_t capacity, unsigned long long* overflows, cudaStream_t s) {
+    k_dup_offsets<<<scan_grid(n_max), kScanThreads, 0, s>>>(ids, dupcount, v_ptr, offsets, status, counter, total_out,
+                                                            sort_n_out, capacity, overflows);
+}
+
+void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const uint32_t* offsets, const uint64_t* v_ptr,
+                             uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* keys, uint32_t* vals,
+                             cudaStream_t s) {
+    k_duplicate_sorted<<<flat_grid(n_max), 256, 0, s>>>(ids, dinfo, offsets, v_ptr, sort_n_ptr, tiles_x, keys, vals);
+}
+
+void launch_ranges(const uint32_t* keys, const uint64_t* n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s) {
+    k_ranges<<<flat_grid(n_max), 256, 0, s>>>(keys, n_ptr, ranges);
+}
+
+void launch_make_keys(const uint32_t* tiles, const uint32_t* ids, const uint4* dinfo, const uint64_t* n_ptr,
+                      uint64_t n_max, uint64_t* out, cudaStream_t s) {
+    k_make_keys<<<flat_grid(n_max), 256, 0, s>>>(tiles, ids, dinfo, n_ptr, out);
+}
+
+}  // namespace hs

@@ -2,10 +2,7 @@
 //   k_preprocess  fused parent/child interpolation (lod.hpp:116-146) + project
 //                 (render.hpp:104-174) + SH deg-3 colour (sh.hpp:20-78) +
 //                 per-splat tile count
-//   k_scan        exclusive scan of tile counts -> duplicate offsets, D
-//   k_duplicate   (tile << 32 | bits(z), splat) keys in splat, ty, tx order
-//   k_ranges      per-tile [start, end) over the sorted keys (render.hpp:279-284)
-//   k_blend       per-tile front-to-back alpha blend (render.hpp:296-336)
+//   (ordering: order.cu + sort.cu; blending: blend.cu)
 //   k_touched     rendered_count (render.hpp:300, :326-327, :337)
 #include "hs_device.cuh"
 #include "hs_kernels.h"
@@ -50,8 +47,6 @@ __device__ __forceinline__ void load_splat(const float4* __restrict__ attr, cons
     float* q = s.q;
     float falloff, pfall = 0.0f, t = 1.0f, u = 1.0f, v = 0.0f;
     int K = 1;
-    // the SH half of the 256-byte record is consumed after projection: start it towards L2 now
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(g + 8));
     const float4 g0 = g[0], g1 = g[1], g2 = g[2];
     bool blend = false;
     {
@@ -61,7 +56,6 @@ __device__ __forceinline__ void load_splat(const float4* __restrict__ attr, cons
             blend = parent != kNoNode && !(te >= 1.0f);  // lod.hpp:128
             if (blend) {
                 p = attr + (uint64_t)parent * kAttrVec4;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 8));
                 t = te;
                 u = te;
                 v = 1.0f - te;
@@ -362,122 +356,6 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ a
     if ((threadIdx.x & 31) == 0 && vis) atomicAdd(n_visible, (unsigned long long)vis);
 }
 
-// -------------------------------------------------------------------------
-// exclusive scan of per-splat tile counts (decoupled look-back), D
-// -------------------------------------------------------------------------
-constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
-
-__global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restrict__ counts,
-                                                       const uint64_t* __restrict__ n_ptr, uint32_t* __restrict__ offsets,
-                                                       uint64_t* status, uint32_t* tile_counter, uint64_t* total_out,
-                                                       uint64_t* sort_n_out, uint64_t capacity,
-                                                       unsigned long long* overflows) {
-    __shared__ uint32_t s_warp[8];
-    __shared__ uint64_t s_base;
-    __shared__ uint32_t s_tile;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t n = *n_ptr;
-    const uint64_t num_tiles = (n + kScanTile - 1) / kScanTile;
-    if (n == 0) {
-        if (blockIdx.x == 0 && tid == 0) *total_out = 0, *sort_n_out = 0;
-        return;
-    }
-    while (true) {
-        if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-        __syncthreads();
-        const uint32_t tile = s_tile;
-        if (tile >= num_tiles) break;
-        const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)tid * kScanItems;
-        uint32_t v[kScanItems];
-        uint32_t sum = 0;
-#pragma unroll
-        for (int k = 0; k < kScanItems; ++k) {
-            v[k] = base + k < n ? counts[base + k] : 0u;
-            sum += v[k];
-        }
-        uint32_t incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += x;
-        }
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t wv = lane < 8 ? s_warp[lane] : 0u;
-            uint32_t wi = wv;
-#pragma unroll
-            for (int o = 1; o < 8; o <<= 1) {
-                const uint32_t x = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += x;
-            }
-            const uint64_t total = __shfl_sync(0xffffffffu, wi, 7);
-            if (lane < 8) s_warp[lane] = wi - wv;
-            uint64_t prefix = 0;
-            if (tile == 0) {
-                if (lane == 0) st_volatile_u64(status, kFlagInc64 | total);
-            } else {
-                if (lane == 0) st_volatile_u64(status + tile, kFlagAgg64 | total);
-                prefix = lookback_u64(status, tile);
-                if (lane == 0) st_volatile_u64(status + tile, kFlagInc64 | (prefix + total));
-            }
-            if (lane == 0) {
-                s_base = prefix;
-                if (tile == num_tiles - 1) {
-                    *total_out = prefix + total;
-                    *sort_n_out = prefix + total <= capacity ? prefix + total : 0;
-                    if (prefix + total > capacity) atomicAdd(overflows, 1ull);
-                }
-            }
-        }
-        __syncthreads();
-        uint64_t run = s_base + s_warp[warp] + (incl - sum);
-#pragma unroll
-        for (int k = 0; k < kScanItems; ++k) {
-            if (base + k < n) offsets[base + k] = (uint32_t)run;
-            run += v[k];
-        }
-        __syncthreads();
-    }
-}
-
-// -------------------------------------------------------------------------
-// key duplication: keys in (splat id asc, ty asc, tx asc) order
-// -------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_duplicate(const uint4* __restrict__ dinfo, const uint32_t* __restrict__ dupcount,
-                                                   const uint32_t* __restrict__ offsets, const uint64_t* __restrict__ n_ptr,
-                                                   const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
-                                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-    const uint64_t n = *n_ptr;
-    if (*sort_n_ptr == 0) return;  // empty or over capacity
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
-        if (dupcount[j] == 0) continue;
-        const uint4 di = dinfo[j];
-        const uint32_t rx = di.x, ry = di.y, zb = di.z;
-        const int tx0 = rx & 0xffff, tx1 = rx >> 16, ty0 = ry & 0xffff, ty1 = ry >> 16;
-        uint64_t o = offsets[j];
-        for (int ty = ty0; ty < ty1; ++ty)
-            for (int tx = tx0; tx < tx1; ++tx) {
-                keys[o] = ((uint64_t)(ty * tiles_x + tx) << 32) | zb;
-                vals[o] = (uint32_t)j;
-                ++o;
-            }
-    }
-}
-
-// -------------------------------------------------------------------------
-// tile ranges over sorted keys
-// -------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ sort_n_ptr,
-                                                uint2* __restrict__ ranges) {
-    const uint64_t n = *sort_n_ptr;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t t = (uint32_t)(keys[i] >> 32);
-        if (i == 0 || (uint32_t)(keys[i - 1] >> 32) != t) ranges[t].x = (uint32_t)i;
-        if (i == n - 1 || (uint32_t)(keys[i + 1] >> 32) != t) ranges[t].y = (uint32_t)(i + 1);
-    }
-}
-
 __global__ void k_count_touched(uint8_t* __restrict__ touched, const uint64_t* __restrict__ n_ptr,
                                 unsigned long long* __restrict__ out) {
     const uint64_t n = *n_ptr;
@@ -521,28 +399,6 @@ void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_no
         k_preprocess<false><<<grid, 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, cam, proj, dinfo, dupcount, dbg16,
                                                  n_visible);
 }
-
-uint64_t scan_status_words(uint64_t n_max) { return (n_max + kScanTile - 1) / kScanTile + 1; }
-
-void launch_scan(const uint32_t* counts, const uint64_t* n_ptr, uint64_t n_max, uint32_t* offsets, uint64_t* status,
-                 uint32_t* tile_counter, uint64_t* total_out, uint64_t* sort_n_out, uint64_t capacity,
-                 unsigned long long* overflows, cudaStream_t s) {
-    const uint64_t tiles = (n_max + kScanTile - 1) / kScanTile;
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)num_sms() * 4));
-    k_scan<<<grid, kScanThreads, 0, s>>>(counts, n_ptr, offsets, status, tile_counter, total_out, sort_n_out, capacity,
-                                         overflows);
-}
-
-void launch_duplicate(const uint4* dinfo, const uint32_t* dupcount, const uint32_t* offsets, const uint64_t* n_ptr,
-                      uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint64_t* keys, uint32_t* vals,
-                      cudaStream_t s) {
-    k_duplicate<<<grid_for(n_max, 8), 256, 0, s>>>(dinfo, dupcount, offsets, n_ptr, sort_n_ptr, tiles_x, keys, vals);
-}
-
-void launch_ranges(const uint64_t* keys, const uint64_t* sort_n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s) {
-    k_ranges<<<grid_for(n_max, 8), 256, 0, s>>>(keys, sort_n_ptr, ranges);
-}
-
 
 void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr,
                      uint64_t n_max, float* mean, float* scale, float* rot, float* sh, float* fall, float* pfall,

@@ -1,14 +1,15 @@
-// sort.cu — stable LSD radix sort of (tile << 32 | bits(z)) keys with 32-bit
-// splat-id values, Onesweep style (Adinets & Merrill 2022):
+// sort.cu — stable LSD radix sort of 32-bit keys with 32-bit values,
+// Onesweep style (Adinets & Merrill 2022):
 //   k_sort_hist   one read of the keys -> 256-bin histograms of every pass
 //   k_sort_offs   exclusive scan of each pass histogram -> digit bases
-//   k_onesweep    per pass: 4096-key tiles; warp-level ranking with
-//                 __match_any_sync, per-digit decoupled look-back across
-//                 tiles, local reorder in shared memory, coalesced scatter.
+//   k_onesweep    per 8-bit pass: 4096-key tiles (256 threads x 16 keys);
+//                 warp-level ranking with __match_any_sync, per-digit
+//                 decoupled look-back across tiles, local reorder in shared
+//                 memory, coalesced scatter.
 // Stability: within a warp keys are ranked in (item, lane) order, warps in
-// index order, tiles in index order — equal keys keep their duplicate-list
-// order, i.e. ascending splat id, which reproduces the reference's
-// std::stable_sort by depth + per-tile bucketing (render.hpp:268-294).
+// index order, tiles in index order — equal keys keep their input order.
+// Used twice per frame (order.cu): depth bits of the visible splats, then the
+// tile index of the duplicated (tile, splat) pairs.
 #include <algorithm>
 
 #include "hs_device.cuh"
@@ -24,14 +25,14 @@ constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys
 constexpr int kRadix = 256;
 constexpr uint32_t kFlagAgg32 = 1u << 30, kFlagInc32 = 2u << 30, kValMask32 = (1u << 30) - 1;
 
-__global__ void __launch_bounds__(256) k_sort_hist(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ n_ptr,
-                                                   uint32_t* __restrict__ hist, int passes) {
-    __shared__ uint32_t s_hist[8 * kRadix];
+__global__ void __launch_bounds__(256) k_sort_hist(const uint32_t* __restrict__ keys, const uint64_t* __restrict__ n_ptr,
+                                                   uint32_t* __restrict__ hist, int begin_bit, int passes) {
+    __shared__ uint32_t s_hist[4 * kRadix];
     const uint64_t n = *n_ptr;
     for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = keys[i];
+        const uint32_t k = keys[i] >> begin_bit;
         for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p * kRadix + ((k >> (8 * p)) & 0xff)], 1u);
     }
     __syncthreads();
@@ -39,12 +40,13 @@ __global__ void __launch_bounds__(256) k_sort_hist(const uint64_t* __restrict__ 
         if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
 }
 
-__global__ void k_sort_offs(uint32_t* hist, int passes) {
+__global__ void k_sort_offs(uint32_t* hist) {
     // one block of 256 threads per pass; exclusive scan in place
     const int p = blockIdx.x;
     __shared__ uint32_t s[kRadix];
     const int tid = threadIdx.x;
-    s[tid] = hist[p * kRadix + tid];
+    const uint32_t mine = hist[p * kRadix + tid];
+    s[tid] = mine;
     __syncthreads();
     for (int o = 1; o < kRadix; o <<= 1) {
         const uint32_t v = tid >= o ? s[tid - o] : 0u;
@@ -52,21 +54,33 @@ __global__ void k_sort_offs(uint32_t* hist, int passes) {
         s[tid] += v;
         __syncthreads();
     }
-    hist[p * kRadix + tid] = s[tid] - hist[p * kRadix + tid];
+    hist[p * kRadix + tid] = s[tid] - mine;
+}
+
+// Zero the look-back words this sort will use (sized from the device-side n).
+__global__ void k_sort_zero(uint32_t* __restrict__ status, const uint64_t* __restrict__ n_ptr, uint64_t words_per_pass,
+                            int passes) {
+    const uint64_t tiles = (*n_ptr + kSortTile - 1) / kSortTile;
+    const uint64_t used = tiles * kRadix;
+    for (int p = 0; p < passes; ++p)
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < used;
+             i += (uint64_t)gridDim.x * blockDim.x)
+            status[p * words_per_pass + i] = 0;
 }
 
 struct SortSmem {
-    uint64_t keys[kSortTile];
+    uint32_t keys[kSortTile];
     uint32_t vals[kSortTile];
     uint32_t wcnt[kSortWarps][kRadix];
     uint32_t local_off[kRadix];
     uint32_t gbase[kRadix];
+    uint32_t wsum[kSortWarps];
     uint32_t tile;
 };
 
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint64_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const uint32_t* __restrict__ keys_in,
                                                            const uint32_t* __restrict__ vals_in,
-                                                           uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                                                           uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                            const uint64_t* __restrict__ n_ptr, int shift,
                                                            const uint32_t* __restrict__ digit_base, uint32_t* status,
                                                            uint32_t* tile_counter) {
@@ -86,34 +100,33 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint64_t* __res
         const uint32_t tcount = (n - tbase) < (uint64_t)kSortTile ? (uint32_t)(n - tbase) : (uint32_t)kSortTile;
         const uint64_t wbase = tbase + (uint64_t)warp * (32 * kSortItems);
 
-        uint64_t k[kSortItems];
-        uint32_t v[kSortItems];
-        uint32_t rank[kSortItems];
+        uint32_t k[kSortItems], v[kSortItems];
+        uint16_t rank[kSortItems];
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
             const uint64_t idx = wbase + it * 32 + lane;
             const bool valid = idx < n;
-            k[it] = valid ? keys_in[idx] : 0ull;
+            k[it] = valid ? keys_in[idx] : 0u;
             v[it] = valid ? vals_in[idx] : 0u;
         }
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
-            const uint64_t idx = wbase + it * 32 + lane;
-            const bool valid = idx < n;
-            const uint32_t d = valid ? (uint32_t)((k[it] >> shift) & 0xff) : 0x100u;
+            const bool valid = wbase + it * 32 + lane < n;
+            const uint32_t d = valid ? ((k[it] >> shift) & 0xff) : 0x100u;
             const uint32_t peers = __match_any_sync(0xffffffffu, d);
             uint32_t r = 0;
             if (valid) r = sm.wcnt[warp][d] + __popc(peers & lt_mask);
             __syncwarp();
             if (valid && lane == 31 - __clz(peers)) sm.wcnt[warp][d] += __popc(peers);
             __syncwarp();
-            rank[it] = r;
+            rank[it] = (uint16_t)r;
         }
         __syncthreads();
-        // per digit: warp-exclusive offsets and the tile's digit count
+        // per digit: warp-exclusive offsets and the tile's digit count; publish it
         uint32_t dcount = 0;
         {
             const int d = tid;  // kSortThreads == kRadix
+#pragma unroll
             for (int w = 0; w < kSortWarps; ++w) {
                 const uint32_t c = sm.wcnt[w][d];
                 sm.wcnt[w][d] = dcount;
@@ -129,11 +142,11 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint64_t* __res
                 const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += x;
             }
-            __shared__ uint32_t s_wsum[kSortWarps];
-            if (lane == 31) s_wsum[warp] = incl;
+            if (lane == 31) sm.wsum[warp] = incl;
             __syncthreads();
             uint32_t wpre = 0;
-            for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+#pragma unroll
+            for (int w = 0; w < kSortWarps; ++w) wpre += w < warp ? sm.wsum[w] : 0u;
             sm.local_off[tid] = wpre + incl - dcount;
         }
         // per digit look-back across tiles
@@ -159,9 +172,8 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint64_t* __res
         // local reorder
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
-            const uint64_t idx = wbase + it * 32 + lane;
-            if (idx < n) {
-                const uint32_t d = (uint32_t)((k[it] >> shift) & 0xff);
+            if (wbase + it * 32 + lane < n) {
+                const uint32_t d = (k[it] >> shift) & 0xff;
                 const uint32_t pos = sm.local_off[d] + sm.wcnt[warp][d] + rank[it];
                 sm.keys[pos] = k[it];
                 sm.vals[pos] = v[it];
@@ -169,8 +181,8 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint64_t* __res
         }
         __syncthreads();
         for (uint32_t i = tid; i < tcount; i += kSortThreads) {
-            const uint64_t key = sm.keys[i];
-            const uint32_t d = (uint32_t)((key >> shift) & 0xff);
+            const uint32_t key = sm.keys[i];
+            const uint32_t d = (key >> shift) & 0xff;
             const uint32_t g = sm.gbase[d] + (i - sm.local_off[d]);
             keys_out[g] = key;
             vals_out[g] = sm.vals[i];
@@ -191,30 +203,38 @@ static int sort_sms() {
 }
 
 uint64_t sort_status_words(uint64_t n_max) { return ((n_max + kSortTile - 1) / kSortTile + 1) * kRadix; }
+uint64_t sort_scratch_words(uint64_t n_max, int passes) {
+    return (uint64_t)passes * (kRadix + 1) + (uint64_t)passes * sort_status_words(n_max);
+}
 
-// Sorts keys[0]/vals[0] (ping-pong with keys[1]/vals[1]); result in buffer
-// (passes % 2).  `scratch_hist` holds 8*256 u32, `status` sort_status_words()
-// u32 per pass (zeroed by the caller), `counters` one u32 per pass (zeroed).
-void launch_radix_sort(uint64_t* keys[2], uint32_t* vals[2], const uint64_t* n_ptr, uint64_t n_max, int passes,
-                       uint32_t* scratch_hist, uint32_t* status, uint32_t* counters, cudaStream_t s) {
+// Sorts bits [begin_bit, begin_bit + 8 * passes) of keys[0]/vals[0] (ping-pong
+// with keys[1]/vals[1]); the result lands in buffer (passes % 2).  `scratch`
+// holds sort_scratch_words(n_max, passes) u32 and is zeroed here on the device.
+void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_ptr, uint64_t n_max, int begin_bit,
+                       int passes, uint32_t* scratch, cudaStream_t s) {
     const int sms = sort_sms();
+    uint32_t* hist = scratch;                        // passes * 256
+    uint32_t* counters = scratch + passes * kRadix;  // passes
+    uint32_t* status = counters + passes;            // passes * words
+    const uint64_t words = sort_status_words(n_max);
+    cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * passes * (kRadix + 1), s);
+    k_sort_zero<<<sms * 2, 256, 0, s>>>(status, n_ptr, words, passes);
     const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)sms * 4));
-    k_sort_hist<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, scratch_hist, passes);
-    k_sort_offs<<<passes, kRadix, 0, s>>>(scratch_hist, passes);
+    k_sort_hist<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, hist, begin_bit, passes);
+    k_sort_offs<<<passes, kRadix, 0, s>>>(hist);
     const size_t smem = sizeof(SortSmem);
     static bool attr_set = false;
+    static int per_sm = 1;
     if (!attr_set) {
         cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep, kSortThreads, smem);
         attr_set = true;
     }
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_onesweep, kSortThreads, smem);
     const uint64_t tiles = (n_max + kSortTile - 1) / kSortTile;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)sms * std::max(1, per_sm)));
-    const uint64_t words = sort_status_words(n_max);
     for (int p = 0; p < passes; ++p) {
         k_onesweep<<<grid, kSortThreads, smem, s>>>(keys[p & 1], vals[p & 1], keys[(p + 1) & 1], vals[(p + 1) & 1],
-                                                    n_ptr, 8 * p, scratch_hist + p * kRadix, status + p * words,
+                                                    n_ptr, begin_bit + 8 * p, hist + p * kRadix, status + p * words,
                                                     counters + p);
     }
 }
