@@ -22,35 +22,43 @@ namespace hs {
 
 constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
 
-// Block-wide exclusive scan of 8 consecutive values per thread with a
-// decoupled look-back across tiles; returns the thread's exclusive prefix and
-// the global total (valid in the last tile only).
-struct ScanResult {
-    uint64_t excl;
-    uint64_t total;
+// Striped tile scan: item k of thread `tid` is index base + k * 256 + tid, so
+// every global load is coalesced.  Index order is (k, warp, lane): warp-level
+// shuffle scans per k, then one 64-entry scan over (k, warp) totals in warp 0
+// together with the decoupled look-back.  Returns each item's exclusive prefix.
+struct StripedScan {
+    uint32_t tot[kScanItems * 8];
+    uint32_t off[kScanItems * 8];
+    uint64_t base[2];
 };
 
-__device__ __forceinline__ ScanResult tile_scan(uint32_t sum, uint32_t tile, uint64_t* status, uint32_t* s_warp,
-                                                uint64_t* s_base) {
+__device__ __forceinline__ uint64_t striped_scan(const uint32_t (&v)[kScanItems], uint32_t (&lane_excl)[kScanItems],
+                                                 uint32_t tile, uint64_t* status, StripedScan& sm) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t incl = sum;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += x;
+    for (int k = 0; k < kScanItems; ++k) {
+        uint32_t incl = v[k];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += x;
+        }
+        lane_excl[k] = incl - v[k];
+        if (lane == 31) sm.tot[k * 8 + warp] = incl;
     }
-    if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        const uint32_t wv = lane < 8 ? s_warp[lane] : 0u;
-        uint32_t wi = wv;
+        const uint32_t c0 = sm.tot[2 * lane], c1 = sm.tot[2 * lane + 1];
+        uint32_t incl = c0 + c1;
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += x;
         }
-        const uint64_t total = __shfl_sync(0xffffffffu, wi, 7);
-        if (lane < 8) s_warp[lane] = wi - wv;
+        const uint64_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - (c0 + c1);
+        sm.off[2 * lane] = excl;
+        sm.off[2 * lane + 1] = excl + c0;
         uint64_t prefix = 0;
         if (tile == 0) {
             if (lane == 0) st_volatile_u64(status, kFlagInc64 | total);
@@ -60,15 +68,12 @@ __device__ __forceinline__ ScanResult tile_scan(uint32_t sum, uint32_t tile, uin
             if (lane == 0) st_volatile_u64(status + tile, kFlagInc64 | (prefix + total));
         }
         if (lane == 0) {
-            s_base[0] = prefix;
-            s_base[1] = prefix + total;
+            sm.base[0] = prefix;
+            sm.base[1] = prefix + total;
         }
     }
     __syncthreads();
-    ScanResult r;
-    r.excl = s_base[0] + s_warp[warp] + (incl - sum);
-    r.total = s_base[1];
-    return r;
+    return sm.base[1];  // inclusive total up to this tile
 }
 
 // Visible splats (tile count > 0) in index order -> (bits(z), id); V.
@@ -78,8 +83,7 @@ __global__ void __launch_bounds__(kScanThreads) k_compact_visible(const uint32_t
                                                                   uint32_t* __restrict__ out_keys,
                                                                   uint32_t* __restrict__ out_vals, uint64_t* status,
                                                                   uint32_t* tile_counter, uint64_t* v_out) {
-    __shared__ uint32_t s_warp[8];
-    __shared__ uint64_t s_base[2];
+    __shared__ StripedScan sm;
     __shared__ uint32_t s_tile;
     const uint64_t n = *n_ptr;
     const uint64_t num_tiles = (n + kScanTile - 1) / kScanTile;
@@ -87,26 +91,30 @@ __global__ void __launch_bounds__(kScanThreads) k_compact_visible(const uint32_t
         if (blockIdx.x == 0 && threadIdx.x == 0) *v_out = 0;
         return;
     }
+    const int warp = threadIdx.x >> 5;
     while (true) {
         if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
         __syncthreads();
         const uint32_t tile = s_tile;
         if (tile >= num_tiles) break;
-        const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
-        uint32_t flags = 0, sum = 0;
+        const uint64_t base = (uint64_t)tile * kScanTile + threadIdx.x;
+        uint32_t v[kScanItems], ex[kScanItems];
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            const uint64_t i = base + (uint64_t)k * kScanThreads;
+            v[k] = (i < n && dupcount[i] != 0) ? 1u : 0u;
+        }
+        const uint64_t incl_total = striped_scan(v, ex, tile, status, sm);
+        const uint64_t blk = sm.base[0];
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k)
-            if (base + k < n && dupcount[base + k] != 0) flags |= 1u << k, ++sum;
-        const ScanResult r = tile_scan(sum, tile, status, s_warp, s_base);
-        uint64_t pos = r.excl;
-#pragma unroll
-        for (int k = 0; k < kScanItems; ++k)
-            if (flags & (1u << k)) {
-                out_keys[pos] = dinfo[base + k].z;
-                out_vals[pos] = (uint32_t)(base + k);
-                ++pos;
+            if (v[k]) {
+                const uint64_t i = base + (uint64_t)k * kScanThreads;
+                const uint64_t pos = blk + sm.off[k * 8 + warp] + ex[k];
+                out_keys[pos] = dinfo[i].z;
+                out_vals[pos] = (uint32_t)i;
             }
-        if (tile == num_tiles - 1 && threadIdx.x == 0) *v_out = r.total;
+        if (tile == num_tiles - 1 && threadIdx.x == 0) *v_out = incl_total;
         __syncthreads();
     }
 }
@@ -120,8 +128,7 @@ __global__ void __launch_bounds__(kScanThreads) k_dup_offsets(const uint32_t* __
                                                               uint32_t* tile_counter, uint64_t* total_out,
                                                               uint64_t* sort_n_out, uint64_t capacity,
                                                               unsigned long long* overflows) {
-    __shared__ uint32_t s_warp[8];
-    __shared__ uint64_t s_base[2];
+    __shared__ StripedScan sm;
     __shared__ uint32_t s_tile;
     const uint64_t n = *v_ptr;
     const uint64_t num_tiles = (n + kScanTile - 1) / kScanTile;
@@ -129,30 +136,30 @@ __global__ void __launch_bounds__(kScanThreads) k_dup_offsets(const uint32_t* __
         if (blockIdx.x == 0 && threadIdx.x == 0) *total_out = 0, *sort_n_out = 0;
         return;
     }
+    const int warp = threadIdx.x >> 5;
     while (true) {
         if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
         __syncthreads();
         const uint32_t tile = s_tile;
         if (tile >= num_tiles) break;
-        const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
-        uint32_t v[kScanItems];
-        uint32_t sum = 0;
+        const uint64_t base = (uint64_t)tile * kScanTile + threadIdx.x;
+        uint32_t v[kScanItems], ex[kScanItems];
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k) {
-            v[k] = base + k < n ? dupcount[ids[base + k]] : 0u;
-            sum += v[k];
+            const uint64_t i = base + (uint64_t)k * kScanThreads;
+            v[k] = i < n ? dupcount[ids[i]] : 0u;
         }
-        const ScanResult r = tile_scan(sum, tile, status, s_warp, s_base);
-        uint64_t run = r.excl;
+        const uint64_t incl_total = striped_scan(v, ex, tile, status, sm);
+        const uint64_t blk = sm.base[0];
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k) {
-            if (base + k < n) offsets[base + k] = (uint32_t)run;
-            run += v[k];
+            const uint64_t i = base + (uint64_t)k * kScanThreads;
+            if (i < n) offsets[i] = (uint32_t)(blk + sm.off[k * 8 + warp] + ex[k]);
         }
         if (tile == num_tiles - 1 && threadIdx.x == 0) {
-            *total_out = r.total;
-            *sort_n_out = r.total <= capacity ? r.total : 0;
-            if (r.total > capacity) atomicAdd(overflows, 1ull);
+            *total_out = incl_total;
+            *sort_n_out = incl_total <= capacity ? incl_total : 0;
+            if (incl_total > capacity) atomicAdd(overflows, 1ull);
         }
         __syncthreads();
     }

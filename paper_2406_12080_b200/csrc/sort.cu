@@ -151,18 +151,29 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const uint32_t* __
         }
         // per digit look-back across tiles
         {
+            // Windowed: 8 predecessors' words are loaded at once (independent loads in
+            // flight), then summed up to the nearest inclusive one.  All tiles of a pass
+            // run concurrently, so a one-word-at-a-time walk would serialise on latency.
             const int d = tid;
             uint32_t prefix = 0;
             if (tile > 0) {
                 int64_t t = (int64_t)tile - 1;
+                constexpr int kWin = 8;
                 while (true) {
-                    uint32_t s;
-                    do {
-                        s = ld_volatile_u32(status + (uint64_t)t * kRadix + d);
-                    } while ((s >> 30) == 0);
-                    prefix += s & kValMask32;
-                    if ((s >> 30) == 2) break;
-                    --t;
+                    uint32_t w[kWin];
+#pragma unroll
+                    for (int q = 0; q < kWin; ++q)
+                        w[q] = t - q >= 0 ? ld_volatile_u32(status + (uint64_t)(t - q) * kRadix + d) : kFlagInc32;
+                    bool found = false;
+#pragma unroll
+                    for (int q = 0; q < kWin; ++q) {
+                        if (found) break;
+                        while ((w[q] >> 30) == 0) w[q] = ld_volatile_u32(status + (uint64_t)(t - q) * kRadix + d);
+                        prefix += w[q] & kValMask32;
+                        found = (w[q] >> 30) == 2;
+                    }
+                    if (found) break;
+                    t -= kWin;
                 }
                 st_volatile_u32(status + (uint64_t)tile * kRadix + d, kFlagInc32 | (prefix + dcount));
             }
