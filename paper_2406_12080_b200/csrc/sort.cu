@@ -149,16 +149,27 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const uint32_t* __
             for (int w = 0; w < kSortWarps; ++w) wpre += w < warp ? sm.wsum[w] : 0u;
             sm.local_off[tid] = wpre + incl - dcount;
         }
-        // per digit look-back across tiles
+        __syncthreads();
+        // local reorder into shared memory first: frees the key/value registers for
+        // the look-back window below
+#pragma unroll
+        for (int it = 0; it < kSortItems; ++it) {
+            if (wbase + it * 32 + lane < n) {
+                const uint32_t d = (k[it] >> shift) & 0xff;
+                const uint32_t pos = sm.local_off[d] + sm.wcnt[warp][d] + rank[it];
+                sm.keys[pos] = k[it];
+                sm.vals[pos] = v[it];
+            }
+        }
+        // per digit look-back across tiles.  All tiles of a pass run concurrently, so a
+        // one-word-at-a-time walk would serialise on L2 latency; 16 predecessors' words
+        // are loaded at once and summed up to the nearest inclusive one.
         {
-            // Windowed: 8 predecessors' words are loaded at once (independent loads in
-            // flight), then summed up to the nearest inclusive one.  All tiles of a pass
-            // run concurrently, so a one-word-at-a-time walk would serialise on latency.
             const int d = tid;
             uint32_t prefix = 0;
             if (tile > 0) {
                 int64_t t = (int64_t)tile - 1;
-                constexpr int kWin = 8;
+                constexpr int kWin = 16;
                 while (true) {
                     uint32_t w[kWin];
 #pragma unroll
@@ -178,17 +189,6 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const uint32_t* __
                 st_volatile_u32(status + (uint64_t)tile * kRadix + d, kFlagInc32 | (prefix + dcount));
             }
             sm.gbase[d] = digit_base[d] + prefix;
-        }
-        __syncthreads();
-        // local reorder
-#pragma unroll
-        for (int it = 0; it < kSortItems; ++it) {
-            if (wbase + it * 32 + lane < n) {
-                const uint32_t d = (k[it] >> shift) & 0xff;
-                const uint32_t pos = sm.local_off[d] + sm.wcnt[warp][d] + rank[it];
-                sm.keys[pos] = k[it];
-                sm.vals[pos] = v[it];
-            }
         }
         __syncthreads();
         for (uint32_t i = tid; i < tcount; i += kSortThreads) {
