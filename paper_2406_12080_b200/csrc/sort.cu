@@ -109,17 +109,19 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const uint32_t* __
             k[it] = valid ? keys_in[idx] : 0u;
             v[it] = valid ? vals_in[idx] : 0u;
         }
+        // Warp ranking: the lowest lane of each digit group bumps the warp's digit
+        // counter with one shared atomic (program order keeps items in order) and
+        // broadcasts the old count; items are independent, so their latencies overlap.
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
             const bool valid = wbase + it * 32 + lane < n;
             const uint32_t d = valid ? ((k[it] >> shift) & 0xff) : 0x100u;
             const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            uint32_t r = 0;
-            if (valid) r = sm.wcnt[warp][d] + __popc(peers & lt_mask);
-            __syncwarp();
-            if (valid && lane == 31 - __clz(peers)) sm.wcnt[warp][d] += __popc(peers);
-            __syncwarp();
-            rank[it] = (uint16_t)r;
+            const int leader = __ffs(peers) - 1;
+            uint32_t old = 0;
+            if (valid && lane == leader) old = atomicAdd(&sm.wcnt[warp][d], (uint32_t)__popc(peers));
+            old = __shfl_sync(0xffffffffu, old, leader);
+            rank[it] = (uint16_t)(old + __popc(peers & lt_mask));
         }
         __syncthreads();
         // per digit: warp-exclusive offsets and the tile's digit count; publish it
