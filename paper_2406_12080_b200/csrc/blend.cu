@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
             // 2. per-pixel power and liveness (cheap, all lanes)
             uint32_t live = 0;
             if (!done) {
+                n_eval += __popc(bits);
                 for (uint32_t m = bits; m; m &= m - 1) {
                     const int k = __ffs(m) - 1;
                     const float4 p0 = rec[k][0];
@@ -201,13 +202,13 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
                 }
                 __syncwarp();
             }
-            // 4. composite in depth order
+            // 4. composite in depth order, over the entries live for at least one lane
+            //    (an entry no lane can see is a no-op for every pixel of the block)
             uint32_t tmask = 0;
-            for (uint32_t m = bits; m; m &= m - 1) {
+            for (uint32_t m = __reduce_or_sync(0xffffffffu, live); m; m &= m - 1) {
                 const int k = __ffs(m) - 1;
                 bool contrib = false;
                 if (!done) {
-                    ++n_eval;
                     if ((live >> k) & 1u) {
                         const float alpha = sv[k][lane];
                         if (alpha > 0.0f) {
