@@ -31,8 +31,8 @@ namespace hs {
 constexpr int kBlendThreads = 128;
 constexpr int kBlendWarps = kBlendThreads / 32;
 constexpr size_t kSmemRec = sizeof(float4) * kBlendWarps * 2 * 32 * 4;  // 2-stage record staging
-constexpr size_t kSmemV = sizeof(float) * kBlendWarps * 32 * 33;        // power / alpha per (entry, lane)
-constexpr size_t kSmemQ = sizeof(uint16_t) * kBlendWarps * 1024;        // live-pair queue
+constexpr size_t kSmemV = sizeof(float) * kBlendWarps * 16 * 33;        // power / alpha per (entry, lane)
+constexpr size_t kSmemQ = sizeof(uint16_t) * kBlendWarps * 512;         // live-pair queue
 
 // May the entry reach alpha >= 1/255 somewhere in the pixel-centre rectangle
 // [x0, x0+7] x [y0, y0+3] (relative to the splat mean)?  qthr (p3.y) already
@@ -62,7 +62,7 @@ __device__ __forceinline__ bool may_touch(const float4& p0, const float4& p1, co
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restrict__ ranges,
+__global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restrict__ ranges,
                                                             const uint32_t* __restrict__ vals,
                                                             const ProjRec* __restrict__ proj,
                                                             const uint64_t* __restrict__ sort_n_ptr, CamParams cam,
@@ -71,11 +71,11 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
                                                             unsigned long long* __restrict__ eval_counts,
                                                             uint32_t* __restrict__ task_counter) {
     // per warp: two stages of 32 staged 64-byte records (cp.async double buffer)
-    // (dynamic) s_rec[warps][2][32][4] float4 | s_v[warps][32][33] float | s_q[warps][1024] u16
+    // (dynamic) s_rec[warps][2][32][4] float4 | s_v[warps][16][33] float | s_q[warps][512] u16
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto s_rec = reinterpret_cast<float4(*)[2][32][4]>(smem_raw);
-    auto s_v = reinterpret_cast<float(*)[32][33]>(smem_raw + kSmemRec);
-    auto s_q = reinterpret_cast<uint16_t(*)[1024]>(smem_raw + kSmemRec + kSmemV);
+    auto s_v = reinterpret_cast<float(*)[16][33]>(smem_raw + kSmemRec);
+    auto s_q = reinterpret_cast<uint16_t(*)[512]>(smem_raw + kSmemRec + kSmemV);
     __shared__ uint64_t s_et[32], s_lt[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 32) {
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
     const bool any_keys = *sort_n_ptr != 0;
     uint32_t n_eval = 0, n_contrib = 0;
     float(*sv)[33] = s_v[warp];  // [entry][lane]: power, then alpha (row padding: conflict free both ways)
-    uint16_t* sq = s_q[warp];    // queue of live (lane << 5 | entry) pairs
+    uint16_t* sq = s_q[warp];    // queue of live (lane << 4 | entry) pairs
     // stage entry `e` (if in range) of the current task into stage `st`, lane slot
     auto issue = [&](int st, uint32_t e, uint32_t end, uint32_t id) {
         if (e < end) {
@@ -134,19 +134,26 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
                 hit = may_touch(rec[lane][0], rec[lane][1], rec[lane][3], ox - (double)rec[lane][0].x,
                                 oy - (double)rec[lane][0].y);
             const uint32_t bits = __ballot_sync(0xffffffffu, hit);
+            // Phases 2-4 run on the two halves of the batch in turn (16 entries each):
+            // halves the power/alpha scratch, which buys occupancy.
+            uint32_t tmask = 0;
+#pragma unroll 1
+            for (int h = 0; h < 32; h += 16) {
+            const uint32_t hbits = (bits >> h) & 0xffffu;
+            if (!hbits) continue;
             // 2. per-pixel power and liveness (cheap, all lanes)
             uint32_t live = 0;
             if (!done) {
-                n_eval += __popc(bits);
-                for (uint32_t m = bits; m; m &= m - 1) {
+                n_eval += __popc(hbits);
+                for (uint32_t m = hbits; m; m &= m - 1) {
                     const int k = __ffs(m) - 1;
-                    const float4 p0 = rec[k][0];
-                    const float4 p1 = rec[k][1];
+                    const float4 p0 = rec[h + k][0];
+                    const float4 p1 = rec[h + k][1];
                     const float dx = px - p0.x, dy = py - p0.y;
                     const float power = -0.5f * (p0.z * dx * dx + p1.x * dy * dy) - p0.w * dx * dy;
                     // live iff the alpha can reach the 1/255 floor: m e^power >= 1/255 needs
                     // power >= -ln(255 m) >= -qthr/2 (qthr carries the margin; *0.5 is exact)
-                    const bool lv = (power <= 0.0f) && (power >= -0.5f * rec[k][3].y);
+                    const bool lv = (power <= 0.0f) && (power >= -0.5f * rec[h + k][3].y);
                     if (lv) {
                         live |= 1u << k;
                         sv[k][lane] = power;
@@ -166,45 +173,44 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
                 }
                 const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
                 uint32_t pos = incl - cnt;
-                for (uint32_t m = live; m; m &= m - 1) sq[pos++] = (uint16_t)((lane << 5) | (__ffs(m) - 1));
+                for (uint32_t m = live; m; m &= m - 1) sq[pos++] = (uint16_t)((lane << 4) | (__ffs(m) - 1));
                 __syncwarp();
                 for (uint32_t pq = lane; pq < total; pq += 32) {
                     const uint32_t pr = sq[pq];
-                    const int src = (int)(pr >> 5), k = (int)(pr & 31);
+                    const int src = (int)(pr >> 4), k = (int)(pr & 15);
                     const float power = sv[k][src];
-                    const float4 p1 = rec[k][1];
-                float g;
-                if (kMode == 0)
-                    g = hs_libm::expf_glibc(power, s_et);
-                else
-                    g = __expf(power);
-                const float tt = p1.w;
-                const float self_raw = p1.y * g;
-                const float self = self_raw > kAlphaMax ? kAlphaMax : self_raw;
-                const float a_self = self >= kAlphaMin ? self : 0.0f;
-                float alpha;
-                if (tt < 1.0f) {
-                    const float par_raw = p1.z * g;
-                    const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
-                    float split = 0.0f;
-                    if (par >= kAlphaMin) {
-                        const float ik = rec[k][3].x;
-                        if (kMode == 0)
-                            split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, ik, s_lt, s_et);
-                        else
-                            split = 1.0f - exp2f(ik * __log2f(1.0f - par));
+                    const float4 p1 = rec[h + k][1];
+                    float g;
+                    if (kMode == 0)
+                        g = hs_libm::expf_glibc(power, s_et);
+                    else
+                        g = __expf(power);
+                    const float tt = p1.w;
+                    const float self_raw = p1.y * g;
+                    const float self = self_raw > kAlphaMax ? kAlphaMax : self_raw;
+                    const float a_self = self >= kAlphaMin ? self : 0.0f;
+                    float alpha;
+                    if (tt < 1.0f) {
+                        const float par_raw = p1.z * g;
+                        const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
+                        float split = 0.0f;
+                        if (par >= kAlphaMin) {
+                            const float ik = rec[h + k][3].x;
+                            if (kMode == 0)
+                                split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, ik, s_lt, s_et);
+                            else
+                                split = 1.0f - exp2f(ik * __log2f(1.0f - par));
+                        }
+                        alpha = tt * a_self + (1.0f - tt) * split;
+                    } else {
+                        alpha = a_self;
                     }
-                    alpha = tt * a_self + (1.0f - tt) * split;
-                } else {
-                    alpha = a_self;
-                }
-                sv[k][src] = alpha;
+                    sv[k][src] = alpha;
                 }
                 __syncwarp();
             }
             // 4. composite in depth order, over the entries live for at least one lane
             //    (an entry no lane can see is a no-op for every pixel of the block)
-            uint32_t tmask = 0;
             for (uint32_t m = __reduce_or_sync(0xffffffffu, live); m; m &= m - 1) {
                 const int k = __ffs(m) - 1;
                 bool contrib = false;
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
                             if (test < kTransmittanceEps) {
                                 done = true;
                             } else {
-                                const float4 p2 = rec[k][2];
+                                const float4 p2 = rec[h + k][2];
                                 const float wgt = alpha * T;
                                 c0 = c0 + p2.x * wgt;
                                 c1 = c1 + p2.y * wgt;
@@ -229,7 +235,9 @@ __global__ void __launch_bounds__(kBlendThreads, 5) k_blend(const uint2* __restr
                         }
                     }
                 }
-                if (__any_sync(0xffffffffu, contrib)) tmask |= 1u << k;
+                if (__any_sync(0xffffffffu, contrib)) tmask |= 1u << (h + k);
+            }
+            __syncwarp();
             }
             if ((tmask >> lane) & 1u) touched[id_b] = 1;  // rendered_count flags, one store per entry
             __syncwarp();
