@@ -112,6 +112,7 @@ struct hs_frame {
     hs_context* ctx = nullptr;
     uint64_t cap_splats = 0, cap_dup = 0;
     int W = 0, H = 0, tiles_x = 0, tiles_y = 0, passes = 0;
+    DBuf tile_order;
     DBuf proj, dinfo, dupcount, offsets, zkeys[2], zvals[2], keys[2], vals[2], dupk, dupv, keys64, ranges, color, depth, trans, touched, dbg16,
         splat_attr, stats, scratch;
     DevStats* h_stats = nullptr;  // pinned
@@ -282,6 +283,7 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
         HS_CUDA(ctx, f->dbg16.ensure(cs * 64));
     }
     HS_CUDA(ctx, f->ranges.ensure((size_t)tiles * 8));
+    HS_CUDA(ctx, f->tile_order.ensure((size_t)tiles * 4));
     const size_t plane = (size_t)cp.width * cp.height;
     HS_CUDA(ctx, f->color.ensure(plane * 12));
     HS_CUDA(ctx, f->depth.ensure(plane * 4));
@@ -347,9 +349,10 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     const int fin = f->passes & 1;
     hs::launch_ranges(kb[fin], &ds->sort_n, f->cap_dup, f->ranges.as<uint2>(), s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[4], s));
+    hs::launch_tile_order(f->ranges.as<uint2>(), cp.tiles_x * cp.tiles_y, &ds->sort_n, f->tile_order.as<uint32_t>(), s);
     hs::launch_blend(ctx->blend_mode, f->ranges.as<uint2>(), vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
                      f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(),
-                     &ds->n_eval, reinterpret_cast<uint32_t*>(sc + L.blend_counter), s);
+                     &ds->n_eval, reinterpret_cast<uint32_t*>(sc + L.blend_counter), f->tile_order.as<uint32_t>(), s);
     hs::launch_count_touched(f->touched.as<uint8_t>(), f->n_ptr, f->n_max, &ds->rendered, s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[5], s));
     HS_CUDA(ctx, cudaGetLastError());

@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                                                             float* __restrict__ color, float* __restrict__ depth,
                                                             float* __restrict__ trans, uint8_t* __restrict__ touched,
                                                             unsigned long long* __restrict__ eval_counts,
-                                                            uint32_t* __restrict__ task_counter) {
+                                                            uint32_t* __restrict__ task_counter,
+                                                            const uint32_t* __restrict__ tile_order) {
     // per warp: two stages of 32 staged 64-byte records (cp.async double buffer)
     // (dynamic) s_rec[warps][2][32][4] float4 | s_v[warps][16][33] float | s_q[warps][512] u16
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
         if (lane == 0) task = atomicAdd(task_counter, 1u);
         task = __shfl_sync(0xffffffffu, task, 0);
         if (task >= num_tasks) break;
-        const int tile = (int)(task >> 3), blk = (int)(task & 7);
+        const int tile = (int)tile_order[task >> 3], blk = (int)(task & 7);
         const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
         const int bx = tx * kTile + (blk & 1) * 8, by = ty * kTile + (blk >> 1) * 4;
         const int x = bx + (lane & 7), y = by + (lane >> 3);
@@ -266,7 +267,8 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
 
 void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
-                  unsigned long long* eval_counts, uint32_t* task_counter, cudaStream_t s) {
+                  unsigned long long* eval_counts, uint32_t* task_counter, const uint32_t* tile_order,
+                  cudaStream_t s) {
     constexpr size_t kSmem = kSmemRec + kSmemV + kSmemQ;
     static int grid[2] = {0, 0};
     if (!grid[mode]) {
@@ -286,10 +288,10 @@ void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const Pro
     const unsigned g = (unsigned)std::min<int>(grid[mode], std::max(1, tasks / kBlendWarps));
     if (mode == 0)
         k_blend<0><<<g, kBlendThreads, kSmem, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
-                                                   eval_counts, task_counter);
+                                                   eval_counts, task_counter, tile_order);
     else
         k_blend<1><<<g, kBlendThreads, kSmem, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
-                                                   eval_counts, task_counter);
+                                                   eval_counts, task_counter, tile_order);
 }
 
 }  // namespace hs

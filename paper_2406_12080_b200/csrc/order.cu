@@ -258,3 +258,37 @@ void launch_make_keys(const uint32_t* tiles, const uint32_t* ids, const uint4* d
 }
 
 }  // namespace hs
+
+namespace hs {
+
+// Blend work order: tiles by descending entry count (log2 buckets), so the
+// longest (tile, block) tasks start first and short ones fill the tail.  The
+// image does not depend on task order (every task owns its pixels).
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ ranges, int tiles,
+                                                     const uint64_t* __restrict__ sort_n_ptr,
+                                                     uint32_t* __restrict__ order) {
+    __shared__ uint32_t hist[33], offs[33];
+    const bool any = *sort_n_ptr != 0;
+    if (threadIdx.x < 33) hist[threadIdx.x] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+        const uint32_t c = any ? ranges[t].y - ranges[t].x : 0u;
+        atomicAdd(&hist[__clz(c + 1u)], 1u);  // fewer leading zeros = heavier = earlier
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int b = 0; b < 33; ++b) offs[b] = run, run += hist[b];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+        const uint32_t c = any ? ranges[t].y - ranges[t].x : 0u;
+        order[atomicAdd(&offs[__clz(c + 1u)], 1u)] = (uint32_t)t;
+    }
+}
+
+void launch_tile_order(const uint2* ranges, int tiles, const uint64_t* sort_n_ptr, uint32_t* order, cudaStream_t s) {
+    k_tile_order<<<1, 1024, 0, s>>>(ranges, tiles, sort_n_ptr, order);
+}
+
+}  // namespace hs
