@@ -337,20 +337,20 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
                            &ds->overflows, s);
     uint32_t* kb[2] = {f->keys[0].as<uint32_t>(), f->keys[1].as<uint32_t>()};
     uint32_t* vb[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
-    hs::launch_duplicate_sorted(ids, f->dinfo.as<uint4>(), f->offsets.as<uint32_t>(), &ds->n_visible_sorted, f->n_max,
+    hs::launch_duplicate_sorted(ids, f->dinfo.as<uint4>(), f->proj.as<ProjRec>(), f->offsets.as<uint32_t>(), &ds->n_visible_sorted, f->n_max,
                                 &ds->sort_n, cp.tiles_x, kb[0], vb[0], s);
     if (ctx->debug) {
         hs::launch_make_keys(kb[0], vb[0], f->dinfo.as<uint4>(), &ds->sort_n, f->cap_dup, f->dupk.as<uint64_t>(), s);
         HS_CUDA(ctx, cudaMemcpyAsync(f->dupv.p, f->vals[0].p, f->cap_dup * 4, cudaMemcpyDeviceToDevice, s));
     }
-    hs::launch_radix_sort(kb, vb, &ds->sort_n, f->cap_dup, 0, f->passes, reinterpret_cast<uint32_t*>(sc + L.tile_sort),
+    hs::launch_radix_sort(kb, vb, &ds->sort_n, f->cap_dup, 8, f->passes, reinterpret_cast<uint32_t*>(sc + L.tile_sort),
                           s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[3], s));
     const int fin = f->passes & 1;
     hs::launch_ranges(kb[fin], &ds->sort_n, f->cap_dup, f->ranges.as<uint2>(), s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[4], s));
     hs::launch_tile_order(f->ranges.as<uint2>(), cp.tiles_x * cp.tiles_y, &ds->sort_n, f->tile_order.as<uint32_t>(), s);
-    hs::launch_blend(ctx->blend_mode, f->ranges.as<uint2>(), vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
+    hs::launch_blend(ctx->blend_mode, f->ranges.as<uint2>(), kb[fin], vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
                      f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(),
                      &ds->n_eval, reinterpret_cast<uint32_t*>(sc + L.blend_counter), f->tile_order.as<uint32_t>(), s);
     hs::launch_count_touched(f->touched.as<uint8_t>(), f->n_ptr, f->n_max, &ds->rendered, s);

@@ -34,35 +34,9 @@ constexpr size_t kSmemRec = sizeof(float4) * kBlendWarps * 2 * 32 * 4;  // 2-sta
 constexpr size_t kSmemV = sizeof(float) * kBlendWarps * 16 * 33;        // power / alpha per (entry, lane)
 constexpr size_t kSmemQ = sizeof(uint16_t) * kBlendWarps * 512;         // live-pair queue
 
-// May the entry reach alpha >= 1/255 somewhere in the pixel-centre rectangle
-// [x0, x0+7] x [y0, y0+3] (relative to the splat mean)?  qthr (p3.y) already
-// carries the rounding margin; ia/ic are 1/a, 1/c (only pick the point where Q
-// is evaluated exactly, so their rounding cannot make the test unsafe beyond
-// a ~1e-14 relative change that the margin covers).
-__device__ __forceinline__ bool may_touch(const float4& p0, const float4& p1, const float4& p3, double x0,
-                                          double y0) {
-    const float qthr = p3.y;
-    if (qthr < 0.0f) return false;
-    const double x1 = x0 + 7.0, y1 = y0 + 3.0;
-    if (x0 <= 0.0 && 0.0 <= x1 && y0 <= 0.0 && 0.0 <= y1) return true;
-    const double a = p0.z, b = p0.w, c = p1.x, ia = p3.z, ic = p3.w;
-    double qm = 1e300;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const double x = e ? x1 : x0;
-        double y = -b * x * ic;
-        y = y < y0 ? y0 : (y > y1 ? y1 : y);
-        qm = fmin(qm, (a * x + 2.0 * b * y) * x + c * y * y);
-        const double yy = e ? y1 : y0;
-        double xx = -b * yy * ia;
-        xx = xx < x0 ? x0 : (xx > x1 ? x1 : xx);
-        qm = fmin(qm, (a * xx + 2.0 * b * yy) * xx + c * yy * yy);
-    }
-    return !(qm > (double)qthr);
-}
-
 template <int kMode>
 __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restrict__ ranges,
+                                                            const uint32_t* __restrict__ keys,
                                                             const uint32_t* __restrict__ vals,
                                                             const ProjRec* __restrict__ proj,
                                                             const uint64_t* __restrict__ sort_n_ptr, CamParams cam,
@@ -90,8 +64,8 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
     float(*sv)[33] = s_v[warp];  // [entry][lane]: power, then alpha (row padding: conflict free both ways)
     uint16_t* sq = s_q[warp];    // queue of live (lane << 4 | entry) pairs
     // stage entry `e` (if in range) of the current task into stage `st`, lane slot
-    auto issue = [&](int st, uint32_t e, uint32_t end, uint32_t id) {
-        if (e < end) {
+    auto issue = [&](int st, bool hit, uint32_t id) {
+        if (hit) {
             const float4* src = reinterpret_cast<const float4*>(proj + id);
 #pragma unroll
             for (int q = 0; q < 4; ++q) __pipeline_memcpy_async(&s_rec[warp][st][lane][q], src + q, 16);
@@ -114,27 +88,37 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
         if (any_keys) range = ranges[tile];
         float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, d = 0.0f;
         bool done = !inside;
-        // prologue: ids of batches 0 and 1, records of batch 0 in flight
-        uint32_t id_cur = range.x + lane < range.y ? vals[range.x + lane] : 0u;
-        uint32_t id_nxt = range.x + 32 + lane < range.y ? vals[range.x + 32 + lane] : 0u;
-        issue(0, range.x + lane, range.y, id_cur);
+        // The sorted keys carry, in their low 8 bits, which of the tile's 8 blocks each
+        // entry can reach (k_duplicate_sorted, block_may_touch): entries outside this
+        // block are never staged.  Ids/keys run two batches ahead, records one.
+        const uint32_t bmask = 1u << blk;
+        auto fetch = [&](uint32_t e, uint32_t& id, bool& hit) {
+            hit = false;
+            id = 0;
+            if (e < range.y) {
+                hit = (keys[e] & bmask) != 0;
+                id = vals[e];
+            }
+        };
+        uint32_t id_cur, id_nxt;
+        bool hit_cur, hit_nxt;
+        fetch(range.x + lane, id_cur, hit_cur);
+        fetch(range.x + 32 + lane, id_nxt, hit_nxt);
+        issue(0, hit_cur, id_cur);
         int b = 0;
         for (uint32_t base = range.x; base < range.y; base += 32, ++b) {
             // records of the next batch in flight while this one is processed
-            issue((b + 1) & 1, base + 32 + lane, range.y, id_nxt);
+            issue((b + 1) & 1, hit_nxt, id_nxt);
             const uint32_t id_b = id_cur;
+            const uint32_t bits = __ballot_sync(0xffffffffu, hit_cur);
             id_cur = id_nxt;
-            id_nxt = base + 64 + lane < range.y ? vals[base + 64 + lane] : 0u;
+            hit_cur = hit_nxt;
+            fetch(base + 64 + lane, id_nxt, hit_nxt);
             __pipeline_wait_prior(1);
             __syncwarp();
             if (__all_sync(0xffffffffu, done)) break;
+            if (!bits) continue;
             const float4(*rec)[4] = s_rec[warp][b & 1];
-            // 1. which staged entries may touch this block
-            bool hit = false;
-            if (base + lane < range.y)
-                hit = may_touch(rec[lane][0], rec[lane][1], rec[lane][3], ox - (double)rec[lane][0].x,
-                                oy - (double)rec[lane][0].y);
-            const uint32_t bits = __ballot_sync(0xffffffffu, hit);
             // Phases 2-4 run on the two halves of the batch in turn (16 entries each):
             // halves the power/alpha scratch, which buys occupancy.
             uint32_t tmask = 0;
@@ -265,7 +249,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
     }
 }
 
-void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
+void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
                   unsigned long long* eval_counts, uint32_t* task_counter, const uint32_t* tile_order,
                   cudaStream_t s) {
@@ -287,10 +271,10 @@ void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const Pro
     const int tasks = cam.tiles_x * cam.tiles_y * 8;
     const unsigned g = (unsigned)std::min<int>(grid[mode], std::max(1, tasks / kBlendWarps));
     if (mode == 0)
-        k_blend<0><<<g, kBlendThreads, kSmem, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
+        k_blend<0><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
                                                    eval_counts, task_counter, tile_order);
     else
-        k_blend<1><<<g, kBlendThreads, kSmem, s>>>(ranges, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
+        k_blend<1><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
                                                    eval_counts, task_counter, tile_order);
 }
 

@@ -93,4 +93,31 @@ __device__ __forceinline__ float interp_weight(float en, float ep, float tau) {
     return smin(1.0f, smax(0.0f, v));
 }
 
+// May the entry reach alpha >= 1/255 somewhere in the pixel-centre rectangle
+// [x0, x0+7] x [y0, y0+3] (relative to the splat mean)?  qthr (p3.y) already
+// carries the rounding margin; ia/ic are 1/a, 1/c (only pick the point where Q
+// is evaluated exactly, so their rounding cannot make the test unsafe beyond
+// a ~1e-14 relative change that the margin covers).
+__device__ __forceinline__ bool block_may_touch(const float4& p0, const float4& p1, const float4& p3, double x0,
+                                          double y0) {
+    const float qthr = p3.y;
+    if (qthr < 0.0f) return false;
+    const double x1 = x0 + 7.0, y1 = y0 + 3.0;
+    if (x0 <= 0.0 && 0.0 <= x1 && y0 <= 0.0 && 0.0 <= y1) return true;
+    const double a = p0.z, b = p0.w, c = p1.x, ia = p3.z, ic = p3.w;
+    double qm = 1e300;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const double x = e ? x1 : x0;
+        double y = -b * x * ic;
+        y = y < y0 ? y0 : (y > y1 ? y1 : y);
+        qm = fmin(qm, (a * x + 2.0 * b * y) * x + c * y * y);
+        const double yy = e ? y1 : y0;
+        double xx = -b * yy * ia;
+        xx = xx < x0 ? x0 : (xx > x1 ? x1 : xx);
+        qm = fmin(qm, (a * xx + 2.0 * b * yy) * xx + c * yy * yy);
+    }
+    return !(qm > (double)qthr);
+}
+
 }  // namespace hs

@@ -19,7 +19,7 @@ uint64_t select_cut_status_words(uint64_t n);
 void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,
                        const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint4* dinfo,
                        uint32_t* dupcount, float* dbg16, unsigned long long* n_visible, cudaStream_t s);
-void launch_blend(int mode, const uint2* ranges, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
+void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
                   unsigned long long* eval_counts, uint32_t* task_counter, const uint32_t* tile_order,
                   cudaStream_t s);
@@ -38,7 +38,7 @@ void launch_compact_visible(const uint32_t* dupcount, const uint4* dinfo, const 
 void launch_dup_offsets(const uint32_t* ids, const uint32_t* dupcount, const uint64_t* v_ptr, uint64_t n_max,
                         uint32_t* offsets, uint64_t* status, uint32_t* counter, uint64_t* total_out,
                         uint64_t* sort_n_out, uint64_t capacity, unsigned long long* overflows, cudaStream_t s);
-void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const uint32_t* offsets, const uint64_t* v_ptr,
+void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const ProjRec* proj, const uint32_t* offsets, const uint64_t* v_ptr,
                              uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* keys, uint32_t* vals,
                              cudaStream_t s);
 void launch_ranges(const uint32_t* keys, const uint64_t* n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s);

@@ -166,8 +166,13 @@ __global__ void __launch_bounds__(kScanThreads) k_dup_offsets(const uint32_t* __
 }
 
 // (tile, id) pairs of the depth-sorted splats, tiles of a splat row-major.
+// Key = tile << 8 | block mask: bit b set when the splat's alpha can pass the
+// 1/255 floor somewhere in 8x4 block b of the tile (block_may_touch).  The
+// tile sort orders by bits [8, 32) and carries the mask along; the blend then
+// never stages entries that cannot touch its block.
 __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __restrict__ ids,
                                                           const uint4* __restrict__ dinfo,
+                                                          const ProjRec* __restrict__ proj,
                                                           const uint32_t* __restrict__ offsets,
                                                           const uint64_t* __restrict__ v_ptr,
                                                           const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
@@ -177,11 +182,19 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __rest
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t id = ids[i];
         const uint4 di = dinfo[id];
+        const float4 p0 = proj[id].p0, p1 = proj[id].p1, p3 = proj[id].p3;
         const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
         uint64_t o = offsets[i];
         for (int ty = ty0; ty < ty1; ++ty)
             for (int tx = tx0; tx < tx1; ++tx) {
-                keys[o] = (uint32_t)(ty * tiles_x + tx);
+                uint32_t mask = 0;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const double bx = (double)(tx * kTile + (b & 1) * 8) + 0.5 - (double)p0.x;
+                    const double by = (double)(ty * kTile + (b >> 1) * 4) + 0.5 - (double)p0.y;
+                    if (block_may_touch(p0, p1, p3, bx, by)) mask |= 1u << b;
+                }
+                keys[o] = ((uint32_t)(ty * tiles_x + tx) << 8) | mask;
                 vals[o] = id;
                 ++o;
             }
@@ -192,9 +205,9 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
                                                 uint2* __restrict__ ranges) {
     const uint64_t n = *n_ptr;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t t = keys[i];
-        if (i == 0 || keys[i - 1] != t) ranges[t].x = (uint32_t)i;
-        if (i == n - 1 || keys[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+        const uint32_t t = keys[i] >> 8;
+        if (i == 0 || (keys[i - 1] >> 8) != t) ranges[t].x = (uint32_t)i;
+        if (i == n - 1 || (keys[i + 1] >> 8) != t) ranges[t].y = (uint32_t)(i + 1);
     }
 }
 
@@ -204,7 +217,7 @@ __global__ void k_make_keys(const uint32_t* __restrict__ tiles, const uint32_t* 
                             uint64_t* __restrict__ out) {
     const uint64_t n = *n_ptr;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        out[i] = ((uint64_t)tiles[i] << 32) | dinfo[ids[i]].z;
+        out[i] = ((uint64_t)(tiles[i] >> 8) << 32) | dinfo[ids[i]].z;
 }
 
 // ------------------------------------------------------------------ launchers
@@ -242,10 +255,11 @@ void launch_dup_offsets(const uint32_t* ids, const uint32_t* dupcount, const uin
                                                             sort_n_out, capacity, overflows);
 }
 
-void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const uint32_t* offsets, const uint64_t* v_ptr,
+void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const ProjRec* proj, const uint32_t* offsets,
+                             const uint64_t* v_ptr,
                              uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* keys, uint32_t* vals,
                              cudaStream_t s) {
-    k_duplicate_sorted<<<flat_grid(n_max), 256, 0, s>>>(ids, dinfo, offsets, v_ptr, sort_n_ptr, tiles_x, keys, vals);
+    k_duplicate_sorted<<<flat_grid(n_max), 256, 0, s>>>(ids, dinfo, proj, offsets, v_ptr, sort_n_ptr, tiles_x, keys, vals);
 }
 
 void launch_ranges(const uint32_t* keys, const uint64_t* n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s) {
