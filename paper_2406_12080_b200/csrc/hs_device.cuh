@@ -93,31 +93,34 @@ __device__ __forceinline__ float interp_weight(float en, float ep, float tau) {
     return smin(1.0f, smax(0.0f, v));
 }
 
-// May the entry reach alpha >= 1/255 somewhere in the pixel-centre rectangle
-// [x0, x0+7] x [y0, y0+3] (relative to the splat mean)?  qthr (p3.y) already
-// carries the rounding margin; ia/ic are 1/a, 1/c (only pick the point where Q
-// is evaluated exactly, so their rounding cannot make the test unsafe beyond
-// a ~1e-14 relative change that the margin covers).
-__device__ __forceinline__ bool block_may_touch(const float4& p0, const float4& p1, const float4& p3, double x0,
-                                          double y0) {
+// May the splat's alpha reach 1/255 somewhere in the pixel-centre rectangle
+// [x0, x0+7] x [y0, y0+3] (relative to the splat mean)?  Conservative: the
+// minimum of the conic quadratic Q over the rectangle (edge minimisers clamped,
+// Q evaluated in float) is compared with qthr (p3.y), which k_preprocess
+// computed in double as 2 ln(255 max(fa, pa)) inflated by a relative margin of
+// 2e-5 (a+c)^2/det >= 2e-5 cond(conic).  That margin covers both the float
+// rounding of the reference's per-pixel power (~1.5e-6 cond) and of this
+// evaluation (~8e-7 cond); ia/ic (1/a, 1/c) only place the evaluation point.
+__device__ __forceinline__ bool block_may_touch(const float4& p0, const float4& p1, const float4& p3, float x0,
+                                                float y0) {
     const float qthr = p3.y;
     if (qthr < 0.0f) return false;
-    const double x1 = x0 + 7.0, y1 = y0 + 3.0;
-    if (x0 <= 0.0 && 0.0 <= x1 && y0 <= 0.0 && 0.0 <= y1) return true;
-    const double a = p0.z, b = p0.w, c = p1.x, ia = p3.z, ic = p3.w;
-    double qm = 1e300;
+    const float x1 = x0 + 7.0f, y1 = y0 + 3.0f;
+    if (x0 <= 0.0f && 0.0f <= x1 && y0 <= 0.0f && 0.0f <= y1) return true;
+    const float a = p0.z, b = p0.w, c = p1.x, ia = p3.z, ic = p3.w;
+    float qm = __int_as_float(0x7f800000);
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-        const double x = e ? x1 : x0;
-        double y = -b * x * ic;
+        const float x = e ? x1 : x0;
+        float y = -b * x * ic;
         y = y < y0 ? y0 : (y > y1 ? y1 : y);
-        qm = fmin(qm, (a * x + 2.0 * b * y) * x + c * y * y);
-        const double yy = e ? y1 : y0;
-        double xx = -b * yy * ia;
+        qm = fminf(qm, (a * x + 2.0f * b * y) * x + c * y * y);
+        const float yy = e ? y1 : y0;
+        float xx = -b * yy * ia;
         xx = xx < x0 ? x0 : (xx > x1 ? x1 : xx);
-        qm = fmin(qm, (a * xx + 2.0 * b * yy) * xx + c * yy * yy);
+        qm = fminf(qm, (a * xx + 2.0f * b * yy) * xx + c * yy * yy);
     }
-    return !(qm > (double)qthr);
+    return !(qm > qthr);
 }
 
 }  // namespace hs

@@ -170,6 +170,20 @@ __global__ void __launch_bounds__(kScanThreads) k_dup_offsets(const uint32_t* __
 // 1/255 floor somewhere in 8x4 block b of the tile (block_may_touch).  The
 // tile sort orders by bits [8, 32) and carries the mask along; the blend then
 // never stages entries that cannot touch its block.
+__device__ __forceinline__ uint32_t tile_reach_mask(const float4& p0, const float4& p1, const float4& p3, int tx,
+                                                    int ty) {
+    uint32_t mask = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const float bx = (float)(tx * kTile + (b & 1) * 8) + 0.5f - p0.x;
+        const float by = (float)(ty * kTile + (b >> 1) * 4) + 0.5f - p0.y;
+        if (block_may_touch(p0, p1, p3, bx, by)) mask |= 1u << b;
+    }
+    return mask;
+}
+
+// One lane per splat for small footprints; splats covering more than 4 tiles
+// are then emitted cooperatively by the whole warp (one lane per tile).
 __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __restrict__ ids,
                                                           const uint4* __restrict__ dinfo,
                                                           const ProjRec* __restrict__ proj,
@@ -179,25 +193,51 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __rest
                                                           uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     const uint64_t n = *v_ptr;
     if (*sort_n_ptr == 0) return;  // nothing to emit, or over capacity
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t id = ids[i];
-        const uint4 di = dinfo[id];
-        const float4 p0 = proj[id].p0, p1 = proj[id].p1, p3 = proj[id].p3;
-        const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
-        uint64_t o = offsets[i];
-        for (int ty = ty0; ty < ty1; ++ty)
-            for (int tx = tx0; tx < tx1; ++tx) {
-                uint32_t mask = 0;
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    const double bx = (double)(tx * kTile + (b & 1) * 8) + 0.5 - (double)p0.x;
-                    const double by = (double)(ty * kTile + (b >> 1) * 4) + 0.5 - (double)p0.y;
-                    if (block_may_touch(p0, p1, p3, bx, by)) mask |= 1u << b;
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+        const uint64_t i = base + lane;
+        uint32_t id = 0, o = 0;
+        int tx0 = 0, tx1 = 0, ty0 = 0, ty1 = 0;
+        float4 p0 = make_float4(0, 0, 0, 0), p1 = p0, p3 = p0;
+        if (i < n) {
+            id = ids[i];
+            const uint4 di = dinfo[id];
+            p0 = proj[id].p0;
+            p1 = proj[id].p1;
+            p3 = proj[id].p3;
+            tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
+            o = offsets[i];
+        }
+        const int w = tx1 - tx0, area = w * (ty1 - ty0);
+        const bool big = area > 4;
+        if (!big) {
+            uint32_t oo = o;
+            for (int ty = ty0; ty < ty1; ++ty)
+                for (int tx = tx0; tx < tx1; ++tx) {
+                    keys[oo] = ((uint32_t)(ty * tiles_x + tx) << 8) | tile_reach_mask(p0, p1, p3, tx, ty);
+                    vals[oo] = id;
+                    ++oo;
                 }
-                keys[o] = ((uint32_t)(ty * tiles_x + tx) << 8) | mask;
-                vals[o] = id;
-                ++o;
+        }
+        for (uint32_t m = __ballot_sync(0xffffffffu, big); m; m &= m - 1) {
+            const int src = __ffs(m) - 1;
+            const uint32_t sid = __shfl_sync(0xffffffffu, id, src), so = __shfl_sync(0xffffffffu, o, src);
+            const int sx0 = __shfl_sync(0xffffffffu, tx0, src), sy0 = __shfl_sync(0xffffffffu, ty0, src);
+            const int sw = __shfl_sync(0xffffffffu, w, src), sa = __shfl_sync(0xffffffffu, area, src);
+            float4 q0, q1, q3;
+            q0.x = __shfl_sync(0xffffffffu, p0.x, src), q0.y = __shfl_sync(0xffffffffu, p0.y, src);
+            q0.z = __shfl_sync(0xffffffffu, p0.z, src), q0.w = __shfl_sync(0xffffffffu, p0.w, src);
+            q1.x = __shfl_sync(0xffffffffu, p1.x, src), q1.y = __shfl_sync(0xffffffffu, p1.y, src);
+            q1.z = __shfl_sync(0xffffffffu, p1.z, src), q1.w = __shfl_sync(0xffffffffu, p1.w, src);
+            q3.x = __shfl_sync(0xffffffffu, p3.x, src), q3.y = __shfl_sync(0xffffffffu, p3.y, src);
+            q3.z = __shfl_sync(0xffffffffu, p3.z, src), q3.w = __shfl_sync(0xffffffffu, p3.w, src);
+            for (int t = lane; t < sa; t += 32) {
+                const int tx = sx0 + t % sw, ty = sy0 + t / sw;
+                keys[so + t] = ((uint32_t)(ty * tiles_x + tx) << 8) | tile_reach_mask(q0, q1, q3, tx, ty);
+                vals[so + t] = sid;
             }
+        }
     }
 }
 
