@@ -337,8 +337,8 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
                            &ds->overflows, s);
     uint32_t* kb[2] = {f->keys[0].as<uint32_t>(), f->keys[1].as<uint32_t>()};
     uint32_t* vb[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
-    hs::launch_duplicate_sorted(ids, f->dinfo.as<uint4>(), f->proj.as<ProjRec>(), f->offsets.as<uint32_t>(), &ds->n_visible_sorted, f->n_max,
-                                &ds->sort_n, cp.tiles_x, kb[0], vb[0], s);
+    hs::launch_duplicate_sorted(ids, f->dinfo.as<uint4>(), f->proj.as<ProjRec>(), f->offsets.as<uint32_t>(),
+                                &ds->n_visible_sorted, f->n_max, &ds->sort_n, f->cap_dup, cp.tiles_x, kb[0], vb[0], s);
     if (ctx->debug) {
         hs::launch_make_keys(kb[0], vb[0], f->dinfo.as<uint4>(), &ds->sort_n, f->cap_dup, f->dupk.as<uint64_t>(), s);
         HS_CUDA(ctx, cudaMemcpyAsync(f->dupv.p, f->vals[0].p, f->cap_dup * 4, cudaMemcpyDeviceToDevice, s));

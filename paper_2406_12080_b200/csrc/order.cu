@@ -166,27 +166,10 @@ __global__ void __launch_bounds__(kScanThreads) k_dup_offsets(const uint32_t* __
 }
 
 // (tile, id) pairs of the depth-sorted splats, tiles of a splat row-major.
-// Key = tile << 8 | block mask: bit b set when the splat's alpha can pass the
-// 1/255 floor somewhere in 8x4 block b of the tile (block_may_touch).  The
-// tile sort orders by bits [8, 32) and carries the mask along; the blend then
-// never stages entries that cannot touch its block.
-__device__ __forceinline__ uint32_t tile_reach_mask(const float4& p0, const float4& p1, const float4& p3, int tx,
-                                                    int ty) {
-    uint32_t mask = 0;
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-        const float bx = (float)(tx * kTile + (b & 1) * 8) + 0.5f - p0.x;
-        const float by = (float)(ty * kTile + (b >> 1) * 4) + 0.5f - p0.y;
-        if (block_may_touch(p0, p1, p3, bx, by)) mask |= 1u << b;
-    }
-    return mask;
-}
-
 // One lane per splat for small footprints; splats covering more than 4 tiles
-// are then emitted cooperatively by the whole warp (one lane per tile).
+// are emitted cooperatively by the whole warp (one lane per tile).
 __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __restrict__ ids,
                                                           const uint4* __restrict__ dinfo,
-                                                          const ProjRec* __restrict__ proj,
                                                           const uint32_t* __restrict__ offsets,
                                                           const uint64_t* __restrict__ v_ptr,
                                                           const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
@@ -199,13 +182,9 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __rest
         const uint64_t i = base + lane;
         uint32_t id = 0, o = 0;
         int tx0 = 0, tx1 = 0, ty0 = 0, ty1 = 0;
-        float4 p0 = make_float4(0, 0, 0, 0), p1 = p0, p3 = p0;
         if (i < n) {
             id = ids[i];
             const uint4 di = dinfo[id];
-            p0 = proj[id].p0;
-            p1 = proj[id].p1;
-            p3 = proj[id].p3;
             tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
             o = offsets[i];
         }
@@ -215,7 +194,7 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __rest
             uint32_t oo = o;
             for (int ty = ty0; ty < ty1; ++ty)
                 for (int tx = tx0; tx < tx1; ++tx) {
-                    keys[oo] = ((uint32_t)(ty * tiles_x + tx) << 8) | tile_reach_mask(p0, p1, p3, tx, ty);
+                    keys[oo] = (uint32_t)(ty * tiles_x + tx) << 8;
                     vals[oo] = id;
                     ++oo;
                 }
@@ -225,19 +204,35 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __rest
             const uint32_t sid = __shfl_sync(0xffffffffu, id, src), so = __shfl_sync(0xffffffffu, o, src);
             const int sx0 = __shfl_sync(0xffffffffu, tx0, src), sy0 = __shfl_sync(0xffffffffu, ty0, src);
             const int sw = __shfl_sync(0xffffffffu, w, src), sa = __shfl_sync(0xffffffffu, area, src);
-            float4 q0, q1, q3;
-            q0.x = __shfl_sync(0xffffffffu, p0.x, src), q0.y = __shfl_sync(0xffffffffu, p0.y, src);
-            q0.z = __shfl_sync(0xffffffffu, p0.z, src), q0.w = __shfl_sync(0xffffffffu, p0.w, src);
-            q1.x = __shfl_sync(0xffffffffu, p1.x, src), q1.y = __shfl_sync(0xffffffffu, p1.y, src);
-            q1.z = __shfl_sync(0xffffffffu, p1.z, src), q1.w = __shfl_sync(0xffffffffu, p1.w, src);
-            q3.x = __shfl_sync(0xffffffffu, p3.x, src), q3.y = __shfl_sync(0xffffffffu, p3.y, src);
-            q3.z = __shfl_sync(0xffffffffu, p3.z, src), q3.w = __shfl_sync(0xffffffffu, p3.w, src);
             for (int t = lane; t < sa; t += 32) {
-                const int tx = sx0 + t % sw, ty = sy0 + t / sw;
-                keys[so + t] = ((uint32_t)(ty * tiles_x + tx) << 8) | tile_reach_mask(q0, q1, q3, tx, ty);
+                keys[so + t] = (uint32_t)((sy0 + t / sw) * tiles_x + sx0 + t % sw) << 8;
                 vals[so + t] = sid;
             }
         }
+    }
+}
+
+// Reach masks: bit b of the key's low byte is set when the splat's alpha can
+// pass the 1/255 floor somewhere in 8x4 block b of the tile (block_may_touch).
+// The tile sort orders by bits [8, 32) and carries the mask along; the blend
+// never stages entries that cannot touch its block.  One thread per entry.
+__global__ void __launch_bounds__(256) k_reach_masks(uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                                     const ProjRec* __restrict__ proj,
+                                                     const uint64_t* __restrict__ n_ptr, int tiles_x) {
+    const uint64_t n = *n_ptr;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t key = keys[i];
+        const ProjRec* r = proj + vals[i];
+        const float4 p0 = r->p0, p1 = r->p1, p3 = r->p3;
+        const int t = (int)(key >> 8);
+        uint32_t mask = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const float bx = (float)((t % tiles_x) * kTile + (b & 1) * 8) + 0.5f - p0.x;
+            const float by = (float)((t / tiles_x) * kTile + (b >> 1) * 4) + 0.5f - p0.y;
+            if (block_may_touch(p0, p1, p3, bx, by)) mask |= 1u << b;
+        }
+        keys[i] = key | mask;
     }
 }
 
@@ -296,10 +291,10 @@ void launch_dup_offsets(const uint32_t* ids, const uint32_t* dupcount, const uin
 }
 
 void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const ProjRec* proj, const uint32_t* offsets,
-                             const uint64_t* v_ptr,
-                             uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* keys, uint32_t* vals,
-                             cudaStream_t s) {
-    k_duplicate_sorted<<<flat_grid(n_max), 256, 0, s>>>(ids, dinfo, proj, offsets, v_ptr, sort_n_ptr, tiles_x, keys, vals);
+                             const uint64_t* v_ptr, uint64_t n_max, const uint64_t* sort_n_ptr, uint64_t dup_max,
+                             int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+    k_duplicate_sorted<<<flat_grid(n_max), 256, 0, s>>>(ids, dinfo, offsets, v_ptr, sort_n_ptr, tiles_x, keys, vals);
+    k_reach_masks<<<flat_grid(dup_max), 256, 0, s>>>(keys, vals, proj, sort_n_ptr, tiles_x);
 }
 
 void launch_ranges(const uint32_t* keys, const uint64_t* n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s) {
