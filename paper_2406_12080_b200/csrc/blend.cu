@@ -83,13 +83,12 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
         const int x = bx + (lane & 7), y = by + (lane >> 3);
         const bool inside = x < cam.width && y < cam.height;
         const float px = (float)x + 0.5f, py = (float)y + 0.5f;
-        const double ox = (double)bx + 0.5, oy = (double)by + 0.5;
         uint2 range = make_uint2(0, 0);
         if (any_keys) range = ranges[tile];
         float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, d = 0.0f;
         bool done = !inside;
         // The sorted keys carry, in their low 8 bits, which of the tile's 8 blocks each
-        // entry can reach (k_duplicate_sorted, block_may_touch): entries outside this
+        // entry can reach (k_reach_masks, tile_reach_mask): entries outside this
         // block are never staged.  Ids/keys run two batches ahead, records one.
         const uint32_t bmask = 1u << blk;
         auto fetch = [&](uint32_t e, uint32_t& id, bool& hit) {

@@ -93,34 +93,65 @@ __device__ __forceinline__ float interp_weight(float en, float ep, float tau) {
     return smin(1.0f, smax(0.0f, v));
 }
 
-// May the splat's alpha reach 1/255 somewhere in the pixel-centre rectangle
-// [x0, x0+7] x [y0, y0+3] (relative to the splat mean)?  Conservative: the
-// minimum of the conic quadratic Q over the rectangle (edge minimisers clamped,
-// Q evaluated in float) is compared with qthr (p3.y), which k_preprocess
-// computed in double as 2 ln(255 max(fa, pa)) inflated by a relative margin of
-// 2e-5 (a+c)^2/det >= 2e-5 cond(conic).  That margin covers both the float
-// rounding of the reference's per-pixel power (~1.5e-6 cond) and of this
-// evaluation (~8e-7 cond); ia/ic (1/a, 1/c) only place the evaluation point.
-__device__ __forceinline__ bool block_may_touch(const float4& p0, const float4& p1, const float4& p3, float x0,
-                                                float y0) {
+// Reach mask of one tile: bit (2 r + j) is set when the splat's alpha may
+// pass 1/255 somewhere in the 8x4 pixel block of column j, row r, i.e. in the
+// pixel-centre rectangle [px0 + 8j, px0 + 8j + 7] x [py0 + 4r, py0 + 4r + 3]
+// (pixel (px0, py0) is the tile's first).  Each edge coordinate is formed
+// exactly as the blend forms d = ((float)x + 0.5) - mean, so the blend's d
+// values of the block's pixels lie inside the float rectangle.  Conservative:
+// the minimum of the conic quadratic Q over each rectangle -- 0 when it holds
+// the mean, else the least of its four edge minima (edge minimiser clamped to
+// the edge, Q evaluated in float with fma) -- is compared with qthr (p3.y),
+// which k_preprocess computed in double as 2 ln(255 max(fa, pa)) inflated by a
+// relative margin of 2e-5 (a+c)^2/det >= 2e-5 cond(conic).  That margin covers
+// both the float rounding of the reference's per-pixel power (~1.5e-6 cond)
+// and of this evaluation (< 1e-6 cond); ia/ic (1/a, 1/c) only place the
+// evaluation points.  Edge quantities are shared between the blocks: 4 column
+// edges and 8 row edges instead of 32 edge evaluations from scratch.
+__device__ __forceinline__ uint32_t tile_reach_mask(const float4& p0, const float4& p1, const float4& p3, int px0,
+                                                    int py0) {
     const float qthr = p3.y;
-    if (qthr < 0.0f) return false;
-    const float x1 = x0 + 7.0f, y1 = y0 + 3.0f;
-    if (x0 <= 0.0f && 0.0f <= x1 && y0 <= 0.0f && 0.0f <= y1) return true;
-    const float a = p0.z, b = p0.w, c = p1.x, ia = p3.z, ic = p3.w;
-    float qm = __int_as_float(0x7f800000);
+    if (qthr < 0.0f) return 0u;
+    const float a = p0.z, b = p0.w, c = p1.x;
+    const float b2 = 2.0f * b, sx = -b * p3.w, sy = -b * p3.z;
+    // column edges x = X + {0, 7, 8, 15}: Q on the edge is (c y + 2 b x) y + a x^2
+    float xe[4], bx2[4], axx[4], ymin[4];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const float x = e ? x1 : x0;
-        float y = -b * x * ic;
-        y = y < y0 ? y0 : (y > y1 ? y1 : y);
-        qm = fminf(qm, (a * x + 2.0f * b * y) * x + c * y * y);
-        const float yy = e ? y1 : y0;
-        float xx = -b * yy * ia;
-        xx = xx < x0 ? x0 : (xx > x1 ? x1 : xx);
-        qm = fminf(qm, (a * xx + 2.0f * b * yy) * xx + c * yy * yy);
+    for (int k = 0; k < 4; ++k) {
+        xe[k] = ((float)(px0 + (k >> 1) * 8 + (k & 1) * 7) + 0.5f) - p0.x;
+        bx2[k] = b2 * xe[k];
+        axx[k] = a * xe[k] * xe[k];
+        ymin[k] = sx * xe[k];
     }
-    return !(qm > qthr);
+    // row edges y = Y + {0, 3, 4, 7, 8, 11, 12, 15}: Q on the edge is (a x + 2 b y) x + c y^2
+    float ye[8], by2[8], cyy[8], xmin[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        ye[k] = ((float)(py0 + (k >> 1) * 4 + (k & 1) * 3) + 0.5f) - p0.y;
+        by2[k] = b2 * ye[k];
+        cyy[k] = c * ye[k] * ye[k];
+        xmin[k] = sy * ye[k];
+    }
+    uint32_t mask = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const float y0 = ye[2 * r], y1 = ye[2 * r + 1];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float x0 = xe[2 * j], x1 = xe[2 * j + 1];
+            float qm = (x0 <= 0.0f && 0.0f <= x1 && y0 <= 0.0f && 0.0f <= y1) ? 0.0f : __int_as_float(0x7f800000);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int kx = 2 * j + e, ky = 2 * r + e;
+                const float y = fminf(fmaxf(ymin[kx], y0), y1);
+                qm = fminf(qm, __fmaf_rn(__fmaf_rn(c, y, bx2[kx]), y, axx[kx]));
+                const float x = fminf(fmaxf(xmin[ky], x0), x1);
+                qm = fminf(qm, __fmaf_rn(__fmaf_rn(a, x, by2[ky]), x, cyy[ky]));
+            }
+            if (!(qm > qthr)) mask |= 1u << (2 * r + j);
+        }
+    }
+    return mask;
 }
 
 }  // namespace hs

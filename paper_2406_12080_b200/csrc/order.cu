@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __rest
 }
 
 // Reach masks: bit b of the key's low byte is set when the splat's alpha can
-// pass the 1/255 floor somewhere in 8x4 block b of the tile (block_may_touch).
+// pass the 1/255 floor somewhere in 8x4 block b of the tile (tile_reach_mask).
 // The tile sort orders by bits [8, 32) and carries the mask along; the blend
 // never stages entries that cannot touch its block.  One thread per entry.
 __global__ void __launch_bounds__(256) k_reach_masks(uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
@@ -225,13 +225,7 @@ __global__ void __launch_bounds__(256) k_reach_masks(uint32_t* __restrict__ keys
         const ProjRec* r = proj + vals[i];
         const float4 p0 = r->p0, p1 = r->p1, p3 = r->p3;
         const int t = (int)(key >> 8);
-        uint32_t mask = 0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            const float bx = (float)((t % tiles_x) * kTile + (b & 1) * 8) + 0.5f - p0.x;
-            const float by = (float)((t / tiles_x) * kTile + (b >> 1) * 4) + 0.5f - p0.y;
-            if (block_may_touch(p0, p1, p3, bx, by)) mask |= 1u << b;
-        }
+        const uint32_t mask = tile_reach_mask(p0, p1, p3, (t % tiles_x) * kTile, (t / tiles_x) * kTile);
         keys[i] = key | mask;
     }
 }
