@@ -54,6 +54,8 @@ struct DevStats {
     unsigned long long overflows;  // sticky: frames whose D exceeded capacity since the last wait
 };
 
+static_assert(sizeof(DevStats) % 8 == 0, "DevStats is copied as 64-bit words");
+
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -99,7 +101,8 @@ struct hs_cut {
     hs_context* ctx = nullptr;
     uint64_t cap = 0;
     DBuf node, t, alpha, count;
-    uint64_t* h_count = nullptr;  // pinned
+    uint64_t* h_count = nullptr;  // pinned, mapped
+    uint64_t* h_count_dev = nullptr;  // device alias of h_count
     const hs_hierarchy* h = nullptr;
     cudaEvent_t done = nullptr;
     ~hs_cut() {
@@ -115,7 +118,8 @@ struct hs_frame {
     DBuf tile_order;
     DBuf proj, dinfo, dupcount, offsets, zkeys[2], zvals[2], keys[2], vals[2], dupk, dupv, keys64, ranges, color, depth, trans, touched, dbg16,
         splat_attr, stats, scratch;
-    DevStats* h_stats = nullptr;  // pinned
+    DevStats* h_stats = nullptr;  // pinned, mapped
+    DevStats* h_stats_dev = nullptr;  // device alias of h_stats
     DevStats* h_stats_dl = nullptr;  // pinned, snapshot taken with an async read-back
     uint64_t* h_n = nullptr;      // pinned
     cudaEvent_t ev[6] = {};
@@ -291,7 +295,10 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
     HS_CUDA(ctx, f->stats.ensure(sizeof(DevStats)));
     f->passes = sort_passes_for(tiles);
     HS_CUDA(ctx, f->scratch.ensure(scratch_layout(cs, f->cap_dup, f->passes).total));
-    if (!f->h_stats) HS_CUDA(ctx, cudaMallocHost(&f->h_stats, sizeof(DevStats)));
+    if (!f->h_stats) {
+        HS_CUDA(ctx, cudaHostAlloc(&f->h_stats, sizeof(DevStats), cudaHostAllocMapped));
+        HS_CUDA(ctx, cudaHostGetDevicePointer(&f->h_stats_dev, f->h_stats, 0));
+    }
     if (!f->h_n) HS_CUDA(ctx, cudaMallocHost(&f->h_n, 8));
     for (auto& e : f->ev)
         if (!e) HS_CUDA(ctx, cudaEventCreate(&e));
@@ -314,7 +321,7 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     if (f->copy_pending) HS_CUDA(ctx, cudaStreamWaitEvent(s, f->copy_done, 0));
     HS_CUDA(ctx, cudaMemsetAsync(sc, 0, L.zero_bytes, s));
     HS_CUDA(ctx, cudaMemsetAsync(&ds->n_visible, 0, offsetof(DevStats, overflows) - 8, s));
-    if (f->from_cut) HS_CUDA(ctx, cudaMemcpyAsync(&ds->n_splats, f->n_ptr, 8, cudaMemcpyDeviceToDevice, s));
+    if (f->from_cut) hs::launch_copy_words(f->n_ptr, &ds->n_splats, 8, s);
     HS_CUDA(ctx, cudaMemsetAsync(f->ranges.p, 0, (size_t)cp.tiles_x * cp.tiles_y * 8, s));
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[1], s));
     hs::launch_preprocess(f->from_cut, f->attr, f->cut_node, f->cut_t, f->n_ptr, f->n_max, cp, f->proj.as<ProjRec>(),
@@ -356,7 +363,7 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     hs::launch_count_touched(f->touched.as<uint8_t>(), f->n_ptr, f->n_max, &ds->rendered, s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[5], s));
     HS_CUDA(ctx, cudaGetLastError());
-    HS_CUDA(ctx, cudaMemcpyAsync(f->h_stats, ds, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    hs::launch_copy_words(ds, f->h_stats_dev, sizeof(DevStats), s);
     HS_CUDA(ctx, cudaEventRecord(f->done, s));
     f->pending = true;
     return HS_OK;
@@ -416,7 +423,10 @@ hs_status ensure_cut(hs_context* ctx, hs_cut* cut, uint64_t cap) {
         cut->cap = cap;
     }
     HS_CUDA(ctx, cut->count.ensure(8));
-    if (!cut->h_count) HS_CUDA(ctx, cudaMallocHost(&cut->h_count, 8));
+    if (!cut->h_count) {
+        HS_CUDA(ctx, cudaHostAlloc(&cut->h_count, 8, cudaHostAllocMapped));
+        HS_CUDA(ctx, cudaHostGetDevicePointer(&cut->h_count_dev, cut->h_count, 0));
+    }
     if (!cut->done) HS_CUDA(ctx, cudaEventCreateWithFlags(&cut->done, cudaEventDisableTiming));
     return HS_OK;
 }
@@ -431,12 +441,12 @@ hs_status enqueue_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* c
     unsigned char* sc = ctx->cut_scratch.as<unsigned char>();
     HS_CUDA(ctx, cudaMemsetAsync(sc, 0, 64 + words * 8, ctx->stream));
     const CamParams cp = make_cam(cam);
-    hs::launch_select_cut(h->cull_a.as<float4>(), h->cull_b.as<float4>(), h->attr.as<float4>(), h->n, cp, tau,
+    hs::launch_select_cut(h->cull_a.as<float4>(), h->cull_b.as<float4>(), h->n, cp, tau,
                           cut->node.as<uint32_t>(), cut->t.as<float>(), cut->alpha.as<float>(),
                           reinterpret_cast<uint64_t*>(sc + 64), reinterpret_cast<uint32_t*>(sc),
                           cut->count.as<uint64_t>(), ctx->stream);
     HS_CUDA(ctx, cudaGetLastError());
-    HS_CUDA(ctx, cudaMemcpyAsync(cut->h_count, cut->count.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    hs::launch_copy_words(cut->count.p, cut->h_count_dev, 8, ctx->stream);
     HS_CUDA(ctx, cudaEventRecord(cut->done, ctx->stream));
     cut->h = h;
     return HS_OK;
@@ -580,6 +590,7 @@ hs_status hs_hierarchy_upload(hs_context* ctx, const hs_node_soa* nodes, uint64_
         cudaMemcpyAsync(h->attr.as<float4>() + 16 * lo, at, m * 256, cudaMemcpyHostToDevice, ctx->stream);
         cudaEventRecord(evs[b], ctx->stream);
     }
+    hs::launch_child_alpha(h->attr.as<float4>(), h->cull_b.as<float4>(), n, ctx->stream);
     e = cudaStreamSynchronize(ctx->stream);
     cudaEventDestroy(evs[0]);
     cudaEventDestroy(evs[1]);

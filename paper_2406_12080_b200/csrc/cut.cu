@@ -11,11 +11,18 @@
 // Output is written in ascending node order via a single-pass decoupled
 // look-back scan over 2048-node tiles, so no second pass or sort is needed.
 //
+// The transition alpha depends only on the parent (its falloff and child
+// count), so it is precomputed once per hierarchy (k_child_alpha) into the
+// parent's cull record: the per-frame pass needs two dependent loads, no libm.
+//
 // Bytes per node: 32 (own cull record) + <= 32 (parent cull record, shared by
-// siblings) + 4 (parent falloff, selected nodes only); 12 per cut entry out.
+// siblings); 12 per cut entry out.
 #include "hs_device.cuh"
 #include "hs_kernels.h"
 #include "hs_scan.cuh"
+#include "hs_libm.cuh"
+
+#include <algorithm>
 
 namespace hs {
 
@@ -23,30 +30,47 @@ constexpr int kCutThreads = 256;
 constexpr int kCutItems = 8;
 constexpr int kCutTile = kCutThreads * kCutItems;
 
-__global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __restrict__ cull_a,
-                                                            const float4* __restrict__ cull_b,
-                                                            const float4* __restrict__ attr, uint64_t n, CamParams cam,
-                                                            float tau, uint32_t* __restrict__ out_node,
+// Per-node camera-independent part of transition_alpha (lod.hpp:41-45): the
+// alpha a child of node p receives depends only on p's falloff and child count,
+// so it is computed once at upload into cull_b[p].w (leaves: kLeafMark).
+__global__ void __launch_bounds__(256) k_child_alpha(const float4* __restrict__ attr, float4* __restrict__ cull_b,
+                                                     uint64_t n) {
+    __shared__ uint64_t s_exp_tab[32];
+    __shared__ uint64_t s_log_tab[32];
+    if (threadIdx.x < 32) {
+        s_exp_tab[threadIdx.x] = c_exp2f_tab[threadIdx.x];
+        s_log_tab[threadIdx.x] = c_powf_log2_tab[threadIdx.x];
+    }
+    __syncthreads();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = __float_as_uint(attr[i * kAttrVec4 + 15].x);
+        uint32_t bits = kLeafMark;
+        if (k != 0) {
+            const float f = attr[i * kAttrVec4].w;
+            const float aa = smin(smax(smin(f, kAlphaMax), 0.0f), kAlphaMax);
+            bits = __float_as_uint(1.0f - hs_libm::powf_glibc(1.0f - aa, 1.0f / (float)(int)k, s_log_tab, s_exp_tab));
+            if (bits == kLeafMark) bits = 0x7FFFFFFFu;  // a NaN stays a NaN, never the leaf mark
+        }
+        cull_b[i].w = __uint_as_float(bits);
+    }
+}
+
+__global__ void __launch_bounds__(kCutThreads, 6) k_select_cut(const float4* __restrict__ cull_a,
+                                                            const float4* __restrict__ cull_b, uint64_t n,
+                                                            CamParams cam, float tau, uint32_t* __restrict__ out_node,
                                                             float* __restrict__ out_t, float* __restrict__ out_alpha,
                                                             uint64_t* status, uint32_t* tile_counter,
                                                             uint64_t* count_out) {
-    __shared__ uint64_t s_exp_tab[32];
-    __shared__ uint64_t s_log_tab[32];
     __shared__ uint32_t s_cnt[kCutItems * 8], s_off[kCutItems * 8];
     __shared__ uint64_t s_base;
     __shared__ uint32_t s_tile;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid < 32) {
-        s_exp_tab[tid] = c_exp2f_tab[tid];
-        s_log_tab[tid] = c_powf_log2_tab[tid];
-    }
     if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint64_t base = (uint64_t)tile * kCutTile;
     const uint64_t num_tiles = (n + kCutTile - 1) / kCutTile;
 
-    uint32_t ballots[kCutItems];
     uint32_t sel_mask = 0;
     float tv[kCutItems], av[kCutItems], eps[kCutItems];
     uint32_t par[kCutItems];
@@ -61,9 +85,8 @@ __global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __rest
             const float4 a = cull_a[i];
             const float4 b = cull_b[i];
             const uint32_t parent = __float_as_uint(b.z);
-            const uint32_t cc = __float_as_uint(b.w);
             eps[k] = granularity(a.x, a.y, a.z, a.w, b.x, b.y, cam);
-            if (eps[k] <= tau || cc == 0) {  // fine enough, or a leaf (lod.hpp:64-65)
+            if (eps[k] <= tau || __float_as_uint(b.w) == kLeafMark) {  // fine enough, or a leaf (lod.hpp:64-65)
                 if (parent == kNoNode)
                     sel_mask |= 1u << k;  // the root: t = 1, alpha' = 0
                 else
@@ -71,13 +94,12 @@ __global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __rest
             }
         }
     }
-    // phase 2: parent cull records for the candidates, parent granularity, t
-    uint32_t kk[kCutItems];
+    // phase 2: parent cull records for the candidates: parent granularity, t,
+    // and the transition alpha the parent hands its children
 #pragma unroll
     for (int k = 0; k < kCutItems; ++k) {
         tv[k] = 1.0f;
         av[k] = 0.0f;
-        kk[k] = 0;
         if (need & (1u << k)) {
             const float4 pa = cull_a[par[k]];
             const float4 pb = cull_b[par[k]];
@@ -85,12 +107,12 @@ __global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __rest
             if (ep > tau) {  // parent not yet fine enough (lod.hpp:67-69)
                 sel_mask |= 1u << k;
                 tv[k] = interp_weight(eps[k], ep, tau);
-                kk[k] = __float_as_uint(pb.w);
+                av[k] = pb.w;
             }
         }
     }
-    // selection is final: publish this tile's count and let warp 0 run the look-back
-    // while every warp (warp 0 afterwards) does phase 3
+    // selection is final: tile count, block offsets, decoupled look-back (warp 0)
+    uint32_t ballots[kCutItems];
 #pragma unroll
     for (int k = 0; k < kCutItems; ++k) {
         ballots[k] = __ballot_sync(0xffffffffu, (sel_mask >> k) & 1u);
@@ -123,15 +145,6 @@ __global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __rest
             if (tile == num_tiles - 1) *count_out = prefix + total;
         }
     }
-    // phase 3: transition_alpha from the parent's falloff (lod.hpp:84-88)
-#pragma unroll
-    for (int k = 0; k < kCutItems; ++k) {
-        if (kk[k]) {
-            const float pf = attr[(uint64_t)par[k] * kAttrVec4].w;
-            const float aa = smin(smax(smin(pf, kAlphaMax), 0.0f), kAlphaMax);
-            av[k] = 1.0f - hs_libm::powf_glibc(1.0f - aa, 1.0f / (float)(int)kk[k], s_log_tab, s_exp_tab);
-        }
-    }
     __syncthreads();
     const uint64_t blk = s_base;
     const uint32_t lt_mask = (1u << lane) - 1u;
@@ -146,12 +159,17 @@ __global__ void __launch_bounds__(kCutThreads) k_select_cut(const float4* __rest
     }
 }
 
-void launch_select_cut(const float4* cull_a, const float4* cull_b, const float4* attr, uint64_t n,
-                       const CamParams& cam, float tau, uint32_t* out_node, float* out_t, float* out_alpha,
-                       uint64_t* status, uint32_t* tile_counter, uint64_t* count_out, cudaStream_t stream) {
+void launch_child_alpha(const float4* attr, float4* cull_b, uint64_t n, cudaStream_t stream) {
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148 * 16);
+    k_child_alpha<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, stream>>>(attr, cull_b, n);
+}
+
+void launch_select_cut(const float4* cull_a, const float4* cull_b, uint64_t n, const CamParams& cam, float tau,
+                       uint32_t* out_node, float* out_t, float* out_alpha, uint64_t* status, uint32_t* tile_counter,
+                       uint64_t* count_out, cudaStream_t stream) {
     const uint64_t tiles = (n + kCutTile - 1) / kCutTile;
-    k_select_cut<<<(unsigned)tiles, kCutThreads, 0, stream>>>(cull_a, cull_b, attr, n, cam, tau, out_node, out_t,
-                                                              out_alpha, status, tile_counter, count_out);
+    k_select_cut<<<(unsigned)tiles, kCutThreads, 0, stream>>>(cull_a, cull_b, n, cam, tau, out_node, out_t, out_alpha,
+                                                              status, tile_counter, count_out);
 }
 
 uint64_t select_cut_status_words(uint64_t n) { return (n + kCutTile - 1) / kCutTile; }

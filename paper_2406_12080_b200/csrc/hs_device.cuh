@@ -22,11 +22,14 @@ constexpr float kTransmittanceEps = 1e-4f;      // math.hpp:30
 constexpr float kDilation2d = 0.3f;             // math.hpp:31
 constexpr float kNearPlane = 0.01f;             // math.hpp:32
 constexpr uint32_t kNoNode = 0xFFFFFFFFu;       // model.hpp:15
+constexpr uint32_t kLeafMark = 0xFFFFFFFFu;     // cull_b[i].w of a leaf
 
 // ------------------------------------------------------------------ layout
 // Hierarchy in HBM (reference node order, structure of arrays):
 //   cull_a[i] = {min.x, min.y, min.z, max.x}            16 B
-//   cull_b[i] = {max.y, max.z, bits(parent), bits(child_count)}   16 B
+//   cull_b[i] = {max.y, max.z, bits(parent), child_alpha}   16 B
+//     child_alpha = transition alpha node i hands its children (k_child_alpha),
+//     bits kLeafMark for a leaf
 //   attr[16*i + 0] = {mean.xyz, falloff}
 //   attr[16*i + 1] = {scale.xyz, bits(parent)}
 //   attr[16*i + 2] = rotation (w, x, y, z)
@@ -40,7 +43,7 @@ constexpr int kAttrVec4 = 16;
 //   p0 = {mean2d.x, mean2d.y, conic0, conic1}
 //   p1 = {conic2, falloff_eff*alpha_scale, parent_falloff_eff*alpha_scale, t}
 //   p2 = {color.r, color.g, color.b, inv_depth}
-//   p3 = {inv_k, bits(tx0 | tx1 << 16), bits(ty0 | ty1 << 16), bits(cam z)}
+//   p3 = {inv_k, qthr (block-cull threshold), 1/conic0, 1/conic2}
 struct __align__(16) ProjRec {
     float4 p0, p1, p2, p3;
 };

@@ -369,6 +369,13 @@ __global__ void k_count_touched(uint8_t* __restrict__ touched, const uint64_t* _
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
 }
 
+// Small device->device / device->mapped-host word copies in stream order.  A
+// kernel instead of cudaMemcpyAsync keeps these off the copy engines, where
+// they would queue behind a previous frame's image read-back.
+__global__ void k_copy_words(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
 // -------------------------------------------------------------------------
 // launchers
 // -------------------------------------------------------------------------
@@ -410,6 +417,10 @@ void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* 
 void launch_count_touched(uint8_t* touched, const uint64_t* n_ptr, uint64_t n_max, unsigned long long* out,
                           cudaStream_t s) {
     k_count_touched<<<grid_for(n_max, 4), 256, 0, s>>>(touched, n_ptr, out);
+}
+
+void launch_copy_words(const void* src, void* dst, size_t bytes, cudaStream_t s) {
+    k_copy_words<<<1, 32, 0, s>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), (int)(bytes / 8));
 }
 
 }  // namespace hs
