@@ -30,7 +30,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "frames/sec at 1080p, tau=3px, 10M-leaf hierarchy; cut+render ms/frame"
 UNIT = "frames/s"
-KERNELS_PER_FRAME = 15  # cut, preprocess, scan, duplicate, sort hist+offs+6 passes, ranges, blend, count
 
 
 def peaks():
@@ -218,10 +217,12 @@ def main():
     time.sleep(0.3)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = L.hs_kernel_launch_count()
     e0.record(stream)
     for c in timed:
         hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, None), r.ctx)
     e1.record(stream)
+    launches = L.hs_kernel_launch_count() - launches0
     e1.synchronize()
     r.synchronize()
     clocks = sampler.stop()
@@ -335,7 +336,7 @@ def main():
             "per_frame": {"cut_entries": C_, "visible": V_, "duplicates": D_, "n_eval": NE, "n_contrib": NC},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": KERNELS_PER_FRAME * len(timed),
+            "gpu_launches": int(launches),
             "clocks": clocks,
             "setup_s": {"generate": gen_s, "upload": upload_s},
         }

@@ -210,6 +210,8 @@ hs_status hs_frame_download(hs_context* ctx, hs_frame* f, float* color, float* d
  * hs_frame_download_wait returns when the bytes have landed. */
 hs_status hs_frame_download_async(hs_context* ctx, hs_frame* f, float* color, float* depth, float* transmittance);
 hs_status hs_frame_download_wait(hs_context* ctx, hs_frame* f, int32_t* rendered_count);
+/* kernels this library has launched so far (process-wide; for launch accounting) */
+uint64_t hs_kernel_launch_count(void);
 hs_status hs_host_alloc(size_t bytes, void** out); /* pinned host memory */
 void hs_host_free(void* p);
 /* Parity hooks (ForwardContext, render.hpp:87-98, expressed as sort keys):

@@ -950,6 +950,11 @@ extern "C" hs_status hs_frame_download_wait(hs_context* ctx, hs_frame* f, int32_
     return HS_OK;
 }
 
+namespace hs {
+std::atomic<unsigned long long> g_kernel_launches{0};
+}
+extern "C" uint64_t hs_kernel_launch_count(void) { return hs::g_kernel_launches.load(); }
+
 extern "C" hs_status hs_host_alloc(size_t bytes, void** out) {
     if (!out) return HS_INVALID_ARGUMENT;
     return cudaMallocHost(out, bytes) == cudaSuccess ? HS_OK : HS_OUT_OF_MEMORY;

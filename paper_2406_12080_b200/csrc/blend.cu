@@ -269,12 +269,14 @@ void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uin
     }
     const int tasks = cam.tiles_x * cam.tiles_y * 8;
     const unsigned g = (unsigned)std::min<int>(grid[mode], std::max(1, tasks / kBlendWarps));
-    if (mode == 0)
+    if (mode == 0) {
         k_blend<0><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
                                                    eval_counts, task_counter, tile_order);
-    else
+    } else {
         k_blend<1><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
                                                    eval_counts, task_counter, tile_order);
+    }
+    note_launch();
 }
 
 }  // namespace hs

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(kCutThreads, 6) k_select_cut(const float4* __r
 void launch_child_alpha(const float4* attr, float4* cull_b, uint64_t n, cudaStream_t stream) {
     const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148 * 16);
     k_child_alpha<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, stream>>>(attr, cull_b, n);
+    note_launch();
 }
 
 void launch_select_cut(const float4* cull_a, const float4* cull_b, uint64_t n, const CamParams& cam, float tau,
@@ -170,6 +171,7 @@ void launch_select_cut(const float4* cull_a, const float4* cull_b, uint64_t n, c
     const uint64_t tiles = (n + kCutTile - 1) / kCutTile;
     k_select_cut<<<(unsigned)tiles, kCutThreads, 0, stream>>>(cull_a, cull_b, n, cam, tau, out_node, out_t, out_alpha,
                                                               status, tile_counter, count_out);
+    note_launch();
 }
 
 uint64_t select_cut_status_words(uint64_t n) { return (n + kCutTile - 1) / kCutTile; }

@@ -2,9 +2,14 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 namespace hs {
+
+// Process-wide count of kernels launched by this library (hs_kernel_launch_count).
+extern std::atomic<unsigned long long> g_kernel_launches;
+inline void note_launch() { g_kernel_launches.fetch_add(1, std::memory_order_relaxed); }
 
 struct CamParams;
 struct ProjRec;

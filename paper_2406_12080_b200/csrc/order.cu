@@ -275,6 +275,7 @@ void launch_compact_visible(const uint32_t* dupcount, const uint4* dinfo, const 
                             cudaStream_t s) {
     k_compact_visible<<<scan_grid(n_max), kScanThreads, 0, s>>>(dupcount, dinfo, n_ptr, keys, vals, status, counter,
                                                                 v_out);
+    note_launch();
 }
 
 void launch_dup_offsets(const uint32_t* ids, const uint32_t* dupcount, const uint64_t* v_ptr, uint64_t n_max,
@@ -282,22 +283,27 @@ void launch_dup_offsets(const uint32_t* ids, const uint32_t* dupcount, const uin
                         uint64_t* sort_n_out, uint64_t capacity, unsigned long long* overflows, cudaStream_t s) {
     k_dup_offsets<<<scan_grid(n_max), kScanThreads, 0, s>>>(ids, dupcount, v_ptr, offsets, status, counter, total_out,
                                                             sort_n_out, capacity, overflows);
+    note_launch();
 }
 
 void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const ProjRec* proj, const uint32_t* offsets,
                              const uint64_t* v_ptr, uint64_t n_max, const uint64_t* sort_n_ptr, uint64_t dup_max,
                              int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
     k_duplicate_sorted<<<flat_grid(n_max), 256, 0, s>>>(ids, dinfo, offsets, v_ptr, sort_n_ptr, tiles_x, keys, vals);
+    note_launch();
     k_reach_masks<<<flat_grid(dup_max), 256, 0, s>>>(keys, vals, proj, sort_n_ptr, tiles_x);
+    note_launch();
 }
 
 void launch_ranges(const uint32_t* keys, const uint64_t* n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s) {
     k_ranges<<<flat_grid(n_max), 256, 0, s>>>(keys, n_ptr, ranges);
+    note_launch();
 }
 
 void launch_make_keys(const uint32_t* tiles, const uint32_t* ids, const uint4* dinfo, const uint64_t* n_ptr,
                       uint64_t n_max, uint64_t* out, cudaStream_t s) {
     k_make_keys<<<flat_grid(n_max), 256, 0, s>>>(tiles, ids, dinfo, n_ptr, out);
+    note_launch();
 }
 
 }  // namespace hs
@@ -332,6 +338,7 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
 
 void launch_tile_order(const uint2* ranges, int tiles, const uint64_t* sort_n_ptr, uint32_t* order, cudaStream_t s) {
     k_tile_order<<<1, 1024, 0, s>>>(ranges, tiles, sort_n_ptr, order);
+    note_launch();
 }
 
 }  // namespace hs

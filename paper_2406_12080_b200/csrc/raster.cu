@@ -405,6 +405,7 @@ void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_no
     else
         k_preprocess<false><<<grid, 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, cam, proj, dinfo, dupcount, dbg16,
                                                  n_visible);
+    note_launch();
 }
 
 void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr,
@@ -412,15 +413,18 @@ void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* 
                      float* t, int* k, cudaStream_t s) {
     k_assemble<<<grid_for(n_max, 8), 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, mean, scale, rot, sh, fall, pfall, t,
                                                    k);
+    note_launch();
 }
 
 void launch_count_touched(uint8_t* touched, const uint64_t* n_ptr, uint64_t n_max, unsigned long long* out,
                           cudaStream_t s) {
     k_count_touched<<<grid_for(n_max, 4), 256, 0, s>>>(touched, n_ptr, out);
+    note_launch();
 }
 
 void launch_copy_words(const void* src, void* dst, size_t bytes, cudaStream_t s) {
     k_copy_words<<<1, 32, 0, s>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst), (int)(bytes / 8));
+    note_launch();
 }
 
 }  // namespace hs

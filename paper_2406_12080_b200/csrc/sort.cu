@@ -232,9 +232,12 @@ void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_p
     const uint64_t words = sort_status_words(n_max);
     cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * passes * (kRadix + 1), s);
     k_sort_zero<<<sms * 2, 256, 0, s>>>(status, n_ptr, words, passes);
+    note_launch();
     const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)sms * 4));
     k_sort_hist<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, hist, begin_bit, passes);
+    note_launch();
     k_sort_offs<<<passes, kRadix, 0, s>>>(hist);
+    note_launch();
     const size_t smem = sizeof(SortSmem);
     static bool attr_set = false;
     static int per_sm = 1;
@@ -249,6 +252,7 @@ void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_p
         k_onesweep<<<grid, kSortThreads, smem, s>>>(keys[p & 1], vals[p & 1], keys[(p + 1) & 1], vals[(p + 1) & 1],
                                                     n_ptr, begin_bit + 8 * p, hist + p * kRadix, status + p * words,
                                                     counters + p);
+        note_launch();
     }
 }
 
