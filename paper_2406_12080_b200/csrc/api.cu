@@ -231,11 +231,12 @@ CamParams make_cam(const hs_camera* c) {
 }
 
 // 8-bit passes of the tile-index sort (order.cu): 2 at 1080p (8160 tiles, 13 bits)
-int sort_passes_for(int tiles) {
+int tile_bits(int tiles) {
     int tb = 0;
     while ((1ll << tb) < tiles) ++tb;
-    return std::max(1, (tb + 7) / 8);
+    return std::max(1, tb);
 }
+int sort_passes_for(int tiles) { return (tile_bits(tiles) + 7) / 8; }
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
@@ -334,7 +335,7 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     hs::launch_compact_visible(f->dupcount.as<uint32_t>(), f->dinfo.as<uint4>(), f->n_ptr, f->n_max, zk[0], zv[0],
                                reinterpret_cast<uint64_t*>(sc + L.vis_status),
                                reinterpret_cast<uint32_t*>(sc + L.vis_counter), &ds->n_visible_sorted, s);
-    hs::launch_radix_sort(zk, zv, &ds->n_visible_sorted, f->n_max, 0, 4,
+    hs::launch_radix_sort(zk, zv, &ds->n_visible_sorted, f->n_max, 0, 4, 32,
                           reinterpret_cast<uint32_t*>(sc + L.depth_sort), s);
     const uint32_t* ids = zv[0];  // 4 passes: result back in buffer 0
     // (tile, splat) pairs in depth order, then a stable sort by tile (render.hpp:273-294)
@@ -350,7 +351,8 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
         hs::launch_make_keys(kb[0], vb[0], f->dinfo.as<uint4>(), &ds->sort_n, f->cap_dup, f->dupk.as<uint64_t>(), s);
         HS_CUDA(ctx, cudaMemcpyAsync(f->dupv.p, f->vals[0].p, f->cap_dup * 4, cudaMemcpyDeviceToDevice, s));
     }
-    hs::launch_radix_sort(kb, vb, &ds->sort_n, f->cap_dup, 8, f->passes, reinterpret_cast<uint32_t*>(sc + L.tile_sort),
+    hs::launch_radix_sort(kb, vb, &ds->sort_n, f->cap_dup, 8, f->passes, tile_bits(cp.tiles_x * cp.tiles_y),
+                          reinterpret_cast<uint32_t*>(sc + L.tile_sort),
                           s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[3], s));
     const int fin = f->passes & 1;

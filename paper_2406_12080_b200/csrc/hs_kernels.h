@@ -56,6 +56,6 @@ void launch_make_keys(const uint32_t* tiles, const uint32_t* ids, const uint4* d
 uint64_t sort_status_words(uint64_t n_max);
 uint64_t sort_scratch_words(uint64_t n_max, int passes);
 void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_ptr, uint64_t n_max, int begin_bit,
-                       int passes, uint32_t* scratch, cudaStream_t s);
+                       int passes, int key_bits, uint32_t* scratch, cudaStream_t s);
 
 }  // namespace hs

@@ -3,7 +3,7 @@
 //   k_sort_hist   one read of the keys -> 256-bin histograms of every pass
 //   k_sort_offs   exclusive scan of each pass histogram -> digit bases
 //   k_onesweep    per 8-bit pass: 4096-key tiles (256 threads x 16 keys);
-//                 warp-level ranking with __match_any_sync, per-digit
+//                 warp-level ranking with bit-sliced ballots, per-digit
 //                 decoupled look-back across tiles, local reorder in shared
 //                 memory, coalesced scatter.
 // Stability: within a warp keys are ranked in (item, lane) order, warps in
@@ -25,19 +25,77 @@ constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys
 constexpr int kRadix = 256;
 constexpr uint32_t kFlagAgg32 = 1u << 30, kFlagInc32 = 2u << 30, kValMask32 = (1u << 30) - 1;
 
+// Digit histograms of every pass from one read of the keys (uint4 loads),
+// counted in per-warp shared histograms (less same-address contention on the
+// clustered tile keys), merged per block, then one global atomic per bin.
 __global__ void __launch_bounds__(256) k_sort_hist(const uint32_t* __restrict__ keys, const uint64_t* __restrict__ n_ptr,
                                                    uint32_t* __restrict__ hist, int begin_bit, int passes) {
-    __shared__ uint32_t s_hist[4 * kRadix];
+    __shared__ uint32_t s_hist[8][4 * kRadix];
     const uint64_t n = *n_ptr;
-    for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) s_hist[i] = 0;
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 8 * 4 * kRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0;
     __syncthreads();
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t k = keys[i] >> begin_bit;
-        for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p * kRadix + ((k >> (8 * p)) & 0xff)], 1u);
+    uint32_t* h = s_hist[warp];
+    const uint64_t n4 = n / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    auto count = [&](uint32_t key) {
+        const uint32_t k = key >> begin_bit;
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p * kRadix + ((k >> (8 * p)) & 0xff)], 1u);
+    };
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const uint4 q = reinterpret_cast<const uint4*>(keys)[i];
+        count(q.x);
+        count(q.y);
+        count(q.z);
+        count(q.w);
+    }
+    for (uint64_t i = 4 * n4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) count(keys[i]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) c += s_hist[w][i];
+        if (c) atomicAdd(&hist[i], c);
+    }
+}
+
+// Histograms for short keys (key_bits <= 13, e.g. tile indices): one shared
+// atomic per key on the full 2^key_bits-bin histogram -- spread over thousands
+// of bins instead of 256 per pass -- folded into the per-pass digit
+// histograms at the end.
+constexpr int kDirectBitsMax = 13;
+__global__ void __launch_bounds__(256) k_sort_hist_direct(const uint32_t* __restrict__ keys,
+                                                          const uint64_t* __restrict__ n_ptr,
+                                                          uint32_t* __restrict__ hist, int begin_bit, int key_bits,
+                                                          int passes) {
+    __shared__ uint32_t s_bins[1 << kDirectBitsMax];
+    __shared__ uint32_t s_pass[4 * kRadix];
+    const uint64_t n = *n_ptr;
+    const int nb = 1 << key_bits;
+    const uint32_t mask = (uint32_t)nb - 1u;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) s_bins[i] = 0;
+    for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) s_pass[i] = 0;
+    __syncthreads();
+    const uint64_t n4 = n / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const uint4 q = reinterpret_cast<const uint4*>(keys)[i];
+        atomicAdd(&s_bins[(q.x >> begin_bit) & mask], 1u);
+        atomicAdd(&s_bins[(q.y >> begin_bit) & mask], 1u);
+        atomicAdd(&s_bins[(q.z >> begin_bit) & mask], 1u);
+        atomicAdd(&s_bins[(q.w >> begin_bit) & mask], 1u);
+    }
+    for (uint64_t i = 4 * n4 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        atomicAdd(&s_bins[(keys[i] >> begin_bit) & mask], 1u);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        const uint32_t c = s_bins[b];
+        if (c)
+            for (int p = 0; p < passes; ++p) atomicAdd(&s_pass[p * kRadix + ((b >> (8 * p)) & 0xff)], c);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x)
-        if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
+        if (s_pass[i]) atomicAdd(&hist[i], s_pass[i]);
 }
 
 __global__ void k_sort_offs(uint32_t* hist) {
@@ -100,7 +158,8 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const uint32_t* __
         const uint32_t tcount = (n - tbase) < (uint64_t)kSortTile ? (uint32_t)(n - tbase) : (uint32_t)kSortTile;
         const uint64_t wbase = tbase + (uint64_t)warp * (32 * kSortItems);
 
-        uint32_t k[kSortItems], v[kSortItems];
+        uint32_t k[kSortItems];
+        uint32_t v[kSortItems];
         uint16_t rank[kSortItems];
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
@@ -109,18 +168,24 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const uint32_t* __
             k[it] = valid ? keys_in[idx] : 0u;
             v[it] = valid ? vals_in[idx] : 0u;
         }
-        // Warp ranking: the lowest lane of each digit group bumps the warp's digit
-        // counter with one shared atomic (program order keeps items in order) and
-        // broadcasts the old count; items are independent, so their latencies overlap.
+        // Warp ranking: lanes holding the same digit are found with eight bit-sliced
+        // ballots (cheaper than match.any here); the lowest lane of each digit group
+        // bumps the warp's digit counter with one shared atomic (program order keeps
+        // items in order) and broadcasts the old count.
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
             const bool valid = wbase + it * 32 + lane < n;
-            const uint32_t d = valid ? ((k[it] >> shift) & 0xff) : 0x100u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const uint32_t d = (k[it] >> shift) & 0xff;
+            uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+                peers &= ((d >> b) & 1u) ? bal : ~bal;
+            }
             const int leader = __ffs(peers) - 1;
             uint32_t old = 0;
             if (valid && lane == leader) old = atomicAdd(&sm.wcnt[warp][d], (uint32_t)__popc(peers));
-            old = __shfl_sync(0xffffffffu, old, leader);
+            old = __shfl_sync(0xffffffffu, old, leader < 0 ? 0 : leader);
             rank[it] = (uint16_t)(old + __popc(peers & lt_mask));
         }
         __syncthreads();
@@ -221,10 +286,12 @@ uint64_t sort_scratch_words(uint64_t n_max, int passes) {
 }
 
 // Sorts bits [begin_bit, begin_bit + 8 * passes) of keys[0]/vals[0] (ping-pong
+// key_bits: significant bits above begin_bit when known (<= 13 selects the
+// direct histogram), 0 otherwise;
 // with keys[1]/vals[1]); the result lands in buffer (passes % 2).  `scratch`
 // holds sort_scratch_words(n_max, passes) u32 and is zeroed here on the device.
 void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_ptr, uint64_t n_max, int begin_bit,
-                       int passes, uint32_t* scratch, cudaStream_t s) {
+                       int passes, int key_bits, uint32_t* scratch, cudaStream_t s) {
     const int sms = sort_sms();
     uint32_t* hist = scratch;                        // passes * 256
     uint32_t* counters = scratch + passes * kRadix;  // passes
@@ -233,8 +300,11 @@ void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_p
     cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * passes * (kRadix + 1), s);
     k_sort_zero<<<sms * 2, 256, 0, s>>>(status, n_ptr, words, passes);
     note_launch();
-    const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)sms * 4));
-    k_sort_hist<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, hist, begin_bit, passes);
+    const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)sms));
+    if (key_bits > 0 && key_bits <= kDirectBitsMax && key_bits <= 8 * passes)
+        k_sort_hist_direct<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, hist, begin_bit, key_bits, passes);
+    else
+        k_sort_hist<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, hist, begin_bit, passes);
     note_launch();
     k_sort_offs<<<passes, kRadix, 0, s>>>(hist);
     note_launch();

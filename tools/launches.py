@@ -7,7 +7,7 @@ h = rows[0]
 ki, vi = h.index("Kernel Name"), h.index("Metric Value")
 data = [(r[ki].split("(")[0].replace("void ", "")[:40], float(r[vi].replace(",", ""))) for r in rows[1:] if len(r) > vi]
 starts = [j for j, (k, v) in enumerate(data) if "k_select_cut" in k]
-fr = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+fr = int(sys.argv[2]) if len(sys.argv) > 2 else len(starts) - 2
 s, e = starts[fr], starts[fr + 1]
 tot = sum(v for _, v in data[s:e])
 for k, v in data[s:e]:
