@@ -3,20 +3,20 @@
 //
 // Work unit = one warp on one 8x4 pixel block of a 16x16 tile (8 blocks per
 // tile).  Warps are persistent and pull (tile, block) tasks from an atomic
-// counter: no CTA-wide barrier, no per-tile load imbalance.  A warp walks its
-// tile's depth-sorted range 32 entries at a time:
-//   1. each lane loads one 64-byte projected record and tests it against the
-//      warp's block — skipped when its alpha provably stays under the 1/255
-//      floor on every pixel of the block (minimum of the conic quadratic over
-//      the block's pixel centres, in double, above the per-splat threshold
-//      k_preprocess stored in p3.y).  A skipped entry is one the reference
-//      `continue`s past at every pixel of the block: results are unchanged;
-//   2. every lane computes its pixel's power for the surviving entries and
-//      marks the ones whose alpha can pass the floor ("live");
-//   3. each lane computes alpha for ITS live entries in a compacted loop.
-//      Alpha does not depend on transmittance, so this expensive part (the
-//      exact expf/powf replicas in double) runs out of order with all lanes
-//      busy instead of once per entry for whichever lanes happen to be live;
+// counter in heavy-tiles-first order (k_tile_order): no CTA-wide barrier, no
+// tail of one long tile.  A warp walks its tile's depth-sorted range 32
+// entries at a time:
+//   1. each lane reads one key; its low byte says which of the tile's blocks the
+//      splat's alpha can reach (k_reach_masks) -- entries that cannot touch this
+//      block are ones the reference `continue`s past at every pixel of it, and
+//      are never staged.  The others' 64-byte records are staged in shared
+//      memory with cp.async, one batch ahead;
+//   2. every lane computes its pixel's power for the staged entries and marks
+//      the ones whose alpha can pass the floor ("live");
+//   3. the live (pixel, entry) pairs of all lanes are compacted into a queue and
+//      their alphas computed 32 at a time with every lane busy.  Alpha does not
+//      depend on transmittance, so this expensive part (the exact expf/powf
+//      replicas in double) runs out of order;
 //   4. the warp composites the entries in depth order (test/accumulate/break),
 //      exactly as the reference's per-pixel loop does.
 // Exact mode: expf / powf are device replicas of the host glibc (hs_libm.cuh),
@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                     const float dx = px - p0.x, dy = py - p0.y;
                     const float power = -0.5f * (p0.z * dx * dx + p1.x * dy * dy) - p0.w * dx * dy;
                     // live iff the alpha can reach the 1/255 floor: m e^power >= 1/255 needs
-                    // power >= -ln(255 m) >= -qthr/2 (qthr carries the margin; *0.5 is exact)
-                    const bool lv = (power <= 0.0f) && (power >= -0.5f * rec[h + k][3].y);
+                    // power >= -ln(255 m) >= p3.y = -qthr/2 (qthr carries the margin)
+                    const bool lv = (power <= 0.0f) && (power >= rec[h + k][3].y);
                     if (lv) {
                         live |= 1u << k;
                         sv[k][lane] = power;
@@ -194,17 +194,19 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                 __syncwarp();
             }
             // 4. composite in depth order, over the entries live for at least one lane
-            //    (an entry no lane can see is a no-op for every pixel of the block)
-            for (uint32_t m = __reduce_or_sync(0xffffffffu, live); m; m &= m - 1) {
-                const int k = __ffs(m) - 1;
-                bool contrib = false;
-                if (!done) {
-                    if ((live >> k) & 1u) {
+            //    (an entry no lane can see is a no-op for every pixel of the block).
+            //    Contributions are collected per lane (cm) and reduced once per half.
+            {
+                uint32_t act = done ? 0u : live, cm = 0;
+                for (uint32_t m = __reduce_or_sync(0xffffffffu, act); m; m &= m - 1) {
+                    const int k = __ffs(m) - 1;
+                    if ((act >> k) & 1u) {
                         const float alpha = sv[k][lane];
                         if (alpha > 0.0f) {
                             const float test = T * (1.0f - alpha);
                             if (test < kTransmittanceEps) {
                                 done = true;
+                                act = 0;
                             } else {
                                 const float4 p2 = rec[h + k][2];
                                 const float wgt = alpha * T;
@@ -213,13 +215,13 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                                 c2 = c2 + p2.z * wgt;
                                 d = d + p2.w * alpha * T;
                                 T = test;
-                                contrib = true;
-                                ++n_contrib;
+                                cm |= 1u << k;
                             }
                         }
                     }
                 }
-                if (__any_sync(0xffffffffu, contrib)) tmask |= 1u << (h + k);
+                n_contrib += __popc(cm);
+                tmask |= __reduce_or_sync(0xffffffffu, cm) << h;
             }
             __syncwarp();
             }

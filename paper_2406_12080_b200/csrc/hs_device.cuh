@@ -43,7 +43,7 @@ constexpr int kAttrVec4 = 16;
 //   p0 = {mean2d.x, mean2d.y, conic0, conic1}
 //   p1 = {conic2, falloff_eff*alpha_scale, parent_falloff_eff*alpha_scale, t}
 //   p2 = {color.r, color.g, color.b, inv_depth}
-//   p3 = {inv_k, qthr (block-cull threshold), 1/conic0, 1/conic2}
+//   p3 = {inv_k, -qthr/2 (power floor of the alpha >= 1/255 test), 1/conic0, 1/conic2}
 struct __align__(16) ProjRec {
     float4 p0, p1, p2, p3;
 };
@@ -113,7 +113,7 @@ __device__ __forceinline__ float interp_weight(float en, float ep, float tau) {
 // edges and 8 row edges instead of 32 edge evaluations from scratch.
 __device__ __forceinline__ uint32_t tile_reach_mask(const float4& p0, const float4& p1, const float4& p3, int px0,
                                                     int py0) {
-    const float qthr = p3.y;
+    const float qthr = -2.0f * p3.y;  // p3.y = -qthr / 2 (exact scalings)
     if (qthr < 0.0f) return 0u;
     const float a = p0.z, b = p0.w, c = p1.x;
     const float b2 = 2.0f * b, sx = -b * p3.w, sy = -b * p3.z;

@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ a
                 qthr = shrink > 0.0 ? __double2float_ru(thr / shrink) : __int_as_float(0x7f800000);
             }
         }
-        rec.p3 = make_float4(1.0f / (float)max(1, K), qthr, 1.0f / con0, 1.0f / con2);
+        rec.p3 = make_float4(1.0f / (float)max(1, K), -0.5f * qthr, 1.0f / con0, 1.0f / con2);  // power floor
         proj[j] = rec;
         dinfo[j] = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16),
                               __float_as_uint(tc[2]), 0u);
