@@ -193,31 +193,29 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                 }
                 __syncwarp();
             }
-            // 4. composite in depth order, over the entries live for at least one lane
-            //    (an entry no lane can see is a no-op for every pixel of the block).
-            //    Contributions are collected per lane (cm) and reduced once per half.
+            // 4. composite in depth order: each lane walks its own live entries (an entry
+            //    not live for a pixel is a no-op there).  Contributions are collected per
+            //    lane (cm) and reduced once per half batch.
             {
                 uint32_t act = done ? 0u : live, cm = 0;
-                for (uint32_t m = __reduce_or_sync(0xffffffffu, act); m; m &= m - 1) {
-                    const int k = __ffs(m) - 1;
-                    if ((act >> k) & 1u) {
-                        const float alpha = sv[k][lane];
-                        if (alpha > 0.0f) {
-                            const float test = T * (1.0f - alpha);
-                            if (test < kTransmittanceEps) {
-                                done = true;
-                                act = 0;
-                            } else {
-                                const float4 p2 = rec[h + k][2];
-                                const float wgt = alpha * T;
-                                c0 = c0 + p2.x * wgt;
-                                c1 = c1 + p2.y * wgt;
-                                c2 = c2 + p2.z * wgt;
-                                d = d + p2.w * alpha * T;
-                                T = test;
-                                cm |= 1u << k;
-                            }
+                while (act) {
+                    const int k = __ffs(act) - 1;
+                    act &= act - 1;
+                    const float alpha = sv[k][lane];
+                    if (alpha > 0.0f) {
+                        const float test = T * (1.0f - alpha);
+                        if (test < kTransmittanceEps) {
+                            done = true;
+                            break;
                         }
+                        const float4 p2 = rec[h + k][2];
+                        const float wgt = alpha * T;
+                        c0 = c0 + p2.x * wgt;
+                        c1 = c1 + p2.y * wgt;
+                        c2 = c2 + p2.z * wgt;
+                        d = d + p2.w * alpha * T;
+                        T = test;
+                        cm |= 1u << k;
                     }
                 }
                 n_contrib += __popc(cm);
