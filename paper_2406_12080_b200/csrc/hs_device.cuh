@@ -60,6 +60,14 @@ struct CamParams {
 static __constant__ uint64_t c_exp2f_tab[32] = HS_EXP2F_TAB_INIT;
 static __constant__ uint64_t c_powf_log2_tab[32] = HS_POWF_LOG2_TAB_INIT;
 
+// 32-byte read-only global load (LDG.E.ENL2.256, sm_100): half the L1 requests
+// of two 16-byte loads for gathers of whole records.  p must be 32-byte aligned.
+__device__ __forceinline__ void ldg256(const float4* p, float4& lo, float4& hi) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+        : "l"(p));
+}
+
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ float smin(float a, float b) { return (b < a) ? b : a; }  // std::min
 __device__ __forceinline__ float smax(float a, float b) { return (a < b) ? b : a; }  // std::max

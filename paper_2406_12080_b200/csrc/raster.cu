@@ -47,7 +47,9 @@ __device__ __forceinline__ void load_splat(const float4* __restrict__ attr, cons
     float* q = s.q;
     float falloff, pfall = 0.0f, t = 1.0f, u = 1.0f, v = 0.0f;
     int K = 1;
-    const float4 g0 = g[0], g1 = g[1], g2 = g[2];
+    float4 g0, g1;
+    ldg256(g, g0, g1);
+    const float4 g2 = g[2];
     bool blend = false;
     {
         if (kFromCut) {
@@ -62,7 +64,9 @@ __device__ __forceinline__ void load_splat(const float4* __restrict__ attr, cons
             }
         }
         if (blend) {
-            const float4 p0 = p[0], p1 = p[1], p2 = p[2];
+            float4 p0, p1;
+            ldg256(p, p0, p1);
+            const float4 p2 = p[2];
             mean[0] = u * g0.x + v * p0.x;
             mean[1] = u * g0.y + v * p0.y;
             mean[2] = u * g0.z + v * p0.z;
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(256) k_assemble(const float4* __restrict__ att
 }
 
 template <bool kFromCut>
-__global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ attr, const uint32_t* __restrict__ cut_node,
+__global__ void __launch_bounds__(256, 4) k_preprocess(const float4* __restrict__ attr, const uint32_t* __restrict__ cut_node,
                                                     const float* __restrict__ cut_t, const uint64_t* __restrict__ n_ptr,
                                                     CamParams cam, ProjRec* __restrict__ proj,
                                                     uint4* __restrict__ dinfo,
@@ -277,21 +281,30 @@ __global__ void __launch_bounds__(256) k_preprocess(const float4* __restrict__ a
             b[14] = kSh3_5 * d2 * (xx - yy);
             b[15] = kSh3_6 * d0 * (xx - 3.0f * yy);
             float c[3] = {0.5f, 0.5f, 0.5f};
+            // SH float4 3..14 of the record, read as 32-byte chunks 1..7
 #pragma unroll
-            for (int qv = 0; qv < 12; ++qv) {
-                const float4 gs = g[3 + qv];
-                float s4[4] = {gs.x, gs.y, gs.z, gs.w};
-                if (blend) {
-                    const float4 ps = p[3 + qv];
-                    s4[0] = u * gs.x + v * ps.x;
-                    s4[1] = u * gs.y + v * ps.y;
-                    s4[2] = u * gs.z + v * ps.z;
-                    s4[3] = u * gs.w + v * ps.w;
-                }
+            for (int ch = 1; ch < 8; ++ch) {
+                float4 gq[2], pq[2];
+                ldg256(g + 2 * ch, gq[0], gq[1]);
+                if (blend) ldg256(p + 2 * ch, pq[0], pq[1]);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int idx = 4 * qv + e;
-                    c[idx % 3] += b[idx / 3] * s4[e];
+                for (int half = 0; half < 2; ++half) {
+                    const int qv = 2 * ch + half - 3;
+                    if (qv < 0 || qv >= 12) continue;
+                    const float4 gs = gq[half];
+                    float s4[4] = {gs.x, gs.y, gs.z, gs.w};
+                    if (blend) {
+                        const float4 ps = pq[half];
+                        s4[0] = u * gs.x + v * ps.x;
+                        s4[1] = u * gs.y + v * ps.y;
+                        s4[2] = u * gs.z + v * ps.z;
+                        s4[3] = u * gs.w + v * ps.w;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int idx = 4 * qv + e;
+                        c[idx % 3] += b[idx / 3] * s4[e];
+                    }
                 }
             }
             col[0] = smax(c[0], 0.0f);
