@@ -94,7 +94,7 @@ struct hs_hierarchy {
     hs_context* ctx = nullptr;
     uint64_t n = 0, leaves = 0;
     uint32_t sh_degree = 3;
-    DBuf cull_a, cull_b, attr;
+    DBuf cull, attr;  // cull: interleaved {cull_a, cull_b} 32-byte records
 };
 
 struct hs_cut {
@@ -443,7 +443,7 @@ hs_status enqueue_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* c
     unsigned char* sc = ctx->cut_scratch.as<unsigned char>();
     HS_CUDA(ctx, cudaMemsetAsync(sc, 0, 64 + words * 8, ctx->stream));
     const CamParams cp = make_cam(cam);
-    hs::launch_select_cut(h->cull_a.as<float4>(), h->cull_b.as<float4>(), h->n, cp, tau,
+    hs::launch_select_cut(h->cull.as<float4>(), h->n, cp, tau,
                           cut->node.as<uint32_t>(), cut->t.as<float>(), cut->alpha.as<float>(),
                           reinterpret_cast<uint64_t*>(sc + 64), reinterpret_cast<uint32_t*>(sc),
                           cut->count.as<uint64_t>(), ctx->stream);
@@ -455,16 +455,16 @@ hs_status enqueue_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* c
 }
 
 // Pack host SoA node arrays [lo, hi) into the device layout (hs_device.cuh).
-void pack_nodes(const hs_node_soa* s, uint64_t lo, uint64_t hi, float4* ca, float4* cb, float4* at) {
+void pack_nodes(const hs_node_soa* s, uint64_t lo, uint64_t hi, float4* cu, float4* at) {
     for (uint64_t i = lo; i < hi; ++i) {
         const uint64_t k = i - lo;
         float4* a = at + 16 * k;
-        ca[k] = make_float4(s->bmin[3 * i], s->bmin[3 * i + 1], s->bmin[3 * i + 2], s->bmax[3 * i]);
+        cu[2 * k] = make_float4(s->bmin[3 * i], s->bmin[3 * i + 1], s->bmin[3 * i + 2], s->bmax[3 * i]);
         float pbits, ccbits, fcbits;
         std::memcpy(&pbits, &s->parent[i], 4);
         std::memcpy(&ccbits, &s->child_count[i], 4);
         std::memcpy(&fcbits, &s->first_child[i], 4);
-        cb[k] = make_float4(s->bmax[3 * i + 1], s->bmax[3 * i + 2], pbits, ccbits);
+        cu[2 * k + 1] = make_float4(s->bmax[3 * i + 1], s->bmax[3 * i + 2], pbits, ccbits);
         a[0] = make_float4(s->mean[3 * i], s->mean[3 * i + 1], s->mean[3 * i + 2], s->falloff[i]);
         a[1] = make_float4(s->scale[3 * i], s->scale[3 * i + 1], s->scale[3 * i + 2], pbits);
         a[2] = make_float4(s->rot_wxyz[4 * i], s->rot_wxyz[4 * i + 1], s->rot_wxyz[4 * i + 2], s->rot_wxyz[4 * i + 3]);
@@ -563,8 +563,7 @@ hs_status hs_hierarchy_upload(hs_context* ctx, const hs_node_soa* nodes, uint64_
         return s;
     };
     cudaError_t e;
-    if ((e = h->cull_a.ensure(n * 16)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc cull_a"));
-    if ((e = h->cull_b.ensure(n * 16)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc cull_b"));
+    if ((e = h->cull.ensure(n * 32)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc cull records"));
     if ((e = h->attr.ensure(n * 256)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc attributes"));
     const uint64_t chunk = 1 << 18;
     const size_t stage_bytes = chunk * (16 + 16 + 256);
@@ -582,17 +581,15 @@ hs_status hs_hierarchy_upload(hs_context* ctx, const hs_node_soa* nodes, uint64_
     for (uint64_t lo = 0; lo < n; lo += chunk, b ^= 1) {
         const uint64_t hi = std::min(n, lo + chunk), m = hi - lo;
         cudaEventSynchronize(evs[b]);
-        float4* ca = reinterpret_cast<float4*>(stage[b]);
-        float4* cb = ca + chunk;
-        float4* at = cb + chunk;
-        pack_nodes(nodes, lo, hi, ca, cb, at);
+        float4* cu = reinterpret_cast<float4*>(stage[b]);
+        float4* at = cu + 2 * chunk;
+        pack_nodes(nodes, lo, hi, cu, at);
         for (uint64_t i = lo; i < hi; ++i) leaves += nodes->child_count[i] == 0;
-        cudaMemcpyAsync(h->cull_a.as<float4>() + lo, ca, m * 16, cudaMemcpyHostToDevice, ctx->stream);
-        cudaMemcpyAsync(h->cull_b.as<float4>() + lo, cb, m * 16, cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemcpyAsync(h->cull.as<float4>() + 2 * lo, cu, m * 32, cudaMemcpyHostToDevice, ctx->stream);
         cudaMemcpyAsync(h->attr.as<float4>() + 16 * lo, at, m * 256, cudaMemcpyHostToDevice, ctx->stream);
         cudaEventRecord(evs[b], ctx->stream);
     }
-    hs::launch_child_alpha(h->attr.as<float4>(), h->cull_b.as<float4>(), n, ctx->stream);
+    hs::launch_child_alpha(h->attr.as<float4>(), h->cull.as<float4>(), n, ctx->stream);
     e = cudaStreamSynchronize(ctx->stream);
     cudaEventDestroy(evs[0]);
     cudaEventDestroy(evs[1]);

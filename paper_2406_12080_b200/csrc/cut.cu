@@ -32,8 +32,8 @@ constexpr int kCutTile = kCutThreads * kCutItems;
 
 // Per-node camera-independent part of transition_alpha (lod.hpp:41-45): the
 // alpha a child of node p receives depends only on p's falloff and child count,
-// so it is computed once at upload into cull_b[p].w (leaves: kLeafMark).
-__global__ void __launch_bounds__(256) k_child_alpha(const float4* __restrict__ attr, float4* __restrict__ cull_b,
+// so it is computed once at upload into the cull record (cull[2p+1].w; leaves: kLeafMark).
+__global__ void __launch_bounds__(256) k_child_alpha(const float4* __restrict__ attr, float4* __restrict__ cull,
                                                      uint64_t n) {
     __shared__ uint64_t s_exp_tab[32];
     __shared__ uint64_t s_log_tab[32];
@@ -51,12 +51,11 @@ __global__ void __launch_bounds__(256) k_child_alpha(const float4* __restrict__ 
             bits = __float_as_uint(1.0f - hs_libm::powf_glibc(1.0f - aa, 1.0f / (float)(int)k, s_log_tab, s_exp_tab));
             if (bits == kLeafMark) bits = 0x7FFFFFFFu;  // a NaN stays a NaN, never the leaf mark
         }
-        cull_b[i].w = __uint_as_float(bits);
+        cull[2 * i + 1].w = __uint_as_float(bits);
     }
 }
 
-__global__ void __launch_bounds__(kCutThreads, 6) k_select_cut(const float4* __restrict__ cull_a,
-                                                            const float4* __restrict__ cull_b, uint64_t n,
+__global__ void __launch_bounds__(kCutThreads, 6) k_select_cut(const float4* __restrict__ cull, uint64_t n,
                                                             CamParams cam, float tau, uint32_t* __restrict__ out_node,
                                                             float* __restrict__ out_t, float* __restrict__ out_alpha,
                                                             uint64_t* status, uint32_t* tile_counter,
@@ -82,8 +81,8 @@ __global__ void __launch_bounds__(kCutThreads, 6) k_select_cut(const float4* __r
         par[k] = kNoNode;
         eps[k] = 0.0f;
         if (i < n) {
-            const float4 a = cull_a[i];
-            const float4 b = cull_b[i];
+            float4 a, b;
+            ldg256(cull + 2 * i, a, b);
             const uint32_t parent = __float_as_uint(b.z);
             eps[k] = granularity(a.x, a.y, a.z, a.w, b.x, b.y, cam);
             if (eps[k] <= tau || __float_as_uint(b.w) == kLeafMark) {  // fine enough, or a leaf (lod.hpp:64-65)
@@ -101,8 +100,8 @@ __global__ void __launch_bounds__(kCutThreads, 6) k_select_cut(const float4* __r
         tv[k] = 1.0f;
         av[k] = 0.0f;
         if (need & (1u << k)) {
-            const float4 pa = cull_a[par[k]];
-            const float4 pb = cull_b[par[k]];
+            float4 pa, pb;
+            ldg256(cull + 2 * (uint64_t)par[k], pa, pb);
             const float ep = granularity(pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, cam);
             if (ep > tau) {  // parent not yet fine enough (lod.hpp:67-69)
                 sel_mask |= 1u << k;
@@ -159,17 +158,17 @@ __global__ void __launch_bounds__(kCutThreads, 6) k_select_cut(const float4* __r
     }
 }
 
-void launch_child_alpha(const float4* attr, float4* cull_b, uint64_t n, cudaStream_t stream) {
+void launch_child_alpha(const float4* attr, float4* cull, uint64_t n, cudaStream_t stream) {
     const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148 * 16);
-    k_child_alpha<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, stream>>>(attr, cull_b, n);
+    k_child_alpha<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, stream>>>(attr, cull, n);
     note_launch();
 }
 
-void launch_select_cut(const float4* cull_a, const float4* cull_b, uint64_t n, const CamParams& cam, float tau,
+void launch_select_cut(const float4* cull, uint64_t n, const CamParams& cam, float tau,
                        uint32_t* out_node, float* out_t, float* out_alpha, uint64_t* status, uint32_t* tile_counter,
                        uint64_t* count_out, cudaStream_t stream) {
     const uint64_t tiles = (n + kCutTile - 1) / kCutTile;
-    k_select_cut<<<(unsigned)tiles, kCutThreads, 0, stream>>>(cull_a, cull_b, n, cam, tau, out_node, out_t, out_alpha,
+    k_select_cut<<<(unsigned)tiles, kCutThreads, 0, stream>>>(cull, n, cam, tau, out_node, out_t, out_alpha,
                                                               status, tile_counter, count_out);
     note_launch();
 }

@@ -22,12 +22,13 @@ constexpr float kTransmittanceEps = 1e-4f;      // math.hpp:30
 constexpr float kDilation2d = 0.3f;             // math.hpp:31
 constexpr float kNearPlane = 0.01f;             // math.hpp:32
 constexpr uint32_t kNoNode = 0xFFFFFFFFu;       // model.hpp:15
-constexpr uint32_t kLeafMark = 0xFFFFFFFFu;     // cull_b[i].w of a leaf
+constexpr uint32_t kLeafMark = 0xFFFFFFFFu;     // cull[2i+1].w of a leaf
 
 // ------------------------------------------------------------------ layout
 // Hierarchy in HBM (reference node order, structure of arrays):
-//   cull_a[i] = {min.x, min.y, min.z, max.x}            16 B
-//   cull_b[i] = {max.y, max.z, bits(parent), child_alpha}   16 B
+//   cull[2i]     = {min.x, min.y, min.z, max.x}                  16 B
+//   cull[2i + 1] = {max.y, max.z, bits(parent), child_alpha}      16 B
+//     (one 32-byte record per node, read with a single LDG.256)
 //     child_alpha = transition alpha node i hands its children (k_child_alpha),
 //     bits kLeafMark for a leaf
 //   attr[16*i + 0] = {mean.xyz, falloff}

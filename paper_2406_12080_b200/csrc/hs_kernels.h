@@ -15,11 +15,11 @@ struct CamParams;
 struct ProjRec;
 
 // cut.cu
-void launch_select_cut(const float4* cull_a, const float4* cull_b, uint64_t n, const CamParams& cam, float tau,
+void launch_select_cut(const float4* cull, uint64_t n, const CamParams& cam, float tau,
                        uint32_t* out_node, float* out_t, float* out_alpha, uint64_t* status, uint32_t* tile_counter,
                        uint64_t* count_out, cudaStream_t stream);
 void launch_copy_words(const void* src, void* dst, size_t bytes, cudaStream_t s);  // bytes % 8 == 0
-void launch_child_alpha(const float4* attr, float4* cull_b, uint64_t n, cudaStream_t stream);
+void launch_child_alpha(const float4* attr, float4* cull, uint64_t n, cudaStream_t stream);
 uint64_t select_cut_status_words(uint64_t n);
 
 // raster.cu
