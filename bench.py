@@ -40,6 +40,25 @@ def peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+# kernels behind each HBM-bound stage (for the per-stage ncu DRAM traffic)
+STAGE_KERNELS = {"cut": ("k_select_cut",), "preprocess": ("k_preprocess<1>",),
+                 "duplicate+sort": ("k_compact_visible", "k_sort_hist", "k_dup_offsets", "k_duplicate_sorted",
+                                    "k_reach_masks", "k_sort_hist_direct")}
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes per kernel from the newest committed ncu --set full capture
+    (profiles/r*_traffic_v*.json, written by tools/ncu_traffic.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic_v*.json")),
+                   key=lambda f: int(f.rsplit("_v", 1)[1].split(".")[0]))
+    if not files:
+        return {}, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    return d.get("kernels", {}), os.path.relpath(files[-1], ROOT)
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -189,13 +208,20 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    t0 = time.perf_counter()
-    h = scenes.hierarchy(cfg)
-    gen_s = time.perf_counter() - t0
     r = hs.Renderer(local, exact=(args.mode == "exact"))
     t0 = time.perf_counter()
-    dh = r.upload(h, validate=False)
-    upload_s = time.perf_counter() - t0
+    if cfg.name.startswith("c5"):
+        # 16 chunks + skybox generated one at a time and consolidated on the device
+        # (the 58 GB hierarchy never exists on the host)
+        h = None
+        dh = scenes.multichunk(r, cfg.leaves)
+        gen_s, upload_s = time.perf_counter() - t0, 0.0
+    else:
+        h = scenes.hierarchy(cfg)
+        gen_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        dh = r.upload(h, validate=False)
+        upload_s = time.perf_counter() - t0
     L = N.lib()
     first, count = frames_for_rank(rank, world, args.steps, args.warmup)
     cams = scenes.trajectory(cfg, count, first=first)
@@ -233,6 +259,29 @@ def main():
     ms_total = max_over_ranks(ms_local)
     value = world * len(timed) / (ms_total / 1e3)
 
+    # ---- reference cadence (bench.hpp:70-84): cut refreshed on even frames, reused on odd ones
+    r.set_async(True)
+    barrier()
+    torch.cuda.synchronize()
+    r.synchronize()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for i, c in enumerate(timed):
+        if i % 2 == 0:
+            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, None), r.ctx)
+        else:
+            hs._check(L.hs_render_cut(r.ctx, dh.handle, r._cut, c, r._frame, None), r.ctx)
+    e3.record(stream)
+    e3.synchronize()
+    r.synchronize()
+    barrier()
+    hs._check(L.hs_frame_wait(r.ctx, r._frame), r.ctx)
+    r.set_async(False)
+    cad_ms = max_over_ranks(e2.elapsed_time(e3))
+    cadence = {"value": world * len(timed) / (cad_ms / 1e3), "unit": UNIT, "ms_per_step": cad_ms / len(timed),
+               "what": "bench_path cadence: select_cut on even frames only (bench.hpp:70-84), same frames"}
+
     # ---- stage breakdown + roofline inputs: the same frames, per-stage CUDA events
     st = hs.StageTimes()
     infos = []
@@ -250,6 +299,7 @@ def main():
     C_, V_, D_ = mean("n_splats"), mean("n_visible"), mean("n_duplicates")
     NE, NC = mean("n_eval"), mean("n_contrib")
     nodes = dh.n
+    W, H = cfg.width, cfg.height
     pk, pk_kind = peaks()
     hbm = pk.get("hbm_gbs", 6450.9)
     # algorithmic bytes per frame
@@ -274,11 +324,19 @@ def main():
     fp32_peak = props.multi_processor_count * 128 * 2 * sm_mhz * 1e6 / 1e12
     blend_flops = 12 * NE + 24 * NC
     blend_tf = blend_flops / (stage_ms["alpha_blend"] * 1e-3) / 1e12
+    traffic, traffic_src = ncu_traffic()
+    blend_key = "k_blend<0>" if args.mode == "exact" else "k_blend<1>"
     roofline = {"bound": "fp32", "kernel": "k_blend", "achieved": blend_tf, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": blend_tf / fp32_peak, "traffic": None,
+                "frac": blend_tf / fp32_peak,
+                "traffic": traffic.get(blend_key, {}).get("dram_bytes"),
+                "traffic_source": traffic_src,
+                "algorithmic_bytes": 8 * D_ + 64 * D_ + 20 * W * H,
                 "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz "
                                f"(no measured FP32 peak in MEASURED_PEAKS.json)",
-                "hbm_stages": {k: {"gbs": v.get("gbs"), "frac": (v["gbs"] / hbm) if v.get("gbs") else None}
+                "hbm_stages": {k: {"gbs": v.get("gbs"), "frac": (v["gbs"] / hbm) if v.get("gbs") else None,
+                                   "bytes": v.get("bytes"),
+                                   "traffic": sum(traffic.get(kk, {}).get("dram_bytes", 0.0)
+                                                  for kk in STAGE_KERNELS.get(k, ())) or None}
                                for k, v in stages.items() if v.get("bound") == "hbm"},
                 "hbm_peak_gbs": hbm, "hbm_peak_source": pk_kind}
 
@@ -286,7 +344,6 @@ def main():
     # the whole RenderOutput (colour, inverse depth, transmittance) out to pinned host
     # memory every frame.  Two frame objects: frame i's read-back (copy stream) overlaps
     # frame i+1's kernels; a frame object is re-rendered only after its read-back landed.
-    W, H = cfg.width, cfg.height
     f32 = N.C.POINTER(N.C.c_float)
     frames = [r._frame, N.C.c_void_p()]
     hs._check(L.hs_frame_create(r.ctx, N.C.byref(frames[1])), r.ctx)
@@ -318,8 +375,11 @@ def main():
            "pipelining": "2 frame objects; read-back of frame i on a copy stream overlaps frame i+1"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and h is not None:
         cpu = cpu_baseline(cfg, h)
+    elif h is None:
+        cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+               "sample": "not run: the oracle's 304 B/node AoS copy of 2e8 nodes exceeds host RAM"}
 
     if rank == 0:
         line = {
@@ -329,11 +389,12 @@ def main():
             "config": {"workload": cfg.name, "leaves": cfg.leaves, "nodes": nodes, "width": W, "height": H,
                        "tau": cfg.tau, "blend_mode": args.mode, "frames": f"trajectory frames {first}.. per rank",
                        "parallelism": f"view-parallel x{world} (hierarchy replicated)",
-                       "l2": "inputs larger than L2 (hierarchy 5.8 GB resident; no flush needed)"},
+                       "l2": f"inputs larger than L2 (hierarchy {nodes * 288 / 1e9:.1f} GB resident; no flush needed)"},
             "roofline": roofline,
             "stages_ms": stage_ms,
             "stages": stages,
             "per_frame": {"cut_entries": C_, "visible": V_, "duplicates": D_, "n_eval": NE, "n_contrib": NC},
+            "reference_cadence": cadence,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

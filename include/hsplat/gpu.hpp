@@ -472,7 +472,10 @@ inline BenchReport bench_path(const Hierarchy& h, const CameraPath& path, float 
     BenchReport rep;
     rep.leaf_count = h.leaf_count();
     rep.tau = tau;
-    std::vector<std::uint32_t> prev, cur;
+    // transferred = |cut \ previous cut| (bench.hpp:79-82), counted on the device
+    hs_transfer_tracker* tr = nullptr;
+    c.check(hs_transfer_tracker_create(c.ctx(), dh, &tr));
+    std::unique_ptr<hs_transfer_tracker, void (*)(hs_transfer_tracker*)> tracker(tr, hs_transfer_tracker_destroy);
     std::size_t cut_size = 0;
     for (std::size_t i = 0; i < path.cameras.size(); ++i) {
         FrameStats fs;
@@ -480,16 +483,11 @@ inline BenchReport bench_path(const Hierarchy& h, const CameraPath& path, float 
         hs_stage_times st{};
         if (i % 2 == 0) {
             c.check(hs_render_hierarchy(c.ctx(), dh, &cc, tau, c.cut(), c.frame(), &st));
-            const auto cut = gpu::download_cut(c, c.cut());
-            cut_size = cut.size();
-            cur.clear();
-            for (const auto& e : cut) cur.push_back(e.node);  // ascending node order
-            std::size_t j = 0;
-            for (std::uint32_t n : cur) {  // |cur \ prev| by merge of two sorted lists
-                while (j < prev.size() && prev[j] < n) ++j;
-                fs.transferred += (j == prev.size() || prev[j] != n);
-            }
-            prev.swap(cur);
+            std::uint64_t n = 0, fresh = 0;
+            c.check(hs_cut_size(c.ctx(), c.cut(), &n));
+            c.check(hs_transfer_count(c.ctx(), tracker.get(), c.cut(), &fresh));
+            cut_size = n;
+            fs.transferred = fresh;
         } else {
             c.check(hs_render_cut(c.ctx(), dh, c.cut(), &cc, c.frame(), &st));
         }

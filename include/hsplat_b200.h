@@ -140,6 +140,7 @@ typedef struct hs_context hs_context;
 typedef struct hs_hierarchy hs_hierarchy;
 typedef struct hs_cut hs_cut;
 typedef struct hs_frame hs_frame;
+typedef struct hs_transfer_tracker hs_transfer_tracker;
 
 /* ------------------------------------------------------------ context */
 const char* hs_status_name(hs_status s);
@@ -163,6 +164,15 @@ hs_status hs_hierarchy_upload(hs_context* ctx, const hs_node_soa* nodes, uint64_
                               int validate, hs_hierarchy** out);
 /* replaces: read_hierarchy (io.hpp:375-408) */
 hs_status hs_hierarchy_load_h3dg(hs_context* ctx, const char* path, hs_hierarchy** out);
+/* replaces: consolidate's global assembly (scene.hpp:228-316) for chunk
+ * hierarchies already on the device (no cross-chunk backdrop pruning: every
+ * part's leaves belong to it).  The k parts (chunk trees, then the skybox tree)
+ * hang under one merged root (merge.hpp:86-118; k == 1: the part itself) and
+ * the result is serialised breadth-first (children contiguous, parent < child)
+ * into a new device hierarchy.  The parts stay valid; k <= 64. */
+hs_status hs_hierarchy_assemble(hs_context* ctx, const hs_hierarchy* const* parts, uint32_t k, hs_hierarchy** out);
+/* device hierarchy -> host SoA (for write_hierarchy, io.hpp:350-373, and parity) */
+hs_status hs_hierarchy_download(hs_context* ctx, const hs_hierarchy* h, const hs_node_soa_out* out);
 void hs_hierarchy_destroy(hs_hierarchy* h);
 uint64_t hs_hierarchy_node_count(const hs_hierarchy* h);
 uint64_t hs_hierarchy_leaf_count(const hs_hierarchy* h); /* Hierarchy::leaf_count (model.hpp:108-112) */
@@ -183,6 +193,13 @@ hs_status hs_cut_upload(hs_context* ctx, const hs_hierarchy* h, const uint32_t* 
 /* replaces: cut_render_splats (lod.hpp:148-153) — the interpolated RenderSplats
  * the fused preprocess computes, downloaded for inspection */
 hs_status hs_cut_render_splats(hs_context* ctx, const hs_hierarchy* h, const hs_cut* cut, hs_splat_soa_out* out);
+/* replaces: bench_path's cut-churn count (bench.hpp:79-82, std::set difference):
+ * `transferred` = nodes of `cut` absent from the cut previously passed to this
+ * tracker (all of them for the first).  Device-resident per-node state (4 B/node);
+ * the call enqueues one kernel and waits for its 8-byte result. */
+hs_status hs_transfer_tracker_create(hs_context* ctx, const hs_hierarchy* h, hs_transfer_tracker** out);
+void hs_transfer_tracker_destroy(hs_transfer_tracker* t);
+hs_status hs_transfer_count(hs_context* ctx, hs_transfer_tracker* t, const hs_cut* cut, uint64_t* transferred);
 
 /* ------------------------------------------------------------ frames */
 hs_status hs_frame_create(hs_context* ctx, hs_frame** out);
@@ -231,6 +248,13 @@ hs_status hs_frame_debug(hs_context* ctx, hs_frame* f, uint64_t* tile_start, uin
 uint64_t hs_synth_node_count(uint64_t leaves);
 float hs_synth_scene_side(uint64_t leaves);
 hs_status hs_synth_city(uint64_t leaves, uint64_t seed, int threads, const hs_node_soa_out* out);
+/* one chunk of a multi-chunk scene: the same city statistics centred at (cx, 0, cz) */
+hs_status hs_synth_city_chunk(uint64_t leaves, uint64_t seed, float cx, float cz, int threads,
+                              const hs_node_soa_out* out);
+/* make_skybox (scene.hpp:111-137) + build_bvh: `count` mid-gray splats on a shell
+ * 5 scene diameters around `centroid` */
+hs_status hs_synth_skybox(uint64_t count, float scene_diameter, uint64_t seed, const float centroid[3], int threads,
+                          const hs_node_soa_out* out);
 /* build_bvh (build.hpp:73-149) over caller leaves (mean 3N, scale 3N, rotation
  * wxyz 4N, falloff N, sh 48N) into arrays sized 2N-1 (test fixtures) */
 hs_status hs_build_bvh(const float* mean, const float* scale, const float* rot_wxyz, const float* falloff,

@@ -307,3 +307,55 @@ def expf(x: float) -> float:
 
 def powf(x: float, y: float) -> float:
     return float(lib().or_powf(x, y))
+
+
+def consolidate_bfs(parts, root=None):
+    """consolidate's breadth-first serialisation (scene.hpp:281-316) of a forest
+    in numpy, for forests without cross-chunk pruning.  `parts` are host
+    Hierarchy objects (root 0, children contiguous); `root` is None for a single
+    part, else a dict with the merged root's fields (mean, scale, rot_wxyz,
+    falloff, sh, bmin, bmax) and the re-matched forest roots' `kid_scale` and
+    `kid_rot` (k x 3, k x 4).  Returns a dict of SoA arrays in the serialised
+    order: children contiguous, parent index < child index."""
+    k = len(parts)
+    fields = ("bmin", "bmax", "mean", "scale", "rot_wxyz", "falloff", "sh")
+    off = 1 if k > 1 else 0  # the merged global root takes index 0
+    # BFS level by level: a level is, in order, every previous-level node's child range
+    level = [(p, np.zeros(1, np.int64), np.full(1, 0 if k > 1 else 0xFFFFFFFF, np.int64)) for p in range(k)]
+    order_p, order_j, order_par = [], [], []
+    pos = off
+    while level:
+        nxt = []
+        for p, j, par in level:
+            h = parts[p]
+            order_p.append(np.full(len(j), p)), order_j.append(j), order_par.append(par)
+            cc = h.child_count[j].astype(np.int64)
+            fc = h.first_child[j].astype(np.int64)
+            kids = np.repeat(fc, cc) + (np.arange(cc.sum()) - np.repeat(np.cumsum(cc) - cc, cc))
+            if len(kids):
+                nxt.append((p, kids, np.repeat(pos + np.arange(len(j)), cc)))
+            pos += len(j)
+        level = nxt
+    P, J, PAR = np.concatenate(order_p), np.concatenate(order_j), np.concatenate(order_par)
+    n = len(P) + off
+    out = {f: np.zeros((n,) + getattr(parts[0], f).shape[1:], np.float32) for f in fields}
+    out["parent"] = np.zeros(n, np.uint32)
+    out["child_count"] = np.zeros(n, np.uint32)
+    for p in range(k):
+        sel = np.flatnonzero(P == p)
+        for f in fields:
+            out[f][off + sel] = getattr(parts[p], f)[J[sel]]
+        out["child_count"][off + sel] = parts[p].child_count[J[sel]]
+    out["parent"][off:] = PAR.astype(np.uint32)
+    if k > 1:
+        for f in fields:
+            out[f][0] = root[f]
+        out["parent"][0] = 0xFFFFFFFF
+        out["child_count"][0] = k
+        out["scale"][1:1 + k] = root["kid_scale"]
+        out["rot_wxyz"][1:1 + k] = root["kid_rot"]
+    # children of node i start after the root and all earlier nodes' children
+    cc = out["child_count"].astype(np.int64)
+    first = 1 + np.cumsum(cc) - cc
+    out["first_child"] = np.where(cc > 0, first, 0xFFFFFFFF).astype(np.uint32)
+    return out

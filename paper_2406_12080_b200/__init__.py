@@ -187,6 +187,26 @@ def synth_city(leaves: int, seed: int = 1, threads: int = 0) -> Hierarchy:
     return h
 
 
+def synth_city_chunk(leaves: int, seed: int, cx: float, cz: float, threads: int = 0) -> Hierarchy:
+    """One chunk of a multi-chunk scene: synth_city statistics centred at (cx, 0, cz)."""
+    n = int(N.lib().hs_synth_node_count(leaves))
+    h = Hierarchy.empty(n)
+    _check(N.lib().hs_synth_city_chunk(leaves, seed, float(cx), float(cz), threads, C.byref(h.soa())),
+           what="hs_synth_city_chunk")
+    return h
+
+
+def synth_skybox(count: int, scene_diameter: float, seed: int = 0, centroid=(0.0, 0.0, 0.0),
+                 threads: int = 0) -> Hierarchy:
+    """make_skybox (scene.hpp:111-137) + build_bvh: mid-gray shell 5 diameters out."""
+    n = int(N.lib().hs_synth_node_count(count))
+    h = Hierarchy.empty(n)
+    c = (C.c_float * 3)(*[float(v) for v in centroid])
+    _check(N.lib().hs_synth_skybox(count, float(scene_diameter), seed, c, threads, C.byref(h.soa())),
+           what="hs_synth_skybox")
+    return h
+
+
 def build_bvh(mean, scale, rot_wxyz, falloff, sh, threads: int = 0) -> Hierarchy:
     """build_bvh (build.hpp:73-149): median-split BVH + moment-matched interior nodes."""
     n = len(falloff)
@@ -433,6 +453,35 @@ class DeviceHierarchy:
             pass
 
 
+class TransferTracker:
+    """bench_path's cut-churn count (bench.hpp:79-82) on the device: count(cut)
+    returns how many nodes of the renderer's current cut were absent from the
+    cut passed to the previous count() call (all of them the first time)."""
+
+    def __init__(self, renderer: "Renderer", dh: DeviceHierarchy):
+        self.r = renderer
+        self.dh = dh
+        h = C.c_void_p()
+        _check(N.lib().hs_transfer_tracker_create(renderer.ctx, dh.handle, C.byref(h)), renderer.ctx)
+        self.handle = h
+
+    def count(self, cut_handle=None) -> int:
+        n = C.c_uint64()
+        _check(N.lib().hs_transfer_count(self.r.ctx, self.handle, cut_handle or self.r._cut, C.byref(n)), self.r.ctx)
+        return int(n.value)
+
+    def close(self):
+        if getattr(self, "handle", None) and getattr(self.r, "ctx", None):
+            N.lib().hs_transfer_tracker_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Renderer:
     """One CUDA context (device, stream) running the hot path.  Mirrors the
     reference's free functions as methods; module-level wrappers use
@@ -500,6 +549,23 @@ class Renderer:
         return DeviceHierarchy(self, out, int(N.lib().hs_hierarchy_node_count(out)),
                                int(N.lib().hs_hierarchy_leaf_count(out)))
 
+    def assemble(self, parts) -> DeviceHierarchy:
+        """consolidate's global assembly (scene.hpp:228-316) on the device: the parts
+        (chunk trees, then the skybox) under one merged root, serialised breadth-first."""
+        devs = [self._dev(p) for p in parts]
+        arr = (C.c_void_p * max(1, len(devs)))(*[d.handle for d in devs])
+        out = C.c_void_p()
+        _check(N.lib().hs_hierarchy_assemble(self.ctx, arr, len(devs), C.byref(out)), self.ctx)
+        return DeviceHierarchy(self, out, int(N.lib().hs_hierarchy_node_count(out)),
+                               int(N.lib().hs_hierarchy_leaf_count(out)))
+
+    def download(self, h) -> Hierarchy:
+        """Device hierarchy -> host Hierarchy (reference node order)."""
+        dh = self._dev(h)
+        out = Hierarchy.empty(dh.n)
+        _check(N.lib().hs_hierarchy_download(self.ctx, dh.handle, C.byref(out.soa())), self.ctx)
+        return out
+
     def _dev(self, h) -> DeviceHierarchy:
         if isinstance(h, DeviceHierarchy):
             return h
@@ -524,6 +590,17 @@ class Renderer:
         dh = self._dev(h)
         _check(N.lib().hs_select_cut(self.ctx, dh.handle, C.byref(cam.to_c()), float(tau), self._cut), self.ctx)
         return self._cut_arrays(self._cut)
+
+    def select_cut_device(self, h, cam: CameraModel, tau: float) -> int:
+        """select_cut keeping the entries on the device (the renderer's current cut); returns its size."""
+        dh = self._dev(h)
+        _check(N.lib().hs_select_cut(self.ctx, dh.handle, C.byref(cam.to_c()), float(tau), self._cut), self.ctx)
+        n = C.c_uint64()
+        _check(N.lib().hs_cut_size(self.ctx, self._cut, C.byref(n)), self.ctx)
+        return int(n.value)
+
+    def transfer_tracker(self, h) -> "TransferTracker":
+        return TransferTracker(self, self._dev(h))
 
     def _install_cut(self, dh: DeviceHierarchy, cut: CutEntries):
         node = np.ascontiguousarray(cut.node, np.uint32)
@@ -704,16 +781,16 @@ def bench_path(h, cameras, tau: float, timestamps=None, renderer: Renderer | Non
         raise Error(int(Errc.DimensionMismatch) + 1, "DimensionMismatch: one timestamp per camera")
     dh = r._dev(h)
     rep = BenchReport(leaf_count=dh.leaf_count(), tau=float(tau))
-    prev = np.empty(0, np.uint32)
+    tracker = r.transfer_tracker(dh)  # |cut \ previous cut| on the device
     cut_size = 0
     for i, cam in enumerate(cameras):
         fs = FrameStats()
         if i % 2 == 0:
             out = r.render_hierarchy(dh, cam, tau, stages=fs.stages)
-            cut = r._cut_arrays(r._cut)
-            cut_size = len(cut)
-            fs.transferred = int(np.count_nonzero(~np.isin(cut.node, prev, assume_unique=True)))
-            prev = cut.node
+            n = C.c_uint64()
+            _check(N.lib().hs_cut_size(r.ctx, r._cut, C.byref(n)), r.ctx)
+            cut_size = int(n.value)
+            fs.transferred = tracker.count()
         else:
             out = r.render_cut(dh, cam, stages=fs.stages)
         del out
@@ -725,6 +802,7 @@ def bench_path(h, cameras, tau: float, timestamps=None, renderer: Renderer | Non
         for k in ("cut_expand", "weights", "preprocess", "duplicate", "tile_ranges", "alpha_blend"):
             setattr(rep.total_stages, k, getattr(rep.total_stages, k) + getattr(fs.stages, k))
         rep.frames.append(fs)
+    tracker.close()
     rep.mean_rendered /= len(rep.frames)
     rep.mean_rendered_pct /= len(rep.frames)
     return rep

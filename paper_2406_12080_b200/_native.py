@@ -70,6 +70,8 @@ _SIGS = {
     "hs_hierarchy_upload": (C.c_int, [_vp, C.POINTER(hs_node_soa), C.c_uint64, C.c_uint32, C.c_int,
                                       C.POINTER(_vp)]),
     "hs_hierarchy_load_h3dg": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
+    "hs_hierarchy_assemble": (C.c_int, [_vp, C.POINTER(_vp), C.c_uint32, C.POINTER(_vp)]),
+    "hs_hierarchy_download": (C.c_int, [_vp, _vp, C.POINTER(hs_node_soa)]),
     "hs_hierarchy_destroy": (None, [_vp]),
     "hs_hierarchy_node_count": (C.c_uint64, [_vp]),
     "hs_hierarchy_leaf_count": (C.c_uint64, [_vp]),
@@ -80,6 +82,9 @@ _SIGS = {
     "hs_cut_download": (C.c_int, [_vp, _vp, u32p, f32p, f32p]),
     "hs_cut_upload": (C.c_int, [_vp, _vp, u32p, f32p, f32p, C.c_uint64, _vp]),
     "hs_cut_render_splats": (C.c_int, [_vp, _vp, _vp, C.POINTER(hs_splat_soa)]),
+    "hs_transfer_tracker_create": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
+    "hs_transfer_tracker_destroy": (None, [_vp]),
+    "hs_transfer_count": (C.c_int, [_vp, _vp, _vp, u64p]),
     "hs_frame_create": (C.c_int, [_vp, C.POINTER(_vp)]),
     "hs_frame_destroy": (None, [_vp]),
     "hs_render_hierarchy": (C.c_int, [_vp, _vp, C.POINTER(hs_camera), C.c_float, _vp, _vp,
@@ -99,6 +104,10 @@ _SIGS = {
     "hs_synth_node_count": (C.c_uint64, [C.c_uint64]),
     "hs_synth_scene_side": (C.c_float, [C.c_uint64]),
     "hs_synth_city": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.POINTER(hs_node_soa)]),
+    "hs_synth_city_chunk": (C.c_int, [C.c_uint64, C.c_uint64, C.c_float, C.c_float, C.c_int,
+                                      C.POINTER(hs_node_soa)]),
+    "hs_synth_skybox": (C.c_int, [C.c_uint64, C.c_float, C.c_uint64, C.POINTER(C.c_float), C.c_int,
+                                  C.POINTER(hs_node_soa)]),
     "hs_build_bvh": (C.c_int, [f32p, f32p, f32p, f32p, f32p, C.c_uint64, C.c_int, C.POINTER(hs_node_soa)]),
     "hs_h3dg_read_header":(C.c_int, [C.c_char_p, u64p, C.POINTER(C.c_uint32)]),
     "hs_h3dg_read": (C.c_int, [C.c_char_p, C.POINTER(hs_node_soa), C.c_uint64]),

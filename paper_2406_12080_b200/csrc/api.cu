@@ -111,6 +111,20 @@ struct hs_cut {
     }
 };
 
+struct hs_transfer_tracker {
+    hs_context* ctx = nullptr;
+    const hs_hierarchy* h = nullptr;
+    DBuf epoch, count;
+    uint64_t* h_count = nullptr;      // pinned, mapped
+    uint64_t* h_count_dev = nullptr;  // device alias of h_count
+    uint32_t refresh = 0;             // id of the last refresh counted (0: none yet)
+    cudaEvent_t done = nullptr;
+    ~hs_transfer_tracker() {
+        if (h_count) cudaFreeHost(h_count);
+        if (done) cudaEventDestroy(done);
+    }
+};
+
 struct hs_frame {
     hs_context* ctx = nullptr;
     uint64_t cap_splats = 0, cap_dup = 0;
@@ -601,6 +615,158 @@ hs_status hs_hierarchy_upload(hs_context* ctx, const hs_node_soa* nodes, uint64_
     return HS_OK;
 }
 
+hs_status hs_hierarchy_assemble(hs_context* ctx, const hs_hierarchy* const* parts, uint32_t k, hs_hierarchy** out) {
+    if (!ctx || !parts || !out) return HS_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (k == 0) return set_err(ctx, HS_EMPTY_SCENE, "consolidation removed every splat");  // scene.hpp:261
+    if (k > (uint32_t)hs::kMaxParts) return set_err(ctx, HS_INVALID_ARGUMENT, "at most 64 parts");
+    uint64_t total = k > 1 ? 1 : 0, leaves = 0, widest = k;
+    hs::PartTable pt{};
+    for (uint32_t p = 0; p < k; ++p) {
+        if (!parts[p] || parts[p]->n == 0 || parts[p]->ctx != ctx)
+            return set_err(ctx, HS_INVALID_ARGUMENT, "chunk hierarchy is empty");  // scene.hpp:237
+        pt.cull[p] = parts[p]->cull.as<float4>();
+        pt.attr[p] = parts[p]->attr.as<float4>();
+        total += parts[p]->n;
+        leaves += parts[p]->leaves;
+        widest += parts[p]->n;
+    }
+    if (total >= 0xFFFFFFFFull) return set_err(ctx, HS_INVALID_ARGUMENT, "node indices must fit in 32 bits");
+    cudaSetDevice(ctx->device);
+    auto* h = new hs_hierarchy();
+    h->ctx = ctx;
+    h->n = total;
+    h->leaves = leaves;
+    h->sh_degree = parts[0]->sh_degree;
+    auto fail = [&](hs_status st) {
+        delete h;
+        return st;
+    };
+    cudaError_t e;
+    if ((e = h->cull.ensure(total * 32)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc cull records"));
+    if ((e = h->attr.ensure(total * 256)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc attributes"));
+    // frontier buffers: a level never holds more than all part nodes
+    DBuf fr[2], scratch;
+    if ((e = fr[0].ensure(widest * 16)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc frontier"));
+    if ((e = fr[1].ensure(widest * 16)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc frontier"));
+    const uint64_t words = hs::assemble_status_words(widest);
+    if ((e = scratch.ensure(64 + words * 8)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc scan state"));
+    std::vector<uint4> first(k);
+    std::vector<float> gout(59 * k);
+    if (k > 1) {
+        // the merged global root (scene.hpp:264-279) from the part roots' records
+        std::vector<float> gin(59 * k), bmin(3 * k), bmax(3 * k);
+        for (uint32_t p = 0; p < k; ++p) {
+            float4 a[16], c[2];
+            if ((e = cudaMemcpy(a, pt.attr[p], 256, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+                (e = cudaMemcpy(c, pt.cull[p], 32, cudaMemcpyDeviceToHost)) != cudaSuccess)
+                return fail(cuda_err(ctx, e, "read part roots"));
+            float* g = gin.data() + 59 * p;
+            g[0] = a[0].x, g[1] = a[0].y, g[2] = a[0].z;
+            g[3] = a[1].x, g[4] = a[1].y, g[5] = a[1].z;
+            g[6] = a[2].x, g[7] = a[2].y, g[8] = a[2].z, g[9] = a[2].w;
+            g[10] = a[0].w;
+            std::memcpy(g + 11, &a[3], 48 * 4);
+            bmin[3 * p] = c[0].x, bmin[3 * p + 1] = c[0].y, bmin[3 * p + 2] = c[0].z;
+            bmax[3 * p] = c[0].w, bmax[3 * p + 1] = c[1].x, bmax[3 * p + 2] = c[1].y;
+        }
+        float root[59], rmin[3], rmax[3];
+        hs_merge_root_internal(gin.data(), k, bmin.data(), bmax.data(), root, rmin, rmax, gout.data());
+        float4 rc[2], ra[16];
+        float nob;
+        const uint32_t none = HS_NO_NODE, one = 1;
+        std::memcpy(&nob, &none, 4);
+        float kb, fb;
+        std::memcpy(&kb, &k, 4);
+        std::memcpy(&fb, &one, 4);
+        rc[0] = make_float4(rmin[0], rmin[1], rmin[2], rmax[0]);
+        rc[1] = make_float4(rmax[1], rmax[2], nob, 0.0f);
+        ra[0] = make_float4(root[0], root[1], root[2], root[10]);
+        ra[1] = make_float4(root[3], root[4], root[5], nob);
+        ra[2] = make_float4(root[6], root[7], root[8], root[9]);
+        std::memcpy(&ra[3], root + 11, 48 * 4);
+        ra[15] = make_float4(kb, fb, 0.0f, 0.0f);
+        if ((e = cudaMemcpy(h->cull.p, rc, 32, cudaMemcpyHostToDevice)) != cudaSuccess ||
+            (e = cudaMemcpy(h->attr.p, ra, 256, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return fail(cuda_err(ctx, e, "write root"));
+        for (uint32_t p = 0; p < k; ++p) first[p] = make_uint4(p, 0, 0, 0);  // parent: the root
+    } else {
+        first[0] = make_uint4(0, 0, HS_NO_NODE, 0);
+    }
+    if ((e = cudaMemcpy(fr[0].p, first.data(), 16 * k, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(cuda_err(ctx, e, "frontier"));
+    uint64_t pos = k > 1 ? 1 : 0, n_in = k;
+    int cur = 0;
+    uint64_t* n_next = nullptr;
+    if ((e = cudaMallocHost(&n_next, 8)) != cudaSuccess) return fail(cuda_err(ctx, e, "pinned"));
+    unsigned char* sc = scratch.as<unsigned char>();
+    while (n_in > 0) {
+        cudaMemsetAsync(sc, 0, 64 + hs::assemble_status_words(n_in) * 8, ctx->stream);
+        hs::launch_assemble_level(pt, fr[cur].as<uint4>(), n_in, pos, h->cull.as<float4>(), h->attr.as<float4>(),
+                                  fr[cur ^ 1].as<uint4>(), reinterpret_cast<uint64_t*>(sc + 64),
+                                  reinterpret_cast<uint32_t*>(sc), reinterpret_cast<uint64_t*>(sc + 8), ctx->stream);
+        cudaMemcpyAsync(n_next, sc + 8, 8, cudaMemcpyDeviceToHost, ctx->stream);
+        if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) {
+            cudaFreeHost(n_next);
+            return fail(cuda_err(ctx, e, "assemble level"));
+        }
+        pos += n_in;
+        n_in = *n_next;
+        cur ^= 1;
+        if (pos + n_in > total) break;
+    }
+    cudaFreeHost(n_next);
+    if (pos != total || n_in != 0) return fail(set_err(ctx, HS_INVALID_ARGUMENT, "part hierarchies are not trees"));
+    if (k > 1) {  // forest roots re-matched to the new root's axis convention (scene.hpp:307-313)
+        for (uint32_t p = 0; p < k; ++p) {
+            const float* g = gout.data() + 59 * p;
+            float4* a = h->attr.as<float4>() + (uint64_t)(1 + p) * 16;
+            float4 sc1, q;
+            if ((e = cudaMemcpy(&sc1, a + 1, 16, cudaMemcpyDeviceToHost)) != cudaSuccess)
+                return fail(cuda_err(ctx, e, "patch forest roots"));
+            sc1.x = g[3], sc1.y = g[4], sc1.z = g[5];
+            q = make_float4(g[6], g[7], g[8], g[9]);
+            if ((e = cudaMemcpy(a + 1, &sc1, 16, cudaMemcpyHostToDevice)) != cudaSuccess ||
+                (e = cudaMemcpy(a + 2, &q, 16, cudaMemcpyHostToDevice)) != cudaSuccess)
+                return fail(cuda_err(ctx, e, "patch forest roots"));
+        }
+    }
+    hs::launch_child_alpha(h->attr.as<float4>(), h->cull.as<float4>(), total, ctx->stream);
+    if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) return fail(cuda_err(ctx, e, "assemble"));
+    *out = h;
+    return HS_OK;
+}
+
+hs_status hs_hierarchy_download(hs_context* ctx, const hs_hierarchy* h, const hs_node_soa_out* o) {
+    if (!ctx || !h || !o) return HS_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const uint64_t chunk = 1 << 18;
+    std::vector<float4> cu(2 * chunk), at(16 * chunk);
+    for (uint64_t lo = 0; lo < h->n; lo += chunk) {
+        const uint64_t m = std::min(chunk, h->n - lo);
+        HS_CUDA(ctx, cudaMemcpy(cu.data(), h->cull.as<float4>() + 2 * lo, m * 32, cudaMemcpyDeviceToHost));
+        HS_CUDA(ctx, cudaMemcpy(at.data(), h->attr.as<float4>() + 16 * lo, m * 256, cudaMemcpyDeviceToHost));
+        for (uint64_t k = 0; k < m; ++k) {
+            const uint64_t i = lo + k;
+            const float4 a = cu[2 * k], b = cu[2 * k + 1];
+            const float4* g = &at[16 * k];
+            std::memcpy(&o->parent[i], &b.z, 4);
+            std::memcpy(&o->child_count[i], &g[15].x, 4);
+            std::memcpy(&o->first_child[i], &g[15].y, 4);
+            o->bmin[3 * i] = a.x, o->bmin[3 * i + 1] = a.y, o->bmin[3 * i + 2] = a.z;
+            o->bmax[3 * i] = a.w, o->bmax[3 * i + 1] = b.x, o->bmax[3 * i + 2] = b.y;
+            o->mean[3 * i] = g[0].x, o->mean[3 * i + 1] = g[0].y, o->mean[3 * i + 2] = g[0].z;
+            o->falloff[i] = g[0].w;
+            o->scale[3 * i] = g[1].x, o->scale[3 * i + 1] = g[1].y, o->scale[3 * i + 2] = g[1].z;
+            o->rot_wxyz[4 * i] = g[2].x, o->rot_wxyz[4 * i + 1] = g[2].y;
+            o->rot_wxyz[4 * i + 2] = g[2].z, o->rot_wxyz[4 * i + 3] = g[2].w;
+            std::memcpy(o->sh + 48 * i, &g[3], 48 * 4);
+        }
+    }
+    return HS_OK;
+}
+
 void hs_hierarchy_destroy(hs_hierarchy* h) {
     if (!h) return;
     cudaSetDevice(h->ctx->device);
@@ -671,6 +837,54 @@ hs_status hs_cut_upload(hs_context* ctx, const hs_hierarchy* h, const uint32_t* 
     HS_TRY(copy_sync(ctx, cut->count.p, &n, 8, cudaMemcpyHostToDevice));
     HS_CUDA(ctx, cudaEventRecord(cut->done, ctx->stream));
     cut->h = h;
+    return HS_OK;
+}
+
+// ------------------------------------------------------------------ cut churn (bench.hpp:79-82)
+hs_status hs_transfer_tracker_create(hs_context* ctx, const hs_hierarchy* h, hs_transfer_tracker** out) {
+    if (!ctx || !h || !out) return HS_INVALID_ARGUMENT;
+    *out = nullptr;
+    cudaSetDevice(ctx->device);
+    auto* t = new hs_transfer_tracker();
+    t->ctx = ctx;
+    t->h = h;
+    auto fail = [&](cudaError_t e) {
+        delete t;
+        return cuda_err(ctx, e, "transfer tracker");
+    };
+    cudaError_t e;
+    if ((e = t->epoch.ensure(h->n * 4)) != cudaSuccess) return fail(e);
+    if ((e = t->count.ensure(8)) != cudaSuccess) return fail(e);
+    if ((e = cudaHostAlloc(&t->h_count, 8, cudaHostAllocMapped)) != cudaSuccess) return fail(e);
+    if ((e = cudaHostGetDevicePointer(&t->h_count_dev, t->h_count, 0)) != cudaSuccess) return fail(e);
+    if ((e = cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+    if ((e = cudaMemsetAsync(t->epoch.p, 0, h->n * 4, ctx->stream)) != cudaSuccess) return fail(e);
+    *out = t;
+    return HS_OK;
+}
+
+void hs_transfer_tracker_destroy(hs_transfer_tracker* t) {
+    if (!t) return;
+    cudaStreamSynchronize(t->ctx->stream);
+    delete t;
+}
+
+hs_status hs_transfer_count(hs_context* ctx, hs_transfer_tracker* t, const hs_cut* cut, uint64_t* transferred) {
+    if (!ctx || !t || !cut) return HS_INVALID_ARGUMENT;
+    if (cut->cap == 0 || !cut->done) return set_err(ctx, HS_INVALID_ARGUMENT, "cut has not been selected");
+    if (cut->h != t->h) return set_err(ctx, HS_INVALID_ARGUMENT, "cut and tracker belong to different hierarchies");
+    // epoch 0 = never in a cut; the first refresh compares against an id no node carries
+    const uint32_t prev = t->refresh == 0 ? 0xFFFFFFFFu : t->refresh;
+    const uint32_t cur = t->refresh + 1;
+    HS_CUDA(ctx, cudaMemsetAsync(t->count.p, 0, 8, ctx->stream));
+    hs::launch_transfer_count(cut->node.as<uint32_t>(), cut->count.as<uint64_t>(), cut->cap, t->epoch.as<uint32_t>(),
+                              prev, cur, t->count.as<unsigned long long>(), ctx->stream);
+    HS_CUDA(ctx, cudaGetLastError());
+    hs::launch_copy_words(t->count.p, t->h_count_dev, 8, ctx->stream);
+    HS_CUDA(ctx, cudaEventRecord(t->done, ctx->stream));
+    t->refresh = cur;
+    HS_CUDA(ctx, cudaEventSynchronize(t->done));
+    if (transferred) *transferred = *t->h_count;
     return HS_OK;
 }
 

@@ -158,6 +158,33 @@ __global__ void __launch_bounds__(kCutThreads, 6) k_select_cut(const float4* __r
     }
 }
 
+// bench_path's `transferred` (bench.hpp:79-82): the number of nodes of this
+// refresh's cut that were not in the previous refresh's cut.  epoch[node] holds
+// the id of the last refresh whose cut contained the node, so membership of the
+// previous cut is one gather and the update one store per cut entry (the cut is
+// in ascending node order, so both are nearly coalesced).  4 + 4 + 4 B/entry.
+__global__ void __launch_bounds__(256) k_transfer_count(const uint32_t* __restrict__ node,
+                                                        const uint64_t* __restrict__ n_ptr,
+                                                        uint32_t* __restrict__ epoch, uint32_t prev, uint32_t cur,
+                                                        unsigned long long* __restrict__ out) {
+    const uint64_t n = *n_ptr;
+    uint32_t fresh = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = node[i];
+        fresh += epoch[v] != prev;
+        epoch[v] = cur;
+    }
+    for (int o = 16; o; o >>= 1) fresh += __shfl_xor_sync(0xffffffffu, fresh, o);
+    if ((threadIdx.x & 31) == 0 && fresh) atomicAdd(out, (unsigned long long)fresh);
+}
+
+void launch_transfer_count(const uint32_t* node, const uint64_t* n_ptr, uint64_t n_max, uint32_t* epoch,
+                           uint32_t prev, uint32_t cur, unsigned long long* out, cudaStream_t stream) {
+    const uint64_t blocks = std::min<uint64_t>((n_max + 255) / 256, 148 * 8);
+    k_transfer_count<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, stream>>>(node, n_ptr, epoch, prev, cur, out);
+    note_launch();
+}
+
 void launch_child_alpha(const float4* attr, float4* cull, uint64_t n, cudaStream_t stream) {
     const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148 * 16);
     k_child_alpha<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, stream>>>(attr, cull, n);

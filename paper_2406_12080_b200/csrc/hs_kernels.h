@@ -21,6 +21,19 @@ void launch_select_cut(const float4* cull, uint64_t n, const CamParams& cam, flo
 void launch_copy_words(const void* src, void* dst, size_t bytes, cudaStream_t s);  // bytes % 8 == 0
 void launch_child_alpha(const float4* attr, float4* cull, uint64_t n, cudaStream_t stream);
 uint64_t select_cut_status_words(uint64_t n);
+void launch_transfer_count(const uint32_t* node, const uint64_t* n_ptr, uint64_t n_max, uint32_t* epoch,
+                           uint32_t prev, uint32_t cur, unsigned long long* out, cudaStream_t stream);
+
+// assemble.cu (consolidate's BFS serialisation, scene.hpp:281-316)
+constexpr int kMaxParts = 64;
+struct PartTable {
+    const float4* cull[kMaxParts];
+    const float4* attr[kMaxParts];
+};
+void launch_assemble_level(const PartTable& parts, const uint4* fin, uint64_t n_in, uint64_t pos_base,
+                           float4* out_cull, float4* out_attr, uint4* fout, uint64_t* status,
+                           uint32_t* tile_counter, uint64_t* n_out, cudaStream_t s);
+uint64_t assemble_status_words(uint64_t n_in);
 
 // raster.cu
 void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,

@@ -332,43 +332,84 @@ float hs_synth_scene_side(uint64_t leaves) {
     return static_cast<float>(28.0 * std::sqrt(clusters / 240.0));
 }
 
-hs_status hs_synth_city(uint64_t leaves, uint64_t seed, int threads, const hs_node_soa_out* out) {
-    if (leaves < 1 || leaves > 0x7fffffffull || !out) return HS_INVALID_ARGUMENT;
-    const int nthreads = threads > 0 ? threads : std::max(1u, std::thread::hardware_concurrency());
+// City-like leaves: `leaves` Gaussians in 21-leaf clusters over a square of
+// side hs_synth_scene_side(leaves) centred at (cx, 0, cz).
+static void city_leaves(std::vector<G>& lv, uint64_t leaves, uint64_t seed, float cx, float cz, int nthreads) {
     const uint64_t clusters = (leaves + 20) / 21;
     const float side = hs_synth_scene_side(leaves);
-    std::vector<G> lv(leaves);
-    {
-        std::vector<std::thread> pool;
-        for (int w = 0; w < nthreads; ++w)
-            pool.emplace_back([&, w] {
-                for (uint64_t c = w; c < clusters; c += nthreads) {
-                    Rng rng(seed * 0x632BE59BD9B4E019ull + c * 0x9E3779B97F4A7C15ull + 1);
-                    float center[3] = {rng.uniform(-0.5f * side, 0.5f * side), rng.uniform(-4.2f, 4.2f),
-                                       rng.uniform(-0.5f * side, 0.5f * side)};
-                    float tone[2][3];
-                    for (auto& t : tone)
-                        for (float& v : t) v = rng.uniform(-1.2f, 1.5f);
-                    for (uint64_t i = c * 21; i < std::min<uint64_t>(leaves, c * 21 + 21); ++i) {
-                        G& g = lv[i];
-                        for (int k = 0; k < 3; ++k) g.mean[k] = center[k] + rng.uniform(-0.55f, 0.55f);
-                        for (int k = 0; k < 3; ++k) g.scale[k] = rng.uniform(0.06f, 0.2f);
-                        float q[4];
-                        for (float& v : q) v = rng.normal();
-                        const float qn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
-                        for (int k = 0; k < 4; ++k) g.q[k] = q[k] / qn;
-                        g.falloff = rng.uniform(0.4f, 0.9f);
-                        const float* tn = tone[(i - c * 21) % 2];
-                        for (int ch = 0; ch < 3; ++ch) {
-                            g.sh[ch] = tn[ch];
-                            for (int k = 1; k < 16; ++k) g.sh[k * 3 + ch] = rng.uniform(-0.08f, 0.08f);
-                        }
+    lv.resize(leaves);
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nthreads; ++w)
+        pool.emplace_back([&, w] {
+            for (uint64_t c = w; c < clusters; c += nthreads) {
+                Rng rng(seed * 0x632BE59BD9B4E019ull + c * 0x9E3779B97F4A7C15ull + 1);
+                float center[3] = {cx + rng.uniform(-0.5f * side, 0.5f * side), rng.uniform(-4.2f, 4.2f),
+                                   cz + rng.uniform(-0.5f * side, 0.5f * side)};
+                float tone[2][3];
+                for (auto& t : tone)
+                    for (float& v : t) v = rng.uniform(-1.2f, 1.5f);
+                for (uint64_t i = c * 21; i < std::min<uint64_t>(leaves, c * 21 + 21); ++i) {
+                    G& g = lv[i];
+                    for (int k = 0; k < 3; ++k) g.mean[k] = center[k] + rng.uniform(-0.55f, 0.55f);
+                    for (int k = 0; k < 3; ++k) g.scale[k] = rng.uniform(0.06f, 0.2f);
+                    float q[4];
+                    for (float& v : q) v = rng.normal();
+                    const float qn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+                    for (int k = 0; k < 4; ++k) g.q[k] = q[k] / qn;
+                    g.falloff = rng.uniform(0.4f, 0.9f);
+                    const float* tn = tone[(i - c * 21) % 2];
+                    for (int ch = 0; ch < 3; ++ch) {
+                        g.sh[ch] = tn[ch];
+                        for (int k = 1; k < 16; ++k) g.sh[k * 3 + ch] = rng.uniform(-0.08f, 0.08f);
                     }
                 }
-            });
-        for (auto& t : pool) t.join();
-    }
+            }
+        });
+    for (auto& t : pool) t.join();
+}
+
+static int thread_count(int threads) {
+    return threads > 0 ? threads : std::max(1u, std::thread::hardware_concurrency());
+}
+
+hs_status hs_synth_city(uint64_t leaves, uint64_t seed, int threads, const hs_node_soa_out* out) {
+    return hs_synth_city_chunk(leaves, seed, 0.0f, 0.0f, threads, out);
+}
+
+hs_status hs_synth_city_chunk(uint64_t leaves, uint64_t seed, float cx, float cz, int threads,
+                              const hs_node_soa_out* out) {
+    if (leaves < 1 || leaves > 0x7fffffffull || !out) return HS_INVALID_ARGUMENT;
+    const int nthreads = thread_count(threads);
+    std::vector<G> lv;
+    city_leaves(lv, leaves, seed, cx, cz, nthreads);
     return hs_synth_build_bvh_internal(lv.data(), leaves, nthreads, out);
+}
+
+// make_skybox (scene.hpp:111-137): a shell of mid-gray splats (SH zero) 5 scene
+// diameters out, scale = circumference / sqrt(count), falloff 0.7, identity
+// rotation; then build_bvh over it, as consolidate does (scene.hpp:256-258).
+hs_status hs_synth_skybox(uint64_t count, float scene_diameter, uint64_t seed, const float centroid[3], int threads,
+                          const hs_node_soa_out* out) {
+    if (!(scene_diameter > 0.0f)) return HS_INVALID_ARGUMENT;  // scene.hpp:115
+    if (count < 1 || count > 0x7fffffffull || !out) return HS_INVALID_ARGUMENT;
+    const float radius = 5.0f * scene_diameter;
+    const float spacing = 2.0f * 3.14159265358979323846f * radius / std::sqrt(static_cast<float>(count));
+    Rng rng(seed * 0xD1B54A32D192ED03ull + 7);
+    std::vector<G> lv(count);
+    for (uint64_t i = 0; i < count; ++i) {
+        const float z = 1.0f - 2.0f * rng.u01();
+        const float phi = 2.0f * 3.14159265358979323846f * rng.u01();
+        const float r = std::sqrt(std::max(0.0f, 1.0f - z * z));
+        G& g = lv[i];
+        g.mean[0] = centroid[0] + radius * (r * std::cos(phi));
+        g.mean[1] = centroid[1] + radius * z;
+        g.mean[2] = centroid[2] + radius * (r * std::sin(phi));
+        for (float& v : g.scale) v = spacing;
+        g.q[0] = 1.0f, g.q[1] = g.q[2] = g.q[3] = 0.0f;
+        g.falloff = 0.7f;
+        std::fill(std::begin(g.sh), std::end(g.sh), 0.0f);
+    }
+    return hs_synth_build_bvh_internal(lv.data(), count, thread_count(threads), out);
 }
 
 }  // extern "C"
@@ -470,6 +511,30 @@ hs_status hs_synth_build_bvh_internal(const void* leaves_v, uint64_t n, int nthr
         std::memcpy(out->sh + 48 * i, g[i].sh, 48 * sizeof(float));
     }
     return HS_OK;
+}
+
+// consolidate's global root (scene.hpp:264-279, 307-313): the moment-matched merge
+// of the k forest roots, their bounds' union, then each forest root re-matched to
+// the new root's axis convention.  gin/gout: k records of 59 floats
+// {mean3, scale3, quat wxyz 4, falloff, sh48}; root: one record + bounds.
+void hs_merge_root_internal(const float* gin, uint32_t k, const float* bmin, const float* bmax, float* root,
+                            float* root_bmin, float* root_bmax, float* gout) {
+    std::vector<G> kids(k);
+    for (uint32_t i = 0; i < k; ++i) std::memcpy(&kids[i], gin + 59 * i, sizeof(G));
+    G r = merge(kids.data(), static_cast<int>(k));
+    std::memcpy(root, &r, sizeof(G));
+    for (int a = 0; a < 3; ++a) {
+        root_bmin[a] = INFINITY;
+        root_bmax[a] = -INFINITY;
+        for (uint32_t i = 0; i < k; ++i) {
+            root_bmin[a] = std::min(root_bmin[a], bmin[3 * i + a]);
+            root_bmax[a] = std::max(root_bmax[a], bmax[3 * i + a]);
+        }
+    }
+    for (uint32_t i = 0; i < k; ++i) {
+        match_orientation(kids[i], r.q);
+        std::memcpy(gout + 59 * i, &kids[i], sizeof(G));
+    }
 }
 
 extern "C" hs_status hs_build_bvh(const float* mean, const float* scale, const float* rot_wxyz, const float* falloff,

@@ -28,10 +28,12 @@ def partition(n_frames: int, world: int, rank: int) -> tuple[int, int]:
 
 
 class FrameSource:
-    """What a rank needs to replay frames: `select(cam, tau) -> ascending node ids`
-    and `render(cam) -> dict of stage seconds (+ n_duplicates)` for the last cut."""
+    """What a rank needs to replay frames: `refresh(cam, tau) -> (cut size,
+    transferred)` selects a new cut and counts its nodes absent from the
+    previous refresh (bench.hpp:79-82), and `render(cam) -> dict of stage
+    seconds (+ n_duplicates)` renders the last cut."""
 
-    def select(self, cam, tau):  # pragma: no cover - interface
+    def refresh(self, cam, tau) -> tuple[int, int]:  # pragma: no cover - interface
         raise NotImplementedError
 
     def render(self, cam, refreshed: bool) -> dict:  # pragma: no cover - interface
@@ -47,9 +49,11 @@ class GpuFrameSource(FrameSource):
     def __init__(self, renderer, dh):
         self.r = renderer
         self.dh = dh
+        self.tracker = renderer.transfer_tracker(dh)  # cut churn counted on the device
 
-    def select(self, cam, tau):
-        return self.r.select_cut(self.dh, cam, tau).node
+    def refresh(self, cam, tau):
+        n = self.r.select_cut_device(self.dh, cam, tau)
+        return n, self.tracker.count(self.r._cut)
 
     def render(self, cam, refreshed):
         from . import StageTimes
@@ -68,17 +72,15 @@ def replay_block(src: FrameSource, cams, tau: float, start: int, stop: int) -> n
     a (stop-start, len(STAT_FIELDS)) float64 array."""
     leaves = src.leaf_count()
     out = np.zeros((stop - start, len(STAT_FIELDS)), np.float64)
-    prev = np.empty(0, np.uint32)
+    cut_size = 0
     if start > 0:  # the previous refresh, for the transferred statistic
-        prev = np.asarray(src.select(cams[start - 2 if start >= 2 else 0], tau))
-    cut = prev
+        cut_size, _ = src.refresh(cams[start - 2 if start >= 2 else 0], tau)
     for i in range(start, stop):
         refreshed = i % 2 == 0
         row = dict.fromkeys(STAT_FIELDS, 0.0)
         if refreshed:
-            cut = np.asarray(src.select(cams[i], tau))
-            row["transferred"] = float(np.count_nonzero(~np.isin(cut, prev, assume_unique=True)))
-            prev = cut
+            cut_size, transferred = src.refresh(cams[i], tau)
+            row["transferred"] = float(transferred)
         st = src.render(cams[i], refreshed)
         for k, v in st.items():
             if k in row and k not in ("rendered", "rendered_pct", "transferred"):
@@ -86,8 +88,8 @@ def replay_block(src: FrameSource, cams, tau: float, start: int, stop: int) -> n
         if not refreshed:
             row["cut_expand"] = 0.0
             row["weights"] = 0.0
-        row["rendered"] = float(len(cut))
-        row["rendered_pct"] = 100.0 * len(cut) / leaves
+        row["rendered"] = float(cut_size)
+        row["rendered_pct"] = 100.0 * cut_size / leaves
         out[i - start] = [row[k] for k in STAT_FIELDS]
     return out
 

@@ -18,7 +18,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import CameraModel, look_at_camera, scene_side, synth_city
+from . import CameraModel, look_at_camera, scene_side, synth_city, synth_city_chunk, synth_skybox
 
 
 @dataclass(frozen=True)
@@ -40,7 +40,8 @@ CONFIGS = {
                  lookahead=50.0),
     # configs[1]: 10M leaves, 1920x1080, tau = 3 px, 1 B200 (the headline metric)
     "c2": Config("c2_10m_1080p_tau3", 10_000_000, 1920, 1080, 1100.0, 3.0),
-    # configs[4]: 100M leaves multi-chunk, 3840x2160 (generated on demand; ~54 GB of SoA)
+    # configs[4]: 100M leaves multi-chunk (4 x 4 chunks of 6.25M + a 100K skybox under one root,
+    # assembled on the device: multichunk()), 3840x2160; ~58 GB resident
     "c5": Config("c5_100m_2160p_tau3", 100_000_000, 3840, 2160, 2200.0, 3.0, altitude=60.0, standoff=40.0,
                  lookahead=250.0),
 }
@@ -85,3 +86,31 @@ def camera(cfg: Config, frame: int = 0) -> CameraModel:
 
 def hierarchy(cfg: Config, seed: int = 1, threads: int = 0):
     return synth_city(cfg.leaves, seed=seed, threads=threads)
+
+
+def chunk_parts(leaves: int, grid: int = 4, sky: int = 100_000, seed: int = 1):
+    """The parts of a multi-chunk scene: grid x grid city chunks
+    of leaves / grid^2 leaves each, tiled edge to edge around the origin, then a
+    make_skybox shell (scene.hpp:111-137) 5 scene diameters out.  Yields
+    (name, host Hierarchy) one part at a time so the caller can upload and free."""
+    per = leaves // (grid * grid)
+    side = scene_side(per)
+    for iz in range(grid):
+        for ix in range(grid):
+            cx, cz = (ix - 0.5 * (grid - 1)) * side, (iz - 0.5 * (grid - 1)) * side
+            yield f"chunk_{ix}_{iz}", synth_city_chunk(per, seed * 1009 + iz * grid + ix, cx, cz)
+    if sky:
+        yield "skybox", synth_skybox(sky, grid * side * math.sqrt(2.0), seed)
+
+
+def multichunk(renderer, leaves: int, grid: int = 4, sky: int = 100_000, seed: int = 1, validate: bool = False):
+    """Generate the chunks + skybox, upload each, and consolidate them on the device
+    (hs_hierarchy_assemble: one merged root, breadth-first layout).  The parts are
+    released once assembled; only the consolidated hierarchy stays resident."""
+    parts = []
+    for _, h in chunk_parts(leaves, grid, sky, seed):
+        parts.append(renderer.upload(h, validate=validate))
+        del h
+    dh = renderer.assemble(parts)
+    del parts
+    return dh

@@ -103,6 +103,27 @@ def test_trajectory_replay_single_gpu_matches_bench_path(renderer):
     assert list(stats[:, 2].astype(int)) == [f.transferred for f in rep.frames]
 
 
+def test_transfer_tracker_matches_set_difference(renderer):
+    """hs_transfer_count == |cut \\ previous cut| (bench.hpp:79-82) over a trajectory
+    with churn, a repeated cut (0 new) and a tau jump (large churn)."""
+    cfg = scenes.CONFIGS["c1"]
+    h = scenes.hierarchy(cfg)
+    dh = renderer.upload(h)
+    tr = renderer.transfer_tracker(dh)
+    cams = scenes.trajectory(cfg, 6, first=300)
+    steps = [(c, cfg.tau) for c in cams] + [(cams[-1], cfg.tau), (cams[-1], 12.0), (cams[0], 0.0)]
+    prev = np.empty(0, np.uint32)
+    for cam, tau in steps:
+        cut = renderer.select_cut(dh, cam, tau)
+        want = int(np.count_nonzero(~np.isin(cut.node, prev, assume_unique=True)))
+        assert tr.count() == want
+        prev = cut.node
+    other = renderer.upload(scenes.hierarchy(scenes.Config("o", 500, 64, 48, 60.0, 3.0)))
+    with pytest.raises(hs.Error):
+        renderer.transfer_tracker(other).count()  # the current cut belongs to `dh`
+    tr.close()
+
+
 def test_duplicate_buffer_grows(renderer):
     """Splats covering every tile overflow the initial key buffer; the synchronous
     call grows it and re-runs (results still bit-exact)."""

@@ -29,11 +29,14 @@ class OracleSource(multi.FrameSource):
         self.orc = orc
         self.oh = orc.OracleHierarchy(h)
         self.cut = None
+        self.prev = np.empty(0, np.uint32)
 
-    def select(self, cam, tau):
+    def refresh(self, cam, tau):
         node, t, a = self.orc.select_cut(self.oh, cam, tau)
         self.cut = (node, t, a)
-        return node
+        fresh = int(np.count_nonzero(~np.isin(node, self.prev, assume_unique=True)))
+        self.prev = node
+        return len(node), fresh
 
     def render(self, cam, refreshed):
         sp = self.orc.cut_render_splats(self.oh, *self.cut)

@@ -14,6 +14,12 @@ for r in rows:
             data.append((fname, int(r[0]), r[1], float(r[7] or 0), float(r[4] or 0)))
         except ValueError:
             pass
+agg = {}
+for f, ln, src, ins, smp in data:  # several launches of the kernel: sum per source line
+    a = agg.setdefault((f, ln), [f, ln, src, 0.0, 0.0])
+    a[3] += ins
+    a[4] += smp
+data = sorted(agg.values(), key=lambda a: (a[0], a[1]))
 ti = sum(d[3] for d in data) or 1
 ts = sum(d[4] for d in data) or 1
 print(f"total warp instructions {ti:.4g}")

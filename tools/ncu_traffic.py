@@ -1,0 +1,28 @@
+"""Per-kernel DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum, bytes per
+launch, averaged over the captured launches of each kernel) from an ncu --set
+full report -> JSON consumed by bench.py's roofline.traffic.
+Usage: ncu_traffic.py REP OUT.json"""
+import csv, io, json, subprocess, sys
+from collections import defaultdict
+rep, out = sys.argv[1], sys.argv[2]
+txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                      "dram__bytes_read.sum,dram__bytes_write.sum"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(txt)))
+h, units = rows[0], rows[1]
+ki = h.index("Kernel Name")
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6}
+acc = defaultdict(lambda: [0.0, 0.0, 0.0, 0])
+for r in rows[2:]:
+    name = r[ki].split("(")[0].replace("void ", "")
+    a = acc[name]
+    for j, key in enumerate(("dram__bytes_read.sum", "dram__bytes_write.sum")):
+        i = h.index(key)
+        a[j] += float(r[i].replace(",", "")) * scale.get(units[i], 1)
+    a[3] += 1
+res = {"source": rep.split("/")[-1], "how": "ncu --set full --clock-control none, one C2 frame; per-launch mean",
+       "kernels": {k: {"dram_bytes": (v[0] + v[1]) / v[3], "read": v[0] / v[3], "write": v[1] / v[3],
+                       "launches": v[3]} for k, v in acc.items()}}
+json.dump(res, open(out, "w"), indent=1)
+for k, v in res["kernels"].items():
+    print(f"{k:28s} {v['dram_bytes'] / 1e6:10.2f} MB  x{v['launches']}")
