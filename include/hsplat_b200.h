@@ -171,6 +171,12 @@ hs_status hs_hierarchy_load_h3dg(hs_context* ctx, const char* path, hs_hierarchy
  * the result is serialised breadth-first (children contiguous, parent < child)
  * into a new device hierarchy.  The parts stay valid; k <= 64. */
 hs_status hs_hierarchy_assemble(hs_context* ctx, const hs_hierarchy* const* parts, uint32_t k, hs_hierarchy** out);
+/* replaces: compact (build.hpp:168-272): drop interior nodes no cut of any of
+ * the `ncams` cameras uses at tau_min, 2 tau_min, ... <= tau_max (tau_max <= 0:
+ * half the largest camera dimension); children hoisted to the nearest surviving
+ * ancestor; the result is serialised breadth first into a new device hierarchy. */
+hs_status hs_hierarchy_compact(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cams, uint64_t ncams,
+                               float tau_min, float tau_max, hs_hierarchy** out);
 /* device hierarchy -> host SoA (for write_hierarchy, io.hpp:350-373, and parity) */
 hs_status hs_hierarchy_download(hs_context* ctx, const hs_hierarchy* h, const hs_node_soa_out* out);
 void hs_hierarchy_destroy(hs_hierarchy* h);

@@ -1066,6 +1066,130 @@ int or_bench_path(void* hv, const or_camera* cams, uint64_t ncam, const double* 
     });
 }
 
+// compact (build.hpp:168-272): remove interior nodes no cut at the probed
+// granularity ladder {tau_min, 2 tau_min, ...} <= tau_max uses; children are
+// hoisted to the nearest surviving ancestor; the survivors are re-serialised
+// breadth first.  Restated with the reference's serial structure.
+static std::vector<std::uint32_t> alive_parents(const Hierarchy& h, const std::vector<unsigned char>& alive) {
+    std::vector<std::uint32_t> ap(h.nodes.size(), kNoNode);  // build.hpp:153-163
+    for (std::size_t i = 1; i < h.nodes.size(); ++i) {
+        if (!alive[i]) continue;
+        std::uint32_t p = h.nodes[i].parent;
+        while (p != kNoNode && !alive[p]) p = h.nodes[p].parent;
+        ap[i] = p;
+    }
+    return ap;
+}
+
+static Hierarchy compact(const Hierarchy& h, const std::vector<Camera>& cams, float tau_min, float tau_max) {
+    require(!h.nodes.empty(), kInvalidArgument, "compact needs a hierarchy");
+    require(!cams.empty(), kInvalidArgument, "compact needs at least one camera");
+    require(tau_min > 0.0f, kInvalidArgument, "tau_min must be positive");
+    if (h.nodes.size() == 1) return h;
+    if (tau_max <= 0.0f)
+        for (const auto& c : cams) tau_max = std::max(tau_max, 0.5f * static_cast<float>(std::max(c.width, c.height)));
+    const std::size_t n = h.nodes.size();
+    std::vector<unsigned char> alive(n, 1), marked(n, 0);
+    for (std::size_t i = 0; i < n; ++i) marked[i] = h.nodes[i].is_leaf();
+    for (float tau = tau_min; tau <= tau_max; tau *= 2.0f) {
+        auto ap = alive_parents(h, alive);
+        std::vector<unsigned char> in_union(n, 0);
+        for (const auto& cam : cams)
+            for (std::size_t i = 0; i < n; ++i) {
+                if (!alive[i] || in_union[i]) continue;
+                const float eps = granularity(h.nodes[i].bounds, cam);
+                const bool fine_enough = eps <= tau;
+                if (!fine_enough && !h.nodes[i].is_leaf()) continue;
+                if (ap[i] != kNoNode && !(granularity(h.nodes[ap[i]].bounds, cam) > tau)) continue;
+                in_union[i] = 1;
+            }
+        for (std::size_t i = 0; i < n; ++i)
+            if (in_union[i]) marked[i] = 1;
+        std::vector<unsigned char> has_union_below(n, 0);
+        for (std::size_t i = 0; i < n; ++i) {
+            if (!in_union[i]) continue;
+            for (std::uint32_t p = ap[i]; p != kNoNode; p = ap[p]) {
+                if (has_union_below[p]) break;
+                has_union_below[p] = 1;
+            }
+        }
+        std::vector<std::vector<std::uint32_t>> kids(n);
+        for (std::size_t i = 1; i < n; ++i)
+            if (alive[i] && ap[i] != kNoNode) kids[ap[i]].push_back(static_cast<std::uint32_t>(i));
+        for (std::size_t b = 0; b < n; ++b) {
+            if (!in_union[b] || has_union_below[b]) continue;
+            std::vector<std::uint32_t> walk(kids[b]);
+            while (!walk.empty()) {
+                const std::uint32_t c = walk.back();
+                walk.pop_back();
+                if (marked[c]) continue;
+                alive[c] = 0;
+                for (std::uint32_t gc : kids[c]) walk.push_back(gc);
+            }
+        }
+    }
+    auto ap = alive_parents(h, alive);
+    std::vector<std::vector<std::uint32_t>> kids(n);
+    for (std::size_t i = 1; i < n; ++i)
+        if (alive[i] && ap[i] != kNoNode) kids[ap[i]].push_back(static_cast<std::uint32_t>(i));
+    Hierarchy out;
+    out.sh_degree = h.sh_degree;
+    std::vector<std::uint32_t> new_index(n, kNoNode);
+    std::vector<std::uint32_t> bfs{0};
+    new_index[0] = 0;
+    out.nodes.push_back(h.nodes[0]);
+    out.nodes[0].parent = kNoNode;
+    for (std::size_t head = 0; head < bfs.size(); ++head) {
+        const std::uint32_t old = bfs[head];
+        const std::uint32_t me = new_index[old];
+        out.nodes[me].first_child = kids[old].empty() ? kNoNode : static_cast<std::uint32_t>(out.nodes.size());
+        out.nodes[me].child_count = static_cast<std::uint32_t>(kids[old].size());
+        for (std::uint32_t c : kids[old]) {
+            new_index[c] = static_cast<std::uint32_t>(out.nodes.size());
+            out.nodes.push_back(h.nodes[c]);
+            out.nodes.back().parent = me;
+            out.nodes.back().first_child = kNoNode;
+            out.nodes.back().child_count = 0;
+            bfs.push_back(c);
+        }
+    }
+    return out;
+}
+
+int or_compact(void* hv, const or_camera* cams, uint64_t ncam, float tau_min, float tau_max, void** out) {
+    OR_TRY({
+        std::vector<Camera> cs;
+        for (uint64_t i = 0; i < ncam; ++i) cs.push_back(to_cam(&cams[i]));
+        *out = new Hierarchy(compact(*static_cast<Hierarchy*>(hv), cs, tau_min, tau_max));
+    });
+}
+
+uint64_t or_hierarchy_size(void* hv) { return static_cast<Hierarchy*>(hv)->nodes.size(); }
+
+// Hierarchy -> caller SoA arrays (sized or_hierarchy_size)
+void or_hierarchy_export(void* hv, uint32_t* parent, uint32_t* first_child, uint32_t* child_count, float* bmin,
+                         float* bmax, float* mean, float* scale, float* rot_wxyz, float* falloff, float* sh) {
+    const Hierarchy& h = *static_cast<Hierarchy*>(hv);
+    for (std::size_t i = 0; i < h.nodes.size(); ++i) {
+        const HierarchyNode& nd = h.nodes[i];
+        parent[i] = nd.parent;
+        first_child[i] = nd.first_child;
+        child_count[i] = nd.child_count;
+        for (int k = 0; k < 3; ++k) {
+            bmin[3 * i + k] = nd.bounds.mn[k];
+            bmax[3 * i + k] = nd.bounds.mx[k];
+            mean[3 * i + k] = nd.g.mean[k];
+            scale[3 * i + k] = nd.g.scale[k];
+        }
+        rot_wxyz[4 * i] = nd.g.q_xyzw[3];
+        rot_wxyz[4 * i + 1] = nd.g.q_xyzw[0];
+        rot_wxyz[4 * i + 2] = nd.g.q_xyzw[1];
+        rot_wxyz[4 * i + 3] = nd.g.q_xyzw[2];
+        falloff[i] = nd.g.falloff;
+        std::memcpy(sh + 48 * i, nd.g.sh, 48 * sizeof(float));
+    }
+}
+
 // psnr (image.hpp:111-122): over all channels in double; mse <= 0 -> 99 dB; capped at 99.
 double or_psnr(const float* a, const float* b, uint64_t n) {
     double mse = 0.0;

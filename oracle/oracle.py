@@ -57,6 +57,9 @@ _SIGS = {
     "or_hierarchy_create": (_vp, [C.POINTER(or_nodes), C.c_uint64]),
     "or_hierarchy_free": (None, [_vp]),
     "or_hierarchy_leaf_count": (C.c_uint64, [_vp]),
+    "or_hierarchy_size": (C.c_uint64, [_vp]),
+    "or_hierarchy_export": (None, [_vp, u32p, u32p, u32p, f32p, f32p, f32p, f32p, f32p, f32p, f32p]),
+    "or_compact": (C.c_int, [_vp, C.POINTER(or_camera), C.c_uint64, C.c_float, C.c_float, C.POINTER(_vp)]),
     "or_select_cut": (C.c_int, [_vp, C.POINTER(or_camera), C.c_float, u32p, f32p, f32p, u64p, f64p]),
     "or_cut_render_splats": (C.c_int, [_vp, u32p, f32p, f32p, C.c_uint64, f32p, f32p, f32p, f32p, f32p, f32p,
                                        f32p, i32p]),
@@ -359,3 +362,24 @@ def consolidate_bfs(parts, root=None):
     first = 1 + np.cumsum(cc) - cc
     out["first_child"] = np.where(cc > 0, first, 0xFFFFFFFF).astype(np.uint32)
     return out
+
+
+def compact(oh: OracleHierarchy, cams, tau_min: float = 3.0, tau_max: float = 0.0) -> dict:
+    """compact (build.hpp:168-272) -> dict of SoA arrays (parent, first_child, child_count,
+    bmin, bmax, mean, scale, rot_wxyz, falloff, sh)."""
+    cs = (or_camera * len(cams))(*[camera(c) for c in cams])
+    out = C.c_void_p()
+    _chk(lib().or_compact(oh.handle, cs, len(cams), float(tau_min), float(tau_max), C.byref(out)))
+    try:
+        n = int(lib().or_hierarchy_size(out))
+        d = {"parent": np.empty(n, np.uint32), "first_child": np.empty(n, np.uint32),
+             "child_count": np.empty(n, np.uint32), "bmin": np.empty((n, 3), np.float32),
+             "bmax": np.empty((n, 3), np.float32), "mean": np.empty((n, 3), np.float32),
+             "scale": np.empty((n, 3), np.float32), "rot_wxyz": np.empty((n, 4), np.float32),
+             "falloff": np.empty(n, np.float32), "sh": np.empty((n, 48), np.float32)}
+        lib().or_hierarchy_export(out, *[_p(d[k], C.c_uint32 if d[k].dtype == np.uint32 else C.c_float)
+                                         for k in ("parent", "first_child", "child_count", "bmin", "bmax", "mean",
+                                                   "scale", "rot_wxyz", "falloff", "sh")])
+    finally:
+        lib().or_hierarchy_free(out)
+    return d

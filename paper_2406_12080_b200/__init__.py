@@ -559,6 +559,17 @@ class Renderer:
         return DeviceHierarchy(self, out, int(N.lib().hs_hierarchy_node_count(out)),
                                int(N.lib().hs_hierarchy_leaf_count(out)))
 
+    def compact(self, h, cams, tau_min: float = 3.0, tau_max: float = 0.0) -> DeviceHierarchy:
+        """compact (build.hpp:168-272) on the device: a new, breadth-first hierarchy without the
+        interior nodes no probed cut of `cams` uses."""
+        dh = self._dev(h)
+        cc = (N.hs_camera * max(1, len(cams)))(*[c.to_c() for c in cams])
+        out = C.c_void_p()
+        _check(N.lib().hs_hierarchy_compact(self.ctx, dh.handle, cc, len(cams), float(tau_min), float(tau_max),
+                                            C.byref(out)), self.ctx)
+        return DeviceHierarchy(self, out, int(N.lib().hs_hierarchy_node_count(out)),
+                               int(N.lib().hs_hierarchy_leaf_count(out)))
+
     def download(self, h) -> Hierarchy:
         """Device hierarchy -> host Hierarchy (reference node order)."""
         dh = self._dev(h)

@@ -72,6 +72,8 @@ _SIGS = {
     "hs_hierarchy_load_h3dg": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
     "hs_hierarchy_assemble": (C.c_int, [_vp, C.POINTER(_vp), C.c_uint32, C.POINTER(_vp)]),
     "hs_hierarchy_download": (C.c_int, [_vp, _vp, C.POINTER(hs_node_soa)]),
+    "hs_hierarchy_compact": (C.c_int, [_vp, _vp, C.POINTER(hs_camera), C.c_uint64, C.c_float, C.c_float,
+                                       C.POINTER(_vp)]),
     "hs_hierarchy_destroy": (None, [_vp]),
     "hs_hierarchy_node_count": (C.c_uint64, [_vp]),
     "hs_hierarchy_leaf_count": (C.c_uint64, [_vp]),

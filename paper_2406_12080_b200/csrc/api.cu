@@ -452,15 +452,13 @@ hs_status enqueue_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* c
         return set_err(ctx, HS_INVALID_ARGUMENT, "select_cut needs tau >= 0 and nodes");  // lod.hpp:53
     hs_status st = ensure_cut(ctx, cut, h->n);
     if (st != HS_OK) return st;
-    const uint64_t words = hs::select_cut_status_words(h->n);
-    HS_CUDA(ctx, ctx->cut_scratch.ensure(64 + words * 8));
-    unsigned char* sc = ctx->cut_scratch.as<unsigned char>();
-    HS_CUDA(ctx, cudaMemsetAsync(sc, 0, 64 + words * 8, ctx->stream));
+    const uint64_t words = hs::select_cut_scratch_words(h->n);
+    HS_CUDA(ctx, ctx->cut_scratch.ensure(words * 4));
+    uint32_t* sc = ctx->cut_scratch.as<uint32_t>();
+    HS_CUDA(ctx, cudaMemsetAsync(sc, 0, hs::select_cut_zero_words(h->n) * 4, ctx->stream));  // counters
     const CamParams cp = make_cam(cam);
-    hs::launch_select_cut(h->cull.as<float4>(), h->n, cp, tau,
-                          cut->node.as<uint32_t>(), cut->t.as<float>(), cut->alpha.as<float>(),
-                          reinterpret_cast<uint64_t*>(sc + 64), reinterpret_cast<uint32_t*>(sc),
-                          cut->count.as<uint64_t>(), ctx->stream);
+    hs::launch_select_cut(h->cull.as<float4>(), h->n, cp, tau, cut->node.as<uint32_t>(), cut->t.as<float>(),
+                          cut->alpha.as<float>(), sc, cut->count.as<uint64_t>(), ctx->stream);
     HS_CUDA(ctx, cudaGetLastError());
     hs::launch_copy_words(cut->count.p, cut->h_count_dev, 8, ctx->stream);
     HS_CUDA(ctx, cudaEventRecord(cut->done, ctx->stream));
@@ -488,6 +486,41 @@ void pack_nodes(const hs_node_soa* s, uint64_t lo, uint64_t hi, float4* cu, floa
 }
 
 }  // namespace
+
+// Breadth-first serialisation of a forest by levels (assemble.cu); `first` is
+// the level-1 frontier, `pos` the index of its first entry.  Returns the node count.
+static hs_status serialise_levels(hs_context* ctx, hs_hierarchy* h, const hs::PartTable& pt, const hs::ChildTable& kids,
+                                  const std::vector<uint4>& first, uint64_t pos, uint64_t widest, uint64_t limit,
+                                  uint64_t* total) {
+    DBuf fr[2], scratch;
+    HS_CUDA(ctx, fr[0].ensure(widest * 16));
+    HS_CUDA(ctx, fr[1].ensure(widest * 16));
+    HS_CUDA(ctx, scratch.ensure(64 + hs::assemble_status_words(widest) * 8));
+    HS_CUDA(ctx, cudaMemcpy(fr[0].p, first.data(), 16 * first.size(), cudaMemcpyHostToDevice));
+    uint64_t* n_next = nullptr;
+    HS_CUDA(ctx, cudaMallocHost(&n_next, 8));
+    unsigned char* sc = scratch.as<unsigned char>();
+    uint64_t n_in = first.size();
+    int cur = 0;
+    cudaError_t e = cudaSuccess;
+    while (n_in > 0 && e == cudaSuccess) {
+        cudaMemsetAsync(sc, 0, 64 + hs::assemble_status_words(n_in) * 8, ctx->stream);
+        hs::launch_assemble_level(pt, kids, fr[cur].as<uint4>(), n_in, pos, h->cull.as<float4>(),
+                                  h->attr.as<float4>(), fr[cur ^ 1].as<uint4>(), reinterpret_cast<uint64_t*>(sc + 64),
+                                  reinterpret_cast<uint32_t*>(sc), reinterpret_cast<uint64_t*>(sc + 8), ctx->stream);
+        cudaMemcpyAsync(n_next, sc + 8, 8, cudaMemcpyDeviceToHost, ctx->stream);
+        e = cudaStreamSynchronize(ctx->stream);
+        pos += n_in;
+        n_in = *n_next;
+        cur ^= 1;
+        if (pos + n_in > limit) break;
+    }
+    cudaFreeHost(n_next);
+    if (e != cudaSuccess) return cuda_err(ctx, e, "serialise levels");
+    if (n_in != 0) return set_err(ctx, HS_INVALID_ARGUMENT, "hierarchy is not a tree");
+    *total = pos;
+    return HS_OK;
+}
 
 extern "C" {
 
@@ -645,12 +678,6 @@ hs_status hs_hierarchy_assemble(hs_context* ctx, const hs_hierarchy* const* part
     cudaError_t e;
     if ((e = h->cull.ensure(total * 32)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc cull records"));
     if ((e = h->attr.ensure(total * 256)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc attributes"));
-    // frontier buffers: a level never holds more than all part nodes
-    DBuf fr[2], scratch;
-    if ((e = fr[0].ensure(widest * 16)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc frontier"));
-    if ((e = fr[1].ensure(widest * 16)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc frontier"));
-    const uint64_t words = hs::assemble_status_words(widest);
-    if ((e = scratch.ensure(64 + words * 8)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc scan state"));
     std::vector<uint4> first(k);
     std::vector<float> gout(59 * k);
     if (k > 1) {
@@ -693,30 +720,10 @@ hs_status hs_hierarchy_assemble(hs_context* ctx, const hs_hierarchy* const* part
     } else {
         first[0] = make_uint4(0, 0, HS_NO_NODE, 0);
     }
-    if ((e = cudaMemcpy(fr[0].p, first.data(), 16 * k, cudaMemcpyHostToDevice)) != cudaSuccess)
-        return fail(cuda_err(ctx, e, "frontier"));
-    uint64_t pos = k > 1 ? 1 : 0, n_in = k;
-    int cur = 0;
-    uint64_t* n_next = nullptr;
-    if ((e = cudaMallocHost(&n_next, 8)) != cudaSuccess) return fail(cuda_err(ctx, e, "pinned"));
-    unsigned char* sc = scratch.as<unsigned char>();
-    while (n_in > 0) {
-        cudaMemsetAsync(sc, 0, 64 + hs::assemble_status_words(n_in) * 8, ctx->stream);
-        hs::launch_assemble_level(pt, fr[cur].as<uint4>(), n_in, pos, h->cull.as<float4>(), h->attr.as<float4>(),
-                                  fr[cur ^ 1].as<uint4>(), reinterpret_cast<uint64_t*>(sc + 64),
-                                  reinterpret_cast<uint32_t*>(sc), reinterpret_cast<uint64_t*>(sc + 8), ctx->stream);
-        cudaMemcpyAsync(n_next, sc + 8, 8, cudaMemcpyDeviceToHost, ctx->stream);
-        if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) {
-            cudaFreeHost(n_next);
-            return fail(cuda_err(ctx, e, "assemble level"));
-        }
-        pos += n_in;
-        n_in = *n_next;
-        cur ^= 1;
-        if (pos + n_in > total) break;
-    }
-    cudaFreeHost(n_next);
-    if (pos != total || n_in != 0) return fail(set_err(ctx, HS_INVALID_ARGUMENT, "part hierarchies are not trees"));
+    uint64_t placed = 0;
+    hs_status st = serialise_levels(ctx, h, pt, hs::ChildTable{}, first, k > 1 ? 1 : 0, widest, total, &placed);
+    if (st != HS_OK) return fail(st);
+    if (placed != total) return fail(set_err(ctx, HS_INVALID_ARGUMENT, "part hierarchies are not trees"));
     if (k > 1) {  // forest roots re-matched to the new root's axis convention (scene.hpp:307-313)
         for (uint32_t p = 0; p < k; ++p) {
             const float* g = gout.data() + 59 * p;
@@ -734,6 +741,90 @@ hs_status hs_hierarchy_assemble(hs_context* ctx, const hs_hierarchy* const* part
     hs::launch_child_alpha(h->attr.as<float4>(), h->cull.as<float4>(), total, ctx->stream);
     if ((e = cudaStreamSynchronize(ctx->stream)) != cudaSuccess) return fail(cuda_err(ctx, e, "assemble"));
     *out = h;
+    return HS_OK;
+}
+
+hs_status hs_hierarchy_compact(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cams, uint64_t ncams,
+                               float tau_min, float tau_max, hs_hierarchy** out) {
+    if (!ctx || !h || !out || (ncams && !cams)) return HS_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (h->n == 0) return set_err(ctx, HS_INVALID_ARGUMENT, "compact needs a hierarchy");             // build.hpp:176
+    if (ncams == 0) return set_err(ctx, HS_INVALID_ARGUMENT, "compact needs at least one camera");  // build.hpp:177
+    if (!(tau_min > 0.0f)) return set_err(ctx, HS_INVALID_ARGUMENT, "tau_min must be positive");    // build.hpp:178
+    cudaSetDevice(ctx->device);
+    const uint64_t n = h->n;
+    auto* o = new hs_hierarchy();
+    o->ctx = ctx;
+    o->sh_degree = h->sh_degree;
+    o->leaves = h->leaves;  // leaves are always kept
+    auto fail = [&](hs_status st) {
+        delete o;
+        return st;
+    };
+    cudaError_t e;
+    if ((e = o->cull.ensure(n * 32)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc cull records"));
+    if ((e = o->attr.ensure(n * 256)) != cudaSuccess) return fail(cuda_err(ctx, e, "alloc attributes"));
+    if (n == 1) {  // build.hpp:179
+        HS_CUDA(ctx, cudaMemcpy(o->cull.p, h->cull.p, 32, cudaMemcpyDeviceToDevice));
+        HS_CUDA(ctx, cudaMemcpy(o->attr.p, h->attr.p, 256, cudaMemcpyDeviceToDevice));
+        o->n = 1;
+        *out = o;
+        return HS_OK;
+    }
+    if (tau_max <= 0.0f)  // build.hpp:181-184
+        for (uint64_t k = 0; k < ncams; ++k)
+            tau_max = std::max(tau_max, 0.5f * static_cast<float>(std::max(cams[k].width, cams[k].height)));
+    std::vector<CamParams> cps(ncams);
+    for (uint64_t k = 0; k < ncams; ++k) cps[k] = make_cam(&cams[k]);
+    DBuf d_cams, parent, ap, alive, marked, in_union, below;
+    if ((e = d_cams.ensure(sizeof(CamParams) * ncams)) != cudaSuccess || (e = parent.ensure(n * 4)) != cudaSuccess ||
+        (e = ap.ensure(n * 4)) != cudaSuccess || (e = alive.ensure(n)) != cudaSuccess ||
+        (e = marked.ensure(n)) != cudaSuccess || (e = in_union.ensure(n)) != cudaSuccess ||
+        (e = below.ensure(((n + 31) / 32) * 4)) != cudaSuccess)
+        return fail(cuda_err(ctx, e, "compact state"));
+    if ((e = cudaMemcpy(d_cams.p, cps.data(), sizeof(CamParams) * ncams, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(cuda_err(ctx, e, "cameras"));
+    hs::CompactState cs{h->cull.as<float4>(), parent.as<uint32_t>(), ap.as<uint32_t>(), alive.as<uint8_t>(),
+                        marked.as<uint8_t>(), in_union.as<uint8_t>(), below.as<uint32_t>(), n};
+    cudaStream_t s = ctx->stream;
+    hs::launch_compact_init(cs, s);
+    for (float tau = tau_min; tau <= tau_max; tau *= 2.0f) {  // build.hpp:186
+        hs::launch_alive_parents(cs, s);
+        hs::launch_cut_union(cs, d_cams.as<CamParams>(), (int)ncams, tau, s);
+        hs::launch_union_below(cs, s);
+        hs::launch_kill(cs, s);
+    }
+    hs::launch_alive_parents(cs, s);
+    // survivors listed per alive parent in ascending node order (stable sort by parent)
+    int key_bits = 1;
+    while ((1ull << key_bits) <= n) ++key_bits;
+    const int passes = (key_bits + 7) / 8;
+    DBuf kb[2], vb[2], sort_scratch, n_dev, seg_start, seg_count;
+    if ((e = kb[0].ensure(n * 4)) != cudaSuccess || (e = kb[1].ensure(n * 4)) != cudaSuccess ||
+        (e = vb[0].ensure(n * 4)) != cudaSuccess || (e = vb[1].ensure(n * 4)) != cudaSuccess ||
+        (e = sort_scratch.ensure(hs::sort_scratch_words(n, passes) * 4)) != cudaSuccess ||
+        (e = n_dev.ensure(8)) != cudaSuccess || (e = seg_start.ensure(n * 4)) != cudaSuccess ||
+        (e = seg_count.ensure(n * 4)) != cudaSuccess)
+        return fail(cuda_err(ctx, e, "compact sort buffers"));
+    HS_CUDA(ctx, cudaMemcpyAsync(n_dev.p, &n, 8, cudaMemcpyHostToDevice, s));
+    hs::launch_child_keys(cs, kb[0].as<uint32_t>(), vb[0].as<uint32_t>(), s);
+    uint32_t* kk[2] = {kb[0].as<uint32_t>(), kb[1].as<uint32_t>()};
+    uint32_t* vv[2] = {vb[0].as<uint32_t>(), vb[1].as<uint32_t>()};
+    hs::launch_radix_sort(kk, vv, n_dev.as<uint64_t>(), n, 0, passes, key_bits, sort_scratch.as<uint32_t>(), s);
+    const int fin = passes & 1;
+    hs::launch_child_segments(kk[fin], n, seg_start.as<uint32_t>(), seg_count.as<uint32_t>(), s);
+    HS_CUDA(ctx, cudaStreamSynchronize(s));
+    hs::PartTable pt{};
+    pt.cull[0] = h->cull.as<float4>();
+    pt.attr[0] = h->attr.as<float4>();
+    hs::ChildTable kids{seg_start.as<uint32_t>(), seg_count.as<uint32_t>(), vv[fin]};
+    uint64_t total = 0;
+    hs_status st = serialise_levels(ctx, o, pt, kids, {make_uint4(0, 0, HS_NO_NODE, 0)}, 0, n, n, &total);
+    if (st != HS_OK) return fail(st);
+    o->n = total;
+    hs::launch_child_alpha(o->attr.as<float4>(), o->cull.as<float4>(), total, s);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(cuda_err(ctx, e, "compact"));
+    *out = o;
     return HS_OK;
 }
 

@@ -11,6 +11,8 @@
 // look-back), copies its 32-byte cull and 256-byte attribute records to its new
 // index with parent / first_child rewritten, and emits its children as the next
 // frontier.  A node's new index is its frontier position + the level's base.
+// The same pass serialises compact's survivors (build.hpp:248-271), whose
+// children are no longer contiguous: then a ChildTable lists them per parent.
 #include "hs_device.cuh"
 #include "hs_kernels.h"
 #include "hs_scan.cuh"
@@ -19,7 +21,8 @@ namespace hs {
 
 constexpr int kAsmThreads = 256;
 
-__global__ void __launch_bounds__(kAsmThreads) k_assemble_level(PartTable parts, const uint4* __restrict__ fin,
+__global__ void __launch_bounds__(kAsmThreads) k_assemble_level(PartTable parts, ChildTable kids,
+                                                                const uint4* __restrict__ fin,
                                                                 uint64_t n_in, uint64_t pos_base,
                                                                 float4* __restrict__ out_cull,
                                                                 float4* __restrict__ out_attr,
@@ -40,9 +43,14 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble_level(PartTable parts,
     if (e < n_in) {
         f = fin[e];
         attr = parts.attr[f.x] + (uint64_t)f.y * kAttrVec4;
-        const float4 w = attr[15];
-        cc = __float_as_uint(w.x);
-        fc = __float_as_uint(w.y);
+        if (kids.count) {  // compaction: the surviving children, listed per parent
+            cc = kids.count[f.y];
+            fc = kids.start[f.y];
+        } else {
+            const float4 w = attr[15];
+            cc = __float_as_uint(w.x);
+            fc = __float_as_uint(w.y);
+        }
     }
     // block-exclusive scan of child counts
     uint32_t incl = cc;
@@ -95,15 +103,16 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble_level(PartTable parts,
         dst[q] = v;
     }
     dst[15] = make_float4(__uint_as_float(cc), __uint_as_float(new_fc), 0.0f, 0.0f);
-    for (uint32_t c = 0; c < cc; ++c) fout[excl + c] = make_uint4(f.x, fc + c, (uint32_t)pos, 0);
+    for (uint32_t c = 0; c < cc; ++c)
+        fout[excl + c] = make_uint4(f.x, kids.count ? kids.list[fc + c] : fc + c, (uint32_t)pos, 0);
 }
 
-void launch_assemble_level(const PartTable& parts, const uint4* fin, uint64_t n_in, uint64_t pos_base,
-                           float4* out_cull, float4* out_attr, uint4* fout, uint64_t* status,
+void launch_assemble_level(const PartTable& parts, const ChildTable& kids, const uint4* fin, uint64_t n_in,
+                           uint64_t pos_base, float4* out_cull, float4* out_attr, uint4* fout, uint64_t* status,
                            uint32_t* tile_counter, uint64_t* n_out, cudaStream_t s) {
     const uint64_t tiles = (n_in + kAsmThreads - 1) / kAsmThreads;
-    k_assemble_level<<<(unsigned)tiles, kAsmThreads, 0, s>>>(parts, fin, n_in, pos_base, out_cull, out_attr, fout,
-                                                             status, tile_counter, n_out);
+    k_assemble_level<<<(unsigned)tiles, kAsmThreads, 0, s>>>(parts, kids, fin, n_in, pos_base, out_cull, out_attr,
+                                                             fout, status, tile_counter, n_out);
     note_launch();
 }
 

@@ -16,11 +16,12 @@ struct ProjRec;
 
 // cut.cu
 void launch_select_cut(const float4* cull, uint64_t n, const CamParams& cam, float tau,
-                       uint32_t* out_node, float* out_t, float* out_alpha, uint64_t* status, uint32_t* tile_counter,
-                       uint64_t* count_out, cudaStream_t stream);
+                       uint32_t* out_node, float* out_t, float* out_alpha, uint32_t* scratch, uint64_t* count_out,
+                       cudaStream_t stream);
 void launch_copy_words(const void* src, void* dst, size_t bytes, cudaStream_t s);  // bytes % 8 == 0
 void launch_child_alpha(const float4* attr, float4* cull, uint64_t n, cudaStream_t stream);
-uint64_t select_cut_status_words(uint64_t n);
+uint64_t select_cut_scratch_words(uint64_t n);
+uint64_t select_cut_zero_words(uint64_t n);
 void launch_transfer_count(const uint32_t* node, const uint64_t* n_ptr, uint64_t n_max, uint32_t* epoch,
                            uint32_t prev, uint32_t cur, unsigned long long* out, cudaStream_t stream);
 
@@ -30,9 +31,36 @@ struct PartTable {
     const float4* cull[kMaxParts];
     const float4* attr[kMaxParts];
 };
-void launch_assemble_level(const PartTable& parts, const uint4* fin, uint64_t n_in, uint64_t pos_base,
-                           float4* out_cull, float4* out_attr, uint4* fout, uint64_t* status,
+// children of node j (part 0) = list[start[j] .. start[j] + count[j]); count == nullptr:
+// the parts' own contiguous child ranges
+struct ChildTable {
+    const uint32_t* start = nullptr;
+    const uint32_t* count = nullptr;
+    const uint32_t* list = nullptr;
+};
+void launch_assemble_level(const PartTable& parts, const ChildTable& kids, const uint4* fin, uint64_t n_in,
+                           uint64_t pos_base, float4* out_cull, float4* out_attr, uint4* fout, uint64_t* status,
                            uint32_t* tile_counter, uint64_t* n_out, cudaStream_t s);
+
+// compact.cu (build.hpp:168-272)
+struct CompactState {  // per node (n): reference node order
+    const float4* cull;
+    uint32_t* parent;       // parent (from the cull record)
+    uint32_t* ap;           // nearest alive ancestor
+    uint8_t* alive;
+    uint8_t* marked;
+    uint8_t* in_union;
+    uint32_t* below;        // has_union_below bits
+    uint64_t n;
+};
+void launch_compact_init(const CompactState& c, cudaStream_t s);
+void launch_alive_parents(const CompactState& c, cudaStream_t s);
+void launch_cut_union(const CompactState& c, const CamParams* cams, int ncams, float tau, cudaStream_t s);
+void launch_union_below(const CompactState& c, cudaStream_t s);
+void launch_kill(const CompactState& c, cudaStream_t s);
+void launch_child_keys(const CompactState& c, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+void launch_child_segments(const uint32_t* sorted_keys, uint64_t n, uint32_t* start, uint32_t* count,
+                           cudaStream_t s);
 uint64_t assemble_status_words(uint64_t n_in);
 
 // raster.cu
