@@ -348,6 +348,48 @@ inline void add(StageTimes* s, const hs_stage_times& t) {
     s->alpha_blend += t.alpha_blend;
 }
 
+// Device hierarchy -> host Hierarchy (reference node layout)
+inline Hierarchy download_hierarchy(Context& c, const hs_hierarchy* dh, std::uint32_t sh_degree) {
+    const std::uint64_t n = hs_hierarchy_node_count(dh);
+    std::vector<std::uint32_t> parent(n), fc(n), cc(n);
+    std::vector<float> bmin(3 * n), bmax(3 * n), mean(3 * n), scale(3 * n), rot(4 * n), fall(n), sh(48 * n);
+    hs_node_soa_out o{parent.data(), fc.data(), cc.data(), bmin.data(), bmax.data(),
+                      mean.data(),   scale.data(), rot.data(), fall.data(), sh.data()};
+    c.check(hs_hierarchy_download(c.ctx(), dh, &o));
+    Hierarchy h;
+    h.sh_degree = sh_degree;
+    h.nodes.resize(n);
+    for (std::uint64_t i = 0; i < n; ++i) {
+        HierarchyNode& nd = h.nodes[i];
+        nd.parent = parent[i];
+        nd.first_child = fc[i];
+        nd.child_count = cc[i];
+        for (int k = 0; k < 3; ++k) {
+            nd.bounds.min[k] = bmin[3 * i + k];
+            nd.bounds.max[k] = bmax[3 * i + k];
+            nd.g.mean[k] = mean[3 * i + k];
+            nd.g.scale[k] = scale[3 * i + k];
+        }
+        nd.g.rotation = Quatf{rot[4 * i], rot[4 * i + 1], rot[4 * i + 2], rot[4 * i + 3]};
+        nd.g.falloff = fall[i];
+        for (int k = 0; k < kShValues; ++k) nd.g.sh[k] = sh[48 * i + k];
+    }
+    return h;
+}
+
+// consolidate's global assembly (scene.hpp:228-316) on the device for parts
+// without cross-chunk backdrop pruning: chunk trees then the skybox tree under
+// one merged root, serialised breadth first.
+inline Hierarchy assemble(std::span<const Hierarchy> parts) {
+    auto& c = context();
+    std::vector<const hs_hierarchy*> dev;
+    for (const Hierarchy& p : parts) dev.push_back(c.device(p));
+    hs_hierarchy* out = nullptr;
+    c.check(hs_hierarchy_assemble(c.ctx(), dev.data(), static_cast<std::uint32_t>(dev.size()), &out));
+    std::unique_ptr<hs_hierarchy, void (*)(hs_hierarchy*)> keep(out, hs_hierarchy_destroy);
+    return download_hierarchy(c, out, parts.empty() ? 3u : parts[0].sh_degree);
+}
+
 }  // namespace gpu
 
 // ------------------------------------------------------------------ lod.hpp:52-92
@@ -422,6 +464,19 @@ inline RenderOutput render_hierarchy(const Hierarchy& h, const CameraModel& cam,
     c.check(hs_render_hierarchy(c.ctx(), c.device(h), &cc, tau, c.cut(), c.frame(), stages ? &st : nullptr));
     gpu::add(stages, st);
     return gpu::download_frame(c, ctx, cam);
+}
+
+// ------------------------------------------------------------------ build.hpp:168-272
+inline Hierarchy compact(const Hierarchy& h, std::span<const CameraModel> cams, float tau_min = 3.0f,
+                         float tau_max = 0.0f) {
+    if (h.nodes.empty()) throw Error(Errc::InvalidArgument, "InvalidArgument: compact needs a hierarchy");
+    auto& c = gpu::context();
+    std::vector<hs_camera> cc;
+    for (const CameraModel& cam : cams) cc.push_back(gpu::to_c(cam));
+    hs_hierarchy* out = nullptr;
+    c.check(hs_hierarchy_compact(c.ctx(), c.device(h), cc.data(), cc.size(), tau_min, tau_max, &out));
+    std::unique_ptr<hs_hierarchy, void (*)(hs_hierarchy*)> keep(out, hs_hierarchy_destroy);
+    return gpu::download_hierarchy(c, out, h.sh_degree);
 }
 
 // ------------------------------------------------------------------ io.hpp:375-408

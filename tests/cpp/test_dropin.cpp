@@ -112,6 +112,30 @@ int main() {
     for (std::size_t i = 1; i < 6; ++i) CHECK(rep.frames[i].transferred == 0);
     for (std::size_t i = 1; i < 6; i += 2) CHECK(rep.frames[i].stages.cut_expand == 0.0);
 
+    // compact (build.hpp:168-272): leaves kept, every interior node has >= 2 children
+    {
+        std::vector<CameraModel> cams{cam};
+        const Hierarchy c = compact(h, cams, 3.0f);
+        CHECK(c.nodes.size() <= h.nodes.size());
+        CHECK(c.leaf_count() == h.leaf_count());
+        for (const auto& nd : c.nodes) CHECK(nd.is_leaf() || nd.child_count >= 2);
+        threw = false;
+        try {
+            compact(h, std::span<const CameraModel>{}, 3.0f);
+        } catch (const Error& err) {
+            threw = err.code() == Errc::InvalidArgument;
+        }
+        CHECK(threw);
+    }
+    // assemble (consolidate's BFS layout): two parts under one root
+    {
+        const Hierarchy parts[2] = {h, h};
+        const Hierarchy a = gpu::assemble(parts);
+        CHECK(a.nodes.size() == 2 * h.nodes.size() + 1);
+        CHECK(a.nodes[0].child_count == 2 && a.nodes[0].first_child == 1);
+        CHECK(a.leaf_count() == 2 * h.leaf_count());
+    }
+
     // read_hierarchy error code (io.hpp:375-387)
     threw = false;
     try {

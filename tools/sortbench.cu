@@ -6,6 +6,7 @@
 #include <random>
 #include <algorithm>
 #include "../paper_2406_12080_b200/csrc/hs_kernels.h"
+#include <cub/device/device_radix_sort.cuh>
 
 namespace hs { std::atomic<unsigned long long> g_kernel_launches{0}; }
 #ifdef SORT_PROF
@@ -68,6 +69,23 @@ int main() {
         }
         printf("dist=%d n=%9llu passes=%d: %8.1f us (%.1f us/pass) %s err=%s\n", dist, (unsigned long long)n, passes,
                best * 1e3, best * 1e3 / passes, good ? "sorted" : "NOT SORTED", cudaGetErrorString(cudaGetLastError()));
+        {   // calibration only: CUB's onesweep on the same keys and bit range (not used by the library)
+            size_t tmp_bytes = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k[0], k[1], v[0], v[1], (int)n, begin, begin + 8 * passes);
+            void* tmp; cudaMalloc(&tmp, tmp_bytes);
+            float cbest = 1e9;
+            for (int rep = 0; rep < 10; ++rep) {
+                cudaMemcpy(k[0], hk.data(), n * 4, cudaMemcpyHostToDevice);
+                cudaMemcpy(v[0], hv.data(), n * 4, cudaMemcpyHostToDevice);
+                cudaEventRecord(e0);
+                cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k[0], k[1], v[0], v[1], (int)n, begin, begin + 8 * passes);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms; cudaEventElapsedTime(&ms, e0, e1); cbest = std::min(cbest, ms);
+            }
+            printf("   cub SortPairs same bits: %8.1f us\n", cbest * 1e3);
+            cudaFree(tmp);
+        }
         for (int b = 0; b < 2; ++b) { cudaFree(k[b]); cudaFree(v[b]); }
         cudaFree(scratch); cudaFree(dn);
     }
