@@ -396,6 +396,8 @@ struct Projected {  // render.hpp:52-73
     float falloff_eff = 0, parent_falloff_eff = 0;
     float t = 1.0f;
     float inv_k = 1.0f;
+    bool color_clamped[3] = {false, false, false};  // render.hpp:160-163 (backward only)
+    bool falloff_pos = false, parent_falloff_pos = false;
 };
 
 // x86-64 cvttss2si: NaN, +-inf and out-of-range values produce INT_MIN.
@@ -508,10 +510,15 @@ inline Projected project(const RenderSplat& s, const Camera& cam) {  // render.h
     float c[3] = {0.5f, 0.5f, 0.5f};
     for (int k = 0; k < kShCoeffs; ++k)
         for (int ch = 0; ch < 3; ++ch) c[ch] += b[k] * s.sh[k * 3 + ch];
-    for (int ch = 0; ch < 3; ++ch) p.color[ch] = smax(c[ch], 0.0f);
+    for (int ch = 0; ch < 3; ++ch) {
+        p.color_clamped[ch] = c[ch] < 0.0f;
+        p.color[ch] = smax(c[ch], 0.0f);
+    }
 
     p.falloff_eff = smax(s.falloff, 0.0f);
     p.parent_falloff_eff = smax(s.parent_falloff, 0.0f);
+    p.falloff_pos = s.falloff > 0.0f;
+    p.parent_falloff_pos = s.parent_falloff > 0.0f;
     p.t = s.t;
     p.inv_k = 1.0f / static_cast<float>(std::max(1, s.transition_siblings));
     p.culled = false;
@@ -737,6 +744,315 @@ inline void render_hierarchy(const Hierarchy& h, const Camera& cam, float tau, R
 // C ABI (include/hsplat_b200.h) so tests feed identical host buffers to both.
 // =====================================================================
 using namespace oracle;
+
+// ---------------------------------------------------------------- render_backward (render.hpp:427-702)
+// Restated for T = float with the reference's structure: a per-tile pixel walk
+// mirroring the forward blend into per-(tile, entry) accumulators, an ordered
+// reduction over tiles, then the per-splat chain rule (SH, conic -> covariance,
+// EWA Jacobian, quaternion, scale).  Test infrastructure: the GPU backward is
+// held to it within a tolerance (summation orders differ).
+struct PixelAlphaFull {  // render.hpp:189-200
+    bool skip = true;
+    float alpha = 0, g = 0, a_self = 0, a_parent = 0, split = 0;
+    bool self_live = false, parent_live = false, self_clamped = false, parent_clamped = false;
+};
+
+inline PixelAlphaFull splat_alpha_full(const Projected& p, float px, float py) {  // render.hpp:201-231
+    PixelAlphaFull r;
+    const float dx = px - p.mean2d[0];
+    const float dy = py - p.mean2d[1];
+    const float power = -0.5f * (p.conic[0] * dx * dx + p.conic[2] * dy * dy) - p.conic[1] * dx * dy;
+    if (!(power <= 0.0f)) return r;
+    r.g = std::exp(power);
+    const float self_raw = p.falloff_eff * p.alpha_scale * r.g;
+    r.self_clamped = self_raw > kAlphaMax;
+    const float self = r.self_clamped ? kAlphaMax : self_raw;
+    r.self_live = self >= kAlphaMin;
+    r.a_self = r.self_live ? self : 0.0f;
+    if (p.t < 1.0f) {
+        const float par_raw = p.parent_falloff_eff * p.alpha_scale * r.g;
+        r.parent_clamped = par_raw > kAlphaMax;
+        const float par = r.parent_clamped ? kAlphaMax : par_raw;
+        r.parent_live = par >= kAlphaMin;
+        if (r.parent_live) {
+            r.a_parent = par;
+            r.split = 1.0f - std::pow(1.0f - par, p.inv_k);
+        }
+        r.alpha = p.t * r.a_self + (1.0f - p.t) * r.split;
+    } else {
+        r.alpha = r.a_self;
+    }
+    r.skip = !(r.alpha > 0.0f);
+    return r;
+}
+
+inline void sh_basis_grad(float x, float y, float z, float g[16][3]) {  // sh.hpp:46-68
+    const float xx = x * x, yy = y * y, zz = z * z;
+    const float c1 = (float)kSh1, c2[5] = {(float)kSh2[0], (float)kSh2[1], (float)kSh2[2], (float)kSh2[3],
+                                          (float)kSh2[4]};
+    const float c3[7] = {(float)kSh3[0], (float)kSh3[1], (float)kSh3[2], (float)kSh3[3],
+                         (float)kSh3[4], (float)kSh3[5], (float)kSh3[6]};
+    const float v[16][3] = {{0, 0, 0},
+                            {0, -c1, 0},
+                            {0, 0, c1},
+                            {-c1, 0, 0},
+                            {c2[0] * y, c2[0] * x, 0},
+                            {0, c2[1] * z, c2[1] * y},
+                            {c2[2] * (-2.0f * x), c2[2] * (-2.0f * y), c2[2] * (4.0f * z)},
+                            {c2[3] * z, 0, c2[3] * x},
+                            {c2[4] * (2.0f * x), c2[4] * (-2.0f * y), 0},
+                            {c3[0] * (6.0f * x * y), c3[0] * (3.0f * xx - 3.0f * yy), 0},
+                            {c3[1] * (y * z), c3[1] * (x * z), c3[1] * (x * y)},
+                            {c3[2] * (-2.0f * x * y), c3[2] * (4.0f * zz - xx - 3.0f * yy), c3[2] * (8.0f * y * z)},
+                            {c3[3] * (-6.0f * x * z), c3[3] * (-6.0f * y * z), c3[3] * (6.0f * zz - 3.0f * xx - 3.0f * yy)},
+                            {c3[4] * (4.0f * zz - 3.0f * xx - yy), c3[4] * (-2.0f * x * y), c3[4] * (8.0f * x * z)},
+                            {c3[5] * (2.0f * x * z), c3[5] * (-2.0f * y * z), c3[5] * (xx - yy)},
+                            {c3[6] * (3.0f * xx - 3.0f * yy), c3[6] * (-6.0f * x * y), 0}};
+    std::memcpy(g, v, sizeof(v));
+}
+
+struct BlendAcc {  // render.hpp:447-453
+    float mean2d[2] = {0, 0}, conic[3] = {0, 0, 0}, color[3] = {0, 0, 0};
+    float falloff = 0, parent_falloff = 0, t = 0, alpha_scale = 0, inv_depth = 0;
+};
+
+struct Grads {  // RenderGradsT<float> (render.hpp:427-438)
+    std::vector<float> mean, scale, rotation, falloff, parent_falloff, t, sh, mean2d;
+    float exposure[12] = {};
+};
+
+inline void render_backward(const RenderSplat* splats, std::size_t n, const Camera& cam, const RenderOutput& ctx,
+                            const float expo[12], const float* lg_img, const float* dg_img, Grads& out) {
+    require(!ctx.projected.empty() || n == 0, kMissingForwardState,
+            "render_backward needs the context of a previous forward pass");
+    const int w = ctx.width, h = ctx.height;
+    const std::size_t plane = static_cast<std::size_t>(w) * h;
+    out.mean.assign(3 * n, 0.0f);
+    out.scale.assign(3 * n, 0.0f);
+    out.rotation.assign(4 * n, 0.0f);
+    out.falloff.assign(n, 0.0f);
+    out.parent_falloff.assign(n, 0.0f);
+    out.t.assign(n, 0.0f);
+    out.sh.assign(48 * n, 0.0f);
+    out.mean2d.assign(2 * n, 0.0f);
+    for (float& v : out.exposure) v = 0.0f;
+    // exposure: per-pixel outer products in pixel order (render.hpp:481-488)
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            const std::size_t i = static_cast<std::size_t>(y) * w + x;
+            const float lg[3] = {lg_img[i], lg_img[plane + i], lg_img[2 * plane + i]};
+            const float c[3] = {ctx.color[i], ctx.color[plane + i], ctx.color[2 * plane + i]};
+            for (int r = 0; r < 3; ++r) {
+                for (int k = 0; k < 3; ++k) out.exposure[4 * r + k] += lg[r] * c[k];
+                out.exposure[4 * r + 3] += lg[r];
+            }
+        }
+    const std::size_t n_tiles = static_cast<std::size_t>(ctx.tiles_x) * ctx.tiles_y;
+    std::vector<std::vector<BlendAcc>> tile_acc(n_tiles);
+    parallel_for(n_tiles, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t tile = lo; tile < hi; ++tile) {
+            const std::size_t begin = ctx.tile_start[tile], end = ctx.tile_start[tile + 1];
+            tile_acc[tile].assign(end - begin, BlendAcc());
+            if (begin == end) continue;
+            const int bx = static_cast<int>(tile % ctx.tiles_x) * kTileSize;
+            const int by = static_cast<int>(tile / ctx.tiles_x) * kTileSize;
+            for (int y = by; y < std::min(by + kTileSize, h); ++y)
+                for (int x = bx; x < std::min(bx + kTileSize, w); ++x) {
+                    const std::size_t pi = static_cast<std::size_t>(y) * w + x;
+                    const float px = static_cast<float>(x) + 0.5f, py = static_cast<float>(y) + 0.5f;
+                    const float lg[3] = {lg_img[pi], lg_img[plane + pi], lg_img[2 * plane + pi]};
+                    float pre[3];  // E_lin^T lg
+                    for (int k = 0; k < 3; ++k) pre[k] = sum3(expo[k] * lg[0], expo[4 + k] * lg[1], expo[8 + k] * lg[2]);
+                    const float dgrad = dg_img ? dg_img[pi] : 0.0f;
+                    const float ct[3] = {ctx.color[pi], ctx.color[plane + pi], ctx.color[2 * plane + pi]};
+                    const float dt = ctx.depth[pi];
+                    float trans = 1.0f, cp[3] = {0, 0, 0}, dp = 0.0f;
+                    for (std::size_t e = begin; e < end; ++e) {
+                        const Projected& p = ctx.projected[ctx.tile_entries[e]];
+                        const PixelAlphaFull a = splat_alpha_full(p, px, py);
+                        if (a.skip) continue;
+                        const float test = trans * (1.0f - a.alpha);
+                        if (test < kTransmittanceEps) break;
+                        BlendAcc& acc = tile_acc[tile][e - begin];
+                        const float aw = a.alpha * trans;
+                        for (int k = 0; k < 3; ++k) cp[k] += p.color[k] * aw;
+                        dp += p.inv_depth * aw;
+                        for (int k = 0; k < 3; ++k) acc.color[k] += pre[k] * aw;
+                        acc.inv_depth += dgrad * aw;
+                        const float om = 1.0f - a.alpha;
+                        float cs[3];
+                        for (int k = 0; k < 3; ++k) cs[k] = (ct[k] - cp[k]) / om;
+                        float g_alpha = sum3(pre[0] * (p.color[0] * trans - cs[0]), pre[1] * (p.color[1] * trans - cs[1]),
+                                             pre[2] * (p.color[2] * trans - cs[2]));
+                        g_alpha += dgrad * (p.inv_depth * trans - (dt - dp) / om);
+                        float g_g = 0.0f, g_ascale = 0.0f;
+                        const float g_self = p.t < 1.0f ? g_alpha * p.t : g_alpha;
+                        if (p.t < 1.0f) {
+                            acc.t += g_alpha * (a.a_self - a.split);
+                            if (a.parent_live && !a.parent_clamped) {
+                                const float dsplit = p.inv_k * std::pow(1.0f - a.a_parent, p.inv_k - 1.0f);
+                                const float g_par = g_alpha * (1.0f - p.t) * dsplit;
+                                acc.parent_falloff += g_par * p.alpha_scale * a.g;
+                                g_ascale += g_par * p.parent_falloff_eff * a.g;
+                                g_g += g_par * p.parent_falloff_eff * p.alpha_scale;
+                            }
+                        }
+                        if (a.self_live && !a.self_clamped) {
+                            acc.falloff += g_self * p.alpha_scale * a.g;
+                            g_ascale += g_self * p.falloff_eff * a.g;
+                            g_g += g_self * p.falloff_eff * p.alpha_scale;
+                        }
+                        acc.alpha_scale += g_ascale;
+                        const float g_power = g_g * a.g;
+                        const float dx = px - p.mean2d[0], dy = py - p.mean2d[1];
+                        acc.conic[0] += g_power * -0.5f * dx * dx;
+                        acc.conic[1] += g_power * -dx * dy;
+                        acc.conic[2] += g_power * -0.5f * dy * dy;
+                        acc.mean2d[0] += g_power * (p.conic[0] * dx + p.conic[1] * dy);
+                        acc.mean2d[1] += g_power * (p.conic[1] * dx + p.conic[2] * dy);
+                        trans = test;
+                    }
+                }
+        }
+    });
+    std::vector<BlendAcc> sa(n);  // ordered reduction: tile index, then position (render.hpp:595-612)
+    for (std::size_t tile = 0; tile < n_tiles; ++tile) {
+        const std::size_t begin = ctx.tile_start[tile];
+        for (std::size_t e = 0; e < tile_acc[tile].size(); ++e) {
+            const BlendAcc& src = tile_acc[tile][e];
+            BlendAcc& d = sa[ctx.tile_entries[begin + e]];
+            for (int k = 0; k < 2; ++k) d.mean2d[k] += src.mean2d[k];
+            for (int k = 0; k < 3; ++k) d.conic[k] += src.conic[k], d.color[k] += src.color[k];
+            d.falloff += src.falloff;
+            d.parent_falloff += src.parent_falloff;
+            d.t += src.t;
+            d.alpha_scale += src.alpha_scale;
+            d.inv_depth += src.inv_depth;
+        }
+    }
+    const float(&W)[3][4] = cam.w2c;
+    float campos[3];
+    cam.position(campos);
+    const float fx = cam.fx, fy = cam.fy;
+    parallel_for(n, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            const Projected& p = ctx.projected[i];
+            if (p.culled) continue;
+            const RenderSplat& s = splats[i];
+            const BlendAcc& acc = sa[i];
+            out.mean2d[2 * i] = acc.mean2d[0];
+            out.mean2d[2 * i + 1] = acc.mean2d[1];
+            out.t[i] = acc.t;
+            out.falloff[i] = p.falloff_pos ? acc.falloff : 0.0f;
+            out.parent_falloff[i] = p.parent_falloff_pos ? acc.parent_falloff : 0.0f;
+            float cg[3];
+            for (int k = 0; k < 3; ++k) cg[k] = p.color_clamped[k] ? 0.0f : acc.color[k];
+            float tc[3] = {s.mean[0] - campos[0], s.mean[1] - campos[1], s.mean[2] - campos[2]};
+            const float dist = std::sqrt(sum3(tc[0] * tc[0], tc[1] * tc[1], tc[2] * tc[2]));
+            const float dir[3] = {tc[0] / dist, tc[1] / dist, tc[2] / dist};
+            // eval_sh_backward (sh.hpp:83-96)
+            float b[16], gb[16][3], dirg[3] = {0, 0, 0};
+            sh_basis(dir[0], dir[1], dir[2], b);
+            sh_basis_grad(dir[0], dir[1], dir[2], gb);
+            for (int k = 0; k < kShCoeffs; ++k) {
+                float wk = 0.0f;
+                for (int ch = 0; ch < 3; ++ch) {
+                    out.sh[48 * i + 3 * k + ch] += b[k] * cg[ch];
+                    wk += s.sh[3 * k + ch] * cg[ch];
+                }
+                for (int a = 0; a < 3; ++a) dirg[a] += wk * gb[k][a];
+            }
+            const float dd = sum3(dir[0] * dirg[0], dir[1] * dirg[1], dir[2] * dirg[2]);
+            float mg[3];
+            for (int a = 0; a < 3; ++a) mg[a] = (dirg[a] - dir[a] * dd) / dist;
+            // conic -> 2D covariance: gm = -Q gq Q
+            const float gq[2][2] = {{acc.conic[0], acc.conic[1] / 2.0f}, {acc.conic[1] / 2.0f, acc.conic[2]}};
+            const float q[2][2] = {{p.conic[0], p.conic[1]}, {p.conic[1], p.conic[2]}};
+            float t1[2][2], gm[2][2];
+            for (int r = 0; r < 2; ++r)
+                for (int c = 0; c < 2; ++c) t1[r][c] = q[r][0] * gq[0][c] + q[r][1] * gq[1][c];
+            for (int r = 0; r < 2; ++r)
+                for (int c = 0; c < 2; ++c) gm[r][c] = -(t1[r][0] * q[0][c] + t1[r][1] * q[1][c]);
+            if (acc.alpha_scale != 0.0f && p.det_pre > 0.0f) {  // sqrt(det_pre / det_post)
+                const float g_dpre = acc.alpha_scale * p.alpha_scale / (2.0f * p.det_pre);
+                const float g_dpost = -acc.alpha_scale * p.alpha_scale / (2.0f * p.det_post);
+                const float m00 = p.cov2d[0] - kDilation2d, m11 = p.cov2d[3] - kDilation2d;
+                gm[0][0] += g_dpre * m11 + g_dpost * p.cov2d[3];
+                gm[1][1] += g_dpre * m00 + g_dpost * p.cov2d[0];
+                gm[0][1] += -g_dpre * p.cov2d[1] - g_dpost * p.cov2d[1];
+                gm[1][0] += -g_dpre * p.cov2d[2] - g_dpost * p.cov2d[2];
+            }
+            // rotation, camera covariance, Jacobian (recomputed as in project)
+            const float* q4 = s.rot_wxyz;
+            const float qn = std::sqrt(sum4(q4[0] * q4[0], q4[1] * q4[1], q4[2] * q4[2], q4[3] * q4[3]));
+            const float qu[4] = {q4[0] / qn, q4[1] / qn, q4[2] / qn, q4[3] / qn};
+            const float xw = qu[0], xx = qu[1], xy = qu[2], xz = qu[3];
+            const float tx2 = 2.0f * xx, ty2 = 2.0f * xy, tz2q = 2.0f * xz;
+            float R[3][3];
+            R[0][0] = 1.0f - (ty2 * xy + tz2q * xz);
+            R[0][1] = ty2 * xx - tz2q * xw;
+            R[0][2] = tz2q * xx + ty2 * xw;
+            R[1][0] = ty2 * xx + tz2q * xw;
+            R[1][1] = 1.0f - (tx2 * xx + tz2q * xz);
+            R[1][2] = tz2q * xy - tx2 * xw;
+            R[2][0] = tz2q * xx - ty2 * xw;
+            R[2][1] = tz2q * xy + tx2 * xw;
+            R[2][2] = 1.0f - (tx2 * xx + ty2 * xy);
+            float m3[3][3], S3[3][3], A[3][3], cc[3][3];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) m3[r][c] = R[r][c] * s.scale[c];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) S3[r][c] = sum3(m3[r][0] * m3[c][0], m3[r][1] * m3[c][1], m3[r][2] * m3[c][2]);
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) A[r][c] = sum3(W[r][0] * S3[0][c], W[r][1] * S3[1][c], W[r][2] * S3[2][c]);
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) cc[r][c] = sum3(A[r][0] * W[c][0], A[r][1] * W[c][1], A[r][2] * W[c][2]);
+            const float tx = p.cam_point[0], ty = p.cam_point[1], tz = p.cam_point[2], tz2 = tz * tz;
+            const float J[2][3] = {{fx / tz, 0.0f, -fx * tx / tz2}, {0.0f, fy / tz, -fy * ty / tz2}};
+            float gmJ[2][3], gcc[3][3], gJ[2][3];
+            for (int r = 0; r < 2; ++r)
+                for (int c = 0; c < 3; ++c) gmJ[r][c] = gm[r][0] * J[0][c] + gm[r][1] * J[1][c];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) gcc[r][c] = J[0][r] * gmJ[0][c] + J[1][r] * gmJ[1][c];
+            for (int r = 0; r < 2; ++r)
+                for (int c = 0; c < 3; ++c) gJ[r][c] = 2.0f * sum3(gmJ[r][0] * cc[0][c], gmJ[r][1] * cc[1][c], gmJ[r][2] * cc[2][c]);
+            float gc[3] = {0, 0, 0};
+            gc[0] += gJ[0][2] * (-fx / tz2);
+            gc[1] += gJ[1][2] * (-fy / tz2);
+            gc[2] += gJ[0][0] * (-fx / tz2) + gJ[1][1] * (-fy / tz2) + gJ[0][2] * (2.0f * fx * tx / (tz2 * tz)) +
+                     gJ[1][2] * (2.0f * fy * ty / (tz2 * tz));
+            gc[0] += acc.mean2d[0] * fx / tz;
+            gc[1] += acc.mean2d[1] * fy / tz;
+            gc[2] += -acc.mean2d[0] * fx * tx / tz2 - acc.mean2d[1] * fy * ty / tz2;
+            gc[2] += -acc.inv_depth / tz2;
+            for (int a = 0; a < 3; ++a) out.mean[3 * i + a] = mg[a] + sum3(W[0][a] * gc[0], W[1][a] * gc[1], W[2][a] * gc[2]);
+            // camera covariance -> world covariance -> scale and rotation
+            float t2[3][3], g3[3][3], gm3[3][3], rtg[3][3], grot[3][3];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) t2[r][c] = sum3(W[0][r] * gcc[0][c], W[1][r] * gcc[1][c], W[2][r] * gcc[2][c]);
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) g3[r][c] = sum3(t2[r][0] * W[0][c], t2[r][1] * W[1][c], t2[r][2] * W[2][c]);
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) gm3[r][c] = 2.0f * sum3(g3[r][0] * m3[0][c], g3[r][1] * m3[1][c], g3[r][2] * m3[2][c]);
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) rtg[r][c] = sum3(R[0][r] * gm3[0][c], R[1][r] * gm3[1][c], R[2][r] * gm3[2][c]);
+            for (int a = 0; a < 3; ++a) out.scale[3 * i + a] = rtg[a][a];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) grot[r][c] = gm3[r][c] * s.scale[c];
+            // quat_grad_from_rot (render.hpp:458-475)
+            float gqu[4];
+            gqu[0] = 2.0f * (xz * (grot[1][0] - grot[0][1]) + xy * (grot[0][2] - grot[2][0]) + xx * (grot[2][1] - grot[1][2]));
+            gqu[1] = 2.0f * (xy * (grot[0][1] + grot[1][0]) + xz * (grot[0][2] + grot[2][0]) + xw * (grot[2][1] - grot[1][2])) -
+                     4.0f * xx * (grot[1][1] + grot[2][2]);
+            gqu[2] = 2.0f * (xx * (grot[0][1] + grot[1][0]) + xw * (grot[0][2] - grot[2][0]) + xz * (grot[1][2] + grot[2][1])) -
+                     4.0f * xy * (grot[0][0] + grot[2][2]);
+            gqu[3] = 2.0f * (xw * (grot[1][0] - grot[0][1]) + xx * (grot[0][2] + grot[2][0]) + xy * (grot[1][2] + grot[2][1])) -
+                     4.0f * xz * (grot[0][0] + grot[1][1]);
+            const float qd = sum4(qu[0] * gqu[0], qu[1] * gqu[1], qu[2] * gqu[2], qu[3] * gqu[3]);
+            for (int a = 0; a < 4; ++a) out.rotation[4 * i + a] = (gqu[a] - qu[a] * qd) / qn;
+        }
+    });
+}
 
 extern "C" {
 
@@ -1188,6 +1504,32 @@ void or_hierarchy_export(void* hv, uint32_t* parent, uint32_t* first_child, uint
         falloff[i] = nd.g.falloff;
         std::memcpy(sh + 48 * i, nd.g.sh, 48 * sizeof(float));
     }
+}
+
+// render_backward over the context kept by or_render_forward(keep_ctx = 1);
+// exposure: 12 floats row-major [E_lin | E_off] or NULL (identity); depth_grad may be NULL.
+// out: mean 3N, scale 3N, rotation 4N, falloff N, parent_falloff N, t N, sh 48N, mean2d 2N, exposure 12
+int or_render_backward(void* fv, const or_splats* s, uint64_t n, const or_camera* c, const float* exposure,
+                       const float* loss_grad, const float* depth_grad, float* mean, float* scale, float* rot,
+                       float* fall, float* pfall, float* t, float* sh, float* mean2d, float* expo_out) {
+    OR_TRY({
+        auto* f = static_cast<OrFrame*>(fv);
+        require(f->out.tile_start.size() > 0, kMissingForwardState,
+                "render_backward needs the context of a previous forward pass");
+        auto sp = soa_to_splats(s, n);
+        const float ident[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
+        Grads g;
+        render_backward(sp.data(), sp.size(), to_cam(c), f->out, exposure ? exposure : ident, loss_grad, depth_grad, g);
+        std::memcpy(mean, g.mean.data(), 12 * n);
+        std::memcpy(scale, g.scale.data(), 12 * n);
+        std::memcpy(rot, g.rotation.data(), 16 * n);
+        std::memcpy(fall, g.falloff.data(), 4 * n);
+        std::memcpy(pfall, g.parent_falloff.data(), 4 * n);
+        std::memcpy(t, g.t.data(), 4 * n);
+        std::memcpy(sh, g.sh.data(), 192 * n);
+        std::memcpy(mean2d, g.mean2d.data(), 8 * n);
+        std::memcpy(expo_out, g.exposure, 48);
+    });
 }
 
 // psnr (image.hpp:111-122): over all channels in double; mse <= 0 -> 99 dB; capped at 99.

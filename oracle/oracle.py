@@ -59,6 +59,8 @@ _SIGS = {
     "or_hierarchy_leaf_count": (C.c_uint64, [_vp]),
     "or_hierarchy_size": (C.c_uint64, [_vp]),
     "or_hierarchy_export": (None, [_vp, u32p, u32p, u32p, f32p, f32p, f32p, f32p, f32p, f32p, f32p]),
+    "or_render_backward": (C.c_int, [_vp, C.POINTER(or_splats), C.c_uint64, C.POINTER(or_camera), f32p, f32p, f32p,
+                                     f32p, f32p, f32p, f32p, f32p, f32p, f32p, f32p, f32p]),
     "or_compact": (C.c_int, [_vp, C.POINTER(or_camera), C.c_uint64, C.c_float, C.c_float, C.POINTER(_vp)]),
     "or_select_cut": (C.c_int, [_vp, C.POINTER(or_camera), C.c_float, u32p, f32p, f32p, u64p, f64p]),
     "or_cut_render_splats": (C.c_int, [_vp, u32p, f32p, f32p, C.c_uint64, f32p, f32p, f32p, f32p, f32p, f32p,
@@ -383,3 +385,22 @@ def compact(oh: OracleHierarchy, cams, tau_min: float = 3.0, tau_max: float = 0.
     finally:
         lib().or_hierarchy_free(out)
     return d
+
+
+def render_backward(frame: OracleFrame, splats, cam, loss_grad, depth_grad=None, exposure=None) -> dict:
+    """render_backward<float> (render.hpp:427-702) over `frame` (render_forward with keep_ctx)."""
+    s, keep = _splats(splats)
+    n = len(keep)
+    lg = np.ascontiguousarray(loss_grad, np.float32)
+    dg = None if depth_grad is None else np.ascontiguousarray(depth_grad, np.float32)
+    ex = None if exposure is None else np.ascontiguousarray(exposure, np.float32).reshape(12)
+    out = {"mean": np.zeros((n, 3), np.float32), "scale": np.zeros((n, 3), np.float32),
+           "rotation": np.zeros((n, 4), np.float32), "falloff": np.zeros(n, np.float32),
+           "parent_falloff": np.zeros(n, np.float32), "t": np.zeros(n, np.float32),
+           "sh": np.zeros((n, 48), np.float32), "mean2d": np.zeros((n, 2), np.float32),
+           "exposure": np.zeros((3, 4), np.float32)}
+    _chk(lib().or_render_backward(frame.h, C.byref(s), n, C.byref(camera(cam)), _p(ex, C.c_float), _p(lg, C.c_float),
+                                  _p(dg, C.c_float), *[_p(out[k], C.c_float) for k in
+                                                       ("mean", "scale", "rotation", "falloff", "parent_falloff", "t",
+                                                        "sh", "mean2d", "exposure")]))
+    return out
