@@ -220,6 +220,25 @@ hs_status hs_render_cut(hs_context* ctx, const hs_hierarchy* h, const hs_cut* cu
 /* replaces: render_forward<float> (render.hpp:244-354) over caller splats */
 hs_status hs_render_splats(hs_context* ctx, const hs_splat_soa* splats, uint64_t n, const hs_camera* cam, hs_frame* f,
                            hs_stage_times* times);
+/* RenderGradsT<float> (render.hpp:427-438), host arrays for N splats */
+typedef struct hs_grads_out {
+    float* mean;           /* 3N */
+    float* scale;          /* 3N */
+    float* rot_wxyz;       /* 4N, w.r.t. the raw (possibly non-unit) quaternion */
+    float* falloff;        /* N */
+    float* parent_falloff; /* N */
+    float* t;              /* N */
+    float* sh;             /* 48N */
+    float* mean2d;         /* 2N, screen-space positional gradient */
+    float* exposure;       /* 12, row-major 3x4 */
+} hs_grads_out;
+/* replaces: render_backward<float> (render.hpp:427-702) over the context of the
+ * last render into `f` (hs_render_splats: its splats; hs_render_hierarchy /
+ * hs_render_cut: the cut's interpolated RenderSplats): loss_grad 3*H*W plane-major (w.r.t. the
+ * exposed colour), depth_grad H*W or NULL, exposure 12 floats row-major
+ * [E_lin | E_off] or NULL (identity).  Deterministic (no atomics). */
+hs_status hs_render_backward(hs_context* ctx, hs_frame* f, const float* loss_grad, const float* depth_grad,
+                             const float* exposure, const hs_grads_out* out);
 /* completes an async render (no-op when synchronous) */
 hs_status hs_frame_wait(hs_context* ctx, hs_frame* f);
 hs_status hs_frame_get_info(hs_context* ctx, hs_frame* f, hs_frame_info* info);

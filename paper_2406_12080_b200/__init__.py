@@ -682,6 +682,33 @@ class Renderer:
             stages.add(st)
         return self._output(want_context)
 
+    def render_backward(self, loss_grad, depth_grad=None, exposure=None) -> dict:
+        """render_backward<float> (render.hpp:427-702) over the context of the last
+        render_forward of this renderer: gradients w.r.t. every splat attribute and the
+        exposure matrix (3x4), for loss_grad (3, H, W) w.r.t. the exposed colour."""
+        fi = N.hs_frame_info()
+        _check(N.lib().hs_frame_get_info(self.ctx, self._frame, C.byref(fi)), self.ctx)
+        n, H, W = int(fi.n_splats), int(fi.height), int(fi.width)
+        lg = np.ascontiguousarray(loss_grad, np.float32)
+        if lg.shape != (3, H, W):
+            raise Error(int(Errc.DimensionMismatch) + 1, "DimensionMismatch: loss gradient must be H x W x 3")
+        dg = None
+        if depth_grad is not None:
+            dg = np.ascontiguousarray(depth_grad, np.float32)
+            if dg.shape != (H, W):
+                raise Error(int(Errc.DimensionMismatch) + 1, "DimensionMismatch: depth gradient must be H x W x 1")
+        ex = None if exposure is None else np.ascontiguousarray(exposure, np.float32).reshape(12)
+        out = {"mean": np.zeros((n, 3), np.float32), "scale": np.zeros((n, 3), np.float32),
+               "rotation": np.zeros((n, 4), np.float32), "falloff": np.zeros(n, np.float32),
+               "parent_falloff": np.zeros(n, np.float32), "t": np.zeros(n, np.float32),
+               "sh": np.zeros((n, 48), np.float32), "mean2d": np.zeros((n, 2), np.float32),
+               "exposure": np.zeros((3, 4), np.float32)}
+        go = N.hs_grads_out(*[N.ptr(out[k], C.c_float) for k in ("mean", "scale", "rotation", "falloff",
+                                                                  "parent_falloff", "t", "sh", "mean2d", "exposure")])
+        _check(N.lib().hs_render_backward(self.ctx, self._frame, N.ptr(lg, C.c_float), N.ptr(dg, C.c_float),
+                                          N.ptr(ex, C.c_float), C.byref(go)), self.ctx)
+        return out
+
     def render_hierarchy(self, h, cam: CameraModel, tau: float, *, want_context: bool = False,
                          stages: StageTimes | None = None, return_cut: bool = False):
         dh = self._dev(h)
@@ -734,6 +761,11 @@ def render_forward(splats: RenderSplats, cam: CameraModel, ctx_out: dict | None 
     if ctx_out is not None:
         ctx_out.update(out.context)
     return out
+
+
+def render_backward(loss_grad, depth_grad=None, exposure=None) -> dict:
+    """render_backward<float> (render.hpp:427-702) over the last render_forward of the default renderer."""
+    return default_renderer().render_backward(loss_grad, depth_grad, exposure)
 
 
 def render_hierarchy(h, cam: CameraModel, tau: float, ctx_out: dict | None = None,

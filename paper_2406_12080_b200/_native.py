@@ -41,6 +41,11 @@ class hs_splat_soa(C.Structure):
 hs_splat_soa_out = hs_splat_soa
 
 
+class hs_grads_out(C.Structure):
+    _fields_ = [(k, C.POINTER(C.c_float)) for k in ("mean", "scale", "rot_wxyz", "falloff", "parent_falloff", "t",
+                                                    "sh", "mean2d", "exposure")]
+
+
 class hs_stage_times(C.Structure):
     _fields_ = [("cut_expand", C.c_double), ("weights", C.c_double), ("preprocess", C.c_double),
                 ("duplicate", C.c_double), ("tile_ranges", C.c_double), ("alpha_blend", C.c_double)]
@@ -94,6 +99,7 @@ _SIGS = {
     "hs_render_cut": (C.c_int, [_vp, _vp, _vp, C.POINTER(hs_camera), _vp, C.POINTER(hs_stage_times)]),
     "hs_render_splats": (C.c_int, [_vp, C.POINTER(hs_splat_soa), C.c_uint64, C.POINTER(hs_camera), _vp,
                                    C.POINTER(hs_stage_times)]),
+    "hs_render_backward": (C.c_int, [_vp, _vp, f32p, f32p, f32p, C.POINTER(hs_grads_out)]),
     "hs_frame_wait": (C.c_int, [_vp, _vp]),
     "hs_frame_get_info": (C.c_int, [_vp, _vp, C.POINTER(hs_frame_info)]),
     "hs_frame_download": (C.c_int, [_vp, _vp, f32p, f32p, f32p, i32p]),

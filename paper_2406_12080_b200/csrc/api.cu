@@ -131,7 +131,7 @@ struct hs_frame {
     int W = 0, H = 0, tiles_x = 0, tiles_y = 0, passes = 0;
     DBuf tile_order;
     DBuf proj, dinfo, dupcount, offsets, zkeys[2], zvals[2], keys[2], vals[2], dupk, dupv, keys64, ranges, color, depth, trans, touched, dbg16,
-        splat_attr, stats, scratch;
+        splat_attr, stats, scratch, bw;
     DevStats* h_stats = nullptr;  // pinned, mapped
     DevStats* h_stats_dev = nullptr;  // device alias of h_stats
     DevStats* h_stats_dl = nullptr;  // pinned, snapshot taken with an async read-back
@@ -1101,6 +1101,71 @@ hs_status hs_render_splats(hs_context* ctx, const hs_splat_soa* sp, uint64_t n, 
     s = enqueue_raster(ctx, f);
     if (s != HS_OK) return s;
     if (!ctx->async) return finish_frame(ctx, f, true);
+    return HS_OK;
+}
+
+hs_status hs_render_backward(hs_context* ctx, hs_frame* f, const float* loss_grad, const float* depth_grad,
+                             const float* exposure, const hs_grads_out* out) {
+    if (!ctx || !f || !out || !loss_grad) return HS_INVALID_ARGUMENT;
+    if (f->pending) {
+        hs_status st = finish_frame(ctx, f, false);
+        if (st != HS_OK) return st;
+    }
+    if (!f->have_result)  // render.hpp:432-433
+        return set_err(ctx, HS_MISSING_FORWARD_STATE, "render_backward needs the context of a previous forward pass");
+    const uint64_t n = f->h_stats->n_splats, d = f->h_stats->sort_n;
+    const float4* attr = f->attr;
+    if (f->from_cut) {
+        // a hierarchy frame: its context's splats are the cut's interpolated RenderSplats
+        // (render_hierarchy keeps cut_render_splats, render.hpp:706-720)
+        const size_t sw = std::max<uint64_t>(n, 1);
+        HS_CUDA(ctx, f->splat_attr.ensure(sw * 256 + sw * 62 * 4));
+        float4* rec = f->splat_attr.as<float4>();
+        float* so = reinterpret_cast<float*>(rec + 16 * sw);
+        float *mean = so, *scale = so + 3 * sw, *rot = so + 6 * sw, *sh = so + 10 * sw, *fall = so + 58 * sw,
+              *pfall = so + 59 * sw, *t = so + 60 * sw;
+        int* k = reinterpret_cast<int*>(so + 61 * sw);
+        hs::launch_assemble(f->attr, f->cut_node, f->cut_t, f->n_ptr, n, mean, scale, rot, sh, fall, pfall, t, k,
+                            ctx->stream);
+        hs::launch_pack_splats(mean, scale, rot, sh, fall, pfall, t, k, f->n_ptr, n, rec, ctx->stream);
+        attr = rec;
+    }
+    const size_t plane = (size_t)f->W * f->H;
+    // device scratch: lg 3P | dg P | aux 4N | acc 13D | expo partial 256*12 | grads 65N + 12
+    const size_t words = 4 * plane + 4 * n + hs::backward_acc_words(std::max<uint64_t>(d, 1)) + 256 * 12 + 65 * n + 12;
+    HS_CUDA(ctx, f->bw.ensure(words * 4 + 64));
+    float* b = f->bw.as<float>();
+    float* lg = b;
+    float* dg = depth_grad ? lg + 3 * plane : nullptr;
+    float4* aux = reinterpret_cast<float4*>(lg + 4 * plane);  // 4 * plane floats: 16-byte aligned
+    float* acc = reinterpret_cast<float*>(aux + n);
+    float* part = acc + hs::backward_acc_words(std::max<uint64_t>(d, 1));
+    float* g = part + 256 * 12;
+    cudaStream_t s = ctx->stream;
+    HS_CUDA(ctx, cudaMemcpyAsync(lg, loss_grad, plane * 12, cudaMemcpyHostToDevice, s));
+    if (dg) HS_CUDA(ctx, cudaMemcpyAsync(dg, depth_grad, plane * 4, cudaMemcpyHostToDevice, s));
+    HS_CUDA(ctx, cudaMemsetAsync(g, 0, (65 * n + 12) * 4, s));
+    hs::BwExposure ex{{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0}};
+    if (exposure) std::memcpy(ex.e, exposure, sizeof(ex.e));
+    hs::BwGrads go{g, g + 3 * n, g + 6 * n, g + 10 * n, g + 11 * n, g + 12 * n, g + 13 * n, g + 61 * n, g + 63 * n};
+    const int fin = f->passes & 1;
+    hs::launch_backward(attr, n, f->cam, f->ranges.as<uint2>(), f->keys[fin].as<uint32_t>(),
+                        f->vals[fin].as<uint32_t>(), f->proj.as<ProjRec>(), f->dinfo.as<uint4>(),
+                        f->dupcount.as<uint32_t>(), &f->stats.as<DevStats>()->sort_n, std::max<uint64_t>(d, 1),
+                        f->color.as<float>(), f->depth.as<float>(), lg, dg, ex, aux, acc, part, go, s);
+    HS_CUDA(ctx, cudaGetLastError());
+    HS_CUDA(ctx, cudaStreamSynchronize(s));
+    struct {
+        float* dst;
+        const float* src;
+        size_t count;
+    } outs[] = {{out->mean, go.mean, 3 * n},       {out->scale, go.scale, 3 * n},
+                {out->rot_wxyz, go.rot, 4 * n},    {out->falloff, go.falloff, n},
+                {out->parent_falloff, go.parent_falloff, n}, {out->t, go.t, n},
+                {out->sh, go.sh, 48 * n},          {out->mean2d, go.mean2d, 2 * n},
+                {out->exposure, go.exposure, 12}};
+    for (const auto& o : outs)
+        if (o.dst && o.count) HS_TRY(copy_sync(ctx, o.dst, o.src, o.count * 4, cudaMemcpyDeviceToHost));
     return HS_OK;
 }
 

@@ -63,6 +63,23 @@ void launch_child_segments(const uint32_t* sorted_keys, uint64_t n, uint32_t* st
                            cudaStream_t s);
 uint64_t assemble_status_words(uint64_t n_in);
 
+// backward.cu (render_backward, render.hpp:427-702)
+struct BwExposure {
+    float e[12];  // row-major [E_lin | E_off]
+};
+struct BwGrads {  // device outputs, zeroed by the caller
+    float *mean, *scale, *rot, *falloff, *parent_falloff, *t, *sh, *mean2d, *exposure;
+};
+uint64_t backward_acc_words(uint64_t d);
+void launch_pack_splats(const float* mean, const float* scale, const float* rot, const float* sh, const float* fall,
+                        const float* pfall, const float* t, const int* k, const uint64_t* n_ptr, uint64_t n_max,
+                        float4* rec, cudaStream_t s);
+void launch_backward(const float4* attr, uint64_t n, const CamParams& cam, const uint2* ranges, const uint32_t* keys,
+                     const uint32_t* vals, const ProjRec* proj, const uint4* dinfo, const uint32_t* dupcount,
+                     const uint64_t* sort_n, uint64_t d_cap, const float* color, const float* depth, const float* lg,
+                     const float* dg, const BwExposure& expo, float4* aux, float* acc, float* expo_partial,
+                     BwGrads out, cudaStream_t s);
+
 // raster.cu
 void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,
                        const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint4* dinfo,

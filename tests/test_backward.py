@@ -211,3 +211,26 @@ def test_gpu_backward_deterministic_and_band0(renderer):
     g2 = renderer.render_backward(lg)
     for k in GRAD_KEYS + ("exposure",):
         assert np.array_equal(g1[k].view(np.uint32), g2[k].view(np.uint32)), k
+
+
+@pytest.mark.gpu
+def test_gpu_backward_hierarchy_frame_c1(renderer):
+    """Backward over a render_hierarchy frame (C1: 100K leaves, 640x480): gradients w.r.t.
+    the cut's interpolated splats, against the oracle over cut_render_splats."""
+    from paper_2406_12080_b200 import scenes
+    cfg = scenes.CONFIGS["c1"]
+    h = scenes.hierarchy(cfg)
+    cam = scenes.camera(cfg, 250)
+    rng = Rng(91)
+    lg = rng.uniform(-1.0, 1.0, (3, cam.height, cam.width))
+    dg = rng.uniform(-1.0, 1.0, (cam.height, cam.width))
+    out, cut = renderer.render_hierarchy(h, cam, cfg.tau, return_cut=True)
+    got = renderer.render_backward(lg, dg, EXPO)
+    oh = orc.OracleHierarchy(h)
+    sp = orc.cut_render_splats(oh, cut.node, cut.t, cut.alpha_prime)
+    f = orc.render_forward(sp, cam, keep_ctx=True)
+    want = orc.render_backward(f, sp, cam, lg, dg, EXPO)
+    assert got["mean"].shape[0] == len(cut)
+    for k in GRAD_KEYS:
+        scale = float(np.abs(want[k]).max()) + 1e-12
+        assert _close(got[k], want[k], 5e-3, 1e-4 * scale), k
