@@ -22,6 +22,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -109,6 +110,7 @@ struct CameraModel {
     int width = 0, height = 0;
     Vec2f focal, principal;
     Mat34f world_to_camera;
+    Mat34f exposure{{{1, 0, 0, 0}, {0, 1, 0, 0}, {0, 0, 1, 0}}};  // affine colour map (model.hpp), training only
 };
 
 struct HierarchyNode {
@@ -179,7 +181,20 @@ struct ForwardContext {
     std::vector<std::uint32_t> tile_entries;  // splat ids in per-tile depth order
     std::vector<std::uint64_t> sorted_keys;   // tile << 32 | bits(z)
     bool valid = false;
+    std::uint64_t serial = 0;  // the device frame this view was taken from (render_backward)
 };
+
+// RenderGradsT (render.hpp:427-438)
+template <class T>
+struct RenderGradsT {
+    std::vector<Vec3f> mean, scale;
+    std::vector<std::array<float, 4>> rotation;  // w.r.t. the raw wxyz vector
+    std::vector<T> falloff, parent_falloff, t;
+    std::vector<std::array<T, kShValues>> sh;
+    std::vector<Vec2f> mean2d;
+    Mat34f exposure;
+};
+using RenderGrads = RenderGradsT<float>;
 
 struct FrameStats {
     std::size_t rendered = 0;
@@ -231,6 +246,8 @@ public:
     }
     hs_context* ctx() const { return ctx_; }
     hs_frame* frame() const { return frame_; }
+    std::uint64_t next_serial() { return ++serial_; }
+    std::uint64_t serial() const { return serial_; }
     hs_cut* cut() const { return cut_; }
 
     // Device residency of a host hierarchy (uploaded once, cached).
@@ -278,6 +295,7 @@ private:
     hs_context* ctx_ = nullptr;
     hs_frame* frame_ = nullptr;
     hs_cut* cut_ = nullptr;
+    std::uint64_t serial_ = 0;  // renders into frame_ so far
     std::map<std::pair<const void*, std::size_t>, std::unique_ptr<hs_hierarchy, HierarchyDeleter>> cache_;
 };
 
@@ -312,6 +330,7 @@ inline std::vector<CutEntry> download_cut(Context& c, const hs_cut* cut) {
 }
 
 inline RenderOutput download_frame(Context& c, ForwardContext* ctx_out, const CameraModel& cam) {
+    const std::uint64_t serial = c.next_serial();
     hs_frame_info info{};
     c.check(hs_frame_get_info(c.ctx(), c.frame(), &info));
     RenderOutput out;
@@ -334,6 +353,7 @@ inline RenderOutput download_frame(Context& c, ForwardContext* ctx_out, const Ca
         ctx_out->tiles_y = info.tiles_y;
         ctx_out->cam = cam;
         ctx_out->valid = true;
+        ctx_out->serial = serial;
     }
     return out;
 }
@@ -464,6 +484,50 @@ inline RenderOutput render_hierarchy(const Hierarchy& h, const CameraModel& cam,
     c.check(hs_render_hierarchy(c.ctx(), c.device(h), &cc, tau, c.cut(), c.frame(), stages ? &st : nullptr));
     gpu::add(stages, st);
     return gpu::download_frame(c, ctx, cam);
+}
+
+// ------------------------------------------------------------------ render.hpp:427-702
+// Gradients over the device state of the render `ctx` was taken from (the last
+// render_forward / render_hierarchy of this process's context).
+template <class T>
+RenderGradsT<T> render_backward(const ForwardContext& ctx, const Image<T>& loss_grad,
+                                const Image<T>* depth_grad = nullptr) {
+    static_assert(std::is_same_v<T, float>, "the GPU path differentiates in float");
+    auto& c = gpu::context();
+    if (!ctx.valid || ctx.serial != c.serial())
+        throw Error(Errc::MissingForwardState,
+                    "MissingForwardState: render_backward needs the context of a previous forward pass");
+    const int w = ctx.cam.width, h = ctx.cam.height;
+    if (loss_grad.width != w || loss_grad.height != h || loss_grad.channels != 3)
+        throw Error(Errc::DimensionMismatch, "DimensionMismatch: loss gradient must be H x W x 3");
+    if (depth_grad && (depth_grad->width != w || depth_grad->height != h || depth_grad->channels != 1))
+        throw Error(Errc::DimensionMismatch, "DimensionMismatch: depth gradient must be H x W x 1");
+    hs_frame_info info{};
+    c.check(hs_frame_get_info(c.ctx(), c.frame(), &info));
+    const std::size_t n = info.n_splats;
+    std::vector<float> mean(3 * n), scale(3 * n), rot(4 * n), fall(n), pfall(n), tt(n), sh(48 * n), m2(2 * n), ex(12);
+    float expo[12];
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 4; ++k) expo[4 * r + k] = ctx.cam.exposure(r, k);
+    hs_grads_out o{mean.data(), scale.data(), rot.data(), fall.data(), pfall.data(), tt.data(), sh.data(), m2.data(),
+                   ex.data()};
+    c.check(hs_render_backward(c.ctx(), c.frame(), loss_grad.data.data(), depth_grad ? depth_grad->data.data() : nullptr,
+                               expo, &o));
+    RenderGradsT<T> g;
+    g.mean.resize(n), g.scale.resize(n), g.rotation.resize(n), g.sh.resize(n), g.mean2d.resize(n);
+    g.falloff = std::move(fall);
+    g.parent_falloff = std::move(pfall);
+    g.t = std::move(tt);
+    for (std::size_t i = 0; i < n; ++i) {
+        for (int k = 0; k < 3; ++k) g.mean[i][k] = mean[3 * i + k], g.scale[i][k] = scale[3 * i + k];
+        for (int k = 0; k < 4; ++k) g.rotation[i][k] = rot[4 * i + k];
+        for (int k = 0; k < kShValues; ++k) g.sh[i][k] = sh[48 * i + k];
+        g.mean2d[i][0] = m2[2 * i];
+        g.mean2d[i][1] = m2[2 * i + 1];
+    }
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 4; ++k) g.exposure(r, k) = ex[4 * r + k];
+    return g;
 }
 
 // ------------------------------------------------------------------ build.hpp:168-272

@@ -112,6 +112,38 @@ int main() {
     for (std::size_t i = 1; i < 6; ++i) CHECK(rep.frames[i].transferred == 0);
     for (std::size_t i = 1; i < 6; i += 2) CHECK(rep.frames[i].stages.cut_expand == 0.0);
 
+    // render_backward (render.hpp:427-702): band-0 closed form (test_render.cpp:556-576)
+    {
+        CameraModel bc;
+        bc.width = bc.height = 48;
+        bc.focal.x() = bc.focal.y() = 70.0f;
+        bc.principal.x() = bc.principal.y() = 24.0f;
+        for (int r = 0; r < 3; ++r) bc.world_to_camera(r, r) = 1.0f;
+        RenderSplat s;
+        s.mean[2] = 6.0f;
+        s.scale = Vec3f{{0.4f, 0.4f, 0.4f}};
+        s.falloff = 0.5f;
+        s.sh[0] = s.sh[1] = s.sh[2] = 1.0f;
+        std::vector<RenderSplat> one{s};
+        ForwardContext bctx;
+        const RenderOutput bo = render_forward<float>(std::span<const RenderSplat>(one), bc, &bctx);
+        const double n = 48.0 * 48.0 * 3.0;
+        Image<float> lg(48, 48, 3, static_cast<float>(1.0 / n));
+        const RenderGrads g = render_backward<float>(bctx, lg);
+        double mass = 0.0;
+        for (float t : bo.transmittance.data) mass += 1.0 - t;
+        const double want = 0.28209479177387814 * mass / n;
+        CHECK(std::abs(g.sh[0][0] - want) <= 1e-4 * std::abs(want));
+        // a context from an older render is stale
+        (void)render_forward<float>(std::span<const RenderSplat>(one), bc, nullptr);
+        threw = false;
+        try {
+            render_backward<float>(bctx, lg);
+        } catch (const Error& err) {
+            threw = err.code() == Errc::MissingForwardState;
+        }
+        CHECK(threw);
+    }
     // compact (build.hpp:168-272): leaves kept, every interior node has >= 2 children
     {
         std::vector<CameraModel> cams{cam};
