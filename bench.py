@@ -342,37 +342,41 @@ def main():
 
     # ---- end to end through the public API: camera in (host struct -> kernel parameters),
     # the whole RenderOutput (colour, inverse depth, transmittance) out to pinned host
-    # memory every frame.  Two frame objects: frame i's read-back (copy stream) overlaps
-    # frame i+1's kernels; a frame object is re-rendered only after its read-back landed.
+    # memory every frame.  NF frame objects in a ring: frame i's read-back (copy stream)
+    # overlaps the kernels of frames i+1.., and a frame object is re-rendered only after
+    # its previous read-back landed.
+    NF = 3
     f32 = N.C.POINTER(N.C.c_float)
-    frames = [r._frame, N.C.c_void_p()]
-    hs._check(L.hs_frame_create(r.ctx, N.C.byref(frames[1])), r.ctx)
-    hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, timed[0], cfg.tau, r._cut, frames[1], None), r.ctx)
-    pinned = [torch.empty(5 * W * H, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    frames = [r._frame] + [N.C.c_void_p() for _ in range(NF - 1)]
+    for fr in frames[1:]:
+        hs._check(L.hs_frame_create(r.ctx, N.C.byref(fr)), r.ctx)
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, timed[0], cfg.tau, r._cut, fr, None), r.ctx)
+    pinned = [torch.empty(5 * W * H, dtype=torch.float32, pin_memory=True) for _ in range(NF)]
     outs = [(N.C.cast(p.data_ptr(), f32), N.C.cast(p.data_ptr() + 12 * W * H, f32),
              N.C.cast(p.data_ptr() + 16 * W * H, f32)) for p in pinned]
+    e2e_cams = [c.to_c() for c in cams[args.warmup: args.warmup + args.steps]]  # host camera structs
     rc = N.C.c_int32()
     r.set_async(True)
     barrier()
     torch.cuda.synchronize()
     r.synchronize()
     t0 = time.perf_counter()
-    for i, cam in enumerate(cams[args.warmup: args.warmup + args.steps]):
-        fi = i & 1
-        if i >= 2:
+    for i, c in enumerate(e2e_cams):
+        fi = i % NF
+        if i >= NF:
             hs._check(L.hs_frame_download_wait(r.ctx, frames[fi], N.C.byref(rc)), r.ctx)
-        c = cam.to_c()
         hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, frames[fi], None), r.ctx)
         hs._check(L.hs_frame_download_async(r.ctx, frames[fi], *outs[fi]), r.ctx)
-    for i in range(max(0, len(timed) - 2), len(timed)):
-        hs._check(L.hs_frame_download_wait(r.ctx, frames[i & 1], N.C.byref(rc)), r.ctx)
+    for i in range(max(0, len(timed) - NF), len(timed)):
+        hs._check(L.hs_frame_download_wait(r.ctx, frames[i % NF], N.C.byref(rc)), r.ctx)
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     r.set_async(False)
-    hs._check(L.hs_frame_wait(r.ctx, frames[1]), r.ctx)
-    L.hs_frame_destroy(frames[1])
+    for fr in frames[1:]:
+        hs._check(L.hs_frame_wait(r.ctx, fr), r.ctx)
+        L.hs_frame_destroy(fr)
     e2e = {"value": world * len(timed) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": N.C.sizeof(N.hs_camera),
            "d2h_bytes_per_step": 20 * W * H + N.C.sizeof(N.hs_frame_info),
-           "pipelining": "2 frame objects; read-back of frame i on a copy stream overlaps frame i+1"}
+           "pipelining": f"{NF} frame objects; read-back of frame i on a copy stream overlaps frames i+1.."}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and h is not None:
