@@ -131,7 +131,7 @@ struct hs_frame {
     int W = 0, H = 0, tiles_x = 0, tiles_y = 0, passes = 0;
     DBuf tile_order;
     DBuf proj, dinfo, dupcount, offsets, zkeys[2], zvals[2], keys[2], vals[2], dupk, dupv, keys64, ranges, color, depth, trans, touched, dbg16,
-        splat_attr, stats, scratch, bw;
+        splat_attr, stats, scratch, bw, huge;
     DevStats* h_stats = nullptr;  // pinned, mapped
     DevStats* h_stats_dev = nullptr;  // device alias of h_stats
     DevStats* h_stats_dl = nullptr;  // pinned, snapshot taken with an async read-back
@@ -265,7 +265,7 @@ uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 // The two radix sorts zero their own look-back words on the device (sized from
 // the device-side key counts).
 struct ScratchLayout {
-    size_t vis_counter = 0, dup_counter = 4, blend_counter = 8, vis_status = 64, dup_status = 0, zero_bytes = 0,
+    size_t vis_counter = 0, dup_counter = 4, blend_counter = 8, huge_counter = 12, vis_status = 64, dup_status = 0, zero_bytes = 0,
            depth_sort = 0, tile_sort = 0, total = 0;
 };
 ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int tile_passes) {
@@ -301,6 +301,7 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
         HS_CUDA(ctx, f->dupv.ensure(f->cap_dup * 4));
         HS_CUDA(ctx, f->dbg16.ensure(cs * 64));
     }
+    HS_CUDA(ctx, f->huge.ensure(hs::huge_queue_slots(f->cap_dup) * 8));
     HS_CUDA(ctx, f->ranges.ensure((size_t)tiles * 8));
     HS_CUDA(ctx, f->tile_order.ensure((size_t)tiles * 4));
     const size_t plane = (size_t)cp.width * cp.height;
@@ -360,7 +361,8 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     uint32_t* kb[2] = {f->keys[0].as<uint32_t>(), f->keys[1].as<uint32_t>()};
     uint32_t* vb[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
     hs::launch_duplicate_sorted(ids, f->dinfo.as<uint4>(), f->proj.as<ProjRec>(), f->offsets.as<uint32_t>(),
-                                &ds->n_visible_sorted, f->n_max, &ds->sort_n, f->cap_dup, cp.tiles_x, kb[0], vb[0], s);
+                                &ds->n_visible_sorted, f->n_max, &ds->sort_n, f->cap_dup, cp.tiles_x, kb[0], vb[0],
+                                f->huge.as<uint2>(), reinterpret_cast<uint32_t*>(sc + L.huge_counter), s);
     if (ctx->debug) {
         hs::launch_make_keys(kb[0], vb[0], f->dinfo.as<uint4>(), &ds->sort_n, f->cap_dup, f->dupk.as<uint64_t>(), s);
         HS_CUDA(ctx, cudaMemcpyAsync(f->dupv.p, f->vals[0].p, f->cap_dup * 4, cudaMemcpyDeviceToDevice, s));

@@ -157,6 +157,17 @@ __device__ __forceinline__ uint32_t tile_reach_mask(const float4& p0, const floa
     const float qthr = -2.0f * p3.y;  // p3.y = -qthr / 2 (exact scalings)
     if (qthr < 0.0f) return 0u;
     const float a = p0.z, b = p0.w, c = p1.x;
+    {   // fast path: all four corner pixel centres inside the (convex) ellipse => every
+        // block is reachable.  Setting a bit is always safe (the blend evaluates exactly);
+        // only clearing one needs the conservative test below.
+        const float cx0 = ((float)px0 + 0.5f) - p0.x, cx1 = ((float)(px0 + 15) + 0.5f) - p0.x;
+        const float cy0 = ((float)py0 + 0.5f) - p0.y, cy1 = ((float)(py0 + 15) + 0.5f) - p0.y;
+        const float q00 = __fmaf_rn(__fmaf_rn(a, cx0, 2.0f * b * cy0), cx0, c * cy0 * cy0);
+        const float q01 = __fmaf_rn(__fmaf_rn(a, cx0, 2.0f * b * cy1), cx0, c * cy1 * cy1);
+        const float q10 = __fmaf_rn(__fmaf_rn(a, cx1, 2.0f * b * cy0), cx1, c * cy0 * cy0);
+        const float q11 = __fmaf_rn(__fmaf_rn(a, cx1, 2.0f * b * cy1), cx1, c * cy1 * cy1);
+        if (fmaxf(fmaxf(q00, q01), fmaxf(q10, q11)) <= qthr) return 0xFFu;
+    }
     const float b2 = 2.0f * b, sx = -b * p3.w, sy = -b * p3.z;
     // column edges x = X + {0, 7, 8, 15}: Q on the edge is (c y + 2 b x) y + a x^2
     float xe[4], bx2[4], axx[4], ymin[4];

@@ -103,9 +103,11 @@ void launch_compact_visible(const uint32_t* dupcount, const uint4* dinfo, const 
 void launch_dup_offsets(const uint32_t* ids, const uint32_t* dupcount, const uint64_t* v_ptr, uint64_t n_max,
                         uint32_t* offsets, uint64_t* status, uint32_t* counter, uint64_t* total_out,
                         uint64_t* sort_n_out, uint64_t capacity, unsigned long long* overflows, cudaStream_t s);
+uint64_t huge_queue_slots(uint64_t dup_max);
 void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const ProjRec* proj, const uint32_t* offsets,
                              const uint64_t* v_ptr, uint64_t n_max, const uint64_t* sort_n_ptr, uint64_t dup_max,
-                             int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+                             int tiles_x, uint32_t* keys, uint32_t* vals, uint2* huge_q, uint32_t* huge_n,
+                             cudaStream_t s);
 void launch_ranges(const uint32_t* keys, const uint64_t* n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s);
 void launch_make_keys(const uint32_t* tiles, const uint32_t* ids, const uint4* dinfo, const uint64_t* n_ptr,
                       uint64_t n_max, uint64_t* out, cudaStream_t s);

@@ -168,12 +168,19 @@ __global__ void __launch_bounds__(kScanThreads) k_dup_offsets(const uint32_t* __
 // (tile, id) pairs of the depth-sorted splats, tiles of a splat row-major.
 // One lane per splat for small footprints; splats covering more than 4 tiles
 // are emitted cooperatively by the whole warp (one lane per tile).
+// Splats covering more than kHugeArea tiles (e.g. skybox splats near the image
+// plane at 4K: the reference culls only at z <= 0.01) are handed to
+// k_duplicate_huge through a queue instead of being emitted by one warp, which
+// would serialise millions of keys on a few warps.
+constexpr int kHugeArea = 1024;
+
 __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __restrict__ ids,
                                                           const uint4* __restrict__ dinfo,
                                                           const uint32_t* __restrict__ offsets,
                                                           const uint64_t* __restrict__ v_ptr,
                                                           const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
-                                                          uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                                                          uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                          uint2* __restrict__ huge_q, uint32_t* __restrict__ huge_n) {
     const uint64_t n = *v_ptr;
     if (*sort_n_ptr == 0) return;  // nothing to emit, or over capacity
     const int lane = threadIdx.x & 31;
@@ -190,6 +197,7 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __rest
         }
         const int w = tx1 - tx0, area = w * (ty1 - ty0);
         const bool big = area > 4;
+        const bool huge = area > kHugeArea;
         if (!big) {
             uint32_t oo = o;
             for (int ty = ty0; ty < ty1; ++ty)
@@ -199,7 +207,14 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __rest
                     ++oo;
                 }
         }
-        for (uint32_t m = __ballot_sync(0xffffffffu, big); m; m &= m - 1) {
+        const uint32_t hm = __ballot_sync(0xffffffffu, huge);
+        if (hm) {  // one queue slot per huge splat (< D / kHugeArea of them)
+            uint32_t slot = 0;
+            if (lane == __ffs(hm) - 1) slot = atomicAdd(huge_n, (uint32_t)__popc(hm));
+            slot = __shfl_sync(0xffffffffu, slot, __ffs(hm) - 1) + __popc(hm & ((1u << lane) - 1u));
+            if (huge) huge_q[slot] = make_uint2(id, o);
+        }
+        for (uint32_t m = __ballot_sync(0xffffffffu, big && !huge); m; m &= m - 1) {
             const int src = __ffs(m) - 1;
             const uint32_t sid = __shfl_sync(0xffffffffu, id, src), so = __shfl_sync(0xffffffffu, o, src);
             const int sx0 = __shfl_sync(0xffffffffu, tx0, src), sy0 = __shfl_sync(0xffffffffu, ty0, src);
@@ -212,21 +227,64 @@ __global__ void __launch_bounds__(256) k_duplicate_sorted(const uint32_t* __rest
     }
 }
 
+// The huge splats, one CTA at a time each (row-major tiles, rows over warps).
+__global__ void __launch_bounds__(256) k_duplicate_huge(const uint4* __restrict__ dinfo,
+                                                        const uint2* __restrict__ huge_q,
+                                                        const uint32_t* __restrict__ huge_n,
+                                                        const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
+                                                        uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    if (*sort_n_ptr == 0) return;
+    const uint32_t nq = *huge_n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
+        const uint2 e = huge_q[q];
+        const uint4 di = dinfo[e.x];
+        const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
+        const int w = tx1 - tx0;
+        for (int r = warp; r < ty1 - ty0; r += 8) {
+            const uint64_t row = (uint64_t)e.y + (uint64_t)r * w;
+            const uint32_t key0 = (uint32_t)((ty0 + r) * tiles_x + tx0);
+            for (int c = lane; c < w; c += 32) {
+                keys[row + c] = (key0 + c) << 8;
+                vals[row + c] = e.x;
+            }
+        }
+    }
+}
+
 // Reach masks: bit b of the key's low byte is set when the splat's alpha can
 // pass the 1/255 floor somewhere in 8x4 block b of the tile (tile_reach_mask).
 // The tile sort orders by bits [8, 32) and carries the mask along; the blend
-// never stages entries that cannot touch its block.  One thread per entry.
+// never stages entries that cannot touch its block.  Four entries per thread
+// with all their loads issued first (the record gathers are latency-bound).
+constexpr int kMaskItems = 4;
 __global__ void __launch_bounds__(256) k_reach_masks(uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                                                      const ProjRec* __restrict__ proj,
                                                      const uint64_t* __restrict__ n_ptr, int tiles_x) {
     const uint64_t n = *n_ptr;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t key = keys[i];
-        const ProjRec* r = proj + vals[i];
-        const float4 p0 = r->p0, p1 = r->p1, p3 = r->p3;
-        const int t = (int)(key >> 8);
-        const uint32_t mask = tile_reach_mask(p0, p1, p3, (t % tiles_x) * kTile, (t / tiles_x) * kTile);
-        keys[i] = key | mask;
+    const uint64_t chunk = (uint64_t)blockDim.x * kMaskItems;
+    for (uint64_t b0 = (uint64_t)blockIdx.x * chunk; b0 < n; b0 += (uint64_t)gridDim.x * chunk) {
+        uint32_t key[kMaskItems], id[kMaskItems];
+        float4 p0[kMaskItems], p1[kMaskItems], p3[kMaskItems];
+#pragma unroll
+        for (int k = 0; k < kMaskItems; ++k) {
+            const uint64_t i = b0 + (uint64_t)k * blockDim.x + threadIdx.x;
+            key[k] = i < n ? keys[i] : 0u;
+            id[k] = i < n ? vals[i] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < kMaskItems; ++k) {
+            const ProjRec* r = proj + id[k];
+            p0[k] = r->p0, p1[k] = r->p1, p3[k] = r->p3;
+        }
+#pragma unroll
+        for (int k = 0; k < kMaskItems; ++k) {
+            const uint64_t i = b0 + (uint64_t)k * blockDim.x + threadIdx.x;
+            if (i >= n) continue;
+            const int t = (int)(key[k] >> 8);
+            const uint32_t mask = tile_reach_mask(p0[k], p1[k], p3[k], (t % tiles_x) * kTile, (t / tiles_x) * kTile);
+            keys[i] = key[k] | mask;
+        }
     }
 }
 
@@ -286,12 +344,20 @@ void launch_dup_offsets(const uint32_t* ids, const uint32_t* dupcount, const uin
     note_launch();
 }
 
+uint64_t huge_queue_slots(uint64_t dup_max) { return dup_max / kHugeArea + 1; }
+
 void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const ProjRec* proj, const uint32_t* offsets,
                              const uint64_t* v_ptr, uint64_t n_max, const uint64_t* sort_n_ptr, uint64_t dup_max,
-                             int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
-    k_duplicate_sorted<<<flat_grid(n_max), 256, 0, s>>>(ids, dinfo, offsets, v_ptr, sort_n_ptr, tiles_x, keys, vals);
+                             int tiles_x, uint32_t* keys, uint32_t* vals, uint2* huge_q, uint32_t* huge_n,
+                             cudaStream_t s) {
+    k_duplicate_sorted<<<flat_grid(n_max), 256, 0, s>>>(ids, dinfo, offsets, v_ptr, sort_n_ptr, tiles_x, keys, vals,
+                                                        huge_q, huge_n);
     note_launch();
-    k_reach_masks<<<flat_grid(dup_max), 256, 0, s>>>(keys, vals, proj, sort_n_ptr, tiles_x);
+    k_duplicate_huge<<<(unsigned)order_sms() * 4, 256, 0, s>>>(dinfo, huge_q, huge_n, sort_n_ptr, tiles_x,
+                                                                        keys, vals);
+    note_launch();
+    k_reach_masks<<<flat_grid((dup_max + kMaskItems - 1) / kMaskItems), 256, 0, s>>>(keys, vals, proj, sort_n_ptr,
+                                                                                      tiles_x);
     note_launch();
 }
 

@@ -59,17 +59,19 @@ __global__ void __launch_bounds__(256) k_sort_hist(const uint32_t* __restrict__ 
     }
 }
 
-// Histograms for short keys (key_bits <= 13, e.g. tile indices): one shared
-// atomic per key on the full 2^key_bits-bin histogram -- spread over thousands
-// of bins instead of 256 per pass -- folded into the per-pass digit
-// histograms at the end.
-constexpr int kDirectBitsMax = 13;
+// Histograms for short keys (key_bits <= 15, e.g. tile indices: 8160 tiles at
+// 1080p, 32400 at 4K): one shared atomic per key on the full 2^key_bits-bin
+// histogram (dynamic shared memory, up to 128 KB) -- spread over thousands of
+// bins instead of 256 per pass, where runs of equal tile keys would serialise
+// -- folded into the per-pass digit histograms at the end.
+constexpr int kDirectBitsMax = 15;
 __global__ void __launch_bounds__(256) k_sort_hist_direct(const uint32_t* __restrict__ keys,
                                                           const uint64_t* __restrict__ n_ptr,
                                                           uint32_t* __restrict__ hist, int begin_bit, int key_bits,
                                                           int passes) {
-    __shared__ uint32_t s_bins[1 << kDirectBitsMax];
-    __shared__ uint32_t s_pass[4 * kRadix];
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t* s_pass = s_dyn;              // 4 * 256
+    uint32_t* s_bins = s_dyn + 4 * kRadix;  // 1 << key_bits
     const uint64_t n = *n_ptr;
     const int nb = 1 << key_bits;
     const uint32_t mask = (uint32_t)nb - 1u;
@@ -302,7 +304,15 @@ void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_p
     note_launch();
     const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)sms));
     if (key_bits > 0 && key_bits <= kDirectBitsMax && key_bits <= 8 * passes)
-        k_sort_hist_direct<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, hist, begin_bit, key_bits, passes);
+    {
+        const size_t dsm = sizeof(uint32_t) * (4 * kRadix + ((size_t)1 << key_bits));
+        static size_t dsm_set = 0;
+        if (dsm > dsm_set) {
+            cudaFuncSetAttribute(k_sort_hist_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+            dsm_set = dsm;
+        }
+        k_sort_hist_direct<<<hgrid, 256, dsm, s>>>(keys[0], n_ptr, hist, begin_bit, key_bits, passes);
+    }
     else
         k_sort_hist<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, hist, begin_bit, passes);
     note_launch();
