@@ -330,6 +330,8 @@ def main():
                 "frac": blend_tf / fp32_peak,
                 "traffic": traffic.get(blend_key, {}).get("dram_bytes"),
                 "traffic_source": traffic_src,
+                # what bounds it (same ncu capture): instruction issue, not DRAM or one math pipe
+                "ncu_pct_of_peak": traffic.get(blend_key, {}).get("pct_of_peak"),
                 "algorithmic_bytes": 8 * D_ + 64 * D_ + 20 * W * H,
                 "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz "
                                f"(no measured FP32 peak in MEASURED_PEAKS.json)",
