@@ -136,12 +136,12 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                     const float dx = px - p0.x, dy = py - p0.y;
                     const float power = -0.5f * (p0.z * dx * dx + p1.x * dy * dy) - p0.w * dx * dy;
                     // live iff the alpha can reach the 1/255 floor: m e^power >= 1/255 needs
-                    // power >= -ln(255 m) >= p3.y = -qthr/2 (qthr carries the margin)
-                    const bool lv = (power <= 0.0f) && (power >= rec[h + k][3].y);
-                    if (lv) {
-                        live |= 1u << k;
-                        sv[k][lane] = power;
-                    }
+                    // power >= -ln(255 m) >= p3.y = -qthr/2 (qthr carries the margin).
+                    // Branch-free: the power is stored either way (read only for live pairs).
+                    const float fl = rec[h + k][3].y;
+                    const bool lv = (power <= 0.0f) & (power >= fl);
+                    sv[k][lane] = power;
+                    live |= (uint32_t)lv << k;
                 }
             }
             // 3. alpha of every live (pixel, entry) pair.  Alpha does not depend on T, so the
