@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256) k_duplicate_huge(const uint4* __restrict_
 // The tile sort orders by bits [8, 32) and carries the mask along; the blend
 // never stages entries that cannot touch its block.  Four entries per thread
 // with all their loads issued first (the record gathers are latency-bound).
-constexpr int kMaskItems = 4;
+template <int kMaskItems>
 __global__ void __launch_bounds__(256) k_reach_masks(uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                                                      const ProjRec* __restrict__ proj,
                                                      const uint64_t* __restrict__ n_ptr, int tiles_x) {
@@ -356,8 +356,7 @@ void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const Proj
     k_duplicate_huge<<<(unsigned)order_sms() * 4, 256, 0, s>>>(dinfo, huge_q, huge_n, sort_n_ptr, tiles_x,
                                                                         keys, vals);
     note_launch();
-    k_reach_masks<<<flat_grid((dup_max + kMaskItems - 1) / kMaskItems), 256, 0, s>>>(keys, vals, proj, sort_n_ptr,
-                                                                                      tiles_x);
+    k_reach_masks<4><<<flat_grid((dup_max + 3) / 4), 256, 0, s>>>(keys, vals, proj, sort_n_ptr, tiles_x);
     note_launch();
 }
 

@@ -28,7 +28,7 @@ static void dump_prof(uint64_t n) {
 #endif
 
 int main() {
-    const uint64_t sizes[] = {1u << 20, 2300000, 4600000, 9200000};
+    const uint64_t sizes[] = {1u << 20, 2300000, 4600000, 9200000, 36000000, 140000000};
     for (int dist = 0; dist < 2; ++dist)
     for (uint64_t n : sizes) {
         std::vector<uint32_t> hk(n), hv(n);
