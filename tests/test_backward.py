@@ -234,3 +234,16 @@ def test_gpu_backward_hierarchy_frame_c1(renderer):
     for k in GRAD_KEYS:
         scale = float(np.abs(want[k]).max()) + 1e-12
         assert _close(got[k], want[k], 5e-3, 1e-4 * scale), k
+
+
+@pytest.mark.gpu
+def test_gpu_backward_errors_and_empty(renderer):
+    cam = axis_camera(32, 24, 40.0)
+    renderer.render_forward(gray_splat([0, 0, -4], 0.5, 0.5), cam)  # behind the camera: culled
+    g = renderer.render_backward(np.ones((3, 24, 32), np.float32))
+    assert np.all(g["mean"] == 0) and np.all(g["sh"] == 0)
+    assert g["exposure"][0, 3] == pytest.approx(24 * 32)  # sum of the loss gradient
+    with pytest.raises(hs.Error):
+        renderer.render_backward(np.ones((3, 10, 10), np.float32))  # DimensionMismatch
+    with pytest.raises(hs.Error):
+        renderer.render_backward(np.ones((3, 24, 32), np.float32), np.ones((5, 5), np.float32))

@@ -105,3 +105,21 @@ def test_gpu_compact_preserves_cut_coverage(renderer):
             b = renderer.select_cut(dc, cam, tau).node
             assert _leaf_partition(h, a) == _leaf_partition(c, b)
         tau *= 2.0
+
+
+@pytest.mark.gpu
+def test_gpu_compact_edge_cases(renderer):
+    """tau_max below tau_min (no probed level: only the breadth-first relayout), a single
+    camera far away (coarse cuts), and the reference's argument checks."""
+    h = hs.synth_city(2000, seed=5)
+    cams = _ring_cams(2, 60.0, 128, 96, 120.0, y=20.0)
+    oh = orc.OracleHierarchy(h)
+    for tmin, tmax in ((3.0, 1.0), (50.0, 0.0), (3.0, 3.0)):
+        want = orc.compact(oh, cams, tmin, tmax)
+        got = renderer.download(renderer.compact(h, cams, tmin, tmax))
+        for f in FIELDS:
+            assert np.array_equal(getattr(got, f).view(np.uint32), want[f].view(np.uint32)), (tmin, tmax, f)
+    with pytest.raises(hs.Error):
+        renderer.compact(h, [], 3.0)
+    with pytest.raises(hs.Error):
+        renderer.compact(h, cams, 0.0)

@@ -92,3 +92,12 @@ def test_multichunk_render_bit_exact(renderer):
         assert np.array_equal(out.color.view(np.uint32), c.view(np.uint32))
         assert np.array_equal(out.transmittance.view(np.uint32), T.view(np.uint32))
         assert out.rendered_count == rc
+
+
+@pytest.mark.gpu
+def test_assemble_errors(renderer):
+    with pytest.raises(hs.Error):
+        renderer.assemble([])
+    parts = [hs.synth_city(300, seed=s) for s in range(65)]
+    with pytest.raises(hs.Error):
+        renderer.assemble(parts)  # more than 64 parts
