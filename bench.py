@@ -174,6 +174,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tau-sweep", action="store_true")
     ap.add_argument("--reference-budget-s", type=float, default=120.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -281,6 +282,35 @@ def main():
     cad_ms = max_over_ranks(e2.elapsed_time(e3))
     cadence = {"value": world * len(timed) / (cad_ms / 1e3), "unit": UNIT, "ms_per_step": cad_ms / len(timed),
                "what": "bench_path cadence: select_cut on even frames only (bench.hpp:70-84), same frames"}
+
+    # ---- BASELINE configs[2] (C3): the tau sweep on the same hierarchy and frames
+    tau_sweep = {}
+    if not args.no_tau_sweep:
+        r.set_async(True)
+        for tau in (0.0, 1.5, 3.0, 6.0, 12.0):
+            sweep = timed[: min(len(timed), 20)]
+            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, sweep[0], tau, r._cut, r._frame, None), r.ctx)
+            r.set_async(False)
+            hs._check(L.hs_frame_wait(r.ctx, r._frame), r.ctx)  # grows the duplicate buffer if needed
+            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, sweep[0], tau, r._cut, r._frame, None), r.ctx)
+            r.set_async(True)
+            barrier()
+            r.synchronize()
+            e4 = torch.cuda.Event(enable_timing=True)
+            e5 = torch.cuda.Event(enable_timing=True)
+            e4.record(stream)
+            for c in sweep:
+                hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, tau, r._cut, r._frame, None), r.ctx)
+            e5.record(stream)
+            e5.synchronize()
+            r.synchronize()
+            hs._check(L.hs_frame_wait(r.ctx, r._frame), r.ctx)
+            fi = N.hs_frame_info()
+            hs._check(L.hs_frame_get_info(r.ctx, r._frame, fi), r.ctx)
+            ms = max_over_ranks(e4.elapsed_time(e5)) / len(sweep)
+            tau_sweep[str(tau)] = {"frames_per_s": world * 1e3 / ms, "ms_per_frame": ms,
+                                   "cut_entries": int(fi.n_splats), "duplicates": int(fi.n_duplicates)}
+        r.set_async(False)
 
     # ---- stage breakdown + roofline inputs: the same frames, per-stage CUDA events
     st = hs.StageTimes()
@@ -401,6 +431,7 @@ def main():
             "stages": stages,
             "per_frame": {"cut_entries": C_, "visible": V_, "duplicates": D_, "n_eval": NE, "n_contrib": NC},
             "reference_cadence": cadence,
+            "tau_sweep": tau_sweep,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
