@@ -129,8 +129,11 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
             uint32_t live = 0;
             if (!done) {
                 n_eval += __popc(hbits);
-                for (uint32_t m = hbits; m; m &= m - 1) {
-                    const int k = __ffs(m) - 1;
+                // fully unrolled over the 16 slots with a warp-uniform skip: constant
+                // shared-memory offsets, no bit-scan per entry
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    if (!((hbits >> k) & 1u)) continue;
                     const float4 p0 = rec[h + k][0];
                     const float4 p1 = rec[h + k][1];
                     const float dx = px - p0.x, dy = py - p0.y;
