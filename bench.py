@@ -218,7 +218,8 @@ def main():
         dh = scenes.multichunk(r, cfg.leaves)
         gen_s, upload_s = time.perf_counter() - t0, 0.0
     else:
-        h = scenes.hierarchy(cfg)
+        # every rank builds its replica; split the host cores between the ranks
+        h = scenes.hierarchy(cfg, threads=max(1, (os.cpu_count() or 1) // world))
         gen_s = time.perf_counter() - t0
         t0 = time.perf_counter()
         dh = r.upload(h, validate=False)
