@@ -288,13 +288,32 @@ __global__ void __launch_bounds__(256) k_reach_masks(uint32_t* __restrict__ keys
     }
 }
 
+// Tile boundaries of the sorted keys: four keys per thread (one 16-byte load)
+// plus the next key, a boundary where the tile changes.
 __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, const uint64_t* __restrict__ n_ptr,
                                                 uint2* __restrict__ ranges) {
     const uint64_t n = *n_ptr;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t t = keys[i] >> 8;
-        if (i == 0 || (keys[i - 1] >> 8) != t) ranges[t].x = (uint32_t)i;
-        if (i == n - 1 || (keys[i + 1] >> 8) != t) ranges[t].y = (uint32_t)(i + 1);
+    const uint64_t n4 = (n + 3) / 4;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i0 = 4 * q;
+        uint32_t k[5];
+        if (i0 + 4 <= n) {
+            const uint4 v = reinterpret_cast<const uint4*>(keys)[q];
+            k[0] = v.x, k[1] = v.y, k[2] = v.z, k[3] = v.w;
+        } else {
+            for (int e = 0; e < 4; ++e) k[e] = i0 + e < n ? keys[i0 + e] : 0u;
+        }
+        k[4] = i0 + 4 < n ? keys[i0 + 4] : 0u;
+        uint32_t prev_t = i0 > 0 ? (keys[i0 - 1] >> 8) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint64_t i = i0 + e;
+            if (i >= n) break;
+            const uint32_t t = k[e] >> 8;
+            if (i == 0 || prev_t != t) ranges[t].x = (uint32_t)i;
+            if (i == n - 1 || (k[e + 1] >> 8) != t) ranges[t].y = (uint32_t)(i + 1);
+            prev_t = t;
+        }
     }
 }
 
@@ -361,7 +380,7 @@ void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const Proj
 }
 
 void launch_ranges(const uint32_t* keys, const uint64_t* n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s) {
-    k_ranges<<<flat_grid(n_max), 256, 0, s>>>(keys, n_ptr, ranges);
+    k_ranges<<<flat_grid((n_max + 3) / 4), 256, 0, s>>>(keys, n_ptr, ranges);
     note_launch();
 }
 

@@ -371,10 +371,22 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const float4* __restrict_
 
 __global__ void k_count_touched(uint8_t* __restrict__ touched, const uint64_t* __restrict__ n_ptr,
                                 unsigned long long* __restrict__ out) {
+    // 16 flags per thread (one 16-byte load); count them, and leave them zeroed for
+    // the next frame (only the words that held a flag are written back)
     const uint64_t n = *n_ptr;
+    const uint64_t n16 = n / 16;
     uint32_t c = 0;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        if (touched[i]) {  // count, and leave the flags zeroed for the next frame
+    uint4* t16 = reinterpret_cast<uint4*>(touched);
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n16; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 v = t16[q];
+        if (v.x | v.y | v.z | v.w) {
+            c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);  // flags are 0 or 1
+            t16[q] = make_uint4(0, 0, 0, 0);
+        }
+    }
+    for (uint64_t i = 16 * n16 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        if (touched[i]) {
             ++c;
             touched[i] = 0;
         }
@@ -431,7 +443,7 @@ void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* 
 
 void launch_count_touched(uint8_t* touched, const uint64_t* n_ptr, uint64_t n_max, unsigned long long* out,
                           cudaStream_t s) {
-    k_count_touched<<<grid_for(n_max, 4), 256, 0, s>>>(touched, n_ptr, out);
+    k_count_touched<<<grid_for((n_max + 15) / 16, 4), 256, 0, s>>>(touched, n_ptr, out);
     note_launch();
 }
 
