@@ -265,7 +265,7 @@ uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 // The two radix sorts zero their own look-back words on the device (sized from
 // the device-side key counts).
 struct ScratchLayout {
-    size_t vis_counter = 0, dup_counter = 4, blend_counter = 8, huge_counter = 12, vis_status = 64, dup_status = 0, zero_bytes = 0,
+    size_t vis_counter = 0, dup_counter = 4, blend_counter = 8, huge_counter = 12, touch_ticket = 16, vis_status = 64, dup_status = 0, zero_bytes = 0,
            depth_sort = 0, tile_sort = 0, total = 0;
 };
 ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int tile_passes) {
@@ -337,12 +337,12 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     if (f->copy_pending) HS_CUDA(ctx, cudaStreamWaitEvent(s, f->copy_done, 0));
     HS_CUDA(ctx, cudaMemsetAsync(sc, 0, L.zero_bytes, s));
     HS_CUDA(ctx, cudaMemsetAsync(&ds->n_visible, 0, offsetof(DevStats, overflows) - 8, s));
-    if (f->from_cut) hs::launch_copy_words(f->n_ptr, &ds->n_splats, 8, s);
     HS_CUDA(ctx, cudaMemsetAsync(f->ranges.p, 0, (size_t)cp.tiles_x * cp.tiles_y * 8, s));
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[1], s));
     hs::launch_preprocess(f->from_cut, f->attr, f->cut_node, f->cut_t, f->n_ptr, f->n_max, cp, f->proj.as<ProjRec>(),
                           f->dinfo.as<uint4>(), f->dupcount.as<uint32_t>(),
-                          ctx->debug ? f->dbg16.as<float>() : nullptr, &ds->n_visible, s);
+                          ctx->debug ? f->dbg16.as<float>() : nullptr, &ds->n_visible,
+                          f->from_cut ? &ds->n_splats : nullptr, s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[2], s));
     // depth order of the visible splats (stable: ties keep cut order, render.hpp:268-272)
     uint32_t* zk[2] = {f->zkeys[0].as<uint32_t>(), f->zkeys[1].as<uint32_t>()};
@@ -378,10 +378,11 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     hs::launch_blend(ctx->blend_mode, f->ranges.as<uint2>(), kb[fin], vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
                      f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(),
                      &ds->n_eval, reinterpret_cast<uint32_t*>(sc + L.blend_counter), f->tile_order.as<uint32_t>(), s);
-    hs::launch_count_touched(f->touched.as<uint8_t>(), f->n_ptr, f->n_max, &ds->rendered, s);
+    hs::launch_count_touched(f->touched.as<uint8_t>(), f->n_ptr, f->n_max, &ds->rendered,
+                             reinterpret_cast<const uint64_t*>(ds), reinterpret_cast<uint64_t*>(f->h_stats_dev),
+                             (int)(sizeof(DevStats) / 8), reinterpret_cast<uint32_t*>(sc + L.touch_ticket), s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[5], s));
     HS_CUDA(ctx, cudaGetLastError());
-    hs::launch_copy_words(ds, f->h_stats_dev, sizeof(DevStats), s);
     HS_CUDA(ctx, cudaEventRecord(f->done, s));
     f->pending = true;
     return HS_OK;
@@ -460,9 +461,8 @@ hs_status enqueue_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* c
     HS_CUDA(ctx, cudaMemsetAsync(sc, 0, hs::select_cut_zero_words(h->n) * 4, ctx->stream));  // counters
     const CamParams cp = make_cam(cam);
     hs::launch_select_cut(h->cull.as<float4>(), h->n, cp, tau, cut->node.as<uint32_t>(), cut->t.as<float>(),
-                          cut->alpha.as<float>(), sc, cut->count.as<uint64_t>(), ctx->stream);
+                          cut->alpha.as<float>(), sc, cut->count.as<uint64_t>(), cut->h_count_dev, ctx->stream);
     HS_CUDA(ctx, cudaGetLastError());
-    hs::launch_copy_words(cut->count.p, cut->h_count_dev, 8, ctx->stream);
     HS_CUDA(ctx, cudaEventRecord(cut->done, ctx->stream));
     cut->h = h;
     return HS_OK;

@@ -190,7 +190,8 @@ __global__ void __launch_bounds__(kCutThreads, kMinBlocks) k_select_cut(const fl
 // Exclusive scan of the superblock counts (kCutSuper tiles each; one CTA:
 // 610 values at 2e7 nodes, 6.1e3 at 2e8), in place; the total is the cut size.
 __global__ void __launch_bounds__(1024) k_cut_offsets(uint32_t* __restrict__ super_count, uint32_t n_super,
-                                                      uint64_t* __restrict__ count_out) {
+                                                      uint64_t* __restrict__ count_out,
+                                                      uint64_t* __restrict__ count_host) {
     __shared__ uint32_t s_warp[32];
     __shared__ uint32_t s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -224,7 +225,10 @@ __global__ void __launch_bounds__(1024) k_cut_offsets(uint32_t* __restrict__ sup
         if (tid == 1023) s_carry = carry + s_warp[31] + incl;
         __syncthreads();
     }
-    if (tid == 0) *count_out = s_carry;
+    if (tid == 0) {
+        *count_out = s_carry;
+        if (count_host) *count_host = s_carry;  // mapped host memory: the cut size without a copy
+    }
 }
 
 // One warp per tile: its offset is the superblock offset plus the counts of the
@@ -315,7 +319,7 @@ static void run_select(const float4* cull, uint64_t n, const CamParams& cam, flo
 // call) | tile counts | staging node, t, alpha (one slot per node)
 void launch_select_cut(const float4* cull, uint64_t n, const CamParams& cam, float tau,
                        uint32_t* out_node, float* out_t, float* out_alpha, uint32_t* scratch, uint64_t* count_out,
-                       cudaStream_t stream) {
+                       uint64_t* count_host, cudaStream_t stream) {
     constexpr int items = kCutItemsUsed;
     const uint64_t tile_nodes = (uint64_t)kCutThreads * items;
     const uint64_t tiles = (n + tile_nodes - 1) / tile_nodes;
@@ -331,7 +335,7 @@ void launch_select_cut(const float4* cull, uint64_t n, const CamParams& cam, flo
     run_select<kCutItemsUsed, 2, 6>(cull, n, cam, tau, st_node, st_t, st_alpha, counts, supers, counter, tiles,
                                     stream);
     note_launch();
-    k_cut_offsets<<<1, 1024, 0, stream>>>(supers, (uint32_t)n_super, count_out);
+    k_cut_offsets<<<1, 1024, 0, stream>>>(supers, (uint32_t)n_super, count_out, count_host);
     note_launch();
     k_cut_gather<<<(unsigned)((tiles + 7) / 8), 256, 0, stream>>>(supers, counts, (uint32_t)tiles, (uint32_t)tile_nodes,
                                                                   st_node, st_t, st_alpha, out_node, out_t, out_alpha);

@@ -17,7 +17,7 @@ struct ProjRec;
 // cut.cu
 void launch_select_cut(const float4* cull, uint64_t n, const CamParams& cam, float tau,
                        uint32_t* out_node, float* out_t, float* out_alpha, uint32_t* scratch, uint64_t* count_out,
-                       cudaStream_t stream);
+                       uint64_t* count_host, cudaStream_t stream);
 void launch_copy_words(const void* src, void* dst, size_t bytes, cudaStream_t s);  // bytes % 8 == 0
 void launch_child_alpha(const float4* attr, float4* cull, uint64_t n, cudaStream_t stream);
 uint64_t select_cut_scratch_words(uint64_t n);
@@ -83,7 +83,8 @@ void launch_backward(const float4* attr, uint64_t n, const CamParams& cam, const
 // raster.cu
 void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,
                        const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint4* dinfo,
-                       uint32_t* dupcount, float* dbg16, unsigned long long* n_visible, cudaStream_t s);
+                       uint32_t* dupcount, float* dbg16, unsigned long long* n_visible, uint64_t* n_out,
+                       cudaStream_t s);
 void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
                   unsigned long long* eval_counts, uint32_t* task_counter, const uint32_t* tile_order,
@@ -92,8 +93,9 @@ void launch_tile_order(const uint2* ranges, int tiles, const uint64_t* sort_n_pt
 void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr,
                      uint64_t n_max, float* mean, float* scale, float* rot, float* sh, float* fall, float* pfall,
                      float* t, int* k, cudaStream_t s);
+// also copies `words` 64-bit words of `stats` to mapped host memory once the count is final
 void launch_count_touched(uint8_t* touched, const uint64_t* n_ptr, uint64_t n_max, unsigned long long* out,
-                          cudaStream_t s);
+                          const uint64_t* stats, uint64_t* stats_host, int words, uint32_t* ticket, cudaStream_t s);
 
 // order.cu
 uint64_t scan_status_words(uint64_t n_max);

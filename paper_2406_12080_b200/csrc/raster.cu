@@ -148,8 +148,10 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const float4* __restrict_
                                                     CamParams cam, ProjRec* __restrict__ proj,
                                                     uint4* __restrict__ dinfo,
                                                     uint32_t* __restrict__ dupcount, float* __restrict__ dbg16,
-                                                    unsigned long long* __restrict__ n_visible) {
+                                                    unsigned long long* __restrict__ n_visible,
+                                                    uint64_t* __restrict__ n_out) {
     const uint64_t n = *n_ptr;
+    if (n_out && blockIdx.x == 0 && threadIdx.x == 0) *n_out = n;  // frame stats: C
     uint32_t vis = 0;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
         SplatIn si;
@@ -370,7 +372,8 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const float4* __restrict_
 }
 
 __global__ void k_count_touched(uint8_t* __restrict__ touched, const uint64_t* __restrict__ n_ptr,
-                                unsigned long long* __restrict__ out) {
+                                unsigned long long* __restrict__ out, const uint64_t* __restrict__ stats,
+                                uint64_t* __restrict__ stats_host, int words, uint32_t* __restrict__ ticket) {
     // 16 flags per thread (one 16-byte load); count them, and leave them zeroed for
     // the next frame (only the words that held a flag are written back)
     const uint64_t n = *n_ptr;
@@ -392,6 +395,16 @@ __global__ void k_count_touched(uint8_t* __restrict__ touched, const uint64_t* _
         }
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+    // the last block to finish publishes the frame stats to mapped host memory
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last && (int)threadIdx.x < words) {
+        __threadfence();
+        stats_host[threadIdx.x] = ld_volatile_u64(stats + threadIdx.x);
+    }
 }
 
 // Small device->device / device->mapped-host word copies in stream order.  A
@@ -422,14 +435,15 @@ static unsigned grid_for(uint64_t n_max, int per_sm) {
 
 void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,
                        const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint4* dinfo,
-                       uint32_t* dupcount, float* dbg16, unsigned long long* n_visible, cudaStream_t s) {
+                       uint32_t* dupcount, float* dbg16, unsigned long long* n_visible, uint64_t* n_out,
+                       cudaStream_t s) {
     const unsigned grid = grid_for(n_max, 8);
     if (from_cut)
         k_preprocess<true><<<grid, 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, cam, proj, dinfo, dupcount, dbg16,
-                                                n_visible);
+                                                n_visible, n_out);
     else
         k_preprocess<false><<<grid, 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, cam, proj, dinfo, dupcount, dbg16,
-                                                 n_visible);
+                                                 n_visible, n_out);
     note_launch();
 }
 
@@ -442,8 +456,9 @@ void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* 
 }
 
 void launch_count_touched(uint8_t* touched, const uint64_t* n_ptr, uint64_t n_max, unsigned long long* out,
-                          cudaStream_t s) {
-    k_count_touched<<<grid_for((n_max + 15) / 16, 4), 256, 0, s>>>(touched, n_ptr, out);
+                          const uint64_t* stats, uint64_t* stats_host, int words, uint32_t* ticket, cudaStream_t s) {
+    k_count_touched<<<grid_for((n_max + 15) / 16, 4), 256, 0, s>>>(touched, n_ptr, out, stats, stats_host, words,
+                                                                    ticket);
     note_launch();
 }
 
