@@ -204,7 +204,6 @@ hs_status copy_sync(hs_context* ctx, void* dst, const void* src, size_t bytes, c
         if (s__ != HS_OK) return s__; \
     } while (0)
 
-inline float hmin(float a, float b) { return (b < a) ? b : a; }
 inline float hmax(float a, float b) { return (a < b) ? b : a; }
 
 // validate_camera (model.hpp:84-91)
