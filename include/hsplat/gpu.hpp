@@ -397,6 +397,55 @@ inline Hierarchy download_hierarchy(Context& c, const hs_hierarchy* dh, std::uin
     return h;
 }
 
+// A hierarchy resident on the device, owned by the caller (no cache lookup per
+// call): from a host Hierarchy, an .h3dg file (read on the host, validated,
+// uploaded) or a device-side assembly.  The select_cut / render_hierarchy /
+// bench_path / compact overloads below take it instead of a `const Hierarchy&`.
+class DeviceHierarchy {
+public:
+    explicit DeviceHierarchy(const Hierarchy& h) : sh_degree_(h.sh_degree) {
+        auto& c = context();
+        const std::size_t n = h.nodes.size();
+        std::vector<std::uint32_t> parent(n), fc(n), cc(n);
+        std::vector<float> bmin(3 * n), bmax(3 * n), mean(3 * n), scale(3 * n), rot(4 * n), fall(n), sh(48 * n);
+        for (std::size_t i = 0; i < n; ++i) {
+            const HierarchyNode& nd = h.nodes[i];
+            parent[i] = nd.parent, fc[i] = nd.first_child, cc[i] = nd.child_count;
+            for (int k = 0; k < 3; ++k) {
+                bmin[3 * i + k] = nd.bounds.min[k], bmax[3 * i + k] = nd.bounds.max[k];
+                mean[3 * i + k] = nd.g.mean[k], scale[3 * i + k] = nd.g.scale[k];
+            }
+            rot[4 * i] = nd.g.rotation.w(), rot[4 * i + 1] = nd.g.rotation.x();
+            rot[4 * i + 2] = nd.g.rotation.y(), rot[4 * i + 3] = nd.g.rotation.z();
+            fall[i] = nd.g.falloff;
+            for (int k = 0; k < kShValues; ++k) sh[48 * i + k] = nd.g.sh[k];
+        }
+        hs_node_soa soa{parent.data(), fc.data(), cc.data(), bmin.data(), bmax.data(),
+                        mean.data(),   scale.data(), rot.data(), fall.data(), sh.data()};
+        hs_hierarchy* dh = nullptr;
+        c.check(hs_hierarchy_upload(c.ctx(), &soa, n, h.sh_degree, 1, &dh));
+        h_.reset(dh);
+    }
+    explicit DeviceHierarchy(const std::string& h3dg_path) {  // read_hierarchy (io.hpp:375) straight to the device
+        auto& c = context();
+        hs_hierarchy* dh = nullptr;
+        c.check(hs_hierarchy_load_h3dg(c.ctx(), h3dg_path.c_str(), &dh));
+        h_.reset(dh);
+    }
+    explicit DeviceHierarchy(hs_hierarchy* adopt, std::uint32_t sh_degree = 3) : sh_degree_(sh_degree) { h_.reset(adopt); }
+    hs_hierarchy* get() const { return h_.get(); }
+    std::size_t size() const { return hs_hierarchy_node_count(h_.get()); }
+    std::size_t leaf_count() const { return hs_hierarchy_leaf_count(h_.get()); }
+    Hierarchy download() const;
+
+private:
+    struct Deleter {
+        void operator()(hs_hierarchy* h) const { hs_hierarchy_destroy(h); }
+    };
+    std::unique_ptr<hs_hierarchy, Deleter> h_;
+    std::uint32_t sh_degree_ = 3;
+};
+
 // consolidate's global assembly (scene.hpp:228-316) on the device for parts
 // without cross-chunk backdrop pruning: chunk trees then the skybox tree under
 // one merged root, serialised breadth first.
@@ -410,15 +459,35 @@ inline Hierarchy assemble(std::span<const Hierarchy> parts) {
     return download_hierarchy(c, out, parts.empty() ? 3u : parts[0].sh_degree);
 }
 
+inline Hierarchy DeviceHierarchy::download() const { return download_hierarchy(context(), h_.get(), sh_degree_); }
+
+// assemble, keeping the result on the device
+inline DeviceHierarchy assemble_device(std::span<const DeviceHierarchy* const> parts) {
+    auto& c = context();
+    std::vector<const hs_hierarchy*> dev;
+    for (const DeviceHierarchy* p : parts) dev.push_back(p->get());
+    hs_hierarchy* out = nullptr;
+    c.check(hs_hierarchy_assemble(c.ctx(), dev.data(), static_cast<std::uint32_t>(dev.size()), &out));
+    return DeviceHierarchy(out);
+}
+
+inline std::vector<CutEntry> select_cut(hs_hierarchy* dh, const CameraModel& cam, float tau) {
+    auto& c = context();
+    if (!(tau >= 0.0f)) throw Error(Errc::InvalidArgument, "InvalidArgument: select_cut needs tau >= 0 and nodes");
+    const hs_camera cc = to_c(cam);
+    c.check(hs_select_cut(c.ctx(), dh, &cc, tau, c.cut()));
+    return download_cut(c, c.cut());
+}
+
 }  // namespace gpu
 
 // ------------------------------------------------------------------ lod.hpp:52-92
 inline std::vector<CutEntry> select_cut(const Hierarchy& h, const CameraModel& cam, float tau) {
-    auto& c = gpu::context();
     if (!(tau >= 0.0f) || h.empty()) throw Error(Errc::InvalidArgument, "InvalidArgument: select_cut needs tau >= 0 and nodes");
-    const hs_camera cc = gpu::to_c(cam);
-    c.check(hs_select_cut(c.ctx(), c.device(h), &cc, tau, c.cut()));
-    return gpu::download_cut(c, c.cut());
+    return gpu::select_cut(gpu::context().device(h), cam, tau);
+}
+inline std::vector<CutEntry> select_cut(const gpu::DeviceHierarchy& h, const CameraModel& cam, float tau) {
+    return gpu::select_cut(h.get(), cam, tau);
 }
 
 // ------------------------------------------------------------------ lod.hpp:148-153
@@ -476,14 +545,24 @@ RenderOutputT<T> render_forward(std::span<const RenderSplatT<T>> splats, const C
 }
 
 // ------------------------------------------------------------------ render.hpp:706-720
+namespace gpu {
+inline RenderOutput render_hierarchy(hs_hierarchy* dh, const CameraModel& cam, float tau, ForwardContext* ctx,
+                                     StageTimes* stages) {
+    auto& c = context();
+    const hs_camera cc = to_c(cam);
+    hs_stage_times st{};
+    c.check(hs_render_hierarchy(c.ctx(), dh, &cc, tau, c.cut(), c.frame(), stages ? &st : nullptr));
+    add(stages, st);
+    return download_frame(c, ctx, cam);
+}
+}  // namespace gpu
 inline RenderOutput render_hierarchy(const Hierarchy& h, const CameraModel& cam, float tau,
                                      ForwardContext* ctx = nullptr, StageTimes* stages = nullptr) {
-    auto& c = gpu::context();
-    const hs_camera cc = gpu::to_c(cam);
-    hs_stage_times st{};
-    c.check(hs_render_hierarchy(c.ctx(), c.device(h), &cc, tau, c.cut(), c.frame(), stages ? &st : nullptr));
-    gpu::add(stages, st);
-    return gpu::download_frame(c, ctx, cam);
+    return gpu::render_hierarchy(gpu::context().device(h), cam, tau, ctx, stages);
+}
+inline RenderOutput render_hierarchy(const gpu::DeviceHierarchy& h, const CameraModel& cam, float tau,
+                                     ForwardContext* ctx = nullptr, StageTimes* stages = nullptr) {
+    return gpu::render_hierarchy(h.get(), cam, tau, ctx, stages);
 }
 
 // ------------------------------------------------------------------ render.hpp:427-702
@@ -582,14 +661,14 @@ inline Hierarchy read_hierarchy(const std::string& path) {
 }
 
 // ------------------------------------------------------------------ bench.hpp:55-103
-inline BenchReport bench_path(const Hierarchy& h, const CameraPath& path, float tau) {
+namespace gpu {
+inline BenchReport bench_path(hs_hierarchy* dh, std::size_t leaf_count, const CameraPath& path, float tau) {
     if (path.cameras.empty()) throw Error(Errc::InvalidArgument, "InvalidArgument: camera path is empty");
     if (!path.timestamps.empty() && path.timestamps.size() != path.cameras.size())
         throw Error(Errc::DimensionMismatch, "DimensionMismatch: one timestamp per camera");
     auto& c = gpu::context();
-    hs_hierarchy* dh = c.device(h);
     BenchReport rep;
-    rep.leaf_count = h.leaf_count();
+    rep.leaf_count = leaf_count;
     rep.tau = tau;
     // transferred = |cut \ previous cut| (bench.hpp:79-82), counted on the device
     hs_transfer_tracker* tr = nullptr;
@@ -625,6 +704,15 @@ inline BenchReport bench_path(const Hierarchy& h, const CameraPath& path, float 
     rep.mean_rendered /= double(rep.frames.size());
     rep.mean_rendered_pct /= double(rep.frames.size());
     return rep;
+}
+}  // namespace gpu
+
+inline BenchReport bench_path(const Hierarchy& h, const CameraPath& path, float tau) {
+    if (path.cameras.empty()) throw Error(Errc::InvalidArgument, "InvalidArgument: camera path is empty");
+    return gpu::bench_path(gpu::context().device(h), h.leaf_count(), path, tau);
+}
+inline BenchReport bench_path(const gpu::DeviceHierarchy& h, const CameraPath& path, float tau) {
+    return gpu::bench_path(h.get(), h.leaf_count(), path, tau);
 }
 
 }  // namespace hsplat

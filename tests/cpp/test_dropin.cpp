@@ -168,6 +168,24 @@ int main() {
         CHECK(a.leaf_count() == 2 * h.leaf_count());
     }
 
+    // explicit device residency: the DeviceHierarchy overloads agree with the cached ones
+    {
+        const gpu::DeviceHierarchy dh(h);
+        CHECK(dh.size() == h.nodes.size() && dh.leaf_count() == h.leaf_count());
+        const auto a = select_cut(h, cam, 3.0f);
+        const auto b = select_cut(dh, cam, 3.0f);
+        CHECK(a.size() == b.size());
+        for (std::size_t i = 0; i < a.size() && i < b.size(); ++i) CHECK(a[i].node == b[i].node && a[i].t == b[i].t);
+        const RenderOutput ra = render_hierarchy(h, cam, 3.0f);
+        const RenderOutput rb = render_hierarchy(dh, cam, 3.0f);
+        CHECK(ra.color.data == rb.color.data);
+        const Hierarchy back = dh.download();
+        CHECK(back.nodes.size() == h.nodes.size() && back.nodes[1].g.mean[0] == h.nodes[1].g.mean[0]);
+        CameraPath p2;
+        for (int i = 0; i < 4; ++i) p2.cameras.push_back(cam);
+        CHECK(bench_path(dh, p2, 3.0f).frames.size() == 4);
+    }
+
     // read_hierarchy error code (io.hpp:375-387)
     threw = false;
     try {
