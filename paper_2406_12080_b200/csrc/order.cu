@@ -404,9 +404,17 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
     const bool any = *sort_n_ptr != 0;
     if (threadIdx.x < 33) hist[threadIdx.x] = 0;
     __syncthreads();
-    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
-        const uint32_t c = any ? ranges[t].y - ranges[t].x : 0u;
-        atomicAdd(&hist[__clz(c + 1u)], 1u);  // fewer leading zeros = heavier = earlier
+    // warp-aggregated: tiles of similar weight share a bucket, so one atomic per
+    // (warp, bucket) instead of 32 serialised on the same shared address
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int span = (tiles + 31) & ~31;
+    for (int t = threadIdx.x; t < span; t += blockDim.x) {
+        const bool valid = t < tiles;
+        const uint32_t c = valid && any ? ranges[t].y - ranges[t].x : 0u;
+        const uint32_t bkt = valid ? (uint32_t)__clz(c + 1u) : 64u;  // fewer leading zeros = heavier = earlier
+        const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
+        if (valid && (peers & lt) == 0) atomicAdd(&hist[bkt], (uint32_t)__popc(peers));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -414,9 +422,16 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ r
         for (int b = 0; b < 33; ++b) offs[b] = run, run += hist[b];
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
-        const uint32_t c = any ? ranges[t].y - ranges[t].x : 0u;
-        order[atomicAdd(&offs[__clz(c + 1u)], 1u)] = (uint32_t)t;
+    for (int t = threadIdx.x; t < span; t += blockDim.x) {
+        const bool valid = t < tiles;
+        const uint32_t c = valid && any ? ranges[t].y - ranges[t].x : 0u;
+        const uint32_t bkt = valid ? (uint32_t)__clz(c + 1u) : 64u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (valid && lane == leader) base = atomicAdd(&offs[bkt], (uint32_t)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (valid) order[base + __popc(peers & lt)] = (uint32_t)t;
     }
 }
 

@@ -1,8 +1,9 @@
 // sort.cu — stable LSD radix sort of 32-bit keys with 32-bit values,
 // Onesweep style (Adinets & Merrill 2022):
 //   k_sort_hist   one read of the keys -> 256-bin histograms of every pass
-//   k_sort_offs   exclusive scan of each pass histogram -> digit bases
-//   k_onesweep    per 8-bit pass: 4096-key tiles (256 threads x 16 keys);
+//                 (also zeroes the passes' look-back words)
+//   k_onesweep    per 8-bit pass: 4096-key tiles (256 threads x 16 keys); digit
+//                 bases scanned from the pass histogram by every CTA;
 //                 warp-level ranking with bit-sliced ballots, per-digit
 //                 decoupled look-back across tiles, local reorder in shared
 //                 memory, coalesced scatter.
@@ -25,13 +26,26 @@ constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys
 constexpr int kRadix = 256;
 constexpr uint32_t kFlagAgg32 = 1u << 30, kFlagInc32 = 2u << 30, kValMask32 = (1u << 30) - 1;
 
+// Zero the look-back words of every pass (sized from the device-side n); done by
+// the histogram kernels before they count, so no separate launch is needed.
+__device__ __forceinline__ void zero_status(uint32_t* __restrict__ status, uint64_t n, uint64_t words_per_pass,
+                                            int passes) {
+    const uint64_t used = ((n + kSortTile - 1) / kSortTile) * kRadix;
+    for (int p = 0; p < passes; ++p)
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < used;
+             i += (uint64_t)gridDim.x * blockDim.x)
+            status[p * words_per_pass + i] = 0;
+}
+
 // Digit histograms of every pass from one read of the keys (uint4 loads),
 // counted in per-warp shared histograms (less same-address contention on the
 // clustered tile keys), merged per block, then one global atomic per bin.
 __global__ void __launch_bounds__(256) k_sort_hist(const uint32_t* __restrict__ keys, const uint64_t* __restrict__ n_ptr,
-                                                   uint32_t* __restrict__ hist, int begin_bit, int passes) {
+                                                   uint32_t* __restrict__ hist, int begin_bit, int passes,
+                                                   uint32_t* __restrict__ status, uint64_t words_per_pass) {
     __shared__ uint32_t s_hist[8][4 * kRadix];
     const uint64_t n = *n_ptr;
+    zero_status(status, n, words_per_pass, passes);
     const int warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < 8 * 4 * kRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0;
     __syncthreads();
@@ -68,11 +82,13 @@ constexpr int kDirectBitsMax = 15;
 __global__ void __launch_bounds__(256) k_sort_hist_direct(const uint32_t* __restrict__ keys,
                                                           const uint64_t* __restrict__ n_ptr,
                                                           uint32_t* __restrict__ hist, int begin_bit, int key_bits,
-                                                          int passes) {
+                                                          int passes, uint32_t* __restrict__ status,
+                                                          uint64_t words_per_pass) {
     extern __shared__ uint32_t s_dyn[];
     uint32_t* s_pass = s_dyn;              // 4 * 256
     uint32_t* s_bins = s_dyn + 4 * kRadix;  // 1 << key_bits
     const uint64_t n = *n_ptr;
+    zero_status(status, n, words_per_pass, passes);
     const int nb = 1 << key_bits;
     const uint32_t mask = (uint32_t)nb - 1u;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) s_bins[i] = 0;
@@ -100,40 +116,13 @@ __global__ void __launch_bounds__(256) k_sort_hist_direct(const uint32_t* __rest
         if (s_pass[i]) atomicAdd(&hist[i], s_pass[i]);
 }
 
-__global__ void k_sort_offs(uint32_t* hist) {
-    // one block of 256 threads per pass; exclusive scan in place
-    const int p = blockIdx.x;
-    __shared__ uint32_t s[kRadix];
-    const int tid = threadIdx.x;
-    const uint32_t mine = hist[p * kRadix + tid];
-    s[tid] = mine;
-    __syncthreads();
-    for (int o = 1; o < kRadix; o <<= 1) {
-        const uint32_t v = tid >= o ? s[tid - o] : 0u;
-        __syncthreads();
-        s[tid] += v;
-        __syncthreads();
-    }
-    hist[p * kRadix + tid] = s[tid] - mine;
-}
-
-// Zero the look-back words this sort will use (sized from the device-side n).
-__global__ void k_sort_zero(uint32_t* __restrict__ status, const uint64_t* __restrict__ n_ptr, uint64_t words_per_pass,
-                            int passes) {
-    const uint64_t tiles = (*n_ptr + kSortTile - 1) / kSortTile;
-    const uint64_t used = tiles * kRadix;
-    for (int p = 0; p < passes; ++p)
-        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < used;
-             i += (uint64_t)gridDim.x * blockDim.x)
-            status[p * words_per_pass + i] = 0;
-}
-
 struct SortSmem {
     uint32_t keys[kSortTile];
     uint32_t vals[kSortTile];
     uint32_t wcnt[kSortWarps][kRadix];
     uint32_t local_off[kRadix];
     uint32_t gbase[kRadix];
+    uint32_t dbase[kRadix];  // exclusive scan of the pass histogram (the digit bases)
     uint32_t wsum[kSortWarps];
     uint32_t tile;
 };
@@ -142,7 +131,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const uint32_t* __
                                                            const uint32_t* __restrict__ vals_in,
                                                            uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                            const uint64_t* __restrict__ n_ptr, int shift,
-                                                           const uint32_t* __restrict__ digit_base, uint32_t* status,
+                                                           const uint32_t* __restrict__ pass_hist, uint32_t* status,
                                                            uint32_t* tile_counter) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
@@ -150,6 +139,22 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const uint32_t* __
     const uint64_t n = *n_ptr;
     const uint64_t num_tiles = (n + kSortTile - 1) / kSortTile;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    {   // digit bases of this pass: exclusive scan of its histogram (kSortThreads == kRadix)
+        const uint32_t c = pass_hist[tid];
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += x;
+        }
+        if (lane == 31) sm.wsum[warp] = incl;
+        __syncthreads();
+        uint32_t wpre = 0;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) wpre += w < warp ? sm.wsum[w] : 0u;
+        sm.dbase[tid] = wpre + incl - c;
+        __syncthreads();
+    }
     while (true) {
         if (tid == 0) sm.tile = atomicAdd(tile_counter, 1u);
         for (int i = lane; i < kRadix; i += 32) sm.wcnt[warp][i] = 0;
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const uint32_t* __
                 }
                 st_volatile_u32(status + (uint64_t)tile * kRadix + d, kFlagInc32 | (prefix + dcount));
             }
-            sm.gbase[d] = digit_base[d] + prefix;
+            sm.gbase[d] = sm.dbase[d] + prefix;
         }
         __syncthreads();
         for (uint32_t i = tid; i < tcount; i += kSortThreads) {
@@ -300,8 +305,6 @@ void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_p
     uint32_t* status = counters + passes;            // passes * words
     const uint64_t words = sort_status_words(n_max);
     cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * passes * (kRadix + 1), s);
-    k_sort_zero<<<sms * 2, 256, 0, s>>>(status, n_ptr, words, passes);
-    note_launch();
     const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)sms));
     if (key_bits > 0 && key_bits <= kDirectBitsMax && key_bits <= 8 * passes)
     {
@@ -311,12 +314,10 @@ void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_p
             cudaFuncSetAttribute(k_sort_hist_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
             dsm_set = dsm;
         }
-        k_sort_hist_direct<<<hgrid, 256, dsm, s>>>(keys[0], n_ptr, hist, begin_bit, key_bits, passes);
+        k_sort_hist_direct<<<hgrid, 256, dsm, s>>>(keys[0], n_ptr, hist, begin_bit, key_bits, passes, status, words);
     }
     else
-        k_sort_hist<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, hist, begin_bit, passes);
-    note_launch();
-    k_sort_offs<<<passes, kRadix, 0, s>>>(hist);
+        k_sort_hist<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, hist, begin_bit, passes, status, words);
     note_launch();
     const size_t smem = sizeof(SortSmem);
     static bool attr_set = false;
