@@ -270,8 +270,10 @@ struct ScratchLayout {
 ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int tile_passes) {
     ScratchLayout L;
     L.dup_status = round_up(L.vis_status + hs::scan_status_words(n_max) * 8, 256);
-    L.zero_bytes = round_up(L.dup_status + hs::scan_status_words(n_max) * 8, 256);
-    L.depth_sort = L.zero_bytes;
+    // the depth sort's histograms + tile counters are zeroed with the rest (its
+    // look-back words are zeroed by k_compact_visible)
+    L.depth_sort = round_up(L.dup_status + hs::scan_status_words(n_max) * 8, 256);
+    L.zero_bytes = round_up(L.depth_sort + 4 * (256 + 1) * 4, 256);
     L.tile_sort = round_up(L.depth_sort + hs::sort_scratch_words(n_max, 4) * 4, 256);
     L.total = L.tile_sort + hs::sort_scratch_words(cap_dup, tile_passes) * 4;
     return L;
@@ -348,9 +350,10 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     uint32_t* zv[2] = {f->zvals[0].as<uint32_t>(), f->zvals[1].as<uint32_t>()};
     hs::launch_compact_visible(f->dupcount.as<uint32_t>(), f->dinfo.as<uint4>(), f->n_ptr, f->n_max, zk[0], zv[0],
                                reinterpret_cast<uint64_t*>(sc + L.vis_status),
-                               reinterpret_cast<uint32_t*>(sc + L.vis_counter), &ds->n_visible_sorted, s);
+                               reinterpret_cast<uint32_t*>(sc + L.vis_counter), &ds->n_visible_sorted,
+                               reinterpret_cast<uint32_t*>(sc + L.depth_sort), s);
     hs::launch_radix_sort(zk, zv, &ds->n_visible_sorted, f->n_max, 0, 4, 32,
-                          reinterpret_cast<uint32_t*>(sc + L.depth_sort), s);
+                          reinterpret_cast<uint32_t*>(sc + L.depth_sort), s, /*hist_ready=*/true);
     const uint32_t* ids = zv[0];  // 4 passes: result back in buffer 0
     // (tile, splat) pairs in depth order, then a stable sort by tile (render.hpp:273-294)
     hs::launch_dup_offsets(ids, f->dupcount.as<uint32_t>(), &ds->n_visible_sorted, f->n_max, f->offsets.as<uint32_t>(),

@@ -99,9 +99,12 @@ void launch_count_touched(uint8_t* touched, const uint64_t* n_ptr, uint64_t n_ma
 
 // order.cu
 uint64_t scan_status_words(uint64_t n_max);
+// also fills the digit histograms and zeroes the look-back words of the depth sort
+// whose scratch (4 passes) starts at sort_scratch; its histograms and counters
+// must be zero beforehand (then launch_radix_sort(..., hist_ready = true))
 void launch_compact_visible(const uint32_t* dupcount, const uint4* dinfo, const uint64_t* n_ptr, uint64_t n_max,
                             uint32_t* keys, uint32_t* vals, uint64_t* status, uint32_t* counter, uint64_t* v_out,
-                            cudaStream_t s);
+                            uint32_t* sort_scratch, cudaStream_t s);
 void launch_dup_offsets(const uint32_t* ids, const uint32_t* dupcount, const uint64_t* v_ptr, uint64_t n_max,
                         uint32_t* offsets, uint64_t* status, uint32_t* counter, uint64_t* total_out,
                         uint64_t* sort_n_out, uint64_t capacity, unsigned long long* overflows, cudaStream_t s);
@@ -117,7 +120,8 @@ void launch_make_keys(const uint32_t* tiles, const uint32_t* ids, const uint4* d
 // sort.cu
 uint64_t sort_status_words(uint64_t n_max);
 uint64_t sort_scratch_words(uint64_t n_max, int passes);
+uint64_t sort_tile_keys();
 void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_ptr, uint64_t n_max, int begin_bit,
-                       int passes, int key_bits, uint32_t* scratch, cudaStream_t s);
+                       int passes, int key_bits, uint32_t* scratch, cudaStream_t s, bool hist_ready = false);
 
 }  // namespace hs

@@ -77,20 +77,35 @@ __device__ __forceinline__ uint64_t striped_scan(const uint32_t (&v)[kScanItems]
 }
 
 // Visible splats (tile count > 0) in index order -> (bits(z), id); V.
+// Also prepares the depth sort that follows: the 4 digit histograms of the
+// emitted keys (so the sort needs no histogram pass) and its look-back words
+// zeroed (sort_status_words per pass, for up to tiles(C) tiles).
 __global__ void __launch_bounds__(kScanThreads) k_compact_visible(const uint32_t* __restrict__ dupcount,
                                                                   const uint4* __restrict__ dinfo,
                                                                   const uint64_t* __restrict__ n_ptr,
                                                                   uint32_t* __restrict__ out_keys,
                                                                   uint32_t* __restrict__ out_vals, uint64_t* status,
-                                                                  uint32_t* tile_counter, uint64_t* v_out) {
+                                                                  uint32_t* tile_counter, uint64_t* v_out,
+                                                                  uint32_t* __restrict__ dhist,
+                                                                  uint32_t* __restrict__ sort_status,
+                                                                  uint64_t sort_words, uint64_t sort_tile) {
     __shared__ StripedScan sm;
     __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_dh[4][256];
     const uint64_t n = *n_ptr;
     const uint64_t num_tiles = (n + kScanTile - 1) / kScanTile;
+    {
+        const uint64_t used = ((n + sort_tile - 1) / sort_tile) * 256;
+        for (int p = 0; p < 4; ++p)
+            for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < used;
+                 i += (uint64_t)gridDim.x * blockDim.x)
+                sort_status[p * sort_words + i] = 0;
+    }
     if (n == 0) {
         if (blockIdx.x == 0 && threadIdx.x == 0) *v_out = 0;
         return;
     }
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&s_dh[0][0])[i] = 0;
     const int warp = threadIdx.x >> 5;
     while (true) {
         if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
@@ -111,11 +126,18 @@ __global__ void __launch_bounds__(kScanThreads) k_compact_visible(const uint32_t
             if (v[k]) {
                 const uint64_t i = base + (uint64_t)k * kScanThreads;
                 const uint64_t pos = blk + sm.off[k * 8 + warp] + ex[k];
-                out_keys[pos] = dinfo[i].z;
+                const uint32_t key = dinfo[i].z;
+                out_keys[pos] = key;
                 out_vals[pos] = (uint32_t)i;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) atomicAdd(&s_dh[p][(key >> (8 * p)) & 0xffu], 1u);
             }
         if (tile == num_tiles - 1 && threadIdx.x == 0) *v_out = incl_total;
         __syncthreads();
+    }
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
+        const uint32_t c = (&s_dh[0][0])[i];
+        if (c) atomicAdd(&dhist[i], c);
     }
 }
 
@@ -349,9 +371,13 @@ uint64_t scan_status_words(uint64_t n_max) { return (n_max + kScanTile - 1) / kS
 
 void launch_compact_visible(const uint32_t* dupcount, const uint4* dinfo, const uint64_t* n_ptr, uint64_t n_max,
                             uint32_t* keys, uint32_t* vals, uint64_t* status, uint32_t* counter, uint64_t* v_out,
-                            cudaStream_t s) {
+                            uint32_t* sort_scratch, cudaStream_t s) {
+    // sort_scratch: the depth sort's (launch_radix_sort, 4 passes) histograms | counters | status
+    uint32_t* dhist = sort_scratch;
+    uint32_t* sstatus = sort_scratch + 4 * (256 + 1);
     k_compact_visible<<<scan_grid(n_max), kScanThreads, 0, s>>>(dupcount, dinfo, n_ptr, keys, vals, status, counter,
-                                                                v_out);
+                                                                v_out, dhist, sstatus, sort_status_words(n_max),
+                                                                sort_tile_keys());
     note_launch();
 }
 

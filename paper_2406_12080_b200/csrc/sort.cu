@@ -297,17 +297,21 @@ uint64_t sort_scratch_words(uint64_t n_max, int passes) {
 // direct histogram), 0 otherwise;
 // with keys[1]/vals[1]); the result lands in buffer (passes % 2).  `scratch`
 // holds sort_scratch_words(n_max, passes) u32 and is zeroed here on the device.
+uint64_t sort_tile_keys() { return kSortTile; }
+
 void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_ptr, uint64_t n_max, int begin_bit,
-                       int passes, int key_bits, uint32_t* scratch, cudaStream_t s) {
+                       int passes, int key_bits, uint32_t* scratch, cudaStream_t s, bool hist_ready) {
     const int sms = sort_sms();
     uint32_t* hist = scratch;                        // passes * 256
     uint32_t* counters = scratch + passes * kRadix;  // passes
     uint32_t* status = counters + passes;            // passes * words
     const uint64_t words = sort_status_words(n_max);
-    cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * passes * (kRadix + 1), s);
     const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)sms));
-    if (key_bits > 0 && key_bits <= kDirectBitsMax && key_bits <= 8 * passes)
-    {
+    if (hist_ready) {
+        // the producer kernel filled the histograms and zeroed the look-back words;
+        // the caller zeroed the histograms and tile counters beforehand
+    } else if (key_bits > 0 && key_bits <= kDirectBitsMax && key_bits <= 8 * passes) {
+        cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * passes * (kRadix + 1), s);
         const size_t dsm = sizeof(uint32_t) * (4 * kRadix + ((size_t)1 << key_bits));
         static size_t dsm_set = 0;
         if (dsm > dsm_set) {
@@ -315,10 +319,12 @@ void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_p
             dsm_set = dsm;
         }
         k_sort_hist_direct<<<hgrid, 256, dsm, s>>>(keys[0], n_ptr, hist, begin_bit, key_bits, passes, status, words);
-    }
-    else
+        note_launch();
+    } else {
+        cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * passes * (kRadix + 1), s);
         k_sort_hist<<<hgrid, 256, 0, s>>>(keys[0], n_ptr, hist, begin_bit, passes, status, words);
-    note_launch();
+        note_launch();
+    }
     const size_t smem = sizeof(SortSmem);
     static bool attr_set = false;
     static int per_sm = 1;
