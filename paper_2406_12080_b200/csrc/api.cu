@@ -265,7 +265,7 @@ uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 // the device-side key counts).
 struct ScratchLayout {
     size_t vis_counter = 0, dup_counter = 4, blend_counter = 8, huge_counter = 12, touch_ticket = 16, vis_status = 64, dup_status = 0, zero_bytes = 0,
-           depth_sort = 0, tile_sort = 0, total = 0;
+           depth_sort = 0, tile_sort = 0, blend_list = 0, total = 0;
 };
 ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int tile_passes) {
     ScratchLayout L;
@@ -275,7 +275,8 @@ ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int tile_passes) 
     L.depth_sort = round_up(L.dup_status + hs::scan_status_words(n_max) * 8, 256);
     L.zero_bytes = round_up(L.depth_sort + 4 * (256 + 1) * 4, 256);
     L.tile_sort = round_up(L.depth_sort + hs::sort_scratch_words(n_max, 4) * 4, 256);
-    L.total = L.tile_sort + hs::sort_scratch_words(cap_dup, tile_passes) * 4;
+    L.blend_list = round_up(L.tile_sort + hs::sort_scratch_words(cap_dup, tile_passes) * 4, 256);
+    L.total = L.blend_list + hs::blend_list_words() * 4;
     return L;
 }
 
@@ -379,7 +380,8 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     hs::launch_tile_order(f->ranges.as<uint2>(), cp.tiles_x * cp.tiles_y, &ds->sort_n, f->tile_order.as<uint32_t>(), s);
     hs::launch_blend(ctx->blend_mode, f->ranges.as<uint2>(), kb[fin], vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
                      f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(),
-                     &ds->n_eval, reinterpret_cast<uint32_t*>(sc + L.blend_counter), f->tile_order.as<uint32_t>(), s);
+                     &ds->n_eval, reinterpret_cast<uint32_t*>(sc + L.blend_counter), f->tile_order.as<uint32_t>(),
+                     reinterpret_cast<uint32_t*>(sc + L.blend_list), s);
     hs::launch_count_touched(f->touched.as<uint8_t>(), f->n_ptr, f->n_max, &ds->rendered,
                              reinterpret_cast<const uint64_t*>(ds), reinterpret_cast<uint64_t*>(f->h_stats_dev),
                              (int)(sizeof(DevStats) / 8), reinterpret_cast<uint32_t*>(sc + L.touch_ticket), s);

@@ -33,6 +33,7 @@ constexpr int kBlendWarps = kBlendThreads / 32;
 constexpr size_t kSmemRec = sizeof(float4) * kBlendWarps * 2 * 32 * 4;  // 2-stage record staging
 constexpr size_t kSmemV = sizeof(float) * kBlendWarps * 16 * 33;        // power / alpha per (entry, lane)
 constexpr size_t kSmemQ = sizeof(uint16_t) * kBlendWarps * 512;         // live-pair queue
+constexpr uint32_t kListCap = 1024;                                      // per-warp block list (global, L2)
 
 template <int kMode>
 __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restrict__ ranges,
@@ -44,7 +45,8 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                                                             float* __restrict__ trans, uint8_t* __restrict__ touched,
                                                             unsigned long long* __restrict__ eval_counts,
                                                             uint32_t* __restrict__ task_counter,
-                                                            const uint32_t* __restrict__ tile_order) {
+                                                            const uint32_t* __restrict__ tile_order,
+                                                            uint32_t* lists) {
     // per warp: two stages of 32 staged 64-byte records (cp.async double buffer)
     // (dynamic) s_rec[warps][2][32][4] float4 | s_v[warps][16][33] float | s_q[warps][512] u16
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -53,6 +55,8 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
     auto s_q = reinterpret_cast<uint16_t(*)[512]>(smem_raw + kSmemRec + kSmemV);
     __shared__ uint64_t s_et[32], s_lt[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t* lst = lists + ((size_t)blockIdx.x * kBlendWarps + warp) * kListCap;
     if (tid < 32) {
         s_et[tid] = c_exp2f_tab[tid];
         s_lt[tid] = c_powf_log2_tab[tid];
@@ -88,52 +92,68 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
         float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, d = 0.0f;
         bool done = !inside;
         // The sorted keys carry, in their low 8 bits, which of the tile's 8 blocks each
-        // entry can reach (k_reach_masks, tile_reach_mask): entries outside this
-        // block are never staged.  Ids/keys run two batches ahead, records one.
+        // entry can reach (k_reach_masks, tile_reach_mask): entries that cannot touch
+        // this block are ones the reference `continue`s past at every pixel of it.
+        // Phase A scans a segment of the tile's keys (4 loads of 32 in flight) and
+        // compacts the ids of this block's entries, in depth order, into the warp's
+        // list; phase B stages them 32 at a time (records one batch ahead) and
+        // blends them in dense halves of 16.
         const uint32_t bmask = 1u << blk;
-        auto fetch = [&](uint32_t e, uint32_t& id, bool& hit) {
-            hit = false;
-            id = 0;
-            if (e < range.y) {
-                hit = (keys[e] & bmask) != 0;
-                id = vals[e];
-            }
-        };
-        uint32_t id_cur, id_nxt;
-        bool hit_cur, hit_nxt;
-        fetch(range.x + lane, id_cur, hit_cur);
-        fetch(range.x + 32 + lane, id_nxt, hit_nxt);
-        issue(0, hit_cur, id_cur);
-        int b = 0;
-        for (uint32_t base = range.x; base < range.y; base += 32, ++b) {
-            // records of the next batch in flight while this one is processed
-            issue((b + 1) & 1, hit_nxt, id_nxt);
-            const uint32_t id_b = id_cur;
-            const uint32_t bits = __ballot_sync(0xffffffffu, hit_cur);
-            id_cur = id_nxt;
-            hit_cur = hit_nxt;
-            fetch(base + 64 + lane, id_nxt, hit_nxt);
-            __pipeline_wait_prior(1);
+        uint32_t pos = range.x, limit = 64;
+        while (pos < range.y) {
+            uint32_t n = 0;
+            do {
+                uint32_t kk[4], vv[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint32_t e = pos + 32 * c + lane;
+                    kk[c] = 0;
+                    vv[c] = 0;
+                    if (e < range.y) {
+                        kk[c] = keys[e];
+                        vv[c] = vals[e];
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const bool hit = (kk[c] & bmask) != 0;
+                    const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+                    if (hit) lst[n + __popc(hb & lt_mask)] = vv[c];
+                    n += __popc(hb);
+                }
+                pos += 128;
+            } while (pos < range.y && n <= limit);
+            limit = min(2 * limit, kListCap - 128);
             __syncwarp();
-            if (__all_sync(0xffffffffu, done)) break;
-            if (!bits) continue;
-            const float4(*rec)[4] = s_rec[warp][b & 1];
-            // Phases 2-4 run on the two halves of the batch in turn (16 entries each):
-            // halves the power/alpha scratch, which buys occupancy.
-            uint32_t tmask = 0;
+            uint32_t id_cur = lane < n ? lst[lane] : 0u, id_nxt = lane + 32 < n ? lst[32 + lane] : 0u;
+            issue(0, lane < n, id_cur);
+            int b = 0;
+            for (uint32_t base = 0; base < n; base += 32, ++b) {
+                // records of the next batch in flight while this one is processed
+                issue((b + 1) & 1, base + 32 + lane < n, id_nxt);
+                const uint32_t id_b = id_cur;
+                const uint32_t cnt = min(32u, n - base);
+                id_cur = id_nxt;
+                id_nxt = base + 64 + lane < n ? lst[base + 64 + lane] : 0u;
+                __pipeline_wait_prior(1);
+                __syncwarp();
+                if (__all_sync(0xffffffffu, done)) break;
+                const float4(*rec)[4] = s_rec[warp][b & 1];
+                // Phases 2-4 run on the two halves of the batch in turn (16 entries each):
+                // halves the power/alpha scratch, which buys occupancy.
+                uint32_t tmask = 0;
 #pragma unroll 1
-            for (int h = 0; h < 32; h += 16) {
-            const uint32_t hbits = (bits >> h) & 0xffffu;
-            if (!hbits) continue;
+                for (uint32_t h = 0; h < cnt; h += 16) {
+            const uint32_t hc = min(16u, cnt - h);
             // 2. per-pixel power and liveness (cheap, all lanes)
             uint32_t live = 0;
             if (!done) {
-                n_eval += __popc(hbits);
-                // fully unrolled over the 16 slots with a warp-uniform skip: constant
-                // shared-memory offsets, no bit-scan per entry
+                n_eval += hc;
+                // fully unrolled over the 16 slots with a warp-uniform exit: constant
+                // shared-memory offsets
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
-                    if (!((hbits >> k) & 1u)) continue;
+                    if (k >= (int)hc) break;
                     const float4 p0 = rec[h + k][0];
                     const float4 p1 = rec[h + k][1];
                     const float dx = px - p0.x, dy = py - p0.y;
@@ -225,12 +245,14 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                 tmask |= __reduce_or_sync(0xffffffffu, cm) << h;
             }
             __syncwarp();
+                }
+                if ((tmask >> lane) & 1u) touched[id_b] = 1;  // rendered_count flags, one store per entry
+                __syncwarp();
             }
-            if ((tmask >> lane) & 1u) touched[id_b] = 1;  // rendered_count flags, one store per entry
+            __pipeline_wait_prior(0);
             __syncwarp();
+            if (__all_sync(0xffffffffu, done)) break;
         }
-        __pipeline_wait_prior(0);
-        __syncwarp();
         if (inside) {
             const size_t plane = (size_t)cam.width * cam.height;
             const size_t i = (size_t)y * cam.width + x;
@@ -254,7 +276,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
 void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
                   unsigned long long* eval_counts, uint32_t* task_counter, const uint32_t* tile_order,
-                  cudaStream_t s) {
+                  uint32_t* lists, cudaStream_t s) {
     constexpr size_t kSmem = kSmemRec + kSmemV + kSmemQ;
     static int grid[2] = {0, 0};
     if (!grid[mode]) {
@@ -268,18 +290,26 @@ void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uin
             cudaFuncSetAttribute(k_blend<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blend<1>, kBlendThreads, kSmem);
         }
-        grid[mode] = sms * (per > 0 ? per : 1);
+        grid[mode] = sms * std::min(8, per > 0 ? per : 1);  // blend_list_words() covers 8 per SM
     }
     const int tasks = cam.tiles_x * cam.tiles_y * 8;
     const unsigned g = (unsigned)std::min<int>(grid[mode], std::max(1, tasks / kBlendWarps));
     if (mode == 0) {
         k_blend<0><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
-                                                   eval_counts, task_counter, tile_order);
+                                                   eval_counts, task_counter, tile_order, lists);
     } else {
         k_blend<1><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
-                                                   eval_counts, task_counter, tile_order);
+                                                   eval_counts, task_counter, tile_order, lists);
     }
     note_launch();
+}
+
+// Per-warp block lists: grid (at most 8 CTAs per SM) x warps x kListCap ids.
+uint64_t blend_list_words() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (uint64_t)sms * 8 * kBlendWarps * kListCap;
 }
 
 }  // namespace hs

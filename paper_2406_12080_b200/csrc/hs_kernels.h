@@ -88,7 +88,9 @@ void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_no
 void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
                   unsigned long long* eval_counts, uint32_t* task_counter, const uint32_t* tile_order,
-                  cudaStream_t s);
+                  uint32_t* lists, cudaStream_t s);
+// u32 words of the blend's per-warp block lists (scratch, no initialisation needed)
+uint64_t blend_list_words();
 void launch_tile_order(const uint2* ranges, int tiles, const uint64_t* sort_n_ptr, uint32_t* order, cudaStream_t s);
 void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr,
                      uint64_t n_max, float* mean, float* scale, float* rot, float* sh, float* fall, float* pfall,
