@@ -28,9 +28,25 @@
 
 namespace hs {
 
+// (-0, 1, -1, -0.5) pairs as kernel parameters: see phase 2
+struct PairConsts {
+    uint64_t nz, one, neg1, mhalf;
+};
+
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+    return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ uint64_t lds_u64(const float2* p) { return *reinterpret_cast<const uint64_t*>(p); }
+
 constexpr int kBlendThreads = 128;
 constexpr int kBlendWarps = kBlendThreads / 32;
-constexpr size_t kSmemRec = sizeof(float4) * kBlendWarps * 2 * 32 * 4;  // 2-stage record staging
+constexpr size_t kSmemRec = sizeof(float4) * kBlendWarps * 2 * 32 * 3;  // 2-stage staging of p1..p3
+constexpr size_t kSmemPP = sizeof(float2) * kBlendWarps * 2 * 16 * 6;   // 2-stage entry-pair fields
 constexpr size_t kSmemV = sizeof(float) * kBlendWarps * 16 * 33;        // power / alpha per (entry, lane)
 constexpr size_t kSmemQ = sizeof(uint16_t) * kBlendWarps * 512;         // live-pair queue
 constexpr uint32_t kListCap = 1024;                                      // per-warp block list (global, L2)
@@ -46,13 +62,17 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                                                             unsigned long long* __restrict__ eval_counts,
                                                             uint32_t* __restrict__ task_counter,
                                                             const uint32_t* __restrict__ tile_order,
-                                                            uint32_t* lists) {
-    // per warp: two stages of 32 staged 64-byte records (cp.async double buffer)
-    // (dynamic) s_rec[warps][2][32][4] float4 | s_v[warps][16][33] float | s_q[warps][512] u16
+                                                            uint32_t* lists, PairConsts pc) {
+    // per warp, two stages (cp.async double buffer) of 32 staged records: p1..p3 as
+    // they are, and the phase-2 fields of p0/p1/p3 interleaved by entry pairs (the
+    // packed FP32x2 power evaluation of entries 2j, 2j+1)
+    // (dynamic) s_rec[warps][2][32][3] float4 | s_pp[warps][2][16][6] float2 |
+    //           s_v[warps][16][33] float | s_q[warps][512] u16
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto s_rec = reinterpret_cast<float4(*)[2][32][4]>(smem_raw);
-    auto s_v = reinterpret_cast<float(*)[16][33]>(smem_raw + kSmemRec);
-    auto s_q = reinterpret_cast<uint16_t(*)[512]>(smem_raw + kSmemRec + kSmemV);
+    auto s_rec = reinterpret_cast<float4(*)[2][32][3]>(smem_raw);
+    auto s_pp = reinterpret_cast<float2(*)[2][16][6]>(smem_raw + kSmemRec);
+    auto s_v = reinterpret_cast<float(*)[16][33]>(smem_raw + kSmemRec + kSmemPP);
+    auto s_q = reinterpret_cast<uint16_t(*)[512]>(smem_raw + kSmemRec + kSmemPP + kSmemV);
     __shared__ uint64_t s_et[32], s_lt[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
@@ -72,7 +92,12 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
         if (hit) {
             const float4* src = reinterpret_cast<const float4*>(proj + id);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) __pipeline_memcpy_async(&s_rec[warp][st][lane][q], src + q, 16);
+            for (int q = 0; q < 3; ++q) __pipeline_memcpy_async(&s_rec[warp][st][lane][q], src + 1 + q, 16);
+            // x, y, conic0, conic1, conic2, power floor (ProjRec float offsets 0-4, 13)
+            const float* srcf = reinterpret_cast<const float*>(src);
+            float* dst = &s_pp[warp][st][lane >> 1][0].x + (lane & 1);
+#pragma unroll
+            for (int f = 0; f < 6; ++f) __pipeline_memcpy_async(dst + 2 * f, srcf + (f < 5 ? f : 13), 4);
         }
         __pipeline_commit();
     };
@@ -138,7 +163,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                 __pipeline_wait_prior(1);
                 __syncwarp();
                 if (__all_sync(0xffffffffu, done)) break;
-                const float4(*rec)[4] = s_rec[warp][b & 1];
+                const float4(*rec)[3] = s_rec[warp][b & 1];
                 // Phases 2-4 run on the two halves of the batch in turn (16 entries each):
                 // halves the power/alpha scratch, which buys occupancy.
                 uint32_t tmask = 0;
@@ -149,22 +174,35 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
             uint32_t live = 0;
             if (!done) {
                 n_eval += hc;
-                // fully unrolled over the 16 slots with a warp-uniform exit: constant
-                // shared-memory offsets
+                // entries in pairs, packed FP32x2 (FFMA2): each lane evaluates the
+                // reference's float expression for two entries per instruction.  Every
+                // operation is an fma with a runtime 1 / -1 / -0 operand (PairConsts):
+                // exactly the separately rounded mul / add / sub of the reference, and
+                // opaque to the contraction ptxas applies to packed mul + add.
+                const float2(*pp)[6] = s_pp[warp][b & 1] + (h >> 1);
+                const uint64_t PX = pack2(px, px), PY = pack2(py, py);
 #pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    if (k >= (int)hc) break;
-                    const float4 p0 = rec[h + k][0];
-                    const float4 p1 = rec[h + k][1];
-                    const float dx = px - p0.x, dy = py - p0.y;
-                    const float power = -0.5f * (p0.z * dx * dx + p1.x * dy * dy) - p0.w * dx * dy;
+                for (int kp = 0; kp < 8; ++kp) {
+                    if (2 * kp >= (int)hc) break;
+                    const uint64_t X = lds_u64(&pp[kp][0]), Y = lds_u64(&pp[kp][1]);
+                    const uint64_t A = lds_u64(&pp[kp][2]), B = lds_u64(&pp[kp][3]);
+                    const uint64_t C = lds_u64(&pp[kp][4]);
+                    const float2 fl = pp[kp][5];
+                    const uint64_t dx = ffma2(X, pc.neg1, PX), dy = ffma2(Y, pc.neg1, PY);
+                    const uint64_t t1 = ffma2(ffma2(A, dx, pc.nz), dx, pc.nz);  // conic0 * dx * dx
+                    const uint64_t t2 = ffma2(ffma2(C, dy, pc.nz), dy, pc.nz);  // conic2 * dy * dy
+                    const uint64_t t3 = ffma2(ffma2(B, dx, pc.nz), dy, pc.nz);  // conic1 * dx * dy
+                    const uint64_t sm = ffma2(ffma2(t1, pc.one, t2), pc.mhalf, pc.nz);
+                    const uint64_t pw = ffma2(t3, pc.neg1, sm);
+                    const float p_lo = __uint_as_float((uint32_t)pw), p_hi = __uint_as_float((uint32_t)(pw >> 32));
                     // live iff the alpha can reach the 1/255 floor: m e^power >= 1/255 needs
-                    // power >= -ln(255 m) >= p3.y = -qthr/2 (qthr carries the margin).
+                    // power >= -ln(255 m) >= floor = -qthr/2 (qthr carries the margin).
                     // Branch-free: the power is stored either way (read only for live pairs).
-                    const float fl = rec[h + k][3].y;
-                    const bool lv = (power <= 0.0f) & (power >= fl);
-                    sv[k][lane] = power;
-                    live |= (uint32_t)lv << k;
+                    const bool lv0 = (p_lo <= 0.0f) & (p_lo >= fl.x);
+                    const bool lv1 = (p_hi <= 0.0f) & (p_hi >= fl.y) & (2 * kp + 1 < (int)hc);
+                    sv[2 * kp][lane] = p_lo;
+                    sv[2 * kp + 1][lane] = p_hi;
+                    live |= ((uint32_t)lv0 | ((uint32_t)lv1 << 1)) << (2 * kp);
                 }
             }
             // 3. alpha of every live (pixel, entry) pair.  Alpha does not depend on T, so the
@@ -186,7 +224,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                     const uint32_t pr = sq[pq];
                     const int src = (int)(pr >> 4), k = (int)(pr & 15);
                     const float power = sv[k][src];
-                    const float4 p1 = rec[h + k][1];
+                    const float4 p1 = rec[h + k][0];
                     float g;
                     if (kMode == 0)
                         g = hs_libm::expf_glibc(power, s_et);
@@ -202,7 +240,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                         const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
                         float split = 0.0f;
                         if (par >= kAlphaMin) {
-                            const float ik = rec[h + k][3].x;
+                            const float ik = rec[h + k][2].x;
                             if (kMode == 0)
                                 split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, ik, s_lt, s_et);
                             else
@@ -231,7 +269,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                             done = true;
                             break;
                         }
-                        const float4 p2 = rec[h + k][2];
+                        const float4 p2 = rec[h + k][1];
                         const float wgt = alpha * T;
                         c0 = c0 + p2.x * wgt;
                         c1 = c1 + p2.y * wgt;
@@ -277,7 +315,12 @@ void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uin
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
                   unsigned long long* eval_counts, uint32_t* task_counter, const uint32_t* tile_order,
                   uint32_t* lists, cudaStream_t s) {
-    constexpr size_t kSmem = kSmemRec + kSmemV + kSmemQ;
+    constexpr size_t kSmem = kSmemRec + kSmemPP + kSmemV + kSmemQ;
+    PairConsts pc;
+    pc.nz = 0x8000000080000000ull;     // (-0, -0)
+    pc.one = 0x3f8000003f800000ull;    // (1, 1)
+    pc.neg1 = 0xbf800000bf800000ull;   // (-1, -1)
+    pc.mhalf = 0xbf000000bf000000ull;  // (-0.5, -0.5)
     static int grid[2] = {0, 0};
     if (!grid[mode]) {
         int dev = 0, sms = 148, per = 1;
@@ -296,10 +339,10 @@ void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uin
     const unsigned g = (unsigned)std::min<int>(grid[mode], std::max(1, tasks / kBlendWarps));
     if (mode == 0) {
         k_blend<0><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
-                                                   eval_counts, task_counter, tile_order, lists);
+                                                   eval_counts, task_counter, tile_order, lists, pc);
     } else {
         k_blend<1><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
-                                                   eval_counts, task_counter, tile_order, lists);
+                                                   eval_counts, task_counter, tile_order, lists, pc);
     }
     note_launch();
 }
