@@ -176,6 +176,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tau-sweep", action="store_true")
     ap.add_argument("--reference-budget-s", type=float, default=120.0)
+    ap.add_argument("--lanes", type=int, default=2,
+                    help="frame lanes (streams): consecutive frames on different lanes overlap on the device")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -230,9 +232,34 @@ def main():
     ccams = [c.to_c() for c in cams]
     warm, timed = ccams[: args.warmup], ccams[args.warmup: args.warmup + args.steps]
 
-    # warm-up (synchronous: grows the duplicate buffers to this trajectory's needs)
-    for c in warm:
-        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, None), r.ctx)
+    # frame lanes: frame object k (with its own cut object) binds to lane k at its first
+    # render; frame i of the trajectory goes to object i % NL, so consecutive frames
+    # overlap (one frame's latency-bound sort stages beside the next one's HBM-bound
+    # cut and preprocess).  Every frame is still the full cut + render.
+    NL = max(1, min(4, args.lanes))
+    r.set_lanes(NL)
+    lane_frames, lane_cuts = [r._frame], [r._cut]
+    for _ in range(NL - 1):
+        fr, cu = N.C.c_void_p(), N.C.c_void_p()
+        hs._check(L.hs_frame_create(r.ctx, N.C.byref(fr)), r.ctx)
+        hs._check(L.hs_cut_create(r.ctx, N.C.byref(cu)), r.ctx)
+        lane_frames.append(fr)
+        lane_cuts.append(cu)
+
+    def render(c, tau, k, cut_only=False):
+        if cut_only:  # reuse lane k's cut (bench_path's odd frames)
+            hs._check(L.hs_render_cut(r.ctx, dh.handle, lane_cuts[k], c, lane_frames[k], None), r.ctx)
+        else:
+            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, tau, lane_cuts[k], lane_frames[k], None), r.ctx)
+
+    def wait_lanes():
+        for fr in lane_frames:
+            hs._check(L.hs_frame_wait(r.ctx, fr), r.ctx)  # fails if any timed frame overflowed
+
+    # warm-up (synchronous: grows every lane's duplicate buffers to this trajectory's needs)
+    for k in range(NL):
+        for c in warm:
+            render(c, cfg.tau, k)
     stream = torch.cuda.ExternalStream(r.stream_handle())
 
     # ---- timed region: K frames, async enqueue, CUDA events on the renderer stream
@@ -247,19 +274,36 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     launches0 = L.hs_kernel_launch_count()
     e0.record(stream)
-    for c in timed:
-        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, None), r.ctx)
+    for i, c in enumerate(timed):
+        render(c, cfg.tau, i % NL)
+    r.join()
     e1.record(stream)
     launches = L.hs_kernel_launch_count() - launches0
     e1.synchronize()
     r.synchronize()
     clocks = sampler.stop()
     barrier()
-    hs._check(L.hs_frame_wait(r.ctx, r._frame), r.ctx)  # fails if any timed frame overflowed
-    r.set_async(False)
+    wait_lanes()
     ms_local = e0.elapsed_time(e1)
     ms_total = max_over_ranks(ms_local)
     value = world * len(timed) / (ms_total / 1e3)
+
+    # the same frames on one lane (frame after frame: the per-frame latency view)
+    barrier()
+    torch.cuda.synchronize()
+    r.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for c in timed:
+        render(c, cfg.tau, 0)
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    wait_lanes()
+    r.set_async(False)
+    one_ms = max_over_ranks(e0.elapsed_time(e1))
+    single_lane = {"value": world * len(timed) / (one_ms / 1e3), "unit": UNIT, "ms_per_step": one_ms / len(timed),
+                   "what": "same frames, one lane: each frame starts after the previous one ends"}
 
     # ---- reference cadence (bench.hpp:70-84): cut refreshed on even frames, reused on odd ones
     r.set_async(True)
@@ -269,16 +313,14 @@ def main():
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    for i, c in enumerate(timed):
-        if i % 2 == 0:
-            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, None), r.ctx)
-        else:
-            hs._check(L.hs_render_cut(r.ctx, dh.handle, r._cut, c, r._frame, None), r.ctx)
+    for i, c in enumerate(timed):  # a refresh pair stays on one lane; pairs alternate lanes
+        render(c, cfg.tau, (i // 2) % NL, cut_only=(i % 2 == 1))
+    r.join()
     e3.record(stream)
     e3.synchronize()
     r.synchronize()
     barrier()
-    hs._check(L.hs_frame_wait(r.ctx, r._frame), r.ctx)
+    wait_lanes()
     r.set_async(False)
     cad_ms = max_over_ranks(e2.elapsed_time(e3))
     cadence = {"value": world * len(timed) / (cad_ms / 1e3), "unit": UNIT, "ms_per_step": cad_ms / len(timed),
@@ -290,22 +332,25 @@ def main():
         r.set_async(True)
         for tau in (0.0, 1.5, 3.0, 6.0, 12.0):
             sweep = timed[: min(len(timed), 20)]
-            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, sweep[0], tau, r._cut, r._frame, None), r.ctx)
+            for k in range(NL):
+                render(sweep[0], tau, k)
             r.set_async(False)
-            hs._check(L.hs_frame_wait(r.ctx, r._frame), r.ctx)  # grows the duplicate buffer if needed
-            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, sweep[0], tau, r._cut, r._frame, None), r.ctx)
+            wait_lanes()  # grows the duplicate buffers if needed
+            for k in range(NL):
+                render(sweep[0], tau, k)
             r.set_async(True)
             barrier()
             r.synchronize()
             e4 = torch.cuda.Event(enable_timing=True)
             e5 = torch.cuda.Event(enable_timing=True)
             e4.record(stream)
-            for c in sweep:
-                hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, tau, r._cut, r._frame, None), r.ctx)
+            for i, c in enumerate(sweep):
+                render(c, tau, i % NL)
+            r.join()
             e5.record(stream)
             e5.synchronize()
             r.synchronize()
-            hs._check(L.hs_frame_wait(r.ctx, r._frame), r.ctx)
+            wait_lanes()
             fi = N.hs_frame_info()
             hs._check(L.hs_frame_get_info(r.ctx, r._frame, fi), r.ctx)
             ms = max_over_ranks(e4.elapsed_time(e5)) / len(sweep)
@@ -378,12 +423,15 @@ def main():
     # memory every frame.  NF frame objects in a ring: frame i's read-back (copy stream)
     # overlaps the kernels of frames i+1.., and a frame object is re-rendered only after
     # its previous read-back landed.
-    NF = 3
+    # 2 x NL frame objects (each with its own cut), bound round-robin to the lanes
+    NF = 2 * NL
     f32 = N.C.POINTER(N.C.c_float)
-    frames = [r._frame] + [N.C.c_void_p() for _ in range(NF - 1)]
-    for fr in frames[1:]:
+    frames = lane_frames + [N.C.c_void_p() for _ in range(NF - NL)]
+    fcuts = lane_cuts + [N.C.c_void_p() for _ in range(NF - NL)]
+    for fr, cu in zip(frames[NL:], fcuts[NL:]):
         hs._check(L.hs_frame_create(r.ctx, N.C.byref(fr)), r.ctx)
-        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, timed[0], cfg.tau, r._cut, fr, None), r.ctx)
+        hs._check(L.hs_cut_create(r.ctx, N.C.byref(cu)), r.ctx)
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, timed[0], cfg.tau, cu, fr, None), r.ctx)
     pinned = [torch.empty(5 * W * H, dtype=torch.float32, pin_memory=True) for _ in range(NF)]
     outs = [(N.C.cast(p.data_ptr(), f32), N.C.cast(p.data_ptr() + 12 * W * H, f32),
              N.C.cast(p.data_ptr() + 16 * W * H, f32)) for p in pinned]
@@ -398,18 +446,21 @@ def main():
         fi = i % NF
         if i >= NF:
             hs._check(L.hs_frame_download_wait(r.ctx, frames[fi], N.C.byref(rc)), r.ctx)
-        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, frames[fi], None), r.ctx)
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, fcuts[fi], frames[fi], None), r.ctx)
         hs._check(L.hs_frame_download_async(r.ctx, frames[fi], *outs[fi]), r.ctx)
     for i in range(max(0, len(timed) - NF), len(timed)):
         hs._check(L.hs_frame_download_wait(r.ctx, frames[i % NF], N.C.byref(rc)), r.ctx)
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     r.set_async(False)
-    for fr in frames[1:]:
+    for fr in frames:
         hs._check(L.hs_frame_wait(r.ctx, fr), r.ctx)
+    for fr, cu in zip(frames[1:], fcuts[1:]):
         L.hs_frame_destroy(fr)
+        L.hs_cut_destroy(cu)
     e2e = {"value": world * len(timed) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": N.C.sizeof(N.hs_camera),
            "d2h_bytes_per_step": 20 * W * H + N.C.sizeof(N.hs_frame_info),
-           "pipelining": f"{NF} frame objects; read-back of frame i on a copy stream overlaps frames i+1.."}
+           "pipelining": f"{NF} frame objects on {NL} lanes; read-back of frame i on a copy stream overlaps "
+                         "frames i+1.."}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and h is not None:
@@ -425,12 +476,13 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "leaves": cfg.leaves, "nodes": nodes, "width": W, "height": H,
                        "tau": cfg.tau, "blend_mode": args.mode, "frames": f"trajectory frames {first}.. per rank",
-                       "parallelism": f"view-parallel x{world} (hierarchy replicated)",
+                       "parallelism": f"view-parallel x{world} (hierarchy replicated)", "frame_lanes": NL,
                        "l2": f"inputs larger than L2 (hierarchy {nodes * 288 / 1e9:.1f} GB resident; no flush needed)"},
             "roofline": roofline,
             "stages_ms": stage_ms,
             "stages": stages,
             "per_frame": {"cut_entries": C_, "visible": V_, "duplicates": D_, "n_eval": NE, "n_contrib": NC},
+            "single_lane": single_lane,
             "reference_cadence": cadence,
             "tau_sweep": tau_sweep,
             "cpu_baseline": cpu,

@@ -147,13 +147,19 @@ const char* hs_status_name(hs_status s);
 hs_status hs_context_create(int device, hs_context** out);
 void hs_context_destroy(hs_context* ctx);
 const char* hs_last_error(const hs_context* ctx);
-void* hs_context_stream(hs_context* ctx); /* the cudaStream_t all work runs on */
+void* hs_context_stream(hs_context* ctx); /* the context's cudaStream_t (frame lane 0) */
 hs_status hs_context_synchronize(hs_context* ctx);
+/* Make the context stream wait for all work enqueued on the other frame lanes
+ * (HS_OPT_LANES > 1), e.g. before recording a timing event on it.  Every render
+ * call already orders its lane after the context stream. */
+hs_status hs_context_join(hs_context* ctx);
 
 enum {
     HS_OPT_ASYNC = 1,       /* 0 (default): calls block; 1: render calls only enqueue */
     HS_OPT_BLEND_MODE = 2,  /* 0: exact (glibc expf/powf replicas, bit-exact), 1: fast */
-    HS_OPT_DEBUG = 3        /* 1: keep pre-sort keys + per-splat projection dumps */
+    HS_OPT_DEBUG = 3,       /* 1: keep pre-sort keys + per-splat projection dumps */
+    HS_OPT_LANES = 4        /* 1..4 frame lanes (streams); frame objects bind round-robin at
+                               their first render, so frames on different lanes overlap */
 };
 hs_status hs_context_set_option(hs_context* ctx, int option, int64_t value);
 

@@ -529,6 +529,15 @@ class Renderer:
     def set_async(self, on: bool):
         _check(N.lib().hs_context_set_option(self.ctx, N.HS_OPT_ASYNC, 1 if on else 0), self.ctx)
 
+    def set_lanes(self, n: int):
+        """Frame lanes (HS_OPT_LANES): frame objects bind round-robin to n streams at
+        their first render, so frames rendered on different objects overlap."""
+        _check(N.lib().hs_context_set_option(self.ctx, N.HS_OPT_LANES, int(n)), self.ctx)
+
+    def join(self):
+        """Order the context stream after the work enqueued on every lane."""
+        _check(N.lib().hs_context_join(self.ctx), self.ctx)
+
     def stream_handle(self) -> int:
         return int(N.lib().hs_context_stream(self.ctx) or 0)
 

@@ -61,6 +61,7 @@ class hs_frame_info(C.Structure):
 HS_OPT_ASYNC = 1
 HS_OPT_BLEND_MODE = 2
 HS_OPT_DEBUG = 3
+HS_OPT_LANES = 4
 
 # every symbol include/hsplat_b200.h declares: name -> (restype, argtypes)
 _vp = C.c_void_p
@@ -71,6 +72,7 @@ _SIGS = {
     "hs_last_error": (C.c_char_p, [_vp]),
     "hs_context_stream": (_vp, [_vp]),
     "hs_context_synchronize": (C.c_int, [_vp]),
+    "hs_context_join": (C.c_int, [_vp]),
     "hs_context_set_option": (C.c_int, [_vp, C.c_int, C.c_int64]),
     "hs_hierarchy_upload": (C.c_int, [_vp, C.POINTER(hs_node_soa), C.c_uint64, C.c_uint32, C.c_int,
                                       C.POINTER(_vp)]),

@@ -79,6 +79,8 @@ struct DBuf {
 
 }  // namespace
 
+constexpr int kMaxLanes = 4;
+
 struct hs_context {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -87,7 +89,12 @@ struct hs_context {
     bool async = false;
     int blend_mode = 0;
     bool debug = false;
-    DBuf cut_scratch;
+    // Frame lanes (HS_OPT_LANES): lane 0 is `stream`; a frame object is bound to
+    // one lane at its first render, so frames on different lanes overlap on the
+    // device.  Each render forks its lane from `stream`; hs_context_join joins back.
+    int n_lanes = 1, next_lane = 0;
+    cudaStream_t lanes[kMaxLanes] = {};
+    cudaEvent_t fork_ev = nullptr, join_ev[kMaxLanes] = {};
 };
 
 struct hs_hierarchy {
@@ -105,9 +112,14 @@ struct hs_cut {
     uint64_t* h_count_dev = nullptr;  // device alias of h_count
     const hs_hierarchy* h = nullptr;
     cudaEvent_t done = nullptr;
+    DBuf scratch;  // select_cut scratch
+    // cross-lane hazards: the last write or read of this cut, and its stream
+    mutable cudaEvent_t last = nullptr;
+    mutable cudaStream_t last_stream = nullptr;
     ~hs_cut() {
         if (h_count) cudaFreeHost(h_count);
         if (done) cudaEventDestroy(done);
+        if (last) cudaEventDestroy(last);
     }
 };
 
@@ -144,6 +156,9 @@ struct hs_frame {
     hs_stage_times* times = nullptr;
     bool cut_timed = false;
     hs_cut* own_cut = nullptr;
+    int lane = -1;                 // bound at the first render (frame_stream)
+    cudaStream_t s = nullptr;      // the lane's stream
+    const hs_cut* src_cut = nullptr;  // cut read by the last raster call (hazard tracking)
     // last raster call (for an overflow re-run)
     bool from_cut = false;
     const float4* attr = nullptr;
@@ -280,6 +295,38 @@ ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int tile_passes) 
     return L;
 }
 
+// The stream of frame f's lane (binding the frame to a lane at its first use).
+cudaStream_t frame_stream(hs_context* ctx, hs_frame* f) {
+    if (f->lane < 0) {
+        f->lane = ctx->next_lane++ % ctx->n_lanes;
+        f->s = ctx->lanes[f->lane];  // lanes[0] is the context stream
+    }
+    return f->s;
+}
+
+// Order frame f's lane after everything enqueued on the context stream so far.
+hs_status fork_lane(hs_context* ctx, hs_frame* f) {
+    cudaStream_t s = frame_stream(ctx, f);
+    if (s != ctx->stream) {
+        HS_CUDA(ctx, cudaEventRecord(ctx->fork_ev, ctx->stream));
+        HS_CUDA(ctx, cudaStreamWaitEvent(s, ctx->fork_ev, 0));
+    }
+    return HS_OK;
+}
+
+// A cut written or read on stream s waits for its last use on another stream;
+// mark_cut records the use.
+hs_status acquire_cut(hs_context* ctx, const hs_cut* cut, cudaStream_t s) {
+    if (cut->last_stream && cut->last_stream != s) HS_CUDA(ctx, cudaStreamWaitEvent(s, cut->last, 0));
+    return HS_OK;
+}
+hs_status mark_cut(hs_context* ctx, const hs_cut* cut, cudaStream_t s) {
+    if (!cut->last) HS_CUDA(ctx, cudaEventCreateWithFlags(&cut->last, cudaEventDisableTiming));
+    HS_CUDA(ctx, cudaEventRecord(cut->last, s));
+    cut->last_stream = s;
+    return HS_OK;
+}
+
 hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamParams& cp) {
     const int tiles = cp.tiles_x * cp.tiles_y;
     if (f->cap_splats < n_max) f->cap_splats = n_max;
@@ -291,7 +338,7 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
     HS_CUDA(ctx, f->offsets.ensure(cs * 4));
     const bool fresh_touched = f->touched.bytes < cs;
     HS_CUDA(ctx, f->touched.ensure(cs));
-    if (fresh_touched) HS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, f->touched.bytes, ctx->stream));
+    if (fresh_touched) HS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, f->touched.bytes, frame_stream(ctx, f)));
     for (int b = 0; b < 2; ++b) {
         HS_CUDA(ctx, f->zkeys[b].ensure(cs * 4));
         HS_CUDA(ctx, f->zvals[b].ensure(cs * 4));
@@ -330,7 +377,7 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
 
 // Enqueue the raster stages (preprocess .. count) for the call stored in f.
 hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
-    cudaStream_t s = ctx->stream;
+    cudaStream_t s = frame_stream(ctx, f);
     const CamParams& cp = f->cam;
     DevStats* ds = f->stats.as<DevStats>();
     const ScratchLayout L = scratch_layout(std::max<uint64_t>(f->cap_splats, 1), f->cap_dup, f->passes);
@@ -345,6 +392,8 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
                           f->dinfo.as<uint4>(), f->dupcount.as<uint32_t>(),
                           ctx->debug ? f->dbg16.as<float>() : nullptr, &ds->n_visible,
                           f->from_cut ? &ds->n_splats : nullptr, s);
+    // the cut's arrays are not read past preprocess (n_splats holds its count from here)
+    if (f->from_cut && f->src_cut) HS_TRY(mark_cut(ctx, f->src_cut, s));
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[2], s));
     // depth order of the visible splats (stable: ties keep cut order, render.hpp:268-272)
     uint32_t* zk[2] = {f->zkeys[0].as<uint32_t>(), f->zkeys[1].as<uint32_t>()};
@@ -382,7 +431,7 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
                      f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(),
                      &ds->n_eval, reinterpret_cast<uint32_t*>(sc + L.blend_counter), f->tile_order.as<uint32_t>(),
                      reinterpret_cast<uint32_t*>(sc + L.blend_list), s);
-    hs::launch_count_touched(f->touched.as<uint8_t>(), f->n_ptr, f->n_max, &ds->rendered,
+    hs::launch_count_touched(f->touched.as<uint8_t>(), &ds->n_splats, f->n_max, &ds->rendered,
                              reinterpret_cast<const uint64_t*>(ds), reinterpret_cast<uint64_t*>(f->h_stats_dev),
                              (int)(sizeof(DevStats) / 8), reinterpret_cast<uint32_t*>(sc + L.touch_ticket), s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[5], s));
@@ -399,13 +448,13 @@ hs_status finish_frame(hs_context* ctx, hs_frame* f, bool allow_retry) {
         f->pending = false;
         const DevStats st = *f->h_stats;
         if (st.overflows > 0 && !allow_retry) {
-            HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, ctx->stream));
+            HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, frame_stream(ctx, f)));
             return set_err(ctx, HS_CAPACITY_EXCEEDED,
                            std::to_string(st.overflows) +
                                " async frame(s) overflowed the duplicate buffer; render once synchronously to grow it");
         }
         if (st.n_dup > 0 && st.sort_n == 0) {
-            HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, ctx->stream));
+            HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, frame_stream(ctx, f)));
             if (!allow_retry)
                 return set_err(ctx, HS_CAPACITY_EXCEEDED,
                                "duplicate buffer too small (" + std::to_string(st.n_dup) + " > " +
@@ -454,20 +503,23 @@ hs_status ensure_cut(hs_context* ctx, hs_cut* cut, uint64_t cap) {
     return HS_OK;
 }
 
-hs_status enqueue_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cam, float tau, hs_cut* cut) {
+hs_status enqueue_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cam, float tau, hs_cut* cut,
+                      cudaStream_t s) {
     if (!(tau >= 0.0f) || h->n == 0)
         return set_err(ctx, HS_INVALID_ARGUMENT, "select_cut needs tau >= 0 and nodes");  // lod.hpp:53
     hs_status st = ensure_cut(ctx, cut, h->n);
     if (st != HS_OK) return st;
     const uint64_t words = hs::select_cut_scratch_words(h->n);
-    HS_CUDA(ctx, ctx->cut_scratch.ensure(words * 4));
-    uint32_t* sc = ctx->cut_scratch.as<uint32_t>();
-    HS_CUDA(ctx, cudaMemsetAsync(sc, 0, hs::select_cut_zero_words(h->n) * 4, ctx->stream));  // counters
+    HS_CUDA(ctx, cut->scratch.ensure(words * 4));
+    uint32_t* sc = cut->scratch.as<uint32_t>();
+    HS_TRY(acquire_cut(ctx, cut, s));
+    HS_CUDA(ctx, cudaMemsetAsync(sc, 0, hs::select_cut_zero_words(h->n) * 4, s));  // counters
     const CamParams cp = make_cam(cam);
     hs::launch_select_cut(h->cull.as<float4>(), h->n, cp, tau, cut->node.as<uint32_t>(), cut->t.as<float>(),
-                          cut->alpha.as<float>(), sc, cut->count.as<uint64_t>(), cut->h_count_dev, ctx->stream);
+                          cut->alpha.as<float>(), sc, cut->count.as<uint64_t>(), cut->h_count_dev, s);
     HS_CUDA(ctx, cudaGetLastError());
-    HS_CUDA(ctx, cudaEventRecord(cut->done, ctx->stream));
+    HS_CUDA(ctx, cudaEventRecord(cut->done, s));
+    HS_TRY(mark_cut(ctx, cut, s));
     cut->h = h;
     return HS_OK;
 }
@@ -554,10 +606,12 @@ hs_status hs_context_create(int device, hs_context** out) {
     auto* ctx = new hs_context();
     ctx->device = device;
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming) != cudaSuccess) {
         delete ctx;
         return HS_CUDA_ERROR;
     }
+    ctx->lanes[0] = ctx->stream;
     *out = ctx;
     return HS_OK;
 }
@@ -567,6 +621,14 @@ void hs_context_destroy(hs_context* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->copy_stream);
+    for (int l = 1; l < kMaxLanes; ++l)
+        if (ctx->lanes[l]) {
+            cudaStreamSynchronize(ctx->lanes[l]);
+            cudaStreamDestroy(ctx->lanes[l]);
+        }
+    for (auto& e : ctx->join_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
     cudaStream_t st = ctx->stream, cs = ctx->copy_stream;
     delete ctx;
     cudaStreamDestroy(st);
@@ -577,7 +639,17 @@ const char* hs_last_error(const hs_context* ctx) { return ctx ? ctx->err.c_str()
 void* hs_context_stream(hs_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 hs_status hs_context_synchronize(hs_context* ctx) {
+    for (int l = 0; l < ctx->n_lanes; ++l) HS_CUDA(ctx, cudaStreamSynchronize(ctx->lanes[l]));
     HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return HS_OK;
+}
+
+hs_status hs_context_join(hs_context* ctx) {
+    if (!ctx) return HS_INVALID_ARGUMENT;
+    for (int l = 1; l < ctx->n_lanes; ++l) {
+        HS_CUDA(ctx, cudaEventRecord(ctx->join_ev[l], ctx->lanes[l]));
+        HS_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join_ev[l], 0));
+    }
     return HS_OK;
 }
 
@@ -589,6 +661,15 @@ hs_status hs_context_set_option(hs_context* ctx, int option, int64_t value) {
             ctx->blend_mode = (int)value;
             return HS_OK;
         case HS_OPT_DEBUG: ctx->debug = value != 0; return HS_OK;
+        case HS_OPT_LANES:
+            if (value < 1 || value > kMaxLanes) return set_err(ctx, HS_INVALID_ARGUMENT, "lanes is 1..4");
+            for (int l = 1; l < value; ++l)
+                if (!ctx->lanes[l]) {
+                    HS_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->lanes[l], cudaStreamNonBlocking));
+                    HS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->join_ev[l], cudaEventDisableTiming));
+                }
+            ctx->n_lanes = (int)value;
+            return HS_OK;
         default: return set_err(ctx, HS_INVALID_ARGUMENT, "unknown option");
     }
 }
@@ -889,7 +970,7 @@ void hs_cut_destroy(hs_cut* cut) {
 
 hs_status hs_select_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cam, float tau, hs_cut* cut) {
     if (!ctx || !h || !cam || !cut) return HS_INVALID_ARGUMENT;
-    hs_status s = enqueue_cut(ctx, h, cam, tau, cut);
+    hs_status s = enqueue_cut(ctx, h, cam, tau, cut, ctx->stream);
     if (s != HS_OK) return s;
     if (!ctx->async) HS_CUDA(ctx, cudaEventSynchronize(cut->done));
     return HS_OK;
@@ -996,6 +1077,7 @@ hs_status hs_frame_create(hs_context* ctx, hs_frame** out) {
 void hs_frame_destroy(hs_frame* f) {
     if (!f) return;
     cudaStreamSynchronize(f->ctx->stream);
+    if (f->s) cudaStreamSynchronize(f->s);
     delete f;
 }
 
@@ -1014,6 +1096,8 @@ static hs_status render_from_cut(hs_context* ctx, const hs_hierarchy* h, const h
     f->times = times;
     f->timed = times != nullptr;
     f->cut_timed = cut_timed;
+    f->src_cut = cut;
+    HS_TRY(acquire_cut(ctx, cut, frame_stream(ctx, f)));
     s = enqueue_raster(ctx, f);
     if (s != HS_OK) return s;
     if (!ctx->async) return finish_frame(ctx, f, true);
@@ -1034,13 +1118,14 @@ hs_status hs_render_hierarchy(hs_context* ctx, const hs_hierarchy* h, const hs_c
         }
         cut = f->own_cut;
     }
-    hs_status s = HS_OK;
+    hs_status s = fork_lane(ctx, f);
+    if (s != HS_OK) return s;
     if (times) {
         s = ensure_frame(ctx, f, std::max<uint64_t>(h->n, 1), make_cam(cam));
         if (s != HS_OK) return s;
-        HS_CUDA(ctx, cudaEventRecord(f->ev[0], ctx->stream));
+        HS_CUDA(ctx, cudaEventRecord(f->ev[0], frame_stream(ctx, f)));
     }
-    s = enqueue_cut(ctx, h, cam, tau, cut);
+    s = enqueue_cut(ctx, h, cam, tau, cut, frame_stream(ctx, f));
     if (s != HS_OK) return s;
     // select_cut does not validate the camera; render_forward does (render.hpp:248)
     s = validate_camera(ctx, cam);
@@ -1057,6 +1142,8 @@ hs_status hs_render_cut(hs_context* ctx, const hs_hierarchy* h, const hs_cut* cu
         if (s != HS_OK) return s;
     }
     hs_status s = validate_camera(ctx, cam);
+    if (s != HS_OK) return s;
+    s = fork_lane(ctx, f);
     if (s != HS_OK) return s;
     return render_from_cut(ctx, h, cut, cam, f, times, false);
 }
@@ -1104,6 +1191,9 @@ hs_status hs_render_splats(hs_context* ctx, const hs_splat_soa* sp, uint64_t n, 
     f->times = times;
     f->timed = times != nullptr;
     f->cut_timed = false;
+    f->src_cut = nullptr;
+    s = fork_lane(ctx, f);
+    if (s != HS_OK) return s;
     s = enqueue_raster(ctx, f);
     if (s != HS_OK) return s;
     if (!ctx->async) return finish_frame(ctx, f, true);

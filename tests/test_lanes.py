@@ -1,0 +1,85 @@
+"""Frame lanes (HS_OPT_LANES): frames rendered on frame objects bound to
+different streams overlap on the device; results must be bit-identical to
+frame-after-frame rendering, including when one cut object is written and read
+from two lanes (the cut's cross-lane hazard tracking)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2406_12080_b200 as hs
+from paper_2406_12080_b200 import _native as N
+from paper_2406_12080_b200 import scenes
+
+pytestmark = pytest.mark.gpu
+
+
+def _images(L, r, fr, w, h):
+    col = np.empty(3 * w * h, np.float32)
+    dep = np.empty(w * h, np.float32)
+    tr = np.empty(w * h, np.float32)
+    rc = C.c_int32()
+    f32 = C.POINTER(C.c_float)
+    hs._check(L.hs_frame_download(r.ctx, fr, col.ctypes.data_as(f32), dep.ctypes.data_as(f32),
+                                  tr.ctypes.data_as(f32), C.byref(rc)), r.ctx)
+    return np.concatenate([col, dep, tr]).view(np.uint32), int(rc.value)
+
+
+def _new(L, r, kind):
+    p = C.c_void_p()
+    hs._check(getattr(L, f"hs_{kind}_create")(r.ctx, C.byref(p)), r.ctx)
+    return p
+
+
+def test_lanes_bit_exact_and_shared_cut():
+    cfg = scenes.CONFIGS["c1"]
+    h = scenes.hierarchy(cfg)
+    cams = [c.to_c() for c in scenes.trajectory(cfg, 8)]
+    w, hh = cfg.width, cfg.height
+    L = N.lib()
+    r = hs.Renderer(0)
+    try:
+        dh = r.upload(h, validate=False)
+        # frame after frame on the default (lane 0) objects
+        ref = []
+        for c in cams:
+            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, None), r.ctx)
+            ref.append(_images(L, r, r._frame, w, hh))
+        # bench_path's odd frame: the previous cut with the next camera
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, cams[2], cfg.tau, r._cut, r._frame, None), r.ctx)
+        hs._check(L.hs_render_cut(r.ctx, dh.handle, r._cut, cams[3], r._frame, None), r.ctx)
+        ref_reuse = _images(L, r, r._frame, w, hh)
+
+        r.set_lanes(2)
+        fa, fb = _new(L, r, "frame"), _new(L, r, "frame")
+        ca, cb = _new(L, r, "cut"), _new(L, r, "cut")
+        # synchronous first renders bind fa -> lane 1, fb -> lane 0 and size their buffers
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, cams[0], cfg.tau, ca, fa, None), r.ctx)
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, cams[0], cfg.tau, cb, fb, None), r.ctx)
+        r.set_async(True)
+        for i in range(0, len(cams), 2):
+            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, cams[i], cfg.tau, ca, fa, None), r.ctx)
+            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, cams[i + 1], cfg.tau, cb, fb, None), r.ctx)
+            r.set_async(False)
+            ia, ib = _images(L, r, fa, w, hh), _images(L, r, fb, w, hh)
+            assert np.array_equal(ia[0], ref[i][0]) and ia[1] == ref[i][1]
+            assert np.array_equal(ib[0], ref[i + 1][0]) and ib[1] == ref[i + 1][1]
+            r.set_async(True)
+        # one cut object across the lanes: written on lane 1 (fa), read on lane 0 (fb),
+        # then rewritten on lane 1 while fb may still be reading it
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, cams[2], cfg.tau, ca, fa, None), r.ctx)
+        hs._check(L.hs_render_cut(r.ctx, dh.handle, ca, cams[3], fb, None), r.ctx)
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, cams[6], cfg.tau, ca, fa, None), r.ctx)
+        r.set_async(False)
+        ib, ia = _images(L, r, fb, w, hh), _images(L, r, fa, w, hh)
+        assert np.array_equal(ib[0], ref_reuse[0]) and ib[1] == ref_reuse[1]
+        assert np.array_equal(ia[0], ref[6][0]) and ia[1] == ref[6][1]
+        # the context stream joins both lanes
+        hs._check(L.hs_context_join(r.ctx), r.ctx)
+        r.synchronize()
+        for p in (fa, fb):
+            L.hs_frame_destroy(p)
+        for p in (ca, cb):
+            L.hs_cut_destroy(p)
+    finally:
+        r.close()
