@@ -237,8 +237,6 @@ def main():
     # overlap (one frame's latency-bound sort stages beside the next one's HBM-bound
     # cut and preprocess).  Every frame is still the full cut + render.
     NL = max(1, min(4, args.lanes))
-    if cfg.name.startswith("c5"):
-        NL = 1  # a frame object is sized for a cut of every node (2e8 x ~120 B): one fits beside the 58 GB scene
     r.set_lanes(NL)
     lane_frames, lane_cuts = [r._frame], [r._cut]
     for _ in range(NL - 1):
@@ -337,7 +335,7 @@ def main():
             for k in range(NL):
                 render(sweep[0], tau, k)
             r.set_async(False)
-            wait_lanes()  # grows the duplicate buffers if needed
+            wait_lanes()
             for k in range(NL):
                 render(sweep[0], tau, k)
             r.set_async(True)

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -51,6 +52,7 @@ struct DevStats {
     unsigned long long n_eval;     // (pixel, entry) pairs evaluated by the blend
     unsigned long long n_contrib;  // pairs that contributed
     uint64_t n_visible_sorted;     // V from the order-preserving compaction (key count of the depth sort)
+    uint64_t n_splats_req;         // C when it exceeded the frame's per-splat capacity (else 0)
     unsigned long long overflows;  // sticky: frames whose D exceeded capacity since the last wait
 };
 
@@ -157,6 +159,8 @@ struct hs_frame {
     bool cut_timed = false;
     hs_cut* own_cut = nullptr;
     int lane = -1;                 // bound at the first render (frame_stream)
+    uint64_t cut_cap = 0;          // per-splat capacity for cut renders (0: not sized yet)
+    uint64_t n_full = 0;           // the cut's own capacity (all nodes)
     cudaStream_t s = nullptr;      // the lane's stream
     const hs_cut* src_cut = nullptr;  // cut read by the last raster call (hazard tracking)
     // last raster call (for an overflow re-run)
@@ -391,14 +395,14 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     hs::launch_preprocess(f->from_cut, f->attr, f->cut_node, f->cut_t, f->n_ptr, f->n_max, cp, f->proj.as<ProjRec>(),
                           f->dinfo.as<uint4>(), f->dupcount.as<uint32_t>(),
                           ctx->debug ? f->dbg16.as<float>() : nullptr, &ds->n_visible,
-                          f->from_cut ? &ds->n_splats : nullptr, s);
+                          f->from_cut ? &ds->n_splats : nullptr, &ds->overflows, &ds->n_splats_req, s);
     // the cut's arrays are not read past preprocess (n_splats holds its count from here)
     if (f->from_cut && f->src_cut) HS_TRY(mark_cut(ctx, f->src_cut, s));
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[2], s));
     // depth order of the visible splats (stable: ties keep cut order, render.hpp:268-272)
     uint32_t* zk[2] = {f->zkeys[0].as<uint32_t>(), f->zkeys[1].as<uint32_t>()};
     uint32_t* zv[2] = {f->zvals[0].as<uint32_t>(), f->zvals[1].as<uint32_t>()};
-    hs::launch_compact_visible(f->dupcount.as<uint32_t>(), f->dinfo.as<uint4>(), f->n_ptr, f->n_max, zk[0], zv[0],
+    hs::launch_compact_visible(f->dupcount.as<uint32_t>(), f->dinfo.as<uint4>(), &ds->n_splats, f->n_max, zk[0], zv[0],
                                reinterpret_cast<uint64_t*>(sc + L.vis_status),
                                reinterpret_cast<uint32_t*>(sc + L.vis_counter), &ds->n_visible_sorted,
                                reinterpret_cast<uint32_t*>(sc + L.depth_sort), s);
@@ -451,7 +455,17 @@ hs_status finish_frame(hs_context* ctx, hs_frame* f, bool allow_retry) {
             HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, frame_stream(ctx, f)));
             return set_err(ctx, HS_CAPACITY_EXCEEDED,
                            std::to_string(st.overflows) +
-                               " async frame(s) overflowed the duplicate buffer; render once synchronously to grow it");
+                               " async frame(s) overflowed the frame buffers; render once synchronously to grow them");
+        }
+        if (st.n_splats_req > 0) {  // a cut larger than the per-splat buffers (sync call: grow, re-run)
+            HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, frame_stream(ctx, f)));
+            f->cut_cap = std::min<uint64_t>(f->n_full, st.n_splats_req + st.n_splats_req / 4 + 1024);
+            f->n_max = f->cut_cap;
+            hs_status s = ensure_frame(ctx, f, f->n_max, f->cam);
+            if (s != HS_OK) return s;
+            s = enqueue_raster(ctx, f);
+            if (s != HS_OK) return s;
+            continue;
         }
         if (st.n_dup > 0 && st.sort_n == 0) {
             HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, frame_stream(ctx, f)));
@@ -1084,7 +1098,13 @@ void hs_frame_destroy(hs_frame* f) {
 static hs_status render_from_cut(hs_context* ctx, const hs_hierarchy* h, const hs_cut* cut, const hs_camera* cam,
                                  hs_frame* f, hs_stage_times* times, bool cut_timed) {
     const CamParams cp = make_cam(cam);
-    hs_status s = ensure_frame(ctx, f, cut->cap, cp);
+    // per-splat buffers for a cut of every leaf (a cut partitions the leaves, so C <=
+    // leaves: about half the nodes); grown by a synchronous call should a cut exceed it
+    if (f->cut_cap == 0) {
+        f->cut_cap = std::max<uint64_t>(1, h->leaves);
+        if (const char* e = getenv("HS_CUT_CAP_INIT")) f->cut_cap = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
+    }
+    hs_status s = ensure_frame(ctx, f, std::min<uint64_t>(cut->cap, f->cut_cap), cp);
     if (s != HS_OK) return s;
     f->cam = cp;
     f->from_cut = true;
@@ -1092,7 +1112,8 @@ static hs_status render_from_cut(hs_context* ctx, const hs_hierarchy* h, const h
     f->cut_node = cut->node.as<uint32_t>();
     f->cut_t = cut->t.as<float>();
     f->n_ptr = cut->count.as<uint64_t>();
-    f->n_max = cut->cap;
+    f->n_full = cut->cap;
+    f->n_max = std::min<uint64_t>(cut->cap, f->cut_cap);
     f->times = times;
     f->timed = times != nullptr;
     f->cut_timed = cut_timed;

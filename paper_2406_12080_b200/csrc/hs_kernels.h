@@ -84,6 +84,7 @@ void launch_backward(const float4* attr, uint64_t n, const CamParams& cam, const
 void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,
                        const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint4* dinfo,
                        uint32_t* dupcount, float* dbg16, unsigned long long* n_visible, uint64_t* n_out,
+                       unsigned long long* overflows, uint64_t* n_req,
                        cudaStream_t s);
 void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,

@@ -149,9 +149,23 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const float4* __restrict_
                                                     uint4* __restrict__ dinfo,
                                                     uint32_t* __restrict__ dupcount, float* __restrict__ dbg16,
                                                     unsigned long long* __restrict__ n_visible,
-                                                    uint64_t* __restrict__ n_out) {
-    const uint64_t n = *n_ptr;
-    if (n_out && blockIdx.x == 0 && threadIdx.x == 0) *n_out = n;  // frame stats: C
+                                                    uint64_t* __restrict__ n_out, uint64_t cap,
+                                                    unsigned long long* __restrict__ overflows,
+                                                    uint64_t* __restrict__ n_req) {
+    uint64_t n = *n_ptr;
+    if (n_out) {
+        // a cut larger than the frame's per-splat buffers: nothing is rendered, the
+        // frame is flagged and a synchronous call grows the buffers and re-runs it
+        if (n > cap) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                *n_out = 0;
+                *n_req = n;
+                atomicAdd(overflows, 1ull);
+            }
+            return;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = n;  // frame stats: C
+    }
     uint32_t vis = 0;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
         SplatIn si;
@@ -436,14 +450,14 @@ static unsigned grid_for(uint64_t n_max, int per_sm) {
 void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,
                        const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint4* dinfo,
                        uint32_t* dupcount, float* dbg16, unsigned long long* n_visible, uint64_t* n_out,
-                       cudaStream_t s) {
+                       unsigned long long* overflows, uint64_t* n_req, cudaStream_t s) {
     const unsigned grid = grid_for(n_max, 8);
     if (from_cut)
         k_preprocess<true><<<grid, 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, cam, proj, dinfo, dupcount, dbg16,
-                                                n_visible, n_out);
+                                                n_visible, n_out, n_max, overflows, n_req);
     else
         k_preprocess<false><<<grid, 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, cam, proj, dinfo, dupcount, dbg16,
-                                                 n_visible, n_out);
+                                                 n_visible, n_out, n_max, overflows, n_req);
     note_launch();
 }
 

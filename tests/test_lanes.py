@@ -83,3 +83,36 @@ def test_lanes_bit_exact_and_shared_cut():
             L.hs_cut_destroy(p)
     finally:
         r.close()
+
+
+def test_cut_capacity_growth(monkeypatch):
+    """A cut larger than a frame object's per-splat buffers is flagged on the device
+    (nothing rendered); a synchronous call grows the buffers and re-runs the frame,
+    an asynchronous one reports CapacityExceeded at the wait."""
+    cfg = scenes.CONFIGS["c1"]
+    h = scenes.hierarchy(cfg)
+    cams = [c.to_c() for c in scenes.trajectory(cfg, 3)]
+    w, hh = cfg.width, cfg.height
+    L = N.lib()
+    ref = hs.Renderer(0)
+    monkeypatch.setenv("HS_CUT_CAP_INIT", "1000")
+    small = hs.Renderer(0)
+    try:
+        dr, ds = ref.upload(h, validate=False), small.upload(h, validate=False)
+        hs._check(L.hs_render_hierarchy(ref.ctx, dr.handle, cams[0], cfg.tau, ref._cut, ref._frame, None), ref.ctx)
+        a = _images(L, ref, ref._frame, w, hh)
+        hs._check(L.hs_render_hierarchy(small.ctx, ds.handle, cams[0], cfg.tau, small._cut, small._frame, None),
+                  small.ctx)
+        b = _images(L, small, small._frame, w, hh)
+        assert np.array_equal(a[0], b[0]) and a[1] == b[1]
+        # async on a fresh small object: the wait reports the overflow
+        fr, cu = _new(L, small, "frame"), _new(L, small, "cut")
+        small.set_async(True)
+        hs._check(L.hs_render_hierarchy(small.ctx, ds.handle, cams[1], cfg.tau, cu, fr, None), small.ctx)
+        assert L.hs_frame_wait(small.ctx, fr) == 103  # HS_CAPACITY_EXCEEDED
+        small.set_async(False)
+        L.hs_frame_destroy(fr)
+        L.hs_cut_destroy(cu)
+    finally:
+        small.close()
+        ref.close()
