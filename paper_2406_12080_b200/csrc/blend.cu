@@ -258,27 +258,31 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
             //    not live for a pixel is a no-op there).  Contributions are collected per
             //    lane (cm) and reduced once per half batch.
             {
+                const float4(*rh)[3] = rec + h;
                 uint32_t act = done ? 0u : live, cm = 0;
                 while (act) {
-                    const int k = __ffs(act) - 1;
-                    act &= act - 1;
+                    const uint32_t bit = act & (0u - act);  // lowest pending entry
+                    act ^= bit;
+                    int k;
+                    asm("bfind.u32 %0, %1;" : "=r"(k) : "r"(bit));
                     const float alpha = sv[k][lane];
                     if (alpha > 0.0f) {
                         const float test = T * (1.0f - alpha);
                         if (test < kTransmittanceEps) {
-                            done = true;
+                            act |= bit;  // the pixel is done: act stays non-zero
                             break;
                         }
-                        const float4 p2 = rec[h + k][1];
+                        const float4 p2 = rh[k][1];
                         const float wgt = alpha * T;
                         c0 = c0 + p2.x * wgt;
                         c1 = c1 + p2.y * wgt;
                         c2 = c2 + p2.z * wgt;
                         d = d + p2.w * alpha * T;
                         T = test;
-                        cm |= 1u << k;
+                        cm |= bit;
                     }
                 }
+                if (act) done = true;
                 n_contrib += __popc(cm);
                 tmask |= __reduce_or_sync(0xffffffffu, cm) << h;
             }
