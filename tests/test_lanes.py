@@ -95,12 +95,15 @@ def test_cut_capacity_growth(monkeypatch):
     w, hh = cfg.width, cfg.height
     L = N.lib()
     ref = hs.Renderer(0)
-    monkeypatch.setenv("HS_CUT_CAP_INIT", "1000")
-    small = hs.Renderer(0)
+    small = None
     try:
-        dr, ds = ref.upload(h, validate=False), small.upload(h, validate=False)
+        dr = ref.upload(h, validate=False)
         hs._check(L.hs_render_hierarchy(ref.ctx, dr.handle, cams[0], cfg.tau, ref._cut, ref._frame, None), ref.ctx)
         a = _images(L, ref, ref._frame, w, hh)
+        # frame objects size their per-splat buffers at their first render
+        monkeypatch.setenv("HS_CUT_CAP_INIT", "1000")
+        small = hs.Renderer(0)
+        ds = small.upload(h, validate=False)
         hs._check(L.hs_render_hierarchy(small.ctx, ds.handle, cams[0], cfg.tau, small._cut, small._frame, None),
                   small.ctx)
         b = _images(L, small, small._frame, w, hh)
@@ -114,5 +117,6 @@ def test_cut_capacity_growth(monkeypatch):
         L.hs_frame_destroy(fr)
         L.hs_cut_destroy(cu)
     finally:
-        small.close()
+        if small is not None:
+            small.close()
         ref.close()
