@@ -1182,6 +1182,9 @@ hs_status hs_render_splats(hs_context* ctx, const hs_splat_soa* sp, uint64_t n, 
     const CamParams cp = make_cam(cam);
     s = ensure_frame(ctx, f, std::max<uint64_t>(n, 1), cp);
     if (s != HS_OK) return s;
+    // the splat records and count go in on the context stream: after this frame's
+    // previous render, which may still be running on its lane (async mode)
+    if (f->pending) HS_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, f->done, 0));
     HS_CUDA(ctx, f->splat_attr.ensure(std::max<uint64_t>(n, 1) * 256));
     HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     if (n) {
