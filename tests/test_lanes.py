@@ -120,3 +120,56 @@ def test_cut_capacity_growth(monkeypatch):
         if small is not None:
             small.close()
         ref.close()
+
+
+def test_lanes_random_schedule():
+    """Random mix of render_hierarchy / render_cut calls over shared cut objects and
+    frame objects bound to three lanes, all asynchronous: every frame object's final
+    image equals a frame-after-frame replay of its last call."""
+    cfg = scenes.CONFIGS["c1"]
+    h = scenes.hierarchy(cfg)
+    cams = [c.to_c() for c in scenes.trajectory(cfg, 6)]
+    w, hh = cfg.width, cfg.height
+    L = N.lib()
+    rng = np.random.default_rng(7)
+    r = hs.Renderer(0)
+    ref = hs.Renderer(0)
+    try:
+        dh = r.upload(h, validate=False)
+        dref = ref.upload(h, validate=False)
+        r.set_lanes(3)
+        frames = [_new(L, r, "frame") for _ in range(3)]
+        cuts = [_new(L, r, "cut") for _ in range(2)]
+        for f in frames:  # bind lanes, size buffers
+            hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, cams[0], cfg.tau, cuts[0], f, None), r.ctx)
+        cut_cam = [0, None]  # camera each cut object was selected for
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, cams[1], cfg.tau, cuts[1], frames[0], None), r.ctx)
+        cut_cam[1] = 1
+        last = {}  # frame index -> (cut camera, render camera)
+        r.set_async(True)
+        for _ in range(24):
+            fi, ci, cam = int(rng.integers(3)), int(rng.integers(2)), int(rng.integers(len(cams)))
+            if rng.random() < 0.5:
+                hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, cams[cam], cfg.tau, cuts[ci], frames[fi], None),
+                          r.ctx)
+                cut_cam[ci] = cam
+                last[fi] = (cam, cam)
+            else:
+                hs._check(L.hs_render_cut(r.ctx, dh.handle, cuts[ci], cams[cam], frames[fi], None), r.ctx)
+                last[fi] = (cut_cam[ci], cam)
+        r.set_async(False)
+        for fi, (cc, rc) in last.items():
+            got = _images(L, r, frames[fi], w, hh)
+            hs._check(L.hs_render_hierarchy(ref.ctx, dref.handle, cams[cc], cfg.tau, ref._cut, ref._frame, None),
+                      ref.ctx)
+            if rc != cc:
+                hs._check(L.hs_render_cut(ref.ctx, dref.handle, ref._cut, cams[rc], ref._frame, None), ref.ctx)
+            want = _images(L, ref, ref._frame, w, hh)
+            assert np.array_equal(got[0], want[0]) and got[1] == want[1], (fi, cc, rc)
+        for p in frames:
+            L.hs_frame_destroy(p)
+        for p in cuts:
+            L.hs_cut_destroy(p)
+    finally:
+        r.close()
+        ref.close()
