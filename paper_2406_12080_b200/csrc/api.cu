@@ -653,14 +653,16 @@ const char* hs_last_error(const hs_context* ctx) { return ctx ? ctx->err.c_str()
 void* hs_context_stream(hs_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 hs_status hs_context_synchronize(hs_context* ctx) {
-    for (int l = 0; l < ctx->n_lanes; ++l) HS_CUDA(ctx, cudaStreamSynchronize(ctx->lanes[l]));
+    for (int l = 0; l < kMaxLanes; ++l)  // every lane ever created (frames stay bound to theirs)
+        if (ctx->lanes[l]) HS_CUDA(ctx, cudaStreamSynchronize(ctx->lanes[l]));
     HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return HS_OK;
 }
 
 hs_status hs_context_join(hs_context* ctx) {
     if (!ctx) return HS_INVALID_ARGUMENT;
-    for (int l = 1; l < ctx->n_lanes; ++l) {
+    for (int l = 1; l < kMaxLanes; ++l) {
+        if (!ctx->lanes[l]) continue;
         HS_CUDA(ctx, cudaEventRecord(ctx->join_ev[l], ctx->lanes[l]));
         HS_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join_ev[l], 0));
     }
