@@ -258,6 +258,15 @@ hs_status hs_frame_download(hs_context* ctx, hs_frame* f, float* color, float* d
  * hs_frame_download_wait returns when the bytes have landed. */
 hs_status hs_frame_download_async(hs_context* ctx, hs_frame* f, float* color, float* depth, float* transmittance);
 hs_status hs_frame_download_wait(hs_context* ctx, hs_frame* f, int32_t* rendered_count);
+
+/* Device-to-device read-back of the frame's planes into caller-owned DEVICE
+ * buffers (e.g. tensors handed to NCCL for the multi-GPU image gather),
+ * enqueued on the caller's CUDA `stream` (cudaStream_t; NULL = the context
+ * stream) after the frame's kernels.  Stream-ordered, returns without waiting;
+ * a later render into the same frame object waits for the copy on the device.
+ * Any pointer may be NULL. */
+hs_status hs_frame_download_device(hs_context* ctx, hs_frame* f, float* color, float* depth, float* transmittance,
+                                   void* stream);
 /* kernels this library has launched so far (process-wide; for launch accounting) */
 uint64_t hs_kernel_launch_count(void);
 hs_status hs_host_alloc(size_t bytes, void** out); /* pinned host memory */

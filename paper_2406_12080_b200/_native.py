@@ -107,6 +107,7 @@ _SIGS = {
     "hs_frame_download": (C.c_int, [_vp, _vp, f32p, f32p, f32p, i32p]),
     "hs_frame_download_async": (C.c_int, [_vp, _vp, f32p, f32p, f32p]),
     "hs_frame_download_wait": (C.c_int, [_vp, _vp, i32p]),
+    "hs_frame_download_device": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "hs_kernel_launch_count": (C.c_uint64, []),
     "hs_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
     "hs_host_free": (None, [_vp]),

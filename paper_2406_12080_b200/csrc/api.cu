@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "hs_device.cuh"
@@ -97,7 +98,15 @@ struct hs_context {
     int n_lanes = 1, next_lane = 0;
     cudaStream_t lanes[kMaxLanes] = {};
     cudaEvent_t fork_ev = nullptr, join_ev[kMaxLanes] = {};
+    // cuts alive in this context (a frame rendered from a cut checks, before its
+    // backward pass, that the cut still exists and still holds the same selection)
+    std::unordered_set<const hs_cut*> live_cuts;
 };
+
+namespace {
+// Generation of cut contents: every write of a cut takes a fresh value.
+std::atomic<unsigned long long> g_cut_generation{0};
+}  // namespace
 
 struct hs_hierarchy {
     hs_context* ctx = nullptr;
@@ -118,6 +127,7 @@ struct hs_cut {
     // cross-lane hazards: the last write or read of this cut, and its stream
     mutable cudaEvent_t last = nullptr;
     mutable cudaStream_t last_stream = nullptr;
+    unsigned long long gen = 0;  // g_cut_generation at the last write
     ~hs_cut() {
         if (h_count) cudaFreeHost(h_count);
         if (done) cudaEventDestroy(done);
@@ -154,6 +164,8 @@ struct hs_frame {
     cudaEvent_t done = nullptr;
     cudaEvent_t copy_done = nullptr;  // last async read-back of this frame's images
     bool copy_pending = false;
+    cudaEvent_t dcopy_done = nullptr;  // last device-to-device read-back (hs_frame_download_device)
+    bool dcopy_pending = false;
     bool pending = false, timed = false, have_result = false;
     hs_stage_times* times = nullptr;
     bool cut_timed = false;
@@ -163,6 +175,7 @@ struct hs_frame {
     uint64_t n_full = 0;           // the cut's own capacity (all nodes)
     cudaStream_t s = nullptr;      // the lane's stream
     const hs_cut* src_cut = nullptr;  // cut read by the last raster call (hazard tracking)
+    unsigned long long src_gen = 0;   // its generation at that call (render_backward checks it)
     // last raster call (for an overflow re-run)
     bool from_cut = false;
     const float4* attr = nullptr;
@@ -179,6 +192,7 @@ struct hs_frame {
             if (e) cudaEventDestroy(e);
         if (done) cudaEventDestroy(done);
         if (copy_done) cudaEventDestroy(copy_done);
+        if (dcopy_done) cudaEventDestroy(dcopy_done);
         delete own_cut;
     }
 };
@@ -388,6 +402,7 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     unsigned char* sc = f->scratch.as<unsigned char>();
     // the images of this frame object may still be streaming to the host
     if (f->copy_pending) HS_CUDA(ctx, cudaStreamWaitEvent(s, f->copy_done, 0));
+    if (f->dcopy_pending) HS_CUDA(ctx, cudaStreamWaitEvent(s, f->dcopy_done, 0));
     HS_CUDA(ctx, cudaMemsetAsync(sc, 0, L.zero_bytes, s));
     HS_CUDA(ctx, cudaMemsetAsync(&ds->n_visible, 0, offsetof(DevStats, overflows) - 8, s));
     HS_CUDA(ctx, cudaMemsetAsync(f->ranges.p, 0, (size_t)cp.tiles_x * cp.tiles_y * 8, s));
@@ -452,12 +467,18 @@ hs_status finish_frame(hs_context* ctx, hs_frame* f, bool allow_retry) {
         f->pending = false;
         const DevStats st = *f->h_stats;
         if (st.overflows > 0 && !allow_retry) {
+            f->have_result = false;  // the buffers hold a partial frame, not the previous result
             HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, frame_stream(ctx, f)));
             return set_err(ctx, HS_CAPACITY_EXCEEDED,
                            std::to_string(st.overflows) +
                                " async frame(s) overflowed the frame buffers; render once synchronously to grow them");
         }
         if (st.n_splats_req > 0) {  // a cut larger than the per-splat buffers (sync call: grow, re-run)
+            f->have_result = false;
+            if (!allow_retry)
+                return set_err(ctx, HS_CAPACITY_EXCEEDED,
+                               "cut of " + std::to_string(st.n_splats_req) +
+                                   " splats exceeds the frame buffers; render once synchronously to grow them");
             HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, frame_stream(ctx, f)));
             f->cut_cap = std::min<uint64_t>(f->n_full, st.n_splats_req + st.n_splats_req / 4 + 1024);
             f->n_max = f->cut_cap;
@@ -469,6 +490,7 @@ hs_status finish_frame(hs_context* ctx, hs_frame* f, bool allow_retry) {
         }
         if (st.n_dup > 0 && st.sort_n == 0) {
             HS_CUDA(ctx, cudaMemsetAsync(&f->stats.as<DevStats>()->overflows, 0, 8, frame_stream(ctx, f)));
+            f->have_result = false;
             if (!allow_retry)
                 return set_err(ctx, HS_CAPACITY_EXCEEDED,
                                "duplicate buffer too small (" + std::to_string(st.n_dup) + " > " +
@@ -498,6 +520,7 @@ hs_status finish_frame(hs_context* ctx, hs_frame* f, bool allow_retry) {
         }
         return HS_OK;
     }
+    f->have_result = false;
     return set_err(ctx, HS_CAPACITY_EXCEEDED, "duplicate buffer kept overflowing");
 }
 
@@ -535,6 +558,7 @@ hs_status enqueue_cut(hs_context* ctx, const hs_hierarchy* h, const hs_camera* c
     HS_CUDA(ctx, cudaEventRecord(cut->done, s));
     HS_TRY(mark_cut(ctx, cut, s));
     cut->h = h;
+    cut->gen = ++g_cut_generation;
     return HS_OK;
 }
 
@@ -975,12 +999,14 @@ hs_status hs_cut_create(hs_context* ctx, hs_cut** out) {
     if (!ctx || !out) return HS_INVALID_ARGUMENT;
     auto* c = new hs_cut();
     c->ctx = ctx;
+    ctx->live_cuts.insert(c);
     *out = c;
     return HS_OK;
 }
 void hs_cut_destroy(hs_cut* cut) {
     if (!cut) return;
-    cudaStreamSynchronize(cut->ctx->stream);
+    hs_context_synchronize(cut->ctx);
+    cut->ctx->live_cuts.erase(cut);
     delete cut;
 }
 
@@ -1018,6 +1044,7 @@ hs_status hs_cut_upload(hs_context* ctx, const hs_hierarchy* h, const uint32_t* 
         if (node[i] >= h->n) return set_err(ctx, HS_INVALID_ARGUMENT, "cut node index out of range");
     hs_status s = ensure_cut(ctx, cut, std::max<uint64_t>(n, 1));
     if (s != HS_OK) return s;
+    HS_TRY(acquire_cut(ctx, cut, ctx->stream));  // a lane may still be reading the old entries
     HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     if (n) {
         HS_TRY(copy_sync(ctx, cut->node.p, node, n * 4, cudaMemcpyHostToDevice));
@@ -1030,7 +1057,9 @@ hs_status hs_cut_upload(hs_context* ctx, const hs_hierarchy* h, const uint32_t* 
     *cut->h_count = n;
     HS_TRY(copy_sync(ctx, cut->count.p, &n, 8, cudaMemcpyHostToDevice));
     HS_CUDA(ctx, cudaEventRecord(cut->done, ctx->stream));
+    HS_TRY(mark_cut(ctx, cut, ctx->stream));
     cut->h = h;
+    cut->gen = ++g_cut_generation;
     return HS_OK;
 }
 
@@ -1070,11 +1099,13 @@ hs_status hs_transfer_count(hs_context* ctx, hs_transfer_tracker* t, const hs_cu
     // epoch 0 = never in a cut; the first refresh compares against an id no node carries
     const uint32_t prev = t->refresh == 0 ? 0xFFFFFFFFu : t->refresh;
     const uint32_t cur = t->refresh + 1;
+    HS_TRY(acquire_cut(ctx, cut, ctx->stream));  // selected on a lane, possibly still running
     HS_CUDA(ctx, cudaMemsetAsync(t->count.p, 0, 8, ctx->stream));
     hs::launch_transfer_count(cut->node.as<uint32_t>(), cut->count.as<uint64_t>(), cut->cap, t->epoch.as<uint32_t>(),
                               prev, cur, t->count.as<unsigned long long>(), ctx->stream);
     HS_CUDA(ctx, cudaGetLastError());
     hs::launch_copy_words(t->count.p, t->h_count_dev, 8, ctx->stream);
+    HS_TRY(mark_cut(ctx, cut, ctx->stream));
     HS_CUDA(ctx, cudaEventRecord(t->done, ctx->stream));
     t->refresh = cur;
     HS_CUDA(ctx, cudaEventSynchronize(t->done));
@@ -1094,6 +1125,7 @@ void hs_frame_destroy(hs_frame* f) {
     if (!f) return;
     cudaStreamSynchronize(f->ctx->stream);
     if (f->s) cudaStreamSynchronize(f->s);
+    if (f->own_cut) f->ctx->live_cuts.erase(f->own_cut);
     delete f;
 }
 
@@ -1120,6 +1152,7 @@ static hs_status render_from_cut(hs_context* ctx, const hs_hierarchy* h, const h
     f->timed = times != nullptr;
     f->cut_timed = cut_timed;
     f->src_cut = cut;
+    f->src_gen = cut->gen;
     HS_TRY(acquire_cut(ctx, cut, frame_stream(ctx, f)));
     s = enqueue_raster(ctx, f);
     if (s != HS_OK) return s;
@@ -1138,14 +1171,15 @@ hs_status hs_render_hierarchy(hs_context* ctx, const hs_hierarchy* h, const hs_c
         if (!f->own_cut) {
             f->own_cut = new hs_cut();
             f->own_cut->ctx = ctx;
+            ctx->live_cuts.insert(f->own_cut);
         }
         cut = f->own_cut;
     }
     hs_status s = fork_lane(ctx, f);
     if (s != HS_OK) return s;
     if (times) {
-        s = ensure_frame(ctx, f, std::max<uint64_t>(h->n, 1), make_cam(cam));
-        if (s != HS_OK) return s;
+        for (auto& e : f->ev)
+            if (!e) HS_CUDA(ctx, cudaEventCreate(&e));
         HS_CUDA(ctx, cudaEventRecord(f->ev[0], frame_stream(ctx, f)));
     }
     s = enqueue_cut(ctx, h, cam, tau, cut, frame_stream(ctx, f));
@@ -1238,6 +1272,13 @@ hs_status hs_render_backward(hs_context* ctx, hs_frame* f, const float* loss_gra
     const uint64_t n = f->h_stats->n_splats, d = f->h_stats->sort_n;
     const float4* attr = f->attr;
     if (f->from_cut) {
+        // the frame's splats are re-assembled from its cut: it must still hold the selection rendered
+        if (!f->src_cut || !ctx->live_cuts.count(f->src_cut) || f->src_cut->gen != f->src_gen)
+            return set_err(ctx, HS_MISSING_FORWARD_STATE,
+                           "the cut this frame was rendered from has been reselected or destroyed since");
+        HS_TRY(acquire_cut(ctx, f->src_cut, ctx->stream));
+    }
+    if (f->from_cut) {
         // a hierarchy frame: its context's splats are the cut's interpolated RenderSplats
         // (render_hierarchy keeps cut_render_splats, render.hpp:706-720)
         const size_t sw = std::max<uint64_t>(n, 1);
@@ -1250,6 +1291,7 @@ hs_status hs_render_backward(hs_context* ctx, hs_frame* f, const float* loss_gra
         hs::launch_assemble(f->attr, f->cut_node, f->cut_t, f->n_ptr, n, mean, scale, rot, sh, fall, pfall, t, k,
                             ctx->stream);
         hs::launch_pack_splats(mean, scale, rot, sh, fall, pfall, t, k, f->n_ptr, n, rec, ctx->stream);
+        HS_TRY(mark_cut(ctx, f->src_cut, ctx->stream));
         attr = rec;
     }
     const size_t plane = (size_t)f->W * f->H;
@@ -1393,9 +1435,11 @@ extern "C" hs_status hs_cut_render_splats(hs_context* ctx, const hs_hierarchy* h
     float *mean = base, *scale = mean + 3 * n, *rot = scale + 3 * n, *sh = rot + 4 * n, *fall = sh + 48 * n,
           *pfall = fall + n, *t = pfall + n;
     int* k = reinterpret_cast<int*>(t + n);
+    HS_TRY(acquire_cut(ctx, cut, ctx->stream));
     hs::launch_assemble(h->attr.as<float4>(), cut->node.as<uint32_t>(), cut->t.as<float>(), cut->count.as<uint64_t>(),
                         n, mean, scale, rot, sh, fall, pfall, t, k, ctx->stream);
     HS_CUDA(ctx, cudaGetLastError());
+    HS_TRY(mark_cut(ctx, cut, ctx->stream));
     HS_TRY(copy_sync(ctx, out->mean, mean, n * 12, cudaMemcpyDeviceToHost));
     HS_TRY(copy_sync(ctx, out->scale, scale, n * 12, cudaMemcpyDeviceToHost));
     HS_TRY(copy_sync(ctx, out->rot_wxyz, rot, n * 16, cudaMemcpyDeviceToHost));
@@ -1429,14 +1473,30 @@ extern "C" hs_status hs_frame_download_async(hs_context* ctx, hs_frame* f, float
     return HS_OK;
 }
 
+extern "C" hs_status hs_frame_download_device(hs_context* ctx, hs_frame* f, float* color, float* depth,
+                                              float* trans, void* stream) {
+    if (!ctx || !f) return HS_INVALID_ARGUMENT;
+    if (!f->pending && !f->have_result) return set_err(ctx, HS_MISSING_FORWARD_STATE, "frame has not been rendered");
+    if (!f->dcopy_done) HS_CUDA(ctx, cudaEventCreateWithFlags(&f->dcopy_done, cudaEventDisableTiming));
+    cudaStream_t cs = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    HS_CUDA(ctx, cudaStreamWaitEvent(cs, f->done, 0));
+    const size_t plane = (size_t)f->W * f->H;
+    if (color) HS_CUDA(ctx, cudaMemcpyAsync(color, f->color.p, plane * 12, cudaMemcpyDeviceToDevice, cs));
+    if (depth) HS_CUDA(ctx, cudaMemcpyAsync(depth, f->depth.p, plane * 4, cudaMemcpyDeviceToDevice, cs));
+    if (trans) HS_CUDA(ctx, cudaMemcpyAsync(trans, f->trans.p, plane * 4, cudaMemcpyDeviceToDevice, cs));
+    HS_CUDA(ctx, cudaEventRecord(f->dcopy_done, cs));
+    f->dcopy_pending = true;
+    return HS_OK;
+}
+
 extern "C" hs_status hs_frame_download_wait(hs_context* ctx, hs_frame* f, int32_t* rendered_count) {
     if (!ctx || !f) return HS_INVALID_ARGUMENT;
     if (!f->copy_pending) return set_err(ctx, HS_MISSING_FORWARD_STATE, "no read-back in flight");
     HS_CUDA(ctx, cudaEventSynchronize(f->copy_done));
     f->copy_pending = false;
     const DevStats st = *f->h_stats_dl;
-    if (st.n_dup > 0 && st.sort_n == 0)
-        return set_err(ctx, HS_CAPACITY_EXCEEDED, "the frame overflowed the duplicate buffer; render it synchronously");
+    if ((st.n_dup > 0 && st.sort_n == 0) || st.n_splats_req > 0 || st.overflows > 0)
+        return set_err(ctx, HS_CAPACITY_EXCEEDED, "the frame overflowed its buffers; render it synchronously");
     if (rendered_count) *rendered_count = (int32_t)st.rendered;
     return HS_OK;
 }

@@ -116,8 +116,8 @@ __global__ void __launch_bounds__(256) k_assemble(const float4* __restrict__ att
                                                   float* __restrict__ o_mean, float* __restrict__ o_scale,
                                                   float* __restrict__ o_rot, float* __restrict__ o_sh,
                                                   float* __restrict__ o_fall, float* __restrict__ o_pfall,
-                                                  float* __restrict__ o_t, int* __restrict__ o_k) {
-    const uint64_t n = *n_ptr;
+                                                  float* __restrict__ o_t, int* __restrict__ o_k, uint64_t n_max) {
+    const uint64_t n = min(*n_ptr, n_max);  // the caller's buffers hold n_max entries
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
         SplatIn s;
         load_splat<true>(attr, cut_node, cut_t, j, s);
@@ -465,7 +465,7 @@ void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* 
                      uint64_t n_max, float* mean, float* scale, float* rot, float* sh, float* fall, float* pfall,
                      float* t, int* k, cudaStream_t s) {
     k_assemble<<<grid_for(n_max, 8), 256, 0, s>>>(attr, cut_node, cut_t, n_ptr, mean, scale, rot, sh, fall, pfall, t,
-                                                   k);
+                                                   k, n_max);
     note_launch();
 }
 

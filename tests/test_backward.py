@@ -247,3 +247,21 @@ def test_gpu_backward_errors_and_empty(renderer):
         renderer.render_backward(np.ones((3, 10, 10), np.float32))  # DimensionMismatch
     with pytest.raises(hs.Error):
         renderer.render_backward(np.ones((3, 24, 32), np.float32), np.ones((5, 5), np.float32))
+
+
+@pytest.mark.gpu
+def test_gpu_backward_rejects_reselected_cut(renderer):
+    """A hierarchy frame's backward re-assembles the splats from its cut: once the cut
+    object holds another selection (select_cut on the same renderer), the frame's
+    forward state is gone and backward reports MissingForwardState instead of
+    differentiating the wrong cut."""
+    from paper_2406_12080_b200 import scenes
+    cfg = scenes.CONFIGS["c1"]
+    h = scenes.hierarchy(cfg)
+    lg = np.ones((3, cfg.height, cfg.width), np.float32)
+    renderer.render_hierarchy(h, scenes.camera(cfg, 10), cfg.tau)
+    renderer.render_backward(lg)  # fine: the cut is the one rendered
+    renderer.select_cut(h, scenes.camera(cfg, 400), 0.5 * cfg.tau)  # a larger, different cut
+    with pytest.raises(hs.Error) as e:
+        renderer.render_backward(lg)
+    assert e.value.code == hs.Errc.MissingForwardState
