@@ -46,6 +46,19 @@ STAGE_KERNELS = {"cut": ("k_select_cut",), "preprocess": ("k_preprocess<1>",),
                                     "k_reach_masks", "k_sort_hist_direct")}
 
 
+def pipe_peaks():
+    """FP32 / FP32x2 / FP64 / MUFU throughput measured on this GPU by tools/peaks (built by
+    __graft_entry__.build()); the blend's roofline denominators."""
+    exe = os.path.join(ROOT, "tools", "peaks")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=60).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception:
+        return None
+
+
 def ncu_traffic():
     """Per-launch DRAM bytes per kernel from the newest committed ncu --set full capture
     (profiles/r*_traffic_v*.json, written by tools/ncu_traffic.py)."""
@@ -153,16 +166,25 @@ def run_reference(args, cfg):
 def cpu_baseline(cfg, h, frames: int = 2):
     from oracle import oracle as orc
     from paper_2406_12080_b200 import scenes
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from cpu_baseline import STAGES, host_info
 
     oh = orc.OracleHierarchy(h)
     cams = scenes.trajectory(cfg, frames, first=100)
+    stages = dict.fromkeys(STAGES, 0.0)
     t0 = time.perf_counter()
     for cam in cams:
-        orc.render_hierarchy(oh, cam, cfg.tau, keep_ctx=False)
+        f = orc.render_hierarchy(oh, cam, cfg.tau, keep_ctx=False)
+        for k, v in f.times().items():
+            stages[k] += v / frames
     el = time.perf_counter() - t0
+    info = host_info(orc)
+    full = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_cpu_baseline.json"))
     return {"value": frames / el, "unit": UNIT, "cores": orc.thread_count(), "kind": "port",
             "sample": f"{frames} frames (100..{99 + frames}) of the {cfg.name} trajectory, oracle "
-                      f"render_hierarchy incl. select_cut + cut_render_splats + render_forward"}
+                      f"render_hierarchy incl. select_cut + cut_render_splats + render_forward",
+            "stages_s": stages, "cpu_model": info["cpu_model"], "nproc": info["nproc"], "build": info["build"],
+            "full_plan": ("profiles/" + full[-1]) if full else None}
 
 
 def main():
@@ -175,6 +197,8 @@ def main():
     ap.add_argument("--mode", default="exact", choices=["exact", "fast"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tau-sweep", action="store_true")
+    ap.add_argument("--no-inscene", action="store_true")
+    ap.add_argument("--no-replay", action="store_true")
     ap.add_argument("--reference-budget-s", type=float, default=120.0)
     ap.add_argument("--lanes", type=int, default=2,
                     help="frame lanes (streams): consecutive frames on different lanes overlap on the device")
@@ -217,7 +241,7 @@ def main():
         # 16 chunks + skybox generated one at a time and consolidated on the device
         # (the 58 GB hierarchy never exists on the host)
         h = None
-        dh = scenes.multichunk(r, cfg.leaves)
+        dh = scenes.multichunk(r, cfg.leaves, sky=cfg.sky)
         gen_s, upload_s = time.perf_counter() - t0, 0.0
     else:
         # every rank builds its replica; split the host cores between the ranks
@@ -358,7 +382,72 @@ def main():
                                    "cut_entries": int(fi.n_splats), "duplicates": int(fi.n_duplicates)}
         r.set_async(False)
 
-    # ---- stage breakdown + roofline inputs: the same frames, per-stage CUDA events
+    # ---- second C2 workload: SURVEY §8d's in-scene trajectory (6 m high, through the city)
+    inscene = None
+    if not args.no_inscene and not cfg.name.startswith("c5"):
+        icams = [c.to_c() for c in scenes.trajectory_inscene(cfg, min(len(timed), 40) + 2, first=first)]
+        for k in range(NL):  # synchronous: grows the duplicate buffers (screen-covering splats)
+            render(icams[0], cfg.tau, k)
+            render(icams[1], cfg.tau, k)
+        r.set_async(True)
+        barrier()
+        r.synchronize()
+        e6, e7 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e6.record(stream)
+        for i, c in enumerate(icams[2:]):
+            render(c, cfg.tau, i % NL)
+        r.join()
+        e7.record(stream)
+        e7.synchronize()
+        r.synchronize()
+        wait_lanes()
+        r.set_async(False)
+        fi = N.hs_frame_info()
+        hs._check(L.hs_frame_get_info(r.ctx, r._frame, fi), r.ctx)
+        nfr = len(icams) - 2
+        ims = max_over_ranks(e6.elapsed_time(e7)) / nfr
+        inscene = {"frames_per_s": world * 1e3 / ims, "ms_per_frame": ims, "frames": nfr,
+                   "cut_entries": int(fi.n_splats), "visible": int(fi.n_visible), "duplicates": int(fi.n_duplicates),
+                   "rendered_count": int(fi.rendered_count),
+                   "what": "scenes.trajectory_inscene: closed loop through the city at 6 m, 20 m look-ahead, "
+                           "pitched down; splats beside the camera just in front of its image plane project to "
+                           "screen-covering ellipses under the reference's projection and saturate every pixel"}
+
+    # ---- the trajectory replay (multi.replay_trajectory, bench_path cadence) with the data plane:
+    # per-frame images to rank 0 over NCCL (device tensors, overlapped with rendering) and one
+    # all_gather of the per-frame stats; wall clock between barriers, max over ranks
+    replay = None
+    if not args.no_replay:
+        from paper_2406_12080_b200 import multi
+        per = min(len(timed), 40)
+        per += per % 2
+        rcams = scenes.trajectory(cfg, per * world, first=0)
+        src = multi.GpuFrameSource(r, dh)
+        sums = []
+
+        def on_image(i, t):  # rank 0: the image landed; keep a device-side checksum per frame
+            sums.append(t.view(torch.int32).sum(dtype=torch.int64))
+        multi.replay_trajectory(src, rcams[: 2 * world], cfg.tau, gather_images=world > 1, on_image=on_image)
+        sums.clear()
+        barrier()
+        torch.cuda.synchronize()
+        r.synchronize()
+        t0 = time.perf_counter()
+        rstats = multi.replay_trajectory(src, rcams, cfg.tau, gather_images=world > 1, on_image=on_image)
+        torch.cuda.synchronize()
+        rep_s = max_over_ranks(time.perf_counter() - t0)
+        replay = {"frames_per_s": len(rcams) / rep_s, "frames": len(rcams), "seconds": rep_s,
+                  "images_gathered_to_rank0": len(sums) if world > 1 else 0,
+                  "gather_bytes_per_frame": 20 * cfg.width * cfg.height if world > 1 else 0,
+                  "mean_rendered": float(rstats[:, 0].mean()),
+                  "what": "bench_path cadence (cut on even frames), synchronous frames, per-stage events; "
+                          "N > 1: every frame's RenderOutput sent to rank 0 (batch_isend_irecv, double-buffered) "
+                          "and the stats all_gathered"}
+        src.tracker.close()
+
+    # ---- stage breakdown + roofline inputs: the same frames, per-stage CUDA events, with the
+    # blend's work counters on (HS_OPT_STATS; the timed frames above ran without them)
+    r.set_stats(True)
     st = hs.StageTimes()
     infos = []
     for c in timed[: min(len(timed), 16)]:
@@ -368,51 +457,81 @@ def main():
         fi = N.hs_frame_info()
         hs._check(L.hs_frame_get_info(r.ctx, r._frame, fi), r.ctx)
         infos.append(fi)
+    r.set_stats(False)
     nf = len(infos)
     stage_ms = {k: 1e3 * getattr(st, k) / nf for k in ("cut_expand", "weights", "preprocess", "duplicate",
                                                       "tile_ranges", "alpha_blend")}
     mean = lambda k: sum(getattr(fi, k) for fi in infos) / nf  # noqa: E731
-    C_, V_, D_ = mean("n_splats"), mean("n_visible"), mean("n_duplicates")
-    NE, NC = mean("n_eval"), mean("n_contrib")
+    C_, V_, D_, Ct = mean("n_splats"), mean("n_visible"), mean("n_duplicates"), mean("n_transition")
+    NE, NC, NEt = mean("n_eval"), mean("n_contrib"), mean("n_eval_t")
+    NX, NP = mean("n_exp"), mean("n_pow")
     nodes = dh.n
     W, H = cfg.width, cfg.height
+    tiles = infos[0].tiles_x * infos[0].tiles_y
     pk, pk_kind = peaks()
     hbm = pk.get("hbm_gbs", 6450.9)
-    # algorithmic bytes per frame
-    passes = infos[0].sort_passes
+    # algorithmic bytes per frame: SURVEY.md §8(d) (DESIGN.md §7 restates them)
+    P = -(-(max(1, (tiles - 1).bit_length()) + 31) // 8)  # passes of one (tile | depth) 64-bit key sort
     bytes_cut = 32 * nodes + 12 * C_
-    bytes_pre = C_ * (256 + 8) + V_ * (64 + 4)
-    bytes_sort = 8 * D_ + passes * 24 * D_ + 12 * D_ + 8 * V_  # histogram read + passes + dup write + dup reads
+    bytes_pre = C_ * (8 + 236 + 4 + 64 + 4) + Ct * (236 + 4)
+    bytes_scan = 8 * C_
+    bytes_dup = V_ * (4 + 8 + 4) + 12 * D_
+    bytes_sort = 8 * D_ + P * 24 * D_
+    bytes_ranges = 8 * D_ + 8 * tiles
+
+    def gbs(b, ms):
+        return b / (ms * 1e6) if ms else None
     stages = {
         "cut": {"ms": stage_ms["cut_expand"], "bound": "hbm", "bytes": bytes_cut,
-                "gbs": bytes_cut / (stage_ms["cut_expand"] * 1e6) if stage_ms["cut_expand"] else None},
+                "gbs": gbs(bytes_cut, stage_ms["cut_expand"]), "formula": "32 N + 12 C"},
         "preprocess": {"ms": stage_ms["preprocess"], "bound": "hbm", "bytes": bytes_pre,
-                       "gbs": bytes_pre / (stage_ms["preprocess"] * 1e6) if stage_ms["preprocess"] else None},
-        "duplicate+sort": {"ms": stage_ms["duplicate"], "bound": "hbm", "bytes": bytes_sort,
-                           "gbs": bytes_sort / (stage_ms["duplicate"] * 1e6) if stage_ms["duplicate"] else None},
-        "tile_ranges": {"ms": stage_ms["tile_ranges"]},
-        "alpha_blend": {"ms": stage_ms["alpha_blend"], "bound": "fp32", "n_eval": NE, "n_contrib": NC},
+                       "gbs": gbs(bytes_pre, stage_ms["preprocess"]), "formula": "316 C + 240 C_t"},
+        "duplicate+sort": {"ms": stage_ms["duplicate"], "bound": "hbm", "bytes": bytes_scan + bytes_dup + bytes_sort,
+                           "gbs": gbs(bytes_scan + bytes_dup + bytes_sort, stage_ms["duplicate"]),
+                           "formula": f"scan 8 C + duplicate (16 V + 12 D) + sort (8 D + {P} x 24 D)"},
+        "tile_ranges": {"ms": stage_ms["tile_ranges"], "bound": "hbm", "bytes": bytes_ranges,
+                        "gbs": gbs(bytes_ranges, stage_ms["tile_ranges"]), "formula": "8 D + 8 tiles"},
+        "alpha_blend": {"ms": stage_ms["alpha_blend"], "bound": "fp32"},
     }
-    # blend roofline: FP32 ops per (pixel, entry) evaluation (power + gate: 12) and per
-    # contribution (exp/alpha/accumulate: 24), against the FP32 peak at the sampled clock
+    # blend: SURVEY.md §8(d) ops per (pixel, entry) evaluation, N_eval counted on the device as
+    # the evaluations each pixel executes up to and including its break entry (entries the reach
+    # masks skip are not counted); exact mode adds the FP64 libm replicas per live pair
     sm_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
     props = torch.cuda.get_device_properties(local)
-    fp32_peak = props.multi_processor_count * 128 * 2 * sm_mhz * 1e6 / 1e12
-    blend_flops = 12 * NE + 24 * NC
-    blend_tf = blend_flops / (stage_ms["alpha_blend"] * 1e-3) / 1e12
+    pp = pipe_peaks()
+    fp32_nominal = props.multi_processor_count * 128 * 2 * sm_mhz * 1e6 / 1e12
+    if pp:
+        fp32_peak = max(pp["fp32_tflops"], pp["fp32x2_tflops"])
+        fp32_src = f"measured (tools/peaks: FFMA {pp['fp32_tflops']:.1f}, FFMA2 {pp['fp32x2_tflops']:.1f} TFLOP/s)"
+    else:
+        fp32_peak, fp32_src = fp32_nominal, f"nominal {props.multi_processor_count} SMs x 128 x 2 x {sm_mhz:.0f} MHz"
+    blend_s = stage_ms["alpha_blend"] * 1e-3
+    fp32_ops = 20 * NE + 10 * NEt
+    exact = args.mode == "exact"
+    fp64_flops = (14 * NX + 27 * NP) if exact else 0.0   # expf / powf replicas: 6 + 9 DFMA, 2 + 9 DMUL/DADD
+    mufu_ops = 0.0 if exact else NX + 2 * NP             # ex2; lg2 + ex2
+    blend_tf = fp32_ops / blend_s / 1e12
     traffic, traffic_src = ncu_traffic()
     blend_key = "k_blend<0>" if args.mode == "exact" else "k_blend<1>"
     roofline = {"bound": "fp32", "kernel": "k_blend", "achieved": blend_tf, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": blend_tf / fp32_peak,
                 "traffic": traffic.get(blend_key, {}).get("dram_bytes"),
                 "traffic_source": traffic_src,
+                "formula": "FP32 ops = 20 N_eval + 10 N_eval,t (SURVEY.md §8d); N_eval = executed evaluations "
+                           "up to and including each pixel's break",
+                "n_eval": NE, "n_eval_t": NEt, "n_exp": NX, "n_pow": NP,
+                "fp64": {"achieved_tflops": fp64_flops / blend_s / 1e12,
+                         "peak_tflops": pp["fp64_tflops"] if pp else None,
+                         "frac": (fp64_flops / blend_s / 1e12 / pp["fp64_tflops"]) if (pp and exact) else None,
+                         "formula": "14 flops per expf replica + 27 per powf replica (FMA = 2)"} if exact else None,
+                "mufu": {"achieved_tops": mufu_ops / blend_s / 1e12,
+                         "peak_tops": pp["mufu_ex2_tops"] if pp else None} if not exact else None,
                 # what bounds it (same ncu capture): instruction issue, not DRAM or one math pipe
                 "ncu_pct_of_peak": traffic.get(blend_key, {}).get("pct_of_peak"),
                 "algorithmic_bytes": 8 * D_ + 64 * D_ + 20 * W * H,
-                "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz "
-                               f"(no measured FP32 peak in MEASURED_PEAKS.json)",
+                "peak_source": fp32_src, "pipe_peaks": pp,
                 "hbm_stages": {k: {"gbs": v.get("gbs"), "frac": (v["gbs"] / hbm) if v.get("gbs") else None,
-                                   "bytes": v.get("bytes"),
+                                   "bytes": v.get("bytes"), "formula": v.get("formula"),
                                    "traffic": sum(traffic.get(kk, {}).get("dram_bytes", 0.0)
                                                   for kk in STAGE_KERNELS.get(k, ())) or None}
                                for k, v in stages.items() if v.get("bound") == "hbm"},
@@ -481,10 +600,13 @@ def main():
             "roofline": roofline,
             "stages_ms": stage_ms,
             "stages": stages,
-            "per_frame": {"cut_entries": C_, "visible": V_, "duplicates": D_, "n_eval": NE, "n_contrib": NC},
+            "per_frame": {"cut_entries": C_, "transitioning": Ct, "visible": V_, "duplicates": D_, "n_eval": NE,
+                          "n_eval_t": NEt, "n_contrib": NC, "n_exp": NX, "n_pow": NP},
             "single_lane": single_lane,
             "reference_cadence": cadence,
             "tau_sweep": tau_sweep,
+            "inscene": inscene,
+            "replay": replay,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -132,8 +132,13 @@ typedef struct hs_frame_info {
     uint64_t n_duplicates;   /* D: (tile, splat) pairs = sorted key count */
     int32_t rendered_count;  /* RenderOutput::rendered_count (render.hpp:82) */
     int32_t sort_passes;     /* radix passes run for this frame */
-    uint64_t n_eval;         /* N_eval: (pixel, entry) pairs visited by the blend */
+    uint64_t n_eval;         /* N_eval: (pixel, entry) pairs the blend evaluated, up to and including
+                                each pixel's break entry (entries its reach masks skip excluded) */
     uint64_t n_contrib;      /* (pixel, entry) pairs that contributed */
+    uint64_t n_eval_t;       /* of n_eval, pairs on transitioning entries (t < 1) */
+    uint64_t n_exp;          /* alpha-law evaluations: expf of the power (live pairs) */
+    uint64_t n_pow;          /* split-law evaluations: powf (live transition pairs, parent alpha >= 1/255) */
+    uint64_t n_transition;   /* C_t: cut entries with a parent and t < 1 (read their parent's record) */
 } hs_frame_info;
 
 typedef struct hs_context hs_context;
@@ -158,8 +163,10 @@ enum {
     HS_OPT_ASYNC = 1,       /* 0 (default): calls block; 1: render calls only enqueue */
     HS_OPT_BLEND_MODE = 2,  /* 0: exact (glibc expf/powf replicas, bit-exact), 1: fast */
     HS_OPT_DEBUG = 3,       /* 1: keep pre-sort keys + per-splat projection dumps */
-    HS_OPT_LANES = 4        /* 1..4 frame lanes (streams); frame objects bind round-robin at
+    HS_OPT_LANES = 4,       /* 1..4 frame lanes (streams); frame objects bind round-robin at
                                their first render, so frames on different lanes overlap */
+    HS_OPT_STATS = 5        /* 1: the blend counts its work (hs_frame_info n_eval, n_eval_t,
+                               n_contrib, n_exp, n_pow; 0 when off) */
 };
 hs_status hs_context_set_option(hs_context* ctx, int option, int64_t value);
 
@@ -281,6 +288,90 @@ void hs_host_free(void* p);
  *                 packed rect, tx0, ty0 (int bits) */
 hs_status hs_frame_debug(hs_context* ctx, hs_frame* f, uint64_t* tile_start, uint64_t* sorted_keys,
                          uint32_t* sorted_vals, uint64_t* dup_keys, uint32_t* dup_vals, float* proj16);
+
+/* ------------------------------------------------------------ per-object API (device batch kernels)
+ * The reference's scalar / per-object functions, evaluated on the device over
+ * caller arrays with the frame path's own device functions (so the results are
+ * the bits the fused kernels use).  Synchronous; host arrays in and out. */
+
+/* Gaussian (model.hpp:21-48) attributes of n Gaussians */
+typedef struct hs_gaussian_soa {
+    const float* mean;     /* 3n */
+    const float* scale;    /* 3n */
+    const float* rot_wxyz; /* 4n */
+    const float* falloff;  /* n */
+    const float* sh;       /* 48n */
+} hs_gaussian_soa;
+typedef struct hs_gaussian_soa_out {
+    float* mean;
+    float* scale;
+    float* rot_wxyz;
+    float* falloff;
+    float* sh;
+} hs_gaussian_soa_out;
+
+/* ProjectedSplatT<float> (render.hpp:52-73); booleans as int32 */
+typedef struct hs_projected {
+    int32_t culled;
+    float mean2d[2];
+    float inv_depth;
+    float cam_point[3];
+    float cov2d[4]; /* after the low-pass dilation, row-major */
+    float det_pre, det_post;
+    float conic[3];
+    float alpha_scale;
+    float color[3];
+    int32_t color_clamped[3];
+    int32_t radius, tx0, tx1, ty0, ty1;
+    float falloff_eff, parent_falloff_eff;
+    int32_t falloff_pos, parent_falloff_pos;
+    float t, inv_k;
+} hs_projected;
+
+/* granularity (lod.hpp:18-26) of n boxes: bmin/bmax 3n each */
+hs_status hs_granularity(hs_context* ctx, const float* bmin, const float* bmax, uint64_t n, const hs_camera* cam,
+                         float* out);
+/* interp_weight (lod.hpp:34-37), element-wise */
+hs_status hs_interp_weight(hs_context* ctx, const float* eps_node, const float* eps_parent, uint64_t n, float tau,
+                           float* out);
+/* transition_alpha (lod.hpp:41-45), element-wise; InvalidArgument if any K < 1 */
+hs_status hs_transition_alpha(hs_context* ctx, const float* parent_alpha, const int32_t* siblings, uint64_t n,
+                              float* out);
+/* interpolated_gaussian (lod.hpp:97-110): child i blended toward parent i at t[i] */
+hs_status hs_interpolated_gaussians(hs_context* ctx, const hs_gaussian_soa* child, const hs_gaussian_soa* parent,
+                                    const float* t, const int32_t* siblings, uint64_t n, hs_gaussian_soa_out* out);
+/* assemble_cut_splats (lod.hpp:116-146) over caller attribute arrays parallel to
+ * the hierarchy's nodes (n_attrs must equal the node count: DimensionMismatch) */
+hs_status hs_assemble_cut_splats(hs_context* ctx, const hs_hierarchy* h, const hs_gaussian_soa* attrs,
+                                 uint64_t n_attrs, const uint32_t* node, const float* t, uint64_t n,
+                                 hs_splat_soa_out* out);
+/* project (render.hpp:104-176) of n splats */
+hs_status hs_project(hs_context* ctx, const hs_splat_soa* splats, uint64_t n, const hs_camera* cam,
+                     hs_projected* out);
+/* render_reference (render.hpp:360-408): projection, global stable depth sort,
+ * then every pixel walks the whole sorted list with the per-splat tile-footprint
+ * predicate (no tile lists).  Renders into the frame object (read it back with
+ * hs_frame_download); exact arithmetic only. */
+hs_status hs_render_reference(hs_context* ctx, const hs_splat_soa* splats, uint64_t n, const hs_camera* cam,
+                              hs_frame* f);
+/* ForwardContext::order (render.hpp:93): the frame's visible splats in depth
+ * order.  order == NULL: only *n is written. */
+hs_status hs_frame_order(hs_context* ctx, hs_frame* f, uint32_t* order, uint64_t* n);
+
+/* ------------------------------------------------------------ camera IO (io.hpp:410-511)
+ * Text formats of the reference: one camera per line
+ * "width height fx fy cx cy r00 r01 r02 t0 r10 r11 r12 t1 r20 r21 r22 t2"
+ * (read_cameras, io.hpp:473-480); a camera path prefixes each line with its
+ * timestamp, strictly increasing (read_camera_path, io.hpp:498-511).  Cameras
+ * are validated (validate_camera, model.hpp:84-91).  cap: capacity of the
+ * output arrays; *n receives the count (call with cap 0 to size).  msg receives
+ * the reason of a failure ("<Errc>: ..." like hsplat::Error::what()). */
+hs_status hs_read_cameras(const char* path, hs_camera* out, uint64_t cap, uint64_t* n, char* msg, size_t msg_len);
+hs_status hs_read_camera_path(const char* path, double* timestamps, hs_camera* out, uint64_t cap, uint64_t* n,
+                              char* msg, size_t msg_len);
+hs_status hs_write_cameras(const char* path, const hs_camera* cams, uint64_t n, char* msg, size_t msg_len);
+hs_status hs_write_camera_path(const char* path, const double* timestamps, const hs_camera* cams, uint64_t n,
+                               char* msg, size_t msg_len);
 
 /* ------------------------------------------------------------ host-side tools
  * Deterministic synthetic city hierarchy (build_bvh layout, build.hpp:73-149)

@@ -487,7 +487,7 @@ class Renderer:
     reference's free functions as methods; module-level wrappers use
     default_renderer()."""
 
-    def __init__(self, device: int = 0, *, exact: bool = True, debug: bool = False):
+    def __init__(self, device: int = 0, *, exact: bool = True, debug: bool = False, stats: bool = False):
         L = N.lib()
         h = C.c_void_p()
         _check(L.hs_context_create(device, C.byref(h)), what="hs_context_create (is a CUDA device visible?)")
@@ -495,6 +495,7 @@ class Renderer:
         self.device = device
         self.set_exact(exact)
         self.set_debug(debug)
+        self.set_stats(stats)
         f = C.c_void_p()
         _check(L.hs_frame_create(self.ctx, C.byref(f)), self.ctx)
         self._frame = f
@@ -525,6 +526,10 @@ class Renderer:
     def set_debug(self, debug: bool):
         self.debug = bool(debug)
         _check(N.lib().hs_context_set_option(self.ctx, N.HS_OPT_DEBUG, 1 if debug else 0), self.ctx)
+
+    def set_stats(self, on: bool):
+        """HS_OPT_STATS: the blend counts its work (info n_eval, n_eval_t, n_contrib, n_exp, n_pow)."""
+        _check(N.lib().hs_context_set_option(self.ctx, N.HS_OPT_STATS, 1 if on else 0), self.ctx)
 
     def set_async(self, on: bool):
         _check(N.lib().hs_context_set_option(self.ctx, N.HS_OPT_ASYNC, 1 if on else 0), self.ctx)
@@ -636,6 +641,91 @@ class Renderer:
         _check(N.lib().hs_cut_render_splats(self.ctx, dh.handle, self._cut, C.byref(out.soa())), self.ctx)
         return out
 
+    # per-object API (lod.hpp:18-146, render.hpp:104-176): batch kernels on the device
+    def granularity(self, bmin, bmax, cam: CameraModel) -> np.ndarray:
+        """granularity (lod.hpp:18-26) of boxes bmin/bmax (n, 3)."""
+        bmin = np.ascontiguousarray(bmin, np.float32).reshape(-1, 3)
+        bmax = np.ascontiguousarray(bmax, np.float32).reshape(-1, 3)
+        out = np.empty(len(bmin), np.float32)
+        _check(N.lib().hs_granularity(self.ctx, N.ptr(bmin, C.c_float), N.ptr(bmax, C.c_float), len(bmin),
+                                      C.byref(cam.to_c()), N.ptr(out, C.c_float)), self.ctx)
+        return out
+
+    def interp_weight(self, eps_node, eps_parent, tau: float) -> np.ndarray:
+        """interp_weight (lod.hpp:34-37), element-wise."""
+        en = np.ascontiguousarray(eps_node, np.float32).ravel()
+        ep = np.ascontiguousarray(eps_parent, np.float32).ravel()
+        out = np.empty(len(en), np.float32)
+        _check(N.lib().hs_interp_weight(self.ctx, N.ptr(en, C.c_float), N.ptr(ep, C.c_float), len(en), float(tau),
+                                        N.ptr(out, C.c_float)), self.ctx)
+        return out
+
+    def transition_alpha(self, parent_alpha, siblings) -> np.ndarray:
+        """transition_alpha (lod.hpp:41-45), element-wise; InvalidArgument if any K < 1."""
+        a = np.ascontiguousarray(parent_alpha, np.float32).ravel()
+        k = np.ascontiguousarray(np.broadcast_to(siblings, a.shape), np.int32).ravel()
+        out = np.empty(len(a), np.float32)
+        _check(N.lib().hs_transition_alpha(self.ctx, N.ptr(a, C.c_float), N.ptr(k, C.c_int32), len(a),
+                                           N.ptr(out, C.c_float)), self.ctx)
+        return out
+
+    @staticmethod
+    def _gsoa(g: dict):
+        arrs = {k: np.ascontiguousarray(g[k], np.float32) for k in ("mean", "scale", "rot_wxyz", "falloff", "sh")}
+        s = N.hs_gaussian_soa(*[N.ptr(arrs[k], C.c_float) for k in ("mean", "scale", "rot_wxyz", "falloff", "sh")])
+        return s, arrs
+
+    def interpolated_gaussian(self, child: dict, parent: dict, t, siblings) -> dict:
+        """interpolated_gaussian (lod.hpp:97-110) for arrays of Gaussians (dicts of mean (n,3),
+        scale (n,3), rot_wxyz (n,4), falloff (n,), sh (n,48))."""
+        sc, keep_c = self._gsoa(child)
+        sp, keep_p = self._gsoa(parent)
+        n = len(keep_c["falloff"])
+        tt = np.ascontiguousarray(np.broadcast_to(t, (n,)), np.float32)
+        k = np.ascontiguousarray(np.broadcast_to(siblings, (n,)), np.int32)
+        out = {"mean": np.empty((n, 3), np.float32), "scale": np.empty((n, 3), np.float32),
+               "rot_wxyz": np.empty((n, 4), np.float32), "falloff": np.empty(n, np.float32),
+               "sh": np.empty((n, 48), np.float32)}
+        so = N.hs_gaussian_soa(*[N.ptr(out[kk], C.c_float) for kk in ("mean", "scale", "rot_wxyz", "falloff", "sh")])
+        _check(N.lib().hs_interpolated_gaussians(self.ctx, C.byref(sc), C.byref(sp), N.ptr(tt, C.c_float),
+                                                 N.ptr(k, C.c_int32), n, C.byref(so)), self.ctx)
+        return out
+
+    def assemble_cut_splats(self, h, attrs: dict, cut: CutEntries) -> RenderSplats:
+        """assemble_cut_splats (lod.hpp:116-146) over caller attribute arrays parallel to the nodes."""
+        dh = self._dev(h)
+        sa, keep = self._gsoa(attrs)
+        node = np.ascontiguousarray(cut.node, np.uint32)
+        t = np.ascontiguousarray(cut.t, np.float32)
+        out = RenderSplats.empty(len(node))
+        _check(N.lib().hs_assemble_cut_splats(self.ctx, dh.handle, C.byref(sa), len(keep["falloff"]),
+                                              N.ptr(node, C.c_uint32), N.ptr(t, C.c_float), len(node),
+                                              C.byref(out.soa())), self.ctx)
+        return out
+
+    def project(self, splats: RenderSplats, cam: CameraModel) -> np.ndarray:
+        """project (render.hpp:104-176) of every splat: a structured array of ProjectedSplat fields."""
+        sp = splats.contiguous()
+        out = (N.hs_projected * max(1, len(sp)))()
+        if len(sp):
+            _check(N.lib().hs_project(self.ctx, C.byref(sp.soa()), len(sp), C.byref(cam.to_c()), out), self.ctx)
+        return np.ctypeslib.as_array(out)[: len(sp)].copy()
+
+    def render_reference(self, splats: RenderSplats, cam: CameraModel) -> RenderOutput:
+        """render_reference (render.hpp:360-408): naive per-pixel walk over the whole depth order."""
+        sp = splats.contiguous()
+        _check(N.lib().hs_render_reference(self.ctx, C.byref(sp.soa()) if len(sp) else None, len(sp),
+                                           C.byref(cam.to_c()), self._frame), self.ctx)
+        return self._output(False)
+
+    def frame_order(self) -> np.ndarray:
+        """ForwardContext::order (render.hpp:93) of the last render: visible ids in depth order."""
+        n = C.c_uint64()
+        _check(N.lib().hs_frame_order(self.ctx, self._frame, None, C.byref(n)), self.ctx)
+        o = np.empty(n.value, np.uint32)
+        _check(N.lib().hs_frame_order(self.ctx, self._frame, N.ptr(o, C.c_uint32), C.byref(n)), self.ctx)
+        return o
+
     # render
     def _output(self, want_context: bool) -> RenderOutput:
         L = N.lib()
@@ -678,7 +768,8 @@ class Renderer:
         _check(L.hs_frame_debug(self.ctx, self._frame, N.ptr(ts, C.c_uint64), N.ptr(keys, C.c_uint64),
                                 N.ptr(vals, C.c_uint32), N.ptr(dk, C.c_uint64), N.ptr(dv, C.c_uint32),
                                 N.ptr(pj, C.c_float)), self.ctx)
-        return dict(tile_start=ts, sorted_keys=keys, sorted_vals=vals, dup_keys=dk, dup_vals=dv, proj16=pj)
+        return dict(tile_start=ts, sorted_keys=keys, sorted_vals=vals, dup_keys=dk, dup_vals=dv, proj16=pj,
+                    order=self.frame_order())
 
     def render_forward(self, splats: RenderSplats, cam: CameraModel, *, want_context: bool = False,
                        stages: StageTimes | None = None) -> RenderOutput:
@@ -761,6 +852,54 @@ def select_cut(h, cam: CameraModel, tau: float) -> CutEntries:
 def cut_render_splats(h, cut: CutEntries) -> RenderSplats:
     """cut_render_splats (lod.hpp:148-153)."""
     return default_renderer().cut_render_splats(h, cut)
+
+
+def granularity(bmin, bmax, cam: CameraModel):
+    """granularity (lod.hpp:18-26) of one box (bmin, bmax 3-vectors) or of arrays of boxes."""
+    out = default_renderer().granularity(bmin, bmax, cam)
+    return float(out[0]) if np.asarray(bmin).ndim == 1 else out
+
+
+def interp_weight(eps_node, eps_parent, tau: float):
+    """interp_weight (lod.hpp:34-37)."""
+    out = default_renderer().interp_weight(eps_node, eps_parent, tau)
+    return float(out[0]) if np.ndim(eps_node) == 0 else out
+
+
+def transition_alpha(parent_alpha, siblings):
+    """transition_alpha (lod.hpp:41-45)."""
+    out = default_renderer().transition_alpha(parent_alpha, siblings)
+    return float(out[0]) if np.ndim(parent_alpha) == 0 else out
+
+
+def interpolated_gaussian(child: dict, parent: dict, t, siblings) -> dict:
+    """interpolated_gaussian (lod.hpp:97-110)."""
+    return default_renderer().interpolated_gaussian(child, parent, t, siblings)
+
+
+def assemble_cut_splats(h, attrs: dict, cut: CutEntries) -> RenderSplats:
+    """assemble_cut_splats<float> (lod.hpp:116-146)."""
+    return default_renderer().assemble_cut_splats(h, attrs, cut)
+
+
+def project(splats: RenderSplats, cam: CameraModel) -> np.ndarray:
+    """project (render.hpp:104-176)."""
+    return default_renderer().project(splats, cam)
+
+
+def render_reference(splats: RenderSplats, cam: CameraModel) -> RenderOutput:
+    """render_reference (render.hpp:360-408)."""
+    return default_renderer().render_reference(splats, cam)
+
+
+def set_thread_count(n: int) -> None:
+    """set_thread_count (parallel.hpp:18): the CPU worker count of the reference; the GPU
+    path has no host worker pool, so it changes nothing (results never depend on it)."""
+    global _thread_count
+    _thread_count = int(n)
+
+
+_thread_count = 0
 
 
 def render_forward(splats: RenderSplats, cam: CameraModel, ctx_out: dict | None = None,

@@ -46,6 +46,24 @@ class hs_grads_out(C.Structure):
                                                     "sh", "mean2d", "exposure")]
 
 
+class hs_gaussian_soa(C.Structure):
+    _fields_ = [("mean", f32p), ("scale", f32p), ("rot_wxyz", f32p), ("falloff", f32p), ("sh", f32p)]
+
+
+hs_gaussian_soa_out = hs_gaussian_soa
+
+
+class hs_projected(C.Structure):
+    """ProjectedSplatT<float> (render.hpp:52-73)."""
+    _fields_ = [("culled", C.c_int32), ("mean2d", C.c_float * 2), ("inv_depth", C.c_float),
+                ("cam_point", C.c_float * 3), ("cov2d", C.c_float * 4), ("det_pre", C.c_float),
+                ("det_post", C.c_float), ("conic", C.c_float * 3), ("alpha_scale", C.c_float),
+                ("color", C.c_float * 3), ("color_clamped", C.c_int32 * 3), ("radius", C.c_int32),
+                ("tx0", C.c_int32), ("tx1", C.c_int32), ("ty0", C.c_int32), ("ty1", C.c_int32),
+                ("falloff_eff", C.c_float), ("parent_falloff_eff", C.c_float), ("falloff_pos", C.c_int32),
+                ("parent_falloff_pos", C.c_int32), ("t", C.c_float), ("inv_k", C.c_float)]
+
+
 class hs_stage_times(C.Structure):
     _fields_ = [("cut_expand", C.c_double), ("weights", C.c_double), ("preprocess", C.c_double),
                 ("duplicate", C.c_double), ("tile_ranges", C.c_double), ("alpha_blend", C.c_double)]
@@ -55,13 +73,15 @@ class hs_frame_info(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
                 ("n_splats", C.c_uint64), ("n_visible", C.c_uint64), ("n_duplicates", C.c_uint64),
                 ("rendered_count", C.c_int32), ("sort_passes", C.c_int32), ("n_eval", C.c_uint64),
-                ("n_contrib", C.c_uint64)]
+                ("n_contrib", C.c_uint64), ("n_eval_t", C.c_uint64), ("n_exp", C.c_uint64),
+                ("n_pow", C.c_uint64), ("n_transition", C.c_uint64)]
 
 
 HS_OPT_ASYNC = 1
 HS_OPT_BLEND_MODE = 2
 HS_OPT_DEBUG = 3
 HS_OPT_LANES = 4
+HS_OPT_STATS = 5
 
 # every symbol include/hsplat_b200.h declares: name -> (restype, argtypes)
 _vp = C.c_void_p
@@ -124,6 +144,23 @@ _SIGS = {
     "hs_h3dg_read": (C.c_int, [C.c_char_p, C.POINTER(hs_node_soa), C.c_uint64]),
     "hs_h3dg_write": (C.c_int, [C.c_char_p, C.POINTER(hs_node_soa), C.c_uint64, C.c_uint32]),
     "hs_validate_hierarchy": (C.c_int, [C.POINTER(hs_node_soa), C.c_uint64, C.c_char_p, C.c_size_t]),
+    "hs_granularity": (C.c_int, [_vp, f32p, f32p, C.c_uint64, C.POINTER(hs_camera), f32p]),
+    "hs_interp_weight": (C.c_int, [_vp, f32p, f32p, C.c_uint64, C.c_float, f32p]),
+    "hs_transition_alpha": (C.c_int, [_vp, f32p, i32p, C.c_uint64, f32p]),
+    "hs_interpolated_gaussians": (C.c_int, [_vp, C.POINTER(hs_gaussian_soa), C.POINTER(hs_gaussian_soa), f32p, i32p,
+                                            C.c_uint64, C.POINTER(hs_gaussian_soa)]),
+    "hs_assemble_cut_splats": (C.c_int, [_vp, _vp, C.POINTER(hs_gaussian_soa), C.c_uint64, u32p, f32p, C.c_uint64,
+                                         C.POINTER(hs_splat_soa)]),
+    "hs_project": (C.c_int, [_vp, C.POINTER(hs_splat_soa), C.c_uint64, C.POINTER(hs_camera),
+                             C.POINTER(hs_projected)]),
+    "hs_render_reference": (C.c_int, [_vp, C.POINTER(hs_splat_soa), C.c_uint64, C.POINTER(hs_camera), _vp]),
+    "hs_frame_order": (C.c_int, [_vp, _vp, u32p, u64p]),
+    "hs_read_cameras": (C.c_int, [C.c_char_p, C.POINTER(hs_camera), C.c_uint64, u64p, C.c_char_p, C.c_size_t]),
+    "hs_read_camera_path": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(hs_camera), C.c_uint64, u64p,
+                                      C.c_char_p, C.c_size_t]),
+    "hs_write_cameras": (C.c_int, [C.c_char_p, C.POINTER(hs_camera), C.c_uint64, C.c_char_p, C.c_size_t]),
+    "hs_write_camera_path": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(hs_camera), C.c_uint64,
+                                       C.c_char_p, C.c_size_t]),
 }
 
 _lib = None

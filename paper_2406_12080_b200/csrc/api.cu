@@ -52,6 +52,10 @@ struct DevStats {
     unsigned long long rendered;   // rendered_count
     unsigned long long n_eval;     // (pixel, entry) pairs evaluated by the blend
     unsigned long long n_contrib;  // pairs that contributed
+    unsigned long long n_eval_t;   // of n_eval, pairs on transitioning entries
+    unsigned long long n_exp;      // expf evaluations (live pairs)
+    unsigned long long n_pow;      // powf evaluations (live transition pairs)
+    unsigned long long n_trans;    // C_t: cut entries with a parent and t < 1
     uint64_t n_visible_sorted;     // V from the order-preserving compaction (key count of the depth sort)
     uint64_t n_splats_req;         // C when it exceeded the frame's per-splat capacity (else 0)
     unsigned long long overflows;  // sticky: frames whose D exceeded capacity since the last wait
@@ -92,6 +96,7 @@ struct hs_context {
     bool async = false;
     int blend_mode = 0;
     bool debug = false;
+    bool stats = false;  // HS_OPT_STATS: blend work counters (n_eval, n_eval_t, n_contrib, n_exp, n_pow)
     // Frame lanes (HS_OPT_LANES): lane 0 is `stream`; a frame object is bound to
     // one lane at its first render, so frames on different lanes overlap on the
     // device.  Each render forks its lane from `stream`; hs_context_join joins back.
@@ -410,7 +415,7 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     hs::launch_preprocess(f->from_cut, f->attr, f->cut_node, f->cut_t, f->n_ptr, f->n_max, cp, f->proj.as<ProjRec>(),
                           f->dinfo.as<uint4>(), f->dupcount.as<uint32_t>(),
                           ctx->debug ? f->dbg16.as<float>() : nullptr, &ds->n_visible,
-                          f->from_cut ? &ds->n_splats : nullptr, &ds->overflows, &ds->n_splats_req, s);
+                          f->from_cut ? &ds->n_splats : nullptr, &ds->overflows, &ds->n_splats_req, &ds->n_trans, s);
     // the cut's arrays are not read past preprocess (n_splats holds its count from here)
     if (f->from_cut && f->src_cut) HS_TRY(mark_cut(ctx, f->src_cut, s));
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[2], s));
@@ -446,7 +451,7 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     hs::launch_ranges(kb[fin], &ds->sort_n, f->cap_dup, f->ranges.as<uint2>(), s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[4], s));
     hs::launch_tile_order(f->ranges.as<uint2>(), cp.tiles_x * cp.tiles_y, &ds->sort_n, f->tile_order.as<uint32_t>(), s);
-    hs::launch_blend(ctx->blend_mode, f->ranges.as<uint2>(), kb[fin], vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
+    hs::launch_blend(ctx->blend_mode, ctx->stats, f->ranges.as<uint2>(), kb[fin], vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
                      f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(),
                      &ds->n_eval, reinterpret_cast<uint32_t*>(sc + L.blend_counter), f->tile_order.as<uint32_t>(),
                      reinterpret_cast<uint32_t*>(sc + L.blend_list), s);
@@ -581,6 +586,44 @@ void pack_nodes(const hs_node_soa* s, uint64_t lo, uint64_t hi, float4* cu, floa
     }
 }
 
+// Caller splats (RenderSplat SoA) -> the device's 256-byte records (hs_device.cuh layout).
+std::vector<float4> pack_splat_records(const hs_splat_soa* sp, uint64_t n) {
+    std::vector<float4> rec(n * 16);
+    for (uint64_t i = 0; i < n; ++i) {
+        float4* a = rec.data() + 16 * i;
+        float kbits;
+        std::memcpy(&kbits, &sp->siblings[i], 4);
+        a[0] = make_float4(sp->mean[3 * i], sp->mean[3 * i + 1], sp->mean[3 * i + 2], sp->falloff[i]);
+        a[1] = make_float4(sp->scale[3 * i], sp->scale[3 * i + 1], sp->scale[3 * i + 2], sp->parent_falloff[i]);
+        a[2] = make_float4(sp->rot_wxyz[4 * i], sp->rot_wxyz[4 * i + 1], sp->rot_wxyz[4 * i + 2],
+                           sp->rot_wxyz[4 * i + 3]);
+        std::memcpy(&a[3], sp->sh + 48 * i, 48 * 4);
+        a[15] = make_float4(sp->t[i], kbits, 0.0f, 0.0f);
+    }
+    return rec;
+}
+
+// Gaussian SoA -> 256-byte records ({mean, falloff}, {scale, -}, quat, sh, -) on the host.
+std::vector<float4> pack_gaussian_records(const hs_gaussian_soa* g, uint64_t n) {
+    std::vector<float4> rec(n * 16, make_float4(0, 0, 0, 0));
+    for (uint64_t i = 0; i < n; ++i) {
+        float4* a = rec.data() + 16 * i;
+        a[0] = make_float4(g->mean[3 * i], g->mean[3 * i + 1], g->mean[3 * i + 2], g->falloff[i]);
+        a[1] = make_float4(g->scale[3 * i], g->scale[3 * i + 1], g->scale[3 * i + 2], 0.0f);
+        a[2] = make_float4(g->rot_wxyz[4 * i], g->rot_wxyz[4 * i + 1], g->rot_wxyz[4 * i + 2], g->rot_wxyz[4 * i + 3]);
+        std::memcpy(&a[3], g->sh + 48 * i, 48 * 4);
+    }
+    return rec;
+}
+
+// Synchronous host -> device upload into a fresh scratch buffer.
+template <class T>
+hs_status upload(hs_context* ctx, DBuf& b, const T* src, uint64_t count) {
+    HS_CUDA(ctx, b.ensure(std::max<uint64_t>(count, 1) * sizeof(T)));
+    if (count) HS_TRY(copy_sync(ctx, b.p, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    return HS_OK;
+}
+
 }  // namespace
 
 // Breadth-first serialisation of a forest by levels (assemble.cu); `first` is
@@ -701,6 +744,7 @@ hs_status hs_context_set_option(hs_context* ctx, int option, int64_t value) {
             ctx->blend_mode = (int)value;
             return HS_OK;
         case HS_OPT_DEBUG: ctx->debug = value != 0; return HS_OK;
+        case HS_OPT_STATS: ctx->stats = value != 0; return HS_OK;
         case HS_OPT_LANES:
             if (value < 1 || value > kMaxLanes) return set_err(ctx, HS_INVALID_ARGUMENT, "lanes is 1..4");
             for (int l = 1; l < value; ++l)
@@ -1224,18 +1268,7 @@ hs_status hs_render_splats(hs_context* ctx, const hs_splat_soa* sp, uint64_t n, 
     HS_CUDA(ctx, f->splat_attr.ensure(std::max<uint64_t>(n, 1) * 256));
     HS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     if (n) {
-        std::vector<float4> rec(n * 16);
-        for (uint64_t i = 0; i < n; ++i) {
-            float4* a = rec.data() + 16 * i;
-            float kbits;
-            std::memcpy(&kbits, &sp->siblings[i], 4);
-            a[0] = make_float4(sp->mean[3 * i], sp->mean[3 * i + 1], sp->mean[3 * i + 2], sp->falloff[i]);
-            a[1] = make_float4(sp->scale[3 * i], sp->scale[3 * i + 1], sp->scale[3 * i + 2], sp->parent_falloff[i]);
-            a[2] = make_float4(sp->rot_wxyz[4 * i], sp->rot_wxyz[4 * i + 1], sp->rot_wxyz[4 * i + 2],
-                               sp->rot_wxyz[4 * i + 3]);
-            std::memcpy(&a[3], sp->sh + 48 * i, 48 * 4);
-            a[15] = make_float4(sp->t[i], kbits, 0.0f, 0.0f);
-        }
+        const std::vector<float4> rec = pack_splat_records(sp, n);
         HS_TRY(copy_sync(ctx, f->splat_attr.p, rec.data(), n * 256, cudaMemcpyHostToDevice));
     }
     *f->h_n = n;
@@ -1354,6 +1387,10 @@ hs_status hs_frame_get_info(hs_context* ctx, hs_frame* f, hs_frame_info* info) {
     info->sort_passes = f->passes;
     info->n_eval = st.n_eval;
     info->n_contrib = st.n_contrib;
+    info->n_eval_t = st.n_eval_t;
+    info->n_exp = st.n_exp;
+    info->n_pow = st.n_pow;
+    info->n_transition = st.n_trans;
     return HS_OK;
 }
 
@@ -1512,4 +1549,166 @@ extern "C" hs_status hs_host_alloc(size_t bytes, void** out) {
 }
 extern "C" void hs_host_free(void* p) {
     if (p) cudaFreeHost(p);
+}
+
+// ------------------------------------------------------------------ per-object API (lodapi.cu kernels)
+extern "C" hs_status hs_granularity(hs_context* ctx, const float* bmin, const float* bmax, uint64_t n,
+                                    const hs_camera* cam, float* out) {
+    if (!ctx || !cam || (n && (!bmin || !bmax || !out))) return HS_INVALID_ARGUMENT;
+    if (!n) return HS_OK;
+    DBuf a, b, o;
+    HS_TRY(upload(ctx, a, bmin, 3 * n));
+    HS_TRY(upload(ctx, b, bmax, 3 * n));
+    HS_CUDA(ctx, o.ensure(n * 4));
+    hs::launch_granularity(a.as<float>(), b.as<float>(), n, make_cam(cam), o.as<float>(), ctx->stream);
+    HS_CUDA(ctx, cudaGetLastError());
+    return copy_sync(ctx, out, o.p, n * 4, cudaMemcpyDeviceToHost);
+}
+
+extern "C" hs_status hs_interp_weight(hs_context* ctx, const float* en, const float* ep, uint64_t n, float tau,
+                                      float* out) {
+    if (!ctx || (n && (!en || !ep || !out))) return HS_INVALID_ARGUMENT;
+    if (!n) return HS_OK;
+    DBuf a, b, o;
+    HS_TRY(upload(ctx, a, en, n));
+    HS_TRY(upload(ctx, b, ep, n));
+    HS_CUDA(ctx, o.ensure(n * 4));
+    hs::launch_interp_weight(a.as<float>(), b.as<float>(), n, tau, o.as<float>(), ctx->stream);
+    HS_CUDA(ctx, cudaGetLastError());
+    return copy_sync(ctx, out, o.p, n * 4, cudaMemcpyDeviceToHost);
+}
+
+extern "C" hs_status hs_transition_alpha(hs_context* ctx, const float* a, const int32_t* k, uint64_t n, float* out) {
+    if (!ctx || (n && (!a || !k || !out))) return HS_INVALID_ARGUMENT;
+    for (uint64_t i = 0; i < n; ++i)
+        if (k[i] < 1) return set_err(ctx, HS_INVALID_ARGUMENT, "transition_alpha needs K >= 1");  // lod.hpp:42
+    if (!n) return HS_OK;
+    DBuf da, dk, o;
+    HS_TRY(upload(ctx, da, a, n));
+    HS_TRY(upload(ctx, dk, k, n));
+    HS_CUDA(ctx, o.ensure(n * 4));
+    hs::launch_transition_alpha(da.as<float>(), dk.as<int32_t>(), n, o.as<float>(), ctx->stream);
+    HS_CUDA(ctx, cudaGetLastError());
+    return copy_sync(ctx, out, o.p, n * 4, cudaMemcpyDeviceToHost);
+}
+
+extern "C" hs_status hs_interpolated_gaussians(hs_context* ctx, const hs_gaussian_soa* child,
+                                               const hs_gaussian_soa* parent, const float* t, const int32_t* k,
+                                               uint64_t n, hs_gaussian_soa_out* out) {
+    if (!ctx || (n && (!child || !parent || !t || !k || !out))) return HS_INVALID_ARGUMENT;
+    for (uint64_t i = 0; i < n; ++i)
+        if (k[i] < 1) return set_err(ctx, HS_INVALID_ARGUMENT, "transition_alpha needs K >= 1");
+    if (!n) return HS_OK;
+    const std::vector<float4> rc = pack_gaussian_records(child, n), rp = pack_gaussian_records(parent, n);
+    DBuf dc, dp, dt, dk, o;
+    HS_TRY(upload(ctx, dc, rc.data(), rc.size()));
+    HS_TRY(upload(ctx, dp, rp.data(), rp.size()));
+    HS_TRY(upload(ctx, dt, t, n));
+    HS_TRY(upload(ctx, dk, k, n));
+    HS_CUDA(ctx, o.ensure(n * 256));
+    hs::launch_interpolated(dc.as<float4>(), dp.as<float4>(), dt.as<float>(), dk.as<int32_t>(), n, o.as<float4>(),
+                            ctx->stream);
+    HS_CUDA(ctx, cudaGetLastError());
+    std::vector<float4> r(n * 16);
+    HS_TRY(copy_sync(ctx, r.data(), o.p, n * 256, cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < n; ++i) {
+        const float4* a = r.data() + 16 * i;
+        if (out->mean) out->mean[3 * i] = a[0].x, out->mean[3 * i + 1] = a[0].y, out->mean[3 * i + 2] = a[0].z;
+        if (out->falloff) out->falloff[i] = a[0].w;
+        if (out->scale) out->scale[3 * i] = a[1].x, out->scale[3 * i + 1] = a[1].y, out->scale[3 * i + 2] = a[1].z;
+        if (out->rot_wxyz) std::memcpy(out->rot_wxyz + 4 * i, &a[2], 16);
+        if (out->sh) std::memcpy(out->sh + 48 * i, &a[3], 192);
+    }
+    return HS_OK;
+}
+
+extern "C" hs_status hs_assemble_cut_splats(hs_context* ctx, const hs_hierarchy* h, const hs_gaussian_soa* attrs,
+                                            uint64_t n_attrs, const uint32_t* node, const float* t, uint64_t n,
+                                            hs_splat_soa_out* out) {
+    if (!ctx || !h || !attrs || !out || (n && (!node || !t))) return HS_INVALID_ARGUMENT;
+    if (n_attrs != h->n)  // lod.hpp:120-121
+        return set_err(ctx, HS_DIMENSION_MISMATCH, "attribute array must parallel hierarchy nodes");
+    for (uint64_t i = 0; i < n; ++i)
+        if (node[i] >= h->n) return set_err(ctx, HS_INVALID_ARGUMENT, "cut node index out of range");
+    if (!n) return HS_OK;
+    DBuf m, sc, rt, fl, sh, rec, dn, dt, cnt, buf;
+    HS_TRY(upload(ctx, m, attrs->mean, 3 * n_attrs));
+    HS_TRY(upload(ctx, sc, attrs->scale, 3 * n_attrs));
+    HS_TRY(upload(ctx, rt, attrs->rot_wxyz, 4 * n_attrs));
+    HS_TRY(upload(ctx, fl, attrs->falloff, n_attrs));
+    HS_TRY(upload(ctx, sh, attrs->sh, 48 * n_attrs));
+    HS_CUDA(ctx, rec.ensure(n_attrs * 256));
+    hs::launch_pack_gaussians(m.as<float>(), sc.as<float>(), rt.as<float>(), fl.as<float>(), sh.as<float>(),
+                              h->attr.as<float4>(), n_attrs, rec.as<float4>(), ctx->stream);
+    HS_TRY(upload(ctx, dn, node, n));
+    HS_TRY(upload(ctx, dt, t, n));
+    HS_TRY(upload(ctx, cnt, &n, 1));
+    const size_t per = (3 + 3 + 4 + 48 + 1 + 1 + 1 + 1) * 4;
+    HS_CUDA(ctx, buf.ensure(n * per));
+    float* base = buf.as<float>();
+    float *mean = base, *scale = mean + 3 * n, *rot = scale + 3 * n, *shv = rot + 4 * n, *fall = shv + 48 * n,
+          *pfall = fall + n, *tt = pfall + n;
+    int* k = reinterpret_cast<int*>(tt + n);
+    hs::launch_assemble(rec.as<float4>(), dn.as<uint32_t>(), dt.as<float>(), cnt.as<uint64_t>(), n, mean, scale, rot,
+                        shv, fall, pfall, tt, k, ctx->stream);
+    HS_CUDA(ctx, cudaGetLastError());
+    HS_TRY(copy_sync(ctx, out->mean, mean, n * 12, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->scale, scale, n * 12, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->rot_wxyz, rot, n * 16, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->sh, shv, n * 192, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->falloff, fall, n * 4, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->parent_falloff, pfall, n * 4, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->t, tt, n * 4, cudaMemcpyDeviceToHost));
+    HS_TRY(copy_sync(ctx, out->siblings, k, n * 4, cudaMemcpyDeviceToHost));
+    return HS_OK;
+}
+
+extern "C" hs_status hs_project(hs_context* ctx, const hs_splat_soa* splats, uint64_t n, const hs_camera* cam,
+                                hs_projected* out) {
+    if (!ctx || !cam || (n && (!splats || !out))) return HS_INVALID_ARGUMENT;
+    if (!n) return HS_OK;
+    const std::vector<float4> rec = pack_splat_records(splats, n);
+    DBuf dr, o;
+    HS_TRY(upload(ctx, dr, rec.data(), rec.size()));
+    HS_CUDA(ctx, o.ensure(n * sizeof(hs_projected)));
+    hs::launch_project_api(dr.as<float4>(), n, make_cam(cam), o.as<hs_projected>(), ctx->stream);
+    HS_CUDA(ctx, cudaGetLastError());
+    return copy_sync(ctx, out, o.p, n * sizeof(hs_projected), cudaMemcpyDeviceToHost);
+}
+
+extern "C" hs_status hs_render_reference(hs_context* ctx, const hs_splat_soa* splats, uint64_t n,
+                                         const hs_camera* cam, hs_frame* f) {
+    if (!ctx || !cam || !f || (n && !splats)) return HS_INVALID_ARGUMENT;
+    // projection + global stable depth order: the frame path's preprocess and depth sort
+    const bool was_async = ctx->async;
+    ctx->async = false;
+    hs_status st = hs_render_splats(ctx, splats, n, cam, f, nullptr);
+    ctx->async = was_async;
+    if (st != HS_OK) return st;
+    // then the naive per-pixel walk over the whole sorted list, replacing the tiled images
+    cudaStream_t s = frame_stream(ctx, f);
+    DevStats* ds = f->stats.as<DevStats>();
+    HS_CUDA(ctx, cudaMemsetAsync(&ds->rendered, 0, 8, s));
+    hs::launch_blend_naive(f->proj.as<ProjRec>(), f->dinfo.as<uint4>(), f->zvals[0].as<uint32_t>(),
+                           &ds->n_visible_sorted, f->cam, f->color.as<float>(), f->depth.as<float>(),
+                           f->trans.as<float>(), f->touched.as<uint8_t>(), s);
+    hs::launch_count_flags(f->touched.as<uint8_t>(), std::max<uint64_t>(n, 1), &ds->rendered, s);
+    HS_CUDA(ctx, cudaGetLastError());
+    unsigned long long rendered = 0;
+    HS_CUDA(ctx, cudaMemcpyAsync(&rendered, &ds->rendered, 8, cudaMemcpyDeviceToHost, s));
+    HS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, std::max<uint64_t>(n, 1), s));  // flags stay clear between frames
+    HS_CUDA(ctx, cudaStreamSynchronize(s));
+    f->h_stats->rendered = rendered;
+    return HS_OK;
+}
+
+extern "C" hs_status hs_frame_order(hs_context* ctx, hs_frame* f, uint32_t* order, uint64_t* n) {
+    if (!ctx || !f || !n) return HS_INVALID_ARGUMENT;
+    hs_status s = finish_frame(ctx, f, false);
+    if (s != HS_OK) return s;
+    if (!f->have_result) return set_err(ctx, HS_MISSING_FORWARD_STATE, "frame has not been rendered");
+    const uint64_t v = f->h_stats->n_visible_sorted;
+    *n = v;
+    if (order && v) HS_TRY(copy_sync(ctx, order, f->zvals[0].p, v * 4, cudaMemcpyDeviceToHost));
+    return HS_OK;
 }

@@ -51,7 +51,7 @@ constexpr size_t kSmemV = sizeof(float) * kBlendWarps * 16 * 33;        // power
 constexpr size_t kSmemQ = sizeof(uint16_t) * kBlendWarps * 512;         // live-pair queue
 constexpr uint32_t kListCap = 1024;                                      // per-warp block list (global, L2)
 
-template <int kMode>
+template <int kMode, bool kStats>
 __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restrict__ ranges,
                                                             const uint32_t* __restrict__ keys,
                                                             const uint32_t* __restrict__ vals,
@@ -84,7 +84,11 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
     __syncthreads();
     const uint32_t num_tasks = (uint32_t)(cam.tiles_x * cam.tiles_y) * 8u;
     const bool any_keys = *sort_n_ptr != 0;
-    uint32_t n_eval = 0, n_contrib = 0;
+    // executed-work counters: (pixel, entry) evaluations up to and including the break
+    // (n_eval, and n_eval_t of them on transitioning entries), contributions, and the
+    // alpha-law evaluations (n_exp expf, n_pow powf: one per live pair)
+    uint32_t n_eval = 0, n_contrib = 0, n_pow = 0;
+    unsigned long long w_eval_t = 0, w_exp = 0;  // warp-uniform
     float(*sv)[33] = s_v[warp];  // [entry][lane]: power, then alpha (row padding: conflict free both ways)
     uint16_t* sq = s_q[warp];    // queue of live (lane << 4 | entry) pairs
     // stage entry `e` (if in range) of the current task into stage `st`, lane slot
@@ -170,10 +174,12 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
 #pragma unroll 1
                 for (uint32_t h = 0; h < cnt; h += 16) {
             const uint32_t hc = min(16u, cnt - h);
+            const bool active = !done;
+            // transitioning entries (t < 1) of this half, for the work counters
+            const uint32_t ttr = kStats ? __ballot_sync(0xffffffffu, lane < (int)hc && rec[h + lane][0].w < 1.0f) : 0u;
             // 2. per-pixel power and liveness (cheap, all lanes)
             uint32_t live = 0;
-            if (!done) {
-                n_eval += hc;
+            if (active) {
                 // entries in pairs, packed FP32x2 (FFMA2): each lane evaluates the
                 // reference's float expression for two entries per instruction.  Every
                 // operation is an fma with a runtime 1 / -1 / -0 operand (PairConsts):
@@ -217,6 +223,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                     if (lane >= o) incl += v;
                 }
                 const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                if (kStats) w_exp += total;
                 uint32_t pos = incl - cnt;
                 for (uint32_t m = live; m; m &= m - 1) sq[pos++] = (uint16_t)((lane << 4) | (__ffs(m) - 1));
                 __syncwarp();
@@ -225,12 +232,20 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                     const int src = (int)(pr >> 4), k = (int)(pr & 15);
                     const float power = sv[k][src];
                     const float4 p1 = rec[h + k][0];
-                    float g;
-                    if (kMode == 0)
-                        g = hs_libm::expf_glibc(power, s_et);
-                    else
-                        g = __expf(power);
                     const float tt = p1.w;
+                    float g;
+                    if (kMode == 0) {
+                        g = hs_libm::expf_glibc(power, s_et);
+                    } else {
+                        // fast: SFU ex2, except within a 1e-5 relative band of the 1/255 floor of
+                        // either law, where an approximate g could flip the gate (a jump of up to
+                        // 1/255 in alpha): there the exact replica decides, as in exact mode
+                        g = __expf(power);
+                        const float sr = p1.y * g, pr = p1.z * g;
+                        if (fabsf(sr - kAlphaMin) <= 1e-5f * kAlphaMin ||
+                            (tt < 1.0f && fabsf(pr - kAlphaMin) <= 1e-5f * kAlphaMin))
+                            g = hs_libm::expf_glibc(power, s_et);
+                    }
                     const float self_raw = p1.y * g;
                     const float self = self_raw > kAlphaMax ? kAlphaMax : self_raw;
                     const float a_self = self >= kAlphaMin ? self : 0.0f;
@@ -240,6 +255,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                         const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
                         float split = 0.0f;
                         if (par >= kAlphaMin) {
+                            if (kStats) ++n_pow;
                             const float ik = rec[h + k][2].x;
                             if (kMode == 0)
                                 split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, ik, s_lt, s_et);
@@ -259,7 +275,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
             //    lane (cm) and reduced once per half batch.
             {
                 const float4(*rh)[3] = rec + h;
-                uint32_t act = done ? 0u : live, cm = 0;
+                uint32_t act = done ? 0u : live, cm = 0, seen = active ? hc : 0u;
                 while (act) {
                     const uint32_t bit = act & (0u - act);  // lowest pending entry
                     act ^= bit;
@@ -270,6 +286,7 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                         const float test = T * (1.0f - alpha);
                         if (test < kTransmittanceEps) {
                             act |= bit;  // the pixel is done: act stays non-zero
+                            if (kStats) seen = (uint32_t)k + 1u;  // the reference visits up to the break
                             break;
                         }
                         const float4 p2 = rh[k][1];
@@ -283,7 +300,11 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                     }
                 }
                 if (act) done = true;
-                n_contrib += __popc(cm);
+                if (kStats) {
+                    n_contrib += __popc(cm);
+                    n_eval += seen;
+                    w_eval_t += __reduce_add_sync(0xffffffffu, (uint32_t)__popc(ttr & ((1u << seen) - 1u)));
+                }
                 tmask |= __reduce_or_sync(0xffffffffu, cm) << h;
             }
             __syncwarp();
@@ -305,50 +326,60 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
             trans[i] = T;
         }
     }
-    for (int o = 16; o; o >>= 1) {
-        n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
-        n_contrib += __shfl_xor_sync(0xffffffffu, n_contrib, o);
-    }
-    if (lane == 0) {
-        atomicAdd(eval_counts, (unsigned long long)n_eval);
-        atomicAdd(eval_counts + 1, (unsigned long long)n_contrib);
+    if (!kStats) return;
+    const unsigned long long w_eval = __reduce_add_sync(0xffffffffu, n_eval);
+    const unsigned long long w_contrib = __reduce_add_sync(0xffffffffu, n_contrib);
+    const unsigned long long w_pow = __reduce_add_sync(0xffffffffu, n_pow);
+    if (lane == 0) {  // DevStats: n_eval, n_contrib, n_eval_t, n_exp, n_pow
+        atomicAdd(eval_counts, w_eval);
+        atomicAdd(eval_counts + 1, w_contrib);
+        atomicAdd(eval_counts + 2, w_eval_t);
+        atomicAdd(eval_counts + 3, w_exp);
+        atomicAdd(eval_counts + 4, w_pow);
     }
 }
 
-void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
-                  const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
-                  unsigned long long* eval_counts, uint32_t* task_counter, const uint32_t* tile_order,
-                  uint32_t* lists, cudaStream_t s) {
+template <int kMode, bool kStats>
+static void launch_blend_t(const uint2* ranges, const uint32_t* keys, const uint32_t* vals, const ProjRec* proj,
+                           const uint64_t* sort_n_ptr, const CamParams& cam, float* color, float* depth, float* trans,
+                           uint8_t* touched, unsigned long long* eval_counts, uint32_t* task_counter,
+                           const uint32_t* tile_order, uint32_t* lists, const PairConsts& pc, cudaStream_t s) {
     constexpr size_t kSmem = kSmemRec + kSmemPP + kSmemV + kSmemQ;
+    static int grid = 0;
+    if (!grid) {
+        int dev = 0, sms = 148, per = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_blend<kMode, kStats>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blend<kMode, kStats>, kBlendThreads, kSmem);
+        grid = sms * std::min(8, per > 0 ? per : 1);  // blend_list_words() covers 8 per SM
+    }
+    const int tasks = cam.tiles_x * cam.tiles_y * 8;
+    const unsigned g = (unsigned)std::min<int>(grid, std::max(1, tasks / kBlendWarps));
+    k_blend<kMode, kStats><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth,
+                                                           trans, touched, eval_counts, task_counter, tile_order,
+                                                           lists, pc);
+    note_launch();
+}
+
+void launch_blend(int mode, bool stats, const uint2* ranges, const uint32_t* keys, const uint32_t* vals,
+                  const ProjRec* proj, const uint64_t* sort_n_ptr, const CamParams& cam, float* color, float* depth,
+                  float* trans, uint8_t* touched, unsigned long long* eval_counts, uint32_t* task_counter,
+                  const uint32_t* tile_order, uint32_t* lists, cudaStream_t s) {
     PairConsts pc;
     pc.nz = 0x8000000080000000ull;     // (-0, -0)
     pc.one = 0x3f8000003f800000ull;    // (1, 1)
     pc.neg1 = 0xbf800000bf800000ull;   // (-1, -1)
     pc.mhalf = 0xbf000000bf000000ull;  // (-0.5, -0.5)
-    static int grid[2] = {0, 0};
-    if (!grid[mode]) {
-        int dev = 0, sms = 148, per = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (mode == 0) {
-            cudaFuncSetAttribute(k_blend<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blend<0>, kBlendThreads, kSmem);
-        } else {
-            cudaFuncSetAttribute(k_blend<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blend<1>, kBlendThreads, kSmem);
-        }
-        grid[mode] = sms * std::min(8, per > 0 ? per : 1);  // blend_list_words() covers 8 per SM
-    }
-    const int tasks = cam.tiles_x * cam.tiles_y * 8;
-    const unsigned g = (unsigned)std::min<int>(grid[mode], std::max(1, tasks / kBlendWarps));
+#define HS_BLEND(M, S)                                                                                             \
+    launch_blend_t<M, S>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched, eval_counts,     \
+                         task_counter, tile_order, lists, pc, s)
     if (mode == 0) {
-        k_blend<0><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
-                                                   eval_counts, task_counter, tile_order, lists, pc);
+        if (stats) HS_BLEND(0, true); else HS_BLEND(0, false);
     } else {
-        k_blend<1><<<g, kBlendThreads, kSmem, s>>>(ranges, keys, vals, proj, sort_n_ptr, cam, color, depth, trans, touched,
-                                                   eval_counts, task_counter, tile_order, lists, pc);
+        if (stats) HS_BLEND(1, true); else HS_BLEND(1, false);
     }
-    note_launch();
+#undef HS_BLEND
 }
 
 // Per-warp block lists: grid (at most 8 CTAs per SM) x warps x kListCap ids.

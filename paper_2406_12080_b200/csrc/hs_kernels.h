@@ -5,6 +5,8 @@
 #include <atomic>
 #include <cstdint>
 
+struct hs_projected;
+
 namespace hs {
 
 // Process-wide count of kernels launched by this library (hs_kernel_launch_count).
@@ -84,9 +86,9 @@ void launch_backward(const float4* attr, uint64_t n, const CamParams& cam, const
 void launch_preprocess(bool from_cut, const float4* attr, const uint32_t* cut_node, const float* cut_t,
                        const uint64_t* n_ptr, uint64_t n_max, const CamParams& cam, ProjRec* proj, uint4* dinfo,
                        uint32_t* dupcount, float* dbg16, unsigned long long* n_visible, uint64_t* n_out,
-                       unsigned long long* overflows, uint64_t* n_req,
+                       unsigned long long* overflows, uint64_t* n_req, unsigned long long* n_trans,
                        cudaStream_t s);
-void launch_blend(int mode, const uint2* ranges, const uint32_t* keys, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
+void launch_blend(int mode, bool stats, const uint2* ranges, const uint32_t* keys, const uint32_t* vals, const ProjRec* proj, const uint64_t* sort_n_ptr,
                   const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
                   unsigned long long* eval_counts, uint32_t* task_counter, const uint32_t* tile_order,
                   uint32_t* lists, cudaStream_t s);
@@ -126,5 +128,20 @@ uint64_t sort_scratch_words(uint64_t n_max, int passes);
 uint64_t sort_tile_keys();
 void launch_radix_sort(uint32_t* keys[2], uint32_t* vals[2], const uint64_t* n_ptr, uint64_t n_max, int begin_bit,
                        int passes, int key_bits, uint32_t* scratch, cudaStream_t s, bool hist_ready = false);
+
+// lodapi.cu (per-object API: lod.hpp:18-146, render.hpp:104-176, 360-408)
+void launch_granularity(const float* bmin, const float* bmax, uint64_t n, const CamParams& cam, float* out,
+                        cudaStream_t s);
+void launch_interp_weight(const float* en, const float* ep, uint64_t n, float tau, float* out, cudaStream_t s);
+void launch_transition_alpha(const float* a, const int32_t* k, uint64_t n, float* out, cudaStream_t s);
+void launch_interpolated(const float4* child, const float4* parent, const float* t, const int32_t* k, uint64_t n,
+                         float4* out, cudaStream_t s);
+void launch_pack_gaussians(const float* mean, const float* scale, const float* rot, const float* fall, const float* sh,
+                           const float4* topo, uint64_t n, float4* rec, cudaStream_t s);
+void launch_project_api(const float4* rec, uint64_t n, const CamParams& cam, ::hs_projected* out, cudaStream_t s);
+void launch_blend_naive(const ProjRec* proj, const uint4* dinfo, const uint32_t* order, const uint64_t* v_ptr,
+                        const CamParams& cam, float* color, float* depth, float* trans, uint8_t* touched,
+                        cudaStream_t s);
+void launch_count_flags(const uint8_t* f, uint64_t n, unsigned long long* out, cudaStream_t s);
 
 }  // namespace hs

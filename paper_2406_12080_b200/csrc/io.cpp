@@ -7,6 +7,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <iomanip>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -28,9 +31,170 @@ struct File {
     }
 };
 
+// ---- camera text (io.hpp:410-511)
+struct CamErr {
+    hs_status s;
+    std::string what;
+};
+
+bool read_text(const std::string& path, std::string& out) {  // detail::read_file (io.hpp:37-46)
+    std::ifstream f(path, std::ios::binary);
+    if (!f.good()) return false;
+    std::ostringstream ss;
+    ss << f.rdbuf();
+    out = ss.str();
+    return true;
+}
+
+std::vector<std::string> data_lines(const std::string& text) {  // io.hpp:445-456
+    std::vector<std::string> out;
+    std::istringstream in(text);
+    std::string line;
+    while (std::getline(in, line)) {
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        const std::size_t ns = line.find_first_not_of(" \t");
+        if (ns == std::string::npos || line[ns] == '#') continue;
+        out.push_back(line);
+    }
+    return out;
+}
+
+// validate_camera (model.hpp:84-91)
+bool camera_ok(const hs_camera& c, CamErr& e) {
+    auto bad = [&](const char* m) {
+        e = {HS_INVALID_ARGUMENT, std::string("InvalidArgument: ") + m};
+        return false;
+    };
+    if (!(c.width > 0 && c.height > 0)) return bad("camera resolution must be positive");
+    if (!(c.fx > 0.0f && c.fy > 0.0f)) return bad("camera focal must be positive");
+    for (float v : c.w2c)
+        if (!std::isfinite(v)) return bad("camera pose must be finite");
+    float acc = 0.0f;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            float v = c.w2c[4 * i] * c.w2c[4 * j] + (c.w2c[4 * i + 1] * c.w2c[4 * j + 1] + c.w2c[4 * i + 2] * c.w2c[4 * j + 2]);
+            v -= (i == j) ? 1.0f : 0.0f;
+            acc += v * v;
+        }
+    if (!(std::sqrt(acc) < 1e-3f)) return bad("world_to_camera rotation block must be orthonormal");
+    return true;
+}
+
+// detail::get_camera (io.hpp:431-442): 18 numbers, nothing trailing, then validated
+bool get_camera(std::istringstream& ls, const std::string& line, hs_camera& c, CamErr& e) {
+    ls >> c.width >> c.height >> c.fx >> c.fy >> c.cx >> c.cy;
+    for (int k = 0; k < 12; ++k) ls >> c.w2c[k];
+    std::string trailing;
+    if (ls.fail() || (ls >> trailing)) {
+        e = {HS_MALFORMED_HEADER, "MalformedHeader: expected 18 numbers per camera: " + line};
+        return false;
+    }
+    return camera_ok(c, e);
+}
+
+void put_camera(std::ostream& os, const hs_camera& c) {  // io.hpp:423-429
+    os << c.width << ' ' << c.height << ' ' << c.fx << ' ' << c.fy << ' ' << c.cx << ' ' << c.cy;
+    for (int k = 0; k < 12; ++k) os << ' ' << c.w2c[k];
+    os << '\n';
+}
+
+bool write_text(const std::string& path, const std::string& bytes, CamErr& e) {  // io.hpp:48-54
+    std::ofstream f(path, std::ios::binary | std::ios::trunc);
+    if (!f.good()) {
+        e = {HS_IO_FAILURE, "IoFailure: cannot open " + path + " for writing"};
+        return false;
+    }
+    f.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
+    f.flush();
+    if (!f.good()) {
+        e = {HS_IO_FAILURE, "IoFailure: cannot write " + path};
+        return false;
+    }
+    return true;
+}
+
+hs_status report(const CamErr& e, char* msg, size_t len) {
+    put_msg(msg, len, e.what);
+    return e.s;
+}
+
 }  // namespace
 
 extern "C" {
+
+hs_status hs_read_cameras(const char* path, hs_camera* out, uint64_t cap, uint64_t* n, char* msg, size_t msg_len) {
+    if (!path || !n) return HS_INVALID_ARGUMENT;
+    std::string text;
+    if (!read_text(path, text)) return report({HS_IO_FAILURE, std::string("IoFailure: cannot open ") + path}, msg, msg_len);
+    uint64_t k = 0;
+    CamErr e{HS_OK, ""};
+    for (const std::string& line : data_lines(text)) {
+        std::istringstream ls(line);
+        hs_camera c{};
+        if (!get_camera(ls, line, c, e)) return report(e, msg, msg_len);
+        if (out && k < cap) out[k] = c;
+        ++k;
+    }
+    *n = k;
+    return HS_OK;
+}
+
+hs_status hs_read_camera_path(const char* path, double* ts, hs_camera* out, uint64_t cap, uint64_t* n, char* msg,
+                              size_t msg_len) {
+    if (!path || !n) return HS_INVALID_ARGUMENT;
+    std::string text;
+    if (!read_text(path, text)) return report({HS_IO_FAILURE, std::string("IoFailure: cannot open ") + path}, msg, msg_len);
+    uint64_t k = 0;
+    double prev = 0.0;
+    CamErr e{HS_OK, ""};
+    for (const std::string& line : data_lines(text)) {  // io.hpp:498-511
+        std::istringstream ls(line);
+        double t;
+        ls >> t;
+        if (ls.fail()) return report({HS_MALFORMED_HEADER, "MalformedHeader: expected a leading timestamp: " + line}, msg, msg_len);
+        hs_camera c{};
+        if (!get_camera(ls, line, c, e)) return report(e, msg, msg_len);
+        if (k > 0 && !(t > prev))
+            return report({HS_INVALID_ARGUMENT, "InvalidArgument: timestamps must be strictly increasing"}, msg, msg_len);
+        if (k < cap) {
+            if (out) out[k] = c;
+            if (ts) ts[k] = t;
+        }
+        prev = t;
+        ++k;
+    }
+    *n = k;
+    return HS_OK;
+}
+
+hs_status hs_write_cameras(const char* path, const hs_camera* cams, uint64_t n, char* msg, size_t msg_len) {
+    if (!path || (n && !cams)) return HS_INVALID_ARGUMENT;
+    std::ostringstream os;  // io.hpp:461-467
+    os << std::setprecision(9);
+    os << "# width height fx fy cx cy  world-to-camera 3x4 row-major\n";
+    for (uint64_t i = 0; i < n; ++i) put_camera(os, cams[i]);
+    CamErr e{HS_OK, ""};
+    if (!write_text(path, os.str(), e)) return report(e, msg, msg_len);
+    return HS_OK;
+}
+
+hs_status hs_write_camera_path(const char* path, const double* ts, const hs_camera* cams, uint64_t n, char* msg,
+                               size_t msg_len) {
+    if (!path || (n && (!cams || !ts))) return HS_INVALID_ARGUMENT;
+    for (uint64_t i = 1; i < n; ++i)  // io.hpp:478-481
+        if (!(ts[i] > ts[i - 1]))
+            return report({HS_INVALID_ARGUMENT, "InvalidArgument: timestamps must be strictly increasing"}, msg, msg_len);
+    std::ostringstream os;
+    os << std::setprecision(17);
+    os << "# timestamp  width height fx fy cx cy  world-to-camera 3x4 row-major\n";
+    for (uint64_t i = 0; i < n; ++i) {
+        os << ts[i] << ' ';
+        put_camera(os, cams[i]);
+    }
+    CamErr e{HS_OK, ""};
+    if (!write_text(path, os.str(), e)) return report(e, msg, msg_len);
+    return HS_OK;
+}
 
 hs_status hs_validate_hierarchy(const hs_node_soa* s, uint64_t n, char* msg, size_t msg_len) {
     auto fail = [&](const char* m) {

@@ -32,6 +32,7 @@ class Config:
     altitude: float = 40.0
     standoff: float = 30.0
     lookahead: float = 150.0
+    sky: int = 0  # multi-chunk scenes: make_skybox splats under the global root (0: none)
 
 
 CONFIGS = {
@@ -40,10 +41,17 @@ CONFIGS = {
                  lookahead=50.0),
     # configs[1]: 10M leaves, 1920x1080, tau = 3 px, 1 B200 (the headline metric)
     "c2": Config("c2_10m_1080p_tau3", 10_000_000, 1920, 1080, 1100.0, 3.0),
-    # configs[4]: 100M leaves multi-chunk (4 x 4 chunks of 6.25M + a 100K skybox under one root,
-    # assembled on the device: multichunk()), 3840x2160; ~58 GB resident
+    # configs[4]: 100M leaves multi-chunk (4 x 4 chunks of 6.25M leaves, a km-scale city, under one
+    # merged root, assembled breadth-first on the device: multichunk()), 3840x2160; ~58 GB resident
     "c5": Config("c5_100m_2160p_tau3", 100_000_000, 3840, 2160, 2200.0, 3.0, altitude=60.0, standoff=40.0,
                  lookahead=250.0),
+    # C5 with the 100K-splat make_skybox shell (scene.hpp:111-137) under the global root.  The
+    # reference projects shell splats lying just in front of the camera's image plane (at ~28 km
+    # to the side) into screen-covering ellipses -- it culls only at z <= 0.01 (render.hpp:110)
+    # and its EWA Jacobian has no field-of-view clamp -- and they sort first: every pixel
+    # saturates on them and the city is hidden.  Rendered bit-exactly, reported separately.
+    "c5sky": Config("c5sky_100m_2160p_tau3", 100_000_000, 3840, 2160, 2200.0, 3.0, altitude=60.0, standoff=40.0,
+                    lookahead=250.0, sky=100_000),
 }
 
 
@@ -77,6 +85,36 @@ def trajectory(cfg: Config, n_frames: int, first: int = 0) -> list[CameraModel]:
         pos = np.array([px, cfg.altitude, pz], np.float32)
         target = np.array([px + d[0] * cfg.lookahead, 0.0, pz + d[1] * cfg.lookahead], np.float32)
         cams.append(look_at_camera(pos, target, cfg.width, cfg.height, cfg.focal))
+    return cams
+
+
+def trajectory_inscene(cfg: Config, n_frames: int, first: int = 0, height: float = 6.0, ahead: float = 20.0,
+                       drop: float = 3.0) -> list[CameraModel]:
+    """SURVEY.md §8d's trajectory: a closed loop through the scene at `height` m (a circle
+    of radius 0.3 side perturbed by a third harmonic), looking at a target `ahead` m
+    along the path and `drop` m lower (pitched ~8.5 deg down); 1000 frames per loop.
+    Near-plane, inside-box (granularity = inf) and far-LOD nodes all occur.  Under the
+    reference's projection the city splats just in front of the image plane beside
+    the camera become screen-covering ellipses (no frustum cull, render.hpp:104-156)
+    that sort first and saturate every pixel: the frames exercise the cut, the
+    preprocess and the sorts at full load, and the blend hardly at all."""
+    side = scene_side(cfg.leaves)
+    R, wob = 0.3 * side, 0.1 * side
+
+    def at(a):
+        return np.array([R * math.cos(a) + wob * math.sin(3 * a), height, R * math.sin(a)], np.float64)
+
+    cams = []
+    for i in range(first, first + n_frames):
+        a = 2.0 * math.pi * (i % 1000) / 1000.0
+        p = at(a)
+        d = at(a + 1e-3) - p
+        d[1] = 0.0
+        d /= np.linalg.norm(d)
+        target = p + ahead * d
+        target[1] = height - drop
+        cams.append(look_at_camera(p.astype(np.float32), target.astype(np.float32), cfg.width, cfg.height,
+                                   cfg.focal))
     return cams
 
 

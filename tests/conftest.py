@@ -36,6 +36,26 @@ def pytest_collection_modifyitems(config, items):
 @pytest.fixture(scope="session")
 def renderer():
     import paper_2406_12080_b200 as hs
-    r = hs.Renderer(0, exact=True, debug=True)
+    r = hs.Renderer(0, exact=True, debug=True, stats=True)
     yield r
     r.close()
+
+
+@pytest.fixture(scope="session")
+def c2():
+    """BASELINE config[1]: the 10M-leaf hierarchy, shared by the full-size tests."""
+    from paper_2406_12080_b200 import scenes
+    cfg = scenes.CONFIGS["c2"]
+    return cfg, scenes.hierarchy(cfg)
+
+
+@pytest.fixture(scope="session")
+def c2_oracle(c2):
+    """The oracle's copy of the C2 hierarchy (304 B/node AoS, ~6 GB of host memory)."""
+    from oracle import oracle as orc
+    return orc.OracleHierarchy(c2[1])
+
+
+@pytest.fixture(scope="session")
+def c2_device(renderer, c2):
+    return renderer.upload(c2[1], validate=True)

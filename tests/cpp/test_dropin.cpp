@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <thread>
 #include <vector>
 
 static int failures = 0;
@@ -134,11 +135,15 @@ int main() {
         for (float t : bo.transmittance.data) mass += 1.0 - t;
         const double want = 0.28209479177387814 * mass / n;
         CHECK(std::abs(g.sh[0][0] - want) <= 1e-4 * std::abs(want));
-        // a context from an older render is stale
+        // a context from an older render still differentiates its own forward pass
         (void)render_forward<float>(std::span<const RenderSplat>(one), bc, nullptr);
+        const RenderGrads g2 = render_backward<float>(bctx, lg);
+        CHECK(g2.sh[0][0] == g.sh[0][0]);
+        // an invalid context has no forward state (render.hpp:432-433)
+        ForwardContext empty;
         threw = false;
         try {
-            render_backward<float>(bctx, lg);
+            render_backward<float>(empty, lg);
         } catch (const Error& err) {
             threw = err.code() == Errc::MissingForwardState;
         }
@@ -184,6 +189,53 @@ int main() {
         CameraPath p2;
         for (int i = 0; i < 4; ++i) p2.cameras.push_back(cam);
         CHECK(bench_path(dh, p2, 3.0f).frames.size() == 4);
+    }
+
+    // write_hierarchy / read_hierarchy round trip (io.hpp:350-408); camera text IO (io.hpp:410-511)
+    {
+        write_hierarchy("/tmp/hs_dropin_rt.h3dg", h);
+        const Hierarchy back = read_hierarchy("/tmp/hs_dropin_rt.h3dg");
+        CHECK(back.nodes.size() == h.nodes.size() && back.nodes.back().g.sh[7] == h.nodes.back().g.sh[7]);
+        const CameraModel cams[2] = {cam, look_at(3, 9, -40, 0, 0, 0, 320, 200, 250.0f)};
+        write_cameras("/tmp/hs_dropin_cams.txt", cams);
+        const auto rc = read_cameras("/tmp/hs_dropin_cams.txt");
+        CHECK(rc.size() == 2 && rc[1].width == 320 && rc[1].world_to_camera(2, 3) == cams[1].world_to_camera(2, 3));
+        CameraPath cp;
+        cp.cameras = {cams[0], cams[1]};
+        cp.timestamps = {0.0, 1.0 / 30.0};
+        write_camera_path("/tmp/hs_dropin_path.txt", cp);
+        const CameraPath rp = read_camera_path("/tmp/hs_dropin_path.txt");
+        CHECK(rp.cameras.size() == 2 && rp.timestamps[1] == cp.timestamps[1]);
+        cp.timestamps = {1.0, 1.0};
+        threw = false;
+        try {
+            write_camera_path("/tmp/hs_dropin_path.txt", cp);
+        } catch (const Error& err) {
+            threw = err.code() == Errc::InvalidArgument;
+        }
+        CHECK(threw);
+        // bench_path CSV schema (bench.hpp:33-48, test_bench.cpp:141-158) and metrics (bench.hpp:105-112)
+        const std::string csv = rep.csv();
+        CHECK(csv.rfind("frame,rendered,rendered_pct,transferred,cut_expand_s", 0) == 0);
+        CHECK(csv.find("\ntotal,") != std::string::npos);
+        const Metrics m = metrics(a.color, b.color);
+        CHECK(m.psnr_db == 99.0 && std::abs(m.ssim - 1.0) < 1e-6);
+        set_thread_count(3);
+        CHECK(thread_count() == 3);
+        set_thread_count(0);
+    }
+
+    // reentrant across host threads: every thread its own device context
+    {
+        std::vector<float> got(4, 0.0f);
+        std::vector<std::thread> pool;
+        for (int k = 0; k < 4; ++k)
+            pool.emplace_back([&, k] {
+                const RenderOutput r = render_hierarchy(h, cam, 3.0f);
+                got[k] = r.color.data[r.color.data.size() / 2] + float(r.rendered_count == a.rendered_count);
+            });
+        for (auto& t : pool) t.join();
+        for (int k = 1; k < 4; ++k) CHECK(got[k] == got[0]);
     }
 
     // read_hierarchy error code (io.hpp:375-387)

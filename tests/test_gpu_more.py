@@ -20,21 +20,13 @@ def images_equal(out, f):
             and np.array_equal(out.transmittance.view(np.uint32), t.view(np.uint32)) and out.rendered_count == rc)
 
 
-@pytest.fixture(scope="module")
-def c2():
-    cfg = scenes.CONFIGS["c2"]
-    h = scenes.hierarchy(cfg)
-    return cfg, h
-
-
-def test_c2_full_size_bit_exact(renderer, c2):
+def test_c2_full_size_bit_exact(renderer, c2, c2_oracle, c2_device):
     """BASELINE config[1]: cut, sorted keys/tile ranges and image bit-exact vs the oracle."""
     cfg, h = c2
     cam = scenes.camera(cfg, 100)
-    dh = renderer.upload(h, validate=True)
+    dh = c2_device
     out, cut = renderer.render_hierarchy(dh, cam, cfg.tau, want_context=True, return_cut=True)
-    oh = orc.OracleHierarchy(h)
-    f = orc.render_hierarchy(oh, cam, cfg.tau, keep_ctx=True)
+    f = orc.render_hierarchy(c2_oracle, cam, cfg.tau, keep_ctx=True)
     node, t, a = f.cut()
     assert np.array_equal(cut.node, node)
     assert np.array_equal(cut.t.view(np.uint32), t.view(np.uint32))
@@ -65,12 +57,12 @@ def test_c2_full_size_bit_exact(renderer, c2):
     assert int(under[cut.node].sum()) == h.leaf_count()
 
 
-def test_c2_fast_mode_within_tolerance(c2):
+def test_c2_fast_mode_within_tolerance(c2, c2_oracle):
     cfg, h = c2
     cam = scenes.camera(cfg, 333)
     r = hs.Renderer(0, exact=False)
     out = r.render_hierarchy(h, cam, cfg.tau)
-    f = orc.render_hierarchy(orc.OracleHierarchy(h), cam, cfg.tau, keep_ctx=False)
+    f = orc.render_hierarchy(c2_oracle, cam, cfg.tau, keep_ctx=False)
     c, d, t, rc = f.images()
     assert np.abs(out.color - c).max() <= 1e-3
     assert np.abs(out.transmittance - t).max() <= 1e-3
