@@ -445,15 +445,19 @@ def main():
                           "and the stats all_gathered"}
         src.tracker.close()
 
-    # ---- stage breakdown + roofline inputs: the same frames, per-stage CUDA events, with the
-    # blend's work counters on (HS_OPT_STATS; the timed frames above ran without them)
-    r.set_stats(True)
+    # ---- stage breakdown + roofline inputs: the same frames twice, per-stage CUDA events as
+    # timed above (no counters), then with the blend's work counters on (HS_OPT_STATS) for the
+    # frames' work (the frames are deterministic: the same work both times)
     st = hs.StageTimes()
-    infos = []
-    for c in timed[: min(len(timed), 16)]:
+    breakdown = timed[: min(len(timed), 16)]
+    for c in breakdown:
         s = N.hs_stage_times()
         hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, s), r.ctx)
         st.add(s)
+    r.set_stats(True)
+    infos = []
+    for c in breakdown:
+        hs._check(L.hs_render_hierarchy(r.ctx, dh.handle, c, cfg.tau, r._cut, r._frame, None), r.ctx)
         fi = N.hs_frame_info()
         hs._check(L.hs_frame_get_info(r.ctx, r._frame, fi), r.ctx)
         infos.append(fi)

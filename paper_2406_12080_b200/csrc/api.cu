@@ -827,8 +827,10 @@ hs_status hs_hierarchy_assemble(hs_context* ctx, const hs_hierarchy* const* part
     uint64_t total = k > 1 ? 1 : 0, leaves = 0, widest = k;
     hs::PartTable pt{};
     for (uint32_t p = 0; p < k; ++p) {
-        if (!parts[p] || parts[p]->n == 0 || parts[p]->ctx != ctx)
+        if (!parts[p] || parts[p]->n == 0)
             return set_err(ctx, HS_INVALID_ARGUMENT, "chunk hierarchy is empty");  // scene.hpp:237
+        if (parts[p]->ctx->device != ctx->device)
+            return set_err(ctx, HS_INVALID_ARGUMENT, "chunk hierarchies must live on the context's device");
         pt.cull[p] = parts[p]->cull.as<float4>();
         pt.attr[p] = parts[p]->attr.as<float4>();
         total += parts[p]->n;

@@ -113,6 +113,6 @@ def test_c5_multichunk_4m_leaves_4k_bit_exact(renderer, sky):
         out, f = full_parity(renderer, dh, oh, scenes.camera(cfg, frame), cfg.tau, projection=False)
         if sky:  # the reference's projection turns shell splats beside the camera into screen-covering
             # ellipses (no frustum cull, render.hpp:104-156): every pixel saturates on them
-            assert float(out.transmittance.max()) < 1e-4
+            assert float(out.transmittance.max()) < 1e-3  # (the break leaves T >= 1e-4)
         else:
             assert float(out.transmittance.mean()) > 0.05  # the city is composited, with sky gaps
