@@ -380,7 +380,10 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
     HS_CUDA(ctx, f->color.ensure(plane * 12));
     HS_CUDA(ctx, f->depth.ensure(plane * 4));
     HS_CUDA(ctx, f->trans.ensure(plane * 4));
-    HS_CUDA(ctx, f->stats.ensure(sizeof(DevStats)));
+    if (!f->stats.p) {  // the sticky overflow counter must start at zero
+        HS_CUDA(ctx, f->stats.ensure(sizeof(DevStats)));
+        HS_CUDA(ctx, cudaMemsetAsync(f->stats.p, 0, sizeof(DevStats), frame_stream(ctx, f)));
+    }
     f->passes = sort_passes_for(tiles);
     HS_CUDA(ctx, f->scratch.ensure(scratch_layout(cs, f->cap_dup, f->passes).total));
     if (!f->h_stats) {

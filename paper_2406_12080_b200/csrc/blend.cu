@@ -26,6 +26,10 @@
 #include "hs_device.cuh"
 #include "hs_kernels.h"
 
+#ifndef HS_BLEND_QFLO
+#define HS_BLEND_QFLO 1
+#endif
+
 namespace hs {
 
 // (-0, 1, -1, -0.5) pairs as kernel parameters: see phase 2
@@ -102,10 +106,16 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
             float* dst = &s_pp[warp][st][lane >> 1][0].x + (lane & 1);
 #pragma unroll
             for (int f = 0; f < 6; ++f) __pipeline_memcpy_async(dst + 2 * f, srcf + (f < 5 ? f : 13), 4);
+        } else {
+            // no entry in this slot: a power floor of +inf is never reached, so the slot is
+            // never live (the power loop needs no per-entry bound check)
+            (&s_pp[warp][st][lane >> 1][5].x)[lane & 1] = __int_as_float(0x7f800000);
         }
         __pipeline_commit();
     };
     while (true) {
+        // (fetching the next task one task ahead was measured 18% slower: heavy-first
+        // tasks reserved by busy warps lengthen the tail)
         uint32_t task = 0;
         if (lane == 0) task = atomicAdd(task_counter, 1u);
         task = __shfl_sync(0xffffffffu, task, 0);
@@ -203,12 +213,16 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                     const float p_lo = __uint_as_float((uint32_t)pw), p_hi = __uint_as_float((uint32_t)(pw >> 32));
                     // live iff the alpha can reach the 1/255 floor: m e^power >= 1/255 needs
                     // power >= -ln(255 m) >= floor = -qthr/2 (qthr carries the margin).
-                    // Branch-free: the power is stored either way (read only for live pairs).
-                    const bool lv0 = (p_lo <= 0.0f) & (p_lo >= fl.x);
-                    const bool lv1 = (p_hi <= 0.0f) & (p_hi >= fl.y) & (2 * kp + 1 < (int)hc);
+                    // Branch-free: the power is stored either way (read only for live pairs);
+                    // the tests are set.* masks (all ones / zero) folded into the bit field.
                     sv[2 * kp][lane] = p_lo;
                     sv[2 * kp + 1][lane] = p_hi;
-                    live |= ((uint32_t)lv0 | ((uint32_t)lv1 << 1)) << (2 * kp);
+                    uint32_t a0, b0, a1, b1;
+                    asm("set.le.u32.f32 %0, %1, 0f00000000;" : "=r"(a0) : "f"(p_lo));
+                    asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(b0) : "f"(p_lo), "f"(fl.x));
+                    asm("set.le.u32.f32 %0, %1, 0f00000000;" : "=r"(a1) : "f"(p_hi));
+                    asm("set.ge.u32.f32 %0, %1, %2;" : "=r"(b1) : "f"(p_hi), "f"(fl.y));
+                    live |= (a0 & b0 & (1u << (2 * kp))) | (a1 & b1 & (2u << (2 * kp)));
                 }
             }
             // 3. alpha of every live (pixel, entry) pair.  Alpha does not depend on T, so the
@@ -225,7 +239,16 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                 const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
                 if (kStats) w_exp += total;
                 uint32_t pos = incl - cnt;
+#if HS_BLEND_QFLO
+                // highest pending bit first (one FLO per pair; the queue order is free)
+                for (uint32_t m = live; m;) {
+                    const int k = 31 - __clz(m);
+                    sq[pos++] = (uint16_t)((lane << 4) | k);
+                    m ^= 1u << k;
+                }
+#else
                 for (uint32_t m = live; m; m &= m - 1) sq[pos++] = (uint16_t)((lane << 4) | (__ffs(m) - 1));
+#endif
                 __syncwarp();
                 for (uint32_t pq = lane; pq < total; pq += 32) {
                     const uint32_t pr = sq[pq];

@@ -115,18 +115,34 @@ __device__ __forceinline__ int f2i_x86(float v) {
 }
 __device__ __forceinline__ int iclamp(int v, int lo, int hi) { return v < lo ? lo : (hi < v ? hi : v); }
 
+#ifndef HS_GRAN_FMNMX
+#define HS_GRAN_FMNMX 0
+#endif
 // granularity (lod.hpp:18-26) of a node box.
 __device__ __forceinline__ float granularity(float mnx, float mny, float mnz, float mxx, float mxy, float mxz,
                                              const CamParams& c) {
     if ((c.pos[0] >= mnx && c.pos[1] >= mny && c.pos[2] >= mnz) &&
         (c.pos[0] <= mxx && c.pos[1] <= mxy && c.pos[2] <= mxz))
         return __int_as_float(0x7f800000);
+#if HS_GRAN_FMNMX
+    // FMNMX instead of std::min/max's compare + select: the same value for non-NaN
+    // operands (finite boxes and camera); the sign of a zero product or difference
+    // cannot change the sums that follow (z is only compared with the near plane
+    // after adding it, a zero extent is +0 either way)
+    float z = c.w2c[11];
+    z = z + fminf(c.w2c[8] * mnx, c.w2c[8] * mxx);
+    z = z + fminf(c.w2c[9] * mny, c.w2c[9] * mxy);
+    z = z + fminf(c.w2c[10] * mnz, c.w2c[10] * mxz);
+    if (z <= kNearPlane) return __int_as_float(0x7f800000);
+    const float L = fmaxf(mxx - mnx, fmaxf(mxy - mny, mxz - mnz));
+#else
     float z = c.w2c[11];
     z = z + smin(c.w2c[8] * mnx, c.w2c[8] * mxx);
     z = z + smin(c.w2c[9] * mny, c.w2c[9] * mxy);
     z = z + smin(c.w2c[10] * mnz, c.w2c[10] * mxz);
     if (z <= kNearPlane) return __int_as_float(0x7f800000);
     const float L = smax(mxx - mnx, smax(mxy - mny, mxz - mnz));
+#endif
     return c.maxf * L / z;
 }
 

@@ -10,7 +10,7 @@ PCT = ["smsp__issue_active.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
-       "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
+       "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
 txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                       ",".join(["dram__bytes_read.sum", "dram__bytes_write.sum"] + PCT)],
                      capture_output=True, text=True).stdout
@@ -36,7 +36,7 @@ for r in rows[2:]:
 res = {"source": rep.split("/")[-1], "how": "ncu --set full --clock-control none, one C2 frame; per-launch mean",
        "kernels": {k: {"dram_bytes": (v[0] + v[1]) / v[3], "read": v[0] / v[3], "write": v[1] / v[3],
                        "launches": v[3],
-                       "pct_of_peak": {m.split(".")[0].replace("sm__inst_executed_", "").replace("smsp__", "")
+                       "pct_of_peak": {m.split(".")[0].replace("sm__inst_executed_", "").replace("smsp__", "").replace("gpu__", "")
                                        .replace("__", "_"): pct[k][m] / v[3] for m in PCT}}
                    for k, v in acc.items()}}
 json.dump(res, open(out, "w"), indent=1)

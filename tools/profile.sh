@@ -8,10 +8,10 @@ TAG=${1:-cur}
 OUT=gpurun_out/prof_$TAG
 mkdir -p $OUT
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $OUT/launches.csv \
-    python bench.py --steps 4 --warmup 3 --lanes 1 --no-cpu-baseline --no-tau-sweep > $OUT/launches_bench.log 2>&1
+    python bench.py --steps 4 --warmup 3 --lanes 1 --no-cpu-baseline --no-tau-sweep --no-inscene --no-replay > $OUT/launches_bench.log 2>&1
 echo "launch list rc=$?"
 # the warm-up frames are synchronous; skip them (25-27 launches each) and take one launch per kernel
 ncu --set full --import-source on --clock-control none --launch-skip 120 --launch-count 30 \
-    -o $OUT/full python bench.py --steps 4 --warmup 3 --lanes 1 --no-cpu-baseline --no-tau-sweep > $OUT/full_bench.log 2>&1
+    -o $OUT/full python bench.py --steps 4 --warmup 3 --lanes 1 --no-cpu-baseline --no-tau-sweep --no-inscene --no-replay > $OUT/full_bench.log 2>&1
 echo "full rc=$?"
 ls -la $OUT
