@@ -29,6 +29,14 @@
 #ifndef HS_BLEND_QFLO
 #define HS_BLEND_QFLO 1
 #endif
+// HS_BLEND_TQ: split-law pairs first in the alpha queue (homogeneous rounds).  Measured
+// 6% slower (the divergent two-way push costs more than the powf idling it saves).
+#ifndef HS_BLEND_TQ
+#define HS_BLEND_TQ 0
+#endif
+#ifndef HS_BLEND_CM
+#define HS_BLEND_CM 0
+#endif
 
 namespace hs {
 
@@ -186,7 +194,9 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
             const uint32_t hc = min(16u, cnt - h);
             const bool active = !done;
             // transitioning entries (t < 1) of this half, for the work counters
-            const uint32_t ttr = kStats ? __ballot_sync(0xffffffffu, lane < (int)hc && rec[h + lane][0].w < 1.0f) : 0u;
+            const uint32_t ttr = (kStats || HS_BLEND_TQ)
+                                     ? __ballot_sync(0xffffffffu, lane < (int)hc && rec[h + lane][0].w < 1.0f)
+                                     : 0u;
             // 2. per-pixel power and liveness (cheap, all lanes)
             uint32_t live = 0;
             if (active) {
@@ -229,17 +239,41 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
             //    pairs of all lanes are compacted into one queue and evaluated 32 at a time
             //    with every lane busy (the exact expf/powf replicas are the costly part).
             {
+#if HS_BLEND_TQ
+                // pairs of transitioning entries (the split law's powf) first, the others
+                // after them: the queue's rounds are then almost all of one kind, so the
+                // plain rounds skip the powf replica instead of idling through it
+                const uint32_t cnt = __popc(live & ttr) | (__popc(live & ~ttr) << 16);
+#else
                 const uint32_t cnt = __popc(live);
+#endif
                 uint32_t incl = cnt;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
                     if (lane >= o) incl += v;
                 }
+#if HS_BLEND_TQ
+                const uint32_t tot2 = __shfl_sync(0xffffffffu, incl, 31);
+                const uint32_t total_t = tot2 & 0xffffu, total = total_t + (tot2 >> 16);
+                if (kStats) w_exp += total;
+                uint32_t pos_t = (incl - cnt) & 0xffffu, pos_n = total_t + ((incl - cnt) >> 16);
+                for (uint32_t m = live; m;) {
+                    const int k = 31 - __clz(m);
+                    const uint32_t item = (lane << 4) | (uint32_t)k;
+                    if ((ttr >> k) & 1u)
+                        sq[pos_t++] = (uint16_t)item;
+                    else
+                        sq[pos_n++] = (uint16_t)item;
+                    m ^= 1u << k;
+                }
+#else
                 const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
                 if (kStats) w_exp += total;
                 uint32_t pos = incl - cnt;
-#if HS_BLEND_QFLO
+#endif
+#if HS_BLEND_TQ
+#elif HS_BLEND_QFLO
                 // highest pending bit first (one FLO per pair; the queue order is free)
                 for (uint32_t m = live; m;) {
                     const int k = 31 - __clz(m);
@@ -305,7 +339,14 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                     int k;
                     asm("bfind.u32 %0, %1;" : "=r"(k) : "r"(bit));
                     const float alpha = sv[k][lane];
+#if HS_BLEND_CM
+                    // branch-free skip: an alpha of 0 (both laws gated out) leaves T, the
+                    // colour and the depth bit-identical (T * 1, + 0 to non-negative sums) and
+                    // cannot break (T >= 1e-4), so only its rendered_count flag is masked
+                    {
+#else
                     if (alpha > 0.0f) {
+#endif
                         const float test = T * (1.0f - alpha);
                         if (test < kTransmittanceEps) {
                             act |= bit;  // the pixel is done: act stays non-zero
@@ -319,7 +360,11 @@ __global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restr
                         c2 = c2 + p2.z * wgt;
                         d = d + p2.w * alpha * T;
                         T = test;
+#if HS_BLEND_CM
+                        cm |= alpha > 0.0f ? bit : 0u;
+#else
                         cm |= bit;
+#endif
                     }
                 }
                 if (act) done = true;

@@ -116,7 +116,7 @@ __device__ __forceinline__ int f2i_x86(float v) {
 __device__ __forceinline__ int iclamp(int v, int lo, int hi) { return v < lo ? lo : (hi < v ? hi : v); }
 
 #ifndef HS_GRAN_FMNMX
-#define HS_GRAN_FMNMX 0
+#define HS_GRAN_FMNMX 1
 #endif
 // granularity (lod.hpp:18-26) of a node box.
 __device__ __forceinline__ float granularity(float mnx, float mny, float mnz, float mxx, float mxy, float mxz,
