@@ -37,6 +37,11 @@
 #ifndef HS_BLEND_CM
 #define HS_BLEND_CM 0
 #endif
+// minimum resident CTAs per SM the register allocation must allow (shared memory
+// holds it to 7 anyway; 8 caps the kernel at 64 registers)
+#ifndef HS_BLEND_MINB
+#define HS_BLEND_MINB 8
+#endif
 
 namespace hs {
 
@@ -64,7 +69,7 @@ constexpr size_t kSmemQ = sizeof(uint16_t) * kBlendWarps * 512;         // live-
 constexpr uint32_t kListCap = 1024;                                      // per-warp block list (global, L2)
 
 template <int kMode, bool kStats>
-__global__ void __launch_bounds__(kBlendThreads, 8) k_blend(const uint2* __restrict__ ranges,
+__global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const uint2* __restrict__ ranges,
                                                             const uint32_t* __restrict__ keys,
                                                             const uint32_t* __restrict__ vals,
                                                             const ProjRec* __restrict__ proj,
