@@ -56,7 +56,7 @@ struct DevStats {
     unsigned long long n_exp;      // expf evaluations (live pairs)
     unsigned long long n_pow;      // powf evaluations (live transition pairs)
     unsigned long long n_trans;    // C_t: cut entries with a parent and t < 1
-    uint64_t n_visible_sorted;     // V from the order-preserving compaction (key count of the depth sort)
+    uint64_t n_visible_sorted;     // V from the order-preserving compaction (global depth order, on request)
     uint64_t n_splats_req;         // C when it exceeded the frame's per-splat capacity (else 0)
     unsigned long long overflows;  // sticky: frames whose D exceeded capacity since the last wait
 };
@@ -159,8 +159,9 @@ struct hs_frame {
     uint64_t cap_splats = 0, cap_dup = 0;
     int W = 0, H = 0, tiles_x = 0, tiles_y = 0, passes = 0;
     DBuf tile_order;
-    DBuf proj, dinfo, dupcount, offsets, zkeys[2], zvals[2], keys[2], vals[2], dupk, dupv, keys64, ranges, color, depth, trans, touched, dbg16,
-        splat_attr, stats, scratch, bw, huge;
+    DBuf proj, dinfo, dupcount, zkeys[2], zvals[2], keys[2], vals[2], mkeys, mvals, bmask, dupk, dupv, keys64, ranges, color, depth,
+        trans, touched, dbg16, splat_attr, stats, scratch, bw, huge;
+    bool order_ready = false;  // global depth order (zkeys/zvals) built for the current render
     DevStats* h_stats = nullptr;  // pinned, mapped
     DevStats* h_stats_dev = nullptr;  // device alias of h_stats
     DevStats* h_stats_dl = nullptr;  // pinned, snapshot taken with an async read-back
@@ -281,39 +282,35 @@ CamParams make_cam(const hs_camera* c) {
     return p;
 }
 
-// 8-bit passes of the tile-index sort (order.cu): 2 at 1080p (8160 tiles, 13 bits)
-int tile_bits(int tiles) {
-    int tb = 0;
-    while ((1ll << tb) < tiles) ++tb;
-    return std::max(1, tb);
-}
-int sort_passes_for(int tiles) { return (tile_bits(tiles) + 7) / 8; }
-
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
-// Layout of the per-frame scratch (zeroed once per frame):
-//   [0]        scan tile counter (u32) + pad
-//   [64]       sort counters (8 x u32)
-//   [128]      sort histogram (8 x 256 u32)
-//   [8320]     scan status (u64 words)
-//   [...]      sort status (passes x sort_status_words u32)
-// Per-frame scratch.  [0, zero_bytes) is zeroed once per frame: the tile
-// counters of the two look-back scans and of the blend, and their status words.
-// The two radix sorts zero their own look-back words on the device (sized from
-// the device-side key counts).
+// Per-frame scratch.  [0, zero_bytes) is zeroed once per frame: the work
+// counters of the blend, the bucketing and the in-tile sort, the per-tile
+// counts and row difference marks of the bucketing, and the per-tile chunk
+// completion counters.  Then the tile plan (cursors, chunk offsets, big-tile
+// list, task counts: written by k_tile_plan), the global depth order's scan and
+// sort scratch (zeroed when it is built, build_depth_order), and the blend's
+// per-warp block lists.
 struct ScratchLayout {
-    size_t vis_counter = 0, dup_counter = 4, blend_counter = 8, huge_counter = 12, touch_ticket = 16, vis_status = 64, dup_status = 0, zero_bytes = 0,
-           depth_sort = 0, tile_sort = 0, blend_list = 0, total = 0;
+    size_t blend_counter = 0, huge_counter = 4, touch_ticket = 8, task_counter = 12, plan = 32, tcount = 64,
+           rowdiff = 0, done = 0, zero_bytes = 0, cursor = 0, prange = 0, big_list = 0, extra = 0, vis_counter = 0,
+           vis_status = 0, depth_sort = 0, depth_zero_end = 0, blend_list = 0, total = 0;
 };
-ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int tile_passes) {
+ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int tiles_x, int tiles_y) {
     ScratchLayout L;
-    L.dup_status = round_up(L.vis_status + hs::scan_status_words(n_max) * 8, 256);
-    // the depth sort's histograms + tile counters are zeroed with the rest (its
-    // look-back words are zeroed by k_compact_visible)
-    L.depth_sort = round_up(L.dup_status + hs::scan_status_words(n_max) * 8, 256);
-    L.zero_bytes = round_up(L.depth_sort + 4 * (256 + 1) * 4, 256);
-    L.tile_sort = round_up(L.depth_sort + hs::sort_scratch_words(n_max, 4) * 4, 256);
-    L.blend_list = round_up(L.tile_sort + hs::sort_scratch_words(cap_dup, tile_passes) * 4, 256);
+    const uint64_t tiles = (uint64_t)tiles_x * tiles_y;
+    L.rowdiff = round_up(L.tcount + tiles * 4, 256);
+    L.done = round_up(L.rowdiff + (uint64_t)(tiles_x + 1) * tiles_y * 4, 256);
+    L.zero_bytes = round_up(L.done + tiles * 4, 256);
+    L.cursor = L.zero_bytes;
+    L.prange = round_up(L.cursor + tiles * 4, 256);
+    L.big_list = round_up(L.prange + tiles * 8, 256);
+    L.extra = round_up(L.big_list + tiles * 4, 256);
+    L.vis_counter = round_up(L.extra + hs::tile_sort_extra_slots(cap_dup) * 8, 256);
+    L.vis_status = L.vis_counter + 64;
+    L.depth_sort = round_up(L.vis_status + hs::scan_status_words(n_max) * 8, 256);
+    L.depth_zero_end = round_up(L.depth_sort + 4 * (256 + 1) * 4, 256);
+    L.blend_list = round_up(L.depth_sort + hs::sort_scratch_words(n_max, 4) * 4, 256);
     L.total = L.blend_list + hs::blend_list_words() * 4;
     return L;
 }
@@ -358,7 +355,6 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
     HS_CUDA(ctx, f->proj.ensure(cs * sizeof(ProjRec)));
     HS_CUDA(ctx, f->dupcount.ensure(cs * 4));
     HS_CUDA(ctx, f->dinfo.ensure(cs * 16));
-    HS_CUDA(ctx, f->offsets.ensure(cs * 4));
     const bool fresh_touched = f->touched.bytes < cs;
     HS_CUDA(ctx, f->touched.ensure(cs));
     if (fresh_touched) HS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, f->touched.bytes, frame_stream(ctx, f)));
@@ -368,12 +364,15 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
         HS_CUDA(ctx, f->keys[b].ensure(f->cap_dup * 4));
         HS_CUDA(ctx, f->vals[b].ensure(f->cap_dup * 4));
     }
+    HS_CUDA(ctx, f->mkeys.ensure(f->cap_dup * 4));
+    HS_CUDA(ctx, f->mvals.ensure(f->cap_dup * 4));
+    HS_CUDA(ctx, f->bmask.ensure(f->cap_dup * 2));
     if (ctx->debug) {
         HS_CUDA(ctx, f->dupk.ensure(f->cap_dup * 8));
         HS_CUDA(ctx, f->dupv.ensure(f->cap_dup * 4));
         HS_CUDA(ctx, f->dbg16.ensure(cs * 64));
     }
-    HS_CUDA(ctx, f->huge.ensure(hs::huge_queue_slots(f->cap_dup) * 8));
+    HS_CUDA(ctx, f->huge.ensure(hs::bucket_huge_slots(f->cap_dup) * 4));
     HS_CUDA(ctx, f->ranges.ensure((size_t)tiles * 8));
     HS_CUDA(ctx, f->tile_order.ensure((size_t)tiles * 4));
     const size_t plane = (size_t)cp.width * cp.height;
@@ -384,8 +383,8 @@ hs_status ensure_frame(hs_context* ctx, hs_frame* f, uint64_t n_max, const CamPa
         HS_CUDA(ctx, f->stats.ensure(sizeof(DevStats)));
         HS_CUDA(ctx, cudaMemsetAsync(f->stats.p, 0, sizeof(DevStats), frame_stream(ctx, f)));
     }
-    f->passes = sort_passes_for(tiles);
-    HS_CUDA(ctx, f->scratch.ensure(scratch_layout(cs, f->cap_dup, f->passes).total));
+    f->passes = 0;  // no global sort pass: the final tile lists are keys[0] / vals[0]
+    HS_CUDA(ctx, f->scratch.ensure(scratch_layout(cs, f->cap_dup, cp.tiles_x, cp.tiles_y).total));
     if (!f->h_stats) {
         HS_CUDA(ctx, cudaHostAlloc(&f->h_stats, sizeof(DevStats), cudaHostAllocMapped));
         HS_CUDA(ctx, cudaHostGetDevicePointer(&f->h_stats_dev, f->h_stats, 0));
@@ -406,54 +405,49 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     cudaStream_t s = frame_stream(ctx, f);
     const CamParams& cp = f->cam;
     DevStats* ds = f->stats.as<DevStats>();
-    const ScratchLayout L = scratch_layout(std::max<uint64_t>(f->cap_splats, 1), f->cap_dup, f->passes);
+    const ScratchLayout L = scratch_layout(std::max<uint64_t>(f->cap_splats, 1), f->cap_dup, cp.tiles_x, cp.tiles_y);
     unsigned char* sc = f->scratch.as<unsigned char>();
+    const int tiles = cp.tiles_x * cp.tiles_y;
     // the images of this frame object may still be streaming to the host
     if (f->copy_pending) HS_CUDA(ctx, cudaStreamWaitEvent(s, f->copy_done, 0));
     if (f->dcopy_pending) HS_CUDA(ctx, cudaStreamWaitEvent(s, f->dcopy_done, 0));
     HS_CUDA(ctx, cudaMemsetAsync(sc, 0, L.zero_bytes, s));
     HS_CUDA(ctx, cudaMemsetAsync(&ds->n_visible, 0, offsetof(DevStats, overflows) - 8, s));
-    HS_CUDA(ctx, cudaMemsetAsync(f->ranges.p, 0, (size_t)cp.tiles_x * cp.tiles_y * 8, s));
+    f->order_ready = false;
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[1], s));
+    uint32_t* tcount = reinterpret_cast<uint32_t*>(sc + L.tcount);
+    uint32_t* plan = reinterpret_cast<uint32_t*>(sc + L.plan);
     hs::launch_preprocess(f->from_cut, f->attr, f->cut_node, f->cut_t, f->n_ptr, f->n_max, cp, f->proj.as<ProjRec>(),
                           f->dinfo.as<uint4>(), f->dupcount.as<uint32_t>(),
                           ctx->debug ? f->dbg16.as<float>() : nullptr, &ds->n_visible,
-                          f->from_cut ? &ds->n_splats : nullptr, &ds->overflows, &ds->n_splats_req, &ds->n_trans, s);
+                          f->from_cut ? &ds->n_splats : nullptr, &ds->overflows, &ds->n_splats_req, &ds->n_trans,
+                          s);
     // the cut's arrays are not read past preprocess (n_splats holds its count from here)
     if (f->from_cut && f->src_cut) HS_TRY(mark_cut(ctx, f->src_cut, s));
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[2], s));
-    // depth order of the visible splats (stable: ties keep cut order, render.hpp:268-272)
-    uint32_t* zk[2] = {f->zkeys[0].as<uint32_t>(), f->zkeys[1].as<uint32_t>()};
-    uint32_t* zv[2] = {f->zvals[0].as<uint32_t>(), f->zvals[1].as<uint32_t>()};
-    hs::launch_compact_visible(f->dupcount.as<uint32_t>(), f->dinfo.as<uint4>(), &ds->n_splats, f->n_max, zk[0], zv[0],
-                               reinterpret_cast<uint64_t*>(sc + L.vis_status),
-                               reinterpret_cast<uint32_t*>(sc + L.vis_counter), &ds->n_visible_sorted,
-                               reinterpret_cast<uint32_t*>(sc + L.depth_sort), s);
-    hs::launch_radix_sort(zk, zv, &ds->n_visible_sorted, f->n_max, 0, 4, 32,
-                          reinterpret_cast<uint32_t*>(sc + L.depth_sort), s, /*hist_ready=*/true);
-    const uint32_t* ids = zv[0];  // 4 passes: result back in buffer 0
-    // (tile, splat) pairs in depth order, then a stable sort by tile (render.hpp:273-294)
-    hs::launch_dup_offsets(ids, f->dupcount.as<uint32_t>(), &ds->n_visible_sorted, f->n_max, f->offsets.as<uint32_t>(),
-                           reinterpret_cast<uint64_t*>(sc + L.dup_status),
-                           reinterpret_cast<uint32_t*>(sc + L.dup_counter), &ds->n_dup, &ds->sort_n, f->cap_dup,
-                           &ds->overflows, s);
+    // per-tile lists in depth order (render.hpp:262-294): plan, bucket, in-tile sort
+    hs::launch_tile_count(f->dupcount.as<uint32_t>(), f->dinfo.as<uint4>(), &ds->n_splats, f->n_max, cp.tiles_x, tcount,
+                          reinterpret_cast<uint32_t*>(sc + L.rowdiff), s);
+    hs::launch_tile_plan(tcount, reinterpret_cast<uint32_t*>(sc + L.rowdiff), cp.tiles_x, cp.tiles_y, f->cap_dup,
+                         f->ranges.as<uint2>(), reinterpret_cast<uint32_t*>(sc + L.cursor),
+                         f->tile_order.as<uint32_t>(), reinterpret_cast<uint2*>(sc + L.prange),
+                         reinterpret_cast<uint32_t*>(sc + L.big_list), reinterpret_cast<uint2*>(sc + L.extra), plan,
+                         &ds->n_dup, &ds->sort_n, &ds->overflows,
+                         s);
     uint32_t* kb[2] = {f->keys[0].as<uint32_t>(), f->keys[1].as<uint32_t>()};
     uint32_t* vb[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
-    hs::launch_duplicate_sorted(ids, f->dinfo.as<uint4>(), f->proj.as<ProjRec>(), f->offsets.as<uint32_t>(),
-                                &ds->n_visible_sorted, f->n_max, &ds->sort_n, f->cap_dup, cp.tiles_x, kb[0], vb[0],
-                                f->huge.as<uint2>(), reinterpret_cast<uint32_t*>(sc + L.huge_counter), s);
-    if (ctx->debug) {
-        hs::launch_make_keys(kb[0], vb[0], f->dinfo.as<uint4>(), &ds->sort_n, f->cap_dup, f->dupk.as<uint64_t>(), s);
-        HS_CUDA(ctx, cudaMemcpyAsync(f->dupv.p, f->vals[0].p, f->cap_dup * 4, cudaMemcpyDeviceToDevice, s));
-    }
-    hs::launch_radix_sort(kb, vb, &ds->sort_n, f->cap_dup, 8, f->passes, tile_bits(cp.tiles_x * cp.tiles_y),
-                          reinterpret_cast<uint32_t*>(sc + L.tile_sort),
-                          s);
+    uint8_t* bm = f->bmask.as<uint8_t>();
+    hs::launch_bucket(f->dupcount.as<uint32_t>(), f->dinfo.as<uint4>(), f->proj.as<ProjRec>(), &ds->n_splats, f->n_max,
+                      &ds->sort_n, cp.tiles_x, reinterpret_cast<uint32_t*>(sc + L.cursor), kb[1], vb[1], bm,
+                      f->huge.as<uint32_t>(), reinterpret_cast<uint32_t*>(sc + L.huge_counter),
+                      ctx->debug ? f->dupk.as<uint64_t>() : nullptr, ctx->debug ? f->dupv.as<uint32_t>() : nullptr, s);
+    hs::launch_tile_sort(f->tile_order.as<uint32_t>(), reinterpret_cast<uint2*>(sc + L.prange),
+                         reinterpret_cast<uint32_t*>(sc + L.big_list), reinterpret_cast<uint2*>(sc + L.extra), plan, &ds->sort_n, tiles, kb[1], vb[1], bm, kb[0], vb[0], f->mkeys.as<uint32_t>(),
+                         f->mvals.as<uint32_t>(), bm + f->cap_dup,
+                         reinterpret_cast<uint32_t*>(sc + L.done), reinterpret_cast<uint32_t*>(sc + L.task_counter), s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[3], s));
-    const int fin = f->passes & 1;
-    hs::launch_ranges(kb[fin], &ds->sort_n, f->cap_dup, f->ranges.as<uint2>(), s);
+    const int fin = 0;
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[4], s));
-    hs::launch_tile_order(f->ranges.as<uint2>(), cp.tiles_x * cp.tiles_y, &ds->sort_n, f->tile_order.as<uint32_t>(), s);
     hs::launch_blend(ctx->blend_mode, ctx->stats, f->ranges.as<uint2>(), kb[fin], vb[fin], f->proj.as<ProjRec>(), &ds->sort_n, cp,
                      f->color.as<float>(), f->depth.as<float>(), f->trans.as<float>(), f->touched.as<uint8_t>(),
                      &ds->n_eval, reinterpret_cast<uint32_t*>(sc + L.blend_counter), f->tile_order.as<uint32_t>(),
@@ -1681,6 +1675,29 @@ extern "C" hs_status hs_project(hs_context* ctx, const hs_splat_soa* splats, uin
     return copy_sync(ctx, out, o.p, n * sizeof(hs_projected), cudaMemcpyDeviceToHost);
 }
 
+// The global stable depth order of the visible splats (render.hpp:268-272,
+// ForwardContext::order) of frame f's last render, built on request: the frame
+// path itself only needs the per-tile lists.  Stream-ordered on f's lane.
+static hs_status build_depth_order(hs_context* ctx, hs_frame* f) {
+    if (f->order_ready) return HS_OK;
+    cudaStream_t s = frame_stream(ctx, f);
+    const ScratchLayout L = scratch_layout(std::max<uint64_t>(f->cap_splats, 1), f->cap_dup, f->tiles_x, f->tiles_y);
+    unsigned char* sc = f->scratch.as<unsigned char>();
+    DevStats* ds = f->stats.as<DevStats>();
+    HS_CUDA(ctx, cudaMemsetAsync(sc + L.vis_counter, 0, L.depth_zero_end - L.vis_counter, s));
+    uint32_t* zk[2] = {f->zkeys[0].as<uint32_t>(), f->zkeys[1].as<uint32_t>()};
+    uint32_t* zv[2] = {f->zvals[0].as<uint32_t>(), f->zvals[1].as<uint32_t>()};
+    hs::launch_compact_visible(f->dupcount.as<uint32_t>(), f->dinfo.as<uint4>(), &ds->n_splats, f->n_max, zk[0], zv[0],
+                               reinterpret_cast<uint64_t*>(sc + L.vis_status),
+                               reinterpret_cast<uint32_t*>(sc + L.vis_counter), &ds->n_visible_sorted,
+                               reinterpret_cast<uint32_t*>(sc + L.depth_sort), s);
+    hs::launch_radix_sort(zk, zv, &ds->n_visible_sorted, f->n_max, 0, 4, 32,
+                          reinterpret_cast<uint32_t*>(sc + L.depth_sort), s, /*hist_ready=*/true);
+    HS_CUDA(ctx, cudaGetLastError());
+    f->order_ready = true;  // 4 passes: the order is back in zvals[0]
+    return HS_OK;
+}
+
 extern "C" hs_status hs_render_reference(hs_context* ctx, const hs_splat_soa* splats, uint64_t n,
                                          const hs_camera* cam, hs_frame* f) {
     if (!ctx || !cam || !f || (n && !splats)) return HS_INVALID_ARGUMENT;
@@ -1693,6 +1710,7 @@ extern "C" hs_status hs_render_reference(hs_context* ctx, const hs_splat_soa* sp
     // then the naive per-pixel walk over the whole sorted list, replacing the tiled images
     cudaStream_t s = frame_stream(ctx, f);
     DevStats* ds = f->stats.as<DevStats>();
+    HS_TRY(build_depth_order(ctx, f));
     HS_CUDA(ctx, cudaMemsetAsync(&ds->rendered, 0, 8, s));
     hs::launch_blend_naive(f->proj.as<ProjRec>(), f->dinfo.as<uint4>(), f->zvals[0].as<uint32_t>(),
                            &ds->n_visible_sorted, f->cam, f->color.as<float>(), f->depth.as<float>(),
@@ -1712,8 +1730,12 @@ extern "C" hs_status hs_frame_order(hs_context* ctx, hs_frame* f, uint32_t* orde
     hs_status s = finish_frame(ctx, f, false);
     if (s != HS_OK) return s;
     if (!f->have_result) return set_err(ctx, HS_MISSING_FORWARD_STATE, "frame has not been rendered");
-    const uint64_t v = f->h_stats->n_visible_sorted;
+    const uint64_t v = f->h_stats->n_visible;
     *n = v;
-    if (order && v) HS_TRY(copy_sync(ctx, order, f->zvals[0].p, v * 4, cudaMemcpyDeviceToHost));
+    if (order && v) {
+        HS_TRY(build_depth_order(ctx, f));
+        HS_CUDA(ctx, cudaStreamSynchronize(frame_stream(ctx, f)));
+        HS_TRY(copy_sync(ctx, order, f->zvals[0].p, v * 4, cudaMemcpyDeviceToHost));
+    }
     return HS_OK;
 }

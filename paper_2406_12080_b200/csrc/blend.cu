@@ -7,7 +7,7 @@
 // tail of one long tile.  A warp walks its tile's depth-sorted range 32
 // entries at a time:
 //   1. each lane reads one key; its low byte says which of the tile's blocks the
-//      splat's alpha can reach (k_reach_masks) -- entries that cannot touch this
+//      splat's alpha can reach (k_bucket, tile_reach_mask) -- entries that cannot touch this
 //      block are ones the reference `continue`s past at every pixel of it, and
 //      are never staged.  The others' 64-byte records are staged in shared
 //      memory with cp.async, one batch ahead;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
         float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, d = 0.0f;
         bool done = !inside;
         // The sorted keys carry, in their low 8 bits, which of the tile's 8 blocks each
-        // entry can reach (k_reach_masks, tile_reach_mask): entries that cannot touch
+        // entry can reach (k_bucket, tile_reach_mask): entries that cannot touch
         // this block are ones the reference `continue`s past at every pixel of it.
         // Phase A scans a segment of the tile's keys (4 loads of 32 in flight) and
         // compacts the ids of this block's entries, in depth order, into the warp's

@@ -1,0 +1,1114 @@
+// bucket.cu — per-tile depth order of the visible splats (render.hpp:262-294)
+// by tile bucketing and an in-tile sort, with no global sort pass.
+//
+// The reference stable-sorts the visible splats by camera-space z (ties keep
+// cut order) and then buckets them into tiles preserving that order, so each
+// tile's list is its entries ordered by (bits(z), cut index) -- a unique key.
+// The device builds exactly those lists:
+//   k_tile_count   per-tile entry counts.  Each CTA takes 256 consecutive cut
+//                  entries at a time; cut order is spatially coherent, so their
+//                  (splat, tile) pairs fall on few tiles: they are summed in a
+//                  shared-memory hash table and flushed with one global atomic
+//                  per distinct tile (the hottest C2 tile sees ~190 instead of
+//                  ~15K same-address atomics).  Footprints of more than 8 tiles
+//                  add +1 / -1 row difference marks instead (same table).
+//   k_tile_plan    one CTA: per-tile sizes -> tile ranges (tile_start), bucket
+//                  cursors, D and the capacity check, the heavy-first tile
+//                  order and the sort task table
+//   k_bucket       every (splat, tile) pair to a slot of its tile's bucket:
+//                  block-local ranks from the same shared hash table, one
+//                  global cursor atomic per (block, tile); the reach mask
+//                  (tile_reach_mask) is computed from the splat in registers.
+//                  Footprints of 5..1024 tiles are emitted by the whole warp,
+//                  larger ones by one CTA each (k_bucket_huge).
+//   k_tile_sort    persistent CTAs (1024 threads, one per SM), heavy tiles
+//                  first: a tile of <= 16384 entries is sorted by bits(z) with
+//                  an LSD radix sort in shared memory (8-bit digits, warps rank
+//                  with match.any, 16-bit local indices as payload, bytes equal
+//                  in every key skipped), equal depths are put in cut order
+//                  afterwards; tiles of <= 510 entries are sorted one per warp,
+//                  32 per task; larger tiles are sorted in 16384-entry chunks
+//                  and merged (merge path) once their chunks are done.
+// Output: keys[i] = tile << 8 | reach mask, vals[i] = splat id, in tile order and
+// within a tile in the reference's depth order -- the tile_entries of
+// render.hpp:285-294 bit for bit; ranges[t] = [tile_start[t], tile_start[t+1]).
+#include "hs_device.cuh"
+#include "hs_kernels.h"
+#include "hs_scan.cuh"
+
+namespace hs {
+
+constexpr uint32_t kTileCap = 16384;  // entries one CTA sorts in shared memory
+constexpr int kTsThreads = 1024, kTsWarps = kTsThreads / 32;
+constexpr int kMaxItems = kTileCap / kTsThreads;  // 16 keys per thread (CTA sort) or per lane (warp sort)
+constexpr uint32_t kWarpCap = 32 * kMaxItems;     // per-warp sort capacity (small tiles)
+constexpr uint32_t kSmallMax = 510;   // tiles up to this size are sorted per warp (n + 1 < 512)
+constexpr int kCountDirect = 8;       // k_tile_count: larger footprints use row difference marks
+constexpr int kBigArea = 4;           // k_bucket: larger footprints are emitted by the whole warp
+constexpr int kHugeArea = 1024;       // larger still: one CTA per splat (k_bucket_huge)
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+constexpr uint32_t kMarkBit = 0x80000000u;  // hash keys of row difference marks
+
+// ------------------------------------------------------------------ shared hash table
+// Open addressing over kSlots (key, value) pairs; `used` lists the occupied
+// slots so flushes and resets touch only those.
+template <int kLog>
+struct HashTab {
+    static constexpr int kSlots = 1 << kLog;
+    uint32_t key[kSlots];
+    uint32_t val[kSlots];
+    uint16_t used[kSlots];
+    uint32_t n_used;
+};
+
+template <int kLog>
+__device__ __forceinline__ void hash_init(HashTab<kLog>& h) {
+    for (int i = threadIdx.x; i < HashTab<kLog>::kSlots; i += blockDim.x) h.key[i] = kEmpty, h.val[i] = 0;
+    if (threadIdx.x == 0) h.n_used = 0;
+}
+// Slot of `key`, inserted if absent; -1 when the probe limit is hit (the caller
+// then falls back to a global atomic).
+template <int kLog>
+__device__ __forceinline__ int hash_slot(HashTab<kLog>& h, uint32_t key) {
+    uint32_t s = (key * 0x9E3779B1u) >> (32 - kLog);
+    volatile uint32_t* vk = h.key;
+    for (int p = 0; p < 32; ++p) {
+        const uint32_t k = vk[s];
+        if (k == key) return (int)s;
+        if (k == kEmpty) {
+            const uint32_t old = atomicCAS(&h.key[s], kEmpty, key);
+            if (old == kEmpty) {
+                h.used[atomicAdd(&h.n_used, 1u)] = (uint16_t)s;
+                return (int)s;
+            }
+            if (old == key) return (int)s;
+        }
+        s = (s + 1) & (HashTab<kLog>::kSlots - 1);
+    }
+    return -1;
+}
+// Warp-aggregated add of `add` per lane with `has` to `key` (all 32 lanes call):
+// lanes with the same key share one table update.  Returns the lane's running
+// value before its own add (the block-local rank when add = 1) and its slot; a
+// slot of -1 means the table was full and the add went to global_fallback[key]
+// directly (the return value is then the global one).
+template <int kLog>
+__device__ __forceinline__ uint32_t hash_add(HashTab<kLog>& h, bool has, uint32_t key, uint32_t add, int& slot,
+                                             uint32_t* __restrict__ global_fallback) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t k = has ? key : kEmpty;
+    const uint32_t peers = __match_any_sync(0xffffffffu, k);
+    const int leader = __ffs(peers) - 1;
+    const uint32_t n_peers = __popc(peers);
+    uint32_t base = 0;
+    int sl = -1;
+    if (has && lane == leader) {
+        sl = hash_slot(h, key);
+        if (sl >= 0) base = atomicAdd(&h.val[sl], add * n_peers);
+        else base = atomicAdd(&global_fallback[key & ~kMarkBit], add * n_peers);
+    }
+    sl = __shfl_sync(0xffffffffu, sl, leader);
+    base = __shfl_sync(0xffffffffu, base, leader);
+    slot = sl;
+    return base + add * __popc(peers & ((1u << lane) - 1u));
+}
+// Flush and clear the occupied slots: fn(key, value) per slot (block-wide; ends
+// with the table empty and a barrier).
+template <int kLog, typename Fn>
+__device__ __forceinline__ void hash_drain(HashTab<kLog>& h, Fn fn) {
+    for (uint32_t u = threadIdx.x; u < h.n_used; u += blockDim.x) {
+        const int sl = h.used[u];
+        fn(h.key[sl], h.val[sl]);
+        h.key[sl] = kEmpty;
+        h.val[sl] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) h.n_used = 0;
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ count
+// tcount[t] += entries of tile t; rowdiff[row * (tiles_x + 1) + x] += +1 / -1 at
+// the ends of every tile row crossed by a footprint of more than 8 tiles.
+__global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__ dupcount,
+                                                    const uint4* __restrict__ dinfo, const uint64_t* __restrict__ n_ptr,
+                                                    int tiles_x, uint32_t* __restrict__ tcount,
+                                                    uint32_t* __restrict__ rowdiff) {
+    __shared__ HashTab<11> h;  // 256 entries x <= 8 tiles
+    const uint64_t n = *n_ptr;
+    const int W = tiles_x + 1;
+    hash_init(h);
+    __syncthreads();
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = base + threadIdx.x;
+        const uint32_t cnt = i < n ? dupcount[i] : 0u;
+        int tx0 = 0, tx1 = 0, ty0 = 0, ty1 = 0;
+        if (cnt) {
+            const uint4 di = dinfo[i];
+            tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
+        }
+        const int w = max(tx1 - tx0, 1);
+        const bool direct = cnt != 0 && cnt <= (uint32_t)kCountDirect;
+        int slot;
+        for (int k = 0; k < kCountDirect; ++k) {
+            const bool has = direct && (uint32_t)k < cnt;
+            if (!__any_sync(0xffffffffu, has)) break;
+            const uint32_t tile = (uint32_t)((ty0 + k / w) * tiles_x + tx0 + k % w);
+            hash_add(h, has, tile, 1u, slot, tcount);
+        }
+        // large footprints: +1 at (row, tx0), -1 at (row, tx1) for every row
+        const bool marks = cnt > (uint32_t)kCountDirect;
+        for (int r = 0; __any_sync(0xffffffffu, marks && ty0 + r < ty1); ++r) {
+            const bool has = marks && ty0 + r < ty1;
+            const uint32_t row = (uint32_t)(ty0 + r) * W;
+            hash_add(h, has, kMarkBit | (row + tx0), 1u, slot, rowdiff);
+            hash_add(h, has, kMarkBit | (row + tx1), 0xFFFFFFFFu, slot, rowdiff);
+        }
+        __syncthreads();
+        hash_drain(h, [&](uint32_t key, uint32_t v) {
+            if (key & kMarkBit) atomicAdd(&rowdiff[key & ~kMarkBit], v);
+            else atomicAdd(&tcount[key], v);
+        });
+    }
+}
+
+// ------------------------------------------------------------------ plan
+// One CTA of 1024 threads; per-tile sizes in shared memory (dynamic, 4 B per tile).
+// Heavy-first position p holds tile order[p] with bucket range prange[p].
+// plan[] = {CTA-sorted tiles (= first per-warp position), tiles larger than
+// kTileCap (big_list: their positions, merged), their further chunks (extra:
+// (position, chunk)), non-empty tiles}.
+__global__ void __launch_bounds__(1024) k_tile_plan(const uint32_t* __restrict__ tcount,
+                                                    const uint32_t* __restrict__ rowdiff, int tiles_x, int tiles_y,
+                                                    uint64_t cap_dup, uint2* __restrict__ ranges,
+                                                    uint32_t* __restrict__ cursor, uint32_t* __restrict__ order,
+                                                    uint2* __restrict__ prange, uint32_t* __restrict__ big_list,
+                                                    uint2* __restrict__ extra, uint32_t* __restrict__ plan,
+                                                    uint64_t* __restrict__ n_dup,
+                                                    uint64_t* __restrict__ sort_n,
+                                                    unsigned long long* __restrict__ overflows) {
+    extern __shared__ uint32_t s_n[];  // [tiles]
+    __shared__ uint64_t s_w64[32];
+    __shared__ uint32_t s_hist[33], s_offs[33], s_nbig;
+    __shared__ uint64_t s_total;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tiles = tiles_x * tiles_y;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int t = tid; t < tiles; t += 1024) s_n[t] = tcount[t];
+    if (tid < 33) s_hist[tid] = 0;
+    if (tid == 0) s_nbig = 0;
+    __syncthreads();
+    // 1. large footprints: prefix of each row's difference marks
+    const int W = tiles_x + 1;
+    for (int row = warp; row < tiles_y; row += 32) {
+        uint32_t carry = 0;
+        for (int base = 0; base < tiles_x; base += 32) {
+            const int x = base + lane;
+            uint32_t incl = x < tiles_x ? rowdiff[(size_t)row * W + x] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (x < tiles_x) s_n[row * tiles_x + x] += carry + incl;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    __syncthreads();
+    // 2. exclusive scan of the sizes in tile order (contiguous items per thread)
+    const int E = (tiles + 1023) / 1024;
+    const int t0 = tid * E;
+    uint64_t local = 0;
+    for (int k = 0; k < E; ++k)
+        if (t0 + k < tiles) local += s_n[t0 + k];
+    uint64_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w64[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint64_t w = s_w64[lane];
+        uint64_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_w64[lane] = wi - w;
+        if (lane == 31) s_total = wi;
+    }
+    __syncthreads();
+    const uint64_t D = s_total;
+    const bool fits = D != 0 && D <= cap_dup;
+    if (tid == 0) {
+        *n_dup = D;
+        *sort_n = fits ? D : 0;
+        if (D > cap_dup) atomicAdd(overflows, 1ull);
+    }
+    uint64_t run = s_w64[warp] + incl - local;
+    for (int k = 0; fits && k < E; ++k) {
+        const int t = t0 + k;
+        if (t >= tiles) break;
+        const uint32_t c = s_n[t];
+        ranges[t] = make_uint2((uint32_t)run, (uint32_t)(run + c));
+        cursor[t] = (uint32_t)run;
+        run += c;
+    }
+    // 3. heavy-first order: log2 buckets of the size, warp-aggregated bucket atomics
+    //    (always written: the blend walks every tile, also when nothing is visible)
+    const int span = (tiles + 31) & ~31;
+    for (int t = tid; t < span; t += blockDim.x) {
+        const bool valid = t < tiles;
+        const uint32_t c = valid ? s_n[t] : 0u;
+        const uint32_t bkt = valid ? (uint32_t)__clz(c + 1u) : 64u;  // fewer leading zeros = heavier = earlier
+        const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
+        if (valid && (peers & lt) == 0) atomicAdd(&s_hist[bkt], (uint32_t)__popc(peers));
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t r = 0;
+        for (int b = 0; b < 33; ++b) {
+            if (b == 23) plan[0] = r;  // sizes with n + 1 < 512 (per-warp sorts) start here
+            if (b == 31) plan[3] = r;  // empty tiles start here
+            s_offs[b] = r, r += s_hist[b];
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < span; t += blockDim.x) {
+        const bool valid = t < tiles;
+        const uint32_t c = valid ? s_n[t] : 0u;
+        const uint32_t bkt = valid ? (uint32_t)__clz(c + 1u) : 64u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (valid && lane == leader) base = atomicAdd(&s_offs[bkt], (uint32_t)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (valid) {
+            const uint32_t p = base + __popc(peers & lt);
+            order[p] = (uint32_t)t;
+        }
+    }
+    __syncthreads();
+    if (!fits) {
+        if (tid == 0) plan[0] = plan[1] = plan[3] = plan[4] = 0;
+        return;
+    }
+    // 4. per position: bucket range; tiles of more than one chunk listed for the merge
+    __shared__ uint32_t s_nextra;
+    if (tid == 0) s_nextra = 0;
+    __syncthreads();
+    const uint32_t nonempty = plan[3];
+    for (uint32_t p = tid; p < nonempty; p += blockDim.x) {
+        const uint32_t t = order[p];
+        const uint2 rg = ranges[t];
+        prange[p] = rg;
+        const uint32_t R = (rg.y - rg.x + kTileCap - 1) / kTileCap;
+        if (R > 1) {
+            big_list[atomicAdd(&s_nbig, 1u)] = p;
+            const uint32_t e0 = atomicAdd(&s_nextra, R - 1);
+            for (uint32_t k = 1; k < R; ++k) extra[e0 + k - 1] = make_uint2(p, k);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        plan[1] = s_nbig;
+        plan[4] = s_nextra;
+    }
+}
+
+// ------------------------------------------------------------------ bucket
+__device__ __forceinline__ void put_entry(uint32_t pos, uint32_t tile, uint32_t id, uint32_t zb, uint32_t mask,
+                                          uint32_t* __restrict__ zk, uint32_t* __restrict__ ids,
+                                          uint8_t* __restrict__ bm, uint64_t* __restrict__ dbg_keys,
+                                          uint32_t* __restrict__ dbg_vals) {
+    zk[pos] = zb;
+    ids[pos] = id;
+    bm[pos] = (uint8_t)mask;
+    if (dbg_keys) {
+        dbg_keys[pos] = ((uint64_t)tile << 32) | zb;
+        dbg_vals[pos] = id;
+    }
+}
+
+// Per block of 256 consecutive cut entries: (1) small footprints (<= 4 tiles)
+// get block-local ranks per tile from the shared table and are listed as
+// (tile, rank, slot, splat) pairs with the splat's record staged in shared
+// memory; (2) one cursor atomic per distinct tile reserves the block's range of
+// each tile's bucket; (3) all threads write the listed pairs densely (reach mask
+// + entry); (4) larger footprints are emitted by the whole warp, huge ones
+// queued for k_bucket_huge.
+struct BucketPair {
+    uint32_t rank;
+    int16_t slot;
+    uint16_t local;
+    uint16_t tx, ty;
+};
+__global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ dupcount, const uint4* __restrict__ dinfo,
+                                                const ProjRec* __restrict__ proj, const uint64_t* __restrict__ n_ptr,
+                                                const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
+                                                uint32_t* __restrict__ cursor, uint32_t* __restrict__ zk,
+                                                uint32_t* __restrict__ ids, uint8_t* __restrict__ bm,
+                                                uint32_t* __restrict__ huge_q, uint32_t* __restrict__ huge_n,
+                                                uint64_t* __restrict__ dbg_keys, uint32_t* __restrict__ dbg_vals) {
+    __shared__ HashTab<10> h;  // 256 entries x <= 4 tiles
+    __shared__ BucketPair s_pair[256 * kBigArea];
+    __shared__ float4 s_rec[256][3];  // p0, p1, p3 of the block's small footprints
+    __shared__ uint32_t s_z[256], s_npairs;
+    if (*sort_n_ptr == 0) return;  // nothing visible, or over capacity
+    const uint64_t n = *n_ptr;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    hash_init(h);
+    if (tid == 0) s_npairs = 0;
+    __syncthreads();
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = base + tid;
+        {   // the next block's records travel to L2 while this block is processed
+            const uint64_t nx = i + (uint64_t)gridDim.x * blockDim.x;
+            if (nx < n) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(dupcount + nx));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(dinfo + nx));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(proj + nx));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(proj + nx) + 32));
+            }
+        }
+        const uint32_t cnt = i < n ? dupcount[i] : 0u;
+        uint4 di = make_uint4(0, 0, 0, 0);
+        if (cnt) di = dinfo[i];
+        const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff;
+        const int w = max(tx1 - tx0, 1);
+        const bool small = cnt != 0 && cnt <= (uint32_t)kBigArea;
+        const bool big = cnt > (uint32_t)kBigArea && cnt <= (uint32_t)kHugeArea;
+        float4 p0 = make_float4(0, 0, 0, 0), p1 = p0, p3 = p0;
+        if (small || big) {
+            const ProjRec* r = proj + i;
+            p0 = r->p0, p1 = r->p1, p3 = r->p3;
+        }
+        if (small) {
+            s_rec[tid][0] = p0, s_rec[tid][1] = p1, s_rec[tid][2] = p3;
+            s_z[tid] = di.z;
+        }
+        // 1. block-local ranks, pairs listed warp by warp
+        {
+            const uint32_t np = small ? cnt : 0u;
+            uint32_t incl = np;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            uint32_t wbase = 0;
+            if (lane == 31 && incl) wbase = atomicAdd(&s_npairs, incl);
+            wbase = __shfl_sync(0xffffffffu, wbase, 31);
+            uint32_t q = wbase + incl - np;
+#pragma unroll
+            for (int k = 0; k < kBigArea; ++k) {
+                const bool has = small && (uint32_t)k < cnt;
+                if (!__any_sync(0xffffffffu, has)) break;
+                const uint32_t tile = (uint32_t)((ty0 + k / w) * tiles_x + tx0 + k % w);
+                int slot;
+                const uint32_t rank = hash_add(h, has, tile, 1u, slot, cursor);
+                if (has)
+                    s_pair[q++] = BucketPair{rank, (int16_t)slot, (uint16_t)tid, (uint16_t)(tx0 + k % w),
+                                             (uint16_t)(ty0 + k / w)};
+            }
+        }
+        __syncthreads();
+        // 2. one cursor atomic per (block, tile): the slot's value becomes its base
+        for (uint32_t u = tid; u < h.n_used; u += blockDim.x) {
+            const int sl = h.used[u];
+            h.val[sl] = atomicAdd(&cursor[h.key[sl]], h.val[sl]);
+        }
+        __syncthreads();
+        // 3. the listed pairs, all threads busy
+        const uint32_t npairs = s_npairs;
+        for (uint32_t q = tid; q < npairs; q += blockDim.x) {
+            const BucketPair pr = s_pair[q];
+            const uint32_t pos = pr.slot >= 0 ? h.val[pr.slot] + pr.rank : pr.rank;
+            const uint32_t mask = tile_reach_mask(s_rec[pr.local][0], s_rec[pr.local][1], s_rec[pr.local][2],
+                                                  pr.tx * kTile, pr.ty * kTile);
+            put_entry(pos, (uint32_t)pr.ty * tiles_x + pr.tx, (uint32_t)(base + pr.local), s_z[pr.local], mask, zk,
+                      ids, bm, dbg_keys, dbg_vals);
+        }
+        // 4. huge footprints: one queue slot each (k_bucket_huge)
+        const bool huge = cnt > (uint32_t)kHugeArea;
+        const uint32_t hm = __ballot_sync(0xffffffffu, huge);
+        if (hm) {
+            uint32_t q = 0;
+            if (lane == __ffs(hm) - 1) q = atomicAdd(huge_n, (uint32_t)__popc(hm));
+            q = __shfl_sync(0xffffffffu, q, __ffs(hm) - 1) + __popc(hm & lt);
+            if (huge) huge_q[q] = (uint32_t)i;
+        }
+        // 5. larger footprints: the whole warp emits one splat's tiles (distinct tiles per instruction)
+        for (uint32_t m = __ballot_sync(0xffffffffu, big); m; m &= m - 1) {
+            const int src = __ffs(m) - 1;
+            const uint32_t sid = (uint32_t)(base + (tid & ~31) + src);
+            const uint32_t sa = __shfl_sync(0xffffffffu, cnt, src), sz = __shfl_sync(0xffffffffu, di.z, src);
+            const int sx0 = __shfl_sync(0xffffffffu, tx0, src), sy0 = __shfl_sync(0xffffffffu, ty0, src);
+            const int sw = __shfl_sync(0xffffffffu, w, src);
+            float4 q0, q1, q3;
+            q0.x = __shfl_sync(0xffffffffu, p0.x, src), q0.y = __shfl_sync(0xffffffffu, p0.y, src);
+            q0.z = __shfl_sync(0xffffffffu, p0.z, src), q0.w = __shfl_sync(0xffffffffu, p0.w, src);
+            q1.x = __shfl_sync(0xffffffffu, p1.x, src), q1.y = __shfl_sync(0xffffffffu, p1.y, src);
+            q1.z = __shfl_sync(0xffffffffu, p1.z, src), q1.w = __shfl_sync(0xffffffffu, p1.w, src);
+            q3.x = __shfl_sync(0xffffffffu, p3.x, src), q3.y = __shfl_sync(0xffffffffu, p3.y, src);
+            q3.z = __shfl_sync(0xffffffffu, p3.z, src), q3.w = __shfl_sync(0xffffffffu, p3.w, src);
+            for (uint32_t t = lane; t < sa; t += 32) {
+                const int tx = sx0 + (int)(t % sw), ty = sy0 + (int)(t / sw);
+                const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
+                const uint32_t pos = atomicAdd(&cursor[tile], 1u);
+                const uint32_t mask = tile_reach_mask(q0, q1, q3, tx * kTile, ty * kTile);
+                put_entry(pos, tile, sid, sz, mask, zk, ids, bm, dbg_keys, dbg_vals);
+            }
+        }
+        // reset the table and the pair list for the next block
+        __syncthreads();
+        if (tid == 0) s_npairs = 0;
+        hash_drain(h, [](uint32_t, uint32_t) {});
+    }
+}
+
+// Splats covering more than kHugeArea tiles (e.g. skybox splats near the image
+// plane: the reference culls only at z <= 0.01), one CTA each.
+__global__ void __launch_bounds__(256) k_bucket_huge(const uint4* __restrict__ dinfo, const ProjRec* __restrict__ proj,
+                                                     const uint32_t* __restrict__ huge_q,
+                                                     const uint32_t* __restrict__ huge_n,
+                                                     const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
+                                                     uint32_t* __restrict__ cursor, uint32_t* __restrict__ zk,
+                                                     uint32_t* __restrict__ ids, uint8_t* __restrict__ bm,
+                                                     uint64_t* __restrict__ dbg_keys, uint32_t* __restrict__ dbg_vals) {
+    if (*sort_n_ptr == 0) return;
+    const uint32_t nq = *huge_n;
+    for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
+        const uint32_t id = huge_q[q];
+        const uint4 di = dinfo[id];
+        const ProjRec* r = proj + id;
+        const float4 p0 = r->p0, p1 = r->p1, p3 = r->p3;
+        const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
+        const uint32_t w = (uint32_t)(tx1 - tx0), area = w * (uint32_t)(ty1 - ty0);
+        for (uint32_t t = threadIdx.x; t < area; t += blockDim.x) {
+            const int tx = tx0 + (int)(t % w), ty = ty0 + (int)(t / w);
+            const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
+            const uint32_t pos = atomicAdd(&cursor[tile], 1u);
+            const uint32_t mask = tile_reach_mask(p0, p1, p3, tx * kTile, ty * kTile);
+            put_entry(pos, tile, id, di.z, mask, zk, ids, bm, dbg_keys, dbg_vals);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ in-tile sort
+struct TileBufs {
+    uint32_t *zA, *iA;  // bucketed (bits(z), id, mask); merge ping-pong buffer
+    uint8_t* mA;
+    uint32_t *zB, *iB;  // final (tile << 8 | mask, id)
+    uint32_t *zC, *iC;  // sorted chunks of tiles larger than kTileCap; merge ping-pong buffer
+    uint8_t* mC;
+};
+
+// (merge reads go to L2: the chunks were written by other CTAs during this launch)
+__device__ __forceinline__ uint64_t key_at(const uint32_t* z, const uint32_t* id, uint32_t x) {
+    return ((uint64_t)__ldcg(z + x) << 32) | __ldcg(id + x);
+}
+__device__ __forceinline__ int ceil_log2(uint32_t v) { return v <= 1 ? 0 : 32 - __clz(v - 1); }
+
+// Shared memory of k_tile_sort: one CTA-wide sort (<= 16384 entries) or 32
+// per-warp sorts (<= 512 entries each) over the same bytes.  Keys and 16-bit
+// local indices ping-pong between two buffers; digit counters are 16-bit halves
+// of 32-bit words (two digits per word, bumped with 32-bit shared atomics).
+struct CtaSort {
+    uint32_t key[2][kTileCap];
+    uint16_t idx[2][kTileCap];
+    uint32_t cnt[kTsWarps][128];  // LSD: digit d of warp w = halfword d of row w; MSD: 4096 u32 buckets
+    uint32_t part[kTsWarps / 8][256];
+    uint32_t wsum[8];
+};
+struct WarpSort {
+    uint32_t key[2][kWarpCap];
+    uint16_t idx[2][kWarpCap];
+    uint32_t cnt[1][128];  // LSD: 256 16-bit digit counters; MSD: 128 u32 buckets
+};
+static_assert(sizeof(WarpSort) * kTsWarps <= sizeof(CtaSort), "per-warp slices fit the CTA layout");
+constexpr size_t kTileSortSmem = sizeof(CtaSort);
+
+__device__ __forceinline__ uint16_t* half_row(uint32_t* row) { return reinterpret_cast<uint16_t*>(row); }
+
+// One stable LSD pass over the byte at `shift` (buffers cur -> cur ^ 1), by the G
+// warps of a sort group (this warp is gw).  Element order = position: warp w
+// owns positions [w E 32, (w + 1) E 32), item k of lane l at w E 32 + k 32 + l.
+// Ranking as in the onesweep passes (sort.cu): peers by eight bit-sliced
+// ballots, the lowest peer bumps the warp's digit counter with one shared
+// atomic (program order keeps the items in order); the scan in (digit, warp)
+// order gives stable destinations.
+template <int G, typename S>
+__device__ __forceinline__ void radix_pass(S& sm, int E, int shift, int gw, int cur) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t* mc = sm.cnt[gw];
+    for (int d = lane; d < 128; d += 32) mc[d] = 0;
+    const int b0 = gw * E * 32 + lane;
+    const uint32_t* kin = sm.key[cur];
+    uint32_t ranks[kMaxItems / 2];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kMaxItems; ++k) {
+        if (k >= E) break;
+        const uint32_t d = (kin[b0 + k * 32] >> shift) & 0xffu;
+        uint32_t peers = 0xffffffffu;
+#pragma unroll
+        for (int bt = 0; bt < 8; ++bt) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, (d >> bt) & 1u);
+            peers &= ((d >> bt) & 1u) ? bal : ~bal;
+        }
+        const int leader = __ffs(peers) - 1;
+        const int hs = 16 * (d & 1);
+        uint32_t old = 0;
+        if (lane == leader) old = atomicAdd(&mc[d >> 1], (uint32_t)__popc(peers) << hs) >> hs;
+        old = __shfl_sync(0xffffffffu, old, leader) & 0xffffu;
+        const uint32_t r = old + __popc(peers & lt);
+        if (k & 1) ranks[k >> 1] |= r << 16; else ranks[k >> 1] = r;
+    }
+    if constexpr (G > 1) {
+        // exclusive offsets in (digit, warp) order: thread (group g, digit d) scans
+        // warps [8 g, 8 g + 8); then digit totals and group prefixes
+        __syncthreads();
+        const int tid = threadIdx.x, d = tid & 255, g = tid >> 8;
+        uint32_t part = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            uint16_t* c16 = half_row(sm.cnt[8 * g + w]);
+            const uint32_t c = c16[d];
+            c16[d] = (uint16_t)part;
+            part += c;
+        }
+        sm.part[g][d] = part;
+        __syncthreads();
+        if (tid < 256) {
+            uint32_t tot = 0;
+#pragma unroll
+            for (int q = 0; q < G / 8; ++q) {
+                const uint32_t c = sm.part[q][d];
+                sm.part[q][d] = tot;
+                tot += c;
+            }
+            uint32_t incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) sm.wsum[tid >> 5] = incl;
+            part = incl - tot;  // digit base, exclusive over digits (completed below)
+        }
+        __syncthreads();
+        if (tid < 256) {
+            uint32_t base = part;
+            for (int w = 0; w < (tid >> 5); ++w) base += sm.wsum[w];
+#pragma unroll
+            for (int q = 0; q < G / 8; ++q) sm.part[q][d] += base;
+        }
+        __syncthreads();
+        const uint32_t gb = sm.part[g][d];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) half_row(sm.cnt[8 * g + w])[d] += (uint16_t)gb;
+        __syncthreads();
+    } else {
+        // one warp: 8 digits per lane
+        __syncwarp();
+        uint16_t* c16 = half_row(mc);
+        uint32_t v[8], tot = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = c16[lane * 8 + q], tot += v[q];
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t run = incl - tot;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) c16[lane * 8 + q] = (uint16_t)run, run += v[q];
+        __syncwarp();
+    }
+    const uint16_t* c16 = half_row(mc);
+#pragma unroll
+    for (int k = 0; k < kMaxItems; ++k) {
+        if (k >= E) break;
+        const int pos = b0 + k * 32;
+        const uint32_t key = kin[pos];
+        const uint32_t d = (key >> shift) & 0xffu;
+        const uint32_t r = (ranks[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
+        const uint32_t dst = (uint32_t)c16[d] + r;
+        sm.key[cur ^ 1][dst] = key;
+        sm.idx[cur ^ 1][dst] = sm.idx[cur][pos];
+    }
+    if constexpr (G > 1) __syncthreads(); else __syncwarp();
+}
+
+// LSD passes over the 4 bytes from buffer 0, skipping bytes equal in every key
+// (kand / kor: AND / OR over all keys, pads included).  Returns the buffer
+// holding the result.
+template <int G, typename S>
+__device__ __forceinline__ int sort_group(S& sm, int E, int gw, uint32_t kand, uint32_t kor) {
+    int cur = 0;
+    for (int p = 0; p < 4; ++p) {
+        const int shift = 8 * p;
+        if ((((kand ^ kor) >> shift) & 0xffu) == 0) continue;
+        radix_pass<G>(sm, E, shift, gw, cur);
+        cur ^= 1;
+    }
+    return cur;
+}
+
+// MSD bucket sort, the common case: one counting pass over the top bits of
+// (key - min) (about two buckets per entry, at most 2^kBits), then a scatter
+// through shared-atomic bucket cursors (unordered: the buckets are sorted whole
+// afterwards), then each bucket insertion-sorted by one thread.  With 12 bits the largest C2 bucket holds 33 entries; a group
+// whose largest bucket exceeds kMsdMaxBucket returns false before writing
+// anything and the caller runs the LSD passes instead.  Keys 0 -> 1, indices
+// into idx[0] (the identity is implicit: position i holds entry i).
+constexpr uint32_t kMsdMaxBucket = 64;
+template <int G, int kBits, typename S>
+__device__ __forceinline__ bool msd_sort(S& sm, uint32_t n, uint32_t kmin, uint32_t kmax) {
+    constexpr int T = 32 * G, kPerMax = (1 << kBits) / T;
+    // counters over idx[1] and cnt (contiguous; neither holds live data yet)
+    static_assert(kPerMax >= 1 && (4 << kBits) <= (int)(sizeof(sm.idx[1]) + sizeof(sm.cnt)), "bucket counters fit");
+    static_assert(offsetof(S, cnt) == offsetof(S, idx) + sizeof(sm.idx), "idx[1] and cnt are contiguous");
+    const int t = G > 1 ? (int)threadIdx.x : (int)(threadIdx.x & 31);
+    const int lane = threadIdx.x & 31;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(sm.idx[1]);
+    auto sync = [] { if constexpr (G > 1) __syncthreads(); else __syncwarp(); };
+    // about two buckets per entry, at least one per thread
+    constexpr int kMinBits = G > 1 ? 10 : 5;
+    int bits = n > 1 ? 33 - __clz(n - 1) : 1;
+    bits = bits < kMinBits ? kMinBits : (bits > kBits ? kBits : bits);
+    const int NB = 1 << bits, per = NB / T;
+    const uint32_t diff = kmax - kmin;
+    const int span = diff ? 32 - __clz(diff) : 0;
+    const int sh = span > bits ? span - bits : 0;
+#pragma unroll
+    for (int q = 0; q < kPerMax; ++q)
+        if (q < per) cnt[t * per + q] = 0;
+    sync();
+#pragma unroll
+    for (int k = 0; k < kMaxItems; ++k) {
+        const uint32_t i = t + k * T;
+        if (i >= n) break;
+        atomicAdd(&cnt[(sm.key[0][i] - kmin) >> sh], 1u);
+    }
+    sync();
+    // exclusive scan of the bucket sizes (per consecutive buckets per thread) and the largest
+    uint32_t v[kPerMax], tot = 0, mx = 0;
+#pragma unroll
+    for (int q = 0; q < kPerMax; ++q) {
+        v[q] = q < per ? cnt[t * per + q] : 0u;
+        tot += v[q], mx = max(mx, v[q]);
+    }
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    uint32_t base = incl - tot;
+    if constexpr (G > 1) {
+        __shared__ uint32_t s_w[G], s_maxb;
+        if (lane == 31) s_w[t >> 5] = incl;
+        if (t == 0) s_maxb = 0;
+        __syncthreads();
+        if (lane == 0) atomicMax(&s_maxb, mx);
+        if (t < 32) {  // warp prefix of the warp totals
+            const uint32_t w = t < G ? s_w[t] : 0u;
+            uint32_t wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += y;
+            }
+            if (t < G) s_w[t] = wi - w;
+        }
+        __syncthreads();
+        base += s_w[t >> 5];
+        mx = s_maxb;
+    }
+    if (mx > kMsdMaxBucket) return false;
+#pragma unroll
+    for (int q = 0; q < kPerMax; ++q)
+        if (q < per) cnt[t * per + q] = base, base += v[q];
+    sync();
+    // scatter: the bucket cursors end at the bucket ends (order within a bucket is free)
+#pragma unroll
+    for (int k = 0; k < kMaxItems; ++k) {
+        const uint32_t i = t + k * T;
+        if (i >= n) break;
+        const uint32_t key = sm.key[0][i];
+        const uint32_t dst = atomicAdd(&cnt[(key - kmin) >> sh], 1u);
+        sm.key[1][dst] = key;
+        sm.idx[0][dst] = (uint16_t)i;
+    }
+    sync();
+    // each bucket by one thread (insertion sort on the key; ties are fixed later)
+    uint32_t* ks = sm.key[1];
+    uint16_t* is = sm.idx[0];
+    for (int bk = t; bk < NB; bk += T) {
+        const uint32_t lo = bk ? cnt[bk - 1] : 0u, hi = cnt[bk];
+        for (uint32_t a = lo + 1; a < hi; ++a) {
+            const uint32_t x = ks[a];
+            const uint16_t xi = is[a];
+            uint32_t c = a;
+            while (c > lo && ks[c - 1] > x) {
+                ks[c] = ks[c - 1];
+                is[c] = is[c - 1];
+                --c;
+            }
+            ks[c] = x;
+            is[c] = xi;
+        }
+    }
+    sync();
+    return true;
+}
+
+// Equal depths keep cut order (render.hpp:268-272 stable_sort): runs of equal
+// keys are rare; the thread at a run's start orders its indices by splat id.
+__device__ __forceinline__ void fix_ties(const uint32_t* __restrict__ key, uint16_t* __restrict__ idx, uint32_t n,
+                                         const uint32_t* __restrict__ ids_in, uint32_t s, uint32_t i0,
+                                         uint32_t step) {
+    for (uint32_t i = i0; i + 1 < n; i += step) {
+        if (key[i + 1] != key[i] || (i > 0 && key[i - 1] == key[i])) continue;
+        uint32_t e = i + 1;
+        while (e < n && key[e] == key[i]) ++e;
+        for (uint32_t a = i + 1; a < e; ++a) {  // insertion sort by id
+            const uint16_t x = idx[a];
+            const uint32_t xv = ids_in[s + x];
+            uint32_t b = a;
+            while (b > i && ids_in[s + idx[b - 1]] > xv) {
+                idx[b] = idx[b - 1];
+                --b;
+            }
+            idx[b] = x;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kTsThreads, 1) k_tile_sort(const uint32_t* __restrict__ order,
+                                                             const uint2* __restrict__ prange,
+                                                             const uint32_t* __restrict__ big_list,
+                                                             const uint2* __restrict__ extra,
+                                                             const uint32_t* __restrict__ plan,
+                                                             const uint64_t* __restrict__ sort_n_ptr, TileBufs b,
+                                                             uint32_t* __restrict__ done,
+                                                             uint32_t* __restrict__ task_ctr) {
+    extern __shared__ __align__(16) unsigned char ts_smem[];
+    CtaSort& cs = *reinterpret_cast<CtaSort*>(ts_smem);
+    __shared__ uint32_t s_next, s_and, s_or, s_min, s_max;
+    if (*sort_n_ptr == 0) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // task table: [CTA-sorted tiles (chunk 0)] [further chunks of tiles > kTileCap]
+    //             [groups of 32 per-warp tiles] [merges of tiles > kTileCap]
+    const uint32_t n_cta = plan[0], n_big = plan[1], nonempty = plan[3], n_extra = plan[4];
+    const uint32_t n_small_tasks = (nonempty - n_cta + kTsWarps - 1) / kTsWarps;
+    const uint32_t t_small = n_cta + n_extra, t_merge = t_small + n_small_tasks, n_tasks = t_merge + n_big;
+    if (tid == 0) s_next = atomicAdd(task_ctr, 1u);
+    while (true) {
+        if (tid == 0) {
+            s_and = 0xFFFFFFFFu;
+            s_or = 0;
+            s_min = 0xFFFFFFFFu;
+            s_max = 0;
+        }
+        __syncthreads();
+        const uint32_t task = s_next;
+        if (task >= n_tasks) break;
+        __syncthreads();
+        if (tid == 0) s_next = atomicAdd(task_ctr, 1u);  // the next task's index arrives meanwhile
+        if (task < t_small) {
+            // a CTA-sorted tile, or one further chunk of a tile larger than kTileCap
+            uint32_t p = task, k = 0;
+            if (task >= n_cta) {
+                const uint2 e = extra[task - n_cta];
+                p = e.x, k = e.y;
+            }
+            const uint32_t tile = order[p];
+            const uint2 rg = prange[p];
+            const uint32_t R = (rg.y - rg.x + kTileCap - 1) / kTileCap;
+            const uint32_t s = rg.x + k * kTileCap, n = min(kTileCap, rg.y - s);
+            const int E = (int)((n + kTsThreads - 1) / kTsThreads);
+            const uint32_t N = (uint32_t)E * kTsThreads;
+            uint32_t kand = 0xFFFFFFFFu, kor = 0, kmin = 0xFFFFFFFFu, kmax = 0;
+#pragma unroll
+            for (int q0 = 0; q0 < kMaxItems; q0 += 8) {
+                uint32_t kv[8];  // 8 loads in flight before the first use
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t i = tid + (q0 + q) * kTsThreads;
+                    kv[q] = i < n ? __ldcg(b.zA + s + i) : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t i = tid + (q0 + q) * kTsThreads;
+                    if (i < n) {
+                        cs.key[0][i] = kv[q];
+                        cs.idx[0][i] = (uint16_t)i;
+                        kand &= kv[q], kor |= kv[q], kmin = min(kmin, kv[q]), kmax = max(kmax, kv[q]);
+                    }
+                }
+            }
+            kand = __reduce_and_sync(0xffffffffu, kand);
+            kor = __reduce_or_sync(0xffffffffu, kor);
+            kmin = __reduce_min_sync(0xffffffffu, kmin);
+            kmax = __reduce_max_sync(0xffffffffu, kmax);
+            if (lane == 0) {
+                atomicAnd(&s_and, kand);
+                atomicOr(&s_or, kor);
+                atomicMin(&s_min, kmin);
+                atomicMax(&s_max, kmax);
+            }
+            __syncthreads();
+            kand = s_and, kor = s_or;
+            const uint32_t* rkey = cs.key[1];
+            uint16_t* ridx = cs.idx[0];
+            if (!msd_sort<kTsWarps, 13>(cs, n, s_min, s_max)) {
+                // pads: the OR of all keys is >= every key and shares their common bytes;
+                // they start after every real entry, so the stable passes keep them last
+                for (uint32_t i = n + tid; i < N; i += kTsThreads) cs.key[0][i] = kor, cs.idx[0][i] = (uint16_t)i;
+                __syncthreads();
+                const int cur = sort_group<kTsWarps>(cs, E, warp, kand, kor);
+                rkey = cs.key[cur], ridx = cs.idx[cur];
+            }
+            fix_ties(rkey, ridx, n, b.iA, s, tid, kTsThreads);
+            __syncthreads();
+            if (R == 1) {
+                // gathers of 4 entries in flight per thread
+#pragma unroll
+                for (int q0 = 0; q0 < kMaxItems; q0 += 4) {
+                    uint32_t gi[4], gm[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t i = tid + (q0 + q) * kTsThreads;
+                        if (i < n) {
+                            const uint32_t x = s + ridx[i];
+                            gi[q] = __ldcg(b.iA + x);
+                            gm[q] = __ldcg(b.mA + x);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t i = tid + (q0 + q) * kTsThreads;
+                        if (i < n) {
+                            b.zB[s + i] = (tile << 8) | gm[q];
+                            b.iB[s + i] = gi[q];
+                        }
+                    }
+                }
+            } else {
+                // a sorted run (bits(z), id, mask) for the merge rounds
+                for (uint32_t i = tid; i < n; i += kTsThreads) {
+                    const uint32_t x = s + ridx[i];
+                    b.zC[s + i] = rkey[i];
+                    b.iC[s + i] = b.iA[x];
+                    b.mC[s + i] = b.mA[x];
+                }
+                __threadfence();
+                __syncthreads();
+                if (tid == 0) atomicAdd(&done[p], 1u);
+            }
+        } else if (task < t_merge) {
+            // 32 small tiles, one per warp
+            const uint32_t p = n_cta + (task - t_small) * kTsWarps + warp;
+            WarpSort& ws = reinterpret_cast<WarpSort*>(ts_smem)[warp];
+            if (p < nonempty) {
+                const uint32_t tile = order[p];
+                const uint2 rg = prange[p];
+                const uint32_t s = rg.x, n = rg.y - rg.x;
+                const int E = (int)((n + 31) / 32);
+                uint32_t kand = 0xFFFFFFFFu, kor = 0, kmin = 0xFFFFFFFFu, kmax = 0;
+#pragma unroll
+                for (int q0 = 0; q0 < kMaxItems; q0 += 8) {
+                    uint32_t kv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const uint32_t i = lane + (q0 + q) * 32;
+                        kv[q] = i < n ? __ldcg(b.zA + s + i) : 0u;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const uint32_t i = lane + (q0 + q) * 32;
+                        if (i < n) {
+                            ws.key[0][i] = kv[q];
+                            ws.idx[0][i] = (uint16_t)i;
+                            kand &= kv[q], kor |= kv[q], kmin = min(kmin, kv[q]), kmax = max(kmax, kv[q]);
+                        }
+                    }
+                }
+                kand = __reduce_and_sync(0xffffffffu, kand);
+                kor = __reduce_or_sync(0xffffffffu, kor);
+                kmin = __reduce_min_sync(0xffffffffu, kmin);
+                kmax = __reduce_max_sync(0xffffffffu, kmax);
+                __syncwarp();
+                const uint32_t* rkey = ws.key[1];
+                uint16_t* ridx = ws.idx[0];
+                if (!msd_sort<1, 8>(ws, n, kmin, kmax)) {
+                    for (uint32_t i = n + lane; i < (uint32_t)E * 32; i += 32) ws.key[0][i] = kor, ws.idx[0][i] = (uint16_t)i;
+                    __syncwarp();
+                    const int cur = sort_group<1>(ws, E, 0, kand, kor);
+                    rkey = ws.key[cur], ridx = ws.idx[cur];
+                }
+                fix_ties(rkey, ridx, n, b.iA, s, lane, 32);
+                __syncwarp();
+#pragma unroll
+                for (int q0 = 0; q0 < kMaxItems; q0 += 4) {
+                    uint32_t gi[4], gm[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t i = lane + (q0 + q) * 32;
+                        if (i < n) {
+                            const uint32_t x = s + ridx[i];
+                            gi[q] = __ldcg(b.iA + x);
+                            gm[q] = __ldcg(b.mA + x);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t i = lane + (q0 + q) * 32;
+                        if (i < n) {
+                            b.zB[s + i] = (tile << 8) | gm[q];
+                            b.iB[s + i] = gi[q];
+                        }
+                    }
+                }
+            }
+        } else {
+            // merge of a large tile's sorted chunks: pairwise rounds, merge path per thread
+            const int p = (int)big_list[task - t_merge];
+            const uint32_t tile = order[p];
+            const uint2 rg = prange[p];
+            const uint32_t R = (rg.y - rg.x + kTileCap - 1) / kTileCap;
+            const uint32_t N = rg.y - rg.x, base = rg.x;
+            if (tid == 0) {
+                while (ld_volatile_u32(&done[p]) < R) __nanosleep(256);
+                __threadfence();
+            }
+            __syncthreads();
+            const int rounds = ceil_log2(R);
+            bool srcC = true;
+            for (int r = 0; r < rounds; ++r) {
+                const bool last = r == rounds - 1;
+                const uint32_t* zs = srcC ? b.zC : b.zA;
+                const uint32_t* is = srcC ? b.iC : b.iA;
+                const uint8_t* ms = srcC ? b.mC : b.mA;
+                uint32_t* zd = last ? b.zB : (srcC ? b.zA : b.zC);
+                uint32_t* id = last ? b.iB : (srcC ? b.iA : b.iC);
+                uint8_t* md = srcC ? b.mA : b.mC;
+                const uint32_t w = kTileCap << r;
+                for (uint32_t lo0 = 0; lo0 < N; lo0 += 2 * w) {
+                    const uint32_t La = min(w, N - lo0), Lb = min(w, N - lo0 - La), L = La + Lb;
+                    const uint32_t a0 = base + lo0, b0 = a0 + La;
+                    for (uint32_t d0 = tid * 8; d0 < L; d0 += kTsThreads * 8) {
+                        uint32_t lo = d0 > Lb ? d0 - Lb : 0, hi = min(d0, La);
+                        while (lo < hi) {
+                            const uint32_t mid = (lo + hi) >> 1;
+                            if (key_at(zs, is, a0 + mid) < key_at(zs, is, b0 + d0 - 1 - mid)) lo = mid + 1;
+                            else hi = mid;
+                        }
+                        uint32_t i = lo, j = d0 - lo;
+                        for (uint32_t q = 0; q < 8 && d0 + q < L; ++q) {
+                            bool take_a = j >= Lb;
+                            if (!take_a && i < La) take_a = key_at(zs, is, a0 + i) < key_at(zs, is, b0 + j);
+                            const uint32_t src = take_a ? a0 + i : b0 + j;
+                            if (take_a) ++i; else ++j;
+                            const uint32_t dst = a0 + d0 + q;
+                            const uint32_t iv = __ldcg(is + src);
+                            const uint8_t mv = __ldcg(ms + src);
+                            if (last) {
+                                zd[dst] = (tile << 8) | mv;
+                                id[dst] = iv;
+                            } else {
+                                zd[dst] = __ldcg(zs + src);
+                                id[dst] = iv;
+                                md[dst] = mv;
+                            }
+                        }
+                    }
+                }
+                __threadfence_block();
+                __syncthreads();
+                srcC = !srcC;
+            }
+        }
+        __syncthreads();  // s_and .. s_max and the shared buffers are reused
+    }
+}
+
+// ------------------------------------------------------------------ launchers
+static int bucket_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (!sms) sms = 148;
+    }
+    return sms;
+}
+
+void launch_tile_count(const uint32_t* dupcount, const uint4* dinfo, const uint64_t* n_ptr, uint64_t n_max,
+                       int tiles_x, uint32_t* tcount, uint32_t* rowdiff, cudaStream_t s) {
+    const unsigned grid =
+        (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)bucket_sms() * 8));
+    k_tile_count<<<grid, 256, 0, s>>>(dupcount, dinfo, n_ptr, tiles_x, tcount, rowdiff);
+    note_launch();
+}
+
+void launch_tile_plan(const uint32_t* tcount, const uint32_t* rowdiff, int tiles_x, int tiles_y, uint64_t cap_dup,
+                      uint2* ranges, uint32_t* cursor, uint32_t* order, uint2* prange, uint32_t* big_list,
+                      uint2* extra, uint32_t* plan, uint64_t* n_dup, uint64_t* sort_n, unsigned long long* overflows,
+                      cudaStream_t s) {
+    const size_t smem = (size_t)tiles_x * tiles_y * 4;
+    static size_t opted = 0;
+    if (smem > 48 * 1024 && smem > opted) {
+        cudaFuncSetAttribute(k_tile_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        opted = smem;
+    }
+    k_tile_plan<<<1, 1024, smem, s>>>(tcount, rowdiff, tiles_x, tiles_y, cap_dup, ranges, cursor, order, prange,
+                                      big_list, extra, plan, n_dup, sort_n, overflows);
+    note_launch();
+}
+
+void launch_bucket(const uint32_t* dupcount, const uint4* dinfo, const ProjRec* proj, const uint64_t* n_ptr,
+                   uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* cursor, uint32_t* zk,
+                   uint32_t* ids, uint8_t* bm, uint32_t* huge_q, uint32_t* huge_n, uint64_t* dbg_keys,
+                   uint32_t* dbg_vals, cudaStream_t s) {
+    const unsigned grid =
+        (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)bucket_sms() * 4));
+    k_bucket<<<grid, 256, 0, s>>>(dupcount, dinfo, proj, n_ptr, sort_n_ptr, tiles_x, cursor, zk, ids, bm, huge_q,
+                                  huge_n, dbg_keys, dbg_vals);
+    note_launch();
+    k_bucket_huge<<<(unsigned)bucket_sms() * 4, 256, 0, s>>>(dinfo, proj, huge_q, huge_n, sort_n_ptr, tiles_x, cursor,
+                                                             zk, ids, bm, dbg_keys, dbg_vals);
+    note_launch();
+}
+
+void launch_tile_sort(const uint32_t* order, const uint2* prange, const uint32_t* big_list, const uint2* extra,
+                      const uint32_t* plan, const uint64_t* sort_n_ptr, int tiles, uint32_t* zA, uint32_t* iA,
+                      uint8_t* mA, uint32_t* zB, uint32_t* iB, uint32_t* zC, uint32_t* iC, uint8_t* mC,
+                      uint32_t* done, uint32_t* task_ctr, cudaStream_t s) {
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSortSmem);
+        init = true;
+    }
+    TileBufs b{zA, iA, mA, zB, iB, zC, iC, mC};
+    const unsigned grid = (unsigned)std::max(1, std::min(bucket_sms(), tiles));
+    k_tile_sort<<<grid, kTsThreads, kTileSortSmem, s>>>(order, prange, big_list, extra, plan, sort_n_ptr, b, done,
+                                                        task_ctr);
+    note_launch();
+}
+
+uint64_t bucket_huge_slots(uint64_t dup_max) { return dup_max / kHugeArea + 1; }
+uint64_t tile_sort_extra_slots(uint64_t dup_max) { return dup_max / kTileCap + 1; }
+
+}  // namespace hs

@@ -160,14 +160,13 @@ __device__ __forceinline__ float interp_weight(float en, float ep, float tau) {
 // exactly as the blend forms d = ((float)x + 0.5) - mean, so the blend's d
 // values of the block's pixels lie inside the float rectangle.  Conservative:
 // the minimum of the conic quadratic Q over each rectangle -- 0 when it holds
-// the mean, else the least of its four edge minima (edge minimiser clamped to
-// the edge, Q evaluated in float with fma) -- is compared with qthr (p3.y),
+// the mean, else the lesser of its facing edges' minima (edge minimiser clamped
+// to the edge, Q evaluated in float with fma) -- is compared with qthr (p3.y),
 // which k_preprocess computed in double as 2 ln(255 max(fa, pa)) inflated by a
 // relative margin of 2e-5 (a+c)^2/det >= 2e-5 cond(conic).  That margin covers
 // both the float rounding of the reference's per-pixel power (~1.5e-6 cond)
 // and of this evaluation (< 1e-6 cond); ia/ic (1/a, 1/c) only place the
-// evaluation points.  Edge quantities are shared between the blocks: 4 column
-// edges and 8 row edges instead of 32 edge evaluations from scratch.
+// evaluation points.
 __device__ __forceinline__ uint32_t tile_reach_mask(const float4& p0, const float4& p1, const float4& p3, int px0,
                                                     int py0) {
     const float qthr = -2.0f * p3.y;  // p3.y = -qthr / 2 (exact scalings)
@@ -185,40 +184,45 @@ __device__ __forceinline__ uint32_t tile_reach_mask(const float4& p0, const floa
         if (fmaxf(fmaxf(q00, q01), fmaxf(q10, q11)) <= qthr) return 0xFFu;
     }
     const float b2 = 2.0f * b, sx = -b * p3.w, sy = -b * p3.z;
-    // column edges x = X + {0, 7, 8, 15}: Q on the edge is (c y + 2 b x) y + a x^2
-    float xe[4], bx2[4], axx[4], ymin[4];
+    // The minimum of a convex quadratic over a rectangle not holding its centre
+    // lies on an edge facing the centre (the edge's line separates the centre from
+    // the rectangle), so each block needs at most one column edge and one row edge:
+    // x = X_j (x0 if the mean is left of the block, else x1) and y = Y_r.  An edge
+    // that faces nothing (the mean inside the block's column span) only adds an
+    // upper bound, which leaves the minimum unchanged.
+    float xe[4], ye[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        xe[k] = ((float)(px0 + (k >> 1) * 8 + (k & 1) * 7) + 0.5f) - p0.x;
-        bx2[k] = b2 * xe[k];
-        axx[k] = a * xe[k] * xe[k];
-        ymin[k] = sx * xe[k];
-    }
-    // row edges y = Y + {0, 3, 4, 7, 8, 11, 12, 15}: Q on the edge is (a x + 2 b y) x + c y^2
-    float ye[8], by2[8], cyy[8], xmin[8];
+    for (int k = 0; k < 4; ++k) xe[k] = ((float)(px0 + (k >> 1) * 8 + (k & 1) * 7) + 0.5f) - p0.x;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        ye[k] = ((float)(py0 + (k >> 1) * 4 + (k & 1) * 3) + 0.5f) - p0.y;
-        by2[k] = b2 * ye[k];
-        cyy[k] = c * ye[k] * ye[k];
-        xmin[k] = sy * ye[k];
+    for (int k = 0; k < 8; ++k) ye[k] = ((float)(py0 + (k >> 1) * 4 + (k & 1) * 3) + 0.5f) - p0.y;
+    // column edges: Q on x = X is (c y + 2 b X) y + a X^2, minimised at y = -b X / c
+    float bx2[2], axx[2], ymin[2];
+    bool cin[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const float x0 = xe[2 * j], x1 = xe[2 * j + 1];
+        const float X = x0 > 0.0f ? x0 : x1;
+        bx2[j] = b2 * X;
+        axx[j] = a * X * X;
+        ymin[j] = sx * X;
+        cin[j] = x0 <= 0.0f && 0.0f <= x1;
     }
     uint32_t mask = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
+        // row edge: Q on y = Y is (a x + 2 b Y) x + c Y^2, minimised at x = -b Y / a
         const float y0 = ye[2 * r], y1 = ye[2 * r + 1];
+        const float Y = y0 > 0.0f ? y0 : y1;
+        const float by2 = b2 * Y, cyy = c * Y * Y, xmin = sy * Y;
+        const bool rin = y0 <= 0.0f && 0.0f <= y1;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const float x0 = xe[2 * j], x1 = xe[2 * j + 1];
-            float qm = (x0 <= 0.0f && 0.0f <= x1 && y0 <= 0.0f && 0.0f <= y1) ? 0.0f : __int_as_float(0x7f800000);
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int kx = 2 * j + e, ky = 2 * r + e;
-                const float y = fminf(fmaxf(ymin[kx], y0), y1);
-                qm = fminf(qm, __fmaf_rn(__fmaf_rn(c, y, bx2[kx]), y, axx[kx]));
-                const float x = fminf(fmaxf(xmin[ky], x0), x1);
-                qm = fminf(qm, __fmaf_rn(__fmaf_rn(a, x, by2[ky]), x, cyy[ky]));
-            }
+            const float y = fminf(fmaxf(ymin[j], y0), y1);
+            const float qv = __fmaf_rn(__fmaf_rn(c, y, bx2[j]), y, axx[j]);
+            const float x = fminf(fmaxf(xmin, x0), x1);
+            const float qh = __fmaf_rn(__fmaf_rn(a, x, by2), x, cyy);
+            const float qm = (cin[j] && rin) ? 0.0f : fminf(qv, qh);
             if (!(qm > qthr)) mask |= 1u << (2 * r + j);
         }
     }

@@ -94,7 +94,6 @@ void launch_blend(int mode, bool stats, const uint2* ranges, const uint32_t* key
                   uint32_t* lists, cudaStream_t s);
 // u32 words of the blend's per-warp block lists (scratch, no initialisation needed)
 uint64_t blend_list_words();
-void launch_tile_order(const uint2* ranges, int tiles, const uint64_t* sort_n_ptr, uint32_t* order, cudaStream_t s);
 void launch_assemble(const float4* attr, const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr,
                      uint64_t n_max, float* mean, float* scale, float* rot, float* sh, float* fall, float* pfall,
                      float* t, int* k, cudaStream_t s);
@@ -110,17 +109,26 @@ uint64_t scan_status_words(uint64_t n_max);
 void launch_compact_visible(const uint32_t* dupcount, const uint4* dinfo, const uint64_t* n_ptr, uint64_t n_max,
                             uint32_t* keys, uint32_t* vals, uint64_t* status, uint32_t* counter, uint64_t* v_out,
                             uint32_t* sort_scratch, cudaStream_t s);
-void launch_dup_offsets(const uint32_t* ids, const uint32_t* dupcount, const uint64_t* v_ptr, uint64_t n_max,
-                        uint32_t* offsets, uint64_t* status, uint32_t* counter, uint64_t* total_out,
-                        uint64_t* sort_n_out, uint64_t capacity, unsigned long long* overflows, cudaStream_t s);
-uint64_t huge_queue_slots(uint64_t dup_max);
-void launch_duplicate_sorted(const uint32_t* ids, const uint4* dinfo, const ProjRec* proj, const uint32_t* offsets,
-                             const uint64_t* v_ptr, uint64_t n_max, const uint64_t* sort_n_ptr, uint64_t dup_max,
-                             int tiles_x, uint32_t* keys, uint32_t* vals, uint2* huge_q, uint32_t* huge_n,
-                             cudaStream_t s);
-void launch_ranges(const uint32_t* keys, const uint64_t* n_ptr, uint64_t n_max, uint2* ranges, cudaStream_t s);
 void launch_make_keys(const uint32_t* tiles, const uint32_t* ids, const uint4* dinfo, const uint64_t* n_ptr,
                       uint64_t n_max, uint64_t* out, cudaStream_t s);
+
+// bucket.cu (per-tile depth order: bucketing + in-tile sort, render.hpp:262-294)
+uint64_t bucket_huge_slots(uint64_t dup_max);
+uint64_t tile_sort_extra_slots(uint64_t dup_max);
+void launch_tile_count(const uint32_t* dupcount, const uint4* dinfo, const uint64_t* n_ptr, uint64_t n_max,
+                       int tiles_x, uint32_t* tcount, uint32_t* rowdiff, cudaStream_t s);
+void launch_tile_plan(const uint32_t* tcount, const uint32_t* rowdiff, int tiles_x, int tiles_y, uint64_t cap_dup,
+                      uint2* ranges, uint32_t* cursor, uint32_t* order, uint2* prange, uint32_t* big_list,
+                      uint2* extra, uint32_t* plan, uint64_t* n_dup, uint64_t* sort_n, unsigned long long* overflows,
+                      cudaStream_t s);
+void launch_bucket(const uint32_t* dupcount, const uint4* dinfo, const ProjRec* proj, const uint64_t* n_ptr,
+                   uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* cursor, uint32_t* zk,
+                   uint32_t* ids, uint8_t* bm, uint32_t* huge_q, uint32_t* huge_n, uint64_t* dbg_keys,
+                   uint32_t* dbg_vals, cudaStream_t s);
+void launch_tile_sort(const uint32_t* order, const uint2* prange, const uint32_t* big_list, const uint2* extra,
+                      const uint32_t* plan, const uint64_t* sort_n_ptr, int tiles, uint32_t* zA, uint32_t* iA,
+                      uint8_t* mA, uint32_t* zB, uint32_t* iB, uint32_t* zC, uint32_t* iC, uint8_t* mC,
+                      uint32_t* done, uint32_t* task_ctr, cudaStream_t s);
 
 // sort.cu
 uint64_t sort_status_words(uint64_t n_max);
