@@ -29,6 +29,8 @@
 //                  afterwards; tiles of <= 510 entries are sorted one per warp,
 //                  32 per task; larger tiles are sorted in 16384-entry chunks
 //                  and merged (merge path) once their chunks are done.
+//   k_tile_finalize  the sorted (tile, source slot) lists -> (tile << 8 | reach
+//                  mask, splat id): the gathers of every entry in one wide pass.
 // Output: keys[i] = tile << 8 | reach mask, vals[i] = splat id, in tile order and
 // within a tile in the reference's depth order -- the tile_entries of
 // render.hpp:285-294 bit for bit; ranges[t] = [tile_start[t], tile_start[t+1]).
@@ -48,6 +50,7 @@ constexpr int kBigArea = 4;           // k_bucket: larger footprints are emitted
 constexpr int kHugeArea = 1024;       // larger still: one CTA per splat (k_bucket_huge)
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr uint32_t kMarkBit = 0x80000000u;  // hash keys of row difference marks
+constexpr uint32_t kPending = 0x80000000u;  // sorted key awaiting k_tile_finalize (tiles < 2^23)
 
 // ------------------------------------------------------------------ shared hash table
 // Open addressing over kSlots (key, value) pairs; `used` lists the occupied
@@ -128,90 +131,140 @@ __device__ __forceinline__ void hash_drain(HashTab<kLog>& h, Fn fn) {
 }
 
 // ------------------------------------------------------------------ count
-// tcount[t] += entries of tile t; rowdiff[row * (tiles_x + 1) + x] += +1 / -1 at
-// the ends of every tile row crossed by a footprint of more than 8 tiles.
+// CTA c takes the contiguous cut entries [c chunk, (c + 1) chunk), chunk =
+// ceil(C / grid): cut order is spatially coherent, so a chunk's small
+// footprints (<= 4 tiles) fall on few tiles (~60 at C2).  Their per-tile counts
+// are summed in the shared table without a barrier and flushed once: tcount[t]
+// += count, and the table (tile, count) saved for k_bucket, which reserves each
+// tile's range with one atomic and re-ranks the same entries into it.  Larger
+// footprints add +1 / -1 marks at the ends of every tile row they cross
+// (rowdiff[row * (tiles_x + 1) + x]); k_tile_plan takes the row prefixes.
+constexpr int kChunkLog = 11;                     // shared table: 2048 slots
+constexpr int kChunkSlots = 1 << kChunkLog;
+__device__ __forceinline__ void chunk_range(uint64_t n, uint64_t& lo, uint64_t& hi) {
+    const uint64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    lo = min((uint64_t)blockIdx.x * chunk, n);
+    hi = min(lo + chunk, n);
+}
 __global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__ dupcount,
                                                     const uint4* __restrict__ dinfo, const uint64_t* __restrict__ n_ptr,
                                                     int tiles_x, uint32_t* __restrict__ tcount,
-                                                    uint32_t* __restrict__ rowdiff) {
-    __shared__ HashTab<11> h;  // 256 entries x <= 8 tiles
-    const uint64_t n = *n_ptr;
+                                                    uint32_t* __restrict__ rowdiff, uint2* __restrict__ saved,
+                                                    uint32_t* __restrict__ saved_n) {
+    __shared__ HashTab<kChunkLog> h;
     const int W = tiles_x + 1;
+    uint64_t lo, hi;
+    chunk_range(*n_ptr, lo, hi);
     hash_init(h);
     __syncthreads();
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = base + threadIdx.x;
-        const uint32_t cnt = i < n ? dupcount[i] : 0u;
-        int tx0 = 0, tx1 = 0, ty0 = 0, ty1 = 0;
-        if (cnt) {
-            const uint4 di = dinfo[i];
-            tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
+    // loads one block ahead (dinfo unconditionally: stale for culled entries, unused)
+    uint32_t cnt_n = lo + threadIdx.x < hi ? dupcount[lo + threadIdx.x] : 0u;
+    uint4 di_n = lo + threadIdx.x < hi ? dinfo[lo + threadIdx.x] : make_uint4(0, 0, 0, 0);
+    for (uint64_t base = lo; base < hi; base += blockDim.x) {
+        const uint32_t cnt = cnt_n;
+        const uint4 di = di_n;
+        {
+            const uint64_t nx = base + blockDim.x + threadIdx.x;
+            cnt_n = nx < hi ? dupcount[nx] : 0u;
+            di_n = nx < hi ? dinfo[nx] : make_uint4(0, 0, 0, 0);
         }
+        const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
         const int w = max(tx1 - tx0, 1);
-        const bool direct = cnt != 0 && cnt <= (uint32_t)kCountDirect;
+        const bool small = cnt != 0 && cnt <= (uint32_t)kBigArea;
         int slot;
-        for (int k = 0; k < kCountDirect; ++k) {
-            const bool has = direct && (uint32_t)k < cnt;
+        for (int k = 0; k < kBigArea; ++k) {
+            const bool has = small && (uint32_t)k < cnt;
             if (!__any_sync(0xffffffffu, has)) break;
             const uint32_t tile = (uint32_t)((ty0 + k / w) * tiles_x + tx0 + k % w);
             hash_add(h, has, tile, 1u, slot, tcount);
         }
-        // large footprints: +1 at (row, tx0), -1 at (row, tx1) for every row
-        const bool marks = cnt > (uint32_t)kCountDirect;
+        const bool marks = cnt > (uint32_t)kBigArea;
         for (int r = 0; __any_sync(0xffffffffu, marks && ty0 + r < ty1); ++r) {
             const bool has = marks && ty0 + r < ty1;
             const uint32_t row = (uint32_t)(ty0 + r) * W;
             hash_add(h, has, kMarkBit | (row + tx0), 1u, slot, rowdiff);
             hash_add(h, has, kMarkBit | (row + tx1), 0xFFFFFFFFu, slot, rowdiff);
         }
-        __syncthreads();
-        hash_drain(h, [&](uint32_t key, uint32_t v) {
-            if (key & kMarkBit) atomicAdd(&rowdiff[key & ~kMarkBit], v);
-            else atomicAdd(&tcount[key], v);
-        });
     }
+    __syncthreads();
+    const uint32_t nu = h.n_used;
+    uint2* sv = saved + (size_t)blockIdx.x * kChunkSlots;
+    for (uint32_t u = threadIdx.x; u < nu; u += blockDim.x) {
+        const int sl = h.used[u];
+        const uint32_t key = h.key[sl], v = h.val[sl];
+        if (key & kMarkBit) atomicAdd(&rowdiff[key & ~kMarkBit], v);
+        else atomicAdd(&tcount[key], v);
+        sv[u] = make_uint2(key, v);
+    }
+    if (threadIdx.x == 0) saved_n[blockIdx.x] = nu;
 }
 
 // ------------------------------------------------------------------ plan
-// One CTA of 1024 threads; per-tile sizes in shared memory (dynamic, 4 B per tile).
-// Heavy-first position p holds tile order[p] with bucket range prange[p].
-// plan[] = {CTA-sorted tiles (= first per-warp position), tiles larger than
-// kTileCap (big_list: their positions, merged), their further chunks (extra:
-// (position, chunk)), non-empty tiles}.
-__global__ void __launch_bounds__(1024) k_tile_plan(const uint32_t* __restrict__ tcount,
-                                                    const uint32_t* __restrict__ rowdiff, int tiles_x, int tiles_y,
+// One CTA of 1024 threads; per-tile starts in shared memory (dynamic, 4 B per
+// tile + 4).  Heavy-first position p holds tile order[p] with bucket range
+// prange[p].  plan[] = {CTA-sorted tiles (= first per-warp position), tiles
+// larger than kTileCap (big_list: their positions, merged), -, non-empty tiles,
+// their further chunks (extra: (position, chunk))}.  Global loads are issued
+// in batches so each phase waits for memory once.
+constexpr int kPlanRowChunks = 16;  // rows of up to 512 tiles in registers
+__global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const uint32_t* __restrict__ rowdiff,
+                                                    int tiles_x, int tiles_y, bool smem_sizes,
                                                     uint64_t cap_dup, uint2* __restrict__ ranges,
                                                     uint32_t* __restrict__ cursor, uint32_t* __restrict__ order,
                                                     uint2* __restrict__ prange, uint32_t* __restrict__ big_list,
                                                     uint2* __restrict__ extra, uint32_t* __restrict__ plan,
-                                                    uint64_t* __restrict__ n_dup,
-                                                    uint64_t* __restrict__ sort_n,
+                                                    uint64_t* __restrict__ n_dup, uint64_t* __restrict__ sort_n,
                                                     unsigned long long* __restrict__ overflows) {
-    extern __shared__ uint32_t s_n[];  // [tiles]
+    // [tiles + 1]: sizes, then exclusive starts -- in shared memory when it fits
+    // (up to ~56K tiles), else in place in tcount (sized tiles + 1)
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t* s_n = smem_sizes ? s_dyn : tcount;
     __shared__ uint64_t s_w64[32];
-    __shared__ uint32_t s_hist[33], s_offs[33], s_nbig;
+    __shared__ uint32_t s_hist[33], s_offs[33], s_nbig, s_nextra;
     __shared__ uint64_t s_total;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tiles = tiles_x * tiles_y;
     const uint32_t lt = (1u << lane) - 1u;
-    for (int t = tid; t < tiles; t += 1024) s_n[t] = tcount[t];
+    for (int t0 = 0; smem_sizes && t0 < tiles; t0 += 8 * 1024) {
+        uint32_t v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int t = t0 + q * 1024 + tid;
+            v[q] = t < tiles ? tcount[t] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int t = t0 + q * 1024 + tid;
+            if (t < tiles) s_n[t] = v[q];
+        }
+    }
     if (tid < 33) s_hist[tid] = 0;
-    if (tid == 0) s_nbig = 0;
+    if (tid == 0) s_nbig = 0, s_nextra = 0;
     __syncthreads();
     // 1. large footprints: prefix of each row's difference marks
     const int W = tiles_x + 1;
     for (int row = warp; row < tiles_y; row += 32) {
         uint32_t carry = 0;
-        for (int base = 0; base < tiles_x; base += 32) {
-            const int x = base + lane;
-            uint32_t incl = x < tiles_x ? rowdiff[(size_t)row * W + x] : 0u;
+        for (int c0 = 0; c0 < tiles_x; c0 += 32 * kPlanRowChunks) {
+            uint32_t v[kPlanRowChunks];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+            for (int q = 0; q < kPlanRowChunks; ++q) {
+                const int x = c0 + q * 32 + lane;
+                v[q] = x < tiles_x ? rowdiff[(size_t)row * W + x] : 0u;
             }
-            if (x < tiles_x) s_n[row * tiles_x + x] += carry + incl;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+            for (int q = 0; q < kPlanRowChunks; ++q) {
+                const int x = c0 + q * 32 + lane;
+                if (c0 + q * 32 >= tiles_x) break;
+                uint32_t incl = v[q];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (x < tiles_x) s_n[row * tiles_x + x] += carry + incl;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
         }
     }
     __syncthreads();
@@ -249,20 +302,25 @@ __global__ void __launch_bounds__(1024) k_tile_plan(const uint32_t* __restrict__
         if (D > cap_dup) atomicAdd(overflows, 1ull);
     }
     uint64_t run = s_w64[warp] + incl - local;
-    for (int k = 0; fits && k < E; ++k) {
+    for (int k = 0; k < E; ++k) {  // sizes -> starts, in place (each thread owns its items)
         const int t = t0 + k;
         if (t >= tiles) break;
         const uint32_t c = s_n[t];
-        ranges[t] = make_uint2((uint32_t)run, (uint32_t)(run + c));
-        cursor[t] = (uint32_t)run;
+        s_n[t] = (uint32_t)run;
+        if (fits) {
+            ranges[t] = make_uint2((uint32_t)run, (uint32_t)(run + c));
+            cursor[t] = (uint32_t)run;
+        }
         run += c;
     }
+    if (tid == 0) s_n[tiles] = (uint32_t)D;
+    __syncthreads();
     // 3. heavy-first order: log2 buckets of the size, warp-aggregated bucket atomics
     //    (always written: the blend walks every tile, also when nothing is visible)
     const int span = (tiles + 31) & ~31;
     for (int t = tid; t < span; t += blockDim.x) {
         const bool valid = t < tiles;
-        const uint32_t c = valid ? s_n[t] : 0u;
+        const uint32_t c = valid ? s_n[t + 1] - s_n[t] : 0u;
         const uint32_t bkt = valid ? (uint32_t)__clz(c + 1u) : 64u;  // fewer leading zeros = heavier = earlier
         const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
         if (valid && (peers & lt) == 0) atomicAdd(&s_hist[bkt], (uint32_t)__popc(peers));
@@ -271,15 +329,15 @@ __global__ void __launch_bounds__(1024) k_tile_plan(const uint32_t* __restrict__
     if (tid == 0) {
         uint32_t r = 0;
         for (int b = 0; b < 33; ++b) {
-            if (b == 23) plan[0] = r;  // sizes with n + 1 < 512 (per-warp sorts) start here
-            if (b == 31) plan[3] = r;  // empty tiles start here
+            if (b == 23) plan[0] = fits ? r : 0u;  // sizes with n + 1 < 512 (per-warp sorts) start here
+            if (b == 31) plan[3] = fits ? r : 0u;  // empty tiles start here
             s_offs[b] = r, r += s_hist[b];
         }
     }
     __syncthreads();
     for (int t = tid; t < span; t += blockDim.x) {
         const bool valid = t < tiles;
-        const uint32_t c = valid ? s_n[t] : 0u;
+        const uint32_t st = valid ? s_n[t] : 0u, c = valid ? s_n[t + 1] - st : 0u;
         const uint32_t bkt = valid ? (uint32_t)__clz(c + 1u) : 64u;
         const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
         const int leader = __ffs(peers) - 1;
@@ -289,33 +347,21 @@ __global__ void __launch_bounds__(1024) k_tile_plan(const uint32_t* __restrict__
         if (valid) {
             const uint32_t p = base + __popc(peers & lt);
             order[p] = (uint32_t)t;
-        }
-    }
-    __syncthreads();
-    if (!fits) {
-        if (tid == 0) plan[0] = plan[1] = plan[3] = plan[4] = 0;
-        return;
-    }
-    // 4. per position: bucket range; tiles of more than one chunk listed for the merge
-    __shared__ uint32_t s_nextra;
-    if (tid == 0) s_nextra = 0;
-    __syncthreads();
-    const uint32_t nonempty = plan[3];
-    for (uint32_t p = tid; p < nonempty; p += blockDim.x) {
-        const uint32_t t = order[p];
-        const uint2 rg = ranges[t];
-        prange[p] = rg;
-        const uint32_t R = (rg.y - rg.x + kTileCap - 1) / kTileCap;
-        if (R > 1) {
-            big_list[atomicAdd(&s_nbig, 1u)] = p;
-            const uint32_t e0 = atomicAdd(&s_nextra, R - 1);
-            for (uint32_t k = 1; k < R; ++k) extra[e0 + k - 1] = make_uint2(p, k);
+            if (fits && c) {
+                prange[p] = make_uint2(st, st + c);
+                const uint32_t R = (c + kTileCap - 1) / kTileCap;  // tiles merged from several chunks
+                if (R > 1) {
+                    big_list[atomicAdd(&s_nbig, 1u)] = p;
+                    const uint32_t e0 = atomicAdd(&s_nextra, R - 1);
+                    for (uint32_t k = 1; k < R; ++k) extra[e0 + k - 1] = make_uint2(p, k);
+                }
+            }
         }
     }
     __syncthreads();
     if (tid == 0) {
-        plan[1] = s_nbig;
-        plan[4] = s_nextra;
+        plan[1] = fits ? s_nbig : 0u;
+        plan[4] = fits ? s_nextra : 0u;
     }
 }
 
@@ -333,51 +379,80 @@ __device__ __forceinline__ void put_entry(uint32_t pos, uint32_t tile, uint32_t 
     }
 }
 
-// Per block of 256 consecutive cut entries: (1) small footprints (<= 4 tiles)
-// get block-local ranks per tile from the shared table and are listed as
-// (tile, rank, slot, splat) pairs with the splat's record staged in shared
-// memory; (2) one cursor atomic per distinct tile reserves the block's range of
-// each tile's bucket; (3) all threads write the listed pairs densely (reach mask
-// + entry); (4) larger footprints are emitted by the whole warp, huge ones
-// queued for k_bucket_huge.
+// Lookup only: slot of `key` or -1 (absent).
+template <int kLog>
+__device__ __forceinline__ int hash_find(HashTab<kLog>& h, uint32_t key) {
+    uint32_t s = (key * 0x9E3779B1u) >> (32 - kLog);
+    for (int p = 0; p < 32; ++p) {
+        const uint32_t k = h.key[s];
+        if (k == key) return (int)s;
+        if (k == kEmpty) return -1;
+        s = (s + 1) & (HashTab<kLog>::kSlots - 1);
+    }
+    return -1;
+}
+
+// Same chunks as k_tile_count (same grid).  (1) The chunk's saved (tile, count)
+// pairs reserve their bucket ranges: the table value becomes the range's next
+// free slot.  (2) Each warp lists its small footprints' (slot, tile) pairs --
+// positions taken from the table with warp-aggregated shared atomics (pairs the
+// count had sent to the global fallback take theirs from the global cursor) --
+// with the splats' records staged per warp, then writes them densely (reach mask
+// + entry).  (3) Footprints of 5..1024 tiles are emitted by the whole warp with
+// global cursor atomics, larger ones queued for k_bucket_huge.  One barrier.
 struct BucketPair {
-    uint32_t rank;
-    int16_t slot;
-    uint16_t local;
+    uint32_t pos;
     uint16_t tx, ty;
+    uint32_t local;
 };
+constexpr int kBucketWarps = 8;
 __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ dupcount, const uint4* __restrict__ dinfo,
-                                                const ProjRec* __restrict__ proj, const uint64_t* __restrict__ n_ptr,
-                                                const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
-                                                uint32_t* __restrict__ cursor, uint32_t* __restrict__ zk,
-                                                uint32_t* __restrict__ ids, uint8_t* __restrict__ bm,
-                                                uint32_t* __restrict__ huge_q, uint32_t* __restrict__ huge_n,
-                                                uint64_t* __restrict__ dbg_keys, uint32_t* __restrict__ dbg_vals) {
-    __shared__ HashTab<10> h;  // 256 entries x <= 4 tiles
-    __shared__ BucketPair s_pair[256 * kBigArea];
-    __shared__ float4 s_rec[256][3];  // p0, p1, p3 of the block's small footprints
-    __shared__ uint32_t s_z[256], s_npairs;
+                                                   const ProjRec* __restrict__ proj, const uint64_t* __restrict__ n_ptr,
+                                                   const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
+                                                   uint32_t* __restrict__ cursor, const uint2* __restrict__ saved,
+                                                   const uint32_t* __restrict__ saved_n, uint32_t* __restrict__ zk,
+                                                   uint32_t* __restrict__ ids, uint8_t* __restrict__ bm,
+                                                   uint32_t* __restrict__ huge_q, uint32_t* __restrict__ huge_n,
+                                                   uint64_t* __restrict__ dbg_keys, uint32_t* __restrict__ dbg_vals) {
+    __shared__ HashTab<kChunkLog> h;
+    __shared__ BucketPair s_pair[kBucketWarps][32 * kBigArea];
+    __shared__ float4 s_rec[kBucketWarps][32][3];  // p0, p1, p3 of the warp's small footprints
+    __shared__ uint32_t s_z[kBucketWarps][32];
     if (*sort_n_ptr == 0) return;  // nothing visible, or over capacity
-    const uint64_t n = *n_ptr;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
+    uint64_t lo, hi;
+    chunk_range(*n_ptr, lo, hi);
     hash_init(h);
-    if (tid == 0) s_npairs = 0;
     __syncthreads();
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = base + tid;
-        {   // the next block's records travel to L2 while this block is processed
-            const uint64_t nx = i + (uint64_t)gridDim.x * blockDim.x;
-            if (nx < n) {
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(dupcount + nx));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(dinfo + nx));
+    {
+        const uint32_t nu = saved_n[blockIdx.x];
+        const uint2* sv = saved + (size_t)blockIdx.x * kChunkSlots;
+        for (uint32_t u = tid; u < nu; u += blockDim.x) {
+            const uint2 e = sv[u];
+            if (e.x & kMarkBit) continue;
+            const int sl = hash_slot(h, e.x);
+            if (sl >= 0) h.val[sl] = atomicAdd(&cursor[e.x], e.y);  // else: its pairs use the global cursor
+        }
+    }
+    __syncthreads();
+    BucketPair* wp = s_pair[warp];
+    // loads one block ahead; the block after next is prefetched into L2
+    uint32_t cnt_n = lo + tid < hi ? dupcount[lo + tid] : 0u;
+    uint4 di_n = lo + tid < hi ? dinfo[lo + tid] : make_uint4(0, 0, 0, 0);
+    for (uint64_t base = lo + (tid & ~31); base < hi; base += blockDim.x) {
+        const uint64_t i = base + lane;
+        const uint32_t cnt = cnt_n;
+        const uint4 di = di_n;
+        {
+            const uint64_t nx = i + blockDim.x;
+            cnt_n = nx < hi ? dupcount[nx] : 0u;
+            di_n = nx < hi ? dinfo[nx] : make_uint4(0, 0, 0, 0);
+            if (nx < hi) {
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(proj + nx));
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(proj + nx) + 32));
             }
         }
-        const uint32_t cnt = i < n ? dupcount[i] : 0u;
-        uint4 di = make_uint4(0, 0, 0, 0);
-        if (cnt) di = dinfo[i];
         const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff;
         const int w = max(tx1 - tx0, 1);
         const bool small = cnt != 0 && cnt <= (uint32_t)kBigArea;
@@ -387,53 +462,43 @@ __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ 
             const ProjRec* r = proj + i;
             p0 = r->p0, p1 = r->p1, p3 = r->p3;
         }
+        __syncwarp();  // the previous round's staging is consumed
         if (small) {
-            s_rec[tid][0] = p0, s_rec[tid][1] = p1, s_rec[tid][2] = p3;
-            s_z[tid] = di.z;
+            s_rec[warp][lane][0] = p0, s_rec[warp][lane][1] = p1, s_rec[warp][lane][2] = p3;
+            s_z[warp][lane] = di.z;
         }
-        // 1. block-local ranks, pairs listed warp by warp
-        {
-            const uint32_t np = small ? cnt : 0u;
-            uint32_t incl = np;
+        // 1. positions of the small footprints' pairs, listed per warp
+        uint32_t np = 0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+        for (int k = 0; k < kBigArea; ++k) {
+            const bool has = small && (uint32_t)k < cnt;
+            const uint32_t hb = __ballot_sync(0xffffffffu, has);
+            if (!hb) break;
+            const uint16_t tx = (uint16_t)(tx0 + k % w), ty = (uint16_t)(ty0 + k / w);
+            const uint32_t tile = (uint32_t)ty * tiles_x + tx;
+            const uint32_t key = has ? tile : kEmpty;
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            const int leader = __ffs(peers) - 1;
+            uint32_t pos = 0;
+            if (has && lane == leader) {
+                const int sl = hash_find(h, tile);
+                pos = sl >= 0 ? atomicAdd(&h.val[sl], (uint32_t)__popc(peers))
+                              : atomicAdd(&cursor[tile], (uint32_t)__popc(peers));
             }
-            uint32_t wbase = 0;
-            if (lane == 31 && incl) wbase = atomicAdd(&s_npairs, incl);
-            wbase = __shfl_sync(0xffffffffu, wbase, 31);
-            uint32_t q = wbase + incl - np;
-#pragma unroll
-            for (int k = 0; k < kBigArea; ++k) {
-                const bool has = small && (uint32_t)k < cnt;
-                if (!__any_sync(0xffffffffu, has)) break;
-                const uint32_t tile = (uint32_t)((ty0 + k / w) * tiles_x + tx0 + k % w);
-                int slot;
-                const uint32_t rank = hash_add(h, has, tile, 1u, slot, cursor);
-                if (has)
-                    s_pair[q++] = BucketPair{rank, (int16_t)slot, (uint16_t)tid, (uint16_t)(tx0 + k % w),
-                                             (uint16_t)(ty0 + k / w)};
-            }
+            pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(peers & lt);
+            if (has) wp[np + __popc(hb & lt)] = BucketPair{pos, tx, ty, (uint32_t)lane};
+            np += __popc(hb);
         }
-        __syncthreads();
-        // 2. one cursor atomic per (block, tile): the slot's value becomes its base
-        for (uint32_t u = tid; u < h.n_used; u += blockDim.x) {
-            const int sl = h.used[u];
-            h.val[sl] = atomicAdd(&cursor[h.key[sl]], h.val[sl]);
+        __syncwarp();
+        // 2. the listed pairs, every lane busy
+        for (uint32_t q = lane; q < np; q += 32) {
+            const BucketPair pr = wp[q];
+            const uint32_t mask = tile_reach_mask(s_rec[warp][pr.local][0], s_rec[warp][pr.local][1],
+                                                  s_rec[warp][pr.local][2], pr.tx * kTile, pr.ty * kTile);
+            put_entry(pr.pos, (uint32_t)pr.ty * tiles_x + pr.tx, (uint32_t)(base + pr.local), s_z[warp][pr.local],
+                      mask, zk, ids, bm, dbg_keys, dbg_vals);
         }
-        __syncthreads();
-        // 3. the listed pairs, all threads busy
-        const uint32_t npairs = s_npairs;
-        for (uint32_t q = tid; q < npairs; q += blockDim.x) {
-            const BucketPair pr = s_pair[q];
-            const uint32_t pos = pr.slot >= 0 ? h.val[pr.slot] + pr.rank : pr.rank;
-            const uint32_t mask = tile_reach_mask(s_rec[pr.local][0], s_rec[pr.local][1], s_rec[pr.local][2],
-                                                  pr.tx * kTile, pr.ty * kTile);
-            put_entry(pos, (uint32_t)pr.ty * tiles_x + pr.tx, (uint32_t)(base + pr.local), s_z[pr.local], mask, zk,
-                      ids, bm, dbg_keys, dbg_vals);
-        }
-        // 4. huge footprints: one queue slot each (k_bucket_huge)
+        // 3. huge footprints: one queue slot each (k_bucket_huge)
         const bool huge = cnt > (uint32_t)kHugeArea;
         const uint32_t hm = __ballot_sync(0xffffffffu, huge);
         if (hm) {
@@ -442,10 +507,10 @@ __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ 
             q = __shfl_sync(0xffffffffu, q, __ffs(hm) - 1) + __popc(hm & lt);
             if (huge) huge_q[q] = (uint32_t)i;
         }
-        // 5. larger footprints: the whole warp emits one splat's tiles (distinct tiles per instruction)
+        // 4. larger footprints: the whole warp emits one splat's tiles (distinct tiles per instruction)
         for (uint32_t m = __ballot_sync(0xffffffffu, big); m; m &= m - 1) {
             const int src = __ffs(m) - 1;
-            const uint32_t sid = (uint32_t)(base + (tid & ~31) + src);
+            const uint32_t sid = (uint32_t)(base + src);
             const uint32_t sa = __shfl_sync(0xffffffffu, cnt, src), sz = __shfl_sync(0xffffffffu, di.z, src);
             const int sx0 = __shfl_sync(0xffffffffu, tx0, src), sy0 = __shfl_sync(0xffffffffu, ty0, src);
             const int sw = __shfl_sync(0xffffffffu, w, src);
@@ -464,10 +529,6 @@ __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ 
                 put_entry(pos, tile, sid, sz, mask, zk, ids, bm, dbg_keys, dbg_vals);
             }
         }
-        // reset the table and the pair list for the next block
-        __syncthreads();
-        if (tid == 0) s_npairs = 0;
-        hash_drain(h, [](uint32_t, uint32_t) {});
     }
 }
 
@@ -882,27 +943,10 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tile_sort(const uint32_t* __r
             fix_ties(rkey, ridx, n, b.iA, s, tid, kTsThreads);
             __syncthreads();
             if (R == 1) {
-                // gathers of 4 entries in flight per thread
-#pragma unroll
-                for (int q0 = 0; q0 < kMaxItems; q0 += 4) {
-                    uint32_t gi[4], gm[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t i = tid + (q0 + q) * kTsThreads;
-                        if (i < n) {
-                            const uint32_t x = s + ridx[i];
-                            gi[q] = __ldcg(b.iA + x);
-                            gm[q] = __ldcg(b.mA + x);
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t i = tid + (q0 + q) * kTsThreads;
-                        if (i < n) {
-                            b.zB[s + i] = (tile << 8) | gm[q];
-                            b.iB[s + i] = gi[q];
-                        }
-                    }
+                // tile key and source slot; k_tile_finalize gathers id and mask
+                for (uint32_t i = tid; i < n; i += kTsThreads) {
+                    b.zB[s + i] = kPending | tile << 8;
+                    b.iB[s + i] = s + ridx[i];
                 }
             } else {
                 // a sorted run (bits(z), id, mask) for the merge rounds
@@ -959,26 +1003,9 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tile_sort(const uint32_t* __r
                 }
                 fix_ties(rkey, ridx, n, b.iA, s, lane, 32);
                 __syncwarp();
-#pragma unroll
-                for (int q0 = 0; q0 < kMaxItems; q0 += 4) {
-                    uint32_t gi[4], gm[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t i = lane + (q0 + q) * 32;
-                        if (i < n) {
-                            const uint32_t x = s + ridx[i];
-                            gi[q] = __ldcg(b.iA + x);
-                            gm[q] = __ldcg(b.mA + x);
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t i = lane + (q0 + q) * 32;
-                        if (i < n) {
-                            b.zB[s + i] = (tile << 8) | gm[q];
-                            b.iB[s + i] = gi[q];
-                        }
-                    }
+                for (uint32_t i = lane; i < n; i += 32) {
+                    b.zB[s + i] = kPending | tile << 8;
+                    b.iB[s + i] = s + ridx[i];
                 }
             }
         } else {
@@ -1043,6 +1070,44 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tile_sort(const uint32_t* __r
     }
 }
 
+// k_tile_sort leaves the sorted lists as (kPending | tile << 8, source slot in
+// the bucket arrays): gather each entry's splat id and reach mask, many loads in
+// flight per thread.  Entries of merged tiles (written final by the merge's last
+// round, kPending clear) are left as they are.
+__device__ __forceinline__ void finalize_one(uint32_t& z, uint32_t& x, const uint32_t* __restrict__ iA,
+                                             const uint8_t* __restrict__ mA) {
+    if (z & kPending) {
+        const uint32_t src = x;
+        x = __ldcg(iA + src);
+        z = (z & ~kPending) | __ldcg(mA + src);
+    }
+}
+__global__ void __launch_bounds__(256) k_tile_finalize(const uint64_t* __restrict__ sort_n_ptr,
+                                                       const uint32_t* __restrict__ iA, const uint8_t* __restrict__ mA,
+                                                       uint32_t* __restrict__ zB, uint32_t* __restrict__ iB) {
+    const uint64_t n = *sort_n_ptr;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
+    for (uint64_t j0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; j0 < n; j0 += stride) {
+        if (j0 + 4 <= n) {
+            uint4 x = __ldcg(reinterpret_cast<const uint4*>(iB + j0));
+            uint4 z = __ldcg(reinterpret_cast<const uint4*>(zB + j0));
+            finalize_one(z.x, x.x, iA, mA);
+            finalize_one(z.y, x.y, iA, mA);
+            finalize_one(z.z, x.z, iA, mA);
+            finalize_one(z.w, x.w, iA, mA);
+            *reinterpret_cast<uint4*>(iB + j0) = x;
+            *reinterpret_cast<uint4*>(zB + j0) = z;
+        } else {
+            for (uint64_t j = j0; j < n; ++j) {
+                uint32_t x = iB[j], z = zB[j];
+                finalize_one(z, x, iA, mA);
+                iB[j] = x;
+                zB[j] = z;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ launchers
 static int bucket_sms() {
     static int sms = 0;
@@ -1055,37 +1120,45 @@ static int bucket_sms() {
     return sms;
 }
 
+// k_tile_count and k_bucket share the chunking: the same grid
+static unsigned chunk_grid(uint64_t n_max) {
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)bucket_sms() * 8));
+}
+uint64_t bucket_saved_words(uint64_t n_max) { return (uint64_t)chunk_grid(n_max) * (kChunkSlots * 2 + 1); }
+
 void launch_tile_count(const uint32_t* dupcount, const uint4* dinfo, const uint64_t* n_ptr, uint64_t n_max,
-                       int tiles_x, uint32_t* tcount, uint32_t* rowdiff, cudaStream_t s) {
-    const unsigned grid =
-        (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)bucket_sms() * 8));
-    k_tile_count<<<grid, 256, 0, s>>>(dupcount, dinfo, n_ptr, tiles_x, tcount, rowdiff);
+                       int tiles_x, uint32_t* tcount, uint32_t* rowdiff, uint32_t* saved, cudaStream_t s) {
+    const unsigned grid = chunk_grid(n_max);
+    k_tile_count<<<grid, 256, 0, s>>>(dupcount, dinfo, n_ptr, tiles_x, tcount, rowdiff,
+                                      reinterpret_cast<uint2*>(saved), saved + (size_t)grid * kChunkSlots * 2);
     note_launch();
 }
 
-void launch_tile_plan(const uint32_t* tcount, const uint32_t* rowdiff, int tiles_x, int tiles_y, uint64_t cap_dup,
+void launch_tile_plan(uint32_t* tcount, const uint32_t* rowdiff, int tiles_x, int tiles_y, uint64_t cap_dup,
                       uint2* ranges, uint32_t* cursor, uint32_t* order, uint2* prange, uint32_t* big_list,
                       uint2* extra, uint32_t* plan, uint64_t* n_dup, uint64_t* sort_n, unsigned long long* overflows,
                       cudaStream_t s) {
-    const size_t smem = (size_t)tiles_x * tiles_y * 4;
+    size_t smem = ((size_t)tiles_x * tiles_y + 1) * 4;
     static size_t opted = 0;
+    const bool in_smem = smem <= 200 * 1024;
+    if (!in_smem) smem = 0;
     if (smem > 48 * 1024 && smem > opted) {
         cudaFuncSetAttribute(k_tile_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         opted = smem;
     }
-    k_tile_plan<<<1, 1024, smem, s>>>(tcount, rowdiff, tiles_x, tiles_y, cap_dup, ranges, cursor, order, prange,
+    k_tile_plan<<<1, 1024, smem, s>>>(tcount, rowdiff, tiles_x, tiles_y, in_smem, cap_dup, ranges, cursor, order, prange,
                                       big_list, extra, plan, n_dup, sort_n, overflows);
     note_launch();
 }
 
 void launch_bucket(const uint32_t* dupcount, const uint4* dinfo, const ProjRec* proj, const uint64_t* n_ptr,
-                   uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* cursor, uint32_t* zk,
-                   uint32_t* ids, uint8_t* bm, uint32_t* huge_q, uint32_t* huge_n, uint64_t* dbg_keys,
+                   uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* cursor, const uint32_t* saved,
+                   uint32_t* zk, uint32_t* ids, uint8_t* bm, uint32_t* huge_q, uint32_t* huge_n, uint64_t* dbg_keys,
                    uint32_t* dbg_vals, cudaStream_t s) {
-    const unsigned grid =
-        (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)bucket_sms() * 4));
-    k_bucket<<<grid, 256, 0, s>>>(dupcount, dinfo, proj, n_ptr, sort_n_ptr, tiles_x, cursor, zk, ids, bm, huge_q,
-                                  huge_n, dbg_keys, dbg_vals);
+    const unsigned grid = chunk_grid(n_max);
+    k_bucket<<<grid, 256, 0, s>>>(dupcount, dinfo, proj, n_ptr, sort_n_ptr, tiles_x, cursor,
+                                  reinterpret_cast<const uint2*>(saved), saved + (size_t)grid * kChunkSlots * 2, zk,
+                                  ids, bm, huge_q, huge_n, dbg_keys, dbg_vals);
     note_launch();
     k_bucket_huge<<<(unsigned)bucket_sms() * 4, 256, 0, s>>>(dinfo, proj, huge_q, huge_n, sort_n_ptr, tiles_x, cursor,
                                                              zk, ids, bm, dbg_keys, dbg_vals);
@@ -1105,6 +1178,8 @@ void launch_tile_sort(const uint32_t* order, const uint2* prange, const uint32_t
     const unsigned grid = (unsigned)std::max(1, std::min(bucket_sms(), tiles));
     k_tile_sort<<<grid, kTsThreads, kTileSortSmem, s>>>(order, prange, big_list, extra, plan, sort_n_ptr, b, done,
                                                         task_ctr);
+    note_launch();
+    k_tile_finalize<<<(unsigned)bucket_sms() * 8, 256, 0, s>>>(sort_n_ptr, iA, mA, zB, iB);
     note_launch();
 }
 
