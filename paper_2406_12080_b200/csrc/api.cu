@@ -293,7 +293,7 @@ uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 // per-warp block lists.
 struct ScratchLayout {
     size_t blend_counter = 0, huge_counter = 4, touch_ticket = 8, task_counter = 12, plan = 32, tcount = 64,
-           rowdiff = 0, done = 0, zero_bytes = 0, cursor = 0, prange = 0, big_list = 0, extra = 0, saved = 0,
+           rowdiff = 0, zero_bytes = 0, cursor = 0, prange = 0, parts = 0, merges = 0, saved = 0,
            vis_counter = 0,
            vis_status = 0, depth_sort = 0, depth_zero_end = 0, blend_list = 0, total = 0;
 };
@@ -301,13 +301,12 @@ ScratchLayout scratch_layout(uint64_t n_max, uint64_t cap_dup, int tiles_x, int 
     ScratchLayout L;
     const uint64_t tiles = (uint64_t)tiles_x * tiles_y;
     L.rowdiff = round_up(L.tcount + (tiles + 1) * 4, 256);
-    L.done = round_up(L.rowdiff + (uint64_t)(tiles_x + 1) * tiles_y * 4, 256);
-    L.zero_bytes = round_up(L.done + tiles * 4, 256);
+    L.zero_bytes = round_up(L.rowdiff + (uint64_t)(tiles_x + 1) * tiles_y * 4, 256);
     L.cursor = L.zero_bytes;
     L.prange = round_up(L.cursor + tiles * 4, 256);
-    L.big_list = round_up(L.prange + tiles * 8, 256);
-    L.extra = round_up(L.big_list + tiles * 4, 256);
-    L.saved = round_up(L.extra + hs::tile_sort_extra_slots(cap_dup) * 8, 256);
+    L.parts = round_up(L.prange + tiles * 8, 256);
+    L.merges = round_up(L.parts + hs::tile_sort_part_slots(cap_dup, (int)tiles) * 16, 256);
+    L.saved = round_up(L.merges + hs::tile_sort_part_slots(cap_dup, (int)tiles) * 16, 256);
     L.vis_counter = round_up(L.saved + hs::bucket_saved_words(n_max) * 4, 256);
     L.vis_status = L.vis_counter + 64;
     L.depth_sort = round_up(L.vis_status + hs::scan_status_words(n_max) * 8, 256);
@@ -432,10 +431,8 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
                           reinterpret_cast<uint32_t*>(sc + L.rowdiff), reinterpret_cast<uint32_t*>(sc + L.saved), s);
     hs::launch_tile_plan(tcount, reinterpret_cast<uint32_t*>(sc + L.rowdiff), cp.tiles_x, cp.tiles_y, f->cap_dup,
                          f->ranges.as<uint2>(), reinterpret_cast<uint32_t*>(sc + L.cursor),
-                         f->tile_order.as<uint32_t>(), reinterpret_cast<uint2*>(sc + L.prange),
-                         reinterpret_cast<uint32_t*>(sc + L.big_list), reinterpret_cast<uint2*>(sc + L.extra), plan,
-                         &ds->n_dup, &ds->sort_n, &ds->overflows,
-                         s);
+                         f->tile_order.as<uint32_t>(), reinterpret_cast<uint2*>(sc + L.prange), plan, &ds->n_dup,
+                         &ds->sort_n, &ds->overflows, s);
     uint32_t* kb[2] = {f->keys[0].as<uint32_t>(), f->keys[1].as<uint32_t>()};
     uint32_t* vb[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
     uint8_t* bm = f->bmask.as<uint8_t>();
@@ -444,10 +441,10 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
                       reinterpret_cast<uint32_t*>(sc + L.saved), kb[1], vb[1], bm, f->huge.as<uint32_t>(),
                       reinterpret_cast<uint32_t*>(sc + L.huge_counter), ctx->debug ? f->dupk.as<uint64_t>() : nullptr,
                       ctx->debug ? f->dupv.as<uint32_t>() : nullptr, s);
-    hs::launch_tile_sort(f->tile_order.as<uint32_t>(), reinterpret_cast<uint2*>(sc + L.prange),
-                         reinterpret_cast<uint32_t*>(sc + L.big_list), reinterpret_cast<uint2*>(sc + L.extra), plan, &ds->sort_n, tiles, kb[1], vb[1], bm, kb[0], vb[0], f->mkeys.as<uint32_t>(),
-                         f->mvals.as<uint32_t>(), bm + f->cap_dup,
-                         reinterpret_cast<uint32_t*>(sc + L.done), reinterpret_cast<uint32_t*>(sc + L.task_counter), s);
+    hs::launch_tile_sort(f->tile_order.as<uint32_t>(), reinterpret_cast<uint2*>(sc + L.prange), plan, &ds->sort_n,
+                         kb[1], vb[1], bm, kb[0], vb[0], f->mkeys.as<uint32_t>(), f->mvals.as<uint32_t>(),
+                         bm + f->cap_dup, sc + L.parts, sc + L.merges,
+                         reinterpret_cast<uint32_t*>(sc + L.task_counter), s);
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[3], s));
     const int fin = 0;
     if (f->timed) HS_CUDA(ctx, cudaEventRecord(f->ev[4], s));

@@ -40,11 +40,16 @@
 
 namespace hs {
 
-constexpr uint32_t kTileCap = 16384;  // entries one CTA sorts in shared memory
-constexpr int kTsThreads = 1024, kTsWarps = kTsThreads / 32;
+constexpr uint32_t kTileCap = 4096;  // entries one CTA sorts in shared memory
+constexpr int kTsThreads = 256, kTsWarps = kTsThreads / 32;
 constexpr int kMaxItems = kTileCap / kTsThreads;  // 16 keys per thread (CTA sort) or per lane (warp sort)
-constexpr uint32_t kWarpCap = 32 * kMaxItems;     // per-warp sort capacity (small tiles)
-constexpr uint32_t kSmallMax = 510;   // tiles up to this size are sorted per warp (n + 1 < 512)
+constexpr uint32_t kWarpCap = 32 * kMaxItems;     // per-warp sort capacity (tiles of < 512 entries)
+// size classes by clz(n) in the heavy-first order: big (n >= 4096, clz <= 19, split by
+// key range first), regular (512 <= n < 4096, one CTA), small (1 <= n < 512, one warp)
+constexpr uint32_t kBigBucket = 20, kSmallBucket = 23, kEmptyBucket = 32;
+constexpr int kSplitBits = 12;             // k_tile_split: key-range buckets of a big tile
+constexpr uint32_t kPartTarget = kTileCap / 2;  // partitions start every 2048 entries
+constexpr uint32_t kFromC = 0x80000000u;   // source slot in the split buffer (k_tile_finalize)
 constexpr int kCountDirect = 8;       // k_tile_count: larger footprints use row difference marks
 constexpr int kBigArea = 4;           // k_bucket: larger footprints are emitted by the whole warp
 constexpr int kHugeArea = 1024;       // larger still: one CTA per splat (k_bucket_huge)
@@ -202,17 +207,16 @@ __global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__
 // ------------------------------------------------------------------ plan
 // One CTA of 1024 threads; per-tile starts in shared memory (dynamic, 4 B per
 // tile + 4).  Heavy-first position p holds tile order[p] with bucket range
-// prange[p].  plan[] = {CTA-sorted tiles (= first per-warp position), tiles
-// larger than kTileCap (big_list: their positions, merged), -, non-empty tiles,
-// their further chunks (extra: (position, chunk))}.  Global loads are issued
-// in batches so each phase waits for memory once.
+// prange[p]: big tiles (>= 4096 entries) at [0, plan[1]), regular ones at
+// [plan[1], plan[0]), small ones at [plan[0], plan[3]), then the empty ones.
+// plan[4..6] are the split's task counters.  Global loads are issued in
+// batches so each phase waits for memory once.
 constexpr int kPlanRowChunks = 16;  // rows of up to 512 tiles in registers
 __global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const uint32_t* __restrict__ rowdiff,
                                                     int tiles_x, int tiles_y, bool smem_sizes,
                                                     uint64_t cap_dup, uint2* __restrict__ ranges,
                                                     uint32_t* __restrict__ cursor, uint32_t* __restrict__ order,
-                                                    uint2* __restrict__ prange, uint32_t* __restrict__ big_list,
-                                                    uint2* __restrict__ extra, uint32_t* __restrict__ plan,
+                                                    uint2* __restrict__ prange, uint32_t* __restrict__ plan,
                                                     uint64_t* __restrict__ n_dup, uint64_t* __restrict__ sort_n,
                                                     unsigned long long* __restrict__ overflows) {
     // [tiles + 1]: sizes, then exclusive starts -- in shared memory when it fits
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const u
     extern __shared__ uint32_t s_dyn[];
     uint32_t* s_n = smem_sizes ? s_dyn : tcount;
     __shared__ uint64_t s_w64[32];
-    __shared__ uint32_t s_hist[33], s_offs[33], s_nbig, s_nextra;
+    __shared__ uint32_t s_hist[33], s_offs[33];
     __shared__ uint64_t s_total;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tiles = tiles_x * tiles_y;
@@ -239,7 +243,6 @@ __global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const u
         }
     }
     if (tid < 33) s_hist[tid] = 0;
-    if (tid == 0) s_nbig = 0, s_nextra = 0;
     __syncthreads();
     // 1. large footprints: prefix of each row's difference marks
     const int W = tiles_x + 1;
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const u
     for (int t = tid; t < span; t += blockDim.x) {
         const bool valid = t < tiles;
         const uint32_t c = valid ? s_n[t + 1] - s_n[t] : 0u;
-        const uint32_t bkt = valid ? (uint32_t)__clz(c + 1u) : 64u;  // fewer leading zeros = heavier = earlier
+        const uint32_t bkt = valid ? (uint32_t)__clz(c) : 64u;  // fewer leading zeros = heavier = earlier
         const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
         if (valid && (peers & lt) == 0) atomicAdd(&s_hist[bkt], (uint32_t)__popc(peers));
     }
@@ -329,8 +332,9 @@ __global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const u
     if (tid == 0) {
         uint32_t r = 0;
         for (int b = 0; b < 33; ++b) {
-            if (b == 23) plan[0] = fits ? r : 0u;  // sizes with n + 1 < 512 (per-warp sorts) start here
-            if (b == 31) plan[3] = fits ? r : 0u;  // empty tiles start here
+            if (b == (int)kBigBucket) plan[1] = fits ? r : 0u;    // regular tiles start here
+            if (b == (int)kSmallBucket) plan[0] = fits ? r : 0u;  // small tiles start here
+            if (b == (int)kEmptyBucket) plan[3] = fits ? r : 0u;  // empty tiles start here
             s_offs[b] = r, r += s_hist[b];
         }
     }
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const u
     for (int t = tid; t < span; t += blockDim.x) {
         const bool valid = t < tiles;
         const uint32_t st = valid ? s_n[t] : 0u, c = valid ? s_n[t + 1] - st : 0u;
-        const uint32_t bkt = valid ? (uint32_t)__clz(c + 1u) : 64u;
+        const uint32_t bkt = valid ? (uint32_t)__clz(c) : 64u;
         const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
         const int leader = __ffs(peers) - 1;
         uint32_t base = 0;
@@ -347,22 +351,10 @@ __global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const u
         if (valid) {
             const uint32_t p = base + __popc(peers & lt);
             order[p] = (uint32_t)t;
-            if (fits && c) {
-                prange[p] = make_uint2(st, st + c);
-                const uint32_t R = (c + kTileCap - 1) / kTileCap;  // tiles merged from several chunks
-                if (R > 1) {
-                    big_list[atomicAdd(&s_nbig, 1u)] = p;
-                    const uint32_t e0 = atomicAdd(&s_nextra, R - 1);
-                    for (uint32_t k = 1; k < R; ++k) extra[e0 + k - 1] = make_uint2(p, k);
-                }
-            }
+            if (fits && c) prange[p] = make_uint2(st, st + c);
         }
     }
-    __syncthreads();
-    if (tid == 0) {
-        plan[1] = fits ? s_nbig : 0u;
-        plan[4] = fits ? s_nextra : 0u;
-    }
+    if (tid == 0) plan[4] = plan[5] = plan[6] = 0;  // split / merge task counters (k_tile_split)
 }
 
 // ------------------------------------------------------------------ bucket
@@ -565,15 +557,159 @@ struct TileBufs {
     uint32_t *zA, *iA;  // bucketed (bits(z), id, mask); merge ping-pong buffer
     uint8_t* mA;
     uint32_t *zB, *iB;  // final (tile << 8 | mask, id)
-    uint32_t *zC, *iC;  // sorted chunks of tiles larger than kTileCap; merge ping-pong buffer
+    uint32_t *zC, *iC;  // big tiles partitioned by key range (k_tile_split); merge ping-pong buffer
     uint8_t* mC;
 };
+// A partition of a big tile: entries [start, start + count) of the C buffers, all
+// with keys below the next partition's.
+struct Part {
+    uint32_t tile, start, count, pad;
+};
 
-// (merge reads go to L2: the chunks were written by other CTAs during this launch)
+// (merge reads go to L2: the runs were written by this CTA through L1-bypassing stores)
 __device__ __forceinline__ uint64_t key_at(const uint32_t* z, const uint32_t* id, uint32_t x) {
     return ((uint64_t)__ldcg(z + x) << 32) | __ldcg(id + x);
 }
 __device__ __forceinline__ int ceil_log2(uint32_t v) { return v <= 1 ? 0 : 32 - __clz(v - 1); }
+
+// Big tiles (>= 4096 entries; heavy-first positions [0, plan[1])), one CTA each:
+// the key range is cut into 4096 buckets of the top bits of (key - min), the
+// entries are scattered bucket by bucket into the C buffers (same range), and a
+// partition starts at the first bucket beginning after each multiple of 2048
+// entries -- so every partition holds < 2048 + (largest bucket) entries and all
+// its keys lie below the next partition's.  Partitions of <= 4096 entries are
+// sorted like regular tiles (parts[]); larger ones (a bucket of > 2048 nearly
+// equal depths) are sorted in chunks and merged (merges[]).
+constexpr int kSplitThreads = 1024, kSplitItems = 16;  // tiles of <= 16384 entries held in registers
+__global__ void __launch_bounds__(kSplitThreads, 1) k_tile_split(const uint32_t* __restrict__ order,
+                                                                 const uint2* __restrict__ prange,
+                                                                 uint32_t* __restrict__ plan,
+                                                                 const uint64_t* __restrict__ sort_n_ptr, TileBufs b,
+                                                                 Part* __restrict__ parts, Part* __restrict__ merges) {
+    constexpr int NB = 1 << kSplitBits, PER = NB / kSplitThreads;
+    __shared__ uint32_t s_cnt[NB];
+    __shared__ uint32_t s_w[32], s_min, s_max;
+    if (*sort_n_ptr == 0) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n_big = plan[1];
+    for (uint32_t p = blockIdx.x; p < n_big; p += gridDim.x) {
+        const uint32_t tile = order[p];
+        const uint2 rg = prange[p];
+        const uint32_t s = rg.x, n = rg.y - rg.x;
+        const bool in_regs = n <= (uint32_t)(kSplitThreads * kSplitItems);
+        if (tid == 0) s_min = 0xFFFFFFFFu, s_max = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) s_cnt[tid * PER + q] = 0;
+        // one read of the tile (all loads in flight) when it fits the registers
+        uint32_t kv[kSplitItems], iv[kSplitItems], mv[kSplitItems / 4];
+        uint32_t kmin = 0xFFFFFFFFu, kmax = 0;
+        if (in_regs) {
+#pragma unroll
+            for (int k = 0; k < kSplitItems; ++k) {
+                const uint32_t i = tid + k * kSplitThreads;
+                kv[k] = i < n ? __ldcg(b.zA + s + i) : 0u;
+                iv[k] = i < n ? __ldcg(b.iA + s + i) : 0u;
+                const uint32_t m = i < n ? (uint32_t)__ldcg(b.mA + s + i) : 0u;
+                if (k & 3) mv[k >> 2] |= m << (8 * (k & 3)); else mv[k >> 2] = m;
+            }
+#pragma unroll
+            for (int k = 0; k < kSplitItems; ++k)
+                if (tid + k * kSplitThreads < n) kmin = min(kmin, kv[k]), kmax = max(kmax, kv[k]);
+        } else {
+            for (uint32_t i = tid; i < n; i += kSplitThreads) {
+                const uint32_t k = __ldcg(b.zA + s + i);
+                kmin = min(kmin, k), kmax = max(kmax, k);
+            }
+        }
+        kmin = __reduce_min_sync(0xffffffffu, kmin);
+        kmax = __reduce_max_sync(0xffffffffu, kmax);
+        __syncthreads();
+        if (lane == 0) atomicMin(&s_min, kmin), atomicMax(&s_max, kmax);
+        __syncthreads();
+        kmin = s_min;
+        const uint32_t diff = s_max - kmin;
+        const int span = diff ? 32 - __clz(diff) : 0;
+        const int sh = span > kSplitBits ? span - kSplitBits : 0;
+        if (in_regs) {
+#pragma unroll
+            for (int k = 0; k < kSplitItems; ++k)
+                if (tid + k * kSplitThreads < n) atomicAdd(&s_cnt[(kv[k] - kmin) >> sh], 1u);
+        } else {
+            for (uint32_t i = tid; i < n; i += kSplitThreads)
+                atomicAdd(&s_cnt[(__ldcg(b.zA + s + i) - kmin) >> sh], 1u);
+        }
+        __syncthreads();
+        // exclusive scan of the bucket sizes (PER per thread)
+        uint32_t v[PER], tot = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) v[q] = s_cnt[tid * PER + q], tot += v[q];
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_w[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t w = s_w[lane];
+            uint32_t wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += y;
+            }
+            s_w[lane] = wi - w;
+        }
+        __syncthreads();
+        uint32_t base = s_w[warp] + incl - tot;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) s_cnt[tid * PER + q] = base, base += v[q];
+        __syncthreads();
+        // partitions: the q-th starts at the first bucket whose start is >= q * 2048
+        const uint32_t P = (n + kPartTarget - 1) / kPartTarget;
+        auto first_bucket = [&](uint32_t target) {  // first bucket with start >= target (NB if none)
+            uint32_t lo = 0, hi = NB;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (s_cnt[mid] < target) lo = mid + 1; else hi = mid;
+            }
+            return lo;
+        };
+        for (uint32_t q = tid; q < P; q += kSplitThreads) {
+            const uint32_t b0 = q == 0 ? 0u : first_bucket(q * kPartTarget);
+            const uint32_t b1 = q + 1 == P ? (uint32_t)NB : first_bucket((q + 1) * kPartTarget);
+            const uint32_t st = b0 < NB ? s_cnt[b0] : n, en = b1 < NB ? s_cnt[b1] : n;
+            if (en > st) {
+                const Part pt{tile, s + st, en - st, 0u};
+                if (en - st <= kTileCap) parts[atomicAdd(&plan[4], 1u)] = pt;
+                else merges[atomicAdd(&plan[5], 1u)] = pt;
+            }
+        }
+        __syncthreads();
+        // scatter through the bucket cursors (order within a bucket is free:
+        // partitions are sorted whole)
+        if (in_regs) {
+#pragma unroll
+            for (int k = 0; k < kSplitItems; ++k) {
+                if (tid + k * kSplitThreads >= n) continue;
+                const uint32_t dst = s + atomicAdd(&s_cnt[(kv[k] - kmin) >> sh], 1u);
+                b.zC[dst] = kv[k];
+                b.iC[dst] = iv[k];
+                b.mC[dst] = (uint8_t)(mv[k >> 2] >> (8 * (k & 3)));
+            }
+        } else {
+            for (uint32_t i = tid; i < n; i += kSplitThreads) {
+                const uint32_t k = __ldcg(b.zA + s + i);
+                const uint32_t dst = s + atomicAdd(&s_cnt[(k - kmin) >> sh], 1u);
+                b.zC[dst] = k;
+                b.iC[dst] = __ldcg(b.iA + s + i);
+                b.mC[dst] = __ldcg(b.mA + s + i);
+            }
+        }
+        __syncthreads();
+    }
+}
 
 // Shared memory of k_tile_sort: one CTA-wide sort (<= 16384 entries) or 32
 // per-warp sorts (<= 512 entries each) over the same bytes.  Keys and 16-bit
@@ -582,7 +718,7 @@ __device__ __forceinline__ int ceil_log2(uint32_t v) { return v <= 1 ? 0 : 32 - 
 struct CtaSort {
     uint32_t key[2][kTileCap];
     uint16_t idx[2][kTileCap];
-    uint32_t cnt[kTsWarps][128];  // LSD: digit d of warp w = halfword d of row w; MSD: 4096 u32 buckets
+    uint32_t cnt[kTsWarps][128];  // LSD: digit d of warp w = halfword d of row w; MSD: buckets (+ idx[1])
     uint32_t part[kTsWarps / 8][256];
     uint32_t wsum[8];
 };
@@ -855,114 +991,113 @@ __device__ __forceinline__ void fix_ties(const uint32_t* __restrict__ key, uint1
     }
 }
 
-__global__ void __launch_bounds__(kTsThreads, 1) k_tile_sort(const uint32_t* __restrict__ order,
+// Sort n <= kTileCap keys of (zs, s) held by the CTA; returns the sorted keys and
+// their local indices (into [s, s + n)) in shared memory.
+__device__ __forceinline__ void cta_sort(CtaSort& cs, const uint32_t* __restrict__ zs, const uint32_t* __restrict__ is,
+                                         uint32_t s, uint32_t n, uint32_t* s_red, const uint32_t*& rkey,
+                                         uint16_t*& ridx) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int E = (int)((n + kTsThreads - 1) / kTsThreads);
+    const uint32_t N = (uint32_t)E * kTsThreads;
+    uint32_t kand = 0xFFFFFFFFu, kor = 0, kmin = 0xFFFFFFFFu, kmax = 0;
+#pragma unroll
+    for (int q0 = 0; q0 < kMaxItems; q0 += 8) {
+        uint32_t kv[8];  // 8 loads in flight before the first use
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t i = tid + (q0 + q) * kTsThreads;
+            kv[q] = i < n ? __ldcg(zs + s + i) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t i = tid + (q0 + q) * kTsThreads;
+            if (i < n) {
+                cs.key[0][i] = kv[q];
+                cs.idx[0][i] = (uint16_t)i;
+                kand &= kv[q], kor |= kv[q], kmin = min(kmin, kv[q]), kmax = max(kmax, kv[q]);
+            }
+        }
+    }
+    kand = __reduce_and_sync(0xffffffffu, kand);
+    kor = __reduce_or_sync(0xffffffffu, kor);
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if (lane == 0) {
+        atomicAnd(&s_red[0], kand);
+        atomicOr(&s_red[1], kor);
+        atomicMin(&s_red[2], kmin);
+        atomicMax(&s_red[3], kmax);
+    }
+    __syncthreads();
+    kand = s_red[0], kor = s_red[1];
+    rkey = cs.key[1];
+    ridx = cs.idx[0];
+    if (!msd_sort<kTsWarps, 11>(cs, n, s_red[2], s_red[3])) {
+        // pads: the OR of all keys is >= every key and shares their common bytes;
+        // they start after every real entry, so the stable passes keep them last
+        for (uint32_t i = n + tid; i < N; i += kTsThreads) cs.key[0][i] = kor, cs.idx[0][i] = (uint16_t)i;
+        __syncthreads();
+        const int cur = sort_group<kTsWarps>(cs, E, warp, kand, kor);
+        rkey = cs.key[cur], ridx = cs.idx[cur];
+    }
+    fix_ties(rkey, ridx, n, is, s, tid, kTsThreads);
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kTsThreads, 4) k_tile_sort(const uint32_t* __restrict__ order,
                                                              const uint2* __restrict__ prange,
-                                                             const uint32_t* __restrict__ big_list,
-                                                             const uint2* __restrict__ extra,
                                                              const uint32_t* __restrict__ plan,
                                                              const uint64_t* __restrict__ sort_n_ptr, TileBufs b,
-                                                             uint32_t* __restrict__ done,
+                                                             const Part* __restrict__ parts,
+                                                             const Part* __restrict__ merges,
                                                              uint32_t* __restrict__ task_ctr) {
     extern __shared__ __align__(16) unsigned char ts_smem[];
     CtaSort& cs = *reinterpret_cast<CtaSort*>(ts_smem);
-    __shared__ uint32_t s_next, s_and, s_or, s_min, s_max;
+    __shared__ uint32_t s_next, s_red[4];
     if (*sort_n_ptr == 0) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // task table: [CTA-sorted tiles (chunk 0)] [further chunks of tiles > kTileCap]
-    //             [groups of 32 per-warp tiles] [merges of tiles > kTileCap]
-    const uint32_t n_cta = plan[0], n_big = plan[1], nonempty = plan[3], n_extra = plan[4];
-    const uint32_t n_small_tasks = (nonempty - n_cta + kTsWarps - 1) / kTsWarps;
-    const uint32_t t_small = n_cta + n_extra, t_merge = t_small + n_small_tasks, n_tasks = t_merge + n_big;
+    // task table: [partitions of big tiles] [regular tiles] [groups of 8 small tiles]
+    //             [oversized partitions: chunks + merge]
+    const uint32_t n_parts = plan[4], n_merges = plan[5];
+    const uint32_t first_reg = plan[1], first_small = plan[0], nonempty = plan[3];
+    const uint32_t t_reg = n_parts, t_small = t_reg + (first_small - first_reg);
+    const uint32_t t_merge = t_small + (nonempty - first_small + kTsWarps - 1) / kTsWarps;
+    const uint32_t n_tasks = t_merge + n_merges;
     if (tid == 0) s_next = atomicAdd(task_ctr, 1u);
     while (true) {
-        if (tid == 0) {
-            s_and = 0xFFFFFFFFu;
-            s_or = 0;
-            s_min = 0xFFFFFFFFu;
-            s_max = 0;
-        }
+        if (tid == 0) s_red[0] = 0xFFFFFFFFu, s_red[1] = 0, s_red[2] = 0xFFFFFFFFu, s_red[3] = 0;
         __syncthreads();
         const uint32_t task = s_next;
         if (task >= n_tasks) break;
         __syncthreads();
         if (tid == 0) s_next = atomicAdd(task_ctr, 1u);  // the next task's index arrives meanwhile
         if (task < t_small) {
-            // a CTA-sorted tile, or one further chunk of a tile larger than kTileCap
-            uint32_t p = task, k = 0;
-            if (task >= n_cta) {
-                const uint2 e = extra[task - n_cta];
-                p = e.x, k = e.y;
-            }
-            const uint32_t tile = order[p];
-            const uint2 rg = prange[p];
-            const uint32_t R = (rg.y - rg.x + kTileCap - 1) / kTileCap;
-            const uint32_t s = rg.x + k * kTileCap, n = min(kTileCap, rg.y - s);
-            const int E = (int)((n + kTsThreads - 1) / kTsThreads);
-            const uint32_t N = (uint32_t)E * kTsThreads;
-            uint32_t kand = 0xFFFFFFFFu, kor = 0, kmin = 0xFFFFFFFFu, kmax = 0;
-#pragma unroll
-            for (int q0 = 0; q0 < kMaxItems; q0 += 8) {
-                uint32_t kv[8];  // 8 loads in flight before the first use
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const uint32_t i = tid + (q0 + q) * kTsThreads;
-                    kv[q] = i < n ? __ldcg(b.zA + s + i) : 0u;
-                }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const uint32_t i = tid + (q0 + q) * kTsThreads;
-                    if (i < n) {
-                        cs.key[0][i] = kv[q];
-                        cs.idx[0][i] = (uint16_t)i;
-                        kand &= kv[q], kor |= kv[q], kmin = min(kmin, kv[q]), kmax = max(kmax, kv[q]);
-                    }
-                }
-            }
-            kand = __reduce_and_sync(0xffffffffu, kand);
-            kor = __reduce_or_sync(0xffffffffu, kor);
-            kmin = __reduce_min_sync(0xffffffffu, kmin);
-            kmax = __reduce_max_sync(0xffffffffu, kmax);
-            if (lane == 0) {
-                atomicAnd(&s_and, kand);
-                atomicOr(&s_or, kor);
-                atomicMin(&s_min, kmin);
-                atomicMax(&s_max, kmax);
-            }
-            __syncthreads();
-            kand = s_and, kor = s_or;
-            const uint32_t* rkey = cs.key[1];
-            uint16_t* ridx = cs.idx[0];
-            if (!msd_sort<kTsWarps, 13>(cs, n, s_min, s_max)) {
-                // pads: the OR of all keys is >= every key and shares their common bytes;
-                // they start after every real entry, so the stable passes keep them last
-                for (uint32_t i = n + tid; i < N; i += kTsThreads) cs.key[0][i] = kor, cs.idx[0][i] = (uint16_t)i;
-                __syncthreads();
-                const int cur = sort_group<kTsWarps>(cs, E, warp, kand, kor);
-                rkey = cs.key[cur], ridx = cs.idx[cur];
-            }
-            fix_ties(rkey, ridx, n, b.iA, s, tid, kTsThreads);
-            __syncthreads();
-            if (R == 1) {
-                // tile key and source slot; k_tile_finalize gathers id and mask
-                for (uint32_t i = tid; i < n; i += kTsThreads) {
-                    b.zB[s + i] = kPending | tile << 8;
-                    b.iB[s + i] = s + ridx[i];
-                }
+            // a partition of a big tile (keys in C) or a regular tile (keys in A)
+            const bool part = task < t_reg;
+            uint32_t tile, s, n;
+            if (part) {
+                const Part pt = parts[task];
+                tile = pt.tile, s = pt.start, n = pt.count;
             } else {
-                // a sorted run (bits(z), id, mask) for the merge rounds
-                for (uint32_t i = tid; i < n; i += kTsThreads) {
-                    const uint32_t x = s + ridx[i];
-                    b.zC[s + i] = rkey[i];
-                    b.iC[s + i] = b.iA[x];
-                    b.mC[s + i] = b.mA[x];
-                }
-                __threadfence();
-                __syncthreads();
-                if (tid == 0) atomicAdd(&done[p], 1u);
+                const uint32_t p = first_reg + (task - t_reg);
+                tile = order[p];
+                const uint2 rg = prange[p];
+                s = rg.x, n = rg.y - rg.x;
+            }
+            const uint32_t* zs = part ? b.zC : b.zA;
+            const uint32_t* is = part ? b.iC : b.iA;
+            const uint32_t src_flag = part ? kFromC : 0u;
+            const uint32_t* rkey;
+            uint16_t* ridx;
+            cta_sort(cs, zs, is, s, n, s_red, rkey, ridx);
+            // tile key and source slot; k_tile_finalize gathers id and mask
+            for (uint32_t i = tid; i < n; i += kTsThreads) {
+                b.zB[s + i] = kPending | tile << 8;
+                b.iB[s + i] = src_flag | (s + ridx[i]);
             }
         } else if (task < t_merge) {
-            // 32 small tiles, one per warp
-            const uint32_t p = n_cta + (task - t_small) * kTsWarps + warp;
+            // 8 small tiles, one per warp
+            const uint32_t p = first_small + (task - t_small) * kTsWarps + warp;
             WarpSort& ws = reinterpret_cast<WarpSort*>(ts_smem)[warp];
             if (p < nonempty) {
                 const uint32_t tile = order[p];
@@ -1009,27 +1144,38 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tile_sort(const uint32_t* __r
                 }
             }
         } else {
-            // merge of a large tile's sorted chunks: pairwise rounds, merge path per thread
-            const int p = (int)big_list[task - t_merge];
-            const uint32_t tile = order[p];
-            const uint2 rg = prange[p];
-            const uint32_t R = (rg.y - rg.x + kTileCap - 1) / kTileCap;
-            const uint32_t N = rg.y - rg.x, base = rg.x;
-            if (tid == 0) {
-                while (ld_volatile_u32(&done[p]) < R) __nanosleep(256);
-                __threadfence();
+            // an oversized partition (> 4096 entries of nearly equal depth): sorted runs of
+            // 4096 in A (free: its entries moved to C), then pairwise merge-path rounds
+            // A -> C -> ... -> B (final, not pending)
+            const Part pt = merges[task - t_merge];
+            const uint32_t tile = pt.tile, base = pt.start, N = pt.count;
+            const uint32_t R = (N + kTileCap - 1) / kTileCap;
+            for (uint32_t k = 0; k < R; ++k) {
+                const uint32_t s = base + k * kTileCap, n = min(kTileCap, N - k * kTileCap);
+                if (tid == 0) s_red[0] = 0xFFFFFFFFu, s_red[1] = 0, s_red[2] = 0xFFFFFFFFu, s_red[3] = 0;
+                __syncthreads();
+                const uint32_t* rkey;
+                uint16_t* ridx;
+                cta_sort(cs, b.zC, b.iC, s, n, s_red, rkey, ridx);
+                for (uint32_t i = tid; i < n; i += kTsThreads) {
+                    const uint32_t x = s + ridx[i];
+                    b.zA[s + i] = rkey[i];
+                    b.iA[s + i] = __ldcg(b.iC + x);
+                    b.mA[s + i] = __ldcg(b.mC + x);
+                }
+                __syncthreads();
             }
-            __syncthreads();
+            __threadfence_block();
             const int rounds = ceil_log2(R);
-            bool srcC = true;
+            bool srcA = true;
             for (int r = 0; r < rounds; ++r) {
                 const bool last = r == rounds - 1;
-                const uint32_t* zs = srcC ? b.zC : b.zA;
-                const uint32_t* is = srcC ? b.iC : b.iA;
-                const uint8_t* ms = srcC ? b.mC : b.mA;
-                uint32_t* zd = last ? b.zB : (srcC ? b.zA : b.zC);
-                uint32_t* id = last ? b.iB : (srcC ? b.iA : b.iC);
-                uint8_t* md = srcC ? b.mA : b.mC;
+                const uint32_t* zs = srcA ? b.zA : b.zC;
+                const uint32_t* is = srcA ? b.iA : b.iC;
+                const uint8_t* ms = srcA ? b.mA : b.mC;
+                uint32_t* zd = last ? b.zB : (srcA ? b.zC : b.zA);
+                uint32_t* id = last ? b.iB : (srcA ? b.iC : b.iA);
+                uint8_t* md = srcA ? b.mC : b.mA;
                 const uint32_t w = kTileCap << r;
                 for (uint32_t lo0 = 0; lo0 < N; lo0 += 2 * w) {
                     const uint32_t La = min(w, N - lo0), Lb = min(w, N - lo0 - La), L = La + Lb;
@@ -1063,46 +1209,50 @@ __global__ void __launch_bounds__(kTsThreads, 1) k_tile_sort(const uint32_t* __r
                 }
                 __threadfence_block();
                 __syncthreads();
-                srcC = !srcC;
+                srcA = !srcA;
+            }
+            if (rounds == 0) {  // one run: copy it out in the final format
+                for (uint32_t i = tid; i < N; i += kTsThreads) {
+                    b.zB[base + i] = (tile << 8) | __ldcg(b.mA + base + i);
+                    b.iB[base + i] = __ldcg(b.iA + base + i);
+                }
             }
         }
-        __syncthreads();  // s_and .. s_max and the shared buffers are reused
+        __syncthreads();  // s_red and the shared buffers are reused
     }
 }
 
 // k_tile_sort leaves the sorted lists as (kPending | tile << 8, source slot in
-// the bucket arrays): gather each entry's splat id and reach mask, many loads in
-// flight per thread.  Entries of merged tiles (written final by the merge's last
-// round, kPending clear) are left as they are.
-__device__ __forceinline__ void finalize_one(uint32_t& z, uint32_t& x, const uint32_t* __restrict__ iA,
-                                             const uint8_t* __restrict__ mA) {
+// the bucket arrays A, or with kFromC in the split arrays C): gather each
+// entry's splat id and reach mask, many loads in flight per thread.  Entries of
+// merged partitions (written final, kPending clear) are left as they are.
+__device__ __forceinline__ void finalize_one(uint32_t& z, uint32_t& x, const TileBufs& b) {
     if (z & kPending) {
-        const uint32_t src = x;
-        x = __ldcg(iA + src);
-        z = (z & ~kPending) | __ldcg(mA + src);
+        const uint32_t src = x & ~kFromC;
+        const bool c = (x & kFromC) != 0;
+        x = __ldcg((c ? b.iC : b.iA) + src);
+        z = (z & ~kPending) | __ldcg((c ? b.mC : b.mA) + src);
     }
 }
-__global__ void __launch_bounds__(256) k_tile_finalize(const uint64_t* __restrict__ sort_n_ptr,
-                                                       const uint32_t* __restrict__ iA, const uint8_t* __restrict__ mA,
-                                                       uint32_t* __restrict__ zB, uint32_t* __restrict__ iB) {
+__global__ void __launch_bounds__(256) k_tile_finalize(const uint64_t* __restrict__ sort_n_ptr, TileBufs b) {
     const uint64_t n = *sort_n_ptr;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;
     for (uint64_t j0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; j0 < n; j0 += stride) {
         if (j0 + 4 <= n) {
-            uint4 x = __ldcg(reinterpret_cast<const uint4*>(iB + j0));
-            uint4 z = __ldcg(reinterpret_cast<const uint4*>(zB + j0));
-            finalize_one(z.x, x.x, iA, mA);
-            finalize_one(z.y, x.y, iA, mA);
-            finalize_one(z.z, x.z, iA, mA);
-            finalize_one(z.w, x.w, iA, mA);
-            *reinterpret_cast<uint4*>(iB + j0) = x;
-            *reinterpret_cast<uint4*>(zB + j0) = z;
+            uint4 x = __ldcg(reinterpret_cast<const uint4*>(b.iB + j0));
+            uint4 z = __ldcg(reinterpret_cast<const uint4*>(b.zB + j0));
+            finalize_one(z.x, x.x, b);
+            finalize_one(z.y, x.y, b);
+            finalize_one(z.z, x.z, b);
+            finalize_one(z.w, x.w, b);
+            *reinterpret_cast<uint4*>(b.iB + j0) = x;
+            *reinterpret_cast<uint4*>(b.zB + j0) = z;
         } else {
             for (uint64_t j = j0; j < n; ++j) {
-                uint32_t x = iB[j], z = zB[j];
-                finalize_one(z, x, iA, mA);
-                iB[j] = x;
-                zB[j] = z;
+                uint32_t x = b.iB[j], z = b.zB[j];
+                finalize_one(z, x, b);
+                b.iB[j] = x;
+                b.zB[j] = z;
             }
         }
     }
@@ -1135,8 +1285,8 @@ void launch_tile_count(const uint32_t* dupcount, const uint4* dinfo, const uint6
 }
 
 void launch_tile_plan(uint32_t* tcount, const uint32_t* rowdiff, int tiles_x, int tiles_y, uint64_t cap_dup,
-                      uint2* ranges, uint32_t* cursor, uint32_t* order, uint2* prange, uint32_t* big_list,
-                      uint2* extra, uint32_t* plan, uint64_t* n_dup, uint64_t* sort_n, unsigned long long* overflows,
+                      uint2* ranges, uint32_t* cursor, uint32_t* order, uint2* prange, uint32_t* plan,
+                      uint64_t* n_dup, uint64_t* sort_n, unsigned long long* overflows,
                       cudaStream_t s) {
     size_t smem = ((size_t)tiles_x * tiles_y + 1) * 4;
     static size_t opted = 0;
@@ -1147,7 +1297,7 @@ void launch_tile_plan(uint32_t* tcount, const uint32_t* rowdiff, int tiles_x, in
         opted = smem;
     }
     k_tile_plan<<<1, 1024, smem, s>>>(tcount, rowdiff, tiles_x, tiles_y, in_smem, cap_dup, ranges, cursor, order, prange,
-                                      big_list, extra, plan, n_dup, sort_n, overflows);
+                                      plan, n_dup, sort_n, overflows);
     note_launch();
 }
 
@@ -1165,25 +1315,28 @@ void launch_bucket(const uint32_t* dupcount, const uint4* dinfo, const ProjRec* 
     note_launch();
 }
 
-void launch_tile_sort(const uint32_t* order, const uint2* prange, const uint32_t* big_list, const uint2* extra,
-                      const uint32_t* plan, const uint64_t* sort_n_ptr, int tiles, uint32_t* zA, uint32_t* iA,
-                      uint8_t* mA, uint32_t* zB, uint32_t* iB, uint32_t* zC, uint32_t* iC, uint8_t* mC,
-                      uint32_t* done, uint32_t* task_ctr, cudaStream_t s) {
-    static bool init = false;
-    if (!init) {
+void launch_tile_sort(const uint32_t* order, const uint2* prange, uint32_t* plan, const uint64_t* sort_n_ptr,
+                      uint32_t* zA, uint32_t* iA, uint8_t* mA, uint32_t* zB, uint32_t* iB, uint32_t* zC, uint32_t* iC,
+                      uint8_t* mC, void* parts, void* merges, uint32_t* task_ctr, cudaStream_t s) {
+    static int per = 0;
+    if (!per) {
         cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSortSmem);
-        init = true;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_sort, kTsThreads, kTileSortSmem);
+        if (per < 1) per = 1;
     }
     TileBufs b{zA, iA, mA, zB, iB, zC, iC, mC};
-    const unsigned grid = (unsigned)std::max(1, std::min(bucket_sms(), tiles));
-    k_tile_sort<<<grid, kTsThreads, kTileSortSmem, s>>>(order, prange, big_list, extra, plan, sort_n_ptr, b, done,
-                                                        task_ctr);
+    k_tile_split<<<(unsigned)bucket_sms(), kSplitThreads, 0, s>>>(order, prange, plan, sort_n_ptr, b,
+                                                            static_cast<Part*>(parts), static_cast<Part*>(merges));
     note_launch();
-    k_tile_finalize<<<(unsigned)bucket_sms() * 8, 256, 0, s>>>(sort_n_ptr, iA, mA, zB, iB);
+    k_tile_sort<<<(unsigned)(bucket_sms() * per), kTsThreads, kTileSortSmem, s>>>(
+        order, prange, plan, sort_n_ptr, b, static_cast<const Part*>(parts), static_cast<const Part*>(merges),
+        task_ctr);
+    note_launch();
+    k_tile_finalize<<<(unsigned)bucket_sms() * 8, 256, 0, s>>>(sort_n_ptr, b);
     note_launch();
 }
 
 uint64_t bucket_huge_slots(uint64_t dup_max) { return dup_max / kHugeArea + 1; }
-uint64_t tile_sort_extra_slots(uint64_t dup_max) { return dup_max / kTileCap + 1; }
+uint64_t tile_sort_part_slots(uint64_t dup_max, int tiles) { return dup_max / kPartTarget + (uint64_t)tiles + 1; }
 
 }  // namespace hs

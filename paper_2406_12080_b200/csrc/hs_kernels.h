@@ -114,23 +114,22 @@ void launch_make_keys(const uint32_t* tiles, const uint32_t* ids, const uint4* d
 
 // bucket.cu (per-tile depth order: bucketing + in-tile sort, render.hpp:262-294)
 uint64_t bucket_huge_slots(uint64_t dup_max);
-uint64_t tile_sort_extra_slots(uint64_t dup_max);
+uint64_t tile_sort_part_slots(uint64_t dup_max, int tiles);
 // per-CTA (tile, count) tables of k_tile_count for k_bucket (u32 words)
 uint64_t bucket_saved_words(uint64_t n_max);
 void launch_tile_count(const uint32_t* dupcount, const uint4* dinfo, const uint64_t* n_ptr, uint64_t n_max,
                        int tiles_x, uint32_t* tcount, uint32_t* rowdiff, uint32_t* saved, cudaStream_t s);
 void launch_tile_plan(uint32_t* tcount, const uint32_t* rowdiff, int tiles_x, int tiles_y, uint64_t cap_dup,
-                      uint2* ranges, uint32_t* cursor, uint32_t* order, uint2* prange, uint32_t* big_list,
-                      uint2* extra, uint32_t* plan, uint64_t* n_dup, uint64_t* sort_n, unsigned long long* overflows,
-                      cudaStream_t s);
+                      uint2* ranges, uint32_t* cursor, uint32_t* order, uint2* prange, uint32_t* plan,
+                      uint64_t* n_dup, uint64_t* sort_n, unsigned long long* overflows, cudaStream_t s);
 void launch_bucket(const uint32_t* dupcount, const uint4* dinfo, const ProjRec* proj, const uint64_t* n_ptr,
                    uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* cursor, const uint32_t* saved,
                    uint32_t* zk, uint32_t* ids, uint8_t* bm, uint32_t* huge_q, uint32_t* huge_n, uint64_t* dbg_keys,
                    uint32_t* dbg_vals, cudaStream_t s);
-void launch_tile_sort(const uint32_t* order, const uint2* prange, const uint32_t* big_list, const uint2* extra,
-                      const uint32_t* plan, const uint64_t* sort_n_ptr, int tiles, uint32_t* zA, uint32_t* iA,
-                      uint8_t* mA, uint32_t* zB, uint32_t* iB, uint32_t* zC, uint32_t* iC, uint8_t* mC,
-                      uint32_t* done, uint32_t* task_ctr, cudaStream_t s);
+// big-tile split + in-tile sort + finalize; parts / merges hold tile_sort_part_slots 16-byte records each
+void launch_tile_sort(const uint32_t* order, const uint2* prange, uint32_t* plan, const uint64_t* sort_n_ptr,
+                      uint32_t* zA, uint32_t* iA, uint8_t* mA, uint32_t* zB, uint32_t* iB, uint32_t* zC, uint32_t* iC,
+                      uint8_t* mC, void* parts, void* merges, uint32_t* task_ctr, cudaStream_t s);
 
 // sort.cu
 uint64_t sort_status_words(uint64_t n_max);
