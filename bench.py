@@ -42,8 +42,8 @@ def peaks():
 
 # kernels behind each HBM-bound stage (for the per-stage ncu DRAM traffic)
 STAGE_KERNELS = {"cut": ("k_select_cut",), "preprocess": ("k_preprocess<1>",),
-                 "duplicate+sort": ("k_compact_visible", "k_sort_hist", "k_dup_offsets", "k_duplicate_sorted",
-                                    "k_reach_masks", "k_sort_hist_direct")}
+                 "duplicate+sort": ("k_tile_count", "k_tile_plan", "k_bucket", "k_bucket_huge", "k_tile_split",
+                                    "k_tile_sort", "k_tile_finalize")}
 
 
 def pipe_peaks():
