@@ -41,7 +41,7 @@ def peaks():
 
 
 # kernels behind each HBM-bound stage (for the per-stage ncu DRAM traffic)
-STAGE_KERNELS = {"cut": ("k_select_cut",), "preprocess": ("k_preprocess<1>",),
+STAGE_KERNELS = {"cut": ("k_select_cut", "k_cut_offsets", "k_cut_gather"), "preprocess": ("k_preprocess<1>",),
                  "duplicate+sort": ("k_tile_count", "k_tile_plan", "k_bucket", "k_bucket_huge", "k_tile_split",
                                     "k_tile_sort", "k_tile_finalize")}
 
@@ -490,11 +490,14 @@ def main():
                 "gbs": gbs(bytes_cut, stage_ms["cut_expand"]), "formula": "32 N + 12 C"},
         "preprocess": {"ms": stage_ms["preprocess"], "bound": "hbm", "bytes": bytes_pre,
                        "gbs": gbs(bytes_pre, stage_ms["preprocess"]), "formula": "316 C + 240 C_t"},
-        "duplicate+sort": {"ms": stage_ms["duplicate"], "bound": "hbm", "bytes": bytes_scan + bytes_dup + bytes_sort,
-                           "gbs": gbs(bytes_scan + bytes_dup + bytes_sort, stage_ms["duplicate"]),
-                           "formula": f"scan 8 C + duplicate (16 V + 12 D) + sort (8 D + {P} x 24 D)"},
-        "tile_ranges": {"ms": stage_ms["tile_ranges"], "bound": "hbm", "bytes": bytes_ranges,
-                        "gbs": gbs(bytes_ranges, stage_ms["tile_ranges"]), "formula": "8 D + 8 tiles"},
+        # the tile ranges (tile_start) come out of the same kernels (k_tile_plan), so their
+        # bytes are counted with this stage and its time
+        "duplicate+sort": {"ms": stage_ms["duplicate"] + stage_ms["tile_ranges"], "bound": "hbm",
+                           "bytes": bytes_scan + bytes_dup + bytes_sort + bytes_ranges,
+                           "gbs": gbs(bytes_scan + bytes_dup + bytes_sort + bytes_ranges,
+                                      stage_ms["duplicate"] + stage_ms["tile_ranges"]),
+                           "formula": f"scan 8 C + duplicate (16 V + 12 D) + sort (8 D + {P} x 24 D) "
+                                      "+ tile ranges (8 D + 8 tiles)"},
         "alpha_blend": {"ms": stage_ms["alpha_blend"], "bound": "fp32"},
     }
     # blend: SURVEY.md §8(d) ops per (pixel, entry) evaluation, N_eval counted on the device as
@@ -516,10 +519,16 @@ def main():
     mufu_ops = 0.0 if exact else NX + 2 * NP             # ex2; lg2 + ex2
     blend_tf = fp32_ops / blend_s / 1e12
     traffic, traffic_src = ncu_traffic()
-    blend_key = "k_blend<0>" if args.mode == "exact" else "k_blend<1>"
+
+    def tget(name):  # ncu names carry template arguments: k_blend<0, 0>
+        for k, v in traffic.items():
+            if k == name or k.startswith(name + "<") or k.startswith(name.rstrip(">") + ","):
+                return v
+        return {}
+    blend_key = "k_blend<0" if args.mode == "exact" else "k_blend<1"
     roofline = {"bound": "fp32", "kernel": "k_blend", "achieved": blend_tf, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": blend_tf / fp32_peak,
-                "traffic": traffic.get(blend_key, {}).get("dram_bytes"),
+                "traffic": tget(blend_key).get("dram_bytes"),
                 "traffic_source": traffic_src,
                 "formula": "FP32 ops = 20 N_eval + 10 N_eval,t (SURVEY.md §8d); N_eval = executed evaluations "
                            "up to and including each pixel's break",
@@ -531,12 +540,12 @@ def main():
                 "mufu": {"achieved_tops": mufu_ops / blend_s / 1e12,
                          "peak_tops": pp["mufu_ex2_tops"] if pp else None} if not exact else None,
                 # what bounds it (same ncu capture): instruction issue, not DRAM or one math pipe
-                "ncu_pct_of_peak": traffic.get(blend_key, {}).get("pct_of_peak"),
+                "ncu_pct_of_peak": tget(blend_key).get("pct_of_peak"),
                 "algorithmic_bytes": 8 * D_ + 64 * D_ + 20 * W * H,
                 "peak_source": fp32_src, "pipe_peaks": pp,
                 "hbm_stages": {k: {"gbs": v.get("gbs"), "frac": (v["gbs"] / hbm) if v.get("gbs") else None,
                                    "bytes": v.get("bytes"), "formula": v.get("formula"),
-                                   "traffic": sum(traffic.get(kk, {}).get("dram_bytes", 0.0)
+                                   "traffic": sum(tget(kk).get("dram_bytes", 0.0)
                                                   for kk in STAGE_KERNELS.get(k, ())) or None}
                                for k, v in stages.items() if v.get("bound") == "hbm"},
                 "hbm_peak_gbs": hbm, "hbm_peak_source": pk_kind}
