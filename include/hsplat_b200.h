@@ -252,6 +252,28 @@ typedef struct hs_grads_out {
  * [E_lin | E_off] or NULL (identity).  Deterministic (no atomics). */
 hs_status hs_render_backward(hs_context* ctx, hs_frame* f, const float* loss_grad, const float* depth_grad,
                              const float* exposure, const hs_grads_out* out);
+/* RefineConfig (refine.hpp:21-34) */
+typedef struct hs_refine_config {
+    float tau_min, tau_max; /* granularity target range, pixels (tau_max exclusive) */
+    int32_t steps;
+    float lr_mean, lr_scale, lr_rotation, lr_falloff, lr_sh;
+    uint64_t rng_seed;
+} hs_refine_config;
+/* replaces: refine_hierarchy (refine.hpp:253-402): SGD over the interior nodes against
+ * training views.  images[v]: 3*H*W plane-major float of cams[v]; exposures: 12 floats
+ * row-major [E_lin | E_off] per view (CameraModel::exposure) or NULL (identity);
+ * loss: `steps` doubles (RefineStats::loss) or NULL; max_screen_grad: N floats
+ * (RefineStats::max_screen_grad) or NULL.  *out: the refined hierarchy (leaves,
+ * topology and bounds unchanged).  Views are drawn and granularity targets sampled with
+ * the reference's std::mt19937_64(rng_seed) streams. */
+hs_status hs_refine_hierarchy(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cams,
+                              const float* const* images, const float* exposures, uint32_t n_views,
+                              const hs_refine_config* cfg, hs_hierarchy** out, double* loss,
+                              float* max_screen_grad);
+/* replaces: photometric_loss (image.hpp:193-206) on 3*H*W plane-major images: loss and
+ * d loss / d pred (grad 3*H*W or NULL), computed on the device */
+hs_status hs_photometric_loss(hs_context* ctx, const float* pred, const float* target, int32_t w, int32_t h,
+                              float* loss, float* grad);
 /* completes an async render (no-op when synchronous) */
 hs_status hs_frame_wait(hs_context* ctx, hs_frame* f);
 hs_status hs_frame_get_info(hs_context* ctx, hs_frame* f, hs_frame_info* info);

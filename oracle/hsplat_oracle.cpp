@@ -12,6 +12,8 @@
 //   render_hierarchy      render.hpp:706-720
 //   bench_path            bench.hpp:55-103
 //   psnr                  image.hpp:111-122
+//   ssim / photometric_loss image.hpp:57-206, apply_exposure render.hpp:410-425
+//   refine_hierarchy      refine.hpp:21-49, 207-402 (the refine step)
 //   parallel_for          parallel.hpp:13-45
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
 // reference legs may load this library.
@@ -35,6 +37,7 @@
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <random>
 #include <limits>
 #include <set>
 #include <string>
@@ -739,6 +742,8 @@ inline void render_hierarchy(const Hierarchy& h, const Camera& cam, float tau, R
 
 }  // namespace oracle
 
+
+
 // =====================================================================
 // extern "C" surface for tests (ctypes).  Structures mirror the product's
 // C ABI (include/hsplat_b200.h) so tests feed identical host buffers to both.
@@ -1053,6 +1058,319 @@ inline void render_backward(const RenderSplat* splats, std::size_t n, const Came
         }
     });
 }
+
+namespace oracle {
+
+// ---------------------------------------------------------------- image.hpp:57-98, 101-108, 124-203
+// ssim_window / conv_same / ssim (+ gradient) / l1_loss / photometric_loss
+inline const float* ssim_window() {  // image.hpp:57-71: 11-tap Gaussian, sigma 1.5
+    static float k[11];
+    static const bool init = [] {
+        double sum = 0.0;
+        for (int i = 0; i < 11; ++i) {
+            const double d = i - 5;
+            const double v = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+            k[i] = static_cast<float>(v);
+            sum += v;
+        }
+        for (float& v : k) v = static_cast<float>(v / sum);
+        return true;
+    }();
+    (void)init;
+    return k;
+}
+
+inline void conv_same(const float* src, float* dst, float* scratch, int w, int h) {  // image.hpp:74-97
+    const float* k = ssim_window();
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            float acc = 0.0f;
+            for (int i = -5; i <= 5; ++i) {
+                const int xi = x + i;
+                if (xi < 0 || xi >= w) continue;
+                acc += k[i + 5] * src[y * w + xi];
+            }
+            scratch[y * w + x] = acc;
+        }
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            float acc = 0.0f;
+            for (int i = -5; i <= 5; ++i) {
+                const int yi = y + i;
+                if (yi < 0 || yi >= h) continue;
+                acc += k[i + 5] * scratch[yi * w + x];
+            }
+            dst[y * w + x] = acc;
+        }
+}
+
+// ssim (image.hpp:124-191) over 3-channel plane-major images; grad (same size) or null
+inline float ssim(const float* a, const float* b, int w, int h, int ch, float* grad) {
+    const std::size_t plane = static_cast<std::size_t>(w) * h;
+    const float c1 = static_cast<float>(0.01 * 0.01), c2 = static_cast<float>(0.03 * 0.03);
+    const float n_total = static_cast<float>(plane * ch);
+    std::vector<float> mu_x(plane), mu_y(plane), m_xx(plane), m_yy(plane), m_xy(plane);
+    std::vector<float> tmp(plane), scratch(plane), fmu(plane), fxx(plane), fxy(plane);
+    double total = 0.0;
+    for (int c = 0; c < ch; ++c) {
+        const float* x = a + c * plane;
+        const float* y = b + c * plane;
+        conv_same(x, mu_x.data(), scratch.data(), w, h);
+        conv_same(y, mu_y.data(), scratch.data(), w, h);
+        for (std::size_t i = 0; i < plane; ++i) tmp[i] = x[i] * x[i];
+        conv_same(tmp.data(), m_xx.data(), scratch.data(), w, h);
+        for (std::size_t i = 0; i < plane; ++i) tmp[i] = y[i] * y[i];
+        conv_same(tmp.data(), m_yy.data(), scratch.data(), w, h);
+        for (std::size_t i = 0; i < plane; ++i) tmp[i] = x[i] * y[i];
+        conv_same(tmp.data(), m_xy.data(), scratch.data(), w, h);
+        for (std::size_t i = 0; i < plane; ++i) {
+            const float sxx = m_xx[i] - mu_x[i] * mu_x[i];
+            const float syy = m_yy[i] - mu_y[i] * mu_y[i];
+            const float sxy = m_xy[i] - mu_x[i] * mu_y[i];
+            const float a1 = 2.0f * mu_x[i] * mu_y[i] + c1;
+            const float a2 = 2.0f * sxy + c2;
+            const float b1 = mu_x[i] * mu_x[i] + mu_y[i] * mu_y[i] + c1;
+            const float b2 = sxx + syy + c2;
+            const float sv = (a1 * a2) / (b1 * b2);
+            total += static_cast<double>(sv);
+            if (grad) {
+                if (sv < 1.0f) {
+                    fxx[i] = -sv / b2;
+                    fxy[i] = 2.0f * a1 / (b1 * b2);
+                    fmu[i] = 2.0f * mu_y[i] * (a2 - a1) / (b1 * b2) - 2.0f * mu_x[i] * sv * (1.0f / b1 - 1.0f / b2);
+                } else {
+                    fxx[i] = fxy[i] = fmu[i] = 0.0f;
+                }
+            }
+        }
+        if (grad) {
+            float* g = grad + c * plane;
+            conv_same(fmu.data(), tmp.data(), scratch.data(), w, h);
+            for (std::size_t i = 0; i < plane; ++i) g[i] = tmp[i];
+            conv_same(fxx.data(), tmp.data(), scratch.data(), w, h);
+            for (std::size_t i = 0; i < plane; ++i) g[i] += 2.0f * x[i] * tmp[i];
+            conv_same(fxy.data(), tmp.data(), scratch.data(), w, h);
+            for (std::size_t i = 0; i < plane; ++i) g[i] += y[i] * tmp[i];
+            for (std::size_t i = 0; i < plane; ++i) g[i] /= n_total;
+        }
+    }
+    return static_cast<float>(total / static_cast<double>(n_total));
+}
+
+inline float l1_loss(const float* a, const float* b, std::size_t n) {  // image.hpp:101-108
+    float sum = 0.0f;
+    for (std::size_t i = 0; i < n; ++i) sum += std::abs(a[i] - b[i]);
+    return sum / static_cast<float>(n);
+}
+
+// photometric_loss (image.hpp:193-206): 0.8 L1 + 0.2 (1 - SSIM) / 2, grad = d loss / d pred
+inline float photometric_loss(const float* pred, const float* target, int w, int h, float* grad) {
+    const std::size_t n = static_cast<std::size_t>(w) * h * 3;
+    const float sv = ssim(pred, target, w, h, 3, grad);
+    const float loss = 0.8f * l1_loss(pred, target, n) + 0.2f * (1.0f - sv) / 2.0f;
+    if (grad) {
+        const float inv_n = 1.0f / static_cast<float>(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            const float sign = pred[i] > target[i] ? 1.0f : pred[i] < target[i] ? -1.0f : 0.0f;
+            grad[i] = 0.8f * sign * inv_n - 0.1f * grad[i];
+        }
+    }
+    return loss;
+}
+
+// apply_exposure (render.hpp:410-425): C' = E_lin C + E_off, plane-major; e row-major 3x4
+inline void apply_exposure(const float* color, const float e[12], std::size_t plane, float* out) {
+    for (std::size_t i = 0; i < plane; ++i) {
+        const float c0 = color[i], c1 = color[plane + i], c2 = color[2 * plane + i];
+        for (int r = 0; r < 3; ++r)
+            out[r * plane + i] = sum3(e[4 * r] * c0, e[4 * r + 1] * c1, e[4 * r + 2] * c2) + e[4 * r + 3];
+    }
+}
+
+// ---------------------------------------------------------------- refine.hpp:21-49, 207-402
+struct RefineConfig {
+    float tau_min = 3.0f, tau_max = 48.0f;
+    int steps = 200;
+    float lr_mean = 1.6e-5f, lr_scale = 5e-4f, lr_rotation = 1e-4f, lr_falloff = 5e-3f, lr_sh = 2.5e-4f;
+    std::uint64_t rng_seed = 0;
+};
+
+inline void validate_refine_config(const RefineConfig& cfg) {  // refine.hpp:36-43
+    require(cfg.tau_min > 0.0f && cfg.tau_min < cfg.tau_max, kInvalidArgument,
+            "granularity range must satisfy 0 < tau_min < tau_max");
+    require(cfg.steps >= 0, kInvalidArgument, "step count must be non-negative");
+    require(cfg.lr_mean >= 0 && cfg.lr_scale >= 0 && cfg.lr_rotation >= 0 && cfg.lr_falloff >= 0 && cfg.lr_sh >= 0,
+            kInvalidArgument, "learning rates must be non-negative");
+}
+
+inline float sample_tau(float xi, const RefineConfig& cfg) {  // refine.hpp:46-49
+    validate_refine_config(cfg);
+    return std::pow(cfg.tau_max, xi) * std::pow(cfg.tau_min, 1.0f - xi);
+}
+
+struct NodeParams {  // refine.hpp:212-218
+    float mean[3] = {0, 0, 0};
+    float log_scale[3] = {0, 0, 0};
+    float quat[4] = {1, 0, 0, 0};  // w x y z
+    float falloff = 1.0f;
+    float sh[kShValues] = {};
+};
+
+inline NodeParams params_from(const Gaussian& g) {  // refine.hpp:220-228
+    NodeParams p;
+    for (int k = 0; k < 3; ++k) p.mean[k] = g.mean[k], p.log_scale[k] = std::log(smax(g.scale[k], 1e-12f));
+    quat_wxyz(g, p.quat);
+    p.falloff = g.falloff;
+    std::memcpy(p.sh, g.sh, sizeof(p.sh));
+    return p;
+}
+
+inline float norm4(const float q[4]) { return std::sqrt(sum4(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3])); }
+
+inline Gaussian gaussian_from(const NodeParams& p) {  // refine.hpp:230-245
+    Gaussian g;
+    for (int k = 0; k < 3; ++k) g.mean[k] = p.mean[k], g.scale[k] = std::exp(p.log_scale[k]);
+    const float qn = norm4(p.quat);
+    float q[4] = {1, 0, 0, 0};
+    if (qn > 0.0f)
+        for (int k = 0; k < 4; ++k) q[k] = p.quat[k] / qn;
+    g.q_xyzw[0] = q[1], g.q_xyzw[1] = q[2], g.q_xyzw[2] = q[3], g.q_xyzw[3] = q[0];
+    g.falloff = std::abs(p.falloff);
+    std::memcpy(g.sh, p.sh, sizeof(g.sh));
+    return g;
+}
+
+// refine_hierarchy (refine.hpp:253-402); images plane-major 3 x H x W per view,
+// exposures 12 floats per view (row-major [E_lin | E_off]).
+inline Hierarchy refine_hierarchy(const Hierarchy& h, const std::vector<Camera>& cams,
+                                  const std::vector<const float*>& images, const std::vector<const float*>& expos,
+                                  const RefineConfig& cfg, std::vector<double>* loss_out,
+                                  std::vector<float>* max_grad_out) {
+    validate_refine_config(cfg);
+    require(!h.nodes.empty(), kInvalidArgument, "refinement needs a hierarchy");
+    require(cams.size() == images.size() && !cams.empty(), kDimensionMismatch, "need one training image per camera");
+    for (const Camera& c : cams) validate_camera(c);
+    const std::size_t n = h.nodes.size();
+    bool any_interior = false;
+    for (const auto& node : h.nodes) any_interior |= !node.is_leaf();
+    require(any_interior, kNoInteriorNodes, "refinement has nothing to train without interior nodes");
+
+    std::vector<NodeParams> params(n);
+    std::vector<Gaussian> eff(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        if (h.nodes[i].is_leaf()) eff[i] = h.nodes[i].g;
+        else params[i] = params_from(h.nodes[i].g);
+    }
+    if (loss_out) loss_out->clear();
+    if (max_grad_out) max_grad_out->assign(n, 0.0f);
+
+    std::mt19937_64 rng(cfg.rng_seed);
+    std::uniform_int_distribution<std::size_t> pick_view(0, cams.size() - 1);
+    std::uniform_real_distribution<float> uni(0.0f, 1.0f);
+
+    struct Acc {
+        float mean[3], log_scale[3], quat[4], falloff, sh[kShValues];
+    };
+    std::vector<Acc> acc(n);
+    std::vector<std::uint32_t> touched;
+    std::vector<unsigned char> is_touched(n, 0);
+    auto quat_norm_chain = [](const float q[4], const float g[4], float out[4]) {  // refine.hpp:296-301
+        const float qn = norm4(q);
+        if (!(qn > 0.0f)) {
+            out[0] = out[1] = out[2] = out[3] = 0.0f;
+            return;
+        }
+        float qh[4];
+        for (int k = 0; k < 4; ++k) qh[k] = q[k] / qn;
+        const float d = sum4(qh[0] * g[0], qh[1] * g[1], qh[2] * g[2], qh[3] * g[3]);
+        for (int k = 0; k < 4; ++k) out[k] = (g[k] - qh[k] * d) / qn;
+    };
+
+    for (int step = 0; step < cfg.steps; ++step) {
+        const std::size_t view = pick_view(rng);
+        const float tau = sample_tau(uni(rng), cfg);
+        for (std::size_t i = 0; i < n; ++i)
+            if (!h.nodes[i].is_leaf()) eff[i] = gaussian_from(params[i]);
+        const Camera& cam = cams[view];
+        const auto cut = select_cut(h, cam, tau);
+        const auto splats = assemble_cut_splats(h, eff, cut.data(), cut.size());
+        RenderOutput ctx;
+        render_forward(splats.data(), splats.size(), cam, ctx, nullptr, true);
+        const std::size_t plane = static_cast<std::size_t>(cam.width) * cam.height;
+        std::vector<float> exposed(3 * plane), lgrad(3 * plane);
+        apply_exposure(ctx.color.data(), expos[view], plane, exposed.data());
+        const float loss = photometric_loss(exposed.data(), images[view], cam.width, cam.height, lgrad.data());
+        Grads grads;
+        render_backward(splats.data(), splats.size(), cam, ctx, expos[view], lgrad.data(), nullptr, grads);
+        if (loss_out) loss_out->push_back(loss);
+
+        touched.clear();
+        auto mark = [&](std::uint32_t i) {
+            if (is_touched[i]) return;
+            is_touched[i] = 1;
+            touched.push_back(i);
+            std::memset(&acc[i], 0, sizeof(Acc));
+        };
+        for (std::size_t k = 0; k < cut.size(); ++k) {
+            const CutEntry& e = cut[k];
+            const HierarchyNode& node = h.nodes[e.node];
+            if (max_grad_out) {
+                float& mg = (*max_grad_out)[e.node];
+                const float gx = grads.mean2d[2 * k], gy = grads.mean2d[2 * k + 1];
+                mg = smax(mg, std::sqrt(gx * gx + gy * gy));
+            }
+            const bool plain = node.parent == kNoNode || e.t >= 1.0f;
+            const float u = plain ? 1.0f : e.t;
+            auto add = [&](std::uint32_t idx, float w, float quat_sign) {
+                if (h.nodes[idx].is_leaf()) return;
+                mark(idx);
+                Acc& a = acc[idx];
+                for (int c = 0; c < 3; ++c) a.mean[c] += w * grads.mean[3 * k + c];
+                for (int c = 0; c < 3; ++c) a.log_scale[c] += w * (grads.scale[3 * k + c] * eff[idx].scale[c]);
+                const float ws = w * quat_sign;
+                float gq[4], cq[4];
+                for (int c = 0; c < 4; ++c) gq[c] = ws * grads.rotation[4 * k + c];
+                quat_norm_chain(params[idx].quat, gq, cq);
+                for (int c = 0; c < 4; ++c) a.quat[c] += cq[c];
+                for (int s2 = 0; s2 < kShValues; ++s2) a.sh[s2] += w * grads.sh[kShValues * k + s2];
+            };
+            auto add_falloff = [&](std::uint32_t idx, float g) {
+                if (h.nodes[idx].is_leaf()) return;
+                mark(idx);
+                acc[idx].falloff += g * (params[idx].falloff < 0.0f ? -1.0f : 1.0f);
+            };
+            if (plain) {
+                add(e.node, 1.0f, 1.0f);
+                add_falloff(e.node, grads.falloff[k]);
+            } else {
+                float qc[4], qp[4];
+                quat_wxyz(eff[e.node], qc);
+                quat_wxyz(eff[node.parent], qp);
+                const float qsign = sum4(qc[0] * qp[0], qc[1] * qp[1], qc[2] * qp[2], qc[3] * qp[3]) < 0.0f ? -1.0f : 1.0f;
+                add(e.node, u, qsign);
+                add(node.parent, 1.0f - u, 1.0f);
+                add_falloff(e.node, grads.falloff[k]);
+                add_falloff(node.parent, grads.parent_falloff[k]);
+            }
+        }
+        for (std::uint32_t i : touched) {  // refine.hpp:388-396
+            NodeParams& p = params[i];
+            const Acc& a = acc[i];
+            for (int c = 0; c < 3; ++c) p.mean[c] -= cfg.lr_mean * a.mean[c];
+            for (int c = 0; c < 3; ++c) p.log_scale[c] -= cfg.lr_scale * a.log_scale[c];
+            for (int c = 0; c < 4; ++c) p.quat[c] -= cfg.lr_rotation * a.quat[c];
+            p.falloff -= cfg.lr_falloff * a.falloff;
+            for (int s2 = 0; s2 < kShValues; ++s2) p.sh[s2] -= (s2 < 3 ? cfg.lr_sh : cfg.lr_sh / 20.0f) * a.sh[s2];
+            is_touched[i] = 0;
+        }
+    }
+    Hierarchy out = h;
+    for (std::size_t i = 0; i < n; ++i)
+        if (!h.nodes[i].is_leaf()) out.nodes[i].g = gaussian_from(params[i]);
+    return out;
+}
+
+}  // namespace oracle
 
 extern "C" {
 
@@ -1530,6 +1848,47 @@ int or_render_backward(void* fv, const or_splats* s, uint64_t n, const or_camera
         std::memcpy(mean2d, g.mean2d.data(), 8 * n);
         std::memcpy(expo_out, g.exposure, 48);
     });
+}
+
+typedef struct {
+    float tau_min, tau_max;
+    int32_t steps;
+    float lr_mean, lr_scale, lr_rotation, lr_falloff, lr_sh;
+    uint64_t rng_seed;
+} or_refine_config;
+
+// refine_hierarchy (refine.hpp:253-402): images[v] plane-major 3 x H x W of camera v,
+// exposures 12 floats per view (NULL: identity); loss (steps doubles) and max_grad (N)
+// may be NULL; *out receives the refined hierarchy (or_hierarchy_destroy).
+int or_refine_hierarchy(void* hv, const or_camera* cams, uint32_t nviews, const float* const* images,
+                        const float* exposures, const or_refine_config* c, void** out, double* loss,
+                        float* max_grad) {
+    OR_TRY({
+        const auto* h = static_cast<const Hierarchy*>(hv);
+        std::vector<Camera> cv;
+        std::vector<const float*> iv, ev;
+        static const float ident[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
+        for (uint32_t v = 0; v < nviews; ++v) {
+            cv.push_back(to_cam(&cams[v]));
+            iv.push_back(images[v]);
+            ev.push_back(exposures ? exposures + 12 * v : ident);
+        }
+        RefineConfig cfg;
+        cfg.tau_min = c->tau_min, cfg.tau_max = c->tau_max, cfg.steps = c->steps;
+        cfg.lr_mean = c->lr_mean, cfg.lr_scale = c->lr_scale, cfg.lr_rotation = c->lr_rotation;
+        cfg.lr_falloff = c->lr_falloff, cfg.lr_sh = c->lr_sh, cfg.rng_seed = c->rng_seed;
+        std::vector<double> lv;
+        std::vector<float> mg;
+        auto* o = new Hierarchy(refine_hierarchy(*h, cv, iv, ev, cfg, &lv, &mg));
+        *out = o;
+        if (loss) std::memcpy(loss, lv.data(), lv.size() * sizeof(double));
+        if (max_grad) std::memcpy(max_grad, mg.data(), mg.size() * sizeof(float));
+    });
+}
+
+// photometric_loss (image.hpp:193-206) on 3 x H x W images; grad (3HW) may be NULL
+float or_photometric_loss(const float* pred, const float* target, int32_t w, int32_t hgt, float* grad) {
+    return photometric_loss(pred, target, w, hgt, grad);
 }
 
 // psnr (image.hpp:111-122): over all channels in double; mse <= 0 -> 99 dB; capped at 99.

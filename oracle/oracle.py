@@ -38,6 +38,12 @@ class or_splats(C.Structure):
                 ("parent_falloff", f32p), ("t", f32p), ("siblings", i32p)]
 
 
+class or_refine_config(C.Structure):
+    _fields_ = [("tau_min", C.c_float), ("tau_max", C.c_float), ("steps", C.c_int32), ("lr_mean", C.c_float),
+                ("lr_scale", C.c_float), ("lr_rotation", C.c_float), ("lr_falloff", C.c_float),
+                ("lr_sh", C.c_float), ("rng_seed", C.c_uint64)]
+
+
 class or_stage_times(C.Structure):
     _fields_ = [("cut_expand", C.c_double), ("weights", C.c_double), ("preprocess", C.c_double),
                 ("duplicate", C.c_double), ("tile_ranges", C.c_double), ("alpha_blend", C.c_double)]
@@ -78,6 +84,9 @@ _SIGS = {
     "or_project": (C.c_int, [C.POINTER(or_splats), C.POINTER(or_camera), f32p, f32p, f32p]),
     "or_bench_path": (C.c_int, [_vp, C.POINTER(or_camera), C.c_uint64, f64p, C.c_uint64, C.c_float, f64p]),
     "or_psnr": (C.c_double, [f32p, f32p, C.c_uint64]),
+    "or_refine_hierarchy": (C.c_int, [_vp, C.POINTER(or_camera), C.c_uint32, C.POINTER(f32p), f32p,
+                                      C.POINTER(or_refine_config), C.POINTER(_vp), f64p, f32p]),
+    "or_photometric_loss": (C.c_float, [f32p, f32p, C.c_int32, C.c_int32, f32p]),
 }
 
 _lib = None
@@ -404,3 +413,49 @@ def render_backward(frame: OracleFrame, splats, cam, loss_grad, depth_grad=None,
                                                        ("mean", "scale", "rotation", "falloff", "parent_falloff", "t",
                                                         "sh", "mean2d", "exposure")]))
     return out
+
+
+def export_hierarchy(handle) -> dict:
+    """An oracle Hierarchy handle -> SoA numpy arrays (or_hierarchy_export)."""
+    n = int(lib().or_hierarchy_size(handle))
+    d = dict(parent=np.empty(n, np.uint32), first_child=np.empty(n, np.uint32), child_count=np.empty(n, np.uint32),
+             bmin=np.empty((n, 3), np.float32), bmax=np.empty((n, 3), np.float32), mean=np.empty((n, 3), np.float32),
+             scale=np.empty((n, 3), np.float32), rot_wxyz=np.empty((n, 4), np.float32),
+             falloff=np.empty(n, np.float32), sh=np.empty((n, 48), np.float32))
+    lib().or_hierarchy_export(handle, *[_p(d[k], C.c_uint32) for k in ("parent", "first_child", "child_count")],
+                              *[_p(d[k], C.c_float) for k in ("bmin", "bmax", "mean", "scale", "rot_wxyz",
+                                                               "falloff", "sh")])
+    return d
+
+
+def photometric_loss(pred, target, want_grad=True):
+    """photometric_loss (image.hpp:193-206) on (3, H, W) float32 images -> (loss, grad or None)."""
+    p = np.ascontiguousarray(pred, np.float32)
+    t = np.ascontiguousarray(target, np.float32)
+    g = np.empty_like(p) if want_grad else None
+    loss = float(lib().or_photometric_loss(_p(p, C.c_float), _p(t, C.c_float), p.shape[2], p.shape[1],
+                                           _p(g, C.c_float)))
+    return loss, g
+
+
+def refine_hierarchy(oh: OracleHierarchy, cams, images, cfg: dict, exposures=None):
+    """refine_hierarchy (refine.hpp:253-402) -> (refined SoA dict, per-step losses, max_screen_grad)."""
+    nv = len(cams)
+    cv = (or_camera * nv)(*[camera(c) for c in cams])
+    imgs = [np.ascontiguousarray(im, np.float32) for im in images]
+    ptrs = (f32p * nv)(*[_p(im, C.c_float) for im in imgs])
+    ex = None if exposures is None else np.ascontiguousarray(exposures, np.float32).reshape(nv, 12)
+    c = or_refine_config()
+    for k in ("tau_min", "tau_max", "lr_mean", "lr_scale", "lr_rotation", "lr_falloff", "lr_sh"):
+        setattr(c, k, float(cfg[k]))
+    c.steps, c.rng_seed = int(cfg["steps"]), int(cfg.get("rng_seed", 0))
+    loss = np.empty(max(1, c.steps), np.float64)
+    mg = np.empty(oh.n, np.float32)
+    out = _vp()
+    _chk(lib().or_refine_hierarchy(oh.handle, cv, nv, ptrs, _p(ex, C.c_float), C.byref(c), C.byref(out),
+                                   _p(loss, C.c_double), _p(mg, C.c_float)))
+    try:
+        d = export_hierarchy(out)
+    finally:
+        lib().or_hierarchy_free(out)
+    return d, loss[:c.steps], mg

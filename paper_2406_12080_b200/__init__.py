@@ -482,6 +482,27 @@ class TransferTracker:
             pass
 
 
+@dataclass
+class RefineConfig:
+    """RefineConfig (refine.hpp:21-34)."""
+    tau_min: float = 3.0
+    tau_max: float = 48.0
+    steps: int = 200
+    lr_mean: float = 1.6e-5
+    lr_scale: float = 5e-4
+    lr_rotation: float = 1e-4
+    lr_falloff: float = 5e-3
+    lr_sh: float = 2.5e-4
+    rng_seed: int = 0
+
+
+@dataclass
+class RefineStats:
+    """RefineStats (refine.hpp:207-210): loss per step, per-node running max |d loss / d mean2d|."""
+    loss: list
+    max_screen_grad: np.ndarray
+
+
 class Renderer:
     """One CUDA context (device, stream) running the hot path.  Mirrors the
     reference's free functions as methods; module-level wrappers use
@@ -590,6 +611,46 @@ class Renderer:
         out = Hierarchy.empty(dh.n)
         _check(N.lib().hs_hierarchy_download(self.ctx, dh.handle, C.byref(out.soa())), self.ctx)
         return out
+
+    def refine_hierarchy(self, h, cams, images, config: RefineConfig | None = None, exposures=None):
+        """refine_hierarchy (refine.hpp:253-402) on the device: SGD over the interior nodes
+        against the training views (images[v]: (3, H, W) of cams[v]).  Returns (refined
+        DeviceHierarchy, RefineStats).  exposures: (n_views, 3, 4) or None (identity)."""
+        cfg = config or RefineConfig()
+        dh = self._dev(h)
+        nv = len(cams)
+        if nv != len(images):
+            raise Error(int(Errc.DimensionMismatch) + 1, "DimensionMismatch: need one training image per camera")
+        cc = (N.hs_camera * max(1, nv))(*[c.to_c() for c in cams])
+        imgs = []
+        for c, im in zip(cams, images):
+            a = np.ascontiguousarray(im, np.float32)
+            if a.shape != (3, c.height, c.width):
+                raise Error(int(Errc.DimensionMismatch) + 1,
+                            "DimensionMismatch: training image shape must match its camera")
+            imgs.append(a)
+        ptrs = (N.f32p * max(1, nv))(*[N.ptr(a, C.c_float) for a in imgs])
+        ex = None if exposures is None else np.ascontiguousarray(exposures, np.float32).reshape(nv, 12)
+        c = N.hs_refine_config(cfg.tau_min, cfg.tau_max, cfg.steps, cfg.lr_mean, cfg.lr_scale, cfg.lr_rotation,
+                               cfg.lr_falloff, cfg.lr_sh, cfg.rng_seed)
+        loss = np.zeros(max(1, cfg.steps), np.float64)
+        mg = np.zeros(dh.n, np.float32)
+        out = C.c_void_p()
+        _check(N.lib().hs_refine_hierarchy(self.ctx, dh.handle, cc, ptrs, N.ptr(ex, C.c_float), nv, C.byref(c),
+                                           C.byref(out), loss.ctypes.data_as(C.POINTER(C.c_double)),
+                                           N.ptr(mg, C.c_float)), self.ctx)
+        refined = DeviceHierarchy(self, out, dh.n, int(N.lib().hs_hierarchy_leaf_count(out)))
+        return refined, RefineStats(list(loss[:cfg.steps]), mg)
+
+    def photometric_loss(self, pred, target):
+        """photometric_loss (image.hpp:193-206) on (3, H, W) images -> (loss, d loss / d pred)."""
+        p = np.ascontiguousarray(pred, np.float32)
+        t = np.ascontiguousarray(target, np.float32)
+        g = np.empty_like(p)
+        loss = C.c_float()
+        _check(N.lib().hs_photometric_loss(self.ctx, N.ptr(p, C.c_float), N.ptr(t, C.c_float), p.shape[2],
+                                           p.shape[1], C.byref(loss), N.ptr(g, C.c_float)), self.ctx)
+        return float(loss.value), g
 
     def _dev(self, h) -> DeviceHierarchy:
         if isinstance(h, DeviceHierarchy):
@@ -997,6 +1058,18 @@ def bench_path(h, cameras, tau: float, timestamps=None, renderer: Renderer | Non
     rep.mean_rendered /= len(rep.frames)
     rep.mean_rendered_pct /= len(rep.frames)
     return rep
+
+
+def refine_hierarchy(h, cams, images, config: RefineConfig | None = None, exposures=None):
+    """refine_hierarchy (refine.hpp:253-402) -> (refined Hierarchy, RefineStats)."""
+    r = default_renderer()
+    dh, stats = r.refine_hierarchy(h, cams, images, config, exposures)
+    return r.download(dh), stats
+
+
+def photometric_loss(pred, target):
+    """photometric_loss (image.hpp:193-206) -> (loss, d loss / d pred)."""
+    return default_renderer().photometric_loss(pred, target)
 
 
 def psnr(a: np.ndarray, b: np.ndarray) -> float:

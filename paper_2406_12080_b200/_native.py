@@ -46,6 +46,12 @@ class hs_grads_out(C.Structure):
                                                     "sh", "mean2d", "exposure")]
 
 
+class hs_refine_config(C.Structure):
+    _fields_ = [("tau_min", C.c_float), ("tau_max", C.c_float), ("steps", C.c_int32), ("lr_mean", C.c_float),
+                ("lr_scale", C.c_float), ("lr_rotation", C.c_float), ("lr_falloff", C.c_float),
+                ("lr_sh", C.c_float), ("rng_seed", C.c_uint64)]
+
+
 class hs_gaussian_soa(C.Structure):
     _fields_ = [("mean", f32p), ("scale", f32p), ("rot_wxyz", f32p), ("falloff", f32p), ("sh", f32p)]
 
@@ -102,6 +108,9 @@ _SIGS = {
     "hs_hierarchy_compact": (C.c_int, [_vp, _vp, C.POINTER(hs_camera), C.c_uint64, C.c_float, C.c_float,
                                        C.POINTER(_vp)]),
     "hs_hierarchy_destroy": (None, [_vp]),
+    "hs_refine_hierarchy": (C.c_int, [_vp, _vp, C.POINTER(hs_camera), C.POINTER(f32p), f32p, C.c_uint32,
+                                      C.POINTER(hs_refine_config), C.POINTER(_vp), C.POINTER(C.c_double), f32p]),
+    "hs_photometric_loss": (C.c_int, [_vp, f32p, f32p, C.c_int32, C.c_int32, f32p, f32p]),
     "hs_hierarchy_node_count": (C.c_uint64, [_vp]),
     "hs_hierarchy_leaf_count": (C.c_uint64, [_vp]),
     "hs_cut_create": (C.c_int, [_vp, C.POINTER(_vp)]),

@@ -16,6 +16,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <random>
 #include <string>
 #include <unordered_set>
 #include <vector>
@@ -1292,9 +1294,21 @@ hs_status hs_render_splats(hs_context* ctx, const hs_splat_soa* sp, uint64_t n, 
     return HS_OK;
 }
 
-hs_status hs_render_backward(hs_context* ctx, hs_frame* f, const float* loss_grad, const float* depth_grad,
-                             const float* exposure, const hs_grads_out* out) {
-    if (!ctx || !f || !out || !loss_grad) return HS_INVALID_ARGUMENT;
+// render_backward's device half: the context checks, the hierarchy frame's splat
+// re-assembly and the scratch (loss gradient planes first, filled by the caller),
+// then the launches (backward_run) on the context stream, gradients left on the
+// device in b.go (per splat, cut order).
+struct BwScratch {
+    float* lg = nullptr;
+    float* dg = nullptr;
+    float4* aux = nullptr;
+    float* acc = nullptr;
+    float* part = nullptr;
+    const float4* attr = nullptr;
+    uint64_t n = 0, d = 0;
+    hs::BwGrads go{};
+};
+static hs_status backward_prepare(hs_context* ctx, hs_frame* f, bool want_dg, BwScratch& b) {
     if (f->pending) {
         hs_status st = finish_frame(ctx, f, false);
         if (st != HS_OK) return st;
@@ -1309,8 +1323,6 @@ hs_status hs_render_backward(hs_context* ctx, hs_frame* f, const float* loss_gra
             return set_err(ctx, HS_MISSING_FORWARD_STATE,
                            "the cut this frame was rendered from has been reselected or destroyed since");
         HS_TRY(acquire_cut(ctx, f->src_cut, ctx->stream));
-    }
-    if (f->from_cut) {
         // a hierarchy frame: its context's splats are the cut's interpolated RenderSplats
         // (render_hierarchy keeps cut_render_splats, render.hpp:706-720)
         const size_t sw = std::max<uint64_t>(n, 1);
@@ -1330,27 +1342,46 @@ hs_status hs_render_backward(hs_context* ctx, hs_frame* f, const float* loss_gra
     // device scratch: lg 3P | dg P | aux 4N | acc 13D | expo partial 256*12 | grads 65N + 12
     const size_t words = 4 * plane + 4 * n + hs::backward_acc_words(std::max<uint64_t>(d, 1)) + 256 * 12 + 65 * n + 12;
     HS_CUDA(ctx, f->bw.ensure(words * 4 + 64));
-    float* b = f->bw.as<float>();
-    float* lg = b;
-    float* dg = depth_grad ? lg + 3 * plane : nullptr;
-    float4* aux = reinterpret_cast<float4*>(lg + 4 * plane);  // 4 * plane floats: 16-byte aligned
-    float* acc = reinterpret_cast<float*>(aux + n);
-    float* part = acc + hs::backward_acc_words(std::max<uint64_t>(d, 1));
-    float* g = part + 256 * 12;
+    float* base = f->bw.as<float>();
+    b.lg = base;
+    b.dg = want_dg ? b.lg + 3 * plane : nullptr;
+    b.aux = reinterpret_cast<float4*>(b.lg + 4 * plane);  // 4 * plane floats: 16-byte aligned
+    b.acc = reinterpret_cast<float*>(b.aux + n);
+    b.part = b.acc + hs::backward_acc_words(std::max<uint64_t>(d, 1));
+    float* g = b.part + 256 * 12;
+    b.go = hs::BwGrads{g, g + 3 * n, g + 6 * n, g + 10 * n, g + 11 * n, g + 12 * n, g + 13 * n, g + 61 * n, g + 63 * n};
+    b.attr = attr;
+    b.n = n;
+    b.d = d;
+    return HS_OK;
+}
+static hs_status backward_run(hs_context* ctx, hs_frame* f, const BwScratch& b, const float* exposure) {
     cudaStream_t s = ctx->stream;
-    HS_CUDA(ctx, cudaMemcpyAsync(lg, loss_grad, plane * 12, cudaMemcpyHostToDevice, s));
-    if (dg) HS_CUDA(ctx, cudaMemcpyAsync(dg, depth_grad, plane * 4, cudaMemcpyHostToDevice, s));
-    HS_CUDA(ctx, cudaMemsetAsync(g, 0, (65 * n + 12) * 4, s));
+    HS_CUDA(ctx, cudaMemsetAsync(b.go.mean, 0, (65 * b.n + 12) * 4, s));
     hs::BwExposure ex{{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0}};
     if (exposure) std::memcpy(ex.e, exposure, sizeof(ex.e));
-    hs::BwGrads go{g, g + 3 * n, g + 6 * n, g + 10 * n, g + 11 * n, g + 12 * n, g + 13 * n, g + 61 * n, g + 63 * n};
     const int fin = f->passes & 1;
-    hs::launch_backward(attr, n, f->cam, f->ranges.as<uint2>(), f->keys[fin].as<uint32_t>(),
+    hs::launch_backward(b.attr, b.n, f->cam, f->ranges.as<uint2>(), f->keys[fin].as<uint32_t>(),
                         f->vals[fin].as<uint32_t>(), f->proj.as<ProjRec>(), f->dinfo.as<uint4>(),
-                        f->dupcount.as<uint32_t>(), &f->stats.as<DevStats>()->sort_n, std::max<uint64_t>(d, 1),
-                        f->color.as<float>(), f->depth.as<float>(), lg, dg, ex, aux, acc, part, go, s);
+                        f->dupcount.as<uint32_t>(), &f->stats.as<DevStats>()->sort_n, std::max<uint64_t>(b.d, 1),
+                        f->color.as<float>(), f->depth.as<float>(), b.lg, b.dg, ex, b.aux, b.acc, b.part, b.go, s);
     HS_CUDA(ctx, cudaGetLastError());
+    return HS_OK;
+}
+
+hs_status hs_render_backward(hs_context* ctx, hs_frame* f, const float* loss_grad, const float* depth_grad,
+                             const float* exposure, const hs_grads_out* out) {
+    if (!ctx || !f || !out || !loss_grad) return HS_INVALID_ARGUMENT;
+    BwScratch b;
+    HS_TRY(backward_prepare(ctx, f, depth_grad != nullptr, b));
+    const size_t plane = (size_t)f->W * f->H;
+    cudaStream_t s = ctx->stream;
+    HS_CUDA(ctx, cudaMemcpyAsync(b.lg, loss_grad, plane * 12, cudaMemcpyHostToDevice, s));
+    if (b.dg) HS_CUDA(ctx, cudaMemcpyAsync(b.dg, depth_grad, plane * 4, cudaMemcpyHostToDevice, s));
+    HS_TRY(backward_run(ctx, f, b, exposure));
     HS_CUDA(ctx, cudaStreamSynchronize(s));
+    const uint64_t n = b.n;
+    const hs::BwGrads& go = b.go;
     struct {
         float* dst;
         const float* src;
@@ -1737,5 +1768,187 @@ extern "C" hs_status hs_frame_order(hs_context* ctx, hs_frame* f, uint32_t* orde
         HS_CUDA(ctx, cudaStreamSynchronize(frame_stream(ctx, f)));
         HS_TRY(copy_sync(ctx, order, f->zvals[0].p, v * 4, cudaMemcpyDeviceToHost));
     }
+    return HS_OK;
+}
+
+// ------------------------------------------------------------------ refine step (refine.hpp:253-402)
+// Host loop with the reference's random streams (std::mt19937_64, libstdc++
+// distributions, refine.hpp:287-289, :310-311) and per step: gaussian_from of
+// the interior nodes (device), select_cut on the unchanged hierarchy, the
+// frame path over the trainable attributes, photometric loss gradient,
+// render_backward, chain + SGD (refine.cu).  Synchronous.
+extern "C" hs_status hs_photometric_loss(hs_context* ctx, const float* pred, const float* target, int32_t w, int32_t h,
+                                         float* loss, float* grad) {
+    if (!ctx || !pred || !target || w <= 0 || h <= 0) return HS_INVALID_ARGUMENT;
+    const uint64_t plane = (uint64_t)w * h;
+    DBuf d_pred, d_tgt, d_scr, d_grad, d_part;
+    HS_TRY(upload(ctx, d_pred, pred, 3 * plane));
+    HS_TRY(upload(ctx, d_tgt, target, 3 * plane));
+    HS_CUDA(ctx, d_scr.ensure(hs::loss_scratch_floats(plane) * 4));
+    HS_CUDA(ctx, d_grad.ensure(3 * plane * 4));
+    HS_CUDA(ctx, d_part.ensure(8192 * 8));
+    const hs::BwExposure ident{{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0}};
+    const unsigned nb = hs::launch_photometric_loss(d_pred.as<float>(), d_tgt.as<float>(), ident, w, h,
+                                                    d_scr.as<float>(), d_part.as<double>(), d_grad.as<float>(),
+                                                    ctx->stream);
+    HS_CUDA(ctx, cudaGetLastError());
+    std::vector<double> part(8192);
+    HS_TRY(copy_sync(ctx, part.data(), d_part.p, 8192 * 8, cudaMemcpyDeviceToHost));
+    if (grad) HS_TRY(copy_sync(ctx, grad, d_grad.p, 3 * plane * 4, cudaMemcpyDeviceToHost));
+    double l1 = 0.0, tot = 0.0;
+    for (unsigned b = 0; b < (nb & 0xffffu); ++b) l1 += part[b];
+    for (unsigned b = 0; b < (nb >> 16); ++b) tot += part[4096 + b];
+    const float n_total = (float)(3 * plane);
+    const float s = (float)(tot / (double)n_total);
+    if (loss) *loss = 0.8f * ((float)l1 / n_total) + 0.2f * (1.0f - s) / 2.0f;
+    return HS_OK;
+}
+
+extern "C" hs_status hs_refine_hierarchy(hs_context* ctx, const hs_hierarchy* h, const hs_camera* cams,
+                                         const float* const* images, const float* exposures, uint32_t n_views,
+                                         const hs_refine_config* cfg, hs_hierarchy** out, double* loss,
+                                         float* max_screen_grad) {
+    if (!ctx || !h || !cfg || !out || (n_views && (!cams || !images))) return HS_INVALID_ARGUMENT;
+    // validate_refine_config (refine.hpp:36-43)
+    if (!(cfg->tau_min > 0.0f && cfg->tau_min < cfg->tau_max))
+        return set_err(ctx, HS_INVALID_ARGUMENT, "granularity range must satisfy 0 < tau_min < tau_max");
+    if (cfg->steps < 0) return set_err(ctx, HS_INVALID_ARGUMENT, "step count must be non-negative");
+    if (!(cfg->lr_mean >= 0 && cfg->lr_scale >= 0 && cfg->lr_rotation >= 0 && cfg->lr_falloff >= 0 &&
+          cfg->lr_sh >= 0))
+        return set_err(ctx, HS_INVALID_ARGUMENT, "learning rates must be non-negative");
+    if (h->n == 0) return set_err(ctx, HS_INVALID_ARGUMENT, "refinement needs a hierarchy");
+    if (n_views == 0) return set_err(ctx, HS_DIMENSION_MISMATCH, "need one training image per camera");
+    for (uint32_t v = 0; v < n_views; ++v) {
+        hs_status s = validate_camera(ctx, &cams[v]);
+        if (s != HS_OK) return s;
+    }
+    if (h->leaves >= h->n)
+        return set_err(ctx, HS_NO_INTERIOR_NODES, "refinement has nothing to train without interior nodes");
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    HS_CUDA(ctx, cudaStreamSynchronize(s));
+    const uint64_t n = h->n;
+    // params_from (refine.hpp:220-228) on the host: log_scale with the host libm the
+    // reference calls (std::log), then uploaded once
+    DBuf d_params, d_map, d_mg, d_tgt, d_scr, d_part;
+    auto* eff = new hs_hierarchy();
+    eff->ctx = ctx;
+    eff->n = n;
+    eff->leaves = h->leaves;
+    eff->sh_degree = h->sh_degree;
+    std::unique_ptr<hs_hierarchy> eff_guard(eff);
+    HS_CUDA(ctx, eff->attr.ensure(n * 256));
+    HS_CUDA(ctx, cudaMemcpyAsync(eff->attr.p, h->attr.p, n * 256, cudaMemcpyDeviceToDevice, s));
+    {
+        HS_CUDA(ctx, d_params.ensure(n * 256));
+        const uint64_t chunk = 1 << 18;
+        std::vector<float4> at(16 * chunk);
+        for (uint64_t lo = 0; lo < n; lo += chunk) {
+            const uint64_t m = std::min(chunk, n - lo);
+            HS_CUDA(ctx, cudaMemcpy(at.data(), h->attr.as<float4>() + 16 * lo, m * 256, cudaMemcpyDeviceToHost));
+            for (uint64_t k = 0; k < m; ++k) {
+                float4* g = &at[16 * k];
+                g[1].x = std::log(std::max(g[1].x, 1e-12f));
+                g[1].y = std::log(std::max(g[1].y, 1e-12f));
+                g[1].z = std::log(std::max(g[1].z, 1e-12f));
+                g[1].w = 0.0f;
+                g[15] = make_float4(0, 0, 0, 0);
+            }
+            HS_CUDA(ctx, cudaMemcpy(d_params.as<float4>() + 16 * lo, at.data(), m * 256, cudaMemcpyHostToDevice));
+        }
+    }
+    HS_CUDA(ctx, d_map.ensure(n * 8));
+    HS_CUDA(ctx, cudaMemsetAsync(d_map.p, 0, n * 8, s));
+    if (max_screen_grad) {
+        HS_CUDA(ctx, d_mg.ensure(n * 4));
+        HS_CUDA(ctx, cudaMemsetAsync(d_mg.p, 0, n * 4, s));
+    }
+    // training images on the device, the loss scratch sized for the largest view
+    std::vector<uint64_t> img_off(n_views);
+    uint64_t img_total = 0, plane_max = 0;
+    for (uint32_t v = 0; v < n_views; ++v) {
+        img_off[v] = img_total;
+        const uint64_t plane = (uint64_t)cams[v].width * cams[v].height;
+        img_total += 3 * plane;
+        plane_max = std::max(plane_max, plane);
+    }
+    HS_CUDA(ctx, d_tgt.ensure(img_total * 4));
+    for (uint32_t v = 0; v < n_views; ++v)
+        HS_TRY(copy_sync(ctx, d_tgt.as<float>() + img_off[v], images[v],
+                         3ull * cams[v].width * cams[v].height * 4, cudaMemcpyHostToDevice));
+    HS_CUDA(ctx, d_scr.ensure(hs::loss_scratch_floats(plane_max) * 4));
+    HS_CUDA(ctx, d_part.ensure(8192 * 8));
+    std::vector<double> part(8192);
+
+    hs_cut* cut = nullptr;
+    hs_frame* f = nullptr;
+    HS_TRY(hs_cut_create(ctx, &cut));
+    std::unique_ptr<hs_cut, void (*)(hs_cut*)> cut_guard(cut, hs_cut_destroy);
+    HS_TRY(hs_frame_create(ctx, &f));
+    std::unique_ptr<hs_frame, void (*)(hs_frame*)> frame_guard(f, hs_frame_destroy);
+    const bool was_async = ctx->async;
+    ctx->async = false;
+    struct AsyncRestore {
+        hs_context* c;
+        bool v;
+        ~AsyncRestore() { c->async = v; }
+    } restore{ctx, was_async};
+
+    std::mt19937_64 rng(cfg->rng_seed);
+    std::uniform_int_distribution<std::size_t> pick_view(0, n_views - 1);
+    std::uniform_real_distribution<float> uni(0.0f, 1.0f);
+    static const float ident[12] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0};
+    for (int step = 0; step < cfg->steps; ++step) {
+        const std::size_t view = pick_view(rng);
+        const float xi = uni(rng);
+        const float tau = std::pow(cfg->tau_max, xi) * std::pow(cfg->tau_min, 1.0f - xi);  // sample_tau
+        const hs_camera& cam = cams[view];
+        const float* expo = exposures ? exposures + 12 * view : ident;
+        hs::launch_gaussian_from(d_params.as<float4>(), h->attr.as<float4>(), eff->attr.as<float4>(), n, s);
+        HS_TRY(hs_select_cut(ctx, h, &cam, tau, cut));
+        HS_TRY(render_from_cut(ctx, eff, cut, &cam, f, nullptr, false));
+        BwScratch b;
+        HS_TRY(backward_prepare(ctx, f, false, b));
+        hs::BwExposure ex;
+        std::memcpy(ex.e, expo, sizeof(ex.e));
+        const unsigned nb = hs::launch_photometric_loss(f->color.as<float>(), d_tgt.as<float>() + img_off[view], ex,
+                                                        cam.width, cam.height, d_scr.as<float>(),
+                                                        d_part.as<double>(), b.lg, s);
+        HS_TRY(backward_run(ctx, f, b, expo));
+        const uint64_t stamp = (uint64_t)step + 1;
+        hs::launch_refine_step(cut->node.as<uint32_t>(), cut->t.as<float>(), cut->count.as<uint64_t>(),
+                               std::max<uint64_t>(b.n, 1), stamp, d_map.as<uint64_t>(), d_params.as<float4>(),
+                               eff->attr.as<float4>(), n, b.go.mean, b.go.scale, b.go.rot, b.go.falloff,
+                               b.go.parent_falloff, b.go.sh, b.go.mean2d, cfg->lr_mean, cfg->lr_scale,
+                               cfg->lr_rotation, cfg->lr_falloff, cfg->lr_sh,
+                               max_screen_grad ? d_mg.as<float>() : nullptr, s);
+        HS_CUDA(ctx, cudaGetLastError());
+        if (loss) {
+            HS_TRY(copy_sync(ctx, part.data(), d_part.p, 8192 * 8, cudaMemcpyDeviceToHost));
+            double l1 = 0.0, tot = 0.0;
+            for (unsigned q = 0; q < (nb & 0xffffu); ++q) l1 += part[q];
+            for (unsigned q = 0; q < (nb >> 16); ++q) tot += part[4096 + q];
+            const float n_total = (float)(3ull * cam.width * cam.height);
+            const float sv = (float)(tot / (double)n_total);
+            loss[step] = 0.8f * ((float)l1 / n_total) + 0.2f * (1.0f - sv) / 2.0f;
+        }
+    }
+    // the refined hierarchy: gaussian_from of the final parameters, bounds unchanged,
+    // the transition alphas recomputed from the new falloffs
+    auto* o = new hs_hierarchy();
+    o->ctx = ctx;
+    o->n = n;
+    o->leaves = h->leaves;
+    o->sh_degree = h->sh_degree;
+    std::unique_ptr<hs_hierarchy> o_guard(o);
+    HS_CUDA(ctx, o->cull.ensure(n * 32));
+    HS_CUDA(ctx, o->attr.ensure(n * 256));
+    HS_CUDA(ctx, cudaMemcpyAsync(o->cull.p, h->cull.p, n * 32, cudaMemcpyDeviceToDevice, s));
+    hs::launch_gaussian_from(d_params.as<float4>(), h->attr.as<float4>(), o->attr.as<float4>(), n, s);
+    hs::launch_child_alpha(o->attr.as<float4>(), o->cull.as<float4>(), n, s);
+    HS_CUDA(ctx, cudaGetLastError());
+    if (max_screen_grad) HS_TRY(copy_sync(ctx, max_screen_grad, d_mg.p, n * 4, cudaMemcpyDeviceToHost));
+    HS_CUDA(ctx, cudaStreamSynchronize(s));
+    *out = o_guard.release();
     return HS_OK;
 }

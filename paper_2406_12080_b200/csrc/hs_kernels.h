@@ -131,6 +131,19 @@ void launch_tile_sort(const uint32_t* order, const uint2* prange, uint32_t* plan
                       uint32_t* zA, uint32_t* iA, uint8_t* mA, uint32_t* zB, uint32_t* iB, uint32_t* zC, uint32_t* iC,
                       uint8_t* mC, void* parts, void* merges, uint32_t* task_ctr, cudaStream_t s);
 
+// refine.cu (the refine step, refine.hpp:253-402)
+void launch_gaussian_from(const float4* params, const float4* orig, float4* eff, uint64_t n, cudaStream_t s);
+uint64_t loss_scratch_floats(uint64_t plane);
+// photometric_loss gradient into grad; returns (l1 blocks) | (ssim blocks) << 16 of the
+// double partials written at partials[0..) and partials[4096..)
+unsigned launch_photometric_loss(const float* color, const float* target, const BwExposure& e, int w, int h,
+                                 float* scratch, double* partials, float* grad, cudaStream_t s);
+void launch_refine_step(const uint32_t* cut_node, const float* cut_t, const uint64_t* n_ptr, uint64_t n_max,
+                        uint64_t stamp, uint64_t* map, float4* params, const float4* eff, uint64_t n_nodes,
+                        const float* g_mean, const float* g_scale, const float* g_rot, const float* g_fall,
+                        const float* g_pfall, const float* g_sh, const float* g_mean2d, float lr_mean,
+                        float lr_scale, float lr_rot, float lr_fall, float lr_sh, float* max_grad, cudaStream_t s);
+
 // sort.cu
 uint64_t sort_status_words(uint64_t n_max);
 uint64_t sort_scratch_words(uint64_t n_max, int passes);
