@@ -17,6 +17,7 @@
 //   bench_path             bench.hpp:55     BenchReport::csv     bench.hpp:33
 //   metrics                bench.hpp:105    psnr / ssim          image.hpp:111, :126
 //   set_thread_count       parallel.hpp:18  compact              build.hpp:175
+//   photometric_loss       image.hpp:195    refine_hierarchy     refine.hpp:253
 // Every computation runs on the GPU through the C ABI (per-object functions
 // such as granularity or project are batch kernels evaluated for one object);
 // file IO and the image metrics are host code, as in the reference.
@@ -267,6 +268,7 @@ struct Image {
     T& at(int x, int y, int c) { return data[(std::size_t(c) * height + y) * width + x]; }
     const T& at(int x, int y, int c) const { return data[(std::size_t(c) * height + y) * width + x]; }
 };
+using Imagef = Image<float>;
 
 namespace detail {
 inline void check_pair_shape(int aw, int ah, int ac, int bw, int bh, int bc) {  // image.hpp:50-54
@@ -1142,6 +1144,75 @@ inline Hierarchy compact(const Hierarchy& h, std::span<const CameraModel> cams, 
     hs_hierarchy* out = nullptr;
     c.check(hs_hierarchy_compact(c.ctx(), dh.get(), cc.data(), cc.size(), tau_min, tau_max, &out));
     std::unique_ptr<hs_hierarchy, gpu::HierarchyDeleter> keep(out);
+    return gpu::download_hierarchy(c, out, h.sh_degree);
+}
+
+// ------------------------------------------------------------------ image.hpp:193-206, refine.hpp:21-402
+// photometric_loss: 0.8 L1 + 0.2 (1 - SSIM) / 2 and d loss / d pred, computed on the device
+template <class T>
+T photometric_loss(const Image<T>& pred, const Image<T>& target, Image<T>* grad = nullptr) {
+    static_assert(std::is_same_v<T, float>, "the GPU path computes the loss in float");
+    if (pred.width != target.width || pred.height != target.height || pred.channels != target.channels)
+        throw Error(Errc::DimensionMismatch, "DimensionMismatch: images must have identical shapes");
+    if (pred.channels != 3) throw Error(Errc::DimensionMismatch, "DimensionMismatch: the photometric loss is RGB");
+    auto& c = gpu::context();
+    float loss = 0.0f;
+    if (grad) *grad = Image<T>(pred.width, pred.height, 3);
+    c.check(hs_photometric_loss(c.ctx(), pred.data.data(), target.data.data(), pred.width, pred.height, &loss,
+                                grad ? grad->data.data() : nullptr));
+    return loss;
+}
+
+struct RefineConfig {  // refine.hpp:21-34
+    float tau_min = 3.0f;
+    float tau_max = 48.0f;
+    int steps = 200;
+    float lr_mean = 1.6e-5f;
+    float lr_scale = 5e-4f;
+    float lr_rotation = 1e-4f;
+    float lr_falloff = 5e-3f;
+    float lr_sh = 2.5e-4f;
+    std::uint64_t rng_seed = 0;
+};
+
+struct RefineStats {  // refine.hpp:207-210
+    std::vector<double> loss;
+    std::vector<float> max_screen_grad;
+};
+
+// refine_hierarchy (refine.hpp:253-402) on the device: the views and granularity
+// targets come from the reference's std::mt19937_64(rng_seed) streams.
+inline Hierarchy refine_hierarchy(const Hierarchy& h, std::span<const CameraModel> cams,
+                                  std::span<const Imagef> images, const RefineConfig& cfg,
+                                  RefineStats* stats = nullptr) {
+    if (cams.size() != images.size() || cams.empty())
+        throw Error(Errc::DimensionMismatch, "DimensionMismatch: need one training image per camera");
+    for (std::size_t i = 0; i < cams.size(); ++i)
+        if (images[i].width != cams[i].width || images[i].height != cams[i].height || images[i].channels != 3)
+            throw Error(Errc::DimensionMismatch, "DimensionMismatch: training image shape must match its camera");
+    auto& c = gpu::context();
+    std::vector<hs_camera> cc;
+    std::vector<const float*> ip;
+    std::vector<float> ex;
+    for (std::size_t i = 0; i < cams.size(); ++i) {
+        cc.push_back(gpu::to_c(cams[i]));
+        ip.push_back(images[i].data.data());
+        for (int r = 0; r < 3; ++r)
+            for (int k = 0; k < 4; ++k) ex.push_back(cams[i].exposure(r, k));
+    }
+    const gpu::HierarchyPtr dh = c.device(h);
+    const hs_refine_config rc{cfg.tau_min, cfg.tau_max, cfg.steps,      cfg.lr_mean, cfg.lr_scale,
+                              cfg.lr_rotation, cfg.lr_falloff, cfg.lr_sh, cfg.rng_seed};
+    std::vector<double> loss(std::max(cfg.steps, 1));
+    std::vector<float> mg(h.nodes.size());
+    hs_hierarchy* out = nullptr;
+    c.check(hs_refine_hierarchy(c.ctx(), dh.get(), cc.data(), ip.data(), ex.data(),
+                                static_cast<std::uint32_t>(cams.size()), &rc, &out, loss.data(), mg.data()));
+    std::unique_ptr<hs_hierarchy, gpu::HierarchyDeleter> keep(out);
+    if (stats) {
+        stats->loss.assign(loss.begin(), loss.begin() + std::max(cfg.steps, 0));
+        stats->max_screen_grad = std::move(mg);
+    }
     return gpu::download_hierarchy(c, out, h.sh_degree);
 }
 

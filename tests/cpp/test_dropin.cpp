@@ -238,6 +238,32 @@ int main() {
         for (int k = 1; k < 4; ++k) CHECK(got[k] == got[0]);
     }
 
+    // photometric_loss (image.hpp:193-206) and refine_hierarchy (refine.hpp:253-402) through the shim
+    {
+        Imagef img = a.color, g;
+        CHECK(photometric_loss(img, img, &g) == 0.0f);
+        for (float v : g.data) CHECK(v == 0.0f);
+        std::vector<CameraModel> cams = {cam};
+        std::vector<Imagef> targets = {a.color};
+        for (float& v : targets[0].data) v = std::min(1.0f, v * 0.9f + 0.05f);
+        RefineConfig rc;
+        rc.steps = 3;
+        rc.tau_min = 3.0f;
+        rc.tau_max = 12.0f;
+        RefineStats rs;
+        const Hierarchy out = refine_hierarchy(h, cams, targets, rc, &rs);
+        CHECK(out.nodes.size() == h.nodes.size());
+        CHECK(rs.loss.size() == 3 && rs.loss[0] > 0.0);
+        CHECK(rs.max_screen_grad.size() == h.nodes.size());
+        std::size_t frozen = 0, leaves = 0;
+        for (std::size_t i = 0; i < h.nodes.size(); ++i)
+            if (h.nodes[i].is_leaf()) {
+                ++leaves;
+                frozen += std::memcmp(&out.nodes[i].g, &h.nodes[i].g, sizeof(Gaussian)) == 0;
+            }
+        CHECK(frozen == leaves);
+    }
+
     // read_hierarchy error code (io.hpp:375-387)
     threw = false;
     try {

@@ -4,7 +4,8 @@ A small city (20K leaves, 320x240) rendered through every kernel family the
 frame path launches: cut + raster on two frame lanes in async mode with one
 cut object shared between the lanes (the cross-lane hazard case), a reused cut
 (bench_path's odd frame), a splat render, a backward pass, the fast blend
-mode, and compaction.  Run as
+mode, compaction, heavy tiles through every in-tile sort path, and a short
+refinement.  Run as
 
     compute-sanitizer --tool racecheck python tools/sanitize_frames.py
 
@@ -87,6 +88,16 @@ def main():
     r.set_exact(True)
     # compaction on the device
     r.compact(dh, [scenes.camera(cfg, 40)], 3.0)
+    # heavy tiles: a big tile split by key range, an oversized equal-depth partition
+    # (chunks + merge), the LSD fallbacks (tests/test_gpu_order.py's cases)
+    from tests.fixtures import Rng
+    from tests.test_gpu_order import tile_cluster
+    for n, same in ((12000, False), (9000, True), (3000, True), (400, True)):
+        sp2, cam2 = tile_cluster(Rng(1000 + n), n, 5.0, same)
+        r.render_forward(sp2, cam2)
+    # a short refinement (refine.cu) with a backward per step
+    tgt = [np.clip(out.color * 0.9 + 0.05, 0, 1).astype(np.float32)]
+    r.refine_hierarchy(dh, [scenes.camera(cfg, 40)], tgt, hs.RefineConfig(steps=2, tau_min=3.0, tau_max=12.0))
     r.close()
     print("sanitize workload ok", out.rendered_count)
 
