@@ -136,72 +136,90 @@ __device__ __forceinline__ void hash_drain(HashTab<kLog>& h, Fn fn) {
 }
 
 // ------------------------------------------------------------------ count
-// CTA c takes the contiguous cut entries [c chunk, (c + 1) chunk), chunk =
-// ceil(C / grid): cut order is spatially coherent, so a chunk's small
-// footprints (<= 4 tiles) fall on few tiles (~60 at C2).  Their per-tile counts
-// are summed in the shared table without a barrier and flushed once: tcount[t]
-// += count, and the table (tile, count) saved for k_bucket, which reserves each
-// tile's range with one atomic and re-ranks the same entries into it.  Larger
-// footprints add +1 / -1 marks at the ends of every tile row they cross
-// (rowdiff[row * (tiles_x + 1) + x]); k_tile_plan takes the row prefixes.
-constexpr int kChunkLog = 11;                     // shared table: 2048 slots
+// The cut is cut into chunks of 1024 consecutive entries (CTAs stride over
+// them).  Cut order is spatially coherent, so a chunk's small footprints (<= 4
+// tiles) fall on few tiles (~60 at C2): their per-tile counts are summed in the
+// CTA's shared table without a barrier and flushed once per chunk: tcount[t] +=
+// count, and up to kSavedSlots (tile, count) pairs saved for k_bucket, which
+// reserves each saved tile's range with one atomic and places the same entries
+// into it (a tile not saved -- table full -- takes the global cursor per pair
+// there).  Larger footprints add +1 / -1 marks at the ends of every tile row
+// they cross (rowdiff[row * (tiles_x + 1) + x]); k_tile_plan takes the row
+// prefixes.
+#ifndef HS_CHUNK
+#define HS_CHUNK 1024
+#endif
+constexpr int kChunkLog = 11;        // shared table: 2048 slots
 constexpr int kChunkSlots = 1 << kChunkLog;
-__device__ __forceinline__ void chunk_range(uint64_t n, uint64_t& lo, uint64_t& hi) {
-    const uint64_t chunk = (n + gridDim.x - 1) / gridDim.x;
-    lo = min((uint64_t)blockIdx.x * chunk, n);
-    hi = min(lo + chunk, n);
-}
+constexpr uint32_t kChunk = HS_CHUNK;  // cut entries per chunk
+constexpr uint32_t kSavedSlots = 1024;
 __global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__ dupcount,
                                                     const uint4* __restrict__ dinfo, const uint64_t* __restrict__ n_ptr,
                                                     int tiles_x, uint32_t* __restrict__ tcount,
                                                     uint32_t* __restrict__ rowdiff, uint2* __restrict__ saved,
                                                     uint32_t* __restrict__ saved_n) {
     __shared__ HashTab<kChunkLog> h;
+    __shared__ uint32_t s_nsaved;
     const int W = tiles_x + 1;
-    uint64_t lo, hi;
-    chunk_range(*n_ptr, lo, hi);
+    const uint64_t n = *n_ptr;
+    const uint64_t n_chunks = (n + kChunk - 1) / kChunk;
     hash_init(h);
+    if (threadIdx.x == 0) s_nsaved = 0;
     __syncthreads();
-    // loads one block ahead (dinfo unconditionally: stale for culled entries, unused)
-    uint32_t cnt_n = lo + threadIdx.x < hi ? dupcount[lo + threadIdx.x] : 0u;
-    uint4 di_n = lo + threadIdx.x < hi ? dinfo[lo + threadIdx.x] : make_uint4(0, 0, 0, 0);
-    for (uint64_t base = lo; base < hi; base += blockDim.x) {
-        const uint32_t cnt = cnt_n;
-        const uint4 di = di_n;
-        {
-            const uint64_t nx = base + blockDim.x + threadIdx.x;
-            cnt_n = nx < hi ? dupcount[nx] : 0u;
-            di_n = nx < hi ? dinfo[nx] : make_uint4(0, 0, 0, 0);
+    for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        const uint64_t lo = c * kChunk, hi = min(lo + kChunk, n);
+        // loads one block ahead (dinfo unconditionally: stale for culled entries, unused)
+        uint32_t cnt_n = lo + threadIdx.x < hi ? dupcount[lo + threadIdx.x] : 0u;
+        uint4 di_n = lo + threadIdx.x < hi ? dinfo[lo + threadIdx.x] : make_uint4(0, 0, 0, 0);
+        for (uint64_t base = lo; base < hi; base += blockDim.x) {
+            const uint32_t cnt = cnt_n;
+            const uint4 di = di_n;
+            {
+                const uint64_t nx = base + blockDim.x + threadIdx.x;
+                cnt_n = nx < hi ? dupcount[nx] : 0u;
+                di_n = nx < hi ? dinfo[nx] : make_uint4(0, 0, 0, 0);
+            }
+            const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
+            const int w = max(tx1 - tx0, 1);
+            const bool small = cnt != 0 && cnt <= (uint32_t)kBigArea;
+            int slot;
+            for (int k = 0; k < kBigArea; ++k) {
+                const bool has = small && (uint32_t)k < cnt;
+                if (!__any_sync(0xffffffffu, has)) break;
+                const uint32_t tile = (uint32_t)((ty0 + k / w) * tiles_x + tx0 + k % w);
+                hash_add(h, has, tile, 1u, slot, tcount);
+            }
+            const bool marks = cnt > (uint32_t)kBigArea;
+            for (int r = 0; __any_sync(0xffffffffu, marks && ty0 + r < ty1); ++r) {
+                const bool has = marks && ty0 + r < ty1;
+                const uint32_t row = (uint32_t)(ty0 + r) * W;
+                hash_add(h, has, kMarkBit | (row + tx0), 1u, slot, rowdiff);
+                hash_add(h, has, kMarkBit | (row + tx1), 0xFFFFFFFFu, slot, rowdiff);
+            }
         }
-        const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
-        const int w = max(tx1 - tx0, 1);
-        const bool small = cnt != 0 && cnt <= (uint32_t)kBigArea;
-        int slot;
-        for (int k = 0; k < kBigArea; ++k) {
-            const bool has = small && (uint32_t)k < cnt;
-            if (!__any_sync(0xffffffffu, has)) break;
-            const uint32_t tile = (uint32_t)((ty0 + k / w) * tiles_x + tx0 + k % w);
-            hash_add(h, has, tile, 1u, slot, tcount);
+        __syncthreads();
+        uint2* sv = saved + c * kSavedSlots;
+        for (uint32_t u = threadIdx.x; u < h.n_used; u += blockDim.x) {
+            const int sl = h.used[u];
+            const uint32_t key = h.key[sl], v = h.val[sl];
+            if (key & kMarkBit) {
+                atomicAdd(&rowdiff[key & ~kMarkBit], v);
+            } else {
+                atomicAdd(&tcount[key], v);
+                const uint32_t q = atomicAdd(&s_nsaved, 1u);
+                if (q < kSavedSlots) sv[q] = make_uint2(key, v);
+            }
+            h.key[sl] = kEmpty;
+            h.val[sl] = 0;
         }
-        const bool marks = cnt > (uint32_t)kBigArea;
-        for (int r = 0; __any_sync(0xffffffffu, marks && ty0 + r < ty1); ++r) {
-            const bool has = marks && ty0 + r < ty1;
-            const uint32_t row = (uint32_t)(ty0 + r) * W;
-            hash_add(h, has, kMarkBit | (row + tx0), 1u, slot, rowdiff);
-            hash_add(h, has, kMarkBit | (row + tx1), 0xFFFFFFFFu, slot, rowdiff);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            saved_n[c] = min(s_nsaved, kSavedSlots);
+            s_nsaved = 0;
+            h.n_used = 0;
         }
+        __syncthreads();
     }
-    __syncthreads();
-    const uint32_t nu = h.n_used;
-    uint2* sv = saved + (size_t)blockIdx.x * kChunkSlots;
-    for (uint32_t u = threadIdx.x; u < nu; u += blockDim.x) {
-        const int sl = h.used[u];
-        const uint32_t key = h.key[sl], v = h.val[sl];
-        if (key & kMarkBit) atomicAdd(&rowdiff[key & ~kMarkBit], v);
-        else atomicAdd(&tcount[key], v);
-        sv[u] = make_uint2(key, v);
-    }
-    if (threadIdx.x == 0) saved_n[blockIdx.x] = nu;
 }
 
 // ------------------------------------------------------------------ plan
@@ -271,19 +289,18 @@ __global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const u
         }
     }
     __syncthreads();
-    // 2. exclusive scan of the sizes in tile order (contiguous items per thread)
+    // 2. exclusive scan of the sizes in tile order: warp w owns the segment
+    //    [w S, (w + 1) S), S = 32 E, read lane-striped (conflict-free)
     const int E = (tiles + 1023) / 1024;
-    const int t0 = tid * E;
+    const int S = 32 * E, w0 = warp * S;
     uint64_t local = 0;
-    for (int k = 0; k < E; ++k)
-        if (t0 + k < tiles) local += s_n[t0 + k];
-    uint64_t incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+    for (int k = 0; k < E; ++k) {
+        const int t = w0 + k * 32 + lane;
+        if (t < tiles) local += s_n[t];
     }
-    if (lane == 31) s_w64[warp] = incl;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if (lane == 0) s_w64[warp] = local;
     __syncthreads();
     if (warp == 0) {
         const uint64_t w = s_w64[lane];
@@ -304,17 +321,25 @@ __global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const u
         *sort_n = fits ? D : 0;
         if (D > cap_dup) atomicAdd(overflows, 1ull);
     }
-    uint64_t run = s_w64[warp] + incl - local;
-    for (int k = 0; k < E; ++k) {  // sizes -> starts, in place (each thread owns its items)
-        const int t = t0 + k;
-        if (t >= tiles) break;
-        const uint32_t c = s_n[t];
-        s_n[t] = (uint32_t)run;
-        if (fits) {
-            ranges[t] = make_uint2((uint32_t)run, (uint32_t)(run + c));
-            cursor[t] = (uint32_t)run;
+    uint64_t carry = s_w64[warp];
+    for (int k = 0; k < E; ++k) {  // sizes -> starts, in place
+        const int t = w0 + k * 32 + lane;
+        const uint32_t c = t < tiles ? s_n[t] : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
-        run += c;
+        const uint64_t run = carry + incl - c;
+        if (t < tiles) {
+            s_n[t] = (uint32_t)run;
+            if (fits) {
+                ranges[t] = make_uint2((uint32_t)run, (uint32_t)(run + c));
+                cursor[t] = (uint32_t)run;
+            }
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (tid == 0) s_n[tiles] = (uint32_t)D;
     __syncthreads();
@@ -413,16 +438,17 @@ __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ 
     if (*sort_n_ptr == 0) return;  // nothing visible, or over capacity
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
-    uint64_t lo, hi;
-    chunk_range(*n_ptr, lo, hi);
+    const uint64_t n = *n_ptr;
+    const uint64_t n_chunks = (n + kChunk - 1) / kChunk;
     hash_init(h);
     __syncthreads();
+    for (uint64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
+    const uint64_t lo = chunk * kChunk, hi = min(lo + kChunk, n);
     {
-        const uint32_t nu = saved_n[blockIdx.x];
-        const uint2* sv = saved + (size_t)blockIdx.x * kChunkSlots;
+        const uint32_t nu = saved_n[chunk];
+        const uint2* sv = saved + chunk * kSavedSlots;
         for (uint32_t u = tid; u < nu; u += blockDim.x) {
             const uint2 e = sv[u];
-            if (e.x & kMarkBit) continue;
             const int sl = hash_slot(h, e.x);
             if (sl >= 0) h.val[sl] = atomicAdd(&cursor[e.x], e.y);  // else: its pairs use the global cursor
         }
@@ -521,6 +547,17 @@ __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ 
                 put_entry(pos, tile, sid, sz, mask, zk, ids, bm, dbg_keys, dbg_vals);
             }
         }
+    }
+    // the table for the next chunk
+    __syncthreads();
+    for (uint32_t u = tid; u < h.n_used; u += blockDim.x) {
+        const int sl = h.used[u];
+        h.key[sl] = kEmpty;
+        h.val[sl] = 0;
+    }
+    __syncthreads();
+    if (tid == 0) h.n_used = 0;
+    __syncthreads();
     }
 }
 
@@ -1270,17 +1307,17 @@ static int bucket_sms() {
     return sms;
 }
 
-// k_tile_count and k_bucket share the chunking: the same grid
-static unsigned chunk_grid(uint64_t n_max) {
-    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_max + 255) / 256, (uint64_t)bucket_sms() * 8));
-}
-uint64_t bucket_saved_words(uint64_t n_max) { return (uint64_t)chunk_grid(n_max) * (kChunkSlots * 2 + 1); }
+// k_tile_count and k_bucket walk the same 2048-entry chunks; the saved tables are
+// per chunk: kSavedSlots (tile, count) pairs each, then one count per chunk
+static uint64_t chunks_max(uint64_t n_max) { return std::max<uint64_t>(1, (n_max + kChunk - 1) / kChunk); }
+uint64_t bucket_saved_words(uint64_t n_max) { return chunks_max(n_max) * (2 * kSavedSlots + 1); }
 
 void launch_tile_count(const uint32_t* dupcount, const uint4* dinfo, const uint64_t* n_ptr, uint64_t n_max,
                        int tiles_x, uint32_t* tcount, uint32_t* rowdiff, uint32_t* saved, cudaStream_t s) {
-    const unsigned grid = chunk_grid(n_max);
+    const uint64_t nc = chunks_max(n_max);
+    const unsigned grid = (unsigned)std::min<uint64_t>(nc, (uint64_t)bucket_sms() * 8);
     k_tile_count<<<grid, 256, 0, s>>>(dupcount, dinfo, n_ptr, tiles_x, tcount, rowdiff,
-                                      reinterpret_cast<uint2*>(saved), saved + (size_t)grid * kChunkSlots * 2);
+                                      reinterpret_cast<uint2*>(saved), saved + nc * 2 * kSavedSlots);
     note_launch();
 }
 
@@ -1305,10 +1342,14 @@ void launch_bucket(const uint32_t* dupcount, const uint4* dinfo, const ProjRec* 
                    uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* cursor, const uint32_t* saved,
                    uint32_t* zk, uint32_t* ids, uint8_t* bm, uint32_t* huge_q, uint32_t* huge_n, uint64_t* dbg_keys,
                    uint32_t* dbg_vals, cudaStream_t s) {
-    const unsigned grid = chunk_grid(n_max);
+    const uint64_t nc = chunks_max(n_max);
+#ifndef HS_BUCKET_GRID_ALL
+#define HS_BUCKET_GRID_ALL 1
+#endif
+    const unsigned grid = HS_BUCKET_GRID_ALL ? (unsigned)nc : (unsigned)std::min<uint64_t>(nc, (uint64_t)bucket_sms() * 4);
     k_bucket<<<grid, 256, 0, s>>>(dupcount, dinfo, proj, n_ptr, sort_n_ptr, tiles_x, cursor,
-                                  reinterpret_cast<const uint2*>(saved), saved + (size_t)grid * kChunkSlots * 2, zk,
-                                  ids, bm, huge_q, huge_n, dbg_keys, dbg_vals);
+                                  reinterpret_cast<const uint2*>(saved), saved + nc * 2 * kSavedSlots, zk, ids, bm,
+                                  huge_q, huge_n, dbg_keys, dbg_vals);
     note_launch();
     k_bucket_huge<<<(unsigned)bucket_sms() * 4, 256, 0, s>>>(dinfo, proj, huge_q, huge_n, sort_n_ptr, tiles_x, cursor,
                                                              zk, ids, bm, dbg_keys, dbg_vals);
