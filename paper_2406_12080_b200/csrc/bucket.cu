@@ -5,30 +5,34 @@
 // cut order) and then buckets them into tiles preserving that order, so each
 // tile's list is its entries ordered by (bits(z), cut index) -- a unique key.
 // The device builds exactly those lists:
-//   k_tile_count   per-tile entry counts.  Each CTA takes 256 consecutive cut
-//                  entries at a time; cut order is spatially coherent, so their
-//                  (splat, tile) pairs fall on few tiles: they are summed in a
-//                  shared-memory hash table and flushed with one global atomic
-//                  per distinct tile (the hottest C2 tile sees ~190 instead of
-//                  ~15K same-address atomics).  Footprints of more than 8 tiles
-//                  add +1 / -1 row difference marks instead (same table).
-//   k_tile_plan    one CTA: per-tile sizes -> tile ranges (tile_start), bucket
-//                  cursors, D and the capacity check, the heavy-first tile
-//                  order and the sort task table
-//   k_bucket       every (splat, tile) pair to a slot of its tile's bucket:
-//                  block-local ranks from the same shared hash table, one
-//                  global cursor atomic per (block, tile); the reach mask
-//                  (tile_reach_mask) is computed from the splat in registers.
-//                  Footprints of 5..1024 tiles are emitted by the whole warp,
+//   k_tile_count   per-tile entry counts over 1024-entry chunks of the cut: cut
+//                  order is spatially coherent, so a chunk's (splat, tile) pairs
+//                  fall on few tiles (~20 at C2): they are summed in a shared
+//                  hash table and flushed with one global atomic per distinct
+//                  tile (the hottest C2 tile sees ~100 instead of ~15K
+//                  same-address atomics); the (tile, count) table is saved per
+//                  chunk.  Footprints of more than 4 tiles add +1 / -1 row
+//                  difference marks instead.
+//   k_tile_plan    one CTA: row prefixes + counts -> tile ranges (tile_start),
+//                  bucket cursors, D and the capacity check, the heavy-first
+//                  tile order with size classes (big >= 4096, regular, small
+//                  < 512 entries)
+//   k_bucket       every (splat, tile) pair to a slot of its tile's bucket: a
+//                  chunk's saved table reserves one range per tile (one global
+//                  atomic each) and the pairs take slots from it; the reach
+//                  mask (tile_reach_mask) is computed per pair, every lane busy.
+//                  Footprints of 5..1024 tiles are emitted by a whole warp,
 //                  larger ones by one CTA each (k_bucket_huge).
-//   k_tile_sort    persistent CTAs (1024 threads, one per SM), heavy tiles
-//                  first: a tile of <= 16384 entries is sorted by bits(z) with
-//                  an LSD radix sort in shared memory (8-bit digits, warps rank
-//                  with match.any, 16-bit local indices as payload, bytes equal
-//                  in every key skipped), equal depths are put in cut order
-//                  afterwards; tiles of <= 510 entries are sorted one per warp,
-//                  32 per task; larger tiles are sorted in 16384-entry chunks
-//                  and merged (merge path) once their chunks are done.
+//   k_tile_sort    256-thread CTAs (4 per SM) pulling tasks: first the big
+//                  tiles' splits (split_tile: key-range partitions of < 2048 +
+//                  largest-bucket entries, scattered to the C buffers), then
+//                  regular tiles (one CTA each), small tiles (one warp each),
+//                  and the partitions once every split is done.  A sort is one
+//                  MSD counting pass in shared memory (about two buckets per
+//                  entry) + an insertion sort per bucket, or 4 stable LSD passes
+//                  when a bucket exceeds 64 entries; runs of equal depth are put
+//                  in cut order.  A partition of > 4096 equal-depth entries is
+//                  sorted in chunks and merged (merge path).
 //   k_tile_finalize  the sorted (tile, source slot) lists -> (tile << 8 | reach
 //                  mask, splat id): the gathers of every entry in one wide pass.
 // Output: keys[i] = tile << 8 | reach mask, vals[i] = splat id, in tile order and
@@ -47,7 +51,7 @@ constexpr uint32_t kWarpCap = 32 * kMaxItems;     // per-warp sort capacity (til
 // size classes by clz(n) in the heavy-first order: big (n >= 4096, clz <= 19, split by
 // key range first), regular (512 <= n < 4096, one CTA), small (1 <= n < 512, one warp)
 constexpr uint32_t kBigBucket = 20, kSmallBucket = 23, kEmptyBucket = 32;
-constexpr int kSplitBits = 12;             // k_tile_split: key-range buckets of a big tile
+constexpr int kSplitBits = 12;             // split_tile: key-range buckets of a big tile
 constexpr uint32_t kPartTarget = kTileCap / 2;  // partitions start every 2048 entries
 constexpr uint32_t kFromC = 0x80000000u;   // source slot in the split buffer (k_tile_finalize)
 constexpr int kCountDirect = 8;       // k_tile_count: larger footprints use row difference marks
@@ -152,7 +156,7 @@ __device__ __forceinline__ void hash_drain(HashTab<kLog>& h, Fn fn) {
 constexpr int kChunkLog = 11;        // shared table: 2048 slots
 constexpr int kChunkSlots = 1 << kChunkLog;
 constexpr uint32_t kChunk = HS_CHUNK;  // cut entries per chunk
-constexpr uint32_t kSavedSlots = 1024;
+constexpr uint32_t kSavedSlots = 256;  // a 1024-entry chunk touches ~20 tiles at C2
 __global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__ dupcount,
                                                     const uint4* __restrict__ dinfo, const uint64_t* __restrict__ n_ptr,
                                                     int tiles_x, uint32_t* __restrict__ tcount,
@@ -379,7 +383,7 @@ __global__ void __launch_bounds__(1024, 1) k_tile_plan(uint32_t* tcount, const u
             if (fits && c) prange[p] = make_uint2(st, st + c);
         }
     }
-    if (tid == 0) plan[4] = plan[5] = plan[6] = 0;  // split / merge task counters (k_tile_split)
+    if (tid == 0) plan[4] = plan[5] = plan[6] = 0;  // partitions, merges, big tiles split (split_tile)
 }
 
 // ------------------------------------------------------------------ bucket
@@ -594,7 +598,7 @@ struct TileBufs {
     uint32_t *zA, *iA;  // bucketed (bits(z), id, mask); merge ping-pong buffer
     uint8_t* mA;
     uint32_t *zB, *iB;  // final (tile << 8 | mask, id)
-    uint32_t *zC, *iC;  // big tiles partitioned by key range (k_tile_split); merge ping-pong buffer
+    uint32_t *zC, *iC;  // big tiles partitioned by key range (split_tile); merge ping-pong buffer
     uint8_t* mC;
 };
 // A partition of a big tile: entries [start, start + count) of the C buffers, all
@@ -608,145 +612,6 @@ __device__ __forceinline__ uint64_t key_at(const uint32_t* z, const uint32_t* id
     return ((uint64_t)__ldcg(z + x) << 32) | __ldcg(id + x);
 }
 __device__ __forceinline__ int ceil_log2(uint32_t v) { return v <= 1 ? 0 : 32 - __clz(v - 1); }
-
-// Big tiles (>= 4096 entries; heavy-first positions [0, plan[1])), one CTA each:
-// the key range is cut into 4096 buckets of the top bits of (key - min), the
-// entries are scattered bucket by bucket into the C buffers (same range), and a
-// partition starts at the first bucket beginning after each multiple of 2048
-// entries -- so every partition holds < 2048 + (largest bucket) entries and all
-// its keys lie below the next partition's.  Partitions of <= 4096 entries are
-// sorted like regular tiles (parts[]); larger ones (a bucket of > 2048 nearly
-// equal depths) are sorted in chunks and merged (merges[]).
-constexpr int kSplitThreads = 1024, kSplitItems = 16;  // tiles of <= 16384 entries held in registers
-__global__ void __launch_bounds__(kSplitThreads, 1) k_tile_split(const uint32_t* __restrict__ order,
-                                                                 const uint2* __restrict__ prange,
-                                                                 uint32_t* __restrict__ plan,
-                                                                 const uint64_t* __restrict__ sort_n_ptr, TileBufs b,
-                                                                 Part* __restrict__ parts, Part* __restrict__ merges) {
-    constexpr int NB = 1 << kSplitBits, PER = NB / kSplitThreads;
-    __shared__ uint32_t s_cnt[NB];
-    __shared__ uint32_t s_w[32], s_min, s_max;
-    if (*sort_n_ptr == 0) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t n_big = plan[1];
-    for (uint32_t p = blockIdx.x; p < n_big; p += gridDim.x) {
-        const uint32_t tile = order[p];
-        const uint2 rg = prange[p];
-        const uint32_t s = rg.x, n = rg.y - rg.x;
-        const bool in_regs = n <= (uint32_t)(kSplitThreads * kSplitItems);
-        if (tid == 0) s_min = 0xFFFFFFFFu, s_max = 0;
-#pragma unroll
-        for (int q = 0; q < PER; ++q) s_cnt[tid * PER + q] = 0;
-        // one read of the tile (all loads in flight) when it fits the registers
-        uint32_t kv[kSplitItems], iv[kSplitItems], mv[kSplitItems / 4];
-        uint32_t kmin = 0xFFFFFFFFu, kmax = 0;
-        if (in_regs) {
-#pragma unroll
-            for (int k = 0; k < kSplitItems; ++k) {
-                const uint32_t i = tid + k * kSplitThreads;
-                kv[k] = i < n ? __ldcg(b.zA + s + i) : 0u;
-                iv[k] = i < n ? __ldcg(b.iA + s + i) : 0u;
-                const uint32_t m = i < n ? (uint32_t)__ldcg(b.mA + s + i) : 0u;
-                if (k & 3) mv[k >> 2] |= m << (8 * (k & 3)); else mv[k >> 2] = m;
-            }
-#pragma unroll
-            for (int k = 0; k < kSplitItems; ++k)
-                if (tid + k * kSplitThreads < n) kmin = min(kmin, kv[k]), kmax = max(kmax, kv[k]);
-        } else {
-            for (uint32_t i = tid; i < n; i += kSplitThreads) {
-                const uint32_t k = __ldcg(b.zA + s + i);
-                kmin = min(kmin, k), kmax = max(kmax, k);
-            }
-        }
-        kmin = __reduce_min_sync(0xffffffffu, kmin);
-        kmax = __reduce_max_sync(0xffffffffu, kmax);
-        __syncthreads();
-        if (lane == 0) atomicMin(&s_min, kmin), atomicMax(&s_max, kmax);
-        __syncthreads();
-        kmin = s_min;
-        const uint32_t diff = s_max - kmin;
-        const int span = diff ? 32 - __clz(diff) : 0;
-        const int sh = span > kSplitBits ? span - kSplitBits : 0;
-        if (in_regs) {
-#pragma unroll
-            for (int k = 0; k < kSplitItems; ++k)
-                if (tid + k * kSplitThreads < n) atomicAdd(&s_cnt[(kv[k] - kmin) >> sh], 1u);
-        } else {
-            for (uint32_t i = tid; i < n; i += kSplitThreads)
-                atomicAdd(&s_cnt[(__ldcg(b.zA + s + i) - kmin) >> sh], 1u);
-        }
-        __syncthreads();
-        // exclusive scan of the bucket sizes (PER per thread)
-        uint32_t v[PER], tot = 0;
-#pragma unroll
-        for (int q = 0; q < PER; ++q) v[q] = s_cnt[tid * PER + q], tot += v[q];
-        uint32_t incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) s_w[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-            const uint32_t w = s_w[lane];
-            uint32_t wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += y;
-            }
-            s_w[lane] = wi - w;
-        }
-        __syncthreads();
-        uint32_t base = s_w[warp] + incl - tot;
-#pragma unroll
-        for (int q = 0; q < PER; ++q) s_cnt[tid * PER + q] = base, base += v[q];
-        __syncthreads();
-        // partitions: the q-th starts at the first bucket whose start is >= q * 2048
-        const uint32_t P = (n + kPartTarget - 1) / kPartTarget;
-        auto first_bucket = [&](uint32_t target) {  // first bucket with start >= target (NB if none)
-            uint32_t lo = 0, hi = NB;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (s_cnt[mid] < target) lo = mid + 1; else hi = mid;
-            }
-            return lo;
-        };
-        for (uint32_t q = tid; q < P; q += kSplitThreads) {
-            const uint32_t b0 = q == 0 ? 0u : first_bucket(q * kPartTarget);
-            const uint32_t b1 = q + 1 == P ? (uint32_t)NB : first_bucket((q + 1) * kPartTarget);
-            const uint32_t st = b0 < NB ? s_cnt[b0] : n, en = b1 < NB ? s_cnt[b1] : n;
-            if (en > st) {
-                const Part pt{tile, s + st, en - st, 0u};
-                if (en - st <= kTileCap) parts[atomicAdd(&plan[4], 1u)] = pt;
-                else merges[atomicAdd(&plan[5], 1u)] = pt;
-            }
-        }
-        __syncthreads();
-        // scatter through the bucket cursors (order within a bucket is free:
-        // partitions are sorted whole)
-        if (in_regs) {
-#pragma unroll
-            for (int k = 0; k < kSplitItems; ++k) {
-                if (tid + k * kSplitThreads >= n) continue;
-                const uint32_t dst = s + atomicAdd(&s_cnt[(kv[k] - kmin) >> sh], 1u);
-                b.zC[dst] = kv[k];
-                b.iC[dst] = iv[k];
-                b.mC[dst] = (uint8_t)(mv[k >> 2] >> (8 * (k & 3)));
-            }
-        } else {
-            for (uint32_t i = tid; i < n; i += kSplitThreads) {
-                const uint32_t k = __ldcg(b.zA + s + i);
-                const uint32_t dst = s + atomicAdd(&s_cnt[(k - kmin) >> sh], 1u);
-                b.zC[dst] = k;
-                b.iC[dst] = __ldcg(b.iA + s + i);
-                b.mC[dst] = __ldcg(b.mA + s + i);
-            }
-        }
-        __syncthreads();
-    }
-}
 
 // Shared memory of k_tile_sort: one CTA-wide sort (<= 16384 entries) or 32
 // per-warp sorts (<= 512 entries each) over the same bytes.  Keys and 16-bit
@@ -1028,6 +893,103 @@ __device__ __forceinline__ void fix_ties(const uint32_t* __restrict__ key, uint1
     }
 }
 
+// The split of one big tile inside k_tile_sort (256 threads; three reads of the
+// tile's keys from L2), overlapping the regular tiles' sorts: the key range is
+// cut into 4096 buckets of the top bits of (key - min), the entries scattered
+// bucket by bucket into the C buffers (same range), and a partition starts at
+// the first bucket beginning after each multiple of 2048 entries -- so every
+// partition holds < 2048 + (largest bucket) entries and all its keys lie below
+// the next partition's.  Partitions of <= 4096 entries are sorted like regular
+// tiles (parts[]); larger ones (a bucket of > 2048 nearly equal depths) are
+// sorted in chunks and merged (merges[]).
+__device__ __forceinline__ void split_tile(uint32_t tile, uint32_t s, uint32_t n, uint32_t* cnt, uint32_t* s_red,
+                                           const TileBufs& b, uint32_t* plan, Part* parts, Part* merges) {
+    constexpr int NB = 1 << kSplitBits, PER = NB / kTsThreads;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int q = 0; q < PER; ++q) cnt[tid * PER + q] = 0;
+    uint32_t kmin = 0xFFFFFFFFu, kmax = 0;
+    for (uint32_t i0 = 0; i0 < n; i0 += 8 * kTsThreads) {
+        uint32_t kv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t i = i0 + q * kTsThreads + tid;
+            kv[q] = i < n ? __ldcg(b.zA + s + i) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (i0 + q * kTsThreads + tid < n) kmin = min(kmin, kv[q]), kmax = max(kmax, kv[q]);
+    }
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if (lane == 0) atomicMin(&s_red[2], kmin), atomicMax(&s_red[3], kmax);
+    __syncthreads();
+    kmin = s_red[2];
+    const uint32_t diff = s_red[3] - kmin;
+    const int span = diff ? 32 - __clz(diff) : 0;
+    const int sh = span > kSplitBits ? span - kSplitBits : 0;
+    for (uint32_t i0 = 0; i0 < n; i0 += 8 * kTsThreads) {
+        uint32_t kv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t i = i0 + q * kTsThreads + tid;
+            kv[q] = i < n ? __ldcg(b.zA + s + i) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (i0 + q * kTsThreads + tid < n) atomicAdd(&cnt[(kv[q] - kmin) >> sh], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the bucket sizes (PER consecutive per thread)
+    uint32_t v[PER], tot = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) v[q] = cnt[tid * PER + q], tot += v[q];
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    __shared__ uint32_t s_w[kTsWarps];
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    uint32_t base = incl - tot;
+    for (int w = 0; w < warp; ++w) base += s_w[w];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) cnt[tid * PER + q] = base, base += v[q];
+    __syncthreads();
+    const uint32_t P = (n + kPartTarget - 1) / kPartTarget;
+    auto first_bucket = [&](uint32_t target) {  // first bucket with start >= target (NB if none)
+        uint32_t lo = 0, hi = NB;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (cnt[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
+    for (uint32_t q = tid; q < P; q += kTsThreads) {
+        const uint32_t b0 = q == 0 ? 0u : first_bucket(q * kPartTarget);
+        const uint32_t b1 = q + 1 == P ? (uint32_t)NB : first_bucket((q + 1) * kPartTarget);
+        const uint32_t st = b0 < NB ? cnt[b0] : n, en = b1 < NB ? cnt[b1] : n;
+        if (en > st) {
+            const Part pt{tile, s + st, en - st, 0u};
+            if (en - st <= kTileCap) parts[atomicAdd(&plan[4], 1u)] = pt;
+            else merges[atomicAdd(&plan[5], 1u)] = pt;
+        }
+    }
+    __syncthreads();
+    // scatter through the bucket cursors (order within a bucket is free)
+    for (uint32_t i = tid; i < n; i += kTsThreads) {
+        const uint32_t k = __ldcg(b.zA + s + i);
+        const uint32_t dst = s + atomicAdd(&cnt[(k - kmin) >> sh], 1u);
+        b.zC[dst] = k;
+        b.iC[dst] = __ldcg(b.iA + s + i);
+        b.mC[dst] = __ldcg(b.mA + s + i);
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(&plan[6], 1u);  // one more big tile split
+}
+
 // Sort n <= kTileCap keys of (zs, s) held by the CTA; returns the sorted keys and
 // their local indices (into [s, s + n)) in shared memory.
 __device__ __forceinline__ void cta_sort(CtaSort& cs, const uint32_t* __restrict__ zs, const uint32_t* __restrict__ is,
@@ -1083,42 +1045,59 @@ __device__ __forceinline__ void cta_sort(CtaSort& cs, const uint32_t* __restrict
 
 __global__ void __launch_bounds__(kTsThreads, 4) k_tile_sort(const uint32_t* __restrict__ order,
                                                              const uint2* __restrict__ prange,
-                                                             const uint32_t* __restrict__ plan,
+                                                             uint32_t* plan,
                                                              const uint64_t* __restrict__ sort_n_ptr, TileBufs b,
                                                              const Part* __restrict__ parts,
                                                              const Part* __restrict__ merges,
                                                              uint32_t* __restrict__ task_ctr) {
     extern __shared__ __align__(16) unsigned char ts_smem[];
     CtaSort& cs = *reinterpret_cast<CtaSort*>(ts_smem);
-    __shared__ uint32_t s_next, s_red[4];
+    __shared__ uint32_t s_next, s_red[4], s_parts[2];
     if (*sort_n_ptr == 0) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // task table: [partitions of big tiles] [regular tiles] [groups of 8 small tiles]
-    //             [oversized partitions: chunks + merge]
-    const uint32_t n_parts = plan[4], n_merges = plan[5];
+    // task table: [splits of the big tiles] [regular tiles] [groups of 8 small tiles]
+    //             [partitions of the big tiles] [oversized partitions: chunks + merge]
+    // (heavy-first positions: big [0, first_reg), regular [first_reg, first_small),
+    // small [first_small, nonempty)); the partition tasks wait until every split is done
     const uint32_t first_reg = plan[1], first_small = plan[0], nonempty = plan[3];
-    const uint32_t t_reg = n_parts, t_small = t_reg + (first_small - first_reg);
-    const uint32_t t_merge = t_small + (nonempty - first_small + kTsWarps - 1) / kTsWarps;
-    const uint32_t n_tasks = t_merge + n_merges;
+    const uint32_t t_small = first_small;
+    const uint32_t t_part = t_small + (nonempty - first_small + kTsWarps - 1) / kTsWarps;
+    uint32_t n_tasks = 0xFFFFFFFFu, n_parts = 0;
     if (tid == 0) s_next = atomicAdd(task_ctr, 1u);
     while (true) {
         if (tid == 0) s_red[0] = 0xFFFFFFFFu, s_red[1] = 0, s_red[2] = 0xFFFFFFFFu, s_red[3] = 0;
         __syncthreads();
         const uint32_t task = s_next;
+        if (task >= t_part && n_tasks == 0xFFFFFFFFu) {
+            // the partition counts are final once every big tile is split
+            if (tid == 0) {
+                while (ld_volatile_u32(&plan[6]) < first_reg) __nanosleep(200);
+                __threadfence();
+                s_parts[0] = ld_volatile_u32(&plan[4]);
+                s_parts[1] = ld_volatile_u32(&plan[5]);
+            }
+            __syncthreads();
+            n_parts = s_parts[0];
+            n_tasks = t_part + n_parts + s_parts[1];
+        }
         if (task >= n_tasks) break;
         __syncthreads();
         if (tid == 0) s_next = atomicAdd(task_ctr, 1u);  // the next task's index arrives meanwhile
-        if (task < t_small) {
-            // a partition of a big tile (keys in C) or a regular tile (keys in A)
-            const bool part = task < t_reg;
+        if (task < first_reg) {
+            // split a big tile by key range into partitions
+            const uint2 rg = prange[task];
+            split_tile(order[task], rg.x, rg.y - rg.x, reinterpret_cast<uint32_t*>(ts_smem), s_red, b,
+                       const_cast<uint32_t*>(plan), const_cast<Part*>(parts), const_cast<Part*>(merges));
+        } else if (task < t_small || (task >= t_part && task < t_part + n_parts)) {
+            // a regular tile (keys in A) or a partition of a big tile (keys in C)
+            const bool part = task >= t_part;
             uint32_t tile, s, n;
             if (part) {
-                const Part pt = parts[task];
+                const Part pt = parts[task - t_part];
                 tile = pt.tile, s = pt.start, n = pt.count;
             } else {
-                const uint32_t p = first_reg + (task - t_reg);
-                tile = order[p];
-                const uint2 rg = prange[p];
+                tile = order[task];
+                const uint2 rg = prange[task];
                 s = rg.x, n = rg.y - rg.x;
             }
             const uint32_t* zs = part ? b.zC : b.zA;
@@ -1132,7 +1111,7 @@ __global__ void __launch_bounds__(kTsThreads, 4) k_tile_sort(const uint32_t* __r
                 b.zB[s + i] = kPending | tile << 8;
                 b.iB[s + i] = src_flag | (s + ridx[i]);
             }
-        } else if (task < t_merge) {
+        } else if (task < t_part) {
             // 8 small tiles, one per warp
             const uint32_t p = first_small + (task - t_small) * kTsWarps + warp;
             WarpSort& ws = reinterpret_cast<WarpSort*>(ts_smem)[warp];
@@ -1184,7 +1163,7 @@ __global__ void __launch_bounds__(kTsThreads, 4) k_tile_sort(const uint32_t* __r
             // an oversized partition (> 4096 entries of nearly equal depth): sorted runs of
             // 4096 in A (free: its entries moved to C), then pairwise merge-path rounds
             // A -> C -> ... -> B (final, not pending)
-            const Part pt = merges[task - t_merge];
+            const Part pt = merges[task - t_part - n_parts];
             const uint32_t tile = pt.tile, base = pt.start, N = pt.count;
             const uint32_t R = (N + kTileCap - 1) / kTileCap;
             for (uint32_t k = 0; k < R; ++k) {
@@ -1366,9 +1345,6 @@ void launch_tile_sort(const uint32_t* order, const uint2* prange, uint32_t* plan
         if (per < 1) per = 1;
     }
     TileBufs b{zA, iA, mA, zB, iB, zC, iC, mC};
-    k_tile_split<<<(unsigned)bucket_sms(), kSplitThreads, 0, s>>>(order, prange, plan, sort_n_ptr, b,
-                                                            static_cast<Part*>(parts), static_cast<Part*>(merges));
-    note_launch();
     k_tile_sort<<<(unsigned)(bucket_sms() * per), kTsThreads, kTileSortSmem, s>>>(
         order, prange, plan, sort_n_ptr, b, static_cast<const Part*>(parts), static_cast<const Part*>(merges),
         task_ctr);
