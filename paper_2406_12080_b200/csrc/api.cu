@@ -439,7 +439,7 @@ hs_status enqueue_raster(hs_context* ctx, hs_frame* f) {
     uint32_t* vb[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
     uint8_t* bm = f->bmask.as<uint8_t>();
     hs::launch_bucket(f->dupcount.as<uint32_t>(), f->dinfo.as<uint4>(), f->proj.as<ProjRec>(), &ds->n_splats, f->n_max,
-                      &ds->sort_n, cp.tiles_x, reinterpret_cast<uint32_t*>(sc + L.cursor),
+                      &ds->sort_n, cp.tiles_x, tiles, reinterpret_cast<uint32_t*>(sc + L.cursor),
                       reinterpret_cast<uint32_t*>(sc + L.saved), kb[1], vb[1], bm, f->huge.as<uint32_t>(),
                       reinterpret_cast<uint32_t*>(sc + L.huge_counter), ctx->debug ? f->dupk.as<uint64_t>() : nullptr,
                       ctx->debug ? f->dupv.as<uint32_t>() : nullptr, s);

@@ -565,31 +565,84 @@ __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ 
     }
 }
 
-// Splats covering more than kHugeArea tiles (e.g. skybox splats near the image
-// plane: the reference culls only at z <= 0.01), one CTA each.
+// Splats covering more than kHugeArea tiles (e.g. skybox splats or splats just
+// in front of the image plane: the reference culls only at z <= 0.01), tile-major:
+// a CTA takes kHugeGroup consecutive tiles, counts the huge splats covering each
+// (pass 1 over the queue), reserves each tile's range with one atomic, and
+// writes the entries (pass 2) -- one cursor atomic per (CTA, tile) instead of
+// one per (splat, tile) on cursors every huge splat shares.
+constexpr int kHugeGroup = 8;
 __global__ void __launch_bounds__(256) k_bucket_huge(const uint4* __restrict__ dinfo, const ProjRec* __restrict__ proj,
                                                      const uint32_t* __restrict__ huge_q,
                                                      const uint32_t* __restrict__ huge_n,
-                                                     const uint64_t* __restrict__ sort_n_ptr, int tiles_x,
+                                                     const uint64_t* __restrict__ sort_n_ptr, int tiles_x, int tiles,
                                                      uint32_t* __restrict__ cursor, uint32_t* __restrict__ zk,
                                                      uint32_t* __restrict__ ids, uint8_t* __restrict__ bm,
                                                      uint64_t* __restrict__ dbg_keys, uint32_t* __restrict__ dbg_vals) {
+    __shared__ uint32_t s_cnt[kHugeGroup], s_base[kHugeGroup];
     if (*sort_n_ptr == 0) return;
     const uint32_t nq = *huge_n;
-    for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
-        const uint32_t id = huge_q[q];
-        const uint4 di = dinfo[id];
-        const ProjRec* r = proj + id;
-        const float4 p0 = r->p0, p1 = r->p1, p3 = r->p3;
-        const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
-        const uint32_t w = (uint32_t)(tx1 - tx0), area = w * (uint32_t)(ty1 - ty0);
-        for (uint32_t t = threadIdx.x; t < area; t += blockDim.x) {
-            const int tx = tx0 + (int)(t % w), ty = ty0 + (int)(t / w);
-            const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
-            const uint32_t pos = atomicAdd(&cursor[tile], 1u);
-            const uint32_t mask = tile_reach_mask(p0, p1, p3, tx * kTile, ty * kTile);
-            put_entry(pos, tile, id, di.z, mask, zk, ids, bm, dbg_keys, dbg_vals);
+    if (nq == 0) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int groups = (tiles + kHugeGroup - 1) / kHugeGroup;
+    for (int gi = blockIdx.x; gi < groups; gi += gridDim.x) {
+        const int t0 = gi * kHugeGroup;
+        int gx[kHugeGroup], gy[kHugeGroup];
+#pragma unroll
+        for (int g = 0; g < kHugeGroup; ++g) gx[g] = (t0 + g) % tiles_x, gy[g] = (t0 + g) / tiles_x;
+        if (tid < kHugeGroup) s_cnt[tid] = 0;
+        __syncthreads();
+        // pass 1: how many huge splats cover each tile of the group
+        for (uint32_t q0 = 0; q0 < nq; q0 += blockDim.x) {
+            const uint32_t q = q0 + tid;
+            uint4 di = make_uint4(0, 0, 0, 0);
+            if (q < nq) di = dinfo[huge_q[q]];
+            const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
+#pragma unroll
+            for (int g = 0; g < kHugeGroup; ++g) {
+                const bool cov = q < nq && t0 + g < tiles && gx[g] >= tx0 && gx[g] < tx1 && gy[g] >= ty0 && gy[g] < ty1;
+                const uint32_t bal = __ballot_sync(0xffffffffu, cov);
+                if (lane == 0 && bal) atomicAdd(&s_cnt[g], (uint32_t)__popc(bal));
+            }
         }
+        __syncthreads();
+        if (tid < kHugeGroup && t0 + tid < tiles && s_cnt[tid]) s_base[tid] = atomicAdd(&cursor[t0 + tid], s_cnt[tid]);
+        __syncthreads();
+        if (tid < kHugeGroup) s_cnt[tid] = 0;  // running slot per tile for pass 2
+        __syncthreads();
+        // pass 2: the entries (slots within a tile in any order: the in-tile sort orders them)
+        for (uint32_t q0 = 0; q0 < nq; q0 += blockDim.x) {
+            const uint32_t q = q0 + tid;
+            uint32_t id = 0;
+            uint4 di = make_uint4(0, 0, 0, 0);
+            if (q < nq) id = huge_q[q], di = dinfo[id];
+            const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
+            float4 p0 = make_float4(0, 0, 0, 0), p1 = p0, p3 = p0;
+            bool any = false;
+#pragma unroll
+            for (int g = 0; g < kHugeGroup; ++g)
+                any |= q < nq && t0 + g < tiles && gx[g] >= tx0 && gx[g] < tx1 && gy[g] >= ty0 && gy[g] < ty1;
+            if (any) {
+                const ProjRec* r = proj + id;
+                p0 = r->p0, p1 = r->p1, p3 = r->p3;
+            }
+#pragma unroll
+            for (int g = 0; g < kHugeGroup; ++g) {
+                const bool cov = q < nq && t0 + g < tiles && gx[g] >= tx0 && gx[g] < tx1 && gy[g] >= ty0 && gy[g] < ty1;
+                const uint32_t bal = __ballot_sync(0xffffffffu, cov);
+                if (!bal) continue;
+                uint32_t wb = 0;
+                if (lane == 0) wb = atomicAdd(&s_cnt[g], (uint32_t)__popc(bal));
+                wb = __shfl_sync(0xffffffffu, wb, 0);
+                if (cov) {
+                    const uint32_t pos = s_base[g] + wb + __popc(bal & lt);
+                    const uint32_t mask = tile_reach_mask(p0, p1, p3, gx[g] * kTile, gy[g] * kTile);
+                    put_entry(pos, (uint32_t)(t0 + g), id, di.z, mask, zk, ids, bm, dbg_keys, dbg_vals);
+                }
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -1318,7 +1371,8 @@ void launch_tile_plan(uint32_t* tcount, const uint32_t* rowdiff, int tiles_x, in
 }
 
 void launch_bucket(const uint32_t* dupcount, const uint4* dinfo, const ProjRec* proj, const uint64_t* n_ptr,
-                   uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* cursor, const uint32_t* saved,
+                   uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, int tiles, uint32_t* cursor,
+                   const uint32_t* saved,
                    uint32_t* zk, uint32_t* ids, uint8_t* bm, uint32_t* huge_q, uint32_t* huge_n, uint64_t* dbg_keys,
                    uint32_t* dbg_vals, cudaStream_t s) {
     const uint64_t nc = chunks_max(n_max);
@@ -1330,8 +1384,8 @@ void launch_bucket(const uint32_t* dupcount, const uint4* dinfo, const ProjRec* 
                                   reinterpret_cast<const uint2*>(saved), saved + nc * 2 * kSavedSlots, zk, ids, bm,
                                   huge_q, huge_n, dbg_keys, dbg_vals);
     note_launch();
-    k_bucket_huge<<<(unsigned)bucket_sms() * 4, 256, 0, s>>>(dinfo, proj, huge_q, huge_n, sort_n_ptr, tiles_x, cursor,
-                                                             zk, ids, bm, dbg_keys, dbg_vals);
+    k_bucket_huge<<<(unsigned)bucket_sms() * 4, 256, 0, s>>>(dinfo, proj, huge_q, huge_n, sort_n_ptr, tiles_x,
+                                                             tiles, cursor, zk, ids, bm, dbg_keys, dbg_vals);
     note_launch();
 }
 

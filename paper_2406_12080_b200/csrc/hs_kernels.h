@@ -123,7 +123,8 @@ void launch_tile_plan(uint32_t* tcount, const uint32_t* rowdiff, int tiles_x, in
                       uint2* ranges, uint32_t* cursor, uint32_t* order, uint2* prange, uint32_t* plan,
                       uint64_t* n_dup, uint64_t* sort_n, unsigned long long* overflows, cudaStream_t s);
 void launch_bucket(const uint32_t* dupcount, const uint4* dinfo, const ProjRec* proj, const uint64_t* n_ptr,
-                   uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, uint32_t* cursor, const uint32_t* saved,
+                   uint64_t n_max, const uint64_t* sort_n_ptr, int tiles_x, int tiles, uint32_t* cursor,
+                   const uint32_t* saved,
                    uint32_t* zk, uint32_t* ids, uint8_t* bm, uint32_t* huge_q, uint32_t* huge_n, uint64_t* dbg_keys,
                    uint32_t* dbg_vals, cudaStream_t s);
 // big-tile split + in-tile sort + finalize; parts / merges hold tile_sort_part_slots 16-byte records each
