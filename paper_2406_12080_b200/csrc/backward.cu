@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256) k_bw_blend(const uint2* __restrict__ rang
             if (!done) {
                 const ProjRec& r = s_rec[k];
                 const float dx = px - r.p0.x, dy = py - r.p0.y;
-                const float power = -0.5f * (r.p0.z * dx * dx + r.p1.x * dy * dy) - r.p0.w * dx * dy;
+                const float power = -0.5f * (r.p0.z * dx * dx + r.p3.x * dy * dy) - r.p0.w * dx * dy;
                 if (power <= 0.0f) {
                     // splat_alpha (render.hpp:201-231) with its intermediates
                     const float g = hs_libm::expf_glibc(power, s_et);
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(256) k_bw_blend(const uint2* __restrict__ rang
                         par_live = par >= kAlphaMin;
                         if (par_live) {
                             a_par = par;
-                            split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, r.p3.x, s_lt, s_et);
+                            split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, r.p1.x, s_lt, s_et);
                         }
                         alpha = t * a_self + (1.0f - t) * split;
                     } else {
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(256) k_bw_blend(const uint2* __restrict__ rang
                             done = true;
                         } else {
                             const float4 col = r.p2;
-                            const float as = s_aux[k].x, fe = s_aux[k].y, pe = s_aux[k].z, ik = r.p3.x;
+                            const float as = s_aux[k].x, fe = s_aux[k].y, pe = s_aux[k].z, ik = r.p1.x;
                             const float aw = alpha * T;
                             cp[0] += col.x * aw, cp[1] += col.y * aw, cp[2] += col.z * aw;
                             dp += col.w * aw;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(256) k_bw_blend(const uint2* __restrict__ rang
                             v[3] = g_power * -dx * dy;
                             v[4] = g_power * -0.5f * dy * dy;
                             v[0] = g_power * (r.p0.z * dx + r.p0.w * dy);
-                            v[1] = g_power * (r.p0.w * dx + r.p1.x * dy);
+                            v[1] = g_power * (r.p0.w * dx + r.p3.x * dy);
                             T = test;
                         }
                     }

@@ -37,10 +37,18 @@
 #ifndef HS_BLEND_CM
 #define HS_BLEND_CM 0
 #endif
-// minimum resident CTAs per SM the register allocation must allow (shared memory
-// holds it to 7 anyway; 8 caps the kernel at 64 registers)
+// minimum resident CTAs per SM the register allocation must allow (8 caps the
+// kernel at 64 registers; shared memory allows 8 as well)
 #ifndef HS_BLEND_MINB
 #define HS_BLEND_MINB 8
+#endif
+// resident CTAs per SM the persistent grid uses (at most the occupancy limit)
+#ifndef HS_BLEND_PER
+#define HS_BLEND_PER 6
+#endif
+// 1: the key/value scan reads through L2 only (keeps L1 for the staged records)
+#ifndef HS_BLEND_KEYS_CG
+#define HS_BLEND_KEYS_CG 0
 #endif
 
 namespace hs {
@@ -62,7 +70,7 @@ __device__ __forceinline__ uint64_t lds_u64(const float2* p) { return *reinterpr
 
 constexpr int kBlendThreads = 128;
 constexpr int kBlendWarps = kBlendThreads / 32;
-constexpr size_t kSmemRec = sizeof(float4) * kBlendWarps * 2 * 32 * 3;  // 2-stage staging of p1..p3
+constexpr size_t kSmemRec = sizeof(float4) * kBlendWarps * 2 * 32 * 2;  // 2-stage staging of p1, p2
 constexpr size_t kSmemPP = sizeof(float2) * kBlendWarps * 2 * 16 * 6;   // 2-stage entry-pair fields
 constexpr size_t kSmemV = sizeof(float) * kBlendWarps * 16 * 33;        // power / alpha per (entry, lane)
 constexpr size_t kSmemQ = sizeof(uint16_t) * kBlendWarps * 512;         // live-pair queue
@@ -80,13 +88,13 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
                                                             uint32_t* __restrict__ task_counter,
                                                             const uint32_t* __restrict__ tile_order,
                                                             uint32_t* lists, PairConsts pc) {
-    // per warp, two stages (cp.async double buffer) of 32 staged records: p1..p3 as
+    // per warp, two stages (cp.async double buffer) of 32 staged records: p1, p2 as
     // they are, and the phase-2 fields of p0/p1/p3 interleaved by entry pairs (the
     // packed FP32x2 power evaluation of entries 2j, 2j+1)
-    // (dynamic) s_rec[warps][2][32][3] float4 | s_pp[warps][2][16][6] float2 |
+    // (dynamic) s_rec[warps][2][2][32] float4 (stage, p1/p2, slot: 16-byte stride, as few bank conflicts as 48) | s_pp[warps][2][16][6] float2 |
     //           s_v[warps][16][33] float | s_q[warps][512] u16
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto s_rec = reinterpret_cast<float4(*)[2][32][3]>(smem_raw);
+    auto s_rec = reinterpret_cast<float4(*)[2][2][32]>(smem_raw);
     auto s_pp = reinterpret_cast<float2(*)[2][16][6]>(smem_raw + kSmemRec);
     auto s_v = reinterpret_cast<float(*)[16][33]>(smem_raw + kSmemRec + kSmemPP);
     auto s_q = reinterpret_cast<uint16_t(*)[512]>(smem_raw + kSmemRec + kSmemPP + kSmemV);
@@ -113,12 +121,12 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
         if (hit) {
             const float4* src = reinterpret_cast<const float4*>(proj + id);
 #pragma unroll
-            for (int q = 0; q < 3; ++q) __pipeline_memcpy_async(&s_rec[warp][st][lane][q], src + 1 + q, 16);
-            // x, y, conic0, conic1, conic2, power floor (ProjRec float offsets 0-4, 13)
+            for (int q = 0; q < 2; ++q) __pipeline_memcpy_async(&s_rec[warp][st][q][lane], src + 1 + q, 16);
+            // x, y, conic0, conic1, conic2, power floor (ProjRec float offsets 0-3, 12, 13)
             const float* srcf = reinterpret_cast<const float*>(src);
             float* dst = &s_pp[warp][st][lane >> 1][0].x + (lane & 1);
 #pragma unroll
-            for (int f = 0; f < 6; ++f) __pipeline_memcpy_async(dst + 2 * f, srcf + (f < 5 ? f : 13), 4);
+            for (int f = 0; f < 6; ++f) __pipeline_memcpy_async(dst + 2 * f, srcf + (f < 4 ? f : 8 + f), 4);
         } else {
             // no entry in this slot: a power floor of +inf is never reached, so the slot is
             // never live (the power loop needs no per-entry bound check)
@@ -162,8 +170,13 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
                     kk[c] = 0;
                     vv[c] = 0;
                     if (e < range.y) {
+#if HS_BLEND_KEYS_CG
+                        kk[c] = __ldcg(keys + e);
+                        vv[c] = __ldcg(vals + e);
+#else
                         kk[c] = keys[e];
                         vv[c] = vals[e];
+#endif
                     }
                 }
 #pragma unroll
@@ -190,7 +203,8 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
                 __pipeline_wait_prior(1);
                 __syncwarp();
                 if (__all_sync(0xffffffffu, done)) break;
-                const float4(*rec)[3] = s_rec[warp][b & 1];
+                const float4* rec1 = s_rec[warp][b & 1][0];  // p1 of the staged entries
+                const float4* rec2 = s_rec[warp][b & 1][1];  // p2
                 // Phases 2-4 run on the two halves of the batch in turn (16 entries each):
                 // halves the power/alpha scratch, which buys occupancy.
                 uint32_t tmask = 0;
@@ -200,7 +214,7 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
             const bool active = !done;
             // transitioning entries (t < 1) of this half, for the work counters
             const uint32_t ttr = (kStats || HS_BLEND_TQ)
-                                     ? __ballot_sync(0xffffffffu, lane < (int)hc && rec[h + lane][0].w < 1.0f)
+                                     ? __ballot_sync(0xffffffffu, lane < (int)hc && rec1[h + lane].w < 1.0f)
                                      : 0u;
             // 2. per-pixel power and liveness (cheap, all lanes)
             uint32_t live = 0;
@@ -293,7 +307,7 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
                     const uint32_t pr = sq[pq];
                     const int src = (int)(pr >> 4), k = (int)(pr & 15);
                     const float power = sv[k][src];
-                    const float4 p1 = rec[h + k][0];
+                    const float4 p1 = rec1[h + k];
                     const float tt = p1.w;
                     float g;
                     if (kMode == 0) {
@@ -318,7 +332,7 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
                         float split = 0.0f;
                         if (par >= kAlphaMin) {
                             if (kStats) ++n_pow;
-                            const float ik = rec[h + k][2].x;
+                            const float ik = p1.x;
                             if (kMode == 0)
                                 split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, ik, s_lt, s_et);
                             else
@@ -336,7 +350,7 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
             //    not live for a pixel is a no-op there).  Contributions are collected per
             //    lane (cm) and reduced once per half batch.
             {
-                const float4(*rh)[3] = rec + h;
+                const float4* rh = rec2 + h;
                 uint32_t act = done ? 0u : live, cm = 0, seen = active ? hc : 0u;
                 while (act) {
                     const uint32_t bit = act & (0u - act);  // lowest pending entry
@@ -358,7 +372,7 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
                             if (kStats) seen = (uint32_t)k + 1u;  // the reference visits up to the break
                             break;
                         }
-                        const float4 p2 = rh[k][1];
+                        const float4 p2 = rh[k];
                         const float wgt = alpha * T;
                         c0 = c0 + p2.x * wgt;
                         c1 = c1 + p2.y * wgt;
@@ -425,7 +439,7 @@ static void launch_blend_t(const uint2* ranges, const uint32_t* keys, const uint
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(k_blend<kMode, kStats>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blend<kMode, kStats>, kBlendThreads, kSmem);
-        grid = sms * std::min(8, per > 0 ? per : 1);  // blend_list_words() covers 8 per SM
+        grid = sms * std::min(HS_BLEND_PER, per > 0 ? per : 1);  // blend_list_words() covers 8 per SM
     }
     const int tasks = cam.tiles_x * cam.tiles_y * 8;
     const unsigned g = (unsigned)std::min<int>(grid, std::max(1, tasks / kBlendWarps));

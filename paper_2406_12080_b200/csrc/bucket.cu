@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(256) k_tile_count(const uint32_t* __restrict__
     const int W = tiles_x + 1;
     const uint64_t n = *n_ptr;
     const uint64_t n_chunks = (n + kChunk - 1) / kChunk;
+    if (blockIdx.x >= n_chunks) return;  // the grid covers n_max; the cut may be smaller
     hash_init(h);
     if (threadIdx.x == 0) s_nsaved = 0;
     __syncthreads();
@@ -437,13 +438,14 @@ __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ 
                                                    uint64_t* __restrict__ dbg_keys, uint32_t* __restrict__ dbg_vals) {
     __shared__ HashTab<kChunkLog> h;
     __shared__ BucketPair s_pair[kBucketWarps][32 * kBigArea];
-    __shared__ float4 s_rec[kBucketWarps][32][3];  // p0, p1, p3 of the warp's small footprints
+    __shared__ float4 s_rec[kBucketWarps][32][2];  // p0, p3 of the warp's small footprints
     __shared__ uint32_t s_z[kBucketWarps][32];
     if (*sort_n_ptr == 0) return;  // nothing visible, or over capacity
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const uint64_t n = *n_ptr;
     const uint64_t n_chunks = (n + kChunk - 1) / kChunk;
+    if (blockIdx.x >= n_chunks) return;
     hash_init(h);
     __syncthreads();
     for (uint64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
@@ -479,14 +481,14 @@ __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ 
         const int w = max(tx1 - tx0, 1);
         const bool small = cnt != 0 && cnt <= (uint32_t)kBigArea;
         const bool big = cnt > (uint32_t)kBigArea && cnt <= (uint32_t)kHugeArea;
-        float4 p0 = make_float4(0, 0, 0, 0), p1 = p0, p3 = p0;
+        float4 p0 = make_float4(0, 0, 0, 0), p3 = p0;
         if (small || big) {
             const ProjRec* r = proj + i;
-            p0 = r->p0, p1 = r->p1, p3 = r->p3;
+            p0 = r->p0, p3 = r->p3;
         }
         __syncwarp();  // the previous round's staging is consumed
         if (small) {
-            s_rec[warp][lane][0] = p0, s_rec[warp][lane][1] = p1, s_rec[warp][lane][2] = p3;
+            s_rec[warp][lane][0] = p0, s_rec[warp][lane][1] = p3;
             s_z[warp][lane] = di.z;
         }
         // 1. positions of the small footprints' pairs, listed per warp
@@ -515,8 +517,8 @@ __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ 
         // 2. the listed pairs, every lane busy
         for (uint32_t q = lane; q < np; q += 32) {
             const BucketPair pr = wp[q];
-            const uint32_t mask = tile_reach_mask(s_rec[warp][pr.local][0], s_rec[warp][pr.local][1],
-                                                  s_rec[warp][pr.local][2], pr.tx * kTile, pr.ty * kTile);
+            const uint32_t mask = tile_reach_mask(s_rec[warp][pr.local][0], s_rec[warp][pr.local][1], pr.tx * kTile,
+                                                  pr.ty * kTile, false);
             put_entry(pr.pos, (uint32_t)pr.ty * tiles_x + pr.tx, (uint32_t)(base + pr.local), s_z[warp][pr.local],
                       mask, zk, ids, bm, dbg_keys, dbg_vals);
         }
@@ -536,18 +538,16 @@ __global__ void __launch_bounds__(256, 4) k_bucket(const uint32_t* __restrict__ 
             const uint32_t sa = __shfl_sync(0xffffffffu, cnt, src), sz = __shfl_sync(0xffffffffu, di.z, src);
             const int sx0 = __shfl_sync(0xffffffffu, tx0, src), sy0 = __shfl_sync(0xffffffffu, ty0, src);
             const int sw = __shfl_sync(0xffffffffu, w, src);
-            float4 q0, q1, q3;
+            float4 q0, q3;
             q0.x = __shfl_sync(0xffffffffu, p0.x, src), q0.y = __shfl_sync(0xffffffffu, p0.y, src);
             q0.z = __shfl_sync(0xffffffffu, p0.z, src), q0.w = __shfl_sync(0xffffffffu, p0.w, src);
-            q1.x = __shfl_sync(0xffffffffu, p1.x, src), q1.y = __shfl_sync(0xffffffffu, p1.y, src);
-            q1.z = __shfl_sync(0xffffffffu, p1.z, src), q1.w = __shfl_sync(0xffffffffu, p1.w, src);
             q3.x = __shfl_sync(0xffffffffu, p3.x, src), q3.y = __shfl_sync(0xffffffffu, p3.y, src);
             q3.z = __shfl_sync(0xffffffffu, p3.z, src), q3.w = __shfl_sync(0xffffffffu, p3.w, src);
             for (uint32_t t = lane; t < sa; t += 32) {
                 const int tx = sx0 + (int)(t % sw), ty = sy0 + (int)(t / sw);
                 const uint32_t tile = (uint32_t)(ty * tiles_x + tx);
                 const uint32_t pos = atomicAdd(&cursor[tile], 1u);
-                const uint32_t mask = tile_reach_mask(q0, q1, q3, tx * kTile, ty * kTile);
+                const uint32_t mask = tile_reach_mask(q0, q3, tx * kTile, ty * kTile);
                 put_entry(pos, tile, sid, sz, mask, zk, ids, bm, dbg_keys, dbg_vals);
             }
         }
@@ -618,14 +618,14 @@ __global__ void __launch_bounds__(256) k_bucket_huge(const uint4* __restrict__ d
             uint4 di = make_uint4(0, 0, 0, 0);
             if (q < nq) id = huge_q[q], di = dinfo[id];
             const int tx0 = di.x & 0xffff, tx1 = di.x >> 16, ty0 = di.y & 0xffff, ty1 = di.y >> 16;
-            float4 p0 = make_float4(0, 0, 0, 0), p1 = p0, p3 = p0;
+            float4 p0 = make_float4(0, 0, 0, 0), p3 = p0;
             bool any = false;
 #pragma unroll
             for (int g = 0; g < kHugeGroup; ++g)
                 any |= q < nq && t0 + g < tiles && gx[g] >= tx0 && gx[g] < tx1 && gy[g] >= ty0 && gy[g] < ty1;
             if (any) {
                 const ProjRec* r = proj + id;
-                p0 = r->p0, p1 = r->p1, p3 = r->p3;
+                p0 = r->p0, p3 = r->p3;
             }
 #pragma unroll
             for (int g = 0; g < kHugeGroup; ++g) {
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(256) k_bucket_huge(const uint4* __restrict__ d
                 wb = __shfl_sync(0xffffffffu, wb, 0);
                 if (cov) {
                     const uint32_t pos = s_base[g] + wb + __popc(bal & lt);
-                    const uint32_t mask = tile_reach_mask(p0, p1, p3, gx[g] * kTile, gy[g] * kTile);
+                    const uint32_t mask = tile_reach_mask(p0, p3, gx[g] * kTile, gy[g] * kTile);
                     put_entry(pos, (uint32_t)(t0 + g), id, di.z, mask, zk, ids, bm, dbg_keys, dbg_vals);
                 }
             }

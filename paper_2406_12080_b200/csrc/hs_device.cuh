@@ -42,9 +42,10 @@ constexpr int kAttrVec4 = 16;
 
 // Projected splat record consumed by the blend (64 B):
 //   p0 = {mean2d.x, mean2d.y, conic0, conic1}
-//   p1 = {conic2, falloff_eff*alpha_scale, parent_falloff_eff*alpha_scale, t}
+//   p1 = {inv_k, falloff_eff*alpha_scale, parent_falloff_eff*alpha_scale, t}
 //   p2 = {color.r, color.g, color.b, inv_depth}
-//   p3 = {inv_k, -qthr/2 (power floor of the alpha >= 1/255 test), 1/conic0, 1/conic2}
+//   p3 = {conic2, -qthr/2 (power floor of the alpha >= 1/255 test), 1/conic0, 1/conic2}
+// (the blend stages p1 and p2 per entry: every alpha/composite field in 32 bytes)
 struct __align__(16) ProjRec {
     float4 p0, p1, p2, p3;
 };
@@ -167,16 +168,25 @@ __device__ __forceinline__ float interp_weight(float en, float ep, float tau) {
 // both the float rounding of the reference's per-pixel power (~1.5e-6 cond)
 // and of this evaluation (< 1e-6 cond); ia/ic (1/a, 1/c) only place the
 // evaluation points.
-__device__ __forceinline__ uint32_t tile_reach_mask(const float4& p0, const float4& p1, const float4& p3, int px0,
-                                                    int py0) {
+__device__ __forceinline__ uint32_t tile_reach_mask(const float4& p0, const float4& p3, int px0, int py0,
+                                                    bool full_test = true) {
     const float qthr = -2.0f * p3.y;  // p3.y = -qthr / 2 (exact scalings)
     if (qthr < 0.0f) return 0u;
-    const float a = p0.z, b = p0.w, c = p1.x;
-    {   // fast path: all four corner pixel centres inside the (convex) ellipse => every
+    const float a = p0.z, b = p0.w, c = p3.x;
+    // block edge pixel centres: (float)(px0 + o) + 0.5 == (float)px0 + (o + 0.5) exactly
+    // (integers and halves below 2^23), so one rounding, as the blend's d
+    const float fx0 = (float)px0, fy0 = (float)py0;
+    float xe[4], ye[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) xe[k] = (fx0 + ((float)((k >> 1) * 8 + (k & 1) * 7) + 0.5f)) - p0.x;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ye[k] = (fy0 + ((float)((k >> 1) * 4 + (k & 1) * 3) + 0.5f)) - p0.y;
+    if (full_test) {
+        // fast path: all four corner pixel centres inside the (convex) ellipse => every
         // block is reachable.  Setting a bit is always safe (the blend evaluates exactly);
-        // only clearing one needs the conservative test below.
-        const float cx0 = ((float)px0 + 0.5f) - p0.x, cx1 = ((float)(px0 + 15) + 0.5f) - p0.x;
-        const float cy0 = ((float)py0 + 0.5f) - p0.y, cy1 = ((float)(py0 + 15) + 0.5f) - p0.y;
+        // only clearing one needs the conservative test below.  Skipped for footprints of
+        // at most 4 tiles, which practically never cover a whole tile.
+        const float cx0 = xe[0], cx1 = xe[3], cy0 = ye[0], cy1 = ye[7];
         const float q00 = __fmaf_rn(__fmaf_rn(a, cx0, 2.0f * b * cy0), cx0, c * cy0 * cy0);
         const float q01 = __fmaf_rn(__fmaf_rn(a, cx0, 2.0f * b * cy1), cx0, c * cy1 * cy1);
         const float q10 = __fmaf_rn(__fmaf_rn(a, cx1, 2.0f * b * cy0), cx1, c * cy0 * cy0);
@@ -190,11 +200,6 @@ __device__ __forceinline__ uint32_t tile_reach_mask(const float4& p0, const floa
     // x = X_j (x0 if the mean is left of the block, else x1) and y = Y_r.  An edge
     // that faces nothing (the mean inside the block's column span) only adds an
     // upper bound, which leaves the minimum unchanged.
-    float xe[4], ye[8];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) xe[k] = ((float)(px0 + (k >> 1) * 8 + (k & 1) * 7) + 0.5f) - p0.x;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) ye[k] = ((float)(py0 + (k >> 1) * 4 + (k & 1) * 3) + 0.5f) - p0.y;
     // column edges: Q on x = X is (c y + 2 b X) y + a X^2, minimised at y = -b X / c
     float bx2[2], axx[2], ymin[2];
     bool cin[2];

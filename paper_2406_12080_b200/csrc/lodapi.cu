@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(256) k_blend_naive(const ProjRec* __restrict__
         for (uint32_t e = 0; e < cnt && !done; ++e) {
             const ProjRec r = s_rec[e];
             const float dx = px - r.p0.x, dy = py - r.p0.y;
-            const float power = -0.5f * ((r.p0.z * dx) * dx + (r.p1.x * dy) * dy) - (r.p0.w * dx) * dy;
+            const float power = -0.5f * ((r.p0.z * dx) * dx + (r.p3.x * dy) * dy) - (r.p0.w * dx) * dy;
             if (!(power <= 0.0f)) continue;
             const float g = hs_libm::expf_glibc(power, s_et);
             const float self_raw = r.p1.y * g;
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(256) k_blend_naive(const ProjRec* __restrict__
                 const float par_raw = r.p1.z * g;
                 const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
                 float split = 0.0f;
-                if (par >= kAlphaMin) split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, r.p3.x, s_lt, s_et);
+                if (par >= kAlphaMin) split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, r.p1.x, s_lt, s_et);
                 alpha = r.p1.w * a_self + (1.0f - r.p1.w) * split;
             }
             if (!(alpha > 0.0f)) continue;

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const float4* __restrict_
         const float fe = smax(falloff, 0.0f), pe = smax(pfall, 0.0f);
         ProjRec rec;
         rec.p0 = make_float4(mx, my, con0, con1);
-        rec.p1 = make_float4(con2, fe * ascale, pe * ascale, t);
+        rec.p1 = make_float4(1.0f / (float)max(1, K), fe * ascale, pe * ascale, t);
         rec.p2 = make_float4(col[0], col[1], col[2], invd);
         // Block-culling threshold for the blend (blend.cu may_touch): alpha >= 1/255 needs
         // Q(dx,dy) = conic quadratic <= 2 ln(255 m); inflated by a margin covering the float
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const float4* __restrict_
                 qthr = shrink > 0.0 ? __double2float_ru(thr / shrink) : __int_as_float(0x7f800000);
             }
         }
-        rec.p3 = make_float4(1.0f / (float)max(1, K), -0.5f * qthr, 1.0f / con0, 1.0f / con2);  // power floor
+        rec.p3 = make_float4(con2, -0.5f * qthr, 1.0f / con0, 1.0f / con2);  // power floor
         proj[j] = rec;
         dinfo[j] = make_uint4((uint32_t)tx0 | ((uint32_t)tx1 << 16), (uint32_t)ty0 | ((uint32_t)ty1 << 16),
                               __float_as_uint(tc[2]), 0u);
