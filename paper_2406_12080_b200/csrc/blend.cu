@@ -42,11 +42,16 @@
 #ifndef HS_BLEND_MINB
 #define HS_BLEND_MINB 8
 #endif
-// resident CTAs per SM the persistent grid uses (at most the occupancy limit)
+// resident CTAs per SM the persistent grid uses (at most the occupancy limit).  A/B:
+// 8 -> 7 -> 6 -> 5 -> 4 CTAs = 761 -> 703 -> 690 -> 736 -> 829 us (6 leaves L1 to the records)
 #ifndef HS_BLEND_PER
 #define HS_BLEND_PER 6
 #endif
-// 1: the key/value scan reads through L2 only (keeps L1 for the staged records)
+// Measured and dropped: a software-pipelined composite loop (next alpha/colour loaded
+// during the current step: 5% slower); two pixels per lane, a warp per 16x4 strip with
+// the right block's pixel point-reflected (1.04 vs 0.72 ms under ncu: +7% instructions,
+// fewer resident warps, a longer tail).
+// 1: the key/value scan reads through L2 only (keeps L1 for the staged records; no change)
 #ifndef HS_BLEND_KEYS_CG
 #define HS_BLEND_KEYS_CG 0
 #endif
