@@ -925,23 +925,29 @@ __device__ __forceinline__ bool msd_sort(S& sm, uint32_t n, uint32_t kmin, uint3
 }
 
 // Equal depths keep cut order (render.hpp:268-272 stable_sort): runs of equal
-// keys are rare; the thread at a run's start orders its indices by splat id.
+// keys are rare; the thread at a run's start orders its indices by splat id.  The
+// run's ids are read once into `scratch` (the sort's free key buffer, same
+// positions: runs are disjoint), so the insertion sort compares in shared memory
+// (adaptive: the bucketing leaves a run's ids nearly ascending).
 __device__ __forceinline__ void fix_ties(const uint32_t* __restrict__ key, uint16_t* __restrict__ idx, uint32_t n,
                                          const uint32_t* __restrict__ ids_in, uint32_t s, uint32_t i0,
-                                         uint32_t step) {
+                                         uint32_t step, uint32_t* __restrict__ scratch) {
     for (uint32_t i = i0; i + 1 < n; i += step) {
         if (key[i + 1] != key[i] || (i > 0 && key[i - 1] == key[i])) continue;
         uint32_t e = i + 1;
         while (e < n && key[e] == key[i]) ++e;
+        for (uint32_t a = i; a < e; ++a) scratch[a] = __ldcg(ids_in + s + idx[a]);
         for (uint32_t a = i + 1; a < e; ++a) {  // insertion sort by id
             const uint16_t x = idx[a];
-            const uint32_t xv = ids_in[s + x];
+            const uint32_t xv = scratch[a];
             uint32_t b = a;
-            while (b > i && ids_in[s + idx[b - 1]] > xv) {
+            while (b > i && scratch[b - 1] > xv) {
                 idx[b] = idx[b - 1];
+                scratch[b] = scratch[b - 1];
                 --b;
             }
             idx[b] = x;
+            scratch[b] = xv;
         }
     }
 }
@@ -1092,7 +1098,7 @@ __device__ __forceinline__ void cta_sort(CtaSort& cs, const uint32_t* __restrict
         const int cur = sort_group<kTsWarps>(cs, E, warp, kand, kor);
         rkey = cs.key[cur], ridx = cs.idx[cur];
     }
-    fix_ties(rkey, ridx, n, is, s, tid, kTsThreads);
+    fix_ties(rkey, ridx, n, is, s, tid, kTsThreads, rkey == cs.key[0] ? cs.key[1] : cs.key[0]);
     __syncthreads();
 }
 
@@ -1205,7 +1211,7 @@ __global__ void __launch_bounds__(kTsThreads, 4) k_tile_sort(const uint32_t* __r
                     const int cur = sort_group<1>(ws, E, 0, kand, kor);
                     rkey = ws.key[cur], ridx = ws.idx[cur];
                 }
-                fix_ties(rkey, ridx, n, b.iA, s, lane, 32);
+                fix_ties(rkey, ridx, n, b.iA, s, lane, 32, rkey == ws.key[0] ? ws.key[1] : ws.key[0]);
                 __syncwarp();
                 for (uint32_t i = lane; i < n; i += 32) {
                     b.zB[s + i] = kPending | tile << 8;

@@ -15,6 +15,6 @@ for v in "$@"; do
   python tools/launches.py $OUT/$v.csv > $OUT/$v.frame.txt 2>&1
   python -c "
 import json; d=json.load(open('$OUT/$v.json')); print('$v', 'value', round(d['value'],1), 'single', round(d['single_lane']['value'],1), 'blend_ms', round(d['stages_ms']['alpha_blend'],3))"
-  grep -E "k_blend" $OUT/$v.frame.txt
+  grep -E "${AB_GREP:-k_blend}" $OUT/$v.frame.txt
 done
 cp /tmp/lib_orig.so paper_2406_12080_b200/libhsplat_b200.so
