@@ -34,6 +34,21 @@
 #ifndef HS_BLEND_TQ
 #define HS_BLEND_TQ 0
 #endif
+// HS_BLEND_EQ = N > 0: halves with at least N (of 512) live pairs build the alpha queue
+// entry-major (homogeneous rounds: non-transitioning entries' rounds skip the powf
+// replica); sparser halves keep the lane-major push.  Blend stage, C2 (A/B, stage events):
+// off 0.615 ms; N = 1: 0.658 (the per-entry ballots cost more than they save on sparse
+// halves); 128: 0.605; 256: 0.599; 320: 0.595; 384: 0.597; 448: 0.596
+#ifndef HS_BLEND_EQ
+#define HS_BLEND_EQ 448
+#endif
+// HS_BLEND_FUSE = N > 0: halves with at least N live pairs evaluate and composite each
+// entry in one pass (no queue); sparser halves keep the queue.  Measured slower than the
+// entry-major queue alone (N = 320 / 384 / 448: 0.609 ms vs 0.596): lanes whose pixel is
+// not live or already done idle through the replicas, which the queue packs away
+#ifndef HS_BLEND_FUSE
+#define HS_BLEND_FUSE 0
+#endif
 #ifndef HS_BLEND_CM
 #define HS_BLEND_CM 0
 #endif
@@ -51,12 +66,35 @@
 // during the current step: 5% slower); two pixels per lane, a warp per 16x4 strip with
 // the right block's pixel point-reflected (1.04 vs 0.72 ms under ncu: +7% instructions,
 // fewer resident warps, a longer tail).
+// 1: the warps of a CTA share tiles: each CTA claims whole tiles from the global counter
+// and its warps take the tile's 8 blocks from a CTA-local counter, so a tile's keys and
+// records are gathered into one SM's L1 instead of up to eight.  Measured 46% slower
+// (0.98 vs 0.615 ms): the heaviest tiles' blocks -- tasks of 600-720 us in a 745 us
+// kernel (tools/blend_tasks.py) -- then run two per warp on one SM instead of side by side
+#ifndef HS_BLEND_CTA_TILES
+#define HS_BLEND_CTA_TILES 0
+#endif
 // 1: the key/value scan reads through L2 only (keeps L1 for the staged records; no change)
 #ifndef HS_BLEND_KEYS_CG
 #define HS_BLEND_KEYS_CG 0
 #endif
 
+// 1: per-task timing (globaltimer at the task's start and end, SM id, staged batches)
+// into g_blend_prof, read back with hs_debug_blend_prof (tools/blend_tasks.py)
+#ifndef HS_BLEND_PROF
+#define HS_BLEND_PROF 0
+#endif
+
 namespace hs {
+
+#if HS_BLEND_PROF
+__device__ unsigned long long g_blend_prof[3 * 262144];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 // (-0, 1, -1, -0.5) pairs as kernel parameters: see phase 2
 struct PairConsts {
@@ -81,6 +119,49 @@ constexpr size_t kSmemV = sizeof(float) * kBlendWarps * 16 * 33;        // power
 constexpr size_t kSmemQ = sizeof(uint16_t) * kBlendWarps * 512;         // live-pair queue
 constexpr uint32_t kListCap = 1024;                                      // per-warp block list (global, L2)
 
+// alpha of one (pixel, entry) pair from its power (detail::splat_alpha,
+// render.hpp:201-231): the self law, and for a transitioning entry the split law
+// mixed in by t; exact mode uses the glibc expf/powf replicas
+template <int kMode, bool kStats>
+__device__ __forceinline__ float pair_alpha(float power, const float4& p1, const uint64_t* s_et,
+                                            const uint64_t* s_lt, uint32_t& n_pow) {
+    const float tt = p1.w;
+    float g;
+    if (kMode == 0) {
+        g = hs_libm::expf_glibc(power, s_et);
+    } else {
+        // fast: SFU ex2, except within a 1e-5 relative band of the 1/255 floor of
+        // either law, where an approximate g could flip the gate (a jump of up to
+        // 1/255 in alpha): there the exact replica decides, as in exact mode
+        g = __expf(power);
+        const float sr = p1.y * g, pr = p1.z * g;
+        if (fabsf(sr - kAlphaMin) <= 1e-5f * kAlphaMin ||
+            (tt < 1.0f && fabsf(pr - kAlphaMin) <= 1e-5f * kAlphaMin))
+            g = hs_libm::expf_glibc(power, s_et);
+    }
+    const float self_raw = p1.y * g;
+    const float self = self_raw > kAlphaMax ? kAlphaMax : self_raw;
+    const float a_self = self >= kAlphaMin ? self : 0.0f;
+    float alpha;
+    if (tt < 1.0f) {
+        const float par_raw = p1.z * g;
+        const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
+        float split = 0.0f;
+        if (par >= kAlphaMin) {
+            if (kStats) ++n_pow;
+            const float ik = p1.x;
+            if (kMode == 0)
+                split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, ik, s_lt, s_et);
+            else
+                split = 1.0f - exp2f(ik * __log2f(1.0f - par));
+        }
+        alpha = tt * a_self + (1.0f - tt) * split;
+    } else {
+        alpha = a_self;
+    }
+    return alpha;
+}
+
 template <int kMode, bool kStats>
 __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const uint2* __restrict__ ranges,
                                                             const uint32_t* __restrict__ keys,
@@ -104,9 +185,18 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
     auto s_v = reinterpret_cast<float(*)[16][33]>(smem_raw + kSmemRec + kSmemPP);
     auto s_q = reinterpret_cast<uint16_t(*)[512]>(smem_raw + kSmemRec + kSmemPP + kSmemV);
     __shared__ uint64_t s_et[32], s_lt[32];
+#if HS_BLEND_CTA_TILES
+    // CTA-local block claims: claim c is block (c & 7) of the CTA's (c >> 3)-th tile, whose
+    // global tile rank the claimer of block 0 publishes in a 16-slot ring (tag = c >> 3)
+    __shared__ uint32_t s_claim, s_tag[16], s_tile[16];
+#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     uint32_t* lst = lists + ((size_t)blockIdx.x * kBlendWarps + warp) * kListCap;
+#if HS_BLEND_CTA_TILES
+    if (tid < 16) s_tag[tid] = 0xFFFFFFFFu;
+    if (tid == 0) s_claim = 0;
+#endif
     if (tid < 32) {
         s_et[tid] = c_exp2f_tab[tid];
         s_lt[tid] = c_powf_log2_tab[tid];
@@ -144,9 +234,30 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
         // tasks reserved by busy warps lengthen the tail; 29% slower even when the
         // last 1-4 tasks per resident warp are fetched on demand)
         uint32_t task = 0;
+#if HS_BLEND_CTA_TILES
+        if (lane == 0) {
+            const uint32_t c = atomicAdd(&s_claim, 1u), j = c >> 3, slot = j & 15u;
+            volatile uint32_t* vtag = s_tag;
+            volatile uint32_t* vtile = s_tile;
+            if ((c & 7u) == 0u) {
+                vtile[slot] = atomicAdd(task_counter, 1u);  // counts tiles here
+                __threadfence_block();
+                vtag[slot] = j;
+            } else {
+                while (vtag[slot] != j) __nanosleep(20);
+                __threadfence_block();
+            }
+            task = vtile[slot] * 8u + (c & 7u);
+        }
+#else
         if (lane == 0) task = atomicAdd(task_counter, 1u);
+#endif
         task = __shfl_sync(0xffffffffu, task, 0);
         if (task >= num_tasks) break;
+#if HS_BLEND_PROF
+        const unsigned long long prof_t0 = gtimer();
+        uint32_t prof_batches = 0;
+#endif
         const int tile = (int)tile_order[task >> 3], blk = (int)(task & 7);
         const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
         const int bx = tx * kTile + (blk & 1) * 8, by = ty * kTile + (blk >> 1) * 4;
@@ -200,6 +311,9 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
             issue(0, lane < n, id_cur);
             int b = 0;
             for (uint32_t base = 0; base < n; base += 32, ++b) {
+#if HS_BLEND_PROF
+                ++prof_batches;
+#endif
                 // records of the next batch in flight while this one is processed
                 issue((b + 1) & 1, base + 32 + lane < n, id_nxt);
                 const uint32_t id_b = id_cur;
@@ -260,18 +374,55 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
                     live |= (a0 & b0 & (1u << (2 * kp))) | (a1 & b1 & (2u << (2 * kp)));
                 }
             }
+#if HS_BLEND_FUSE
+            // a dense half (most of its pairs live) skips the queue: phases 3 and 4 fused below
+            const bool fused = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(live)) >= (uint32_t)HS_BLEND_FUSE;
+#else
+            constexpr bool fused = false;
+#endif
             // 3. alpha of every live (pixel, entry) pair.  Alpha does not depend on T, so the
             //    pairs of all lanes are compacted into one queue and evaluated 32 at a time
             //    with every lane busy (the exact expf/powf replicas are the costly part).
-            {
+            if (!fused) {
 #if HS_BLEND_TQ
                 // pairs of transitioning entries (the split law's powf) first, the others
                 // after them: the queue's rounds are then almost all of one kind, so the
                 // plain rounds skip the powf replica instead of idling through it
                 const uint32_t cnt = __popc(live & ttr) | (__popc(live & ~ttr) << 16);
+#elif HS_BLEND_EQ
+                const uint32_t cnt = __popc(live);
+                const uint32_t total = __reduce_add_sync(0xffffffffu, cnt);
+                if (kStats) w_exp += total;
+                if (total >= (uint32_t)HS_BLEND_EQ) {
+                    // dense half: entry-major queue (all of entry k's live pixels together), so
+                    // an alpha round covers one or two entries and the split law's powf runs
+                    // only in the rounds of transitioning entries (t is per entry)
+                    uint32_t pos = 0;
+                    for (uint32_t m = __reduce_or_sync(0xffffffffu, live); m; m &= m - 1) {
+                        const int k = __ffs(m) - 1;
+                        const bool mine = (live >> k) & 1u;
+                        const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+                        if (mine) sq[pos + __popc(bal & lt_mask)] = (uint16_t)((lane << 4) | k);
+                        pos += __popc(bal);
+                    }
+                } else {
+                    uint32_t incl = cnt;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    uint32_t pos = incl - cnt;
+                    for (uint32_t m = live; m;) {
+                        const int k = 31 - __clz(m);
+                        sq[pos++] = (uint16_t)((lane << 4) | k);
+                        m ^= 1u << k;
+                    }
+                }
 #else
                 const uint32_t cnt = __popc(live);
 #endif
+#if !HS_BLEND_EQ || HS_BLEND_TQ
                 uint32_t incl = cnt;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -308,54 +459,62 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
 #else
                 for (uint32_t m = live; m; m &= m - 1) sq[pos++] = (uint16_t)((lane << 4) | (__ffs(m) - 1));
 #endif
+#endif  // !HS_BLEND_EQ || HS_BLEND_TQ
                 __syncwarp();
                 for (uint32_t pq = lane; pq < total; pq += 32) {
                     const uint32_t pr = sq[pq];
                     const int src = (int)(pr >> 4), k = (int)(pr & 15);
                     const float power = sv[k][src];
                     const float4 p1 = rec1[h + k];
-                    const float tt = p1.w;
-                    float g;
-                    if (kMode == 0) {
-                        g = hs_libm::expf_glibc(power, s_et);
-                    } else {
-                        // fast: SFU ex2, except within a 1e-5 relative band of the 1/255 floor of
-                        // either law, where an approximate g could flip the gate (a jump of up to
-                        // 1/255 in alpha): there the exact replica decides, as in exact mode
-                        g = __expf(power);
-                        const float sr = p1.y * g, pr = p1.z * g;
-                        if (fabsf(sr - kAlphaMin) <= 1e-5f * kAlphaMin ||
-                            (tt < 1.0f && fabsf(pr - kAlphaMin) <= 1e-5f * kAlphaMin))
-                            g = hs_libm::expf_glibc(power, s_et);
-                    }
-                    const float self_raw = p1.y * g;
-                    const float self = self_raw > kAlphaMax ? kAlphaMax : self_raw;
-                    const float a_self = self >= kAlphaMin ? self : 0.0f;
-                    float alpha;
-                    if (tt < 1.0f) {
-                        const float par_raw = p1.z * g;
-                        const float par = par_raw > kAlphaMax ? kAlphaMax : par_raw;
-                        float split = 0.0f;
-                        if (par >= kAlphaMin) {
-                            if (kStats) ++n_pow;
-                            const float ik = p1.x;
-                            if (kMode == 0)
-                                split = 1.0f - hs_libm::powf_glibc_normal(1.0f - par, ik, s_lt, s_et);
-                            else
-                                split = 1.0f - exp2f(ik * __log2f(1.0f - par));
-                        }
-                        alpha = tt * a_self + (1.0f - tt) * split;
-                    } else {
-                        alpha = a_self;
-                    }
-                    sv[k][src] = alpha;
+                    sv[k][src] = pair_alpha<kMode, kStats>(power, p1, s_et, s_lt, n_pow);
                 }
                 __syncwarp();
             }
             // 4. composite in depth order: each lane walks its own live entries (an entry
             //    not live for a pixel is a no-op there).  Contributions are collected per
             //    lane (cm) and reduced once per half batch.
-            {
+            if (fused) {
+                // dense half: the entries in depth order, every lane evaluating its own pair's
+                // alpha and compositing it at once (no queue, no alpha round trip through shared
+                // memory).  The record, t and so the law are uniform per entry: the split law's
+                // powf runs only for transitioning entries.
+                const float4* rh = rec2 + h;
+                uint32_t cm = 0, seen = active ? hc : 0u, n_alpha = 0;
+                bool brk = false;
+                for (uint32_t m = __reduce_or_sync(0xffffffffu, live); m; m &= m - 1) {
+                    const int k = __ffs(m) - 1;
+                    if (((live >> k) & 1u) && !brk) {
+                        if (kStats) ++n_alpha;
+                        const float alpha = pair_alpha<kMode, kStats>(sv[k][lane], rec1[h + k], s_et, s_lt, n_pow);
+                        if (alpha > 0.0f) {
+                            const float test = T * (1.0f - alpha);
+                            if (test < kTransmittanceEps) {
+                                brk = true;
+                                if (kStats) seen = (uint32_t)k + 1u;  // the reference visits up to the break
+                            } else {
+                                const float4 p2 = rh[k];
+                                const float wgt = alpha * T;
+                                c0 = c0 + p2.x * wgt;
+                                c1 = c1 + p2.y * wgt;
+                                c2 = c2 + p2.z * wgt;
+                                d = d + p2.w * alpha * T;
+                                T = test;
+                                cm |= 1u << k;
+                            }
+                        }
+                    }
+                    // every pixel broken or past its last live entry
+                    if (__all_sync(0xffffffffu, brk || (live >> k) <= 1u)) break;
+                }
+                if (brk) done = true;
+                if (kStats) {
+                    n_contrib += __popc(cm);
+                    n_eval += seen;
+                    w_eval_t += __reduce_add_sync(0xffffffffu, (uint32_t)__popc(ttr & ((1u << seen) - 1u)));
+                    w_exp += __reduce_add_sync(0xffffffffu, n_alpha);
+                }
+                tmask |= __reduce_or_sync(0xffffffffu, cm) << h;
+            } else {
                 const float4* rh = rec2 + h;
                 uint32_t act = done ? 0u : live, cm = 0, seen = active ? hc : 0u;
                 while (act) {
@@ -409,6 +568,15 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
             __syncwarp();
             if (__all_sync(0xffffffffu, done)) break;
         }
+#if HS_BLEND_PROF
+        if (lane == 0 && task < 262144u) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+            g_blend_prof[3 * task] = prof_t0;
+            g_blend_prof[3 * task + 1] = gtimer();
+            g_blend_prof[3 * task + 2] = ((unsigned long long)smid << 32) | prof_batches;
+        }
+#endif
         if (inside) {
             const size_t plane = (size_t)cam.width * cam.height;
             const size_t i = (size_t)y * cam.width + x;
@@ -484,3 +652,11 @@ uint64_t blend_list_words() {
 }
 
 }  // namespace hs
+
+#if HS_BLEND_PROF
+// (task start ns, end ns, smid << 32 | staged batches) per blend task of the last launch
+extern "C" int hs_debug_blend_prof(unsigned long long* out, unsigned long long n_tasks) {
+    const size_t n = (size_t)(n_tasks < 262144ull ? n_tasks : 262144ull);
+    return (int)cudaMemcpyFromSymbol(out, hs::g_blend_prof, 3 * n * sizeof(unsigned long long));
+}
+#endif

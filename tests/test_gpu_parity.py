@@ -111,6 +111,27 @@ def test_cut_tau_sweep_c1(renderer, c1, tau):
     assert np.array_equal(cut.alpha_prime.view(np.uint32), a.view(np.uint32))
 
 
+def test_cut_tau_on_node_granularities(renderer, c1):
+    """k_select_cut compares RN(num / den) with tau without dividing (GranCmp): tau set
+    to nodes' own granularities and their float neighbours (the comparisons' edges),
+    denormal and extreme taus, all bit-exact against the oracle's divisions."""
+    h, oh, cam = c1
+    eps = renderer.granularity(h.bmin, h.bmax, cam)
+    fin = np.flatnonzero(np.isfinite(eps) & (eps > 0))
+    pick = eps[fin[np.linspace(0, len(fin) - 1, 5).astype(int)]]
+    f32 = np.float32
+    taus = [float(np.median(eps[fin]))]
+    for e in pick:
+        taus += [float(e), float(np.nextafter(f32(e), f32(np.inf))), float(np.nextafter(f32(e), f32(0)))]
+    taus += [float(np.finfo(np.float32).smallest_subnormal), 1e-42, float(np.finfo(np.float32).max)]
+    for tau in taus:
+        node, t, a = orc.select_cut(oh, cam, tau)
+        cut = renderer.select_cut(h, cam, tau)
+        assert np.array_equal(cut.node, node), tau
+        assert np.array_equal(cut.t.view(np.uint32), t.view(np.uint32)), tau
+        assert np.array_equal(cut.alpha_prime.view(np.uint32), a.view(np.uint32)), tau
+
+
 def test_cut_rejects_negative_tau(renderer, c1):
     h, _, cam = c1
     with pytest.raises(hs.Error) as e:
