@@ -42,13 +42,10 @@
 #ifndef HS_BLEND_EQ
 #define HS_BLEND_EQ 448
 #endif
-// HS_BLEND_FUSE = N > 0: halves with at least N live pairs evaluate and composite each
-// entry in one pass (no queue); sparser halves keep the queue.  Measured slower than the
-// entry-major queue alone (N = 320 / 384 / 448: 0.609 ms vs 0.596): lanes whose pixel is
-// not live or already done idle through the replicas, which the queue packs away
-#ifndef HS_BLEND_FUSE
-#define HS_BLEND_FUSE 0
-#endif
+// Measured and dropped: a fused dense path (alpha and composite per entry in one pass, no
+// queue) for halves with >= 320 / 384 / 448 live pairs: 0.609 ms vs 0.596 for the
+// entry-major queue alone -- lanes whose pixel is not live or already done idle through
+// the replicas, which the queue packs away.
 #ifndef HS_BLEND_CM
 #define HS_BLEND_CM 0
 #endif
@@ -66,14 +63,10 @@
 // during the current step: 5% slower); two pixels per lane, a warp per 16x4 strip with
 // the right block's pixel point-reflected (1.04 vs 0.72 ms under ncu: +7% instructions,
 // fewer resident warps, a longer tail).
-// 1: the warps of a CTA share tiles: each CTA claims whole tiles from the global counter
-// and its warps take the tile's 8 blocks from a CTA-local counter, so a tile's keys and
-// records are gathered into one SM's L1 instead of up to eight.  Measured 46% slower
-// (0.98 vs 0.615 ms): the heaviest tiles' blocks -- tasks of 600-720 us in a 745 us
-// kernel (tools/blend_tasks.py) -- then run two per warp on one SM instead of side by side
-#ifndef HS_BLEND_CTA_TILES
-#define HS_BLEND_CTA_TILES 0
-#endif
+// Measured and dropped: CTA-shared tiles (each CTA claims whole tiles and its warps take
+// the tile's 8 blocks, so a tile's records are gathered into one SM's L1): 46% slower
+// (0.98 vs 0.615 ms) -- the heaviest tiles' blocks, tasks of 600-720 us in a 745 us
+// kernel (tools/blend_tasks.py), then run two per warp on one SM instead of side by side.
 // 1: the key/value scan reads through L2 only (keeps L1 for the staged records; no change)
 #ifndef HS_BLEND_KEYS_CG
 #define HS_BLEND_KEYS_CG 0
@@ -185,18 +178,9 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
     auto s_v = reinterpret_cast<float(*)[16][33]>(smem_raw + kSmemRec + kSmemPP);
     auto s_q = reinterpret_cast<uint16_t(*)[512]>(smem_raw + kSmemRec + kSmemPP + kSmemV);
     __shared__ uint64_t s_et[32], s_lt[32];
-#if HS_BLEND_CTA_TILES
-    // CTA-local block claims: claim c is block (c & 7) of the CTA's (c >> 3)-th tile, whose
-    // global tile rank the claimer of block 0 publishes in a 16-slot ring (tag = c >> 3)
-    __shared__ uint32_t s_claim, s_tag[16], s_tile[16];
-#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     uint32_t* lst = lists + ((size_t)blockIdx.x * kBlendWarps + warp) * kListCap;
-#if HS_BLEND_CTA_TILES
-    if (tid < 16) s_tag[tid] = 0xFFFFFFFFu;
-    if (tid == 0) s_claim = 0;
-#endif
     if (tid < 32) {
         s_et[tid] = c_exp2f_tab[tid];
         s_lt[tid] = c_powf_log2_tab[tid];
@@ -234,24 +218,7 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
         // tasks reserved by busy warps lengthen the tail; 29% slower even when the
         // last 1-4 tasks per resident warp are fetched on demand)
         uint32_t task = 0;
-#if HS_BLEND_CTA_TILES
-        if (lane == 0) {
-            const uint32_t c = atomicAdd(&s_claim, 1u), j = c >> 3, slot = j & 15u;
-            volatile uint32_t* vtag = s_tag;
-            volatile uint32_t* vtile = s_tile;
-            if ((c & 7u) == 0u) {
-                vtile[slot] = atomicAdd(task_counter, 1u);  // counts tiles here
-                __threadfence_block();
-                vtag[slot] = j;
-            } else {
-                while (vtag[slot] != j) __nanosleep(20);
-                __threadfence_block();
-            }
-            task = vtile[slot] * 8u + (c & 7u);
-        }
-#else
         if (lane == 0) task = atomicAdd(task_counter, 1u);
-#endif
         task = __shfl_sync(0xffffffffu, task, 0);
         if (task >= num_tasks) break;
 #if HS_BLEND_PROF
@@ -374,16 +341,10 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
                     live |= (a0 & b0 & (1u << (2 * kp))) | (a1 & b1 & (2u << (2 * kp)));
                 }
             }
-#if HS_BLEND_FUSE
-            // a dense half (most of its pairs live) skips the queue: phases 3 and 4 fused below
-            const bool fused = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(live)) >= (uint32_t)HS_BLEND_FUSE;
-#else
-            constexpr bool fused = false;
-#endif
             // 3. alpha of every live (pixel, entry) pair.  Alpha does not depend on T, so the
             //    pairs of all lanes are compacted into one queue and evaluated 32 at a time
             //    with every lane busy (the exact expf/powf replicas are the costly part).
-            if (!fused) {
+            {
 #if HS_BLEND_TQ
                 // pairs of transitioning entries (the split law's powf) first, the others
                 // after them: the queue's rounds are then almost all of one kind, so the
@@ -473,48 +434,7 @@ __global__ void __launch_bounds__(kBlendThreads, HS_BLEND_MINB) k_blend(const ui
             // 4. composite in depth order: each lane walks its own live entries (an entry
             //    not live for a pixel is a no-op there).  Contributions are collected per
             //    lane (cm) and reduced once per half batch.
-            if (fused) {
-                // dense half: the entries in depth order, every lane evaluating its own pair's
-                // alpha and compositing it at once (no queue, no alpha round trip through shared
-                // memory).  The record, t and so the law are uniform per entry: the split law's
-                // powf runs only for transitioning entries.
-                const float4* rh = rec2 + h;
-                uint32_t cm = 0, seen = active ? hc : 0u, n_alpha = 0;
-                bool brk = false;
-                for (uint32_t m = __reduce_or_sync(0xffffffffu, live); m; m &= m - 1) {
-                    const int k = __ffs(m) - 1;
-                    if (((live >> k) & 1u) && !brk) {
-                        if (kStats) ++n_alpha;
-                        const float alpha = pair_alpha<kMode, kStats>(sv[k][lane], rec1[h + k], s_et, s_lt, n_pow);
-                        if (alpha > 0.0f) {
-                            const float test = T * (1.0f - alpha);
-                            if (test < kTransmittanceEps) {
-                                brk = true;
-                                if (kStats) seen = (uint32_t)k + 1u;  // the reference visits up to the break
-                            } else {
-                                const float4 p2 = rh[k];
-                                const float wgt = alpha * T;
-                                c0 = c0 + p2.x * wgt;
-                                c1 = c1 + p2.y * wgt;
-                                c2 = c2 + p2.z * wgt;
-                                d = d + p2.w * alpha * T;
-                                T = test;
-                                cm |= 1u << k;
-                            }
-                        }
-                    }
-                    // every pixel broken or past its last live entry
-                    if (__all_sync(0xffffffffu, brk || (live >> k) <= 1u)) break;
-                }
-                if (brk) done = true;
-                if (kStats) {
-                    n_contrib += __popc(cm);
-                    n_eval += seen;
-                    w_eval_t += __reduce_add_sync(0xffffffffu, (uint32_t)__popc(ttr & ((1u << seen) - 1u)));
-                    w_exp += __reduce_add_sync(0xffffffffu, n_alpha);
-                }
-                tmask |= __reduce_or_sync(0xffffffffu, cm) << h;
-            } else {
+            {
                 const float4* rh = rec2 + h;
                 uint32_t act = done ? 0u : live, cm = 0, seen = active ? hc : 0u;
                 while (act) {
