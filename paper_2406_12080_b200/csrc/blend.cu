@@ -55,7 +55,8 @@
 #define HS_BLEND_MINB 8
 #endif
 // resident CTAs per SM the persistent grid uses (at most the occupancy limit).  A/B:
-// 8 -> 7 -> 6 -> 5 -> 4 CTAs = 761 -> 703 -> 690 -> 736 -> 829 us (6 leaves L1 to the records)
+// 8 -> 7 -> 6 -> 5 -> 4 CTAs = 761 -> 703 -> 690 -> 736 -> 829 us (6 leaves L1 to the records);
+// with the entry-major dense queue (56 registers): 8 / 7 / 6 = 0.668 / 0.640 / 0.601 ms (stage events)
 #ifndef HS_BLEND_PER
 #define HS_BLEND_PER 6
 #endif
@@ -67,6 +68,11 @@
 // the tile's 8 blocks, so a tile's records are gathered into one SM's L1): 46% slower
 // (0.98 vs 0.615 ms) -- the heaviest tiles' blocks, tasks of 600-720 us in a 745 us
 // kernel (tools/blend_tasks.py), then run two per warp on one SM instead of side by side.
+// preferred shared-memory carveout (percent of the maximum; -1: the driver's choice).  A/B: driver,
+// 72, 86, 100 % = 0.601 / 0.598 / 0.597 / 0.600 ms (no effect: L1 is not what the 6-CTA optimum buys)
+#ifndef HS_BLEND_CARVE
+#define HS_BLEND_CARVE -1
+#endif
 // 1: the key/value scan reads through L2 only (keeps L1 for the staged records; no change)
 #ifndef HS_BLEND_KEYS_CG
 #define HS_BLEND_KEYS_CG 0
@@ -532,6 +538,9 @@ static void launch_blend_t(const uint2* ranges, const uint32_t* keys, const uint
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(k_blend<kMode, kStats>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+#if HS_BLEND_CARVE >= 0
+        cudaFuncSetAttribute(k_blend<kMode, kStats>, cudaFuncAttributePreferredSharedMemoryCarveout, HS_BLEND_CARVE);
+#endif
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_blend<kMode, kStats>, kBlendThreads, kSmem);
         grid = sms * std::min(HS_BLEND_PER, per > 0 ? per : 1);  // blend_list_words() covers 8 per SM
     }
