@@ -55,7 +55,9 @@
 #define HS_BLEND_MINB 8
 #endif
 // resident CTAs per SM the persistent grid uses (at most the occupancy limit).  A/B:
-// 8 -> 7 -> 6 -> 5 -> 4 CTAs = 761 -> 703 -> 690 -> 736 -> 829 us (6 leaves L1 to the records);
+// 8 -> 7 -> 6 -> 5 -> 4 CTAs = 761 -> 703 -> 690 -> 736 -> 829 us.  Not an L1 effect (the carveout
+// A/B below changes nothing): more warps per SM slow the heaviest blocks, whose tasks are
+// already ~0.9 of the span (tools/blend_tasks.py), fewer lose throughput;
 // with the entry-major dense queue (56 registers): 8 / 7 / 6 = 0.668 / 0.640 / 0.601 ms (stage events)
 #ifndef HS_BLEND_PER
 #define HS_BLEND_PER 6
