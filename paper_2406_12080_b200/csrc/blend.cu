@@ -42,6 +42,9 @@
 #ifndef HS_BLEND_EQ
 #define HS_BLEND_EQ 448
 #endif
+// Measured and dropped: the replicas' FP64 polynomial constants in the constant bank
+// (ptxas loads them with LDC.64 instead of rebuilding them with moves): 0.634 vs 0.601 ms,
+// 60 registers instead of 56.
 // Measured and dropped: a fused dense path (alpha and composite per entry in one pass, no
 // queue) for halves with >= 320 / 384 / 448 live pairs: 0.609 ms vs 0.596 for the
 // entry-major queue alone -- lanes whose pixel is not live or already done idle through
