@@ -47,8 +47,13 @@ __global__ void __launch_bounds__(256) k_assemble(const float4* __restrict__ att
     }
 }
 
+// resident 256-thread CTAs per SM the register allocation must allow.  A/B (C2): 4 / 5 / 6 =
+// 270 / 435 / 587 us -- the 51- and 42-register caps spill 192 / 272 bytes per thread
+#ifndef HS_PRE_MINB
+#define HS_PRE_MINB 4
+#endif
 template <bool kFromCut>
-__global__ void __launch_bounds__(256, 4) k_preprocess(const float4* __restrict__ attr, const uint32_t* __restrict__ cut_node,
+__global__ void __launch_bounds__(256, HS_PRE_MINB) k_preprocess(const float4* __restrict__ attr, const uint32_t* __restrict__ cut_node,
                                                     const float* __restrict__ cut_t, const uint64_t* __restrict__ n_ptr,
                                                     CamParams cam, ProjRec* __restrict__ proj,
                                                     uint4* __restrict__ dinfo,
